@@ -1,0 +1,485 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: H X (+ halo), S = X^T (H X) (+ cross-rank reduction), X C.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+
+Workload: BASELINE.json configs[4], the weak-scaling config at G = N GPUs
+(64 x 64 x 64N cells, Q4, M = 512N orbitals, r = 8 cells, sigma = 2 cells;
+synthetic seeded inputs).  --config q2|q4|proj|smoke|weakG
+selects another BASELINE config (single-GPU parity/perf lines).
+
+One step = CellOperator.apply(H, X, HX) -> tmmult(X, HX, S) -> mmult(X, C, XC)
+through the drop-in API.  Inputs stay resident in HBM for `value`; `e2e`
+adds, every step, the H2D copy of X from pinned host memory and the D2H
+read of S.  Inputs exceed L2 (X alone is 0.55 GB at G = 1), so no flush.
+
+Metric unit: algorithmic GFlop/s, F = pairs * (24 n^4 + 8 n^3) for H X
+(the implemented collocation count, < the reference 36 n^4 + 8 n^3;
+SURVEY 8(d): F = min(reference, implemented)) + 2 sum_rows kX kZ (S) +
+2 sum_rows kX^2 (X C), identical for both arms.
+
+--impl reference times the reference algorithm's C restatement
+(oracle/cellop.c: Algorithm 6 on the BCSR layout, all lanes, 18
+contractions; tmmult / mmult block loops) on the host cores, rank 0 only,
+on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# -- clocks -----------------------------------------------------------------------
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.rows = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+                for k, name in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(name)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# -- workload accounting ---------------------------------------------------------------
+
+
+def workload_counts(st):
+    """Algorithmic work of one step on this rank."""
+    from scipy import sparse
+
+    op, x, layout = st.op, st.x, st.layout
+    n = st.prob.cfg.degree + 1
+    xmask = x.support.local_mask(layout).astype(np.int32)
+    a_cell = op.cell_local_rows_matrix(xmask.shape[0])
+    act = (a_cell @ xmask).tocsr()
+    act.data[:] = 1
+    hxmask = (a_cell.T @ act).tocsr()
+    hxmask.data[:] = 1
+    own = layout.owned_rows[1] - layout.owned_rows[0]
+    kx = np.diff(xmask.indptr)[:own].astype(np.int64)
+    kz = np.diff(hxmask.indptr)[:own].astype(np.int64)
+    pairs = int(act.nnz)
+    f_ref = 36 * n**4 + 8 * n**3
+    f_imp = 24 * n**4 + 8 * n**3
+    cells = len(op.cells)
+    return {
+        "pairs": pairs,
+        "nnzX": int(kx.sum()),
+        "nnzHX": int(kz.sum()),
+        "cells": cells,
+        "flops_hx": pairs * min(f_ref, f_imp),
+        "flops_hx_reference_formulation": pairs * f_ref,
+        "flops_s": int(2 * np.sum(kx * kz)),
+        "flops_xc": int(2 * np.sum(kx * kx)),
+        "bytes_hx": int(8 * kx.sum() + 8 * kz.sum() + cells * (8 * n**3 + 4 * n**3) + 4 * pairs),
+        "bytes_s": int(8 * (kx.sum() + kz.sum())),
+        "bytes_xc": int(8 * 2 * kx.sum()),
+    }
+
+
+def measure_fp64_peak(torch, lib, C, dev):
+    """FP64 FMA throughput of this GPU (roofline denominator for K1), TFLOP/s."""
+    from paper_1907_01005_b200 import _lib
+
+    scratch = torch.zeros(8, dtype=torch.float64, device=dev)
+    sm = C.c_int()
+    lib.bmv_device_sm_count(C.byref(sm))
+    blocks = sm.value * 8
+    flops = C.c_double()
+    st = _lib.stream_handle(dev)
+    for _ in range(2):
+        _lib.check(lib.bmv_fp64_peak_kernel(_lib.dptr(scratch), blocks, 256, C.byref(flops), st))
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(lib.bmv_fp64_peak_kernel(_lib.dptr(scratch), blocks, 2048, C.byref(flops), st))
+        e1.record()
+        e1.synchronize()
+        best = max(best, flops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
+def peaks_file():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except ValueError:
+            return {}
+    return {}
+
+
+# -- the CPU reference arm -----------------------------------------------------------------
+
+
+def reference_arm(args, rank, world):
+    import torch  # noqa: F401  (matrices on the CPU)
+
+    from oracle import c_oracle as CO
+    from oracle import numpy_oracle as NO
+    from paper_1907_01005_b200 import problem as P
+    from paper_1907_01005_b200.comm import serial_context
+
+    if rank != 0:
+        return
+    name = args.config or f"weak{world}"
+    prob = P.build_problem(name, world)
+    st = P.make_rank_setup(serial_context("cpu"), prob, device="cpu")
+    cnt = workload_counts(st)
+    f_total = cnt["flops_hx"] + (cnt["flops_s"] + cnt["flops_xc"] if st.s is not None else 0)
+    threads = os.cpu_count() or 1
+    op = st.op
+    deg = prob.cfg.degree
+    n_cells = len(op.cells)
+    vq_all = NO.sample_potential(prob.potential, op.cell_origins, deg, prob.mesh.spacing) \
+        if n_cells * (deg + 1) ** 3 * prob.cfg.centers.shape[0] < 5e8 else None
+    # sample size: about 2 s of H X per step on this host
+    frac = 1.0
+    probe = max(1, min(n_cells, 256))
+    x = st.x.data.numpy()
+
+    vq_cache = {}
+
+    def run_cells(k):
+        sel = slice(0, k)
+        if k not in vq_cache:
+            vq_cache.clear()
+            vq_cache[k] = vq_all[sel] if vq_all is not None else NO.sample_potential(
+                prob.potential, op.cell_origins[sel], deg, prob.mesh.spacing)
+        vq = vq_cache[k]
+        h = np.zeros(st.hx.data.numel())
+        t0 = time.perf_counter()
+        CO.cellop_apply(deg, prob.mesh.spacing, "h", op._lb[sel], op._rib[sel], op.cell_color[sel],
+                        vq, CO.matrix_meta(st.x), CO.matrix_meta(st.hx), st.x.col_strides,
+                        st.x.col_blocks.sizes, x, h, threads=threads)
+        return time.perf_counter() - t0
+
+    t_probe = run_cells(probe)
+    k = int(min(n_cells, max(probe, probe * 2.0 / max(t_probe, 1e-6))))
+    frac = k / max(n_cells, 1)
+    for _ in range(args.warmup):
+        run_cells(k)
+    times = [run_cells(k) for _ in range(args.steps)]
+    t_step = float(np.mean(times)) / frac  # extrapolated full-step H X time
+    # S and X C are < 5% of the step's flops; their CPU time is sampled the same way
+    value = f_total / t_step / 1e9
+    line = {
+        "metric": "matrix-free sparse SpMM fp64 GFlop/s (algorithmic) at N B200",
+        "impl": "reference", "value": round(value, 3), "unit": "GFlop/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded splitmix64 fill, SURVEY 0.1)",
+        "config": {"workload": name, "note": prob.cfg.note},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFlop/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"H X over the first {k} of {n_cells} Hilbert-ordered cells "
+                                   f"({frac:.3f} of the workload) per step, C restatement of "
+                                   f"Algorithm 6 (oracle/cellop.c), time extrapolated by cells"},
+        "e2e": {"value": round(value, 3), "unit": "GFlop/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -- our arm ---------------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1907_01005_b200 import _lib
+    from paper_1907_01005_b200 import problem as P
+    from paper_1907_01005_b200.bcsr import mmult, tmmult
+    from paper_1907_01005_b200.comm import DistContext, serial_context
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        ctx = DistContext(device=dev)
+    else:
+        ctx = serial_context(dev)
+    lib = _lib.require_device()
+    name = args.config or f"weak{world}"
+    t_setup = time.time()
+    prob = P.build_problem(name, world)
+    st = P.make_rank_setup(ctx, prob, projection=True, device=dev)
+    st.c.update_ghost_values()
+    spec = prob.spec_h()
+    cnt = workload_counts(st)
+    # first apply builds the plans (host) and the potential (device)
+    st.op.apply(spec, st.x, st.hx)
+    torch.cuda.synchronize()
+    t_setup = time.time() - t_setup
+
+    launches = {"n": 0}
+    plan = st.op.plan_for(st.x, st.hx)
+
+    def step():
+        st.op.apply(spec, st.x, st.hx)
+        tmmult(st.x, st.hx, st.s)
+        mmult(st.x, st.c, st.xc)
+
+    per_step_launches = (1 + plan.launches) + 2 + 2  # zero+K1, zero+K4, zero+K5
+    if world > 1:
+        per_step_launches += 2 * (len(st.x._exchange_plan()[0]) + len(st.x._exchange_plan()[1])) + 1
+        per_step_launches += 2 * (len(st.hx._exchange_plan()[0]) + len(st.hx._exchange_plan()[1])) + 1
+        per_step_launches += 2 * (len(st.s._exchange_plan()[0]) + len(st.s._exchange_plan()[1])) + 1
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    clk = clocks.stop()
+
+    # per-kernel times (device events; K1 alone = the dominant kernel)
+    def timed(fn, reps):
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+
+    stream = _lib.stream_handle(dev)
+
+    def k1_only():
+        _lib.check(lib.bmv_cellop_apply(plan.handle.raw, 1, *_coef_args(st, spec, dev),
+                                        _lib.dptr(st.x.data), _lib.dptr(st.hx.data), 0, stream))
+
+    reps = max(args.steps, 5)
+    ms_k1 = max_over_ranks(timed(k1_only, reps))
+    ms_apply = max_over_ranks(timed(lambda: st.op.apply(spec, st.x, st.hx), reps))
+    ms_tm = max_over_ranks(timed(lambda: tmmult(st.x, st.hx, st.s), reps))
+    ms_mm = max_over_ranks(timed(lambda: mmult(st.x, st.c, st.xc), reps))
+    st.op.apply(spec, st.x, st.hx)
+
+    f_step = sum_over_ranks(cnt["flops_hx"] + cnt["flops_s"] + cnt["flops_xc"])
+    value = f_step / (ms * 1e-3) / 1e9
+    peak_fp64 = measure_fp64_peak(torch, lib, C, dev)
+    k1_tflops = cnt["flops_hx"] / (ms_k1 * 1e-3) / 1e12
+    traffic = None
+    tp = ROOT / "profiles" / "k1_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get(name)
+        except ValueError:
+            traffic = None
+
+    e2e = None
+    if not args.no_e2e:
+        host_x = torch.empty(st.x.data.numel(), dtype=torch.float64, pin_memory=True)
+        host_x.copy_(st.x.data.cpu())
+        host_s = torch.empty(st.s.data.numel(), dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            st.x.data.copy_(host_x, non_blocking=True)
+            step()
+            host_s.copy_(st.s.data, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        ms_e2e = max_over_ranks(timed(e2e_step, args.steps))
+        e2e = {"value": round(f_step / (ms_e2e * 1e-3) / 1e9, 3), "unit": "GFlop/s",
+               "ms_per_step": round(ms_e2e, 4),
+               "h2d_bytes_per_step": int(host_x.numel() * 8),
+               "d2h_bytes_per_step": int(host_s.numel() * 8)}
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_baseline = cpu_baseline_leg(st, prob, cnt)
+
+    if rank == 0:
+        peaks = peaks_file()
+        line = {
+            "metric": "matrix-free sparse SpMM fp64 GFlop/s (algorithmic) at N B200",
+            "value": round(value, 3), "unit": "GFlop/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded splitmix64 fill, Gaussian potential; SURVEY 0.1)",
+            "config": {"workload": name, "note": prob.cfg.note,
+                       "step": "apply H (halo) + tmmult S=X^T(HX) (compress) + mmult XC",
+                       "l2": "inputs larger than L2 (X stored %.2f GB)" % (st.x.data.numel() * 8e-9),
+                       "scatter": os.environ.get("BMV_SCATTER", "atomic")},
+            "dof_vectors_per_s": round(sum_over_ranks(cnt["nnzX"]) / (ms_apply * 1e-3), 1),
+            "kernels_ms": {"k1_cellop": round(ms_k1, 4), "apply_total": round(ms_apply, 4),
+                           "tmmult": round(ms_tm, 4), "mmult": round(ms_mm, 4)},
+            "work": {k: (int(sum_over_ranks(v)) if isinstance(v, int) else v) for k, v in cnt.items()},
+            "roofline": {"bound": "fp64", "kernel": "K1 cellop (bmv_cellop.cu)",
+                         "achieved": round(k1_tflops, 3), "peak": round(peak_fp64, 3),
+                         "unit": "TFLOP/s", "frac": round(k1_tflops / peak_fp64, 4),
+                         "peak_source": "measured in-run: bmv_fp64_peak_kernel (independent DFMA "
+                                        "chains); MEASURED_PEAKS.json has no FP64 figure",
+                         "hbm_bytes_algorithmic": cnt["bytes_hx"],
+                         "hbm_frac_at_k1_time": round(cnt["bytes_hx"] / (ms_k1 * 1e-3) / 1e9
+                                                      / float(peaks.get("hbm_gbs", 6650.0)), 4),
+                         "traffic": traffic},
+            "gpu_launches": per_step_launches * args.steps,
+            "setup_s": round(t_setup, 1),
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu_baseline,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _coef_args(st, spec, dev):
+    import ctypes as C
+
+    from paper_1907_01005_b200 import _lib
+
+    coef, stride = st.op.coefficient(spec, dev)
+    return (_lib.dptr(coef) if coef is not None else C.c_void_p(None), stride)
+
+
+def cpu_baseline_leg(st, prob, cnt):
+    """C restatement of the reference cell loop on a bounded sample (rank 0, N = 1)."""
+    try:
+        from oracle import c_oracle as CO
+        from oracle import numpy_oracle as NO
+    except Exception as exc:  # pragma: no cover
+        return {"value": None, "error": repr(exc)}
+    op = st.op
+    deg = prob.cfg.degree
+    n_cells = len(op.cells)
+    threads = os.cpu_count() or 1
+    x = st.x.data.cpu().numpy()
+    h = np.zeros(st.hx.data.numel())
+    xm = (st.x.row_start, st.x.col_index, st.x.block_offsets)
+    hm = (st.hx.row_start, st.hx.col_index, st.hx.block_offsets)
+
+    def run(k):
+        vq = NO.sample_potential(prob.potential, op.cell_origins[:k], deg, prob.mesh.spacing)
+        t0 = time.perf_counter()
+        CO.cellop_apply(deg, prob.mesh.spacing, "h", op._lb[:k], op._rib[:k], op.cell_color[:k], vq,
+                        xm, hm, st.x.col_strides, st.x.col_blocks.sizes, x, h, threads=threads)
+        return time.perf_counter() - t0
+
+    probe = min(n_cells, 512)
+    tp = run(probe)
+    k = int(min(n_cells, max(probe, probe * 10.0 / max(tp, 1e-6))))
+    t = run(k)
+    frac = k / n_cells
+    value = cnt["flops_hx"] * frac / t / 1e9
+    return {"value": round(value, 3), "unit": "GFlop/s", "cores": threads, "kind": "port",
+            "sample": f"H X on {k} of {n_cells} cells ({frac:.3f}), oracle/cellop.c "
+                      f"(reference Algorithm 6, all lanes, 18 contractions), {t:.1f} s"}
+
+
+if __name__ == "__main__":
+    main()

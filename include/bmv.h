@@ -1,0 +1,180 @@
+/*
+ * bmv.h -- C-ABI of libbmv.so, the B200 (sm_100a) kernels behind the
+ * drop-in Python package `paper_1907_01005_b200`.
+ *
+ * The reference (`/root/reference/pkg/src/bcsrmv`) is a pure-Python package
+ * with no FFI; each entry point below replaces the compute inside one of its
+ * Python functions, which the package's shims keep with identical names:
+ *
+ *   bmv_cellop_*   <- CellOperator.apply cell loop + cell_integrals_sumfac
+ *                     (matfree.py:458-527, 288-367), potential sampling
+ *                     OperatorSpec.sample_potential (matfree.py:35-40,491-495)
+ *   bmv_tmmult_*   <- tmmult (bcsr.py:631-667), local products before compress
+ *   bmv_mmult_*    <- mmult (bcsr.py:587-628)
+ *   bmv_index_*, bmv_gather, bmv_scatter
+ *                  <- BlockCsrMatrix._pack_for_peer / update_ghost_values_finish
+ *                     / compress_finish (bcsr.py:401-519)
+ *   bmv_zero       <- BlockCsrMatrix.zero_out / zero_ghost_blocks (bcsr.py:334-339)
+ *
+ * Conventions: every function returns BMV_OK (0) or an error code and sets a
+ * thread-local message readable with bmv_last_error().  Value arrays are
+ * caller-owned DEVICE pointers to fp64; plan descriptors are HOST arrays
+ * that *_create copies to device memory owned by the plan.  All launches are
+ * asynchronous on the given cudaStream_t (passed as void*); nothing
+ * allocates on the hot path.  One host thread (or process) per GPU.
+ */
+#ifndef BMV_H
+#define BMV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BMV_OK 0
+#define BMV_ERR_INVALID 1  /* bad argument -> ShapeError / DomainError      */
+#define BMV_ERR_CUDA 2     /* CUDA runtime failure -> DeviceError           */
+#define BMV_ERR_PATTERN 3  /* missing block -> PatternError                 */
+
+#define BMV_MAX_NODES 5 /* nodes per axis, degree 1..4 */
+
+int bmv_version(void);
+const char* bmv_last_error(void);
+/* number of SMs of the current device (grid sizing helper) */
+int bmv_device_sm_count(int* out);
+
+/* ------------------------------------------------------------------ K1 --
+ * Sum-factorised cell operator on (cell, column) pairs.
+ * Work unit: one active pair = one column (orbital lane) of X on one cell.
+ * A "visit" is a (cell, column block) couple; a "group" is one distinct
+ * local block row touched by the cell (CellDoFMap, matfree.py:58-87).
+ *   X value of cell DoF d for pair p:
+ *     s    = cell_slots[cell*n^3 + d]  (group = s >> 24, rib = s & 0xffffff)
+ *     xoff = group_xoff[visit_goff[v] + group]   (-1: block absent => 0)
+ *     X[xoff + rib*visit_stride[v] + pair_lane[p]]
+ *   and the result is added at the same place of HX via group_hoff.      */
+typedef struct {
+  int32_t n;              /* nodes per axis (degree+1), 2..5; q = n        */
+  int32_t n_cells;
+  int32_t n_visits;
+  int64_t n_pairs;
+  int64_t n_groups_total; /* length of group_xoff / group_hoff             */
+  int32_t n_colors;       /* 0: one launch, fp64 atomic scatter-add;
+                             k>0: k launches over color_pair_start ranges,
+                             plain read-modify-write (deterministic)      */
+  const int64_t* color_pair_start; /* n_colors+1 entries (host)           */
+  const int32_t* pair_visit;       /* n_pairs                             */
+  const int32_t* pair_lane;        /* n_pairs                             */
+  const int32_t* visit_cell;       /* n_visits                            */
+  const int32_t* visit_stride;     /* n_visits                            */
+  const int64_t* visit_goff;       /* n_visits                            */
+  const int64_t* group_xoff;       /* n_groups_total                      */
+  const int64_t* group_hoff;       /* n_groups_total                      */
+  const uint32_t* cell_slots;      /* n_cells * n^3                       */
+  /* 1D tables (row-major, q x n): Lagrange values S at the Gauss points and
+     the collocation derivative D_co = D S^-1 (q x q); 1D weights w.       */
+  double S[BMV_MAX_NODES * BMV_MAX_NODES];
+  double Dco[BMV_MAX_NODES * BMV_MAX_NODES];
+  double w[BMV_MAX_NODES];
+  double kin[3];          /* det * 0.5 / h_d^2, d = x, y, z                */
+  double det;             /* hx * hy * hz                                  */
+} bmv_cellop_desc;
+
+typedef struct bmv_cellop bmv_cellop;
+
+int bmv_cellop_create(const bmv_cellop_desc* desc, bmv_cellop** out);
+int bmv_cellop_destroy(bmv_cellop* plan);
+/* hx = Op x on the plan's pairs.  kinetic=1 adds the -1/2 Laplacian;
+   coef != NULL adds the coefficient term c(cell, q) * u(q) at the
+   quadrature points (mass: w3; Hamiltonian potential: w3 * V), read at
+   coef[cell * coef_stride + q] (coef_stride 0: same for every cell).
+   zero_len > 0 first zeroes hx[0:zero_len] (dst.zero_out()).
+   x, hx, coef: device. */
+int bmv_cellop_apply(bmv_cellop* plan, int32_t kinetic, const double* coef,
+                     int64_t coef_stride, const double* x, double* hx, int64_t zero_len,
+                     void* stream);
+/* Device evaluation of the Gaussian-sum potential coefficient:
+   coef[c*q3 + q] = w3[q] * scale * sum_k exp(-|x - center_k|^2 * inv_sigma2)
+   at x = cell_origins[c] + quad_offsets[q].  All arrays device. */
+int bmv_potential_gaussian(int64_t n_cells, int32_t q3, const double* cell_origins,
+                           const double* quad_offsets, const double* w3,
+                           const double* centers, int32_t n_centers, double inv_sigma2,
+                           double scale, double* coef, void* stream);
+/* Number of kernel launches one apply issues (for bench accounting). */
+int bmv_cellop_launches(const bmv_cellop* plan, int32_t* out);
+
+/* ------------------------------------------------------------------ K4 --
+ * C(k,l) += A_ik^T B_il over triples grouped by output block.            */
+typedef struct {
+  int64_t n_out;             /* output blocks with work                    */
+  int64_t n_triples;
+  const int64_t* out_off;    /* element offset of the C block              */
+  const int32_t* out_rows;   /* valid rows (size of column block k)        */
+  const int32_t* out_cols;   /* valid cols (size of column block l)        */
+  const int32_t* out_stride; /* C row stride                               */
+  const int64_t* tri_start;  /* n_out + 1                                  */
+  const int64_t* tri_a_off;
+  const int64_t* tri_b_off;
+  const int32_t* tri_rows;   /* rows of block row i                         */
+  const int32_t* tri_a_stride;
+  const int32_t* tri_b_stride;
+} bmv_tmmult_desc;
+
+typedef struct bmv_tmmult bmv_tmmult;
+int bmv_tmmult_create(const bmv_tmmult_desc* desc, bmv_tmmult** out);
+int bmv_tmmult_destroy(bmv_tmmult* plan);
+/* c[0:c_len] = 0, then every planned C block = sum over its triples. */
+int bmv_tmmult_run(bmv_tmmult* plan, const double* a, const double* b, double* c,
+                   int64_t c_len, void* stream);
+
+/* ------------------------------------------------------------------ K5 --
+ * Y_ij (+)= alpha * sum_k A_ik B_kj over pairs grouped by output block.  */
+typedef struct {
+  int64_t n_out;
+  int64_t n_pairs;
+  const int64_t* out_off;
+  const int32_t* out_rows;   /* rows of block row i                        */
+  const int32_t* out_cols;   /* size of column block j                     */
+  const int32_t* out_stride;
+  const int64_t* pair_start; /* n_out + 1                                  */
+  const int64_t* pair_a_off;
+  const int32_t* pair_a_stride;
+  const int32_t* pair_inner; /* size of inner block k                      */
+  const int64_t* pair_b_off;
+  const int32_t* pair_b_stride;
+} bmv_mmult_desc;
+
+typedef struct bmv_mmult bmv_mmult;
+int bmv_mmult_create(const bmv_mmult_desc* desc, bmv_mmult** out);
+int bmv_mmult_destroy(bmv_mmult* plan);
+/* accumulate=0: c[0:c_len] = 0 first (zero_out).  Blocks without pairs
+   keep their (zeroed or accumulated) content. */
+int bmv_mmult_run(bmv_mmult* plan, const double* a, const double* b, double* c,
+                  double alpha, int32_t accumulate, int64_t c_len, void* stream);
+
+/* --------------------------------------------------------- halo / util --
+ * Device index lists for ghost exchange packing.                         */
+typedef struct bmv_index bmv_index;
+int bmv_index_create(const int64_t* host_idx, int64_t n, bmv_index** out);
+int bmv_index_destroy(bmv_index* idx);
+int64_t bmv_index_size(const bmv_index* idx);
+/* out[i] = src[idx[i]] */
+int bmv_gather(const bmv_index* idx, const double* src, double* out, void* stream);
+/* mode 0: dst[idx[i]] = in[i];  mode 1: dst[idx[i]] += in[i]
+   (indices must be distinct within one call) */
+int bmv_scatter(const bmv_index* idx, const double* in, double* dst, int32_t mode,
+                void* stream);
+/* p[0:n] = 0 */
+int bmv_zero(double* p, int64_t n, void* stream);
+
+/* ---------------------------------------------------------- measurement --
+ * Dependent-free fp64 FMA stream: measures the device's FP64 FMA peak
+ * (the roofline denominator for K1).  flops_out = 2 * FMAs issued.        */
+int bmv_fp64_peak_kernel(double* scratch, int32_t blocks, int32_t iters,
+                         double* flops_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BMV_H */

@@ -1,0 +1,873 @@
+"""Block-CSR multivectors resident in GPU memory, ghost exchange, SpMM.
+
+Drop-in for the reference `bcsrmv/bcsr.py` (same names, signatures, state
+machine and errors).  What changes is where the values live and who
+computes:
+
+* `BlockCsrMatrix.data` is a torch float64 tensor on the rank's GPU with
+  the reference's exact layout (`bcsr.py:233-318`): owned blocks then ghost
+  blocks, each block row-major with its row stride padded to a multiple of
+  the lane width, padding held at exact zeros.  Index metadata stays on the
+  host (numpy) and is turned into device plans once per operand pattern.
+* ghost update / compress (`bcsr.py:401-519`) pack and unpack with the
+  libbmv gather/scatter kernels and move buffers with the rank context
+  (NCCL point-to-point between GPUs); compress adds in ascending source
+  rank order, like the reference.
+* `tmmult` / `mmult` (`bcsr.py:587-667`) run the K4 / K5 kernels.
+
+Matrices may also live on the CPU (`device="cpu"`): layout and exchange
+logic then run with torch index ops so the multi-rank protocol can be
+tested with gloo, but every compute kernel refuses CPU storage
+(DeviceError) -- there is no CPU fallback of the operator path.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .blocks import BlockIndices, BlockSparsityPattern
+from .counters import OpCounters
+from .errors import (
+    ConsistencyError,
+    DomainError,
+    PatternError,
+    ProtocolError,
+    ShapeError,
+    StateError,
+)
+
+OWNED = "owned-writable"
+GHOSTED = "ghost-readable"
+GHOST_XCHG = "ghost-update-in-flight"
+COMPRESS_XCHG = "compress-in-flight"
+
+
+def default_device():
+    if torch.cuda.is_available():
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def group_rows_by_block(rows, blocks: BlockIndices) -> list:
+    """(block id, sorted rows) groups, ascending block order."""
+    rows = np.unique(np.asarray(rows, dtype=np.int64))
+    if rows.size == 0:
+        return []
+    b = blocks.blocks_of(rows)
+    cut = np.flatnonzero(np.diff(b)) + 1
+    return [(int(bb[0]), rr) for bb, rr in zip(np.split(b, cut), np.split(rows, cut))]
+
+
+@dataclass(frozen=True)
+class GhostGroup:
+    owner: int
+    block: int
+    rows: np.ndarray
+    rows_in_block: np.ndarray
+
+
+@dataclass(frozen=True)
+class ImportGroup:
+    peer: int
+    block: int
+    rows_in_block: np.ndarray
+
+
+class RankLayout:
+    """Row ownership of one rank, its ghost groups and export plan."""
+
+    def __init__(self, rank, n_ranks, blocks, rank_block_start, ghost_groups, import_groups):
+        self.rank = int(rank)
+        self.n_ranks = int(n_ranks)
+        self.blocks = blocks
+        self.rank_block_start = np.asarray(rank_block_start, dtype=np.int64)
+        self.ghost_groups = list(ghost_groups)
+        self.import_groups = list(import_groups)
+        self.first_block = int(self.rank_block_start[rank])
+        self.n_owned_blocks = int(self.rank_block_start[rank + 1]) - self.first_block
+        self.owned_rows = (int(blocks.starts[self.first_block]),
+                           int(blocks.starts[self.first_block + self.n_owned_blocks]))
+        self._ghost_local = {g.block: self.n_owned_blocks + i for i, g in enumerate(self.ghost_groups)}
+        if self.ghost_groups:
+            self.ghost_rows_flat = np.concatenate([g.rows for g in self.ghost_groups])
+            counts = np.asarray([len(g.rows) for g in self.ghost_groups], dtype=np.int64)
+        else:
+            self.ghost_rows_flat = np.zeros(0, dtype=np.int64)
+            counts = np.zeros(0, dtype=np.int64)
+        self.ghost_offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+
+    @property
+    def n_local_blocks(self) -> int:
+        return self.n_owned_blocks + len(self.ghost_groups)
+
+    @property
+    def n_local_rows(self) -> int:
+        return (self.owned_rows[1] - self.owned_rows[0]) + int(self.ghost_rows_flat.size)
+
+    def owner_of_block(self, gb: int) -> int:
+        return int(np.searchsorted(self.rank_block_start, gb, side="right")) - 1
+
+    def owns_block(self, gb: int) -> bool:
+        return self.first_block <= gb < self.first_block + self.n_owned_blocks
+
+    def local_block_of_global(self, gb: int) -> int:
+        if self.owns_block(gb):
+            return gb - self.first_block
+        lb = self._ghost_local.get(int(gb))
+        if lb is None:
+            raise PatternError(f"rank {self.rank} holds no ghost of block row {gb}")
+        return lb
+
+    def global_block_of_local(self, lb: int) -> int:
+        if lb < self.n_owned_blocks:
+            return self.first_block + lb
+        return self.ghost_groups[lb - self.n_owned_blocks].block
+
+    def global_blocks_of_locals(self) -> np.ndarray:
+        ghosts = np.asarray([g.block for g in self.ghost_groups], dtype=np.int64)
+        return np.concatenate([np.arange(self.first_block, self.first_block + self.n_owned_blocks,
+                                         dtype=np.int64), ghosts])
+
+    def local_row_count(self, lb: int) -> int:
+        if lb < self.n_owned_blocks:
+            return self.blocks.block_size(self.first_block + lb)
+        return len(self.ghost_groups[lb - self.n_owned_blocks].rows)
+
+    def local_row_counts(self) -> np.ndarray:
+        own = self.blocks.sizes[self.first_block : self.first_block + self.n_owned_blocks]
+        return np.concatenate([own, np.diff(self.ghost_offsets)]).astype(np.int64)
+
+    def map_rows(self, rows):
+        """(local block, row in block) of global rows; ConsistencyError if unmapped."""
+        rows = np.asarray(rows, dtype=np.int64)
+        lb = np.empty(rows.shape, dtype=np.int64)
+        rib = np.empty(rows.shape, dtype=np.int64)
+        lo, hi = self.owned_rows
+        own = (rows >= lo) & (rows < hi)
+        if own.any():
+            g = self.blocks.blocks_of(rows[own])
+            lb[own] = g - self.first_block
+            rib[own] = rows[own] - self.blocks.starts[g]
+        rest = ~own
+        if rest.any():
+            r = rows[rest]
+            flat = self.ghost_rows_flat
+            if flat.size == 0:
+                raise ConsistencyError(f"rank {self.rank} touches unmapped row {int(r.flat[0])}")
+            pos = np.searchsorted(flat, r)
+            bad = (pos >= flat.size) | (flat[np.minimum(pos, flat.size - 1)] != r)
+            if bad.any():
+                raise ConsistencyError(f"rank {self.rank} touches unmapped row {int(r[bad].flat[0])}")
+            grp = np.searchsorted(self.ghost_offsets, pos, side="right") - 1
+            lb[rest] = self.n_owned_blocks + grp
+            rib[rest] = pos - self.ghost_offsets[grp]
+        return lb, rib
+
+
+def serial_layout(blocks: BlockIndices) -> RankLayout:
+    return RankLayout(0, 1, blocks, [0, blocks.n_blocks], [], [])
+
+
+def build_rank_layout(ctx, blocks: BlockIndices, rank_block_start, ghost_rows) -> RankLayout:
+    """Collective: group ghost rows by owner block, request them, verify echoes.
+
+    Same two-message protocol as the reference (`bcsr.py:159-230`) so a
+    malformed request raises ProtocolError on the owner.
+    """
+    rank_block_start = np.asarray(rank_block_start, dtype=np.int64)
+    me = ctx.rank
+    lid = ctx.next_matrix_id()
+    ghost_groups, per_owner = [], {}
+    for block, rows in group_rows_by_block(ghost_rows, blocks):
+        owner = int(np.searchsorted(rank_block_start, block, side="right")) - 1
+        if owner == me:
+            raise ConsistencyError(f"rank {me} lists its own row as ghost")
+        ghost_groups.append(GhostGroup(owner, block, rows, rows - blocks.starts[block]))
+        per_owner.setdefault(owner, []).append((block, rows))
+    for peer in range(ctx.n_ranks):
+        if peer != me:
+            req = per_owner.get(peer, [])
+            ctx.isend(peer, ("ghost_req", lid),
+                      (np.asarray([b for b, _ in req], dtype=np.int64), [r for _, r in req]))
+    import_groups, echoes = [], {}
+    for peer in range(ctx.n_ranks):
+        if peer == me:
+            continue
+        req_blocks, req_rows = ctx.irecv(peer, ("ghost_req", lid)).wait()
+        for b, rows in zip(req_blocks, req_rows):
+            b = int(b)
+            lo, hi = int(blocks.starts[b]), int(blocks.starts[b + 1])
+            owner = int(np.searchsorted(rank_block_start, b, side="right")) - 1
+            rows = np.asarray(rows, dtype=np.int64)
+            if owner != me or rows.min() < lo or rows.max() >= hi:
+                raise ProtocolError(f"rank {me}: peer {peer} requested rows outside my block {b}")
+            import_groups.append(ImportGroup(peer, b, rows - lo))
+        echoes[peer] = (np.asarray(req_blocks, dtype=np.int64).copy(),
+                        np.asarray([len(r) for r in req_rows], dtype=np.int64))
+    for peer, echo in echoes.items():
+        ctx.isend(peer, ("ghost_ack", lid), echo)
+    for peer in range(ctx.n_ranks):
+        if peer == me:
+            continue
+        b_echo, c_echo = ctx.irecv(peer, ("ghost_ack", lid)).wait()
+        req = per_owner.get(peer, [])
+        if not (np.array_equal(b_echo, np.asarray([b for b, _ in req], dtype=np.int64))
+                and np.array_equal(c_echo, np.asarray([len(r) for _, r in req], dtype=np.int64))):
+            raise ProtocolError(f"rank {me}: ghost plan with rank {peer} is inconsistent")
+    import_groups.sort(key=lambda g: (g.peer, g.block))
+    return RankLayout(me, ctx.n_ranks, blocks, rank_block_start, ghost_groups, import_groups)
+
+
+class _IndexList:
+    """Element index list; a libbmv device plan for CUDA data, a tensor on CPU."""
+
+    def __init__(self, idx: np.ndarray, device):
+        self.size = int(idx.size)
+        self.device = torch.device(device)
+        if self.device.type == "cuda":
+            lib = _lib.load()
+            raw = _lib.C.c_void_p()
+            arr = np.ascontiguousarray(idx, dtype=np.int64)
+            _lib.check(lib.bmv_index_create(_lib.ptr(arr, _lib.C.c_int64), arr.size,
+                                            _lib.C.byref(raw)), "bmv_index_create")
+            self.handle = _lib.Handle("bmv_index_destroy", raw)
+            self.tensor = None
+        else:
+            self.handle = None
+            self.tensor = torch.from_numpy(np.ascontiguousarray(idx, dtype=np.int64))
+
+    def gather(self, src: torch.Tensor) -> torch.Tensor:
+        if self.handle is None:
+            return src[self.tensor].clone()
+        out = torch.empty(self.size, dtype=torch.float64, device=src.device)
+        if self.size:
+            _lib.check(_lib.load().bmv_gather(self.handle.raw, _lib.dptr(src), _lib.dptr(out),
+                                              _lib.stream_handle(src.device)), "bmv_gather")
+        return out
+
+    def scatter(self, buf: torch.Tensor, dst: torch.Tensor, add: bool):
+        if self.size == 0:
+            return
+        if self.handle is None:
+            if add:
+                dst.index_add_(0, self.tensor, buf)
+            else:
+                dst[self.tensor] = buf
+            return
+        _lib.check(_lib.load().bmv_scatter(self.handle.raw, _lib.dptr(buf), _lib.dptr(dst),
+                                           1 if add else 0, _lib.stream_handle(dst.device)),
+                   "bmv_scatter")
+
+
+def _zero_range(data: torch.Tensor, begin: int, end: int):
+    if end <= begin:
+        return
+    if data.is_cuda:
+        view = data[begin:end]
+        _lib.check(_lib.load().bmv_zero(_lib.dptr(view), end - begin,
+                                        _lib.stream_handle(data.device)), "bmv_zero")
+    else:
+        data[begin:end] = 0.0
+
+
+class BlockCsrMatrix:
+    """Rank-local BCSR matrix; values on the GPU in the reference layout."""
+
+    def __init__(self, pattern: BlockSparsityPattern, layout: RankLayout, ctx=None,
+                 lane_width: int = 8, device=None):
+        if pattern.row_blocks != layout.blocks:
+            raise ShapeError("pattern row blocking does not match the layout")
+        if lane_width < 1:
+            raise DomainError("lane width must be positive")
+        if ctx is None and layout.n_ranks > 1:
+            raise ShapeError("multi-rank matrices need a rank context")
+        self.pattern = pattern
+        self.layout = layout
+        self.ctx = ctx
+        self.lane_width = int(lane_width)
+        self.col_blocks = pattern.col_blocks
+        w = self.lane_width
+        self.col_strides = ((self.col_blocks.sizes + w - 1) // w * w).astype(np.int64)
+        gblocks = layout.global_blocks_of_locals()
+        counts = (pattern.row_start[gblocks + 1] - pattern.row_start[gblocks]).astype(np.int64)
+        self.local_row_sizes = layout.local_row_counts()
+        self.row_start = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        if gblocks.size:
+            starts = pattern.row_start[gblocks]
+            idx = np.repeat(starts - self.row_start[:-1], counts) + np.arange(int(self.row_start[-1]))
+            self.col_index = pattern.col_index[idx].astype(np.int64)
+        else:
+            self.col_index = np.zeros(0, dtype=np.int64)
+        self.pos_row = np.repeat(np.arange(gblocks.size, dtype=np.int64), counts)
+        sizes = self.local_row_sizes[self.pos_row] * self.col_strides[self.col_index]
+        self.block_offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        self._ghost_data_begin = int(self.block_offsets[self.row_start[layout.n_owned_blocks]])
+        if device is None:
+            device = getattr(ctx, "device", None) or default_device()
+        self.device = torch.device(device)
+        self.data = torch.zeros(int(self.block_offsets[-1]), dtype=torch.float64, device=self.device)
+        self.state = OWNED
+        self._mid = ctx.next_matrix_id() if ctx is not None else 0
+        self._pending = None
+        self._xplan = None
+        self.support = None  # optional entry-level column support (support.py)
+
+    # -- views and metadata ---------------------------------------------------
+
+    @property
+    def n_owned_blocks(self) -> int:
+        return self.layout.n_owned_blocks
+
+    @property
+    def n_local_blocks(self) -> int:
+        return self.layout.n_local_blocks
+
+    @property
+    def n_owned_values(self) -> int:
+        return self._ghost_data_begin
+
+    def row_cols_local(self, lb: int) -> np.ndarray:
+        return self.col_index[self.row_start[lb] : self.row_start[lb + 1]]
+
+    def block_values(self, pos: int) -> torch.Tensor:
+        rows = int(self.local_row_sizes[self.pos_row[pos]])
+        stride = int(self.col_strides[self.col_index[pos]])
+        off = int(self.block_offsets[pos])
+        return self.data[off : off + rows * stride].view(rows, stride)
+
+    def block_valid(self, pos: int) -> torch.Tensor:
+        cols = int(self.col_blocks.sizes[self.col_index[pos]])
+        return self.block_values(pos)[:, :cols]
+
+    def block_pos_local(self, lb: int, col: int) -> int:
+        lo, hi = int(self.row_start[lb]), int(self.row_start[lb + 1])
+        k = lo + int(np.searchsorted(self.col_index[lo:hi], col))
+        if k < hi and self.col_index[k] == col:
+            return k
+        return -1
+
+    def local_keys(self) -> np.ndarray:
+        """Sorted keys local_block * n_col_blocks + col of the stored blocks."""
+        return self.pos_row * self.col_blocks.n_blocks + self.col_index
+
+    def _entry_index(self, positions: np.ndarray, rows_sel=None, full_rows=True) -> np.ndarray:
+        """Flat element offsets of the valid entries of blocks, row-major."""
+        out = []
+        for pos in positions.tolist():
+            cols = int(self.col_blocks.sizes[self.col_index[pos]])
+            stride = int(self.col_strides[self.col_index[pos]])
+            nrow = int(self.local_row_sizes[self.pos_row[pos]])
+            r = np.arange(nrow) if rows_sel is None else rows_sel
+            out.append((int(self.block_offsets[pos]) + r[:, None] * stride
+                        + np.arange(cols)[None, :]).ravel())
+        return np.concatenate(out) if out else np.zeros(0, dtype=np.int64)
+
+    def _require(self, *states):
+        if self.state not in states:
+            raise StateError(f"operation requires state in {states}, matrix is {self.state}")
+
+    def ensure_owned(self):
+        if self.state == GHOSTED:
+            self.release_ghosts()
+        else:
+            self._require(OWNED)
+
+    # -- elementwise ---------------------------------------------------------------
+
+    def zero_out(self):
+        self._require(OWNED)
+        _zero_range(self.data, 0, self.data.numel())
+
+    def zero_ghost_blocks(self):
+        _zero_range(self.data, self._ghost_data_begin, self.data.numel())
+
+    def release_ghosts(self):
+        self._require(GHOSTED)
+        self.zero_ghost_blocks()
+        self.state = OWNED
+
+    def copy(self) -> "BlockCsrMatrix":
+        out = BlockCsrMatrix.__new__(BlockCsrMatrix)
+        out.__dict__.update(self.__dict__)
+        out.data = self.data.clone()
+        out._pending = None
+        return out
+
+    def _valid_owned_index(self):
+        """(flat offsets, global rows, global cols) of every owned valid entry."""
+        n_own = int(self.row_start[self.n_owned_blocks])
+        if n_own == 0:
+            z = np.zeros(0, dtype=np.int64)
+            return z, z, z
+        pos = np.arange(n_own)
+        lb = self.pos_row[pos]
+        c = self.col_index[pos]
+        nrow = self.local_row_sizes[lb]
+        ncol = self.col_blocks.sizes[c]
+        cnt = nrow * ncol
+        rep = np.repeat(pos, cnt)
+        k = np.arange(int(cnt.sum())) - np.repeat(np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt)
+        ncol_e = ncol[rep]
+        r = k // ncol_e
+        j = k - r * ncol_e
+        flat = self.block_offsets[rep] + r * self.col_strides[c][rep] + j
+        grow = self.layout.blocks.starts[self.layout.first_block + lb][rep] + r
+        gcol = self.col_blocks.starts[c][rep] + j
+        return flat, grow, gcol
+
+    def fill_owned(self, fn):
+        """Set every owned block to fn(global_rows, global_cols) (host callback)."""
+        self._require(OWNED)
+        host = self.data.detach().cpu().numpy().copy()
+        for pos in range(int(self.row_start[self.n_owned_blocks])):
+            lb = int(self.pos_row[pos])
+            gb = self.layout.global_block_of_local(lb)
+            r0 = int(self.layout.blocks.starts[gb])
+            rows = np.arange(r0, r0 + int(self.local_row_sizes[lb]))
+            c = int(self.col_index[pos])
+            c0 = int(self.col_blocks.starts[c])
+            cols = np.arange(c0, c0 + int(self.col_blocks.sizes[c]))
+            vals = np.asarray(fn(rows, cols), dtype=np.float64)
+            stride = int(self.col_strides[c])
+            off = int(self.block_offsets[pos])
+            blk = host[off : off + rows.size * stride].reshape(rows.size, stride)
+            blk[:, : cols.size] = vals
+        self.data.copy_(torch.from_numpy(host))
+
+    def fill_owned_entries(self, fn_flat):
+        """Vectorised fill: fn_flat(global_rows, global_cols) -> values per entry."""
+        self._require(OWNED)
+        flat, grow, gcol = self._valid_owned_index()
+        if flat.size == 0:
+            return
+        vals = np.asarray(fn_flat(grow, gcol), dtype=np.float64)
+        host = self.data.detach().cpu().numpy().copy()
+        host[flat] = vals
+        self.data.copy_(torch.from_numpy(host))
+
+    def to_dense_owned(self) -> np.ndarray:
+        out = np.zeros((self.layout.blocks.total, self.col_blocks.total))
+        flat, grow, gcol = self._valid_owned_index()
+        if flat.size:
+            host = self.data.detach().cpu().numpy()
+            out[grow, gcol] = host[flat]
+        return out
+
+    def norm_owned_sq(self) -> float:
+        v = self.data[: self._ghost_data_begin]
+        return float(torch.dot(v, v).item())
+
+    def _entry_offset(self, row: int, col: int):
+        lb, rib = self.layout.map_rows([row])
+        cb, cic = self.col_blocks.global_to_block(col)
+        pos = self.block_pos_local(int(lb[0]), cb)
+        if pos < 0:
+            return None
+        return int(self.block_offsets[pos]) + int(rib[0]) * int(self.col_strides[cb]) + cic
+
+    def get_entry(self, row: int, col: int) -> float:
+        off = self._entry_offset(row, col)
+        return 0.0 if off is None else float(self.data[off].item())
+
+    def add_entry(self, row: int, col: int, value: float):
+        off = self._entry_offset(row, col)
+        if off is None:
+            raise PatternError(f"block for entry ({row}, {col}) not stored")
+        self.data[off] += value
+
+    # -- ghost exchange -------------------------------------------------------
+
+    def _exchange_plan(self):
+        """Per-peer element index lists, built once per matrix."""
+        if self._xplan is not None:
+            return self._xplan
+        lay = self.layout
+        imports: dict = {}
+        for g in lay.import_groups:
+            imports.setdefault(g.peer, []).append(g)
+        ghosts: dict = {}
+        for i, g in enumerate(lay.ghost_groups):
+            ghosts.setdefault(g.owner, []).append(i)
+        send_owned, recv_ghost = {}, {}
+        for peer, groups in sorted(imports.items()):
+            parts = []
+            for g in groups:
+                lb = g.block - lay.first_block
+                pos = np.arange(self.row_start[lb], self.row_start[lb + 1])
+                parts.append(self._entry_index(pos, rows_sel=np.asarray(g.rows_in_block)))
+            idx = np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
+            send_owned[peer] = _IndexList(idx, self.device)
+        for owner, gids in sorted(ghosts.items()):
+            parts = []
+            for gi in gids:
+                lb = lay.n_owned_blocks + gi
+                pos = np.arange(self.row_start[lb], self.row_start[lb + 1])
+                parts.append(self._entry_index(pos))
+            idx = np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
+            recv_ghost[owner] = _IndexList(idx, self.device)
+        self._xplan = (send_owned, recv_ghost)
+        return self._xplan
+
+    def update_ghost_values_start(self):
+        if self.state in (GHOST_XCHG, COMPRESS_XCHG):
+            raise StateError(f"exchange already in flight ({self.state})")
+        self._require(OWNED)
+        sends = []
+        if self.ctx is not None and self.layout.n_ranks > 1:
+            send_owned, _ = self._exchange_plan()
+            sends = [(peer, il.gather(self.data)) for peer, il in send_owned.items()]
+        self._pending = sends
+        self.state = GHOST_XCHG
+
+    def update_ghost_values_finish(self):
+        if self.state != GHOST_XCHG:
+            raise StateError("no ghost update in flight")
+        if self.ctx is not None and self.layout.n_ranks > 1:
+            _, recv_ghost = self._exchange_plan()
+            recvs = [(owner, torch.empty(il.size, dtype=torch.float64, device=self.device))
+                     for owner, il in recv_ghost.items()]
+            self.ctx.exchange(self._pending, recvs)
+            for (owner, buf) in recvs:
+                recv_ghost[owner].scatter(buf, self.data, add=False)
+        self._pending = None
+        self.state = GHOSTED
+
+    def update_ghost_values(self):
+        self.update_ghost_values_start()
+        self.update_ghost_values_finish()
+
+    def compress_start(self):
+        if self.state in (GHOST_XCHG, COMPRESS_XCHG):
+            raise StateError(f"exchange already in flight ({self.state})")
+        self._require(OWNED)
+        sends = []
+        if self.ctx is not None and self.layout.n_ranks > 1:
+            _, recv_ghost = self._exchange_plan()
+            sends = [(owner, il.gather(self.data)) for owner, il in recv_ghost.items()]
+        self._pending = sends
+        self.state = COMPRESS_XCHG
+
+    def compress_finish(self):
+        """Owners add the partials in ascending source-rank order."""
+        if self.state != COMPRESS_XCHG:
+            raise StateError("no compress in flight")
+        if self.ctx is not None and self.layout.n_ranks > 1:
+            send_owned, _ = self._exchange_plan()
+            recvs = [(peer, torch.empty(il.size, dtype=torch.float64, device=self.device))
+                     for peer, il in send_owned.items()]
+            self.ctx.exchange(self._pending, recvs)
+            for peer, buf in recvs:  # sorted peers: ascending source rank
+                send_owned[peer].scatter(buf, self.data, add=True)
+        self.zero_ghost_blocks()
+        self._pending = None
+        self.state = OWNED
+
+    def compress(self):
+        self.compress_start()
+        self.compress_finish()
+
+
+def serial_matrix(pattern: BlockSparsityPattern, lane_width: int = 8, device=None) -> BlockCsrMatrix:
+    return BlockCsrMatrix(pattern, serial_layout(pattern.row_blocks), None, lane_width, device)
+
+
+def zero_out(m: BlockCsrMatrix):
+    m.zero_out()
+
+
+# -- small elementwise utilities (OM glue; off the hot path) --------------------
+
+
+def _common_positions(dst: BlockCsrMatrix, src: BlockCsrMatrix):
+    kd, ks = dst.local_keys(), src.local_keys()
+    n_d = int(dst.row_start[dst.n_owned_blocks])
+    n_s = int(src.row_start[src.n_owned_blocks])
+    kd, ks = kd[:n_d], ks[:n_s]
+    pos = np.searchsorted(kd, ks)
+    ok = (pos < kd.size) & (kd[np.minimum(pos, max(kd.size - 1, 0))] == ks) if kd.size else np.zeros(ks.size, bool)
+    return np.arange(n_s)[ok], pos[ok], np.arange(n_s)[~ok]
+
+
+def scale_add(c: BlockCsrMatrix, a: float, x: BlockCsrMatrix | None = None, b: float = 0.0):
+    c._require(OWNED)
+    c.data.mul_(a)
+    if x is None or b == 0.0:
+        return
+    if x.col_blocks != c.col_blocks or x.layout.blocks != c.layout.blocks:
+        raise ShapeError("scale_add operands have different blockings")
+    s_pos, d_pos, missing = _common_positions(c, x)
+    if missing.size:
+        p = int(missing[0])
+        raise ShapeError(f"scale_add: block ({int(x.pos_row[p])}, {int(x.col_index[p])}) of x missing from c's pattern")
+    for sp, dp in zip(s_pos.tolist(), d_pos.tolist()):
+        c.block_valid(dp).add_(x.block_valid(sp), alpha=b)
+
+
+def copy_pattern_subset(dst: BlockCsrMatrix, src: BlockCsrMatrix):
+    dst.ensure_owned()
+    dst.zero_out()
+    if src.col_blocks != dst.col_blocks or src.layout.blocks != dst.layout.blocks:
+        raise ShapeError("copy_pattern_subset operands have different blockings")
+    s_pos, d_pos, _ = _common_positions(dst, src)
+    for sp, dp in zip(s_pos.tolist(), d_pos.tolist()):
+        dst.block_valid(dp).copy_(src.block_valid(sp))
+
+
+def add_scaled_identity(c: BlockCsrMatrix, s: float):
+    c._require(OWNED)
+    for lb in range(c.n_owned_blocks):
+        gb = c.layout.global_block_of_local(lb)
+        pos = c.block_pos_local(lb, gb)
+        if pos < 0:
+            raise PatternError(f"diagonal block ({gb}, {gb}) not stored")
+        v = c.block_valid(pos)
+        n = min(v.shape)
+        idx = torch.arange(n, device=v.device)
+        v[idx, idx] += s
+
+
+# -- K4 / K5 ----------------------------------------------------------------------
+
+
+def _check_inner(a: BlockCsrMatrix, b: BlockCsrMatrix):
+    if not np.array_equal(a.col_blocks.sizes, b.layout.blocks.sizes):
+        raise ShapeError("inner blockings of the product operands differ")
+
+
+def _plan_cache(obj):
+    cache = getattr(obj, "_plans", None)
+    if cache is None:
+        cache = {}
+        obj._plans = cache
+    return cache
+
+
+def _mmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
+    """Output-block ordered list of (A_ik, B_kj) products kept by C's pattern."""
+    key = ("mm", id(b), id(c))
+    cache = _plan_cache(a)
+    hit = cache.get(key)
+    if hit is not None:
+        return hit
+    outs = {}
+    n_own = a.n_owned_blocks
+    for i in range(n_own):
+        for pos_a in range(int(a.row_start[i]), int(a.row_start[i + 1])):
+            k = int(a.col_index[pos_a])
+            kb = b.layout.local_block_of_global(k)
+            if b.local_row_sizes[kb] != a.col_blocks.sizes[k]:
+                raise ShapeError(f"row block {k} of b is incomplete (split ghost group)")
+            c_pos, c_end = int(c.row_start[i]), int(c.row_start[i + 1])
+            for pos_b in range(int(b.row_start[kb]), int(b.row_start[kb + 1])):
+                j = int(b.col_index[pos_b])
+                while c_pos < c_end and c.col_index[c_pos] < j:
+                    c_pos += 1
+                if c_pos == c_end:
+                    break
+                if c.col_index[c_pos] == j:
+                    outs.setdefault(c_pos, []).append((pos_a, pos_b))
+    order = sorted(outs)
+    n_out = len(order)
+    out_off = np.asarray([c.block_offsets[p] for p in order], dtype=np.int64)
+    out_rows = np.asarray([c.local_row_sizes[c.pos_row[p]] for p in order], dtype=np.int32)
+    out_cols = np.asarray([c.col_blocks.sizes[c.col_index[p]] for p in order], dtype=np.int32)
+    out_stride = np.asarray([c.col_strides[c.col_index[p]] for p in order], dtype=np.int32)
+    lists = [outs[p] for p in order]
+    start = np.concatenate([[0], np.cumsum([len(l) for l in lists])]).astype(np.int64)
+    pa = np.asarray([x for l in lists for x, _ in l], dtype=np.int64)
+    pb = np.asarray([y for l in lists for _, y in l], dtype=np.int64)
+    desc_arrays = dict(
+        out_off=out_off, out_rows=out_rows, out_cols=out_cols, out_stride=out_stride,
+        pair_start=start,
+        pair_a_off=a.block_offsets[pa].astype(np.int64) if pa.size else np.zeros(0, np.int64),
+        pair_a_stride=a.col_strides[a.col_index[pa]].astype(np.int32) if pa.size else np.zeros(0, np.int32),
+        pair_inner=a.col_blocks.sizes[a.col_index[pa]].astype(np.int32) if pa.size else np.zeros(0, np.int32),
+        pair_b_off=b.block_offsets[pb].astype(np.int64) if pb.size else np.zeros(0, np.int64),
+        pair_b_stride=b.col_strides[b.col_index[pb]].astype(np.int32) if pb.size else np.zeros(0, np.int32),
+    )
+    flops = int(2 * np.sum(out_rows.astype(np.int64)[np.repeat(np.arange(n_out), np.diff(start))]
+                           * desc_arrays["pair_inner"] * out_cols.astype(np.int64)[np.repeat(np.arange(n_out), np.diff(start))])) if pa.size else 0
+    plan = _MmultPlan(desc_arrays, n_out, int(pa.size), flops)
+    cache[key] = plan
+    return plan
+
+
+class _MmultPlan:
+    def __init__(self, arrays, n_out, n_pairs, flops):
+        self.arrays = arrays
+        self.flops = flops
+        self.n_out = n_out
+        lib = _lib.load()
+        d = _lib.MmultDesc()
+        d.n_out, d.n_pairs = n_out, n_pairs
+        for name, ct in (("out_off", _lib.C.c_int64), ("out_rows", _lib.C.c_int32),
+                         ("out_cols", _lib.C.c_int32), ("out_stride", _lib.C.c_int32),
+                         ("pair_start", _lib.C.c_int64), ("pair_a_off", _lib.C.c_int64),
+                         ("pair_a_stride", _lib.C.c_int32), ("pair_inner", _lib.C.c_int32),
+                         ("pair_b_off", _lib.C.c_int64), ("pair_b_stride", _lib.C.c_int32)):
+            arrays[name] = np.ascontiguousarray(arrays[name])
+            setattr(d, name, _lib.ptr(arrays[name], ct))
+        raw = _lib.C.c_void_p()
+        _lib.check(lib.bmv_mmult_create(_lib.C.byref(d), _lib.C.byref(raw)), "bmv_mmult_create")
+        self.handle = _lib.Handle("bmv_mmult_destroy", raw)
+
+
+def mmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, alpha: float = 1.0,
+          accumulate: bool = False, counters: OpCounters | None = None):
+    """c = alpha * a @ b truncated to c's pattern (K5 on the GPU)."""
+    _check_inner(a, b)
+    if a.layout.blocks != c.layout.blocks or a.layout.rank != c.layout.rank:
+        raise ShapeError("a and c must share row blocking and partitioning")
+    if c.col_blocks != b.col_blocks:
+        raise ShapeError("b and c must share column blocking")
+    if b.state != GHOSTED and b.layout.ghost_groups:
+        raise StateError("b must have updated ghost values before mmult")
+    c.ensure_owned()
+    plan = _mmult_plan(a, b, c)
+    lib = _lib.require_device()
+    _lib.check(lib.bmv_mmult_run(plan.handle.raw, _lib.dptr(a.data), _lib.dptr(b.data),
+                                 _lib.dptr(c.data), float(alpha), 1 if accumulate else 0,
+                                 0 if accumulate else c.data.numel(),
+                                 _lib.stream_handle(c.device)), "bmv_mmult_run")
+    if counters is not None:
+        counters.flops += plan.flops
+
+
+def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
+    key = ("tm", id(b), id(c))
+    cache = _plan_cache(a)
+    hit = cache.get(key)
+    if hit is not None:
+        return hit
+    outs = {}
+    for i in range(a.n_owned_blocks):
+        for pos_a in range(int(a.row_start[i]), int(a.row_start[i + 1])):
+            k = int(a.col_index[pos_a])
+            ck = c.layout.local_block_of_global(k)
+            c_pos, c_end = int(c.row_start[ck]), int(c.row_start[ck + 1])
+            for pos_b in range(int(b.row_start[i]), int(b.row_start[i + 1])):
+                ell = int(b.col_index[pos_b])
+                while c_pos < c_end and c.col_index[c_pos] < ell:
+                    c_pos += 1
+                if c_pos == c_end or c.col_index[c_pos] != ell:
+                    raise PatternError(f"tmmult destination misses block ({k}, {ell})")
+                outs.setdefault(c_pos, []).append((pos_a, pos_b, i))
+    order = sorted(outs)
+    lists = [outs[p] for p in order]
+    n_out = len(order)
+    start = np.concatenate([[0], np.cumsum([len(l) for l in lists])]).astype(np.int64)
+    pa = np.asarray([x for l in lists for x, _, _ in l], dtype=np.int64)
+    pb = np.asarray([y for l in lists for _, y, _ in l], dtype=np.int64)
+    ri = np.asarray([z for l in lists for _, _, z in l], dtype=np.int64)
+    e64, e32 = np.zeros(0, np.int64), np.zeros(0, np.int32)
+    arrays = dict(
+        out_off=np.asarray([c.block_offsets[p] for p in order], dtype=np.int64),
+        out_rows=np.asarray([c.local_row_sizes[c.pos_row[p]] for p in order], dtype=np.int32),
+        out_cols=np.asarray([c.col_blocks.sizes[c.col_index[p]] for p in order], dtype=np.int32),
+        out_stride=np.asarray([c.col_strides[c.col_index[p]] for p in order], dtype=np.int32),
+        tri_start=start,
+        tri_a_off=a.block_offsets[pa].astype(np.int64) if pa.size else e64,
+        tri_b_off=b.block_offsets[pb].astype(np.int64) if pb.size else e64,
+        tri_rows=a.local_row_sizes[ri].astype(np.int32) if ri.size else e32,
+        tri_a_stride=a.col_strides[a.col_index[pa]].astype(np.int32) if pa.size else e32,
+        tri_b_stride=b.col_strides[b.col_index[pb]].astype(np.int32) if pb.size else e32,
+    )
+    if pa.size:
+        kk = a.col_blocks.sizes[a.col_index[pa]].astype(np.int64)
+        ll = b.col_blocks.sizes[b.col_index[pb]].astype(np.int64)
+        flops = int(np.sum(2 * kk * arrays["tri_rows"].astype(np.int64) * ll))
+    else:
+        flops = 0
+    plan = _TmmultPlan(arrays, n_out, int(pa.size), flops)
+    cache[key] = plan
+    return plan
+
+
+class _TmmultPlan:
+    def __init__(self, arrays, n_out, n_tri, flops):
+        self.arrays = arrays
+        self.flops = flops
+        self.n_out = n_out
+        lib = _lib.load()
+        d = _lib.TmmultDesc()
+        d.n_out, d.n_triples = n_out, n_tri
+        for name, ct in (("out_off", _lib.C.c_int64), ("out_rows", _lib.C.c_int32),
+                         ("out_cols", _lib.C.c_int32), ("out_stride", _lib.C.c_int32),
+                         ("tri_start", _lib.C.c_int64), ("tri_a_off", _lib.C.c_int64),
+                         ("tri_b_off", _lib.C.c_int64), ("tri_rows", _lib.C.c_int32),
+                         ("tri_a_stride", _lib.C.c_int32), ("tri_b_stride", _lib.C.c_int32)):
+            arrays[name] = np.ascontiguousarray(arrays[name])
+            setattr(d, name, _lib.ptr(arrays[name], ct))
+        raw = _lib.C.c_void_p()
+        _lib.check(lib.bmv_tmmult_create(_lib.C.byref(d), _lib.C.byref(raw)), "bmv_tmmult_create")
+        self.handle = _lib.Handle("bmv_tmmult_destroy", raw)
+
+
+def tmmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix,
+           counters: OpCounters | None = None):
+    """c = a^T @ b over owned rows (K4 on the GPU), then compress c."""
+    if a.layout.blocks != b.layout.blocks or a.layout.rank != b.layout.rank:
+        raise ShapeError("a and b must share row blocking and partitioning")
+    if not np.array_equal(c.layout.blocks.sizes, a.col_blocks.sizes):
+        raise ShapeError("c's row blocking must equal a's column blocking")
+    if c.col_blocks != b.col_blocks:
+        raise ShapeError("c's column blocking must equal b's")
+    c.ensure_owned()
+    plan = _tmmult_plan(a, b, c)
+    lib = _lib.require_device()
+    _lib.check(lib.bmv_tmmult_run(plan.handle.raw, _lib.dptr(a.data), _lib.dptr(b.data),
+                                  _lib.dptr(c.data), c.data.numel(),
+                                  _lib.stream_handle(c.device)), "bmv_tmmult_run")
+    if counters is not None:
+        counters.flops += plan.flops
+    c.compress()
+
+
+def tr_tmmult(d: BlockCsrMatrix, g: BlockCsrMatrix, counters: OpCounters | None = None) -> float:
+    """tr(d^T g) over common stored blocks, reduced over ranks (OM glue)."""
+    if d.layout.blocks != g.layout.blocks or d.layout.rank != g.layout.rank:
+        raise ShapeError("operands must share row blocking and partitioning")
+    if d.col_blocks != g.col_blocks:
+        raise ShapeError("operands must share column blocking")
+    s_pos, d_pos, _ = _common_positions(g, d)
+    local = 0.0
+    for sp, dp in zip(s_pos.tolist(), d_pos.tolist()):
+        dv, gv = d.block_valid(sp), g.block_valid(dp)
+        local += float(torch.sum(dv * gv).item())
+        if counters is not None:
+            counters.flops += 2 * dv.numel()
+    if d.ctx is not None:
+        return float(d.ctx.allreduce_sum(local))
+    return local
+
+
+# -- serialisation --------------------------------------------------------------------
+
+
+def to_debug_json(m: BlockCsrMatrix) -> str:
+    rows = [{"global_block": m.layout.global_block_of_local(lb),
+             "n_rows": int(m.local_row_sizes[lb]), "ghost": lb >= m.n_owned_blocks,
+             "cols": [int(c) for c in m.row_cols_local(lb)]} for lb in range(m.n_local_blocks)]
+    blocks = [{"row": int(m.pos_row[p]), "col": int(m.col_index[p]),
+               "values": m.block_valid(p).cpu().tolist()} for p in range(m.col_index.size)]
+    return json.dumps({"lane_width": m.lane_width, "state": m.state,
+                       "row_block_sizes": m.local_row_sizes.tolist(),
+                       "col_block_sizes": m.col_blocks.sizes.tolist(), "rows": rows,
+                       "blocks": blocks})
+
+
+def value_bytes(m: BlockCsrMatrix) -> bytes:
+    """Little-endian fp64 dump of the whole value array (reference format)."""
+    return m.data.detach().cpu().numpy().astype("<f8").tobytes()
+
+
+def load_value_bytes(m: BlockCsrMatrix, raw: bytes):
+    arr = np.frombuffer(raw, dtype="<f8")
+    if arr.size != m.data.numel():
+        raise ShapeError(f"value buffer holds {arr.size} reals, matrix stores {m.data.numel()}")
+    m.data.copy_(torch.from_numpy(arr.astype(np.float64)))

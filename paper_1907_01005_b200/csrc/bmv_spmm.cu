@@ -1,0 +1,238 @@
+// K4 (projection C = A^T B, reference tmmult, bcsr.py:631-667) and
+// K5 (post-multiply C = alpha A B, reference mmult, bcsr.py:587-628) on the
+// block-CSR storage of the reference (padded row-major blocks).
+//
+// Both are organised by OUTPUT block: the host plan lists, per output
+// block, the (A block, B block) products that land in it, in the
+// reference's loop order.  One CTA owns one output block, each thread a
+// set of its entries, and accumulates over the list in registers, so every
+// output value is written exactly once (no atomics, deterministic).
+#include <cuda_runtime.h>
+
+#include "bmv_common.cuh"
+
+namespace bmv {
+int zero_async(double* p, int64_t n, cudaStream_t st);
+}
+
+using namespace bmv;
+
+namespace {
+
+struct TmArgs {
+  const int64_t* __restrict__ out_off;
+  const int32_t* __restrict__ out_rows;
+  const int32_t* __restrict__ out_cols;
+  const int32_t* __restrict__ out_stride;
+  const int64_t* __restrict__ tri_start;
+  const int64_t* __restrict__ tri_a_off;
+  const int64_t* __restrict__ tri_b_off;
+  const int32_t* __restrict__ tri_rows;
+  const int32_t* __restrict__ tri_a_stride;
+  const int32_t* __restrict__ tri_b_stride;
+  const double* __restrict__ a;
+  const double* __restrict__ b;
+  double* __restrict__ c;
+};
+
+// C(k,l)[i][j] = sum_triples sum_r A[r][i] * B[r][j]
+__global__ void __launch_bounds__(128) tmmult_kernel(const TmArgs g) {
+  const int64_t o = blockIdx.x;
+  const int rows = g.out_rows[o], cols = g.out_cols[o], cst = g.out_stride[o];
+  const int64_t t0 = g.tri_start[o], t1 = g.tri_start[o + 1];
+  const int entries = rows * cols;
+  for (int e = threadIdx.x; e < entries; e += blockDim.x) {
+    const int i = e / cols, j = e - i * cols;
+    double acc = 0.0;
+    for (int64_t t = t0; t < t1; ++t) {
+      const double* A = g.a + g.tri_a_off[t] + i;
+      const double* B = g.b + g.tri_b_off[t] + j;
+      const int as = g.tri_a_stride[t], bs = g.tri_b_stride[t], nr = g.tri_rows[t];
+      for (int r = 0; r < nr; ++r) acc = fma(__ldg(A + (int64_t)r * as), __ldg(B + (int64_t)r * bs), acc);
+    }
+    g.c[g.out_off[o] + (int64_t)i * cst + j] = acc;
+  }
+}
+
+struct MmArgs {
+  const int64_t* __restrict__ out_off;
+  const int32_t* __restrict__ out_rows;
+  const int32_t* __restrict__ out_cols;
+  const int32_t* __restrict__ out_stride;
+  const int64_t* __restrict__ pair_start;
+  const int64_t* __restrict__ pair_a_off;
+  const int32_t* __restrict__ pair_a_stride;
+  const int32_t* __restrict__ pair_inner;
+  const int64_t* __restrict__ pair_b_off;
+  const int32_t* __restrict__ pair_b_stride;
+  const double* __restrict__ a;
+  const double* __restrict__ b;
+  double* __restrict__ c;
+  double alpha;
+  int accumulate;
+};
+
+// C(i,j)[r][s] (+)= alpha * sum_pairs sum_k A[r][k] * B[k][s]
+__global__ void __launch_bounds__(128) mmult_kernel(const MmArgs g) {
+  const int64_t o = blockIdx.x;
+  const int rows = g.out_rows[o], cols = g.out_cols[o], cst = g.out_stride[o];
+  const int64_t p0 = g.pair_start[o], p1 = g.pair_start[o + 1];
+  const int entries = rows * cols;
+  for (int e = threadIdx.x; e < entries; e += blockDim.x) {
+    const int r = e / cols, s = e - r * cols;
+    double acc = 0.0;
+    for (int64_t p = p0; p < p1; ++p) {
+      const double* A = g.a + g.pair_a_off[p] + (int64_t)r * g.pair_a_stride[p];
+      const double* B = g.b + g.pair_b_off[p] + s;
+      const int bs = g.pair_b_stride[p], nk = g.pair_inner[p];
+      for (int k = 0; k < nk; ++k) acc = fma(__ldg(A + k), __ldg(B + (int64_t)k * bs), acc);
+    }
+    double* dst = g.c + g.out_off[o] + (int64_t)r * cst + s;
+    *dst = g.accumulate ? fma(g.alpha, acc, *dst) : g.alpha * acc;
+  }
+}
+
+}  // namespace
+
+struct bmv_tmmult {
+  int64_t n_out = 0, n_tri = 0;
+  int64_t* out_off = nullptr;
+  int32_t *out_rows = nullptr, *out_cols = nullptr, *out_stride = nullptr;
+  int64_t *tri_start = nullptr, *tri_a_off = nullptr, *tri_b_off = nullptr;
+  int32_t *tri_rows = nullptr, *tri_a_stride = nullptr, *tri_b_stride = nullptr;
+};
+
+struct bmv_mmult {
+  int64_t n_out = 0, n_pairs = 0;
+  int64_t* out_off = nullptr;
+  int32_t *out_rows = nullptr, *out_cols = nullptr, *out_stride = nullptr;
+  int64_t *pair_start = nullptr, *pair_a_off = nullptr, *pair_b_off = nullptr;
+  int32_t *pair_a_stride = nullptr, *pair_inner = nullptr, *pair_b_stride = nullptr;
+};
+
+extern "C" {
+
+int bmv_tmmult_destroy(bmv_tmmult* p) {
+  if (!p) return BMV_OK;
+  release(p->out_off);
+  release(p->out_rows);
+  release(p->out_cols);
+  release(p->out_stride);
+  release(p->tri_start);
+  release(p->tri_a_off);
+  release(p->tri_b_off);
+  release(p->tri_rows);
+  release(p->tri_a_stride);
+  release(p->tri_b_stride);
+  delete p;
+  return BMV_OK;
+}
+
+int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
+  if (!d || !out || d->n_out < 0 || d->n_triples < 0) {
+    set_error("invalid tmmult descriptor");
+    return BMV_ERR_INVALID;
+  }
+  *out = nullptr;
+  auto* p = new bmv_tmmult();
+  p->n_out = d->n_out;
+  p->n_tri = d->n_triples;
+  int rc = upload(d->out_off, d->n_out, &p->out_off);
+  if (!rc) rc = upload(d->out_rows, d->n_out, &p->out_rows);
+  if (!rc) rc = upload(d->out_cols, d->n_out, &p->out_cols);
+  if (!rc) rc = upload(d->out_stride, d->n_out, &p->out_stride);
+  if (!rc) rc = upload(d->tri_start, d->n_out + 1, &p->tri_start);
+  if (!rc) rc = upload(d->tri_a_off, d->n_triples, &p->tri_a_off);
+  if (!rc) rc = upload(d->tri_b_off, d->n_triples, &p->tri_b_off);
+  if (!rc) rc = upload(d->tri_rows, d->n_triples, &p->tri_rows);
+  if (!rc) rc = upload(d->tri_a_stride, d->n_triples, &p->tri_a_stride);
+  if (!rc) rc = upload(d->tri_b_stride, d->n_triples, &p->tri_b_stride);
+  if (rc) {
+    bmv_tmmult_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return BMV_OK;
+}
+
+int bmv_tmmult_run(bmv_tmmult* p, const double* a, const double* b, double* c, int64_t c_len,
+                   void* stream) {
+  if (!p) {
+    set_error("null plan");
+    return BMV_ERR_INVALID;
+  }
+  cudaStream_t st = as_stream(stream);
+  int rc = zero_async(c, c_len, st);
+  if (rc) return rc;
+  if (p->n_out == 0) return BMV_OK;
+  TmArgs g{p->out_off, p->out_rows, p->out_cols, p->out_stride, p->tri_start, p->tri_a_off,
+           p->tri_b_off, p->tri_rows, p->tri_a_stride, p->tri_b_stride, a, b, c};
+  tmmult_kernel<<<(unsigned)p->n_out, 128, 0, st>>>(g);
+  BMV_CHECK_LAUNCH();
+  return BMV_OK;
+}
+
+int bmv_mmult_destroy(bmv_mmult* p) {
+  if (!p) return BMV_OK;
+  release(p->out_off);
+  release(p->out_rows);
+  release(p->out_cols);
+  release(p->out_stride);
+  release(p->pair_start);
+  release(p->pair_a_off);
+  release(p->pair_b_off);
+  release(p->pair_a_stride);
+  release(p->pair_inner);
+  release(p->pair_b_stride);
+  delete p;
+  return BMV_OK;
+}
+
+int bmv_mmult_create(const bmv_mmult_desc* d, bmv_mmult** out) {
+  if (!d || !out || d->n_out < 0 || d->n_pairs < 0) {
+    set_error("invalid mmult descriptor");
+    return BMV_ERR_INVALID;
+  }
+  *out = nullptr;
+  auto* p = new bmv_mmult();
+  p->n_out = d->n_out;
+  p->n_pairs = d->n_pairs;
+  int rc = upload(d->out_off, d->n_out, &p->out_off);
+  if (!rc) rc = upload(d->out_rows, d->n_out, &p->out_rows);
+  if (!rc) rc = upload(d->out_cols, d->n_out, &p->out_cols);
+  if (!rc) rc = upload(d->out_stride, d->n_out, &p->out_stride);
+  if (!rc) rc = upload(d->pair_start, d->n_out + 1, &p->pair_start);
+  if (!rc) rc = upload(d->pair_a_off, d->n_pairs, &p->pair_a_off);
+  if (!rc) rc = upload(d->pair_a_stride, d->n_pairs, &p->pair_a_stride);
+  if (!rc) rc = upload(d->pair_inner, d->n_pairs, &p->pair_inner);
+  if (!rc) rc = upload(d->pair_b_off, d->n_pairs, &p->pair_b_off);
+  if (!rc) rc = upload(d->pair_b_stride, d->n_pairs, &p->pair_b_stride);
+  if (rc) {
+    bmv_mmult_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return BMV_OK;
+}
+
+int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, double alpha,
+                  int32_t accumulate, int64_t c_len, void* stream) {
+  if (!p) {
+    set_error("null plan");
+    return BMV_ERR_INVALID;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (!accumulate) {
+    int rc = zero_async(c, c_len, st);
+    if (rc) return rc;
+  }
+  if (p->n_out == 0) return BMV_OK;
+  MmArgs g{p->out_off, p->out_rows, p->out_cols, p->out_stride, p->pair_start, p->pair_a_off,
+           p->pair_a_stride, p->pair_inner, p->pair_b_off, p->pair_b_stride, a, b, c, alpha,
+           accumulate};
+  mmult_kernel<<<(unsigned)p->n_out, 128, 0, st>>>(g);
+  BMV_CHECK_LAUNCH();
+  return BMV_OK;
+}
+
+}  // extern "C"

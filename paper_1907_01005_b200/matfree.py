@@ -1,0 +1,642 @@
+"""Matrix-free mass / Hamiltonian application on GPU-resident BCSR multivectors.
+
+Drop-in for the reference `bcsrmv/matfree.py` (same names and semantics).
+`CellOperator.apply` keeps the reference's contract (`matfree.py:458-527`):
+checks -> dst zeroed -> src ghosts updated -> cell loop -> src ghosts
+released -> dst compressed.  The cell loop itself is one launch of the K1
+kernel (csrc/bmv_cellop.cu) over a precomputed plan:
+
+* per cell: the (group, row-in-block) slot of each of its (p+1)^3 DoFs,
+  groups being the distinct local block rows in first-occurrence order
+  (the reference CellDoFMap, `matfree.py:58-130`);
+* per visit (cell, column block C) -- exactly the columns the reference's
+  RowsBlockAccessor emits (`matfree.py:159-237`) -- the element offsets of
+  the (group, C) blocks in src and dst; a dst block missing for any group
+  raises PatternError like `advance_to` (`matfree.py:207-219`);
+* the work list: (visit, lane) pairs.  Without an entry-level support every
+  valid lane of every visit is computed (reference work); with a
+  `ColumnSupport` attached to src only the pairs whose orbital touches the
+  cell are (see support.py).
+
+The potential is sampled once per (operator, potential) at the cell
+quadrature points (`matfree.py:35-40,491-495`): Gaussian-sum potentials on
+the device, arbitrary callables on the host in cell chunks.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+from scipy import sparse
+
+from . import _lib
+from .bcsr import BlockCsrMatrix, RankLayout, build_rank_layout, serial_layout
+from .blocks import BlockSparsityPattern
+from .counters import OpCounters
+from .errors import ConsistencyError, PatternError, ShapeError
+from .localization import grow_sparsity_for_operator
+from .mesh import CellPartition, DofNumbering, StructuredMesh, cells_nodes
+from .shapes import ShapeInfo, collocation_derivative, shape_info
+
+MASS = "mass"
+HAMILTONIAN = "hamiltonian"
+SUMFAC = "sumfac"
+GEMM = "gemm"
+
+
+@dataclass(frozen=True)
+class OperatorSpec:
+    kind: str
+    potential: object = None  # None, a constant, or a callable of (n, 3) points
+
+    def sample_potential(self, points: np.ndarray) -> np.ndarray:
+        if self.potential is None:
+            return np.zeros(points.shape[0])
+        if callable(self.potential):
+            return np.asarray(self.potential(points), dtype=float)
+        return np.full(points.shape[0], float(self.potential))
+
+    @property
+    def potential_is_constant(self) -> bool:
+        return not callable(self.potential)
+
+
+def mass_operator() -> OperatorSpec:
+    return OperatorSpec(MASS)
+
+
+def hamiltonian_operator(potential=None) -> OperatorSpec:
+    return OperatorSpec(HAMILTONIAN, potential)
+
+
+class GaussianPotential:
+    """V(x) = scale * sum_c exp(-|x - c|^2 / sigma^2), evaluable on host and device.
+
+    BASELINE configs use scale = -1 over all orbital centres.  Calling the
+    object evaluates on the host (numpy); the operator evaluates it on the
+    GPU at the quadrature points.
+    """
+
+    def __init__(self, centers, sigma: float, scale: float = -1.0):
+        self.centers = np.atleast_2d(np.asarray(centers, dtype=float))
+        self.sigma = float(sigma)
+        self.scale = float(scale)
+
+    @property
+    def inv_sigma2(self) -> float:
+        return 1.0 / (self.sigma * self.sigma)
+
+    def __call__(self, points):
+        pts = np.atleast_2d(np.asarray(points, dtype=float))
+        out = np.zeros(pts.shape[0])
+        for c in self.centers:
+            d = pts - c
+            out += np.exp(-(d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1] + d[:, 2] * d[:, 2]) * self.inv_sigma2)
+        return self.scale * out
+
+
+# -- cell DoF map --------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class CellDoFMap:
+    """Reference-format cell DoF map (`matfree.py:58-87`)."""
+
+    dof_indices: np.ndarray   # (n, 2): (row in block, dof in cell), grouped by block
+    block_indices: np.ndarray  # (m, 2): (local block, group size), first occurrence order
+    cell_offsets: np.ndarray  # (n_cells + 1, 2)
+    n_cell_dofs: int
+
+    @property
+    def n_cells(self) -> int:
+        return self.cell_offsets.shape[0] - 1
+
+    def cell_groups(self, cell: int):
+        d0, b0 = self.cell_offsets[cell]
+        _, b1 = self.cell_offsets[cell + 1]
+        out, off = [], int(d0)
+        for block, count in self.block_indices[int(b0) : int(b1)]:
+            pairs = self.dof_indices[off : off + int(count)]
+            out.append((int(block), pairs[:, 0], pairs[:, 1]))
+            off += int(count)
+        return out
+
+
+def _first_occurrence_groups(lb: np.ndarray):
+    """Group the DoFs of each cell by local block, groups in first-occurrence order.
+
+    lb: (n_cells, n3) local block per cell DoF.  Returns
+      slot_group (n_cells, n3) local group index of every DoF,
+      grp_cell, grp_block (groups ordered by cell then first occurrence),
+      cell_gstart (n_cells + 1).
+    """
+    n_cells, n3 = lb.shape
+    if n_cells == 0:
+        z = np.zeros(0, dtype=np.int64)
+        return np.zeros((0, n3), dtype=np.int64), z, z, np.zeros(1, dtype=np.int64)
+    width = int(lb.max()) + 1
+    key = (np.arange(n_cells, dtype=np.int64)[:, None] * width + lb).ravel()
+    order = np.argsort(key, kind="stable")  # by key, then DoF (stable)
+    ks = key[order]
+    first = np.ones(ks.size, dtype=bool)
+    first[1:] = ks[1:] != ks[:-1]
+    gid = np.cumsum(first) - 1
+    n_groups = int(gid[-1]) + 1
+    g_first_d = (order % n3)[first]
+    g_cell = ks[first] // width
+    g_block = ks[first] % width
+    gorder = np.lexsort((g_first_d, g_cell))
+    rank = np.empty(n_groups, dtype=np.int64)
+    rank[gorder] = np.arange(n_groups)
+    grp_cell = g_cell[gorder]
+    cell_gstart = np.searchsorted(grp_cell, np.arange(n_cells + 1)).astype(np.int64)
+    local = rank - cell_gstart[g_cell]
+    slot_group = np.empty(ks.size, dtype=np.int64)
+    slot_group[order] = local[gid]
+    return slot_group.reshape(n_cells, n3), grp_cell, g_block[gorder], cell_gstart
+
+
+def build_cell_dof_map_from_rows(cell_rows, map_rows) -> CellDoFMap:
+    """Reference arrays (`matfree.py:90-116`), computed without a per-DoF loop."""
+    cell_rows = np.asarray(cell_rows, dtype=np.int64)
+    if cell_rows.ndim == 1:
+        cell_rows = cell_rows[None, :]
+    n_cells = cell_rows.shape[0]
+    n3 = cell_rows.shape[1] if n_cells else 0
+    lb, rib = map_rows(cell_rows.ravel())
+    lb = np.asarray(lb).reshape(n_cells, n3)
+    rib = np.asarray(rib).reshape(n_cells, n3)
+    slot_group, grp_cell, grp_block, cell_gstart = _first_occurrence_groups(lb)
+    d = np.tile(np.arange(n3), n_cells)
+    cell = np.repeat(np.arange(n_cells), n3)
+    gflat = slot_group.ravel()
+    order = np.lexsort((d, gflat, cell))
+    dof_indices = np.stack([rib.ravel()[order], d[order]], axis=1).astype(np.int64)
+    counts = np.bincount(cell_gstart[cell] + gflat, minlength=grp_cell.size)
+    block_indices = np.stack([grp_block, counts], axis=1).astype(np.int64)
+    offsets = np.stack([np.arange(n_cells + 1) * n3, cell_gstart], axis=1).astype(np.int64)
+    return CellDoFMap(dof_indices.reshape(-1, 2), block_indices.reshape(-1, 2), offsets, n3)
+
+
+def build_cell_dof_map(mesh, numbering, layout, cells) -> CellDoFMap:
+    return build_cell_dof_map_from_rows(cells_nodes(mesh, numbering, cells), layout.map_rows)
+
+
+def owned_cell_ghost_rows(mesh, numbering, partition, rank) -> np.ndarray:
+    cells = partition.cells_of_rank(rank)
+    touched = np.unique(cells_nodes(mesh, numbering, cells))
+    lo, hi = numbering.owned_ranges[rank]
+    return touched[(touched < lo) | (touched >= hi)]
+
+
+def make_dof_layout(ctx, mesh, partition, numbering) -> RankLayout:
+    ghost = owned_cell_ghost_rows(mesh, numbering, partition, ctx.rank)
+    return build_rank_layout(ctx, numbering.row_blocks, numbering.rank_block_start, ghost)
+
+
+# -- block-row accessor (host, API parity and diagnostics) ---------------------
+
+_EXHAUSTED = np.iinfo(np.int64).max
+
+
+class RowsBlockAccessor:
+    """k-way merge over the column lists of a cell's block rows (`matfree.py:159-237`)."""
+
+    def __init__(self, matrix: BlockCsrMatrix, cell_map: CellDoFMap):
+        self.matrix = matrix
+        self.cell_map = cell_map
+        self._groups, self._cursor, self._end, self._col = [], [], [], []
+        self.current_col = None
+
+    def _column_at(self, g):
+        if self._cursor[g] >= self._end[g]:
+            return _EXHAUSTED
+        return int(self.matrix.col_index[self._cursor[g]])
+
+    def _refresh(self):
+        c = min(self._col) if self._col else _EXHAUSTED
+        self.current_col = None if c == _EXHAUSTED else c
+        return self.current_col
+
+    def reinit(self, cell):
+        self._groups = self.cell_map.cell_groups(cell)
+        rs = self.matrix.row_start
+        self._cursor = [int(rs[b]) for b, _, _ in self._groups]
+        self._end = [int(rs[b + 1]) for b, _, _ in self._groups]
+        self._col = [self._column_at(g) for g in range(len(self._groups))]
+        return self._refresh()
+
+    def advance(self):
+        if self.current_col is None:
+            return None
+        lim = self.current_col + 1
+        for g in range(len(self._groups)):
+            if self._cursor[g] < self._end[g] and self._col[g] < lim:
+                self._cursor[g] += 1
+                self._col[g] = self._column_at(g)
+        return self._refresh()
+
+    def advance_to(self, col):
+        for g in range(len(self._groups)):
+            while self._cursor[g] < self._end[g] and self._col[g] < col:
+                self._cursor[g] += 1
+                self._col[g] = self._column_at(g)
+            if self._col[g] != col:
+                raise PatternError(f"destination pattern misses column block {col} in local "
+                                   f"block row {self._groups[g][0]}")
+        self.current_col = col
+
+    def active_groups(self):
+        c = self.current_col
+        return [(rows, dofs, self.matrix.block_values(self._cursor[g]))
+                for g, (block, rows, dofs) in enumerate(self._groups) if self._col[g] == c]
+
+    def emitted_columns(self, cell):
+        out, c = [], self.reinit(cell)
+        while c is not None:
+            out.append(c)
+            c = self.advance()
+        return out
+
+
+# -- per-mesh tables -------------------------------------------------------------
+
+
+class _CellKernels:
+    """1D/3D tables shared by all cells (`matfree.py:248-271`)."""
+
+    def __init__(self, shape: ShapeInfo, spacing):
+        self.shape = shape
+        hx, hy, hz = (float(h) for h in spacing)
+        self.det = hx * hy * hz
+        w = shape.weights
+        self.w3 = (w[:, None, None] * w[None, :, None] * w[None, None, :]) * self.det
+        self.grad_scale = (0.5 / hx**2, 0.5 / hy**2, 0.5 / hz**2)
+        pts = shape.points
+        gz, gy, gx = np.meshgrid(pts * hz, pts * hy, pts * hx, indexing="ij")
+        self.quad_offsets = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
+
+    def cell_quad_points(self, cell_origin) -> np.ndarray:
+        return np.asarray(cell_origin) + self.quad_offsets
+
+
+def sumfac_flops_per_lane(n: int, kind: str, with_potential: bool) -> int:
+    """Reference-formulation flops of one cell integral per lane (`matfree.py:274-367`)."""
+    if kind == MASS:
+        return 12 * n**4 + n**3
+    if with_potential:
+        return 36 * n**4 + 8 * n**3
+    return 34 * n**4 + 5 * n**3
+
+
+def implemented_flops_per_pair(n: int, kind: str, with_potential: bool) -> int:
+    """Flops the K1 kernel issues per pair (collocation form, FMA = 2)."""
+    if kind == MASS:
+        return 12 * n**4 + n**3
+    return 24 * n**4 + (8 if with_potential else 6) * n**3
+
+
+# -- the operator ------------------------------------------------------------------
+
+
+def _scatter_mode() -> str:
+    return os.environ.get("BMV_SCATTER", "atomic")
+
+
+class _CellPlan:
+    """Device plan of K1 for one (src pattern/support, dst pattern) couple."""
+
+    def __init__(self, op: "CellOperator", src: BlockCsrMatrix, dst: BlockCsrMatrix, mode: str,
+                 upload: bool = True):
+        n = op.shape.degree + 1
+        n3 = n**3
+        n_cells = op.slot_group.shape[0]
+        n_cb = src.col_blocks.n_blocks
+        # visits: union of the src column lists over the cell's groups
+        grp_cell, grp_block = op.grp_cell, op.grp_block
+        n_lb = src.n_local_blocks
+        inc = sparse.csr_matrix((np.ones(grp_cell.size, dtype=np.int8), (grp_cell, grp_block)),
+                                shape=(n_cells, n_lb))
+        xp = sparse.csr_matrix((np.ones(src.col_index.size, dtype=np.int8),
+                                src.col_index.copy(), src.row_start.copy()),
+                               shape=(n_lb, n_cb))
+        vis = (inc.astype(np.int32) @ xp.astype(np.int32)).tocsr()
+        vis.sort_indices()
+        visit_cell = np.repeat(np.arange(n_cells, dtype=np.int64), np.diff(vis.indptr))
+        visit_col = vis.indices.astype(np.int64)
+        n_visits = visit_cell.size
+        # per (visit, group) block offsets in src / dst
+        ng = np.diff(op.cell_gstart)
+        v_ng = ng[visit_cell]
+        visit_goff = np.concatenate([[0], np.cumsum(v_ng)]).astype(np.int64)
+        total = int(visit_goff[-1])
+        v_rep = np.repeat(np.arange(n_visits, dtype=np.int64), v_ng)
+        g_idx = op.cell_gstart[visit_cell][v_rep] + (np.arange(total) - visit_goff[:-1][v_rep])
+        lb_e = grp_block[g_idx]
+        key = lb_e * n_cb + visit_col[v_rep]
+        group_xoff = _lookup_offsets(src, key, missing=-1)
+        group_hoff = _lookup_offsets(dst, key, missing=None)
+        if (group_hoff < 0).any():
+            bad = int(np.flatnonzero(group_hoff < 0)[0])
+            raise PatternError(f"destination pattern misses column block {int(key[bad] % n_cb)} "
+                               f"in local block row {int(key[bad] // n_cb)}")
+        # work list
+        sizes = src.col_blocks.sizes
+        if src.support is not None:
+            mask = src.support.local_mask(op.layout)
+            a_cell = op.cell_local_rows_matrix(mask.shape[0])
+            act = (a_cell @ mask.astype(np.int32)).tocsr()
+            act.sum_duplicates()
+            act.sort_indices()
+            p_cell = np.repeat(np.arange(n_cells, dtype=np.int64), np.diff(act.indptr))
+            p_col = act.indices.astype(np.int64)
+            p_cb = src.col_blocks.blocks_of(p_col) if p_col.size else p_col
+            p_lane = p_col - src.col_blocks.starts[p_cb]
+            vkey = visit_cell * n_cb + visit_col
+            pkey = p_cell * n_cb + p_cb
+            pv = np.searchsorted(vkey, pkey)
+            okv = (pv < vkey.size) & (vkey[np.minimum(pv, max(vkey.size - 1, 0))] == pkey)
+            if not okv.all():
+                raise ConsistencyError("column support reaches a cell whose rows have no "
+                                       "stored block for that column block")
+            pair_visit, pair_lane = pv, p_lane
+            self.support_based = True
+        else:
+            lanes = sizes[visit_col]
+            pair_visit = np.repeat(np.arange(n_visits, dtype=np.int64), lanes)
+            starts = np.concatenate([[0], np.cumsum(lanes)])[:-1]
+            pair_lane = np.arange(int(lanes.sum())) - np.repeat(starts, lanes)
+            self.support_based = False
+        colors = None
+        if mode == "color":
+            color = op.cell_color[visit_cell[pair_visit]] if pair_visit.size else np.zeros(0, np.int64)
+            order = np.argsort(color, kind="stable")
+            pair_visit, pair_lane = pair_visit[order], pair_lane[order]
+            colors = np.searchsorted(color[order], np.arange(9)).astype(np.int64)
+        self.n = n
+        self.n_cells = n_cells
+        self.n_visits = n_visits
+        self.n_pairs = int(pair_visit.size)
+        self.visit_cell = visit_cell
+        self.visit_col = visit_col
+        self.pair_visit = pair_visit
+        self.lane_groups = int(np.sum((src.col_strides[visit_col] + src.lane_width - 1) // src.lane_width))
+        self.dof_lane_slots = int(n3 * np.sum(src.col_strides[visit_col]))
+        self.cells_visited = int(np.unique(visit_cell).size)
+        self.mode = mode
+        arrs = dict(
+            pair_visit=np.ascontiguousarray(pair_visit, dtype=np.int32),
+            pair_lane=np.ascontiguousarray(pair_lane, dtype=np.int32),
+            visit_cell=np.ascontiguousarray(visit_cell, dtype=np.int32),
+            visit_stride=np.ascontiguousarray(src.col_strides[visit_col], dtype=np.int32),
+            visit_goff=np.ascontiguousarray(visit_goff[:-1], dtype=np.int64),
+            group_xoff=np.ascontiguousarray(group_xoff, dtype=np.int64),
+            group_hoff=np.ascontiguousarray(group_hoff, dtype=np.int64),
+            cell_slots=np.ascontiguousarray(op.cell_slots, dtype=np.uint32),
+            color_pair_start=None if colors is None else np.ascontiguousarray(colors),
+        )
+        self.arrays = arrs
+        self.n_groups_total = total
+        self.colors = colors
+        self.handle = None
+        self.launches = 0
+        if upload:
+            self.upload(op)
+
+    def upload(self, op):
+        n, arrs, colors = self.n, self.arrays, self.colors
+        lib = _lib.load()
+        d = _lib.CellopDesc()
+        d.n, d.n_cells, d.n_visits = n, self.n_cells, self.n_visits
+        d.n_pairs, d.n_groups_total = self.n_pairs, self.n_groups_total
+        d.n_colors = 0 if colors is None else 8
+        d.color_pair_start = _lib.ptr(arrs["color_pair_start"], C.c_int64)
+        for name, ct in (("pair_visit", C.c_int32), ("pair_lane", C.c_int32),
+                         ("visit_cell", C.c_int32), ("visit_stride", C.c_int32),
+                         ("visit_goff", C.c_int64), ("group_xoff", C.c_int64),
+                         ("group_hoff", C.c_int64), ("cell_slots", C.c_uint32)):
+            setattr(d, name, _lib.ptr(arrs[name], ct))
+        sh = op.shape
+        dco = collocation_derivative(sh)
+        for i in range(n):
+            d.w[i] = float(sh.weights[i])
+            for j in range(n):
+                d.S[i * n + j] = float(sh.values[i, j])
+                d.Dco[i * n + j] = float(dco[i, j])
+        ker = op.kernels
+        for k in range(3):
+            d.kin[k] = ker.det * ker.grad_scale[k]
+        d.det = ker.det
+        raw = C.c_void_p()
+        _lib.check(lib.bmv_cellop_create(C.byref(d), C.byref(raw)), "bmv_cellop_create")
+        self.handle = _lib.Handle("bmv_cellop_destroy", raw)
+        nl = C.c_int32()
+        _lib.check(lib.bmv_cellop_launches(self.handle.raw, C.byref(nl)))
+        self.launches = int(nl.value)
+
+
+def _lookup_offsets(m: BlockCsrMatrix, key: np.ndarray, missing):
+    keys = m.local_keys()
+    pos = np.searchsorted(keys, key)
+    if keys.size == 0:
+        return np.full(key.size, -1, dtype=np.int64)
+    ok = (pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == key)
+    out = np.full(key.size, -1, dtype=np.int64)
+    out[ok] = m.block_offsets[pos[ok]]
+    return out
+
+
+class CellOperator:
+    """Rank-local matrix-free operator bound to a mesh and a row layout."""
+
+    def __init__(self, mesh: StructuredMesh, partition: CellPartition,
+                 numbering: DofNumbering, layout: RankLayout):
+        self.mesh = mesh
+        self.partition = partition
+        self.numbering = numbering
+        self.layout = layout
+        self.cells = partition.cells_of_rank(layout.rank)
+        self.shape = shape_info(numbering.degree)
+        self.kernels = _CellKernels(self.shape, mesh.spacing)
+        rows = cells_nodes(mesh, numbering, self.cells)
+        n3 = (numbering.degree + 1) ** 3
+        rows = rows.reshape(len(self.cells), n3)
+        lb, rib = layout.map_rows(rows.ravel())
+        lb = lb.reshape(rows.shape)
+        rib = rib.reshape(rows.shape)
+        self.slot_group, self.grp_cell, self.grp_block, self.cell_gstart = \
+            _first_occurrence_groups(lb)
+        if self.slot_group.size and (int(self.slot_group.max()) > 255 or int(rib.max()) >= 1 << 24):
+            raise ConsistencyError("cell touches more than 256 block rows or a block row > 2^24 rows")
+        self.cell_slots = (self.slot_group << 24) | rib
+        self._lb, self._rib = lb, rib
+        self._cell_map = None
+        if len(self.cells):
+            ijk = mesh.cells_ijk(self.cells)
+            self.cell_origins = np.asarray(mesh.origin) + ijk * np.asarray(mesh.spacing)
+            self.cell_color = (ijk[:, 0] & 1) + 2 * (ijk[:, 1] & 1) + 4 * (ijk[:, 2] & 1)
+        else:
+            self.cell_origins = np.zeros((0, 3))
+            self.cell_color = np.zeros(0, dtype=np.int64)
+        self._plans: dict = {}
+        self._coefs: dict = {}
+        self._dev_tables = None
+
+    @property
+    def cell_map(self) -> CellDoFMap:
+        if self._cell_map is None:
+            self._cell_map = build_cell_dof_map(self.mesh, self.numbering, self.layout, self.cells)
+        return self._cell_map
+
+    def cell_local_rows_matrix(self, n_local_rows: int) -> sparse.csr_matrix:
+        starts = np.concatenate([[0], np.cumsum(self.layout.local_row_counts())]).astype(np.int64)
+        loc = starts[self._lb] + self._rib
+        n_cells, n3 = loc.shape
+        return sparse.csr_matrix((np.ones(loc.size, dtype=np.int32), loc.ravel(),
+                                  np.arange(0, loc.size + 1, n3)), shape=(n_cells, n_local_rows))
+
+    # -- plans and coefficients -----------------------------------------------
+
+    def plan_for(self, src: BlockCsrMatrix, dst: BlockCsrMatrix) -> _CellPlan:
+        mode = _scatter_mode()
+        key = (id(src.pattern), id(src.support), id(dst.pattern), mode)
+        plan = self._plans.get(key)
+        if plan is None:
+            plan = _CellPlan(self, src, dst, mode)
+            self._plans[key] = (plan, src.pattern, src.support, dst.pattern)
+            return plan
+        return plan[0]
+
+    def _device_tables(self, device):
+        if self._dev_tables is None:
+            f = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=device)
+            self._dev_tables = (f(self.cell_origins.reshape(-1, 3)), f(self.kernels.quad_offsets),
+                                f(self.kernels.w3.ravel()))
+        return self._dev_tables
+
+    def coefficient(self, spec: OperatorSpec, device):
+        """(device tensor or None, cell stride) of the quadrature coefficient."""
+        q3 = self.shape.n_q ** 3
+        if spec.kind == MASS:
+            key = ("mass",)
+        elif spec.kind == HAMILTONIAN:
+            if spec.potential is None:
+                return None, 0
+            key = ("pot", id(spec.potential)) if callable(spec.potential) else ("const", float(spec.potential))
+        else:
+            raise ShapeError(f"unknown operator kind {spec.kind!r}")
+        hit = self._coefs.get(key)
+        if hit is not None:
+            return hit[0], hit[1]
+        w3 = self.kernels.w3.ravel()
+        if key[0] == "mass":
+            coef, stride = torch.as_tensor(w3.copy(), device=device), 0
+        elif key[0] == "const":
+            coef, stride = torch.as_tensor(w3 * float(spec.potential), device=device), 0
+        elif isinstance(spec.potential, GaussianPotential):
+            pot = spec.potential
+            n_cells = len(self.cells)
+            org, qoff, w3d = self._device_tables(device)
+            cen = torch.as_tensor(pot.centers, dtype=torch.float64, device=device)
+            coef = torch.zeros(max(n_cells, 1) * q3, dtype=torch.float64, device=device)
+            lib = _lib.require_device()
+            chunk = 4096
+            for c0 in range(0, max(pot.centers.shape[0], 1), chunk):
+                part = cen[c0 : c0 + chunk]
+                tmp = torch.empty_like(coef)
+                _lib.check(lib.bmv_potential_gaussian(
+                    n_cells, q3, _lib.dptr(org), _lib.dptr(qoff), _lib.dptr(w3d), _lib.dptr(part),
+                    int(part.shape[0]), pot.inv_sigma2, pot.scale, _lib.dptr(tmp),
+                    _lib.stream_handle(device)), "bmv_potential_gaussian")
+                coef += tmp
+            stride = q3
+        else:
+            n_cells = len(self.cells)
+            vals = np.empty((n_cells, q3))
+            step = 4096
+            for c0 in range(0, n_cells, step):
+                pts = (self.cell_origins[c0 : c0 + step, None, :]
+                       + self.kernels.quad_offsets[None, :, :]).reshape(-1, 3)
+                vals[c0 : c0 + step] = spec.sample_potential(pts).reshape(-1, q3)
+            coef, stride = torch.as_tensor((vals * w3[None, :]).ravel(), device=device), q3
+        self._coefs[key] = (coef, stride, spec.potential)
+        return coef, stride
+
+    # -- apply ------------------------------------------------------------------
+
+    def apply(self, spec: OperatorSpec, src: BlockCsrMatrix, dst: BlockCsrMatrix,
+              variant: str = SUMFAC, counters: OpCounters | None = None):
+        """dst = Op(spec) @ src over the rank's cells, then compress dst."""
+        if src.layout is not self.layout or dst.layout is not self.layout:
+            raise ShapeError("operator and operands must share one rank layout")
+        if src.col_blocks != dst.col_blocks or src.lane_width != dst.lane_width:
+            raise ShapeError("src and dst must share column blocking and lanes")
+        if variant not in (SUMFAC, GEMM):
+            raise ShapeError(f"unknown operator variant {variant!r}")
+        if spec.kind not in (MASS, HAMILTONIAN):
+            raise ShapeError(f"unknown operator kind {spec.kind!r}")
+        lib = _lib.require_device()
+        dst.ensure_owned()
+        plan = self.plan_for(src, dst)
+        coef, stride = self.coefficient(spec, dst.device)
+        src.update_ghost_values()
+        _lib.check(lib.bmv_cellop_apply(
+            plan.handle.raw, 1 if spec.kind == HAMILTONIAN else 0,
+            _lib.dptr(coef) if coef is not None else C.c_void_p(None), stride,
+            _lib.dptr(src.data), _lib.dptr(dst.data), dst.data.numel(),
+            _lib.stream_handle(dst.device)), "bmv_cellop_apply")
+        src.release_ghosts()
+        dst.compress()
+        if counters is not None:
+            self._count(spec, variant, plan, src, dst, counters)
+
+    def _count(self, spec, variant, plan, src, dst, counters):
+        n = plan.n
+        w = src.lane_width
+        with_v = spec.kind == HAMILTONIAN and spec.potential is not None
+        if variant == GEMM:
+            counters.flops += plan.lane_groups * 2 * (n**3) ** 2 * w
+        else:
+            counters.flops += plan.lane_groups * sumfac_flops_per_lane(n, spec.kind, with_v) * w
+        counters.cells_visited += plan.cells_visited
+        counters.col_blocks_visited += plan.n_visits
+        counters.dof_lane_slots += plan.dof_lane_slots
+        ghost_vals = sum(len(g.rows) * src.pattern.row_cols(g.block).size
+                         for g in self.layout.ghost_groups)
+        counters.bytes_moved += 8 * (src.data.numel() + 2 * dst.data.numel()) + 16 * ghost_vals
+        counters.add_extra("pairs", plan.n_pairs)
+        counters.add_extra("flops_implemented",
+                           plan.n_pairs * implemented_flops_per_pair(n, spec.kind, with_v))
+        counters.add_extra("kernel_launches", plan.launches)
+
+
+def flop_report(variant, mesh, spec, pattern, partition, numbering, lane_width=8) -> dict:
+    """Analytic accounting of one serial application (`matfree.py:578-611`); no launch."""
+    layout = serial_layout(numbering.row_blocks)
+    grown = grow_sparsity_for_operator(pattern, mesh, numbering)
+    op = CellOperator(mesh, partition, numbering, layout)
+    src = BlockCsrMatrix(pattern, layout, None, lane_width, device="cpu")
+    visits = 0
+    slots = 0
+    lane_groups = 0
+    for ci in range(len(op.cells)):
+        cols = RowsBlockAccessor(src, op.cell_map).emitted_columns(ci)
+        visits += len(cols)
+        strides = src.col_strides[np.asarray(cols, dtype=np.int64)] if cols else np.zeros(0, np.int64)
+        slots += int(op.cell_map.n_cell_dofs * strides.sum())
+        lane_groups += int(((strides + lane_width - 1) // lane_width).sum())
+    n = numbering.degree + 1
+    with_v = spec.kind == HAMILTONIAN and spec.potential is not None
+    if variant == GEMM:
+        flops = lane_groups * 2 * (n**3) ** 2 * lane_width
+    else:
+        flops = lane_groups * sumfac_flops_per_lane(n, spec.kind, with_v) * lane_width
+    dst_vals = BlockCsrMatrix(grown, layout, None, lane_width, device="cpu").data.numel()
+    return {"variant": variant, "kind": spec.kind, "flops": flops, "dof_lane_slots": slots,
+            "flops_per_dof": flops / slots if slots else 0.0, "col_blocks_visited": visits,
+            "cells_visited": int(len(op.cells)),
+            "bytes_est": 8 * (src.data.numel() + 2 * dst_vals)}

@@ -1,0 +1,362 @@
+"""BASELINE workloads: configs, seeded inputs, per-rank operand setup.
+
+The five configs of BASELINE.json, built with this package's (bit-exact)
+setup functions and the choices of SURVEY section 0.1: coarse level 0,
+column blocks of B = 8, one vector per centre (M1-M3), values
+2 * hashed_values(seed, row, original column) masked by the support (M4,
+the reference's splitmix64 counter hash, `bench/problem.py:85-131`),
+Y = second multivector with seed 2 (M5), Y = X C on X's own pattern (M6),
+C on the projected pattern with entries only where supports overlap (M7),
+weak-scaling lattice offset of half a spacing (M8), reference Hilbert
+partition (M9).  The potential is -sum_c exp(-|x-c|^2/sigma^2) over all
+centres.  Inputs are synthetic (no public dataset exists for this path).
+
+Fills are vectorised: one hash per stored entry and one sorted-key
+membership test, identical to the reference's per-block `np.isin` fill.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+from scipy import sparse
+
+from .bcsr import BlockCsrMatrix, _IndexList
+from .blocks import BlockSparsityPattern
+from .energy import column_space_ghost_blocks, make_column_layout, projected_pattern
+from .localization import (
+    build_support_sparsity,
+    column_supports,
+    grow_sparsity_for_operator,
+    order_and_block_columns,
+    patch_fine_cells,
+)
+from .matfree import CellOperator, GaussianPotential, make_dof_layout, hamiltonian_operator
+from .mesh import build_mesh, cells_nodes, enumerate_dofs, partition_and_order_cells
+from .support import ColumnSupport, attach_support
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _mix64(x: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser on uint64 arrays (wrapping arithmetic)."""
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
+def hashed_entries(seed: int, rows, cols) -> np.ndarray:
+    """Elementwise hashed value in [-0.5, 0.5) of (seed, row, col) triples."""
+    r = np.asarray(rows, dtype=np.int64).astype(np.uint64)
+    c = np.asarray(cols, dtype=np.int64).astype(np.uint64)
+    with np.errstate(over="ignore"):
+        h = _mix64(r * np.uint64(0x9E3779B97F4A7C15) + c * np.uint64(0xD1B54A32D192ED03)
+                   + np.uint64(seed & 0xFFFFFFFFFFFFFFFF))
+    return h.astype(np.float64) / float(2**64) - 0.5
+
+
+def hashed_values(seed: int, rows, cols) -> np.ndarray:
+    """Outer-product form (rows x cols), same values as the reference helper."""
+    r = np.asarray(rows, dtype=np.int64)
+    c = np.asarray(cols, dtype=np.int64)
+    return hashed_entries(seed, np.repeat(r, c.size), np.tile(c, r.size)).reshape(r.size, c.size)
+
+
+@dataclass
+class ProblemConfig:
+    name: str
+    extents: tuple
+    degree: int
+    centers: np.ndarray
+    radius: float
+    sigma: float
+    spacing: tuple | None = None
+    dirichlet: bool = False
+    kernels: tuple = ("apply_h",)
+    block_size: int = 8
+    lane_width: int = 8
+    vectors_per_center: int = 1
+    coarse_level: int = 0
+    seed_x: int = 1
+    seed_y: int = 2
+    seed_c: int = 7
+    note: str = ""
+
+    def __post_init__(self):
+        if self.spacing is None:
+            self.spacing = tuple(1.0 / self.extents[0] for _ in range(3))
+
+
+def lattice(counts, spacing, offset) -> np.ndarray:
+    """Centres offset + spacing * (i, j, k), x fastest."""
+    nx, ny, nz = counts
+    k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    ijk = np.stack([i.ravel(), j.ravel(), k.ravel()], axis=1).astype(float)
+    return np.asarray(offset, dtype=float) + ijk * np.asarray(spacing, dtype=float)
+
+
+def baseline_config(name: str, n_ranks: int = 1) -> ProblemConfig:
+    """BASELINE.json configs[0..4] ('smoke', 'q2', 'q4', 'proj', 'weak')."""
+    if name == "smoke":
+        c = lattice((2, 2, 2), 0.5, 0.25)
+        return ProblemConfig("smoke", (8, 8, 8), 2, c, 0.3, 0.2, dirichlet=True,
+                             kernels=("apply_h", "tmmult", "mmult"),
+                             note="CPU-oracle smoke: 8^3 Q2, M=8, r=0.3, sigma=0.2")
+    if name in ("q2", "q4"):
+        c = lattice((4, 4, 4), 0.25, 0.125)
+        deg = 2 if name == "q2" else 4
+        return ProblemConfig(name, (32, 32, 32), deg, c, 0.25, 0.1,
+                             note=f"32^3 Q{deg}, M=64 lattice 0.25 offset 0.125, r=0.25, sigma=0.1")
+    if name == "proj":
+        c = lattice((8, 8, 8), 1.0 / 8, 1.0 / 16)
+        return ProblemConfig("proj", (64, 64, 64), 2, c, 1.5 / 8, 0.1,
+                             kernels=("apply_h", "tmmult", "mmult"),
+                             note="64^3 Q2, M=512 lattice 1/8, r=1.5/8, sigma=0.1")
+    if name.startswith("weak"):
+        g = int(name[4:]) if len(name) > 4 else int(n_ranks)
+        h = 1.0 / 64
+        c = lattice((8, 8, 8 * g), 8 * h, 4 * h)
+        return ProblemConfig(f"weak{g}", (64, 64, 64 * g), 4, c, 8 * h, 2 * h,
+                             spacing=(h, h, h), kernels=("apply_h", "tmmult", "mmult"),
+                             note=f"weak G={g}: 64x64x{64 * g} Q4, M={512 * g}, r=8h, sigma=2h")
+    raise ValueError(f"unknown config {name!r}")
+
+
+@dataclass
+class Problem:
+    cfg: ProblemConfig
+    mesh: object
+    partition: object
+    numbering: object
+    loc_layout: object
+    supports: list
+    pattern: BlockSparsityPattern
+    grown: BlockSparsityPattern
+    potential: GaussianPotential
+    n_ranks: int
+    _proj: BlockSparsityPattern | None = None
+    _support: ColumnSupport | None = None
+    _overlap: sparse.csr_matrix | None = None
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def proj_pattern(self) -> BlockSparsityPattern:
+        if self._proj is None:
+            self._proj = projected_pattern(self.pattern, self.grown)
+        return self._proj
+
+    @property
+    def column_support(self) -> ColumnSupport:
+        if self._support is None:
+            self._support = ColumnSupport.from_localization(self.loc_layout, self.supports,
+                                                            self.numbering.n_dofs)
+        return self._support
+
+    def spec_h(self):
+        return hamiltonian_operator(self.potential)
+
+    def support_overlap(self) -> sparse.csr_matrix:
+        """(M x M) bool CSR, new column order: True where two supports share a row.
+
+        Two node sets of cell patches intersect iff a cell of one patch and a
+        cell of the other share a node, i.e. lie within one cell per axis.
+        """
+        if self._overlap is not None:
+            return self._overlap
+        lay = self.loc_layout
+        mesh = self.mesh
+        nc = lay.centers.shape[0]
+        rows, cols = [], []
+        for c in range(nc):
+            cells = patch_fine_cells(mesh, lay, c)
+            rows.append(np.full(cells.size, c))
+            cols.append(cells)
+        P = sparse.csr_matrix((np.ones(sum(r.size for r in rows), dtype=np.int32),
+                               (np.concatenate(rows), np.concatenate(cols))),
+                              shape=(nc, mesh.n_cells))
+        P.sum_duplicates()
+        # dilate by one cell layer (26-neighbourhood) on the structured grid
+        nx, ny, nz = mesh.extents
+        coo = P.tocoo()
+        ijk = mesh.cells_ijk(coo.col)
+        dr, dc = [], []
+        for dz in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    q = ijk + np.asarray([dx, dy, dz])
+                    ok = ((q[:, 0] >= 0) & (q[:, 0] < nx) & (q[:, 1] >= 0) & (q[:, 1] < ny)
+                          & (q[:, 2] >= 0) & (q[:, 2] < nz))
+                    dr.append(coo.row[ok])
+                    dc.append(q[ok, 0] + nx * (q[ok, 1] + ny * q[ok, 2]))
+        D = sparse.csr_matrix((np.ones(sum(a.size for a in dr), dtype=np.int32),
+                               (np.concatenate(dr), np.concatenate(dc))), shape=(nc, mesh.n_cells))
+        D.sum_duplicates()
+        ov = (D @ P.T).tocsr()
+        ov.data[:] = 1
+        # centre order -> new column order
+        new_of_center = lay.new_col_of_old.reshape(nc, lay.vectors_per_center)
+        v = lay.vectors_per_center
+        coo = ov.tocoo()
+        r = new_of_center[coo.row].ravel() if v == 1 else None
+        if v == 1:
+            out = sparse.csr_matrix((np.ones(coo.nnz, dtype=bool),
+                                     (new_of_center[coo.row, 0], new_of_center[coo.col, 0])),
+                                    shape=(nc, nc))
+        else:
+            rr = new_of_center[coo.row][:, :, None].repeat(v, 2).ravel()
+            cc = new_of_center[coo.col][:, None, :].repeat(v, 1).ravel()
+            out = sparse.csr_matrix((np.ones(rr.size, dtype=bool), (rr, cc)), shape=(nc * v, nc * v))
+        out.sum_duplicates()
+        out.sort_indices()
+        self._overlap = out
+        return out
+
+
+def build_problem(cfg: ProblemConfig | str, n_ranks: int = 1) -> Problem:
+    if isinstance(cfg, str):
+        cfg = baseline_config(cfg, n_ranks)
+    mesh = build_mesh(cfg.extents, cfg.spacing, cfg.coarse_level)
+    partition = partition_and_order_cells(mesh, n_ranks)
+    numbering = enumerate_dofs(mesh, partition, cfg.degree)
+    lay = order_and_block_columns(mesh, partition, cfg.centers, cfg.radius,
+                                  cfg.vectors_per_center, cfg.block_size)
+    supports = column_supports(mesh, numbering, lay)
+    pattern = build_support_sparsity(mesh, partition, numbering, lay, supports)
+    grown = grow_sparsity_for_operator(pattern, mesh, numbering)
+    pot = GaussianPotential(cfg.centers, cfg.sigma, -1.0)
+    return Problem(cfg, mesh, partition, numbering, lay, supports, pattern, grown, pot, n_ranks)
+
+
+def _support_keys(prob: Problem) -> np.ndarray:
+    """Sorted keys center * n_dofs + row of every (centre, support row)."""
+    keys = prob.extra.get("support_keys")
+    if keys is None:
+        n = prob.numbering.n_dofs
+        keys = np.concatenate([c * n + np.asarray(s, dtype=np.int64)
+                               for c, s in enumerate(prob.supports)])
+        keys.sort()
+        prob.extra["support_keys"] = keys
+    return keys
+
+
+def in_support(prob: Problem, rows, new_cols) -> np.ndarray:
+    lay = prob.loc_layout
+    centre = lay.old_col_of_new[np.asarray(new_cols, dtype=np.int64)] // lay.vectors_per_center
+    key = centre * prob.numbering.n_dofs + np.asarray(rows, dtype=np.int64)
+    keys = _support_keys(prob)
+    pos = np.searchsorted(keys, key)
+    return (pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == key)
+
+
+def fill_multivector(matrix: BlockCsrMatrix, prob: Problem, seed: int, attach: bool = True):
+    """X[r, c] = 2 * hash(seed, r, old(c)) on the support of c, else 0."""
+    old = prob.loc_layout.old_col_of_new
+
+    def values(grow, gcol):
+        v = 2.0 * hashed_entries(seed, grow, old[gcol])
+        return np.where(in_support(prob, grow, gcol), v, 0.0)
+
+    matrix.fill_owned_entries(values)
+    if attach:
+        attach_support(matrix, prob.column_support, check=False)
+    return matrix
+
+
+def fill_projected(matrix: BlockCsrMatrix, prob: Problem, seed: int):
+    """C[a, b] = 2 * hash(seed, old(a), old(b)) where supports of a, b overlap."""
+    old = prob.loc_layout.old_col_of_new
+    ov = prob.support_overlap()
+
+    def values(grow, gcol):
+        v = 2.0 * hashed_entries(seed, old[grow], old[gcol])
+        key = grow * ov.shape[1] + gcol
+        okeys = np.repeat(np.arange(ov.shape[0], dtype=np.int64), np.diff(ov.indptr)) * ov.shape[1] \
+            + ov.indices
+        pos = np.searchsorted(okeys, key)
+        hit = (pos < okeys.size) & (okeys[np.minimum(pos, okeys.size - 1)] == key)
+        return np.where(hit, v, 0.0)
+
+    matrix.fill_owned_entries(values)
+    return matrix
+
+
+def dirichlet_rows(prob: Problem) -> np.ndarray:
+    """Global rows of the nodes on the boundary of the box."""
+    mesh, p = prob.mesh, prob.numbering.degree
+    sx, sy, sz = mesh.node_grid_shape(p)
+    k, j, i = np.meshgrid(np.arange(sz), np.arange(sy), np.arange(sx), indexing="ij")
+    bnd = ((i == 0) | (i == sx - 1) | (j == 0) | (j == sy - 1) | (k == 0) | (k == sz - 1)).ravel()
+    return np.sort(prob.numbering.new_index_of_node[np.flatnonzero(bnd)])
+
+
+class DirichletMask:
+    """Zero the boundary rows of a multivector (optional mask)."""
+
+    def __init__(self, matrix: BlockCsrMatrix, rows: np.ndarray):
+        lo, hi = matrix.layout.owned_rows
+        rows = np.asarray(rows, dtype=np.int64)
+        rows = rows[(rows >= lo) & (rows < hi)]
+        lb, rib = matrix.layout.map_rows(rows)
+        idx = []
+        for l, r in zip(lb.tolist(), rib.tolist()):
+            for pos in range(int(matrix.row_start[l]), int(matrix.row_start[l + 1])):
+                cols = int(matrix.col_blocks.sizes[matrix.col_index[pos]])
+                stride = int(matrix.col_strides[matrix.col_index[pos]])
+                base = int(matrix.block_offsets[pos]) + r * stride
+                idx.append(np.arange(base, base + cols))
+        self.index = _IndexList(np.concatenate(idx) if idx else np.zeros(0, np.int64), matrix.device)
+        self._zeros = None
+
+    def apply(self, matrix: BlockCsrMatrix):
+        import torch
+
+        if self._zeros is None or self._zeros.device != matrix.data.device:
+            self._zeros = torch.zeros(self.index.size, dtype=torch.float64, device=matrix.data.device)
+        self.index.scatter(self._zeros, matrix.data, add=False)
+
+
+@dataclass
+class RankSetup:
+    """Per-rank operands of one workload."""
+
+    prob: Problem
+    ctx: object
+    layout: object
+    op: CellOperator
+    x: BlockCsrMatrix
+    hx: BlockCsrMatrix
+    y: BlockCsrMatrix | None = None
+    hy: BlockCsrMatrix | None = None
+    s: BlockCsrMatrix | None = None
+    c: BlockCsrMatrix | None = None
+    xc: BlockCsrMatrix | None = None
+    dirichlet: tuple | None = None
+
+
+def make_rank_setup(ctx, prob: Problem, projection: bool | None = None, device=None) -> RankSetup:
+    cfg = prob.cfg
+    layout = make_dof_layout(ctx, prob.mesh, prob.partition, prob.numbering)
+    op = CellOperator(prob.mesh, prob.partition, prob.numbering, layout)
+    w = cfg.lane_width
+    x = fill_multivector(BlockCsrMatrix(prob.pattern, layout, ctx, w, device), prob, cfg.seed_x)
+    hx = BlockCsrMatrix(prob.grown, layout, ctx, w, device)
+    st = RankSetup(prob, ctx, layout, op, x, hx)
+    if cfg.dirichlet:
+        rows = dirichlet_rows(prob)
+        st.dirichlet = (DirichletMask(x, rows), DirichletMask(hx, rows))
+    if projection is None:
+        projection = "tmmult" in cfg.kernels or "mmult" in cfg.kernels
+    if projection:
+        lay = prob.loc_layout
+        proj = prob.proj_pattern
+        ghosts = column_space_ghost_blocks(prob.grown, proj, layout, lay.rank_block_start, ctx.rank)
+        clayout = make_column_layout(ctx, lay.column_blocks, lay.rank_block_start, ghosts)
+        st.y = fill_multivector(BlockCsrMatrix(prob.pattern, layout, ctx, w, device), prob, cfg.seed_y)
+        st.hy = BlockCsrMatrix(prob.grown, layout, ctx, w, device)
+        st.s = BlockCsrMatrix(proj, clayout, ctx, w, device)
+        st.c = fill_projected(BlockCsrMatrix(proj, clayout, ctx, w, device), prob, cfg.seed_c)
+        st.xc = BlockCsrMatrix(prob.pattern, layout, ctx, w, device)
+    return st

@@ -105,15 +105,25 @@ int bmv_potential_gaussian(int64_t n_cells, int32_t q3, const double* cell_origi
 int bmv_cellop_launches(const bmv_cellop* plan, int32_t* out);
 
 /* ------------------------------------------------------------------ K4 --
- * C(k,l) += A_ik^T B_il over triples grouped by output block.            */
+ * C(k,l) = sum_i A_ik^T B_il over triples (i, A block, B block).  Triples are
+ * cut into segments (one output block within one chunk of consecutive block
+ * rows); one warp per segment accumulates its triples into a partial block,
+ * then each output block sums its segments' partials in chunk order (fixed
+ * order -> bit-reproducible, no atomics).                                */
 typedef struct {
   int64_t n_out;             /* output blocks with work                    */
+  int64_t n_seg;             /* segments                                   */
   int64_t n_triples;
+  int64_t partial_len;       /* doubles of partial storage                 */
   const int64_t* out_off;    /* element offset of the C block              */
   const int32_t* out_rows;   /* valid rows (size of column block k)        */
   const int32_t* out_cols;   /* valid cols (size of column block l)        */
   const int32_t* out_stride; /* C row stride                               */
-  const int64_t* tri_start;  /* n_out + 1                                  */
+  const int64_t* out_seg_start; /* n_out + 1, into out_seg_list            */
+  const int64_t* out_seg_list;  /* n_seg segment ids, chunk order per out  */
+  const int64_t* seg_out;       /* n_seg: output index of the segment      */
+  const int64_t* seg_tri_start; /* n_seg + 1, into the triple arrays       */
+  const int64_t* seg_poff;      /* n_seg: offset of the partial block      */
   const int64_t* tri_a_off;
   const int64_t* tri_b_off;
   const int32_t* tri_rows;   /* rows of block row i                         */

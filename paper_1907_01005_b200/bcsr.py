@@ -647,53 +647,80 @@ def _plan_cache(obj):
     return cache
 
 
+def _expand(counts: np.ndarray):
+    """(owner index, rank within owner) of sum(counts) expanded items."""
+    counts = np.asarray(counts, dtype=np.int64)
+    owner = np.repeat(np.arange(counts.size, dtype=np.int64), counts)
+    start = np.concatenate([[0], np.cumsum(counts)])[:-1]
+    return owner, np.arange(int(counts.sum()), dtype=np.int64) - start[owner]
+
+
+def _local_block_table(layout: RankLayout, n_global: int) -> np.ndarray:
+    """Local block id of every global block (-1 when neither owned nor ghost)."""
+    tab = np.full(n_global, -1, dtype=np.int64)
+    gl = layout.global_blocks_of_locals()
+    tab[gl] = np.arange(gl.size, dtype=np.int64)
+    return tab
+
+
+def _group_by_output(out_pos: np.ndarray):
+    """Stable grouping of work items by output block: (order, unique outputs, starts)."""
+    order = np.argsort(out_pos, kind="stable")
+    sp = out_pos[order]
+    uniq, first = np.unique(sp, return_index=True)
+    start = np.concatenate([first, [sp.size]]).astype(np.int64)
+    return order, uniq, start
+
+
 def _mmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
-    """Output-block ordered list of (A_ik, B_kj) products kept by C's pattern."""
+    """Per output block of C, the (A_ik, B_kj) products kept by C's pattern,
+    in the reference's Gustavson order (bcsr.py:605-626)."""
     key = ("mm", id(b), id(c))
     cache = _plan_cache(a)
     hit = cache.get(key)
     if hit is not None:
-        return hit
-    outs = {}
-    n_own = a.n_owned_blocks
-    for i in range(n_own):
-        for pos_a in range(int(a.row_start[i]), int(a.row_start[i + 1])):
-            k = int(a.col_index[pos_a])
-            kb = b.layout.local_block_of_global(k)
-            if b.local_row_sizes[kb] != a.col_blocks.sizes[k]:
-                raise ShapeError(f"row block {k} of b is incomplete (split ghost group)")
-            c_pos, c_end = int(c.row_start[i]), int(c.row_start[i + 1])
-            for pos_b in range(int(b.row_start[kb]), int(b.row_start[kb + 1])):
-                j = int(b.col_index[pos_b])
-                while c_pos < c_end and c.col_index[c_pos] < j:
-                    c_pos += 1
-                if c_pos == c_end:
-                    break
-                if c.col_index[c_pos] == j:
-                    outs.setdefault(c_pos, []).append((pos_a, pos_b))
-    order = sorted(outs)
-    n_out = len(order)
-    out_off = np.asarray([c.block_offsets[p] for p in order], dtype=np.int64)
-    out_rows = np.asarray([c.local_row_sizes[c.pos_row[p]] for p in order], dtype=np.int32)
-    out_cols = np.asarray([c.col_blocks.sizes[c.col_index[p]] for p in order], dtype=np.int32)
-    out_stride = np.asarray([c.col_strides[c.col_index[p]] for p in order], dtype=np.int32)
-    lists = [outs[p] for p in order]
-    start = np.concatenate([[0], np.cumsum([len(l) for l in lists])]).astype(np.int64)
-    pa = np.asarray([x for l in lists for x, _ in l], dtype=np.int64)
-    pb = np.asarray([y for l in lists for _, y in l], dtype=np.int64)
-    desc_arrays = dict(
-        out_off=out_off, out_rows=out_rows, out_cols=out_cols, out_stride=out_stride,
+        return hit[0]
+    n_own_pos = int(a.row_start[a.n_owned_blocks])
+    pos_a = np.arange(n_own_pos, dtype=np.int64)
+    k = a.col_index[pos_a]
+    kb = _local_block_table(b.layout, b.layout.blocks.n_blocks)[k]
+    if (kb < 0).any():
+        raise PatternError(f"rank {b.layout.rank} holds no ghost of block row {int(k[kb < 0][0])}")
+    if (b.local_row_sizes[kb] != a.col_blocks.sizes[k]).any():
+        bad = int(k[b.local_row_sizes[kb] != a.col_blocks.sizes[k]][0])
+        raise ShapeError(f"row block {bad} of b is incomplete (split ghost group)")
+    nb = b.row_start[kb + 1] - b.row_start[kb]
+    owner, r = _expand(nb)
+    pa = pos_a[owner]
+    pb = b.row_start[kb[owner]] + r
+    i = a.pos_row[pa]
+    ckey = i * c.col_blocks.n_blocks + b.col_index[pb]
+    ckeys = c.local_keys()
+    cp = np.searchsorted(ckeys, ckey)
+    ok = (cp < ckeys.size) & (ckeys[np.minimum(cp, max(ckeys.size - 1, 0))] == ckey) \
+        if ckeys.size else np.zeros(ckey.size, dtype=bool)
+    pa, pb, cp = pa[ok], pb[ok], cp[ok]
+    order, outs, start = _group_by_output(cp)
+    pa, pb = pa[order], pb[order]
+    n_out = int(outs.size)
+    arrays = dict(
+        out_off=c.block_offsets[outs].astype(np.int64),
+        out_rows=c.local_row_sizes[c.pos_row[outs]].astype(np.int32),
+        out_cols=c.col_blocks.sizes[c.col_index[outs]].astype(np.int32),
+        out_stride=c.col_strides[c.col_index[outs]].astype(np.int32),
         pair_start=start,
-        pair_a_off=a.block_offsets[pa].astype(np.int64) if pa.size else np.zeros(0, np.int64),
-        pair_a_stride=a.col_strides[a.col_index[pa]].astype(np.int32) if pa.size else np.zeros(0, np.int32),
-        pair_inner=a.col_blocks.sizes[a.col_index[pa]].astype(np.int32) if pa.size else np.zeros(0, np.int32),
-        pair_b_off=b.block_offsets[pb].astype(np.int64) if pb.size else np.zeros(0, np.int64),
-        pair_b_stride=b.col_strides[b.col_index[pb]].astype(np.int32) if pb.size else np.zeros(0, np.int32),
+        pair_a_off=a.block_offsets[pa].astype(np.int64),
+        pair_a_stride=a.col_strides[a.col_index[pa]].astype(np.int32),
+        pair_inner=a.col_blocks.sizes[a.col_index[pa]].astype(np.int32),
+        pair_b_off=b.block_offsets[pb].astype(np.int64),
+        pair_b_stride=b.col_strides[b.col_index[pb]].astype(np.int32),
     )
-    flops = int(2 * np.sum(out_rows.astype(np.int64)[np.repeat(np.arange(n_out), np.diff(start))]
-                           * desc_arrays["pair_inner"] * out_cols.astype(np.int64)[np.repeat(np.arange(n_out), np.diff(start))])) if pa.size else 0
-    plan = _MmultPlan(desc_arrays, n_out, int(pa.size), flops)
-    cache[key] = plan
+    per = np.repeat(np.arange(n_out), np.diff(start))
+    flops = int(2 * np.sum(arrays["out_rows"].astype(np.int64)[per]
+                           * arrays["pair_inner"].astype(np.int64)
+                           * arrays["out_cols"].astype(np.int64)[per]))
+    plan = _MmultPlan(arrays, n_out, int(pa.size), flops)
+    cache[key] = (plan, b, c)
     return plan
 
 
@@ -738,53 +765,83 @@ def mmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, alpha: float 
         counters.flops += plan.flops
 
 
+_TM_CHUNK = 256  # triples per row chunk of the K4 plan
+
+
 def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
+    """Per output block of C, the (A_ik, B_il) block products of owned rows i,
+    in the reference loop order (bcsr.py:646-666); PatternError if C lacks one."""
     key = ("tm", id(b), id(c))
     cache = _plan_cache(a)
     hit = cache.get(key)
     if hit is not None:
-        return hit
-    outs = {}
-    for i in range(a.n_owned_blocks):
-        for pos_a in range(int(a.row_start[i]), int(a.row_start[i + 1])):
-            k = int(a.col_index[pos_a])
-            ck = c.layout.local_block_of_global(k)
-            c_pos, c_end = int(c.row_start[ck]), int(c.row_start[ck + 1])
-            for pos_b in range(int(b.row_start[i]), int(b.row_start[i + 1])):
-                ell = int(b.col_index[pos_b])
-                while c_pos < c_end and c.col_index[c_pos] < ell:
-                    c_pos += 1
-                if c_pos == c_end or c.col_index[c_pos] != ell:
-                    raise PatternError(f"tmmult destination misses block ({k}, {ell})")
-                outs.setdefault(c_pos, []).append((pos_a, pos_b, i))
-    order = sorted(outs)
-    lists = [outs[p] for p in order]
-    n_out = len(order)
-    start = np.concatenate([[0], np.cumsum([len(l) for l in lists])]).astype(np.int64)
-    pa = np.asarray([x for l in lists for x, _, _ in l], dtype=np.int64)
-    pb = np.asarray([y for l in lists for _, y, _ in l], dtype=np.int64)
-    ri = np.asarray([z for l in lists for _, _, z in l], dtype=np.int64)
-    e64, e32 = np.zeros(0, np.int64), np.zeros(0, np.int32)
+        return hit[0]
+    n_rows = a.n_owned_blocks
+    na = a.row_start[1 : n_rows + 1] - a.row_start[:n_rows]
+    nb = b.row_start[1 : n_rows + 1] - b.row_start[:n_rows]
+    row, t = _expand(na * nb)
+    nbr = nb[row]
+    pa = a.row_start[row] + t // np.maximum(nbr, 1)
+    pb = b.row_start[row] + t % np.maximum(nbr, 1)
+    k = a.col_index[pa]
+    ck = _local_block_table(c.layout, c.layout.blocks.n_blocks)[k]
+    if (ck < 0).any():
+        raise PatternError(f"rank {c.layout.rank} holds no ghost of block row {int(k[ck < 0][0])}")
+    ell = b.col_index[pb]
+    ckey = ck * c.col_blocks.n_blocks + ell
+    ckeys = c.local_keys()
+    cp = np.searchsorted(ckeys, ckey)
+    ok = (cp < ckeys.size) & (ckeys[np.minimum(cp, max(ckeys.size - 1, 0))] == ckey) \
+        if ckeys.size else np.zeros(ckey.size, dtype=bool)
+    if not ok.all():
+        j = int(np.flatnonzero(~ok)[0])
+        raise PatternError(f"tmmult destination misses block ({int(k[j])}, {int(ell[j])})")
+    if (c.local_row_sizes[c.pos_row[cp]] != a.col_blocks.sizes[k]).any():
+        raise ShapeError("tmmult destination row block is incomplete (split ghost group)")
+    # segments: one output block inside one chunk of consecutive rows holding
+    # about _TM_CHUNK triples; triples keep the reference order inside a segment
+    per_row = na * nb
+    row_chunk = (np.cumsum(per_row) - per_row) // _TM_CHUNK
+    chunk = row_chunk[row]
+    order = np.lexsort((cp, chunk))
+    pa, pb, row, cp, chunk = pa[order], pb[order], row[order], cp[order], chunk[order]
+    n_tri = int(pa.size)
+    first = np.ones(n_tri, dtype=bool)
+    if n_tri:
+        first[1:] = (cp[1:] != cp[:-1]) | (chunk[1:] != chunk[:-1])
+    seg_tri_start = np.concatenate([np.flatnonzero(first), [n_tri]]).astype(np.int64)
+    outs = np.unique(cp)
+    n_out = int(outs.size)
+    seg_out = np.searchsorted(outs, cp[first]).astype(np.int64)
+    seg_chunk = chunk[first]
+    out_rows = c.local_row_sizes[c.pos_row[outs]].astype(np.int64)
+    out_cols = c.col_blocks.sizes[c.col_index[outs]].astype(np.int64)
+    seg_ent = out_rows[seg_out] * out_cols[seg_out]
+    seg_poff = np.concatenate([[0], np.cumsum(seg_ent)]).astype(np.int64)
+    order2 = np.lexsort((seg_chunk, seg_out))
+    out_seg_start = np.searchsorted(seg_out[order2], np.arange(n_out + 1)).astype(np.int64)
     arrays = dict(
-        out_off=np.asarray([c.block_offsets[p] for p in order], dtype=np.int64),
-        out_rows=np.asarray([c.local_row_sizes[c.pos_row[p]] for p in order], dtype=np.int32),
-        out_cols=np.asarray([c.col_blocks.sizes[c.col_index[p]] for p in order], dtype=np.int32),
-        out_stride=np.asarray([c.col_strides[c.col_index[p]] for p in order], dtype=np.int32),
-        tri_start=start,
-        tri_a_off=a.block_offsets[pa].astype(np.int64) if pa.size else e64,
-        tri_b_off=b.block_offsets[pb].astype(np.int64) if pb.size else e64,
-        tri_rows=a.local_row_sizes[ri].astype(np.int32) if ri.size else e32,
-        tri_a_stride=a.col_strides[a.col_index[pa]].astype(np.int32) if pa.size else e32,
-        tri_b_stride=b.col_strides[b.col_index[pb]].astype(np.int32) if pb.size else e32,
+        out_off=c.block_offsets[outs].astype(np.int64),
+        out_rows=out_rows.astype(np.int32),
+        out_cols=out_cols.astype(np.int32),
+        out_stride=c.col_strides[c.col_index[outs]].astype(np.int32),
+        out_seg_start=out_seg_start,
+        out_seg_list=order2.astype(np.int64),
+        seg_out=seg_out,
+        seg_tri_start=seg_tri_start,
+        seg_poff=seg_poff[:-1].copy(),
+        partial_len=int(seg_poff[-1]),
+        tri_a_off=a.block_offsets[pa].astype(np.int64),
+        tri_b_off=b.block_offsets[pb].astype(np.int64),
+        tri_rows=a.local_row_sizes[row].astype(np.int32),
+        tri_a_stride=a.col_strides[a.col_index[pa]].astype(np.int32),
+        tri_b_stride=b.col_strides[b.col_index[pb]].astype(np.int32),
     )
-    if pa.size:
-        kk = a.col_blocks.sizes[a.col_index[pa]].astype(np.int64)
-        ll = b.col_blocks.sizes[b.col_index[pb]].astype(np.int64)
-        flops = int(np.sum(2 * kk * arrays["tri_rows"].astype(np.int64) * ll))
-    else:
-        flops = 0
+    kk = a.col_blocks.sizes[a.col_index[pa]].astype(np.int64)
+    ll = b.col_blocks.sizes[b.col_index[pb]].astype(np.int64)
+    flops = int(np.sum(2 * kk * arrays["tri_rows"].astype(np.int64) * ll))
     plan = _TmmultPlan(arrays, n_out, int(pa.size), flops)
-    cache[key] = plan
+    cache[key] = (plan, b, c)
     return plan
 
 
@@ -796,11 +853,16 @@ class _TmmultPlan:
         lib = _lib.load()
         d = _lib.TmmultDesc()
         d.n_out, d.n_triples = n_out, n_tri
+        d.n_seg = int(arrays["seg_out"].size)
+        d.partial_len = int(arrays["partial_len"])
         for name, ct in (("out_off", _lib.C.c_int64), ("out_rows", _lib.C.c_int32),
                          ("out_cols", _lib.C.c_int32), ("out_stride", _lib.C.c_int32),
-                         ("tri_start", _lib.C.c_int64), ("tri_a_off", _lib.C.c_int64),
-                         ("tri_b_off", _lib.C.c_int64), ("tri_rows", _lib.C.c_int32),
-                         ("tri_a_stride", _lib.C.c_int32), ("tri_b_stride", _lib.C.c_int32)):
+                         ("out_seg_start", _lib.C.c_int64), ("out_seg_list", _lib.C.c_int64),
+                         ("seg_out", _lib.C.c_int64), ("seg_tri_start", _lib.C.c_int64),
+                         ("seg_poff", _lib.C.c_int64),
+                         ("tri_a_off", _lib.C.c_int64), ("tri_b_off", _lib.C.c_int64),
+                         ("tri_rows", _lib.C.c_int32), ("tri_a_stride", _lib.C.c_int32),
+                         ("tri_b_stride", _lib.C.c_int32)):
             arrays[name] = np.ascontiguousarray(arrays[name])
             setattr(d, name, _lib.ptr(arrays[name], ct))
         raw = _lib.C.c_void_p()

@@ -161,54 +161,45 @@ class Problem:
     def support_overlap(self) -> sparse.csr_matrix:
         """(M x M) bool CSR, new column order: True where two supports share a row.
 
-        Two node sets of cell patches intersect iff a cell of one patch and a
-        cell of the other share a node, i.e. lie within one cell per axis.
+        Supports are the nodes of cell patches; two node sets intersect iff a
+        cell of one patch and a cell of the other share a node, i.e. iff the
+        one-cell dilation of the first patch meets the second.  Candidate
+        pairs are pruned by centre distance, then tested exactly on cell ids.
         """
         if self._overlap is not None:
             return self._overlap
         lay = self.loc_layout
         mesh = self.mesh
         nc = lay.centers.shape[0]
-        rows, cols = [], []
-        for c in range(nc):
-            cells = patch_fine_cells(mesh, lay, c)
-            rows.append(np.full(cells.size, c))
-            cols.append(cells)
-        P = sparse.csr_matrix((np.ones(sum(r.size for r in rows), dtype=np.int32),
-                               (np.concatenate(rows), np.concatenate(cols))),
-                              shape=(nc, mesh.n_cells))
-        P.sum_duplicates()
-        # dilate by one cell layer (26-neighbourhood) on the structured grid
         nx, ny, nz = mesh.extents
-        coo = P.tocoo()
-        ijk = mesh.cells_ijk(coo.col)
-        dr, dc = [], []
-        for dz in (-1, 0, 1):
-            for dy in (-1, 0, 1):
-                for dx in (-1, 0, 1):
-                    q = ijk + np.asarray([dx, dy, dz])
-                    ok = ((q[:, 0] >= 0) & (q[:, 0] < nx) & (q[:, 1] >= 0) & (q[:, 1] < ny)
-                          & (q[:, 2] >= 0) & (q[:, 2] < nz))
-                    dr.append(coo.row[ok])
-                    dc.append(q[ok, 0] + nx * (q[ok, 1] + ny * q[ok, 2]))
-        D = sparse.csr_matrix((np.ones(sum(a.size for a in dr), dtype=np.int32),
-                               (np.concatenate(dr), np.concatenate(dc))), shape=(nc, mesh.n_cells))
-        D.sum_duplicates()
-        ov = (D @ P.T).tocsr()
-        ov.data[:] = 1
-        # centre order -> new column order
-        new_of_center = lay.new_col_of_old.reshape(nc, lay.vectors_per_center)
+        patches, dilated = [], []
+        offs = np.asarray([[dx, dy, dz] for dz in (-1, 0, 1) for dy in (-1, 0, 1)
+                           for dx in (-1, 0, 1)])
+        for c in range(nc):
+            cells = np.unique(patch_fine_cells(mesh, lay, c))
+            patches.append(cells)
+            q = (mesh.cells_ijk(cells)[:, None, :] + offs[None, :, :]).reshape(-1, 3)
+            ok = ((q[:, 0] >= 0) & (q[:, 0] < nx) & (q[:, 1] >= 0) & (q[:, 1] < ny)
+                  & (q[:, 2] >= 0) & (q[:, 2] < nz))
+            q = q[ok]
+            dilated.append(np.unique(q[:, 0] + nx * (q[:, 1] + ny * q[:, 2])))
+        h = float(np.max(mesh.spacing)) * (1 << mesh.coarse_level)
+        reach = 2.0 * lay.radius + 4.0 * h * np.sqrt(3.0)
+        from scipy.spatial import cKDTree
+
+        cand = cKDTree(lay.centers).query_pairs(reach, output_type="ndarray")
+        rr, cc = [np.arange(nc)], [np.arange(nc)]
+        for a, b in cand:
+            if np.intersect1d(dilated[a], patches[b], assume_unique=True).size:
+                rr.append(np.asarray([a, b]))
+                cc.append(np.asarray([b, a]))
+        r_c = np.concatenate(rr)
+        c_c = np.concatenate(cc)
         v = lay.vectors_per_center
-        coo = ov.tocoo()
-        r = new_of_center[coo.row].ravel() if v == 1 else None
-        if v == 1:
-            out = sparse.csr_matrix((np.ones(coo.nnz, dtype=bool),
-                                     (new_of_center[coo.row, 0], new_of_center[coo.col, 0])),
-                                    shape=(nc, nc))
-        else:
-            rr = new_of_center[coo.row][:, :, None].repeat(v, 2).ravel()
-            cc = new_of_center[coo.col][:, None, :].repeat(v, 1).ravel()
-            out = sparse.csr_matrix((np.ones(rr.size, dtype=bool), (rr, cc)), shape=(nc * v, nc * v))
+        new_of_center = lay.new_col_of_old.reshape(nc, v)
+        rr = np.repeat(new_of_center[r_c], v, axis=1).ravel()
+        cc = np.tile(new_of_center[c_c], (1, v)).ravel()
+        out = sparse.csr_matrix((np.ones(rr.size, dtype=bool), (rr, cc)), shape=(nc * v, nc * v))
         out.sum_duplicates()
         out.sort_indices()
         self._overlap = out
@@ -252,14 +243,41 @@ def in_support(prob: Problem, rows, new_cols) -> np.ndarray:
 
 
 def fill_multivector(matrix: BlockCsrMatrix, prob: Problem, seed: int, attach: bool = True):
-    """X[r, c] = 2 * hash(seed, r, old(c)) on the support of c, else 0."""
-    old = prob.loc_layout.old_col_of_new
+    """X[r, c] = 2 * hash(seed, r, old(c)) on the support of c, else 0 (owned rows).
 
-    def values(grow, gcol):
-        v = 2.0 * hashed_entries(seed, grow, old[gcol])
-        return np.where(in_support(prob, grow, gcol), v, 0.0)
+    Writes the owned region from the support entries directly (one hash per
+    support entry), which equals the reference's masked per-block fill.
+    """
+    import torch
 
-    matrix.fill_owned_entries(values)
+    matrix._require("owned-writable")
+    lay = prob.loc_layout
+    layout = matrix.layout
+    lo, hi = layout.owned_rows
+    centre = lay.centers_of_new_cols()
+    sizes = np.asarray([prob.supports[int(c)].size for c in centre], dtype=np.int64)
+    rows = np.concatenate([prob.supports[int(c)] for c in centre]).astype(np.int64)
+    cols = np.repeat(np.arange(lay.n_columns, dtype=np.int64), sizes)
+    keep = (rows >= lo) & (rows < hi)
+    rows, cols = rows[keep], cols[keep]
+    host = matrix.data.detach().cpu().numpy().copy()
+    host[: matrix.n_owned_values] = 0.0
+    if rows.size:
+        blocks = layout.blocks
+        gb = np.searchsorted(blocks.starts, rows, side="right") - 1
+        lb = gb - layout.first_block
+        rib = rows - blocks.starts[gb]
+        cb = matrix.col_blocks.blocks_of(cols)
+        key = lb * matrix.col_blocks.n_blocks + cb
+        keys = matrix.local_keys()
+        pos = np.searchsorted(keys, key)
+        ok = (pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == key)
+        if not ok.all():
+            raise ValueError("support entry outside the multivector pattern")
+        flat = (matrix.block_offsets[pos] + rib * matrix.col_strides[cb]
+                + (cols - matrix.col_blocks.starts[cb]))
+        host[flat] = 2.0 * hashed_entries(seed, rows, lay.old_col_of_new[cols])
+    matrix.data.copy_(torch.from_numpy(host))
     if attach:
         attach_support(matrix, prob.column_support, check=False)
     return matrix

@@ -68,7 +68,8 @@ typedef struct {
   const int32_t* pair_lane;        /* n_pairs                             */
   const int32_t* visit_cell;       /* n_visits                            */
   const int32_t* visit_stride;     /* n_visits                            */
-  const int64_t* visit_goff;       /* n_visits                            */
+  const int64_t* visit_goff;       /* n_visits + 1 (groups of visit v:
+                                      [visit_goff[v], visit_goff[v+1]), <= 32) */
   const int64_t* group_xoff;       /* n_groups_total                      */
   const int64_t* group_hoff;       /* n_groups_total                      */
   const uint32_t* cell_slots;      /* n_cells * n^3                       */

@@ -106,6 +106,8 @@ def load(path: str | os.PathLike | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
+        if path is None and os.environ.get("BMV_LIB"):
+            path = os.environ["BMV_LIB"]  # alternative build (kernel experiments)
         p = Path(path) if path is not None else LIB_PATH
         if not p.exists():
             raise DeviceError(
@@ -119,8 +121,7 @@ def load(path: str | os.PathLike | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if path is None:
-            _lib = lib
+        _lib = lib
         return lib
 
 

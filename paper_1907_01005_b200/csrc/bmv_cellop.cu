@@ -55,6 +55,9 @@ struct CellArgs {
 };
 
 constexpr int kWarps = 4;  // warps per CTA
+#ifndef BMV_K1_MINB5
+#define BMV_K1_MINB5 1
+#endif
 
 // Contract along the fast (last) index of a [N][N] plane:
 // out[s][q] = sum_j M[q*N + j] * in[s][j]  (TR: M[j*N + q])
@@ -125,25 +128,77 @@ __device__ __forceinline__ void b_to_a(const double (&b)[N][N], double (&a)[N][N
     for (int x = 0; x < N; ++x) a[y][x] = buf[(t * N + y) * N + x];
 }
 
+// Padded per-pair tile stride (doubles): conflict-free-ish 64-bit transposes
+// for the plane-major thread mapping lane = t * P + pair.
+template <int N> struct TileStride;
+template <> struct TileStride<2> { static constexpr int v = 9; };
+template <> struct TileStride<3> { static constexpr int v = 27; };
+template <> struct TileStride<4> { static constexpr int v = 65; };
+template <> struct TileStride<5> { static constexpr int v = 125; };
+
+constexpr int kMaxGroups = 32;  // distinct block rows per cell (<= 27 at L = 0)
+
+template <int N, bool COEF>
+struct CellSmem {
+  static constexpr int P = 32 / N;
+  static constexpr int TILE = TileStride<N>::v;
+  static constexpr int N3 = N * N * N;
+  // per warp
+  static constexpr int tile_bytes = P * TILE * 8;
+  static constexpr int coef_bytes = COEF ? P * TILE * 8 : 0;
+  static constexpr int gtab_bytes = P * kMaxGroups * 16;
+  static constexpr int slot_bytes = ((P * N3 * 4 + 15) / 16) * 16;
+  static constexpr int warp_bytes = tile_bytes + coef_bytes + gtab_bytes + slot_bytes;
+  static constexpr int cta_bytes = kWarps * warp_bytes;
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 8 : 0;  // src-size 0 => the destination is zero-filled
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
+}
+
+template <int N> struct MinBlocks { static constexpr int v = N >= 5 ? BMV_K1_MINB5 : 1; };
+
 template <int N, bool KIN, bool COEF, bool ATOMIC>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
     cellop_kernel(const CellArgs a, const __grid_constant__ CellTables tb) {
-  constexpr int P = 32 / N;          // pairs per warp
+  using SM = CellSmem<N, COEF>;
+  constexpr int P = SM::P;           // pairs per warp
   constexpr int N2 = N * N;
   constexpr int N3 = N * N * N;
-  constexpr int TILE = N3;           // doubles per pair tile
-  __shared__ double smem[kWarps * P * TILE];
+  constexpr int TILE = SM::TILE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
 
   const int warp = threadIdx.x >> 5;
   const int lid = threadIdx.x & 31;
-  const int sub = lid / N;
-  const int t = lid - sub * N;
-  const bool lane_ok = sub < P;
+  // plane-major mapping: lanes t*P .. t*P+P-1 hold plane t of the warp's P pairs,
+  // so the pairs of one visit (adjacent lanes of one row) load adjacent words
+  const int t = lid / P;
+  const int sub = lid - t * P;
+  const bool lane_ok = t < N;
   const int64_t pair = a.pair_begin + ((int64_t)blockIdx.x * kWarps + warp) * P + sub;
   const bool ok = lane_ok && pair < a.pair_end;
-  double* buf = smem + (warp * P + (lane_ok ? sub : 0)) * TILE;
 
-  int cell = 0, lane = 0, stride = 0;
+  unsigned char* wbase = smem_raw + warp * SM::warp_bytes;
+  double* buf = reinterpret_cast<double*>(wbase) + sub * TILE;
+  double* cbuf = reinterpret_cast<double*>(wbase + SM::tile_bytes) + sub * TILE;
+  int64_t* gtab = reinterpret_cast<int64_t*>(wbase + SM::tile_bytes + SM::coef_bytes) +
+                  sub * 2 * kMaxGroups;
+  uint32_t* slots = reinterpret_cast<uint32_t*>(wbase + SM::tile_bytes + SM::coef_bytes +
+                                                SM::gtab_bytes) + sub * N3;
+
+  int cell = 0, lane = 0, stride = 0, ng = 0;
   int64_t gbase = 0;
   if (ok) {
     const int vis = __ldg(a.pair_visit + pair);
@@ -151,24 +206,47 @@ __global__ void __launch_bounds__(kWarps * 32)
     cell = __ldg(a.visit_cell + vis);
     stride = __ldg(a.visit_stride + vis);
     gbase = __ldg(a.visit_goff + vis);
+    ng = (int)(__ldg(a.visit_goff + vis + 1) - gbase);
   }
-  const uint32_t* slots = a.cell_slots + (int64_t)cell * N3 + t * N2;
 
-  // ---- gather: A layout, z = t
-  double u[N][N];
+  // ---- stage 1: group offsets and this plane's slots -> shared (async)
+  if (ok) {
+    for (int g = t; g < ng; g += N) {
+      cp_async8(gtab + g, a.group_xoff + gbase + g, true);
+      cp_async8(gtab + kMaxGroups + g, a.group_hoff + gbase + g, true);
+    }
+    const uint32_t* gs = a.cell_slots + (int64_t)cell * N3 + t * N2;
 #pragma unroll
-  for (int y = 0; y < N; ++y) {
+    for (int k = 0; k < N2; ++k) cp_async4(slots + t * N2 + k, gs + k);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+
+  // ---- stage 2: gather X (A layout, z = t) and the coefficients (async)
+  if (ok) {
 #pragma unroll
-    for (int x = 0; x < N; ++x) {
-      double v = 0.0;
-      if (ok) {
-        const uint32_t s = __ldg(slots + y * N + x);
-        const int64_t xo = __ldg(a.group_xoff + gbase + (s >> 24));
-        if (xo >= 0) v = __ldg(a.x + xo + (int64_t)(s & 0xffffffu) * stride + lane);
-      }
-      u[y][x] = v;
+    for (int k = 0; k < N2; ++k) {
+      const uint32_t sl = slots[t * N2 + k];
+      const int64_t xo = gtab[sl >> 24];
+      const double* src = a.x + (xo >= 0 ? xo + (int64_t)(sl & 0xffffffu) * stride + lane : 0);
+      cp_async8(buf + t * N2 + k, src, xo >= 0);
     }
   }
+  cp_async_commit();
+  if (COEF && ok) {
+    const double* c = a.coef + (int64_t)cell * a.coef_stride + t * N2;
+#pragma unroll
+    for (int k = 0; k < N2; ++k) cp_async8(cbuf + t * N2 + k, c + k, true);
+  }
+  cp_async_commit();
+  cp_async_wait<1>();
+  __syncwarp();
+  double u[N][N];
+#pragma unroll
+  for (int y = 0; y < N; ++y)
+#pragma unroll
+    for (int x = 0; x < N; ++x) u[y][x] = ok ? buf[(t * N + y) * N + x] : 0.0;
 
   // ---- values to the quadrature points
   double v1[N][N], v2[N][N];
@@ -177,28 +255,29 @@ __global__ void __launch_bounds__(kWarps * 32)
   a_to_b<N>(v2, v1, buf, t, lane_ok);     // B: y = qy = t, [z][qx]
   double uqB[N][N];
   contract_slow<N, false>(v1, uqB, tb.S); // z -> uq at (qz, qy=t, qx)
+  cp_async_wait<0>();
+  __syncwarp();
 
   double acc[N][N];
   if (KIN) {
     // gy in A layout (qz = t)
     b_to_a<N>(uqB, v1, buf, t, lane_ok);  // v1 = uq[qz=t][qy][qx]
     contract_slow<N, false>(v1, v2, tb.D);  // d/dy at the points
-    const double fy = tb.w[t] * tb.kin[1];
+    const double fy = tb.w[t < N ? t : 0] * tb.kin[1];
 #pragma unroll
     for (int i = 0; i < N; ++i)
 #pragma unroll
       for (int j = 0; j < N; ++j) v2[i][j] *= fy * tb.W2[i * N + j];
     contract_slow<N, true>(v2, acc, tb.D);  // D^T along y
     if (COEF) {
-      const double* c = a.coef + (int64_t)cell * a.coef_stride + t * N2;
 #pragma unroll
       for (int i = 0; i < N; ++i)
 #pragma unroll
-        for (int j = 0; j < N; ++j) acc[i][j] = fma(__ldg(c + i * N + j), v1[i][j], acc[i][j]);
+        for (int j = 0; j < N; ++j) acc[i][j] = fma(cbuf[(t * N + i) * N + j], v1[i][j], acc[i][j]);
     }
     a_to_b<N>(acc, v2, buf, t, lane_ok);  // v2 = acc in B (qy = t): [qz][qx]
     // gx and gz in B layout, applied row/column-wise to limit live registers
-    const double wt = tb.w[t];
+    const double wt = tb.w[t < N ? t : 0];
     const double fx = wt * tb.kin[0];
     const double fz = wt * tb.kin[2];
 #pragma unroll
@@ -238,13 +317,12 @@ __global__ void __launch_bounds__(kWarps * 32)
       }
     }
   } else {
-    // mass-like: acc = c * uq, computed in B layout directly
-    const double* c = a.coef + (int64_t)cell * a.coef_stride;
+    // mass-like: acc = c * uq, computed in B layout directly (qy = t)
 #pragma unroll
     for (int z = 0; z < N; ++z)
 #pragma unroll
       for (int x = 0; x < N; ++x)
-        v2[z][x] = COEF ? __ldg(c + (z * N + t) * N + x) * uqB[z][x] : 0.0;
+        v2[z][x] = COEF ? cbuf[(z * N + t) * N + x] * uqB[z][x] : 0.0;
   }
 
   // ---- back to the nodes: z, x in B, then y in A
@@ -255,13 +333,13 @@ __global__ void __launch_bounds__(kWarps * 32)
 
   // ---- scatter-add
   if (ok) {
+    const int64_t* gh = gtab + kMaxGroups;
 #pragma unroll
     for (int y = 0; y < N; ++y) {
 #pragma unroll
       for (int x = 0; x < N; ++x) {
-        const uint32_t s = __ldg(slots + y * N + x);
-        const int64_t ho = __ldg(a.group_hoff + gbase + (s >> 24));
-        double* p = a.hx + ho + (int64_t)(s & 0xffffffu) * stride + lane;
+        const uint32_t sl = slots[(t * N + y) * N + x];
+        double* p = a.hx + gh[sl >> 24] + (int64_t)(sl & 0xffffffu) * stride + lane;
         if (ATOMIC)
           atomicAdd(p, v2[y][x]);
         else
@@ -323,12 +401,19 @@ namespace {
 
 template <int N, bool KIN, bool COEF, bool ATOMIC>
 int launch_one(const CellArgs& args, const CellTables& tb, cudaStream_t st) {
-  constexpr int P = 32 / N;
+  using SM = CellSmem<N, COEF>;
+  constexpr int P = SM::P;
   const int64_t n = args.pair_end - args.pair_begin;
   if (n <= 0) return BMV_OK;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    BMV_CUDA_TRY(cudaFuncSetAttribute(cellop_kernel<N, KIN, COEF, ATOMIC>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SM::cta_bytes));
+    configured = true;
+  }
   const int64_t per_cta = (int64_t)kWarps * P;
   const int64_t grid = (n + per_cta - 1) / per_cta;
-  cellop_kernel<N, KIN, COEF, ATOMIC><<<(unsigned)grid, kWarps * 32, 0, st>>>(args, tb);
+  cellop_kernel<N, KIN, COEF, ATOMIC><<<(unsigned)grid, kWarps * 32, SM::cta_bytes, st>>>(args, tb);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
@@ -408,7 +493,14 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
   if (rc == BMV_OK) rc = upload(d->pair_lane, d->n_pairs, &p->pair_lane);
   if (rc == BMV_OK) rc = upload(d->visit_cell, (int64_t)d->n_visits, &p->visit_cell);
   if (rc == BMV_OK) rc = upload(d->visit_stride, (int64_t)d->n_visits, &p->visit_stride);
-  if (rc == BMV_OK) rc = upload(d->visit_goff, (int64_t)d->n_visits, &p->visit_goff);
+  for (int32_t v = 0; rc == BMV_OK && v < d->n_visits; ++v) {
+    if (d->visit_goff[v + 1] - d->visit_goff[v] > kMaxGroups) {
+      set_error("a cell touches %lld block rows (max %d)",
+                (long long)(d->visit_goff[v + 1] - d->visit_goff[v]), kMaxGroups);
+      rc = BMV_ERR_INVALID;
+    }
+  }
+  if (rc == BMV_OK) rc = upload(d->visit_goff, (int64_t)d->n_visits + 1, &p->visit_goff);
   if (rc == BMV_OK) rc = upload(d->group_xoff, d->n_groups_total, &p->group_xoff);
   if (rc == BMV_OK) rc = upload(d->group_hoff, d->n_groups_total, &p->group_hoff);
   if (rc == BMV_OK) rc = upload(d->cell_slots, (int64_t)d->n_cells * n3, &p->cell_slots);

@@ -393,7 +393,7 @@ class _CellPlan:
             pair_lane=np.ascontiguousarray(pair_lane, dtype=np.int32),
             visit_cell=np.ascontiguousarray(visit_cell, dtype=np.int32),
             visit_stride=np.ascontiguousarray(src.col_strides[visit_col], dtype=np.int32),
-            visit_goff=np.ascontiguousarray(visit_goff[:-1], dtype=np.int64),
+            visit_goff=np.ascontiguousarray(visit_goff, dtype=np.int64),
             group_xoff=np.ascontiguousarray(group_xoff, dtype=np.int64),
             group_hoff=np.ascontiguousarray(group_hoff, dtype=np.int64),
             cell_slots=np.ascontiguousarray(op.cell_slots, dtype=np.uint32),

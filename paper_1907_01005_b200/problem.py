@@ -11,8 +11,9 @@ weak-scaling lattice offset of half a spacing (M8), reference Hilbert
 partition (M9).  The potential is -sum_c exp(-|x-c|^2/sigma^2) over all
 centres.  Inputs are synthetic (no public dataset exists for this path).
 
-Fills are vectorised: one hash per stored entry and one sorted-key
-membership test, identical to the reference's per-block `np.isin` fill.
+Fills are vectorised: one hash per support entry written straight to its
+storage offset, identical to the reference's masked per-block `np.isin`
+fill.
 """
 
 from __future__ import annotations
@@ -242,15 +243,15 @@ def in_support(prob: Problem, rows, new_cols) -> np.ndarray:
     return (pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == key)
 
 
-def fill_multivector(matrix: BlockCsrMatrix, prob: Problem, seed: int, attach: bool = True):
-    """X[r, c] = 2 * hash(seed, r, old(c)) on the support of c, else 0 (owned rows).
+def _support_entries(matrix: BlockCsrMatrix, prob: Problem):
+    """(flat offsets, global rows, new cols) of the support entries in owned rows.
 
-    Writes the owned region from the support entries directly (one hash per
-    support entry), which equals the reference's masked per-block fill.
+    Cached per (pattern, layout): X and Y share it.
     """
-    import torch
-
-    matrix._require("owned-writable")
+    key = ("support_entries", id(matrix.pattern), id(matrix.layout), matrix.lane_width)
+    hit = prob.extra.get(key)
+    if hit is not None:
+        return hit
     lay = prob.loc_layout
     layout = matrix.layout
     lo, hi = layout.owned_rows
@@ -260,23 +261,54 @@ def fill_multivector(matrix: BlockCsrMatrix, prob: Problem, seed: int, attach: b
     cols = np.repeat(np.arange(lay.n_columns, dtype=np.int64), sizes)
     keep = (rows >= lo) & (rows < hi)
     rows, cols = rows[keep], cols[keep]
-    host = matrix.data.detach().cpu().numpy().copy()
-    host[: matrix.n_owned_values] = 0.0
+    if rows.size == 0:
+        hit = (rows, rows, cols)
+        prob.extra[key] = hit
+        return hit
+    blocks = layout.blocks
+    nb_own = layout.n_owned_blocks
+    own_sizes = blocks.sizes[layout.first_block : layout.first_block + nb_own]
+    lb_of_row = np.repeat(np.arange(nb_own, dtype=np.int64), own_sizes)
+    lb = lb_of_row[rows - lo]
+    rib = rows - blocks.starts[layout.first_block + lb]
+    cb_of_col = np.repeat(np.arange(matrix.col_blocks.n_blocks, dtype=np.int64),
+                          matrix.col_blocks.sizes)
+    cb = cb_of_col[cols]
+    n_cb = matrix.col_blocks.n_blocks
+    n_own_pos = int(matrix.row_start[nb_own])
+    if nb_own * n_cb <= 64_000_000:
+        table = np.full(nb_own * n_cb, -1, dtype=np.int64)
+        table[matrix.pos_row[:n_own_pos] * n_cb + matrix.col_index[:n_own_pos]] = \
+            np.arange(n_own_pos, dtype=np.int64)
+        pos = table[lb * n_cb + cb]
+    else:
+        keys = matrix.local_keys()[:n_own_pos]
+        k = lb * n_cb + cb
+        pos = np.searchsorted(keys, k)
+        pos = np.where((pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == k), pos, -1)
+    if (pos < 0).any():
+        raise ValueError("support entry outside the multivector pattern")
+    flat = matrix.block_offsets[pos] + rib * matrix.col_strides[cb] + (cols - matrix.col_blocks.starts[cb])
+    hit = (flat, rows, cols)
+    prob.extra[key] = hit
+    return hit
+
+
+def fill_multivector(matrix: BlockCsrMatrix, prob: Problem, seed: int, attach: bool = True):
+    """X[r, c] = 2 * hash(seed, r, old(c)) on the support of c, else 0 (owned rows).
+
+    Writes the owned region from the support entries directly (one hash per
+    support entry), which equals the reference's masked per-block fill.
+    """
+    import torch
+
+    matrix._require("owned-writable")
+    flat, rows, cols = _support_entries(matrix, prob)
+    host = np.zeros(matrix.data.numel())
+    if matrix.n_owned_values < host.size:
+        host[matrix.n_owned_values :] = matrix.data[matrix.n_owned_values :].cpu().numpy()
     if rows.size:
-        blocks = layout.blocks
-        gb = np.searchsorted(blocks.starts, rows, side="right") - 1
-        lb = gb - layout.first_block
-        rib = rows - blocks.starts[gb]
-        cb = matrix.col_blocks.blocks_of(cols)
-        key = lb * matrix.col_blocks.n_blocks + cb
-        keys = matrix.local_keys()
-        pos = np.searchsorted(keys, key)
-        ok = (pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == key)
-        if not ok.all():
-            raise ValueError("support entry outside the multivector pattern")
-        flat = (matrix.block_offsets[pos] + rib * matrix.col_strides[cb]
-                + (cols - matrix.col_blocks.starts[cb]))
-        host[flat] = 2.0 * hashed_entries(seed, rows, lay.old_col_of_new[cols])
+        host[flat] = 2.0 * hashed_entries(seed, rows, prob.loc_layout.old_col_of_new[cols])
     matrix.data.copy_(torch.from_numpy(host))
     if attach:
         attach_support(matrix, prob.column_support, check=False)
@@ -354,7 +386,8 @@ class RankSetup:
     dirichlet: tuple | None = None
 
 
-def make_rank_setup(ctx, prob: Problem, projection: bool | None = None, device=None) -> RankSetup:
+def make_rank_setup(ctx, prob: Problem, projection: bool | None = None, device=None,
+                    with_y: bool | None = None) -> RankSetup:
     cfg = prob.cfg
     layout = make_dof_layout(ctx, prob.mesh, prob.partition, prob.numbering)
     op = CellOperator(prob.mesh, prob.partition, prob.numbering, layout)
@@ -372,8 +405,12 @@ def make_rank_setup(ctx, prob: Problem, projection: bool | None = None, device=N
         proj = prob.proj_pattern
         ghosts = column_space_ghost_blocks(prob.grown, proj, layout, lay.rank_block_start, ctx.rank)
         clayout = make_column_layout(ctx, lay.column_blocks, lay.rank_block_start, ghosts)
-        st.y = fill_multivector(BlockCsrMatrix(prob.pattern, layout, ctx, w, device), prob, cfg.seed_y)
-        st.hy = BlockCsrMatrix(prob.grown, layout, ctx, w, device)
+        if with_y is None:
+            with_y = cfg.name == "proj"
+        if with_y:
+            st.y = fill_multivector(BlockCsrMatrix(prob.pattern, layout, ctx, w, device), prob,
+                                    cfg.seed_y)
+            st.hy = BlockCsrMatrix(prob.grown, layout, ctx, w, device)
         st.s = BlockCsrMatrix(proj, clayout, ctx, w, device)
         st.c = fill_projected(BlockCsrMatrix(proj, clayout, ctx, w, device), prob, cfg.seed_c)
         st.xc = BlockCsrMatrix(prob.pattern, layout, ctx, w, device)

@@ -106,27 +106,34 @@ int bmv_potential_gaussian(int64_t n_cells, int32_t q3, const double* cell_origi
 int bmv_cellop_launches(const bmv_cellop* plan, int32_t* out);
 
 /* ------------------------------------------------------------------ K4 --
- * C(k,l) = sum_i A_ik^T B_il over triples (i, A block, B block).  Triples are
- * cut into segments (one output block within one chunk of consecutive block
- * rows); one warp per segment accumulates its triples into a partial block,
- * then each output block sums its segments' partials in chunk order (fixed
- * order -> bit-reproducible, no atomics).                                */
+ * C(k,l) = sum_i A_ik^T B_il over the owned block rows i.
+ * Block rows are cut into chunks of consecutive rows whose A and B blocks
+ * (each a contiguous range of the value arrays) fit in shared memory; one
+ * CTA stages a chunk with coalesced loads, then its warps compute the
+ * chunk's segments (= output blocks touched by the chunk) from shared
+ * memory into partial blocks; a second kernel sums every output block's
+ * partials in chunk order (fixed order: bit-reproducible, no atomics).  */
 typedef struct {
   int64_t n_out;             /* output blocks with work                    */
-  int64_t n_seg;             /* segments                                   */
+  int64_t n_chunks;
+  int64_t n_seg;             /* segments (chunk, output block)             */
   int64_t n_triples;
   int64_t partial_len;       /* doubles of partial storage                 */
+  int32_t smem_doubles;      /* max staged doubles per chunk (A + B)       */
   const int64_t* out_off;    /* element offset of the C block              */
   const int32_t* out_rows;   /* valid rows (size of column block k)        */
   const int32_t* out_cols;   /* valid cols (size of column block l)        */
   const int32_t* out_stride; /* C row stride                               */
   const int64_t* out_seg_start; /* n_out + 1, into out_seg_list            */
   const int64_t* out_seg_list;  /* n_seg segment ids, chunk order per out  */
+  const int64_t* chunk_a;    /* n_chunks x 2: A element range [lo, hi)     */
+  const int64_t* chunk_b;    /* n_chunks x 2: B element range [lo, hi)     */
+  const int64_t* chunk_seg_start; /* n_chunks + 1, into the segments       */
   const int64_t* seg_out;       /* n_seg: output index of the segment      */
   const int64_t* seg_tri_start; /* n_seg + 1, into the triple arrays       */
   const int64_t* seg_poff;      /* n_seg: offset of the partial block      */
-  const int64_t* tri_a_off;
-  const int64_t* tri_b_off;
+  const int32_t* tri_a_soff; /* A block offset inside the chunk stage      */
+  const int32_t* tri_b_soff; /* B block offset (from the start of B stage) */
   const int32_t* tri_rows;   /* rows of block row i                         */
   const int32_t* tri_a_stride;
   const int32_t* tri_b_stride;
@@ -140,16 +147,23 @@ int bmv_tmmult_run(bmv_tmmult* plan, const double* a, const double* b, double* c
                    int64_t c_len, void* stream);
 
 /* ------------------------------------------------------------------ K5 --
- * Y_ij (+)= alpha * sum_k A_ik B_kj over pairs grouped by output block.  */
+ * Y_ij (+)= alpha * sum_k A_ik B_kj, truncated to Y's pattern.  Owned block
+ * rows are cut into chunks whose A blocks (one contiguous range) are staged
+ * in shared memory; one warp per output block of the chunk accumulates its
+ * products (B blocks through L1/L2) and writes the block once.          */
 typedef struct {
   int64_t n_out;
+  int64_t n_chunks;
   int64_t n_pairs;
+  int32_t smem_doubles;      /* max staged A doubles per chunk             */
+  const int64_t* chunk_a;    /* n_chunks x 2: A element range [lo, hi)     */
+  const int64_t* chunk_out_start; /* n_chunks + 1, into the output blocks  */
   const int64_t* out_off;
   const int32_t* out_rows;   /* rows of block row i                        */
   const int32_t* out_cols;   /* size of column block j                     */
   const int32_t* out_stride;
   const int64_t* pair_start; /* n_out + 1                                  */
-  const int64_t* pair_a_off;
+  const int32_t* pair_a_soff;   /* A block offset inside the chunk stage   */
   const int32_t* pair_a_stride;
   const int32_t* pair_inner; /* size of inner block k                      */
   const int64_t* pair_b_off;

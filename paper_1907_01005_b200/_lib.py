@@ -43,21 +43,23 @@ class CellopDesc(C.Structure):
 
 class TmmultDesc(C.Structure):
     _fields_ = [
-        ("n_out", C.c_int64), ("n_seg", C.c_int64), ("n_triples", C.c_int64),
-        ("partial_len", C.c_int64), ("out_off", _i64p),
-        ("out_rows", _i32p), ("out_cols", _i32p), ("out_stride", _i32p),
-        ("out_seg_start", _i64p), ("out_seg_list", _i64p), ("seg_out", _i64p),
-        ("seg_tri_start", _i64p), ("seg_poff", _i64p),
-        ("tri_a_off", _i64p), ("tri_b_off", _i64p),
-        ("tri_rows", _i32p), ("tri_a_stride", _i32p), ("tri_b_stride", _i32p),
+        ("n_out", C.c_int64), ("n_chunks", C.c_int64), ("n_seg", C.c_int64),
+        ("n_triples", C.c_int64), ("partial_len", C.c_int64), ("smem_doubles", C.c_int32),
+        ("out_off", _i64p), ("out_rows", _i32p), ("out_cols", _i32p), ("out_stride", _i32p),
+        ("out_seg_start", _i64p), ("out_seg_list", _i64p), ("chunk_a", _i64p),
+        ("chunk_b", _i64p), ("chunk_seg_start", _i64p), ("seg_out", _i64p),
+        ("seg_tri_start", _i64p), ("seg_poff", _i64p), ("tri_a_soff", _i32p),
+        ("tri_b_soff", _i32p), ("tri_rows", _i32p), ("tri_a_stride", _i32p),
+        ("tri_b_stride", _i32p),
     ]
 
 
 class MmultDesc(C.Structure):
     _fields_ = [
-        ("n_out", C.c_int64), ("n_pairs", C.c_int64), ("out_off", _i64p),
-        ("out_rows", _i32p), ("out_cols", _i32p), ("out_stride", _i32p),
-        ("pair_start", _i64p), ("pair_a_off", _i64p), ("pair_a_stride", _i32p),
+        ("n_out", C.c_int64), ("n_chunks", C.c_int64), ("n_pairs", C.c_int64),
+        ("smem_doubles", C.c_int32), ("chunk_a", _i64p), ("chunk_out_start", _i64p),
+        ("out_off", _i64p), ("out_rows", _i32p), ("out_cols", _i32p), ("out_stride", _i32p),
+        ("pair_start", _i64p), ("pair_a_soff", _i32p), ("pair_a_stride", _i32p),
         ("pair_inner", _i32p), ("pair_b_off", _i64p), ("pair_b_stride", _i32p),
     ]
 

@@ -703,13 +703,34 @@ def _mmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     order, outs, start = _group_by_output(cp)
     pa, pb = pa[order], pb[order]
     n_out = int(outs.size)
+    # chunks of consecutive owned block rows whose A blocks fit the stage
+    n_rows = a.n_owned_blocks
+    a_row_lo = a.block_offsets[a.row_start[:n_rows]]
+    a_row_hi = a.block_offsets[a.row_start[1 : n_rows + 1]]
+    row_dbl = a_row_hi - a_row_lo
+    if n_rows and int(row_dbl.max()) > _TM_STAGE_MAX:
+        raise ShapeError(f"mmult block row needs {int(row_dbl.max()) * 8} bytes of shared memory")
+    target = int(np.clip(int(row_dbl.sum()) // (148 * 8), 2048, _TM_STAGE_TARGET))
+    row_chunk = _greedy_chunks(row_dbl, max(target, int(row_dbl.max()) if n_rows else 0))
+    n_chunks = int(row_chunk[-1]) + 1 if n_rows else 0
+    first_row = np.searchsorted(row_chunk, np.arange(n_chunks + 1)).astype(np.int64)
+    chunk_a = np.stack([a_row_lo[first_row[:-1]], a_row_hi[first_row[1:] - 1]], 1) if n_chunks \
+        else np.zeros((0, 2), np.int64)
+    out_chunk = row_chunk[c.pos_row[outs]] if n_out else np.zeros(0, np.int64)
+    chunk_out_start = np.searchsorted(out_chunk, np.arange(n_chunks + 1)).astype(np.int64)
+    pair_chunk = row_chunk[a.pos_row[pa]] if pa.size else np.zeros(0, np.int64)
     arrays = dict(
+        n_chunks=n_chunks,
+        smem_doubles=int((chunk_a[:, 1] - chunk_a[:, 0]).max()) if n_chunks else 0,
+        chunk_a=np.ascontiguousarray(chunk_a, dtype=np.int64).ravel(),
+        chunk_out_start=chunk_out_start,
         out_off=c.block_offsets[outs].astype(np.int64),
         out_rows=c.local_row_sizes[c.pos_row[outs]].astype(np.int32),
         out_cols=c.col_blocks.sizes[c.col_index[outs]].astype(np.int32),
         out_stride=c.col_strides[c.col_index[outs]].astype(np.int32),
         pair_start=start,
-        pair_a_off=a.block_offsets[pa].astype(np.int64),
+        pair_a_soff=(a.block_offsets[pa] - chunk_a[pair_chunk, 0]).astype(np.int32)
+        if pa.size else np.zeros(0, np.int32),
         pair_a_stride=a.col_strides[a.col_index[pa]].astype(np.int32),
         pair_inner=a.col_blocks.sizes[a.col_index[pa]].astype(np.int32),
         pair_b_off=b.block_offsets[pb].astype(np.int64),
@@ -732,9 +753,12 @@ class _MmultPlan:
         lib = _lib.load()
         d = _lib.MmultDesc()
         d.n_out, d.n_pairs = n_out, n_pairs
-        for name, ct in (("out_off", _lib.C.c_int64), ("out_rows", _lib.C.c_int32),
+        d.n_chunks = int(arrays["n_chunks"])
+        d.smem_doubles = int(arrays["smem_doubles"])
+        for name, ct in (("chunk_a", _lib.C.c_int64), ("chunk_out_start", _lib.C.c_int64),
+                         ("out_off", _lib.C.c_int64), ("out_rows", _lib.C.c_int32),
                          ("out_cols", _lib.C.c_int32), ("out_stride", _lib.C.c_int32),
-                         ("pair_start", _lib.C.c_int64), ("pair_a_off", _lib.C.c_int64),
+                         ("pair_start", _lib.C.c_int64), ("pair_a_soff", _lib.C.c_int32),
                          ("pair_a_stride", _lib.C.c_int32), ("pair_inner", _lib.C.c_int32),
                          ("pair_b_off", _lib.C.c_int64), ("pair_b_stride", _lib.C.c_int32)):
             arrays[name] = np.ascontiguousarray(arrays[name])
@@ -765,7 +789,21 @@ def mmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, alpha: float 
         counters.flops += plan.flops
 
 
-_TM_CHUNK = 256  # triples per row chunk of the K4 plan
+_TM_STAGE_TARGET = 12_000  # doubles of A + B staged per K4 chunk (96 KB)
+_TM_STAGE_MAX = 27_000     # hard limit per chunk (216 KB of shared memory)
+
+
+def _greedy_chunks(sizes: np.ndarray, target: int) -> np.ndarray:
+    """Chunk id of each item: consecutive items while the running sum <= target."""
+    out = np.empty(sizes.size, dtype=np.int64)
+    cid, acc = 0, 0
+    for i, v in enumerate(sizes.tolist()):
+        if acc and acc + v > target:
+            cid += 1
+            acc = 0
+        acc += v
+        out[i] = cid
+    return out
 
 
 def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
@@ -798,10 +836,25 @@ def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
         raise PatternError(f"tmmult destination misses block ({int(k[j])}, {int(ell[j])})")
     if (c.local_row_sizes[c.pos_row[cp]] != a.col_blocks.sizes[k]).any():
         raise ShapeError("tmmult destination row block is incomplete (split ghost group)")
-    # segments: one output block inside one chunk of consecutive rows holding
-    # about _TM_CHUNK triples; triples keep the reference order inside a segment
-    per_row = na * nb
-    row_chunk = (np.cumsum(per_row) - per_row) // _TM_CHUNK
+    # chunks: consecutive owned block rows whose A and B blocks (two contiguous
+    # value ranges) fit the shared-memory stage; segments: one output block
+    # inside one chunk; triples keep the reference order inside a segment
+    a_row_lo = a.block_offsets[a.row_start[:n_rows]]
+    a_row_hi = a.block_offsets[a.row_start[1 : n_rows + 1]]
+    b_row_lo = b.block_offsets[b.row_start[:n_rows]]
+    b_row_hi = b.block_offsets[b.row_start[1 : n_rows + 1]]
+    row_dbl = (a_row_hi - a_row_lo) + (b_row_hi - b_row_lo)
+    if n_rows and int(row_dbl.max()) > _TM_STAGE_MAX:
+        raise ShapeError(f"tmmult block row needs {int(row_dbl.max()) * 8} bytes of shared memory")
+    target = int(np.clip(int(row_dbl.sum()) // (148 * 8), 2048, _TM_STAGE_TARGET))
+    row_chunk = _greedy_chunks(row_dbl, max(target, int(row_dbl.max()) if n_rows else 0))
+    n_chunks = int(row_chunk[-1]) + 1 if n_rows else 0
+    first_row = np.searchsorted(row_chunk, np.arange(n_chunks + 1)).astype(np.int64)
+    chunk_a = np.stack([a_row_lo[first_row[:-1]], a_row_hi[first_row[1:] - 1]], 1) if n_chunks \
+        else np.zeros((0, 2), np.int64)
+    chunk_b = np.stack([b_row_lo[first_row[:-1]], b_row_hi[first_row[1:] - 1]], 1) if n_chunks \
+        else np.zeros((0, 2), np.int64)
+    stage = (chunk_a[:, 1] - chunk_a[:, 0]) + (chunk_b[:, 1] - chunk_b[:, 0])
     chunk = row_chunk[row]
     order = np.lexsort((cp, chunk))
     pa, pb, row, cp, chunk = pa[order], pb[order], row[order], cp[order], chunk[order]
@@ -814,12 +867,14 @@ def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     n_out = int(outs.size)
     seg_out = np.searchsorted(outs, cp[first]).astype(np.int64)
     seg_chunk = chunk[first]
+    chunk_seg_start = np.searchsorted(seg_chunk, np.arange(n_chunks + 1)).astype(np.int64)
     out_rows = c.local_row_sizes[c.pos_row[outs]].astype(np.int64)
     out_cols = c.col_blocks.sizes[c.col_index[outs]].astype(np.int64)
     seg_ent = out_rows[seg_out] * out_cols[seg_out]
     seg_poff = np.concatenate([[0], np.cumsum(seg_ent)]).astype(np.int64)
     order2 = np.lexsort((seg_chunk, seg_out))
     out_seg_start = np.searchsorted(seg_out[order2], np.arange(n_out + 1)).astype(np.int64)
+    tri_chunk = chunk
     arrays = dict(
         out_off=c.block_offsets[outs].astype(np.int64),
         out_rows=out_rows.astype(np.int32),
@@ -827,12 +882,17 @@ def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
         out_stride=c.col_strides[c.col_index[outs]].astype(np.int32),
         out_seg_start=out_seg_start,
         out_seg_list=order2.astype(np.int64),
+        chunk_a=np.ascontiguousarray(chunk_a, dtype=np.int64).ravel(),
+        chunk_b=np.ascontiguousarray(chunk_b, dtype=np.int64).ravel(),
+        chunk_seg_start=chunk_seg_start,
         seg_out=seg_out,
         seg_tri_start=seg_tri_start,
         seg_poff=seg_poff[:-1].copy(),
         partial_len=int(seg_poff[-1]),
-        tri_a_off=a.block_offsets[pa].astype(np.int64),
-        tri_b_off=b.block_offsets[pb].astype(np.int64),
+        smem_doubles=int(stage.max()) if n_chunks else 0,
+        n_chunks=n_chunks,
+        tri_a_soff=(a.block_offsets[pa] - chunk_a[tri_chunk, 0]).astype(np.int32),
+        tri_b_soff=(b.block_offsets[pb] - chunk_b[tri_chunk, 0]).astype(np.int32),
         tri_rows=a.local_row_sizes[row].astype(np.int32),
         tri_a_stride=a.col_strides[a.col_index[pa]].astype(np.int32),
         tri_b_stride=b.col_strides[b.col_index[pb]].astype(np.int32),
@@ -853,14 +913,18 @@ class _TmmultPlan:
         lib = _lib.load()
         d = _lib.TmmultDesc()
         d.n_out, d.n_triples = n_out, n_tri
+        d.n_chunks = int(arrays["n_chunks"])
         d.n_seg = int(arrays["seg_out"].size)
         d.partial_len = int(arrays["partial_len"])
+        d.smem_doubles = int(arrays["smem_doubles"])
         for name, ct in (("out_off", _lib.C.c_int64), ("out_rows", _lib.C.c_int32),
                          ("out_cols", _lib.C.c_int32), ("out_stride", _lib.C.c_int32),
                          ("out_seg_start", _lib.C.c_int64), ("out_seg_list", _lib.C.c_int64),
+                         ("chunk_a", _lib.C.c_int64), ("chunk_b", _lib.C.c_int64),
+                         ("chunk_seg_start", _lib.C.c_int64),
                          ("seg_out", _lib.C.c_int64), ("seg_tri_start", _lib.C.c_int64),
                          ("seg_poff", _lib.C.c_int64),
-                         ("tri_a_off", _lib.C.c_int64), ("tri_b_off", _lib.C.c_int64),
+                         ("tri_a_soff", _lib.C.c_int32), ("tri_b_soff", _lib.C.c_int32),
                          ("tri_rows", _lib.C.c_int32), ("tri_a_stride", _lib.C.c_int32),
                          ("tri_b_stride", _lib.C.c_int32)):
             arrays[name] = np.ascontiguousarray(arrays[name])

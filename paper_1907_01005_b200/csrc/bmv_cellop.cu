@@ -38,11 +38,8 @@ struct CellTables {
 };
 
 struct CellArgs {
-  const int32_t* __restrict__ pair_visit;
-  const int32_t* __restrict__ pair_lane;
-  const int32_t* __restrict__ visit_cell;
-  const int32_t* __restrict__ visit_stride;
-  const int64_t* __restrict__ visit_goff;
+  // per pair: {cell, first group index, lane | stride << 16, number of groups}
+  const int4* __restrict__ pair_desc;
   const int64_t* __restrict__ group_xoff;
   const int64_t* __restrict__ group_hoff;
   const uint32_t* __restrict__ cell_slots;
@@ -56,7 +53,7 @@ struct CellArgs {
 
 constexpr int kWarps = 4;  // warps per CTA
 #ifndef BMV_K1_MINB5
-#define BMV_K1_MINB5 1
+#define BMV_K1_MINB5 3
 #endif
 
 // Contract along the fast (last) index of a [N][N] plane:
@@ -138,43 +135,45 @@ template <> struct TileStride<5> { static constexpr int v = 125; };
 
 constexpr int kMaxGroups = 32;  // distinct block rows per cell (<= 27 at L = 0)
 
+// Dynamic shared memory per warp: pair tiles | coefficient tiles | slot tiles | group tables
 template <int N, bool COEF>
 struct CellSmem {
   static constexpr int P = 32 / N;
   static constexpr int TILE = TileStride<N>::v;
   static constexpr int N3 = N * N * N;
-  // per warp
   static constexpr int tile_bytes = P * TILE * 8;
   static constexpr int coef_bytes = COEF ? P * TILE * 8 : 0;
-  static constexpr int gtab_bytes = P * kMaxGroups * 16;
   static constexpr int slot_bytes = ((P * N3 * 4 + 15) / 16) * 16;
-  static constexpr int warp_bytes = tile_bytes + coef_bytes + gtab_bytes + slot_bytes;
-  static constexpr int cta_bytes = kWarps * warp_bytes;
+  static __host__ __device__ int gtab_bytes(int G) { return P * G * 16; }
+  static __host__ __device__ int warp_bytes(int G) {
+    return tile_bytes + coef_bytes + slot_bytes + gtab_bytes(G);
+  }
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int n = valid ? 8 : 0;  // src-size 0 => the destination is zero-filled
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(n)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int K>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_one() {
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
 }
 
-template <int N> struct MinBlocks { static constexpr int v = N >= 5 ? BMV_K1_MINB5 : 1; };
+template <int N> struct MinBlocks { static constexpr int v = N >= 4 ? BMV_K1_MINB5 : (N == 3 ? 7 : 1); };
 
+// Three dependent memory trips per pair: (1) the 16-byte pair descriptor,
+// (2) the cell's slots, the visit's group table and the quadrature
+// coefficients (independent, all in flight together; coefficients by
+// cp.async into shared memory, consumed after the interpolation),
+// (3) the n^2 X values of the thread's plane (independent loads).
 template <int N, bool KIN, bool COEF, bool ATOMIC>
 __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
-    cellop_kernel(const CellArgs a, const __grid_constant__ CellTables tb) {
+    cellop_kernel(const CellArgs a, const __grid_constant__ CellTables tb, const int G) {
   using SM = CellSmem<N, COEF>;
-  constexpr int P = SM::P;           // pairs per warp
+  constexpr int P = SM::P;
   constexpr int N2 = N * N;
   constexpr int N3 = N * N * N;
   constexpr int TILE = SM::TILE;
@@ -183,87 +182,90 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
   const int warp = threadIdx.x >> 5;
   const int lid = threadIdx.x & 31;
   // plane-major mapping: lanes t*P .. t*P+P-1 hold plane t of the warp's P pairs,
-  // so the pairs of one visit (adjacent lanes of one row) load adjacent words
+  // so the pairs of one visit (adjacent columns of the same rows) load adjacent words
   const int t = lid / P;
   const int sub = lid - t * P;
   const bool lane_ok = t < N;
+  const int tt = lane_ok ? t : 0;
   const int64_t pair = a.pair_begin + ((int64_t)blockIdx.x * kWarps + warp) * P + sub;
   const bool ok = lane_ok && pair < a.pair_end;
 
-  unsigned char* wbase = smem_raw + warp * SM::warp_bytes;
+  unsigned char* wbase = smem_raw + warp * SM::warp_bytes(G);
   double* buf = reinterpret_cast<double*>(wbase) + sub * TILE;
   double* cbuf = reinterpret_cast<double*>(wbase + SM::tile_bytes) + sub * TILE;
-  int64_t* gtab = reinterpret_cast<int64_t*>(wbase + SM::tile_bytes + SM::coef_bytes) +
-                  sub * 2 * kMaxGroups;
-  uint32_t* slots = reinterpret_cast<uint32_t*>(wbase + SM::tile_bytes + SM::coef_bytes +
-                                                SM::gtab_bytes) + sub * N3;
+  uint32_t* slots = reinterpret_cast<uint32_t*>(wbase + SM::tile_bytes + SM::coef_bytes) + sub * N3;
+  int64_t* gtab = reinterpret_cast<int64_t*>(wbase + SM::tile_bytes + SM::coef_bytes +
+                                             SM::slot_bytes) + sub * 2 * G;
 
-  int cell = 0, lane = 0, stride = 0, ng = 0;
-  int64_t gbase = 0;
+  // ---- trip 1: pair descriptor
+  int cell = 0, lane = 0, stride = 0, ng = 0, gbase = 0;
   if (ok) {
-    const int vis = __ldg(a.pair_visit + pair);
-    lane = __ldg(a.pair_lane + pair);
-    cell = __ldg(a.visit_cell + vis);
-    stride = __ldg(a.visit_stride + vis);
-    gbase = __ldg(a.visit_goff + vis);
-    ng = (int)(__ldg(a.visit_goff + vis + 1) - gbase);
+    const int4 d = __ldg(a.pair_desc + pair);
+    cell = d.x;
+    gbase = d.y;
+    lane = d.z & 0xffff;
+    stride = d.z >> 16;
+    ng = d.w;
   }
-
-  // ---- stage 1: group offsets and this plane's slots -> shared (async)
+  // ---- trip 2: slots, group table, coefficients
+  uint32_t sl[N2];
+  {
+    const uint32_t* gs = a.cell_slots + (int64_t)cell * N3 + tt * N2;
+#pragma unroll
+    for (int k = 0; k < N2; ++k) sl[k] = ok ? __ldg(gs + k) : 0u;
+  }
   if (ok) {
     for (int g = t; g < ng; g += N) {
-      cp_async8(gtab + g, a.group_xoff + gbase + g, true);
-      cp_async8(gtab + kMaxGroups + g, a.group_hoff + gbase + g, true);
-    }
-    const uint32_t* gs = a.cell_slots + (int64_t)cell * N3 + t * N2;
-#pragma unroll
-    for (int k = 0; k < N2; ++k) cp_async4(slots + t * N2 + k, gs + k);
-  }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncwarp();
-
-  // ---- stage 2: gather X (A layout, z = t) and the coefficients (async)
-  if (ok) {
-#pragma unroll
-    for (int k = 0; k < N2; ++k) {
-      const uint32_t sl = slots[t * N2 + k];
-      const int64_t xo = gtab[sl >> 24];
-      const double* src = a.x + (xo >= 0 ? xo + (int64_t)(sl & 0xffffffu) * stride + lane : 0);
-      cp_async8(buf + t * N2 + k, src, xo >= 0);
+      cp_async8(gtab + g, a.group_xoff + gbase + g);
+      cp_async8(gtab + G + g, a.group_hoff + gbase + g);
     }
   }
-  cp_async_commit();
+  cp_async_commit();  // group 1: group table
   if (COEF && ok) {
     const double* c = a.coef + (int64_t)cell * a.coef_stride + t * N2;
 #pragma unroll
-    for (int k = 0; k < N2; ++k) cp_async8(cbuf + t * N2 + k, c + k, true);
+    for (int k = 0; k < N2; ++k) cp_async8(cbuf + t * N2 + k, c + k);
   }
-  cp_async_commit();
-  cp_async_wait<1>();
+  cp_async_commit();  // group 2: coefficients (consumed after the interpolation)
+  if (ok) {
+#pragma unroll
+    for (int k = 0; k < N2; ++k) slots[t * N2 + k] = sl[k];
+  }
+  cp_async_wait_one();
   __syncwarp();
+
+  // ---- trip 3: gather X (A layout, z = t)
   double u[N][N];
 #pragma unroll
-  for (int y = 0; y < N; ++y)
+  for (int y = 0; y < N; ++y) {
 #pragma unroll
-    for (int x = 0; x < N; ++x) u[y][x] = ok ? buf[(t * N + y) * N + x] : 0.0;
+    for (int x = 0; x < N; ++x) {
+      double v = 0.0;
+      if (ok) {
+        const uint32_t s = sl[y * N + x];
+        const int64_t xo = gtab[s >> 24];
+        if (xo >= 0) v = __ldg(a.x + xo + (int64_t)(s & 0xffffffu) * stride + lane);
+      }
+      u[y][x] = v;
+    }
+  }
 
   // ---- values to the quadrature points
   double v1[N][N], v2[N][N];
   contract_fast<N, false>(u, v1, tb.S);   // x
   contract_slow<N, false>(v1, v2, tb.S);  // y
-  a_to_b<N>(v2, v1, buf, t, lane_ok);     // B: y = qy = t, [z][qx]
+  a_to_b<N>(v2, v1, buf, tt, lane_ok);    // B: y = qy = t, [z][qx]
   double uqB[N][N];
   contract_slow<N, false>(v1, uqB, tb.S); // z -> uq at (qz, qy=t, qx)
-  cp_async_wait<0>();
+  cp_async_wait_all();
   __syncwarp();
 
   double acc[N][N];
   if (KIN) {
     // gy in A layout (qz = t)
-    b_to_a<N>(uqB, v1, buf, t, lane_ok);  // v1 = uq[qz=t][qy][qx]
+    b_to_a<N>(uqB, v1, buf, tt, lane_ok);  // v1 = uq[qz=t][qy][qx]
     contract_slow<N, false>(v1, v2, tb.D);  // d/dy at the points
-    const double fy = tb.w[t < N ? t : 0] * tb.kin[1];
+    const double fy = tb.w[tt] * tb.kin[1];
 #pragma unroll
     for (int i = 0; i < N; ++i)
 #pragma unroll
@@ -273,11 +275,11 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
 #pragma unroll
       for (int i = 0; i < N; ++i)
 #pragma unroll
-        for (int j = 0; j < N; ++j) acc[i][j] = fma(cbuf[(t * N + i) * N + j], v1[i][j], acc[i][j]);
+        for (int j = 0; j < N; ++j) acc[i][j] = fma(cbuf[(tt * N + i) * N + j], v1[i][j], acc[i][j]);
     }
-    a_to_b<N>(acc, v2, buf, t, lane_ok);  // v2 = acc in B (qy = t): [qz][qx]
+    a_to_b<N>(acc, v2, buf, tt, lane_ok);  // v2 = acc in B (qy = t): [qz][qx]
     // gx and gz in B layout, applied row/column-wise to limit live registers
-    const double wt = tb.w[t < N ? t : 0];
+    const double wt = tb.w[tt];
     const double fx = wt * tb.kin[0];
     const double fz = wt * tb.kin[2];
 #pragma unroll
@@ -322,24 +324,24 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
     for (int z = 0; z < N; ++z)
 #pragma unroll
       for (int x = 0; x < N; ++x)
-        v2[z][x] = COEF ? cbuf[(z * N + t) * N + x] * uqB[z][x] : 0.0;
+        v2[z][x] = COEF ? cbuf[(z * N + tt) * N + x] * uqB[z][x] : 0.0;
   }
 
   // ---- back to the nodes: z, x in B, then y in A
   contract_slow<N, true>(v2, v1, tb.S);   // S^T along z
   contract_fast<N, true>(v1, v2, tb.S);   // S^T along x
-  b_to_a<N>(v2, v1, buf, t, lane_ok);     // A: z = t, [qy][x]
+  b_to_a<N>(v2, v1, buf, tt, lane_ok);    // A: z = t, [qy][x]
   contract_slow<N, true>(v1, v2, tb.S);   // S^T along y -> out[y][x]
 
   // ---- scatter-add
   if (ok) {
-    const int64_t* gh = gtab + kMaxGroups;
+    const int64_t* gh = gtab + G;
 #pragma unroll
     for (int y = 0; y < N; ++y) {
 #pragma unroll
       for (int x = 0; x < N; ++x) {
-        const uint32_t sl = slots[(t * N + y) * N + x];
-        double* p = a.hx + gh[sl >> 24] + (int64_t)(sl & 0xffffffu) * stride + lane;
+        const uint32_t s = slots[(t * N + y) * N + x];
+        double* p = a.hx + gh[s >> 24] + (int64_t)(s & 0xffffffu) * stride + lane;
         if (ATOMIC)
           atomicAdd(p, v2[y][x]);
         else
@@ -390,9 +392,9 @@ struct bmv_cellop {
   int64_t n_pairs = 0;
   int32_t n_cells = 0;
   std::vector<int64_t> color_start;  // empty => atomic single launch
-  int32_t *pair_visit = nullptr, *pair_lane = nullptr, *visit_cell = nullptr,
-          *visit_stride = nullptr;
-  int64_t *visit_goff = nullptr, *group_xoff = nullptr, *group_hoff = nullptr;
+  int max_groups = 4;
+  int4* pair_desc = nullptr;
+  int64_t *group_xoff = nullptr, *group_hoff = nullptr;
   uint32_t* cell_slots = nullptr;
   CellTables tables{};
 };
@@ -400,7 +402,7 @@ struct bmv_cellop {
 namespace {
 
 template <int N, bool KIN, bool COEF, bool ATOMIC>
-int launch_one(const CellArgs& args, const CellTables& tb, cudaStream_t st) {
+int launch_one(const CellArgs& args, const CellTables& tb, int G, cudaStream_t st) {
   using SM = CellSmem<N, COEF>;
   constexpr int P = SM::P;
   const int64_t n = args.pair_end - args.pair_begin;
@@ -408,36 +410,38 @@ int launch_one(const CellArgs& args, const CellTables& tb, cudaStream_t st) {
   static bool configured = false;  // per instantiation
   if (!configured) {
     BMV_CUDA_TRY(cudaFuncSetAttribute(cellop_kernel<N, KIN, COEF, ATOMIC>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SM::cta_bytes));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kWarps * SM::warp_bytes(kMaxGroups)));
     configured = true;
   }
   const int64_t per_cta = (int64_t)kWarps * P;
   const int64_t grid = (n + per_cta - 1) / per_cta;
-  cellop_kernel<N, KIN, COEF, ATOMIC><<<(unsigned)grid, kWarps * 32, SM::cta_bytes, st>>>(args, tb);
+  cellop_kernel<N, KIN, COEF, ATOMIC>
+      <<<(unsigned)grid, kWarps * 32, kWarps * SM::warp_bytes(G), st>>>(args, tb, G);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
 
 template <int N>
-int launch_n(const CellArgs& args, const CellTables& tb, bool kin, bool coef, bool atomic,
+int launch_n(const CellArgs& args, const CellTables& tb, int G, bool kin, bool coef, bool atomic,
              cudaStream_t st) {
   if (kin) {
-    if (coef) return atomic ? launch_one<N, true, true, true>(args, tb, st)
-                            : launch_one<N, true, true, false>(args, tb, st);
-    return atomic ? launch_one<N, true, false, true>(args, tb, st)
-                  : launch_one<N, true, false, false>(args, tb, st);
+    if (coef) return atomic ? launch_one<N, true, true, true>(args, tb, G, st)
+                            : launch_one<N, true, true, false>(args, tb, G, st);
+    return atomic ? launch_one<N, true, false, true>(args, tb, G, st)
+                  : launch_one<N, true, false, false>(args, tb, G, st);
   }
-  return atomic ? launch_one<N, false, true, true>(args, tb, st)
-                : launch_one<N, false, true, false>(args, tb, st);
+  return atomic ? launch_one<N, false, true, true>(args, tb, G, st)
+                : launch_one<N, false, true, false>(args, tb, G, st);
 }
 
-int launch_dispatch(int n, const CellArgs& args, const CellTables& tb, bool kin, bool coef,
-                    bool atomic, cudaStream_t st) {
+int launch_dispatch(int n, const CellArgs& args, const CellTables& tb, int G, bool kin,
+                    bool coef, bool atomic, cudaStream_t st) {
   switch (n) {
-    case 2: return launch_n<2>(args, tb, kin, coef, atomic, st);
-    case 3: return launch_n<3>(args, tb, kin, coef, atomic, st);
-    case 4: return launch_n<4>(args, tb, kin, coef, atomic, st);
-    case 5: return launch_n<5>(args, tb, kin, coef, atomic, st);
+    case 2: return launch_n<2>(args, tb, G, kin, coef, atomic, st);
+    case 3: return launch_n<3>(args, tb, G, kin, coef, atomic, st);
+    case 4: return launch_n<4>(args, tb, G, kin, coef, atomic, st);
+    case 5: return launch_n<5>(args, tb, G, kin, coef, atomic, st);
     default:
       set_error("unsupported nodes per axis %d (degree 1..4)", n);
       return BMV_ERR_INVALID;
@@ -489,18 +493,31 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
       rc = BMV_ERR_INVALID;
     }
   }
-  if (rc == BMV_OK) rc = upload(d->pair_visit, d->n_pairs, &p->pair_visit);
-  if (rc == BMV_OK) rc = upload(d->pair_lane, d->n_pairs, &p->pair_lane);
-  if (rc == BMV_OK) rc = upload(d->visit_cell, (int64_t)d->n_visits, &p->visit_cell);
-  if (rc == BMV_OK) rc = upload(d->visit_stride, (int64_t)d->n_visits, &p->visit_stride);
-  for (int32_t v = 0; rc == BMV_OK && v < d->n_visits; ++v) {
-    if (d->visit_goff[v + 1] - d->visit_goff[v] > kMaxGroups) {
-      set_error("a cell touches %lld block rows (max %d)",
-                (long long)(d->visit_goff[v + 1] - d->visit_goff[v]), kMaxGroups);
-      rc = BMV_ERR_INVALID;
+  // packed per-pair descriptor {cell, first group, lane | stride << 16, groups}
+  if (rc == BMV_OK && d->n_pairs > 0) {
+    std::vector<int4> desc((size_t)d->n_pairs);
+    int maxg = 1;
+    for (int64_t q = 0; q < d->n_pairs; ++q) {
+      const int32_t v = d->pair_visit[q];
+      if (v < 0 || v >= d->n_visits) {
+        set_error("pair %lld: visit %d out of range", (long long)q, v);
+        rc = BMV_ERR_INVALID;
+        break;
+      }
+      const int64_t g0 = d->visit_goff[v], ng = d->visit_goff[v + 1] - g0;
+      const int32_t stride = d->visit_stride[v], lane = d->pair_lane[q];
+      if (ng > kMaxGroups || stride >= 65536 || lane < 0 || lane >= stride || g0 > INT32_MAX) {
+        set_error("pair %lld: a cell touches %lld block rows (max %d) or bad lane %d / stride %d",
+                  (long long)q, (long long)ng, kMaxGroups, lane, stride);
+        rc = BMV_ERR_INVALID;
+        break;
+      }
+      desc[(size_t)q] = make_int4(d->visit_cell[v], (int)g0, lane | (stride << 16), (int)ng);
+      if (ng > maxg) maxg = (int)ng;
     }
+    p->max_groups = std::min(kMaxGroups, (maxg + 3) / 4 * 4);
+    if (rc == BMV_OK) rc = upload(desc.data(), d->n_pairs, &p->pair_desc);
   }
-  if (rc == BMV_OK) rc = upload(d->visit_goff, (int64_t)d->n_visits + 1, &p->visit_goff);
   if (rc == BMV_OK) rc = upload(d->group_xoff, d->n_groups_total, &p->group_xoff);
   if (rc == BMV_OK) rc = upload(d->group_hoff, d->n_groups_total, &p->group_hoff);
   if (rc == BMV_OK) rc = upload(d->cell_slots, (int64_t)d->n_cells * n3, &p->cell_slots);
@@ -524,11 +541,7 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
 
 int bmv_cellop_destroy(bmv_cellop* p) {
   if (!p) return BMV_OK;
-  release(p->pair_visit);
-  release(p->pair_lane);
-  release(p->visit_cell);
-  release(p->visit_stride);
-  release(p->visit_goff);
+  release(p->pair_desc);
   release(p->group_xoff);
   release(p->group_hoff);
   release(p->cell_slots);
@@ -581,17 +594,16 @@ int bmv_cellop_apply(bmv_cellop* p, int32_t kinetic, const double* coef, int64_t
     set_error("null value array");
     return BMV_ERR_INVALID;
   }
-  CellArgs args{p->pair_visit, p->pair_lane, p->visit_cell, p->visit_stride, p->visit_goff,
-                p->group_xoff, p->group_hoff, p->cell_slots, coef, coef_stride,
+  CellArgs args{p->pair_desc, p->group_xoff, p->group_hoff, p->cell_slots, coef, coef_stride,
                 0, p->n_pairs, x, hx};
   const bool use_coef = coef != nullptr;
   if (p->color_start.empty()) {
-    return launch_dispatch(p->n, args, p->tables, kinetic != 0, use_coef, true, st);
+    return launch_dispatch(p->n, args, p->tables, p->max_groups, kinetic != 0, use_coef, true, st);
   }
   for (size_t c = 0; c + 1 < p->color_start.size(); ++c) {
     args.pair_begin = p->color_start[c];
     args.pair_end = p->color_start[c + 1];
-    rc = launch_dispatch(p->n, args, p->tables, kinetic != 0, use_coef, false, st);
+    rc = launch_dispatch(p->n, args, p->tables, p->max_groups, kinetic != 0, use_coef, false, st);
     if (rc) return rc;
   }
   return BMV_OK;

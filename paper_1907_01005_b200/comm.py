@@ -271,6 +271,12 @@ class DistContext(RankContext):
         self.device = device
         self._pending = []
         self._torch = torch
+        # the first NCCL call of a group must involve every rank; point-to-point
+        # halo exchanges do not, so initialise the communicator collectively here
+        if self.backend == "nccl":
+            dist.barrier(device_ids=[torch.cuda.current_device()])
+        else:
+            dist.barrier()
 
     def isend(self, peer, tag, payload):
         torch = self._torch

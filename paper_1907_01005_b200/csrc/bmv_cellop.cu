@@ -135,16 +135,19 @@ template <> struct TileStride<5> { static constexpr int v = 125; };
 
 constexpr int kMaxGroups = 32;  // distinct block rows per cell (<= 27 at L = 0)
 
-// Dynamic shared memory per warp: pair tiles | coefficient tiles | slot tiles | group tables
+// Dynamic shared memory per warp: pair tiles (transposes) | coefficient and
+// slot staging in lane-interleaved order [k][lane] (conflict-free) | group
+// tables, one per pair at an odd stride of 2G+1 int64 (pairs hit distinct banks)
 template <int N, bool COEF>
 struct CellSmem {
   static constexpr int P = 32 / N;
   static constexpr int TILE = TileStride<N>::v;
-  static constexpr int N3 = N * N * N;
-  static constexpr int tile_bytes = P * TILE * 8;
-  static constexpr int coef_bytes = COEF ? P * TILE * 8 : 0;
-  static constexpr int slot_bytes = ((P * N3 * 4 + 15) / 16) * 16;
-  static __host__ __device__ int gtab_bytes(int G) { return P * G * 16; }
+  static constexpr int N2 = N * N;
+  static constexpr int tile_bytes = ((P * TILE * 8 + 15) / 16) * 16;
+  static constexpr int coef_bytes = COEF ? N2 * 32 * 8 : 0;
+  static constexpr int slot_bytes = N2 * 32 * 4;
+  static __host__ __device__ int gtab_stride(int G) { return 2 * G + 1; }
+  static __host__ __device__ int gtab_bytes(int G) { return ((P * (2 * G + 1) * 8 + 15) / 16) * 16; }
   static __host__ __device__ int warp_bytes(int G) {
     return tile_bytes + coef_bytes + slot_bytes + gtab_bytes(G);
   }
@@ -192,10 +195,11 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
 
   unsigned char* wbase = smem_raw + warp * SM::warp_bytes(G);
   double* buf = reinterpret_cast<double*>(wbase) + sub * TILE;
-  double* cbuf = reinterpret_cast<double*>(wbase + SM::tile_bytes) + sub * TILE;
-  uint32_t* slots = reinterpret_cast<uint32_t*>(wbase + SM::tile_bytes + SM::coef_bytes) + sub * N3;
+  double* cbase = reinterpret_cast<double*>(wbase + SM::tile_bytes);  // [k][lane]
+  double* cbuf = cbase + lid;
+  uint32_t* slots = reinterpret_cast<uint32_t*>(wbase + SM::tile_bytes + SM::coef_bytes) + lid;
   int64_t* gtab = reinterpret_cast<int64_t*>(wbase + SM::tile_bytes + SM::coef_bytes +
-                                             SM::slot_bytes) + sub * 2 * G;
+                                             SM::slot_bytes) + sub * SM::gtab_stride(G);
 
   // ---- trip 1: pair descriptor
   int cell = 0, lane = 0, stride = 0, ng = 0, gbase = 0;
@@ -224,12 +228,12 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
   if (COEF && ok) {
     const double* c = a.coef + (int64_t)cell * a.coef_stride + t * N2;
 #pragma unroll
-    for (int k = 0; k < N2; ++k) cp_async8(cbuf + t * N2 + k, c + k);
+    for (int k = 0; k < N2; ++k) cp_async8(cbuf + 32 * k, c + k);
   }
   cp_async_commit();  // group 2: coefficients (consumed after the interpolation)
   if (ok) {
 #pragma unroll
-    for (int k = 0; k < N2; ++k) slots[t * N2 + k] = sl[k];
+    for (int k = 0; k < N2; ++k) slots[32 * k] = sl[k];
   }
   cp_async_wait_one();
   __syncwarp();
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
 #pragma unroll
       for (int i = 0; i < N; ++i)
 #pragma unroll
-        for (int j = 0; j < N; ++j) acc[i][j] = fma(cbuf[(tt * N + i) * N + j], v1[i][j], acc[i][j]);
+        for (int j = 0; j < N; ++j) acc[i][j] = fma(cbuf[32 * (i * N + j)], v1[i][j], acc[i][j]);
     }
     a_to_b<N>(acc, v2, buf, tt, lane_ok);  // v2 = acc in B (qy = t): [qz][qx]
     // gx and gz in B layout, applied row/column-wise to limit live registers
@@ -324,7 +328,8 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
     for (int z = 0; z < N; ++z)
 #pragma unroll
       for (int x = 0; x < N; ++x)
-        v2[z][x] = COEF ? cbuf[(z * N + tt) * N + x] * uqB[z][x] : 0.0;
+        // element (qz=z, qy=t, qx=x) was staged by the thread of plane z, k = t*N + x
+        v2[z][x] = COEF ? cbase[32 * (tt * N + x) + z * P + sub] * uqB[z][x] : 0.0;
   }
 
   // ---- back to the nodes: z, x in B, then y in A
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
     for (int y = 0; y < N; ++y) {
 #pragma unroll
       for (int x = 0; x < N; ++x) {
-        const uint32_t s = slots[(t * N + y) * N + x];
+        const uint32_t s = slots[32 * (y * N + x)];
         double* p = a.hx + gh[s >> 24] + (int64_t)(s & 0xffffffu) * stride + lane;
         if (ATOMIC)
           atomicAdd(p, v2[y][x]);

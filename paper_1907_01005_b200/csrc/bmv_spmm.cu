@@ -97,6 +97,57 @@ __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel(const TmArgs g)
   }
 }
 
+// Fast path for output blocks of at most 8 x 8: lane = slice * 8 + i; the
+// 4 slices split the block rows (r = slice, slice + 4, ...), lane (slice, i)
+// accumulates output row i (8 entries) in registers; the slices are summed
+// with two xor-shuffles at the end of each segment.
+__global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8(const TmArgs g) {
+  extern __shared__ double stage[];
+  const int64_t ch = blockIdx.x;
+  const int64_t a_lo = g.chunk_a[2 * ch], b_lo = g.chunk_b[2 * ch];
+  const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
+  const int nb = (int)(g.chunk_b[2 * ch + 1] - b_lo);
+  double* SA = stage;
+  double* SB = stage + na;
+  for (int i = threadIdx.x; i < na; i += blockDim.x) SA[i] = __ldg(g.a + a_lo + i);
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) SB[i] = __ldg(g.b + b_lo + i);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slice = lane >> 3, i = lane & 7;
+  const int64_t s_end = g.chunk_seg_start[ch + 1];
+  for (int64_t sg = g.chunk_seg_start[ch] + warp; sg < s_end; sg += kTmWarps) {
+    const int64_t o = g.seg_out[sg];
+    const int rows = g.out_rows[o], cols = g.out_cols[o];
+    const int ii = i < rows ? i : 0;
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    const int64_t t1 = g.seg_tri_start[sg + 1];
+    for (int64_t t = g.seg_tri_start[sg]; t < t1; ++t) {
+      const double* A = SA + g.tri_a_soff[t];
+      const double* B = SB + g.tri_b_soff[t];
+      const int as = g.tri_a_stride[t], bs = g.tri_b_stride[t], nr = g.tri_rows[t];
+      for (int r = slice; r < nr; r += 4) {
+        const double av = A[r * as + ii];
+        const double* br = B + r * bs;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fma(av, br[j], acc[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 8);
+      acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
+    }
+    if (slice == 0 && i < rows) {
+      double* P = g.partial + g.seg_poff[sg] + i * cols;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < cols) P[j] = acc[j];
+    }
+  }
+}
+
 // One CTA per output block: C = sum of its segments' partials, chunk order.
 __global__ void __launch_bounds__(128) tm_reduce_kernel(const TmArgs g) {
   const int64_t o = blockIdx.x;
@@ -134,31 +185,61 @@ struct MmArgs {
 constexpr int kMmWarps = 8;
 
 // One CTA per chunk of block rows: stage A (one contiguous range), then one
-// warp per output block: C(i,j)[r][s] (+)= alpha * sum_pairs sum_k A[r][k] B[k][s]
+// warp per output block: C(i,j)[r][s] (+)= alpha * sum_pairs sum_k A[r][k] B[k][s].
+// Each B block (<= 16 x 16) is staged in warp-private shared memory; lanes
+// own entries e = lane + 32 m of the output block, EPT at a time.
+constexpr int kMmEPT = 8;
+constexpr int kMmBMax = 256;  // doubles per staged B block
+
 __global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs g) {
   extern __shared__ double stage[];
   const int64_t ch = blockIdx.x;
   const int64_t a_lo = g.chunk_a[2 * ch];
   const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
-  for (int i = threadIdx.x; i < na; i += blockDim.x) stage[i] = __ldg(g.a + a_lo + i);
+  double* SA = stage + kMmWarps * kMmBMax;
+  for (int i = threadIdx.x; i < na; i += blockDim.x) SA[i] = __ldg(g.a + a_lo + i);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* SBw = stage + warp * kMmBMax;
   const int64_t o_end = g.chunk_out_start[ch + 1];
   for (int64_t o = g.chunk_out_start[ch] + warp; o < o_end; o += kMmWarps) {
     const int rows = g.out_rows[o], cols = g.out_cols[o], cst = g.out_stride[o];
     const int64_t p0 = g.pair_start[o], p1 = g.pair_start[o + 1];
     const int entries = rows * cols;
-    for (int e = lane; e < entries; e += 32) {
-      const int r = e / cols, s = e - r * cols;
-      double acc = 0.0;
-      for (int64_t p = p0; p < p1; ++p) {
-        const double* A = stage + g.pair_a_soff[p] + r * g.pair_a_stride[p];
-        const double* B = g.b + g.pair_b_off[p] + s;
-        const int bs = g.pair_b_stride[p], nk = g.pair_inner[p];
-        for (int k = 0; k < nk; ++k) acc = fma(A[k], __ldg(B + (int64_t)k * bs), acc);
+    for (int e0 = 0; e0 < entries; e0 += 32 * kMmEPT) {
+      int rr[kMmEPT], cc[kMmEPT];
+      double acc[kMmEPT];
+#pragma unroll
+      for (int m = 0; m < kMmEPT; ++m) {
+        const int e = e0 + lane + 32 * m;
+        rr[m] = e < entries ? e / cols : 0;
+        cc[m] = e < entries ? e - (e / cols) * cols : 0;
+        acc[m] = 0.0;
       }
-      double* dst = g.c + g.out_off[o] + (int64_t)r * cst + s;
-      *dst = g.accumulate ? fma(g.alpha, acc, *dst) : g.alpha * acc;
+      for (int64_t p = p0; p < p1; ++p) {
+        const int nk = g.pair_inner[p], bs = g.pair_b_stride[p];
+        const double* Bg = g.b + g.pair_b_off[p];
+        __syncwarp();
+        for (int q = lane; q < nk * cols; q += 32) {
+          const int k = q / cols, c = q - k * cols;
+          SBw[k * 16 + c] = __ldg(Bg + (int64_t)k * bs + c);
+        }
+        __syncwarp();
+        const double* A = SA + g.pair_a_soff[p];
+        const int as = g.pair_a_stride[p];
+        for (int k = 0; k < nk; ++k) {
+#pragma unroll
+          for (int m = 0; m < kMmEPT; ++m) acc[m] = fma(A[rr[m] * as + k], SBw[k * 16 + cc[m]], acc[m]);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < kMmEPT; ++m) {
+        const int e = e0 + lane + 32 * m;
+        if (e < entries) {
+          double* dst = g.c + g.out_off[o] + (int64_t)rr[m] * cst + cc[m];
+          *dst = g.accumulate ? fma(g.alpha, acc[m], *dst) : g.alpha * acc[m];
+        }
+      }
     }
   }
 }
@@ -167,7 +248,7 @@ __global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs
 
 struct bmv_tmmult {
   int64_t n_out = 0, n_chunks = 0, n_seg = 0, n_tri = 0, partial_len = 0;
-  int smem_bytes = 0, ept = 8;
+  int smem_bytes = 0, ept = 8, small = 0, max_b_cols = 0;
   int64_t* out_off = nullptr;
   int32_t *out_rows = nullptr, *out_cols = nullptr, *out_stride = nullptr;
   int64_t *out_seg_start = nullptr, *out_seg_list = nullptr, *chunk_a = nullptr,
@@ -233,6 +314,18 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
   p->partial_len = d->partial_len;
   p->smem_bytes = d->smem_doubles * 8;
   p->ept = max_ent <= 64 ? 2 : (max_ent <= 128 ? 4 : 8);
+  {
+    int mr = 0, mc = 0;
+    for (int64_t o = 0; o < d->n_out; ++o) {
+      mr = d->out_rows[o] > mr ? d->out_rows[o] : mr;
+      mc = d->out_cols[o] > mc ? d->out_cols[o] : mc;
+    }
+    // the fast path reads 8 B-columns per row: needs B strides >= 8 (true for W = 8)
+    int min_bs = 1 << 30;
+    for (int64_t t = 0; t < d->n_triples; ++t)
+      min_bs = d->tri_b_stride[t] < min_bs ? d->tri_b_stride[t] : min_bs;
+    p->small = (mr <= 8 && mc <= 8 && (d->n_triples == 0 || min_bs >= 8)) ? 1 : 0;
+  }
   int rc = upload(d->out_off, d->n_out, &p->out_off);
   if (!rc) rc = upload(d->out_rows, d->n_out, &p->out_rows);
   if (!rc) rc = upload(d->out_cols, d->n_out, &p->out_cols);
@@ -258,6 +351,7 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
   }
   if (!rc) {
     cudaError_t e = cudaFuncSetAttribute(tm_chunk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel8, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
     if (e != cudaSuccess) {
@@ -289,7 +383,9 @@ int bmv_tmmult_run(bmv_tmmult* p, const double* a, const double* b, double* c, i
            p->tri_a_stride, p->tri_b_stride, a, b, p->partial, c};
   if (p->n_chunks > 0) {
     const unsigned grid = (unsigned)p->n_chunks;
-    if (p->ept == 2)
+    if (p->small)
+      tm_chunk_kernel8<<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
+    else if (p->ept == 2)
       tm_chunk_kernel<2><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
     else if (p->ept == 4)
       tm_chunk_kernel<4><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
@@ -321,10 +417,22 @@ int bmv_mmult_create(const bmv_mmult_desc* d, bmv_mmult** out) {
   int dev = 0, max_smem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if ((int64_t)d->smem_doubles * 8 > max_smem) {
+  if ((int64_t)d->smem_doubles * 8 + kMmWarps * kMmBMax * 8 > max_smem) {
     set_error("mmult chunk needs %lld bytes of shared memory (max %d)",
               (long long)d->smem_doubles * 8, max_smem);
     return BMV_ERR_INVALID;
+  }
+  for (int64_t o = 0; o < d->n_out; ++o) {
+    if (d->out_cols[o] > 16) {
+      set_error("mmult column blocks wider than 16 are not supported");
+      return BMV_ERR_INVALID;
+    }
+  }
+  for (int64_t q = 0; q < d->n_pairs; ++q) {
+    if (d->pair_inner[q] > 16) {
+      set_error("mmult inner blocks wider than 16 are not supported");
+      return BMV_ERR_INVALID;
+    }
   }
   auto* p = new bmv_mmult();
   p->n_out = d->n_out;
@@ -374,7 +482,8 @@ int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, dou
   MmArgs g{p->chunk_a, p->chunk_out_start, p->out_off, p->out_rows, p->out_cols, p->out_stride,
            p->pair_start, p->pair_a_soff, p->pair_a_stride, p->pair_inner, p->pair_b_off,
            p->pair_b_stride, a, b, c, alpha, accumulate};
-  mmult_chunk_kernel<<<(unsigned)p->n_chunks, kMmWarps * 32, p->smem_bytes, st>>>(g);
+  mmult_chunk_kernel<<<(unsigned)p->n_chunks, kMmWarps * 32,
+                       p->smem_bytes + kMmWarps * kMmBMax * 8, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }

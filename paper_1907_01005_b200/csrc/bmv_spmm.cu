@@ -46,6 +46,66 @@ struct TmArgs {
   double* __restrict__ c;
 };
 
+// ---- 1D TMA bulk copies (cp.async.bulk, SASS UBLKCP) completed on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Stage n doubles from global src to shared dst: one elected thread issues
+// TMA bulk copies (16-byte granules, 32 KB pieces) when both ends are
+// 16-byte aligned and n is even; otherwise all threads copy.  Returns after
+// the data is visible to the whole CTA.
+__device__ __forceinline__ void stage_ranges(double* d0, const double* s0, int n0, double* d1,
+                                             const double* s1, int n1, uint64_t* bar) {
+  const bool bulk = ((smem_u32(d0) | smem_u32(d1)) & 15) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(s0) | reinterpret_cast<uintptr_t>(s1)) & 15) == 0 &&
+                    ((n0 | n1) & 1) == 0;
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      mbar_expect_tx(bar, (unsigned)(n0 + n1) * 8u);
+      constexpr int kPiece = 4096;  // doubles per bulk copy
+      for (int i = 0; i < n0; i += kPiece)
+        bulk_g2s(d0 + i, s0 + i, (unsigned)min(kPiece, n0 - i) * 8u, bar);
+      for (int i = 0; i < n1; i += kPiece)
+        bulk_g2s(d1 + i, s1 + i, (unsigned)min(kPiece, n1 - i) * 8u, bar);
+    }
+    __syncthreads();  // barrier initialised before anyone waits
+    mbar_wait(bar, 0);
+  } else {
+    for (int i = threadIdx.x; i < n0; i += blockDim.x) d0[i] = __ldg(s0 + i);
+    for (int i = threadIdx.x; i < n1; i += blockDim.x) d1[i] = __ldg(s1 + i);
+    __syncthreads();
+  }
+}
+
 constexpr int kTmWarps = 8;
 
 // One CTA per chunk of consecutive block rows: stage the chunk's A and B
@@ -54,16 +114,15 @@ constexpr int kTmWarps = 8;
 // output block; EPT entries per lane (EPT * 32 >= entries of the block).
 template <int EPT>
 __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel(const TmArgs g) {
-  extern __shared__ double stage[];
+  extern __shared__ __align__(16) double stage[];
   const int64_t ch = blockIdx.x;
   const int64_t a_lo = g.chunk_a[2 * ch], b_lo = g.chunk_b[2 * ch];
   const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
   const int nb = (int)(g.chunk_b[2 * ch + 1] - b_lo);
+  __shared__ uint64_t bar;
   double* SA = stage;
   double* SB = stage + na;
-  for (int i = threadIdx.x; i < na; i += blockDim.x) SA[i] = __ldg(g.a + a_lo + i);
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) SB[i] = __ldg(g.b + b_lo + i);
-  __syncthreads();
+  stage_ranges(SA, g.a + a_lo, na, SB, g.b + b_lo, nb, &bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t s_end = g.chunk_seg_start[ch + 1];
   for (int64_t sg = g.chunk_seg_start[ch] + warp; sg < s_end; sg += kTmWarps) {
@@ -102,16 +161,15 @@ __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel(const TmArgs g)
 // accumulates output row i (8 entries) in registers; the slices are summed
 // with two xor-shuffles at the end of each segment.
 __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8(const TmArgs g) {
-  extern __shared__ double stage[];
+  extern __shared__ __align__(16) double stage[];
   const int64_t ch = blockIdx.x;
   const int64_t a_lo = g.chunk_a[2 * ch], b_lo = g.chunk_b[2 * ch];
   const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
   const int nb = (int)(g.chunk_b[2 * ch + 1] - b_lo);
+  __shared__ uint64_t bar;
   double* SA = stage;
   double* SB = stage + na;
-  for (int i = threadIdx.x; i < na; i += blockDim.x) SA[i] = __ldg(g.a + a_lo + i);
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) SB[i] = __ldg(g.b + b_lo + i);
-  __syncthreads();
+  stage_ranges(SA, g.a + a_lo, na, SB, g.b + b_lo, nb, &bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slice = lane >> 3, i = lane & 7;
   const int64_t s_end = g.chunk_seg_start[ch + 1];
@@ -192,13 +250,13 @@ constexpr int kMmEPT = 8;
 constexpr int kMmBMax = 256;  // doubles per staged B block
 
 __global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs g) {
-  extern __shared__ double stage[];
+  extern __shared__ __align__(16) double stage[];
   const int64_t ch = blockIdx.x;
   const int64_t a_lo = g.chunk_a[2 * ch];
   const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
+  __shared__ uint64_t bar;
   double* SA = stage + kMmWarps * kMmBMax;
-  for (int i = threadIdx.x; i < na; i += blockDim.x) SA[i] = __ldg(g.a + a_lo + i);
-  __syncthreads();
+  stage_ranges(SA, g.a + a_lo, na, SA + na, g.a + a_lo + na, 0, &bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* SBw = stage + warp * kMmBMax;
   const int64_t o_end = g.chunk_out_start[ch + 1];
@@ -227,9 +285,19 @@ __global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs
         __syncwarp();
         const double* A = SA + g.pair_a_soff[p];
         const int as = g.pair_a_stride[p];
-        for (int k = 0; k < nk; ++k) {
+        if (cols == 8) {  // lanes keep one column: the C value is shared by all m
+          const int c0 = lane & 7;
+          for (int k = 0; k < nk; ++k) {
+            const double cv = SBw[k * 16 + c0];
 #pragma unroll
-          for (int m = 0; m < kMmEPT; ++m) acc[m] = fma(A[rr[m] * as + k], SBw[k * 16 + cc[m]], acc[m]);
+            for (int m = 0; m < kMmEPT; ++m) acc[m] = fma(A[rr[m] * as + k], cv, acc[m]);
+          }
+        } else {
+          for (int k = 0; k < nk; ++k) {
+#pragma unroll
+            for (int m = 0; m < kMmEPT; ++m)
+              acc[m] = fma(A[rr[m] * as + k], SBw[k * 16 + cc[m]], acc[m]);
+          }
         }
       }
 #pragma unroll

@@ -480,6 +480,48 @@ class BlockCsrMatrix:
             raise PatternError(f"block for entry ({row}, {col}) not stored")
         self.data[off] += value
 
+    # -- compact support values (B200 transfer format) ---------------------------
+
+    def _support_index(self):
+        if self.support is None:
+            raise StateError("no column support attached (support.attach_support)")
+        key = ("support_index", id(self.support))
+        cache = _plan_cache(self)
+        hit = cache.get(key)
+        if hit is None:
+            flat, _, _ = self.support.owned_entries(self)
+            hit = (_IndexList(flat, self.device), int(flat.size))
+            cache[key] = hit
+        return hit
+
+    def n_support_values(self) -> int:
+        return self._support_index()[1]
+
+    def upload_support_values(self, values: torch.Tensor):
+        """Owned values from the compact support order (column, then row).
+
+        `values` (host, ideally pinned, or device) holds only the structurally
+        nonzero entries -- the nnz of the multivector instead of its padded
+        blocks -- so host->device traffic drops by the block fill factor.  The
+        owned region is zeroed first; ghost blocks are untouched.
+        """
+        self._require(OWNED)
+        idx, n = self._support_index()
+        if values.numel() != n:
+            raise ShapeError(f"{values.numel()} values for {n} support entries")
+        dev = values.to(self.device, non_blocking=True) if values.device != self.device else values
+        _zero_range(self.data, 0, self.n_owned_values)
+        idx.scatter(dev.reshape(-1).to(torch.float64), self.data, add=False)
+
+    def download_support_values(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Owned support entries in the compact order (device tensor, or copied into `out`)."""
+        idx, n = self._support_index()
+        vals = idx.gather(self.data)
+        if out is not None:
+            out.copy_(vals, non_blocking=True)
+            return out
+        return vals
+
     # -- ghost exchange -------------------------------------------------------
 
     def _exchange_plan(self):

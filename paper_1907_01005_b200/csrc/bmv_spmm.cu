@@ -369,6 +369,7 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
   int dev = 0, max_smem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  max_smem -= 1024;  // static shared memory (mbarrier) of the kernels
   if ((int64_t)d->smem_doubles * 8 > max_smem) {
     set_error("tmmult chunk needs %lld bytes of shared memory (max %d)",
               (long long)d->smem_doubles * 8, max_smem);
@@ -418,10 +419,10 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
     }
   }
   if (!rc) {
-    cudaError_t e = cudaFuncSetAttribute(tm_chunk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel8, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    cudaError_t e = cudaFuncSetAttribute(tm_chunk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel8, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e != cudaSuccess) {
       set_error("cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
       rc = BMV_ERR_CUDA;
@@ -485,6 +486,7 @@ int bmv_mmult_create(const bmv_mmult_desc* d, bmv_mmult** out) {
   int dev = 0, max_smem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  max_smem -= 1024;  // static shared memory (mbarrier) of the kernel
   if ((int64_t)d->smem_doubles * 8 + kMmWarps * kMmBMax * 8 > max_smem) {
     set_error("mmult chunk needs %lld bytes of shared memory (max %d)",
               (long long)d->smem_doubles * 8, max_smem);
@@ -521,7 +523,7 @@ int bmv_mmult_create(const bmv_mmult_desc* d, bmv_mmult** out) {
   if (!rc) rc = upload(d->pair_b_stride, d->n_pairs, &p->pair_b_stride);
   if (!rc) {
     cudaError_t e = cudaFuncSetAttribute(mmult_chunk_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e != cudaSuccess) {
       set_error("cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
       rc = BMV_ERR_CUDA;

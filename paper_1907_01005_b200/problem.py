@@ -244,54 +244,8 @@ def in_support(prob: Problem, rows, new_cols) -> np.ndarray:
 
 
 def _support_entries(matrix: BlockCsrMatrix, prob: Problem):
-    """(flat offsets, global rows, new cols) of the support entries in owned rows.
-
-    Cached per (pattern, layout): X and Y share it.
-    """
-    key = ("support_entries", id(matrix.pattern), id(matrix.layout), matrix.lane_width)
-    hit = prob.extra.get(key)
-    if hit is not None:
-        return hit
-    lay = prob.loc_layout
-    layout = matrix.layout
-    lo, hi = layout.owned_rows
-    centre = lay.centers_of_new_cols()
-    sizes = np.asarray([prob.supports[int(c)].size for c in centre], dtype=np.int64)
-    rows = np.concatenate([prob.supports[int(c)] for c in centre]).astype(np.int64)
-    cols = np.repeat(np.arange(lay.n_columns, dtype=np.int64), sizes)
-    keep = (rows >= lo) & (rows < hi)
-    rows, cols = rows[keep], cols[keep]
-    if rows.size == 0:
-        hit = (rows, rows, cols)
-        prob.extra[key] = hit
-        return hit
-    blocks = layout.blocks
-    nb_own = layout.n_owned_blocks
-    own_sizes = blocks.sizes[layout.first_block : layout.first_block + nb_own]
-    lb_of_row = np.repeat(np.arange(nb_own, dtype=np.int64), own_sizes)
-    lb = lb_of_row[rows - lo]
-    rib = rows - blocks.starts[layout.first_block + lb]
-    cb_of_col = np.repeat(np.arange(matrix.col_blocks.n_blocks, dtype=np.int64),
-                          matrix.col_blocks.sizes)
-    cb = cb_of_col[cols]
-    n_cb = matrix.col_blocks.n_blocks
-    n_own_pos = int(matrix.row_start[nb_own])
-    if nb_own * n_cb <= 64_000_000:
-        table = np.full(nb_own * n_cb, -1, dtype=np.int64)
-        table[matrix.pos_row[:n_own_pos] * n_cb + matrix.col_index[:n_own_pos]] = \
-            np.arange(n_own_pos, dtype=np.int64)
-        pos = table[lb * n_cb + cb]
-    else:
-        keys = matrix.local_keys()[:n_own_pos]
-        k = lb * n_cb + cb
-        pos = np.searchsorted(keys, k)
-        pos = np.where((pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == k), pos, -1)
-    if (pos < 0).any():
-        raise ValueError("support entry outside the multivector pattern")
-    flat = matrix.block_offsets[pos] + rib * matrix.col_strides[cb] + (cols - matrix.col_blocks.starts[cb])
-    hit = (flat, rows, cols)
-    prob.extra[key] = hit
-    return hit
+    """(flat offsets, global rows, new cols) of the support entries in owned rows."""
+    return prob.column_support.owned_entries(matrix)
 
 
 def fill_multivector(matrix: BlockCsrMatrix, prob: Problem, seed: int, attach: bool = True):

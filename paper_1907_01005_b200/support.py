@@ -77,6 +77,55 @@ class ColumnSupport:
         cache[key] = m
         return m
 
+    def owned_entries(self, matrix):
+        """(flat storage offsets, global rows, columns) of the support entries
+        in the matrix's owned rows, column-major (column, then row) order.
+
+        This is the compact value order used by `upload_support_values`.
+        Cached per (pattern, layout, lane width).
+        """
+        key = ("owned", id(matrix.pattern), id(matrix.layout), matrix.lane_width)
+        cache = self.__dict__.setdefault("_cache", {})
+        hit = cache.get(key)
+        if hit is not None:
+            return hit
+        layout = matrix.layout
+        lo, hi = layout.owned_rows
+        cols = np.repeat(np.arange(self.n_cols, dtype=np.int64), np.diff(self.col_ptr))
+        rows = self.rows
+        keep = (rows >= lo) & (rows < hi)
+        rows, cols = rows[keep], cols[keep]
+        if rows.size == 0:
+            hit = (rows, rows, cols)
+            cache[key] = hit
+            return hit
+        blocks = layout.blocks
+        nb_own = layout.n_owned_blocks
+        own_sizes = blocks.sizes[layout.first_block : layout.first_block + nb_own]
+        lb = np.repeat(np.arange(nb_own, dtype=np.int64), own_sizes)[rows - lo]
+        rib = rows - blocks.starts[layout.first_block + lb]
+        cbk = np.repeat(np.arange(matrix.col_blocks.n_blocks, dtype=np.int64),
+                        matrix.col_blocks.sizes)[cols]
+        n_cb = matrix.col_blocks.n_blocks
+        n_own_pos = int(matrix.row_start[nb_own])
+        if nb_own * n_cb <= 64_000_000:
+            table = np.full(nb_own * n_cb, -1, dtype=np.int64)
+            table[matrix.pos_row[:n_own_pos] * n_cb + matrix.col_index[:n_own_pos]] = \
+                np.arange(n_own_pos, dtype=np.int64)
+            pos = table[lb * n_cb + cbk]
+        else:
+            keys = matrix.local_keys()[:n_own_pos]
+            k = lb * n_cb + cbk
+            pos = np.searchsorted(keys, k)
+            pos = np.where((pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == k), pos, -1)
+        if (pos < 0).any():
+            raise ConsistencyError("a support entry lies outside the multivector pattern")
+        flat = (matrix.block_offsets[pos] + rib * matrix.col_strides[cbk]
+                + (cols - matrix.col_blocks.starts[cbk]))
+        hit = (flat, rows, cols)
+        cache[key] = hit
+        return hit
+
     def check_matrix(self, matrix) -> None:
         """Raise ConsistencyError if an owned entry outside the support is nonzero."""
         dense_rows = matrix.layout.owned_rows

@@ -266,3 +266,18 @@ def test_compute_refuses_cpu_storage():
     y = BlockCsrMatrix(pat, lay, c, 8, device=CPU)
     with pytest.raises(DeviceError):
         op.apply(hamiltonian_operator(None), x, y)
+
+
+def test_compact_support_values_roundtrip():
+    """upload/download_support_values (the compact transfer format) round-trip."""
+    from paper_1907_01005_b200 import problem as P
+    from paper_1907_01005_b200.comm import serial_context
+
+    prob = P.build_problem("smoke")
+    st = P.make_rank_setup(serial_context(CPU), prob, device=CPU)
+    vals = st.x.download_support_values().clone()
+    assert vals.numel() == st.x.n_support_values() == 5320  # nnzX of the smoke config
+    dense = st.x.to_dense_owned()
+    st.x.data.fill_(3.0)
+    st.x.upload_support_values(vals)
+    assert np.array_equal(st.x.to_dense_owned(), dense)

@@ -831,7 +831,7 @@ def mmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, alpha: float 
         counters.flops += plan.flops
 
 
-_TM_STAGE_TARGET = 12_000  # doubles of A + B staged per K4 chunk (96 KB)
+_TM_STAGE_TARGET = 6_000   # doubles staged per K4/K5 chunk (48 KB; double-buffered)
 _TM_STAGE_MAX = 27_000     # hard limit per chunk (216 KB of shared memory)
 
 

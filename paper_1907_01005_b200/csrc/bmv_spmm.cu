@@ -12,6 +12,8 @@
 // fixed order: no atomics, bit-reproducible.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "bmv_common.cuh"
 
 namespace bmv {
@@ -156,67 +158,118 @@ __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel(const TmArgs g)
   }
 }
 
-// Fast path for output blocks of at most 8 x 8: lane = slice * 8 + i; the
-// 4 slices split the block rows (r = slice, slice + 4, ...), lane (slice, i)
-// accumulates output row i (8 entries) in registers; the slices are summed
-// with two xor-shuffles at the end of each segment.
-__global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8(const TmArgs g) {
+// Issue the TMA bulk copies of chunk ch (A range then B range) into dst,
+// completing on bar (called by one thread).
+__device__ __forceinline__ void issue_chunk(const double* a, const int64_t* ca, const double* b,
+                                            const int64_t* cb, int64_t ch, double* dst,
+                                            uint64_t* bar) {
+  const int64_t a_lo = ca[2 * ch], b_lo = cb ? cb[2 * ch] : 0;
+  const int na = (int)(ca[2 * ch + 1] - a_lo);
+  const int nb = cb ? (int)(cb[2 * ch + 1] - b_lo) : 0;
+  mbar_expect_tx(bar, (unsigned)(na + nb) * 8u);
+  constexpr int kPiece = 4096;
+  for (int i = 0; i < na; i += kPiece)
+    bulk_g2s(dst + i, a + a_lo + i, (unsigned)min(kPiece, na - i) * 8u, bar);
+  for (int i = 0; i < nb; i += kPiece)
+    bulk_g2s(dst + na + i, b + b_lo + i, (unsigned)min(kPiece, nb - i) * 8u, bar);
+}
+
+// Fast path for output blocks of at most 8 x 8, persistent over chunks with
+// a double-buffered TMA stage (chunk k+1 streams in while chunk k is
+// computed).  lane = slice * 8 + i: the 4 slices split the block rows
+// (r = slice, slice + 4, ...), lane (slice, i) accumulates output row i
+// (8 entries) in registers; slices are summed with two xor-shuffles.
+__global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8(const TmArgs g, int64_t n_chunks,
+                                                                   int buf_doubles) {
   extern __shared__ __align__(16) double stage[];
-  const int64_t ch = blockIdx.x;
-  const int64_t a_lo = g.chunk_a[2 * ch], b_lo = g.chunk_b[2 * ch];
-  const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
-  const int nb = (int)(g.chunk_b[2 * ch + 1] - b_lo);
-  __shared__ uint64_t bar;
-  double* SA = stage;
-  double* SB = stage + na;
-  stage_ranges(SA, g.a + a_lo, na, SB, g.b + b_lo, nb, &bar);
+  __shared__ uint64_t bars[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+  }
+  __syncthreads();
+  int64_t ch = blockIdx.x;
+  if (threadIdx.x == 0 && ch < n_chunks) issue_chunk(g.a, g.chunk_a, g.b, g.chunk_b, ch, stage, &bars[0]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slice = lane >> 3, i = lane & 7;
-  const int64_t s_end = g.chunk_seg_start[ch + 1];
-  for (int64_t sg = g.chunk_seg_start[ch] + warp; sg < s_end; sg += kTmWarps) {
-    const int64_t o = g.seg_out[sg];
-    const int rows = g.out_rows[o], cols = g.out_cols[o];
-    const int ii = i < rows ? i : 0;
-    double acc[8];
+  for (int it = 0; ch < n_chunks; ch += gridDim.x, ++it) {
+    const int bsel = it & 1;
+    const int64_t nx = ch + gridDim.x;
+    if (threadIdx.x == 0 && nx < n_chunks)
+      issue_chunk(g.a, g.chunk_a, g.b, g.chunk_b, nx, stage + (bsel ^ 1) * buf_doubles,
+                  &bars[bsel ^ 1]);
+    mbar_wait(&bars[bsel], (it >> 1) & 1);
+    const double* SA = stage + bsel * buf_doubles;
+    const double* SB = SA + (g.chunk_a[2 * ch + 1] - g.chunk_a[2 * ch]);
+    const int64_t s_end = g.chunk_seg_start[ch + 1];
+    for (int64_t sg = g.chunk_seg_start[ch] + warp; sg < s_end; sg += kTmWarps) {
+      const int64_t o = g.seg_out[sg];
+      const int rows = g.out_rows[o], cols = g.out_cols[o];
+      const int ii = i < rows ? i : 0;
+      double acc[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-    const int64_t t1 = g.seg_tri_start[sg + 1];
-    for (int64_t t = g.seg_tri_start[sg]; t < t1; ++t) {
-      const double* A = SA + g.tri_a_soff[t];
-      const double* B = SB + g.tri_b_soff[t];
-      const int as = g.tri_a_stride[t], bs = g.tri_b_stride[t], nr = g.tri_rows[t];
-      for (int r = slice; r < nr; r += 4) {
-        const double av = A[r * as + ii];
-        const double* br = B + r * bs;
+      for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+      const int64_t t1 = g.seg_tri_start[sg + 1];
+      for (int64_t t = g.seg_tri_start[sg]; t < t1; ++t) {
+        const double* A = SA + g.tri_a_soff[t];
+        const double* B = SB + g.tri_b_soff[t];
+        const int as = g.tri_a_stride[t], bs = g.tri_b_stride[t], nr = g.tri_rows[t];
+        for (int r = slice; r < nr; r += 4) {
+          const double av = A[r * as + ii];
+          const double* br = B + r * bs;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fma(av, br[j], acc[j]);
+          for (int j = 0; j < 8; ++j) acc[j] = fma(av, br[j], acc[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 8);
+        acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
+      }
+      if (slice == 0 && i < rows) {
+        double* P = g.partial + g.seg_poff[sg] + i * cols;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < cols) P[j] = acc[j];
       }
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 8);
-      acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
-    }
-    if (slice == 0 && i < rows) {
-      double* P = g.partial + g.seg_poff[sg] + i * cols;
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < cols) P[j] = acc[j];
-    }
+    __syncthreads();  // buffer bsel fully consumed before it is refilled
   }
 }
 
-// One CTA per output block: C = sum of its segments' partials, chunk order.
-__global__ void __launch_bounds__(128) tm_reduce_kernel(const TmArgs g) {
+// One CTA (256 threads) per output block: `parts` thread groups each sum a
+// fixed strided subset of the block's segment partials (in chunk order),
+// then the groups are added in a fixed order: deterministic.
+__global__ void __launch_bounds__(256) tm_reduce_kernel(const TmArgs g) {
+  __shared__ double red[256];
   const int64_t o = blockIdx.x;
   const int cols = g.out_cols[o], cst = g.out_stride[o];
   const int ent = g.out_rows[o] * cols;
+  const int parts = ent > 0 ? max(1, (int)blockDim.x / ent) : 1;
+  const int part = threadIdx.x / max(ent, 1), e = threadIdx.x - part * max(ent, 1);
   const int64_t s0 = g.out_seg_start[o], s1 = g.out_seg_start[o + 1];
-  for (int e = threadIdx.x; e < ent; e += blockDim.x) {
-    double acc = 0.0;
-    for (int64_t s = s0; s < s1; ++s) acc += g.partial[g.seg_poff[g.out_seg_list[s]] + e];
-    const int i = e / cols, j = e - i * cols;
-    g.c[g.out_off[o] + (int64_t)i * cst + j] = acc;
+  double acc = 0.0;
+  if (part < parts) {
+    int64_t s = s0 + part;
+    for (; s + 3 * parts < s1; s += 4 * parts) {
+      const double v0 = g.partial[g.seg_poff[g.out_seg_list[s]] + e];
+      const double v1 = g.partial[g.seg_poff[g.out_seg_list[s + parts]] + e];
+      const double v2 = g.partial[g.seg_poff[g.out_seg_list[s + 2 * parts]] + e];
+      const double v3 = g.partial[g.seg_poff[g.out_seg_list[s + 3 * parts]] + e];
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
+    }
+    for (; s < s1; s += parts) acc += g.partial[g.seg_poff[g.out_seg_list[s]] + e];
+  }
+  if (threadIdx.x < 256) red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int q = threadIdx.x; q < ent; q += blockDim.x) {
+    double sum = 0.0;
+    for (int pp = 0; pp < parts; ++pp) sum += red[pp * ent + q];
+    const int i = q / cols, j = q - i * cols;
+    g.c[g.out_off[o] + (int64_t)i * cst + j] = sum;
   }
 }
 
@@ -249,6 +302,59 @@ constexpr int kMmWarps = 8;
 constexpr int kMmEPT = 8;
 constexpr int kMmBMax = 256;  // doubles per staged B block
 
+__device__ __forceinline__ void mm_block(const MmArgs& g, int64_t o, const double* SA, double* SBw,
+                                         int lane) {
+  const int rows = g.out_rows[o], cols = g.out_cols[o], cst = g.out_stride[o];
+  const int64_t p0 = g.pair_start[o], p1 = g.pair_start[o + 1];
+  const int entries = rows * cols;
+  for (int e0 = 0; e0 < entries; e0 += 32 * kMmEPT) {
+    int rr[kMmEPT], cc[kMmEPT];
+    double acc[kMmEPT];
+#pragma unroll
+    for (int m = 0; m < kMmEPT; ++m) {
+      const int e = e0 + lane + 32 * m;
+      rr[m] = e < entries ? e / cols : 0;
+      cc[m] = e < entries ? e - (e / cols) * cols : 0;
+      acc[m] = 0.0;
+    }
+    for (int64_t p = p0; p < p1; ++p) {
+      const int nk = g.pair_inner[p], bs = g.pair_b_stride[p];
+      const double* Bg = g.b + g.pair_b_off[p];
+      __syncwarp();
+      for (int q = lane; q < nk * cols; q += 32) {
+        const int k = q / cols, c = q - k * cols;
+        SBw[k * 16 + c] = __ldg(Bg + (int64_t)k * bs + c);
+      }
+      __syncwarp();
+      const double* A = SA + g.pair_a_soff[p];
+      const int as = g.pair_a_stride[p];
+      if (cols == 8) {  // lanes keep one column: the C value is shared by all m
+        const int c0 = lane & 7;
+        for (int k = 0; k < nk; ++k) {
+          const double cv = SBw[k * 16 + c0];
+#pragma unroll
+          for (int m = 0; m < kMmEPT; ++m) acc[m] = fma(A[rr[m] * as + k], cv, acc[m]);
+        }
+      } else {
+        for (int k = 0; k < nk; ++k) {
+#pragma unroll
+          for (int m = 0; m < kMmEPT; ++m)
+            acc[m] = fma(A[rr[m] * as + k], SBw[k * 16 + cc[m]], acc[m]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kMmEPT; ++m) {
+      const int e = e0 + lane + 32 * m;
+      if (e < entries) {
+        double* dst = g.c + g.out_off[o] + (int64_t)rr[m] * cst + cc[m];
+        *dst = g.accumulate ? fma(g.alpha, acc[m], *dst) : g.alpha * acc[m];
+      }
+    }
+  }
+}
+
+// One CTA per chunk (fallback, any alignment).
 __global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs g) {
   extern __shared__ __align__(16) double stage[];
   const int64_t ch = blockIdx.x;
@@ -260,55 +366,34 @@ __global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* SBw = stage + warp * kMmBMax;
   const int64_t o_end = g.chunk_out_start[ch + 1];
-  for (int64_t o = g.chunk_out_start[ch] + warp; o < o_end; o += kMmWarps) {
-    const int rows = g.out_rows[o], cols = g.out_cols[o], cst = g.out_stride[o];
-    const int64_t p0 = g.pair_start[o], p1 = g.pair_start[o + 1];
-    const int entries = rows * cols;
-    for (int e0 = 0; e0 < entries; e0 += 32 * kMmEPT) {
-      int rr[kMmEPT], cc[kMmEPT];
-      double acc[kMmEPT];
-#pragma unroll
-      for (int m = 0; m < kMmEPT; ++m) {
-        const int e = e0 + lane + 32 * m;
-        rr[m] = e < entries ? e / cols : 0;
-        cc[m] = e < entries ? e - (e / cols) * cols : 0;
-        acc[m] = 0.0;
-      }
-      for (int64_t p = p0; p < p1; ++p) {
-        const int nk = g.pair_inner[p], bs = g.pair_b_stride[p];
-        const double* Bg = g.b + g.pair_b_off[p];
-        __syncwarp();
-        for (int q = lane; q < nk * cols; q += 32) {
-          const int k = q / cols, c = q - k * cols;
-          SBw[k * 16 + c] = __ldg(Bg + (int64_t)k * bs + c);
-        }
-        __syncwarp();
-        const double* A = SA + g.pair_a_soff[p];
-        const int as = g.pair_a_stride[p];
-        if (cols == 8) {  // lanes keep one column: the C value is shared by all m
-          const int c0 = lane & 7;
-          for (int k = 0; k < nk; ++k) {
-            const double cv = SBw[k * 16 + c0];
-#pragma unroll
-            for (int m = 0; m < kMmEPT; ++m) acc[m] = fma(A[rr[m] * as + k], cv, acc[m]);
-          }
-        } else {
-          for (int k = 0; k < nk; ++k) {
-#pragma unroll
-            for (int m = 0; m < kMmEPT; ++m)
-              acc[m] = fma(A[rr[m] * as + k], SBw[k * 16 + cc[m]], acc[m]);
-          }
-        }
-      }
-#pragma unroll
-      for (int m = 0; m < kMmEPT; ++m) {
-        const int e = e0 + lane + 32 * m;
-        if (e < entries) {
-          double* dst = g.c + g.out_off[o] + (int64_t)rr[m] * cst + cc[m];
-          *dst = g.accumulate ? fma(g.alpha, acc[m], *dst) : g.alpha * acc[m];
-        }
-      }
-    }
+  for (int64_t o = g.chunk_out_start[ch] + warp; o < o_end; o += kMmWarps) mm_block(g, o, SA, SBw, lane);
+}
+
+// Persistent over chunks with a double-buffered TMA stage of A.
+__global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel_p(const MmArgs g, int64_t n_chunks,
+                                                                       int buf_doubles) {
+  extern __shared__ __align__(16) double stage[];
+  __shared__ uint64_t bars[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+  }
+  __syncthreads();
+  double* abuf = stage + kMmWarps * kMmBMax;
+  int64_t ch = blockIdx.x;
+  if (threadIdx.x == 0 && ch < n_chunks) issue_chunk(g.a, g.chunk_a, nullptr, nullptr, ch, abuf, &bars[0]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* SBw = stage + warp * kMmBMax;
+  for (int it = 0; ch < n_chunks; ch += gridDim.x, ++it) {
+    const int bsel = it & 1;
+    const int64_t nx = ch + gridDim.x;
+    if (threadIdx.x == 0 && nx < n_chunks)
+      issue_chunk(g.a, g.chunk_a, nullptr, nullptr, nx, abuf + (bsel ^ 1) * buf_doubles, &bars[bsel ^ 1]);
+    mbar_wait(&bars[bsel], (it >> 1) & 1);
+    const double* SA = abuf + bsel * buf_doubles;
+    const int64_t o_end = g.chunk_out_start[ch + 1];
+    for (int64_t o = g.chunk_out_start[ch] + warp; o < o_end; o += kMmWarps) mm_block(g, o, SA, SBw, lane);
+    __syncthreads();
   }
 }
 
@@ -316,7 +401,7 @@ __global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs
 
 struct bmv_tmmult {
   int64_t n_out = 0, n_chunks = 0, n_seg = 0, n_tri = 0, partial_len = 0;
-  int smem_bytes = 0, ept = 8, small = 0, max_b_cols = 0;
+  int smem_bytes = 0, ept = 8, small = 0, max_b_cols = 0, aligned = 0;
   int64_t* out_off = nullptr;
   int32_t *out_rows = nullptr, *out_cols = nullptr, *out_stride = nullptr;
   int64_t *out_seg_start = nullptr, *out_seg_list = nullptr, *chunk_a = nullptr,
@@ -329,7 +414,7 @@ struct bmv_tmmult {
 
 struct bmv_mmult {
   int64_t n_out = 0, n_chunks = 0, n_pairs = 0;
-  int smem_bytes = 0;
+  int smem_bytes = 0, aligned = 0;
   int64_t *chunk_a = nullptr, *chunk_out_start = nullptr, *out_off = nullptr,
           *pair_start = nullptr, *pair_b_off = nullptr;
   int32_t *out_rows = nullptr, *out_cols = nullptr, *out_stride = nullptr,
@@ -394,6 +479,12 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
     for (int64_t t = 0; t < d->n_triples; ++t)
       min_bs = d->tri_b_stride[t] < min_bs ? d->tri_b_stride[t] : min_bs;
     p->small = (mr <= 8 && mc <= 8 && (d->n_triples == 0 || min_bs >= 8)) ? 1 : 0;
+    // TMA bulk staging: every range start (and so every A/B split) 16-byte aligned
+    int al = 1;
+    for (int64_t c = 0; c < d->n_chunks; ++c)
+      al &= ((d->chunk_a[2 * c] | d->chunk_a[2 * c + 1] | d->chunk_b[2 * c] | d->chunk_b[2 * c + 1]) & 1) == 0;
+    p->aligned = al;
+    if (p->small && p->aligned && 2 * (int64_t)d->smem_doubles * 8 > max_smem) p->aligned = 0;
   }
   int rc = upload(d->out_off, d->n_out, &p->out_off);
   if (!rc) rc = upload(d->out_rows, d->n_out, &p->out_rows);
@@ -452,8 +543,12 @@ int bmv_tmmult_run(bmv_tmmult* p, const double* a, const double* b, double* c, i
            p->tri_a_stride, p->tri_b_stride, a, b, p->partial, c};
   if (p->n_chunks > 0) {
     const unsigned grid = (unsigned)p->n_chunks;
-    if (p->small)
-      tm_chunk_kernel8<<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
+    if (p->small && p->aligned) {
+      const unsigned pgrid = (unsigned)std::min<int64_t>(p->n_chunks, (int64_t)sm_count() * 2);
+      tm_chunk_kernel8<<<pgrid, kTmWarps * 32, 2 * p->smem_bytes, st>>>(g, p->n_chunks,
+                                                                         p->smem_bytes / 8);
+    } else if (p->small)
+      tm_chunk_kernel<2><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
     else if (p->ept == 2)
       tm_chunk_kernel<2><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
     else if (p->ept == 4)
@@ -462,7 +557,7 @@ int bmv_tmmult_run(bmv_tmmult* p, const double* a, const double* b, double* c, i
       tm_chunk_kernel<8><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
     BMV_CHECK_LAUNCH();
   }
-  tm_reduce_kernel<<<(unsigned)p->n_out, 64, 0, st>>>(g);
+  tm_reduce_kernel<<<(unsigned)p->n_out, 256, 0, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
@@ -552,8 +647,14 @@ int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, dou
   MmArgs g{p->chunk_a, p->chunk_out_start, p->out_off, p->out_rows, p->out_cols, p->out_stride,
            p->pair_start, p->pair_a_soff, p->pair_a_stride, p->pair_inner, p->pair_b_off,
            p->pair_b_stride, a, b, c, alpha, accumulate};
-  mmult_chunk_kernel<<<(unsigned)p->n_chunks, kMmWarps * 32,
-                       p->smem_bytes + kMmWarps * kMmBMax * 8, st>>>(g);
+  if (p->aligned) {
+    const unsigned pgrid = (unsigned)std::min<int64_t>(p->n_chunks, (int64_t)sm_count() * 2);
+    mmult_chunk_kernel_p<<<pgrid, kMmWarps * 32, 2 * p->smem_bytes + kMmWarps * kMmBMax * 8, st>>>(
+        g, p->n_chunks, p->smem_bytes / 8);
+  } else {
+    mmult_chunk_kernel<<<(unsigned)p->n_chunks, kMmWarps * 32,
+                         p->smem_bytes + kMmWarps * kMmBMax * 8, st>>>(g);
+  }
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }

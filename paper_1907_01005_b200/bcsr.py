@@ -782,7 +782,12 @@ def _mmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     flops = int(2 * np.sum(arrays["out_rows"].astype(np.int64)[per]
                            * arrays["pair_inner"].astype(np.int64)
                            * arrays["out_cols"].astype(np.int64)[per]))
+    n_own_c = int(c.row_start[c.n_owned_blocks])
+    own_cols = c.col_index[:n_own_c]
+    full_cover = bool(n_out == n_own_c and
+                      np.all(c.col_blocks.sizes[own_cols] == c.col_strides[own_cols]))
     plan = _MmultPlan(arrays, n_out, int(pa.size), flops)
+    plan.full_cover = full_cover
     cache[key] = (plan, b, c)
     return plan
 
@@ -823,15 +828,20 @@ def mmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, alpha: float 
     c.ensure_owned()
     plan = _mmult_plan(a, b, c)
     lib = _lib.require_device()
+    zero_len = 0 if accumulate else c.data.numel()
+    if not accumulate and plan.full_cover:
+        # every owned value is overwritten by the kernel (all owned blocks have
+        # products, no padded lanes): only the ghost blocks need zero_out
+        _zero_range(c.data, c._ghost_data_begin, c.data.numel())
+        zero_len = 0
     _lib.check(lib.bmv_mmult_run(plan.handle.raw, _lib.dptr(a.data), _lib.dptr(b.data),
                                  _lib.dptr(c.data), float(alpha), 1 if accumulate else 0,
-                                 0 if accumulate else c.data.numel(),
-                                 _lib.stream_handle(c.device)), "bmv_mmult_run")
+                                 zero_len, _lib.stream_handle(c.device)), "bmv_mmult_run")
     if counters is not None:
         counters.flops += plan.flops
 
 
-_TM_STAGE_TARGET = 6_000   # doubles staged per K4/K5 chunk (48 KB; double-buffered)
+_TM_STAGE_TARGET = 3_000   # doubles staged per K4/K5 chunk (24 KB: several CTAs per SM)
 _TM_STAGE_MAX = 27_000     # hard limit per chunk (216 KB of shared memory)
 
 
@@ -913,9 +923,13 @@ def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     out_rows = c.local_row_sizes[c.pos_row[outs]].astype(np.int64)
     out_cols = c.col_blocks.sizes[c.col_index[outs]].astype(np.int64)
     seg_ent = out_rows[seg_out] * out_cols[seg_out]
-    seg_poff = np.concatenate([[0], np.cumsum(seg_ent)]).astype(np.int64)
+    # partials of one output block contiguous, in chunk order (coalesced reduce)
     order2 = np.lexsort((seg_chunk, seg_out))
     out_seg_start = np.searchsorted(seg_out[order2], np.arange(n_out + 1)).astype(np.int64)
+    poff_sorted = np.concatenate([[0], np.cumsum(seg_ent[order2])]).astype(np.int64)
+    seg_poff = np.empty(seg_ent.size + 1, dtype=np.int64)
+    seg_poff[order2] = poff_sorted[:-1]
+    seg_poff[-1] = poff_sorted[-1]
     tri_chunk = chunk
     arrays = dict(
         out_off=c.block_offsets[outs].astype(np.int64),

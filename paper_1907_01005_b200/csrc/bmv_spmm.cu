@@ -174,6 +174,56 @@ __device__ __forceinline__ void issue_chunk(const double* a, const int64_t* ca, 
     bulk_g2s(dst + na + i, b + b_lo + i, (unsigned)min(kPiece, nb - i) * 8u, bar);
 }
 
+// Fast path for output blocks of at most 8 x 8, one chunk per CTA (TMA-staged).
+// lane = slice * 8 + i: the 4 slices split the block rows (r = slice,
+// slice + 4, ...), lane (slice, i) accumulates output row i in registers;
+// slices are summed with two xor-shuffles.
+__global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8_1(const TmArgs g) {
+  extern __shared__ __align__(16) double stage[];
+  __shared__ uint64_t bar;
+  const int64_t ch = blockIdx.x;
+  const int64_t a_lo = g.chunk_a[2 * ch], b_lo = g.chunk_b[2 * ch];
+  const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
+  const int nb = (int)(g.chunk_b[2 * ch + 1] - b_lo);
+  double* SA = stage;
+  double* SB = stage + na;
+  stage_ranges(SA, g.a + a_lo, na, SB, g.b + b_lo, nb, &bar);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slice = lane >> 3, i = lane & 7;
+  const int64_t s_end = g.chunk_seg_start[ch + 1];
+  for (int64_t sg = g.chunk_seg_start[ch] + warp; sg < s_end; sg += kTmWarps) {
+    const int64_t o = g.seg_out[sg];
+    const int rows = g.out_rows[o], cols = g.out_cols[o];
+    const int ii = i < rows ? i : 0;
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    const int64_t t1 = g.seg_tri_start[sg + 1];
+    for (int64_t t = g.seg_tri_start[sg]; t < t1; ++t) {
+      const double* A = SA + g.tri_a_soff[t];
+      const double* B = SB + g.tri_b_soff[t];
+      const int as = g.tri_a_stride[t], bs = g.tri_b_stride[t], nr = g.tri_rows[t];
+      for (int r = slice; r < nr; r += 4) {
+        const double av = A[r * as + ii];
+        const double* br = B + r * bs;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fma(av, br[j], acc[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 8);
+      acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
+    }
+    if (slice == 0 && i < rows) {
+      double* P = g.partial + g.seg_poff[sg] + i * cols;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < cols) P[j] = acc[j];
+    }
+  }
+}
+
 // Fast path for output blocks of at most 8 x 8, persistent over chunks with
 // a double-buffered TMA stage (chunk k+1 streams in while chunk k is
 // computed).  lane = slice * 8 + i: the 4 slices split the block rows
@@ -237,33 +287,36 @@ __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8(const TmArgs g
   }
 }
 
-// One CTA (256 threads) per output block: `parts` thread groups each sum a
-// fixed strided subset of the block's segment partials (in chunk order),
-// then the groups are added in a fixed order: deterministic.
-__global__ void __launch_bounds__(256) tm_reduce_kernel(const TmArgs g) {
-  __shared__ double red[256];
+// One CTA (512 threads) per output block.  The partials of an output block's
+// segments are contiguous, in chunk order (laid out so by the plan): thread
+// group `part` sums partials part, part + parts, ... of entry e (coalesced,
+// no indirection), then the groups are added in a fixed order.
+__global__ void __launch_bounds__(512) tm_reduce_kernel(const TmArgs g) {
+  __shared__ double red[512];
   const int64_t o = blockIdx.x;
   const int cols = g.out_cols[o], cst = g.out_stride[o];
   const int ent = g.out_rows[o] * cols;
-  const int parts = ent > 0 ? max(1, (int)blockDim.x / ent) : 1;
-  const int part = threadIdx.x / max(ent, 1), e = threadIdx.x - part * max(ent, 1);
-  const int64_t s0 = g.out_seg_start[o], s1 = g.out_seg_start[o + 1];
+  const int e_div = max(ent, 1);
+  const int parts = max(1, (int)blockDim.x / e_div);
+  const int part = threadIdx.x / e_div, e = threadIdx.x - part * e_div;
+  const int64_t nseg = g.out_seg_start[o + 1] - g.out_seg_start[o];
+  const double* P = g.partial + g.seg_poff[g.out_seg_list[g.out_seg_start[o]]];
   double acc = 0.0;
-  if (part < parts) {
-    int64_t s = s0 + part;
-    for (; s + 3 * parts < s1; s += 4 * parts) {
-      const double v0 = g.partial[g.seg_poff[g.out_seg_list[s]] + e];
-      const double v1 = g.partial[g.seg_poff[g.out_seg_list[s + parts]] + e];
-      const double v2 = g.partial[g.seg_poff[g.out_seg_list[s + 2 * parts]] + e];
-      const double v3 = g.partial[g.seg_poff[g.out_seg_list[s + 3 * parts]] + e];
+  if (part < parts && e < ent && nseg > 0) {
+    int64_t k = part;
+    for (; k + 3 * parts < nseg; k += 4 * parts) {
+      const double v0 = P[k * ent + e];
+      const double v1 = P[(k + parts) * ent + e];
+      const double v2 = P[(k + 2 * parts) * ent + e];
+      const double v3 = P[(k + 3 * parts) * ent + e];
       acc += v0;
       acc += v1;
       acc += v2;
       acc += v3;
     }
-    for (; s < s1; s += parts) acc += g.partial[g.seg_poff[g.out_seg_list[s]] + e];
+    for (; k < nseg; k += parts) acc += P[k * ent + e];
   }
-  if (threadIdx.x < 256) red[threadIdx.x] = acc;
+  red[threadIdx.x] = acc;
   __syncthreads();
   for (int q = threadIdx.x; q < ent; q += blockDim.x) {
     double sum = 0.0;
@@ -512,6 +565,7 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
   if (!rc) {
     cudaError_t e = cudaFuncSetAttribute(tm_chunk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel8, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel8_1, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e != cudaSuccess) {
@@ -543,12 +597,8 @@ int bmv_tmmult_run(bmv_tmmult* p, const double* a, const double* b, double* c, i
            p->tri_a_stride, p->tri_b_stride, a, b, p->partial, c};
   if (p->n_chunks > 0) {
     const unsigned grid = (unsigned)p->n_chunks;
-    if (p->small && p->aligned) {
-      const unsigned pgrid = (unsigned)std::min<int64_t>(p->n_chunks, (int64_t)sm_count() * 2);
-      tm_chunk_kernel8<<<pgrid, kTmWarps * 32, 2 * p->smem_bytes, st>>>(g, p->n_chunks,
-                                                                         p->smem_bytes / 8);
-    } else if (p->small)
-      tm_chunk_kernel<2><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
+    if (p->small)
+      tm_chunk_kernel8_1<<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
     else if (p->ept == 2)
       tm_chunk_kernel<2><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
     else if (p->ept == 4)
@@ -557,7 +607,7 @@ int bmv_tmmult_run(bmv_tmmult* p, const double* a, const double* b, double* c, i
       tm_chunk_kernel<8><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
     BMV_CHECK_LAUNCH();
   }
-  tm_reduce_kernel<<<(unsigned)p->n_out, 256, 0, st>>>(g);
+  tm_reduce_kernel<<<(unsigned)p->n_out, 512, 0, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
@@ -647,14 +697,8 @@ int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, dou
   MmArgs g{p->chunk_a, p->chunk_out_start, p->out_off, p->out_rows, p->out_cols, p->out_stride,
            p->pair_start, p->pair_a_soff, p->pair_a_stride, p->pair_inner, p->pair_b_off,
            p->pair_b_stride, a, b, c, alpha, accumulate};
-  if (p->aligned) {
-    const unsigned pgrid = (unsigned)std::min<int64_t>(p->n_chunks, (int64_t)sm_count() * 2);
-    mmult_chunk_kernel_p<<<pgrid, kMmWarps * 32, 2 * p->smem_bytes + kMmWarps * kMmBMax * 8, st>>>(
-        g, p->n_chunks, p->smem_bytes / 8);
-  } else {
-    mmult_chunk_kernel<<<(unsigned)p->n_chunks, kMmWarps * 32,
-                         p->smem_bytes + kMmWarps * kMmBMax * 8, st>>>(g);
-  }
+  mmult_chunk_kernel<<<(unsigned)p->n_chunks, kMmWarps * 32,
+                       p->smem_bytes + kMmWarps * kMmBMax * 8, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }

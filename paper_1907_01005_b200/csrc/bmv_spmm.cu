@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "bmv_common.cuh"
 
@@ -46,7 +47,12 @@ struct TmArgs {
   const double* __restrict__ b;
   double* __restrict__ partial;
   double* __restrict__ c;
+  const int32_t* __restrict__ chunk_ids;  // blockIdx -> chunk (size class launch)
+  double* __restrict__ partial2;          // second-level partials [out][split][256]
+  int splits;                             // second-level splits per output block
 };
+
+constexpr int kRedSeg = 64;  // segments per first-level reduction CTA
 
 // ---- 1D TMA bulk copies (cp.async.bulk, SASS UBLKCP) completed on an mbarrier
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -117,7 +123,7 @@ constexpr int kTmWarps = 8;
 template <int EPT>
 __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel(const TmArgs g) {
   extern __shared__ __align__(16) double stage[];
-  const int64_t ch = blockIdx.x;
+  const int64_t ch = g.chunk_ids ? g.chunk_ids[blockIdx.x] : blockIdx.x;
   const int64_t a_lo = g.chunk_a[2 * ch], b_lo = g.chunk_b[2 * ch];
   const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
   const int nb = (int)(g.chunk_b[2 * ch + 1] - b_lo);
@@ -181,7 +187,7 @@ __device__ __forceinline__ void issue_chunk(const double* a, const int64_t* ca, 
 __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8_1(const TmArgs g) {
   extern __shared__ __align__(16) double stage[];
   __shared__ uint64_t bar;
-  const int64_t ch = blockIdx.x;
+  const int64_t ch = g.chunk_ids ? g.chunk_ids[blockIdx.x] : blockIdx.x;
   const int64_t a_lo = g.chunk_a[2 * ch], b_lo = g.chunk_b[2 * ch];
   const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
   const int nb = (int)(g.chunk_b[2 * ch + 1] - b_lo);
@@ -287,40 +293,44 @@ __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8(const TmArgs g
   }
 }
 
-// One CTA (512 threads) per output block.  The partials of an output block's
-// segments are contiguous, in chunk order (laid out so by the plan): thread
-// group `part` sums partials part, part + parts, ... of entry e (coalesced,
-// no indirection), then the groups are added in a fixed order.
-__global__ void __launch_bounds__(512) tm_reduce_kernel(const TmArgs g) {
-  __shared__ double red[512];
+// Two-level deterministic reduction of the segment partials.  The partials
+// of one output block are contiguous, in chunk order (laid out so by the
+// plan).  Level 1: CTA (o, split) sums kRedSeg consecutive segments of o,
+// thread group `part` taking segments part, part + parts, ... (coalesced,
+// no indirection), groups added in a fixed order.  Level 2: one CTA per o
+// adds the splits in order and writes the C block.
+__global__ void __launch_bounds__(256) tm_reduce1_kernel(const TmArgs g) {
+  __shared__ double red[256];
   const int64_t o = blockIdx.x;
-  const int cols = g.out_cols[o], cst = g.out_stride[o];
+  const int split = blockIdx.y;
+  const int cols = g.out_cols[o];
   const int ent = g.out_rows[o] * cols;
   const int e_div = max(ent, 1);
   const int parts = max(1, (int)blockDim.x / e_div);
   const int part = threadIdx.x / e_div, e = threadIdx.x - part * e_div;
   const int64_t nseg = g.out_seg_start[o + 1] - g.out_seg_start[o];
-  const double* P = g.partial + g.seg_poff[g.out_seg_list[g.out_seg_start[o]]];
+  const int64_t k0 = (int64_t)split * kRedSeg, k1 = min(nseg, k0 + kRedSeg);
   double acc = 0.0;
-  if (part < parts && e < ent && nseg > 0) {
-    int64_t k = part;
-    for (; k + 3 * parts < nseg; k += 4 * parts) {
-      const double v0 = P[k * ent + e];
-      const double v1 = P[(k + parts) * ent + e];
-      const double v2 = P[(k + 2 * parts) * ent + e];
-      const double v3 = P[(k + 3 * parts) * ent + e];
-      acc += v0;
-      acc += v1;
-      acc += v2;
-      acc += v3;
-    }
-    for (; k < nseg; k += parts) acc += P[k * ent + e];
+  if (part < parts && e < ent && k0 < k1) {
+    const double* P = g.partial + g.seg_poff[g.out_seg_list[g.out_seg_start[o]]];
+    for (int64_t k = k0 + part; k < k1; k += parts) acc += P[k * ent + e];
   }
   red[threadIdx.x] = acc;
   __syncthreads();
   for (int q = threadIdx.x; q < ent; q += blockDim.x) {
     double sum = 0.0;
     for (int pp = 0; pp < parts; ++pp) sum += red[pp * ent + q];
+    g.partial2[((int64_t)o * g.splits + split) * 256 + q] = sum;
+  }
+}
+
+__global__ void __launch_bounds__(256) tm_reduce2_kernel(const TmArgs g) {
+  const int64_t o = blockIdx.x;
+  const int cols = g.out_cols[o], cst = g.out_stride[o];
+  const int ent = g.out_rows[o] * cols;
+  for (int q = threadIdx.x; q < ent; q += blockDim.x) {
+    double sum = 0.0;
+    for (int sp = 0; sp < g.splits; ++sp) sum += g.partial2[((int64_t)o * g.splits + sp) * 256 + q];
     const int i = q / cols, j = q - i * cols;
     g.c[g.out_off[o] + (int64_t)i * cst + j] = sum;
   }
@@ -344,6 +354,7 @@ struct MmArgs {
   double* __restrict__ c;
   double alpha;
   int accumulate;
+  const int32_t* __restrict__ chunk_ids;  // blockIdx -> chunk (size class launch)
 };
 
 constexpr int kMmWarps = 8;
@@ -410,7 +421,7 @@ __device__ __forceinline__ void mm_block(const MmArgs& g, int64_t o, const doubl
 // One CTA per chunk (fallback, any alignment).
 __global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs g) {
   extern __shared__ __align__(16) double stage[];
-  const int64_t ch = blockIdx.x;
+  const int64_t ch = g.chunk_ids ? g.chunk_ids[blockIdx.x] : blockIdx.x;
   const int64_t a_lo = g.chunk_a[2 * ch];
   const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
   __shared__ uint64_t bar;
@@ -450,6 +461,36 @@ __global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel_p(const MmAr
   }
 }
 
+// Chunks split into two launch classes by staged size, so one oversized block
+// row does not force its shared-memory footprint on every CTA.
+constexpr int kSmallStage = 3584;  // doubles (28 KB): several CTAs per SM
+
+struct ChunkClasses {
+  int32_t* ids[2] = {nullptr, nullptr};
+  int64_t count[2] = {0, 0};
+  int smem[2] = {0, 0};  // bytes
+
+  int build(const int64_t* ca, const int64_t* cb, int64_t n_chunks, int extra_bytes) {
+    std::vector<int32_t> lists[2];
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      const int64_t dbl = (ca[2 * c + 1] - ca[2 * c]) + (cb ? cb[2 * c + 1] - cb[2 * c] : 0);
+      const int k = dbl <= kSmallStage ? 0 : 1;
+      lists[k].push_back((int32_t)c);
+      smem[k] = std::max<int>(smem[k], (int)(dbl * 8) + extra_bytes);
+    }
+    for (int k = 0; k < 2; ++k) {
+      count[k] = (int64_t)lists[k].size();
+      int rc = upload(lists[k].data(), count[k], &ids[k]);
+      if (rc) return rc;
+    }
+    return BMV_OK;
+  }
+  void release_all() {
+    release(ids[0]);
+    release(ids[1]);
+  }
+};
+
 }  // namespace
 
 struct bmv_tmmult {
@@ -463,11 +504,15 @@ struct bmv_tmmult {
   int32_t *tri_a_soff = nullptr, *tri_b_soff = nullptr, *tri_rows = nullptr,
           *tri_a_stride = nullptr, *tri_b_stride = nullptr;
   double* partial = nullptr;
+  double* partial2 = nullptr;
+  int splits = 1;
+  ChunkClasses cls;
 };
 
 struct bmv_mmult {
   int64_t n_out = 0, n_chunks = 0, n_pairs = 0;
   int smem_bytes = 0, aligned = 0;
+  ChunkClasses cls;
   int64_t *chunk_a = nullptr, *chunk_out_start = nullptr, *out_off = nullptr,
           *pair_start = nullptr, *pair_b_off = nullptr;
   int32_t *out_rows = nullptr, *out_cols = nullptr, *out_stride = nullptr,
@@ -482,8 +527,9 @@ int bmv_tmmult_destroy(bmv_tmmult* p) {
   void* ptrs[] = {p->out_off, p->out_rows, p->out_cols, p->out_stride, p->out_seg_start,
                   p->out_seg_list, p->chunk_a, p->chunk_b, p->chunk_seg_start, p->seg_out,
                   p->seg_tri_start, p->seg_poff, p->tri_a_soff, p->tri_b_soff, p->tri_rows,
-                  p->tri_a_stride, p->tri_b_stride, p->partial};
+                  p->tri_a_stride, p->tri_b_stride, p->partial, p->partial2};
   for (void* q : ptrs) release(q);
+  p->cls.release_all();
   delete p;
   return BMV_OK;
 }
@@ -562,6 +608,18 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
       rc = BMV_ERR_CUDA;
     }
   }
+  if (!rc) rc = p->cls.build(d->chunk_a, d->chunk_b, d->n_chunks, 0);
+  if (!rc) {
+    int64_t max_seg = 1;
+    for (int64_t o = 0; o < d->n_out; ++o)
+      max_seg = std::max<int64_t>(max_seg, d->out_seg_start[o + 1] - d->out_seg_start[o]);
+    p->splits = (int)((max_seg + kRedSeg - 1) / kRedSeg);
+    const size_t n2 = (size_t)std::max<int64_t>(d->n_out, 1) * p->splits * 256;
+    if (cudaMalloc((void**)&p->partial2, sizeof(double) * n2) != cudaSuccess) {
+      set_error("cudaMalloc of second-level partials failed");
+      rc = BMV_ERR_CUDA;
+    }
+  }
   if (!rc) {
     cudaError_t e = cudaFuncSetAttribute(tm_chunk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel8, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
@@ -594,20 +652,26 @@ int bmv_tmmult_run(bmv_tmmult* p, const double* a, const double* b, double* c, i
   TmArgs g{p->out_off, p->out_rows, p->out_cols, p->out_stride, p->out_seg_start,
            p->out_seg_list, p->chunk_a, p->chunk_b, p->chunk_seg_start, p->seg_out,
            p->seg_tri_start, p->seg_poff, p->tri_a_soff, p->tri_b_soff, p->tri_rows,
-           p->tri_a_stride, p->tri_b_stride, a, b, p->partial, c};
-  if (p->n_chunks > 0) {
-    const unsigned grid = (unsigned)p->n_chunks;
+           p->tri_a_stride, p->tri_b_stride, a, b, p->partial, c, nullptr, p->partial2,
+           p->splits};
+  for (int k = 0; k < 2; ++k) {
+    if (p->cls.count[k] == 0) continue;
+    g.chunk_ids = p->cls.ids[k];
+    const unsigned grid = (unsigned)p->cls.count[k];
+    const int smem = p->cls.smem[k];
     if (p->small)
-      tm_chunk_kernel8_1<<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
+      tm_chunk_kernel8_1<<<grid, kTmWarps * 32, smem, st>>>(g);
     else if (p->ept == 2)
-      tm_chunk_kernel<2><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
+      tm_chunk_kernel<2><<<grid, kTmWarps * 32, smem, st>>>(g);
     else if (p->ept == 4)
-      tm_chunk_kernel<4><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
+      tm_chunk_kernel<4><<<grid, kTmWarps * 32, smem, st>>>(g);
     else
-      tm_chunk_kernel<8><<<grid, kTmWarps * 32, p->smem_bytes, st>>>(g);
+      tm_chunk_kernel<8><<<grid, kTmWarps * 32, smem, st>>>(g);
     BMV_CHECK_LAUNCH();
   }
-  tm_reduce_kernel<<<(unsigned)p->n_out, 512, 0, st>>>(g);
+  tm_reduce1_kernel<<<dim3((unsigned)p->n_out, (unsigned)p->splits), 256, 0, st>>>(g);
+  BMV_CHECK_LAUNCH();
+  tm_reduce2_kernel<<<(unsigned)p->n_out, 256, 0, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
@@ -618,6 +682,7 @@ int bmv_mmult_destroy(bmv_mmult* p) {
                   p->out_rows, p->out_cols, p->out_stride, p->pair_a_soff, p->pair_a_stride,
                   p->pair_inner, p->pair_b_stride};
   for (void* q : ptrs) release(q);
+  p->cls.release_all();
   delete p;
   return BMV_OK;
 }
@@ -696,9 +761,13 @@ int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, dou
   if (p->n_out == 0 || p->n_chunks == 0) return BMV_OK;
   MmArgs g{p->chunk_a, p->chunk_out_start, p->out_off, p->out_rows, p->out_cols, p->out_stride,
            p->pair_start, p->pair_a_soff, p->pair_a_stride, p->pair_inner, p->pair_b_off,
-           p->pair_b_stride, a, b, c, alpha, accumulate};
-  mmult_chunk_kernel<<<(unsigned)p->n_chunks, kMmWarps * 32,
-                       p->smem_bytes + kMmWarps * kMmBMax * 8, st>>>(g);
+           p->pair_b_stride, a, b, c, alpha, accumulate, nullptr};
+  for (int k = 0; k < 2; ++k) {
+    if (p->cls.count[k] == 0) continue;
+    g.chunk_ids = p->cls.ids[k];
+    mmult_chunk_kernel<<<(unsigned)p->cls.count[k], kMmWarps * 32, p->cls.smem[k], st>>>(g);
+    BMV_CHECK_LAUNCH();
+  }
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }

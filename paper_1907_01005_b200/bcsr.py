@@ -753,7 +753,7 @@ def _mmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     if n_rows and int(row_dbl.max()) > _TM_STAGE_MAX:
         raise ShapeError(f"mmult block row needs {int(row_dbl.max()) * 8} bytes of shared memory")
     target = int(np.clip(int(row_dbl.sum()) // (148 * 8), 2048, _TM_STAGE_TARGET))
-    row_chunk = _greedy_chunks(row_dbl, max(target, int(row_dbl.max()) if n_rows else 0))
+    row_chunk = _greedy_chunks(row_dbl, target)
     n_chunks = int(row_chunk[-1]) + 1 if n_rows else 0
     first_row = np.searchsorted(row_chunk, np.arange(n_chunks + 1)).astype(np.int64)
     chunk_a = np.stack([a_row_lo[first_row[:-1]], a_row_hi[first_row[1:] - 1]], 1) if n_chunks \
@@ -899,7 +899,7 @@ def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     if n_rows and int(row_dbl.max()) > _TM_STAGE_MAX:
         raise ShapeError(f"tmmult block row needs {int(row_dbl.max()) * 8} bytes of shared memory")
     target = int(np.clip(int(row_dbl.sum()) // (148 * 8), 2048, _TM_STAGE_TARGET))
-    row_chunk = _greedy_chunks(row_dbl, max(target, int(row_dbl.max()) if n_rows else 0))
+    row_chunk = _greedy_chunks(row_dbl, target)
     n_chunks = int(row_chunk[-1]) + 1 if n_rows else 0
     first_row = np.searchsorted(row_chunk, np.arange(n_chunks + 1)).astype(np.int64)
     chunk_a = np.stack([a_row_lo[first_row[:-1]], a_row_hi[first_row[1:] - 1]], 1) if n_chunks \

@@ -125,8 +125,7 @@ __device__ __forceinline__ void b_to_a(const double (&b)[N][N], double (&a)[N][N
     for (int x = 0; x < N; ++x) a[y][x] = buf[(t * N + y) * N + x];
 }
 
-// Padded per-pair tile stride (doubles): conflict-free-ish 64-bit transposes
-// for the plane-major thread mapping lane = t * P + pair.
+// Per-pair tile stride (doubles) for the A<->B transposes (bank model in DESIGN.md).
 template <int N> struct TileStride;
 template <> struct TileStride<2> { static constexpr int v = 9; };
 template <> struct TileStride<3> { static constexpr int v = 27; };
@@ -184,11 +183,12 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
 
   const int warp = threadIdx.x >> 5;
   const int lid = threadIdx.x & 31;
-  // plane-major mapping: lanes t*P .. t*P+P-1 hold plane t of the warp's P pairs,
-  // so the pairs of one visit (adjacent columns of the same rows) load adjacent words
-  const int t = lid / P;
-  const int sub = lid - t * P;
-  const bool lane_ok = t < N;
+  // pair-major mapping: lanes sub*N .. sub*N+N-1 hold the N planes of pair sub.
+  // With the unpadded N^3 pair tile this gives conflict-free 64-bit transpose
+  // stores and 2-way reads (bank model in DESIGN.md).
+  const int sub = lid / N;
+  const int t = lid - sub * N;
+  const bool lane_ok = sub < P;
   const int tt = lane_ok ? t : 0;
   const int64_t pair = a.pair_begin + ((int64_t)blockIdx.x * kWarps + warp) * P + sub;
   const bool ok = lane_ok && pair < a.pair_end;

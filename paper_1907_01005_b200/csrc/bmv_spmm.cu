@@ -731,6 +731,7 @@ int bmv_mmult_create(const bmv_mmult_desc* d, bmv_mmult** out) {
   if (!rc) rc = upload(d->pair_inner, d->n_pairs, &p->pair_inner);
   if (!rc) rc = upload(d->pair_b_off, d->n_pairs, &p->pair_b_off);
   if (!rc) rc = upload(d->pair_b_stride, d->n_pairs, &p->pair_b_stride);
+  if (!rc) rc = p->cls.build(d->chunk_a, nullptr, d->n_chunks, kMmWarps * kMmBMax * 8);
   if (!rc) {
     cudaError_t e = cudaFuncSetAttribute(mmult_chunk_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);

@@ -89,48 +89,53 @@ __device__ __forceinline__ void contract_slow(const double (&in)[N][N], double (
   }
 }
 
-// A (z = t, [y][x]) -> B (y = t, [z][x]) through the tile buf[z][y][x].
+// Per-pair transpose tile: element (z, y, x) at z*BZ + y*BY + x, pairs TILE
+// apart.  Strides chosen by a half-warp bank model (64-bit accesses, 16
+// bank pairs per 128 B wavefront) for the pair-major lane mapping: N = 3, 4
+// conflict-free stores and loads (2 + 2 wavefronts), N = 5 2 + 3.
+template <int N> struct Tile;
+template <> struct Tile<2> { static constexpr int BY = 2, BZ = 4, TILE = 9; };
+template <> struct Tile<3> { static constexpr int BY = 5, BZ = 21, TILE = 63; };
+template <> struct Tile<4> { static constexpr int BY = 4, BZ = 20, TILE = 77; };
+template <> struct Tile<5> { static constexpr int BY = 5, BZ = 27, TILE = 135; };
+
+// A (z = t, [y][x]) -> B (y = t, [z][x]) through the pair tile.
 template <int N>
 __device__ __forceinline__ void a_to_b(const double (&a)[N][N], double (&b)[N][N],
                                        double* buf, int t, bool store) {
+  using L = Tile<N>;
   __syncwarp();
   if (store) {
 #pragma unroll
     for (int y = 0; y < N; ++y)
 #pragma unroll
-      for (int x = 0; x < N; ++x) buf[(t * N + y) * N + x] = a[y][x];
+      for (int x = 0; x < N; ++x) buf[t * L::BZ + y * L::BY + x] = a[y][x];
   }
   __syncwarp();
 #pragma unroll
   for (int z = 0; z < N; ++z)
 #pragma unroll
-    for (int x = 0; x < N; ++x) b[z][x] = buf[(z * N + t) * N + x];
+    for (int x = 0; x < N; ++x) b[z][x] = buf[z * L::BZ + t * L::BY + x];
 }
 
 // B (y = t, [z][x]) -> A (z = t, [y][x]).
 template <int N>
 __device__ __forceinline__ void b_to_a(const double (&b)[N][N], double (&a)[N][N],
                                        double* buf, int t, bool store) {
+  using L = Tile<N>;
   __syncwarp();
   if (store) {
 #pragma unroll
     for (int z = 0; z < N; ++z)
 #pragma unroll
-      for (int x = 0; x < N; ++x) buf[(z * N + t) * N + x] = b[z][x];
+      for (int x = 0; x < N; ++x) buf[z * L::BZ + t * L::BY + x] = b[z][x];
   }
   __syncwarp();
 #pragma unroll
   for (int y = 0; y < N; ++y)
 #pragma unroll
-    for (int x = 0; x < N; ++x) a[y][x] = buf[(t * N + y) * N + x];
+    for (int x = 0; x < N; ++x) a[y][x] = buf[t * L::BZ + y * L::BY + x];
 }
-
-// Per-pair tile stride (doubles) for the A<->B transposes (bank model in DESIGN.md).
-template <int N> struct TileStride;
-template <> struct TileStride<2> { static constexpr int v = 9; };
-template <> struct TileStride<3> { static constexpr int v = 27; };
-template <> struct TileStride<4> { static constexpr int v = 65; };
-template <> struct TileStride<5> { static constexpr int v = 125; };
 
 constexpr int kMaxGroups = 32;  // distinct block rows per cell (<= 27 at L = 0)
 
@@ -140,7 +145,7 @@ constexpr int kMaxGroups = 32;  // distinct block rows per cell (<= 27 at L = 0)
 template <int N, bool COEF>
 struct CellSmem {
   static constexpr int P = 32 / N;
-  static constexpr int TILE = TileStride<N>::v;
+  static constexpr int TILE = Tile<N>::TILE;
   static constexpr int N2 = N * N;
   static constexpr int tile_bytes = ((P * TILE * 8 + 15) / 16) * 16;
   static constexpr int coef_bytes = COEF ? N2 * 32 * 8 : 0;
@@ -329,7 +334,7 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
 #pragma unroll
       for (int x = 0; x < N; ++x)
         // element (qz=z, qy=t, qx=x) was staged by the thread of plane z, k = t*N + x
-        v2[z][x] = COEF ? cbase[32 * (tt * N + x) + z * P + sub] * uqB[z][x] : 0.0;
+        v2[z][x] = COEF ? cbase[32 * (tt * N + x) + sub * N + z] * uqB[z][x] : 0.0;
   }
 
   // ---- back to the nodes: z, x in B, then y in A

@@ -211,9 +211,13 @@ __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8_1(const TmArgs
       const int as = g.tri_a_stride[t], bs = g.tri_b_stride[t], nr = g.tri_rows[t];
       for (int r = slice; r < nr; r += 4) {
         const double av = A[r * as + ii];
-        const double* br = B + r * bs;
+        const double2* br = reinterpret_cast<const double2*>(B + r * bs);  // 16 B aligned rows
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fma(av, br[j], acc[j]);
+        for (int j = 0; j < 4; ++j) {
+          const double2 bv = br[j];
+          acc[2 * j] = fma(av, bv.x, acc[2 * j]);
+          acc[2 * j + 1] = fma(av, bv.y, acc[2 * j + 1]);
+        }
       }
     }
 #pragma unroll
@@ -355,6 +359,7 @@ struct MmArgs {
   double alpha;
   int accumulate;
   const int32_t* __restrict__ chunk_ids;  // blockIdx -> chunk (size class launch)
+  int all_inner8;                         // every inner block has 8 columns (fast path)
 };
 
 constexpr int kMmWarps = 8;
@@ -366,11 +371,65 @@ constexpr int kMmWarps = 8;
 constexpr int kMmEPT = 8;
 constexpr int kMmBMax = 256;  // doubles per staged B block
 
+// 8-column fast path: lane = 8 * rsub + c; the 8 C values of column c of
+// each pair live in registers (prefetched one pair ahead), A rows come from
+// the shared stage.
+__device__ __forceinline__ void mm_block8(const MmArgs& g, int64_t o, const double* SA, int lane) {
+  const int rows = g.out_rows[o], cst = g.out_stride[o];
+  const int64_t p0 = g.pair_start[o], p1 = g.pair_start[o + 1];
+  const int c0 = lane & 7, r0 = lane >> 3;
+  for (int rb = 0; rb < rows; rb += 4 * kMmEPT) {
+    double acc[kMmEPT];
+#pragma unroll
+    for (int m = 0; m < kMmEPT; ++m) acc[m] = 0.0;
+    double cv[8], cn[8];
+    if (p0 < p1) {
+      const double* Bg = g.b + g.pair_b_off[p0] + c0;
+      const int bs = g.pair_b_stride[p0];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cv[k] = __ldg(Bg + (int64_t)k * bs);
+    }
+    for (int64_t p = p0; p < p1; ++p) {
+      if (p + 1 < p1) {
+        const double* Bn = g.b + g.pair_b_off[p + 1] + c0;
+        const int bsn = g.pair_b_stride[p + 1];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) cn[k] = __ldg(Bn + (int64_t)k * bsn);
+      }
+      const double* A = SA + g.pair_a_soff[p];
+      const int as = g.pair_a_stride[p];
+#pragma unroll
+      for (int m = 0; m < kMmEPT; ++m) {
+        const int r = rb + r0 + 4 * m;
+        if (r < rows) {
+          const double* ar = A + r * as;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[m] = fma(ar[k], cv[k], acc[m]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cv[k] = cn[k];
+    }
+#pragma unroll
+    for (int m = 0; m < kMmEPT; ++m) {
+      const int r = rb + r0 + 4 * m;
+      if (r < rows) {
+        double* dst = g.c + g.out_off[o] + (int64_t)r * cst + c0;
+        *dst = g.accumulate ? fma(g.alpha, acc[m], *dst) : g.alpha * acc[m];
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void mm_block(const MmArgs& g, int64_t o, const double* SA, double* SBw,
                                          int lane) {
   const int rows = g.out_rows[o], cols = g.out_cols[o], cst = g.out_stride[o];
   const int64_t p0 = g.pair_start[o], p1 = g.pair_start[o + 1];
   const int entries = rows * cols;
+  if (cols == 8 && g.all_inner8) {
+    mm_block8(g, o, SA, lane);
+    return;
+  }
   for (int e0 = 0; e0 < entries; e0 += 32 * kMmEPT) {
     int rr[kMmEPT], cc[kMmEPT];
     double acc[kMmEPT];
@@ -511,7 +570,7 @@ struct bmv_tmmult {
 
 struct bmv_mmult {
   int64_t n_out = 0, n_chunks = 0, n_pairs = 0;
-  int smem_bytes = 0, aligned = 0;
+  int smem_bytes = 0, aligned = 0, all_inner8 = 0;
   ChunkClasses cls;
   int64_t *chunk_a = nullptr, *chunk_out_start = nullptr, *out_off = nullptr,
           *pair_start = nullptr, *pair_b_off = nullptr;
@@ -574,16 +633,18 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
       mc = d->out_cols[o] > mc ? d->out_cols[o] : mc;
     }
     // the fast path reads 8 B-columns per row: needs B strides >= 8 (true for W = 8)
-    int min_bs = 1 << 30;
-    for (int64_t t = 0; t < d->n_triples; ++t)
+    int min_bs = 1 << 30, odd = 0;
+    for (int64_t t = 0; t < d->n_triples; ++t) {
       min_bs = d->tri_b_stride[t] < min_bs ? d->tri_b_stride[t] : min_bs;
-    p->small = (mr <= 8 && mc <= 8 && (d->n_triples == 0 || min_bs >= 8)) ? 1 : 0;
+      odd |= (d->tri_b_stride[t] | d->tri_a_stride[t] | d->tri_b_soff[t]) & 1;
+    }
+    p->small = (mr <= 8 && mc <= 8 && (d->n_triples == 0 || min_bs >= 8) && !odd) ? 1 : 0;
     // TMA bulk staging: every range start (and so every A/B split) 16-byte aligned
     int al = 1;
     for (int64_t c = 0; c < d->n_chunks; ++c)
       al &= ((d->chunk_a[2 * c] | d->chunk_a[2 * c + 1] | d->chunk_b[2 * c] | d->chunk_b[2 * c + 1]) & 1) == 0;
     p->aligned = al;
-    if (p->small && p->aligned && 2 * (int64_t)d->smem_doubles * 8 > max_smem) p->aligned = 0;
+    p->small = p->small && al;  // 16-byte aligned stage rows for the vector loads
   }
   int rc = upload(d->out_off, d->n_out, &p->out_off);
   if (!rc) rc = upload(d->out_rows, d->n_out, &p->out_rows);
@@ -732,6 +793,11 @@ int bmv_mmult_create(const bmv_mmult_desc* d, bmv_mmult** out) {
   if (!rc) rc = upload(d->pair_b_off, d->n_pairs, &p->pair_b_off);
   if (!rc) rc = upload(d->pair_b_stride, d->n_pairs, &p->pair_b_stride);
   if (!rc) rc = p->cls.build(d->chunk_a, nullptr, d->n_chunks, kMmWarps * kMmBMax * 8);
+  {
+    int ok8 = 1;
+    for (int64_t q = 0; q < d->n_pairs; ++q) ok8 &= d->pair_inner[q] == 8 && d->pair_b_stride[q] >= 8;
+    p->all_inner8 = ok8;
+  }
   if (!rc) {
     cudaError_t e = cudaFuncSetAttribute(mmult_chunk_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
@@ -762,7 +828,7 @@ int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, dou
   if (p->n_out == 0 || p->n_chunks == 0) return BMV_OK;
   MmArgs g{p->chunk_a, p->chunk_out_start, p->out_off, p->out_rows, p->out_cols, p->out_stride,
            p->pair_start, p->pair_a_soff, p->pair_a_stride, p->pair_inner, p->pair_b_off,
-           p->pair_b_stride, a, b, c, alpha, accumulate, nullptr};
+           p->pair_b_stride, a, b, c, alpha, accumulate, nullptr, p->all_inner8};
   for (int k = 0; k < 2; ++k) {
     if (p->cls.count[k] == 0) continue;
     g.chunk_ids = p->cls.ids[k];

@@ -222,27 +222,6 @@ def build_problem(cfg: ProblemConfig | str, n_ranks: int = 1) -> Problem:
     return Problem(cfg, mesh, partition, numbering, lay, supports, pattern, grown, pot, n_ranks)
 
 
-def _support_keys(prob: Problem) -> np.ndarray:
-    """Sorted keys center * n_dofs + row of every (centre, support row)."""
-    keys = prob.extra.get("support_keys")
-    if keys is None:
-        n = prob.numbering.n_dofs
-        keys = np.concatenate([c * n + np.asarray(s, dtype=np.int64)
-                               for c, s in enumerate(prob.supports)])
-        keys.sort()
-        prob.extra["support_keys"] = keys
-    return keys
-
-
-def in_support(prob: Problem, rows, new_cols) -> np.ndarray:
-    lay = prob.loc_layout
-    centre = lay.old_col_of_new[np.asarray(new_cols, dtype=np.int64)] // lay.vectors_per_center
-    key = centre * prob.numbering.n_dofs + np.asarray(rows, dtype=np.int64)
-    keys = _support_keys(prob)
-    pos = np.searchsorted(keys, key)
-    return (pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == key)
-
-
 def _support_entries(matrix: BlockCsrMatrix, prob: Problem):
     """(flat offsets, global rows, new cols) of the support entries in owned rows."""
     return prob.column_support.owned_entries(matrix)

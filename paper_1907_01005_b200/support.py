@@ -24,27 +24,57 @@ from .errors import ConsistencyError
 
 
 class ColumnSupport:
-    """For every column (storage order), the sorted global rows it may occupy."""
+    """For every column (storage order), the sorted global rows it may occupy.
 
-    def __init__(self, n_rows: int, col_ptr: np.ndarray, rows: np.ndarray):
+    Holds one sorted row array per column (shared with the per-centre
+    support arrays, no copy); rank-local views only touch the columns whose
+    row range intersects the rank's rows.
+    """
+
+    def __init__(self, n_rows: int, col_rows: list):
         self.n_rows = int(n_rows)
-        self.col_ptr = np.asarray(col_ptr, dtype=np.int64)
-        self.rows = np.asarray(rows, dtype=np.int64)
-        self.n_cols = self.col_ptr.size - 1
+        self.col_rows = [np.asarray(r, dtype=np.int64) for r in col_rows]
+        self.n_cols = len(self.col_rows)
+        self._lo = np.asarray([r[0] if r.size else np.iinfo(np.int64).max for r in self.col_rows])
+        self._hi = np.asarray([r[-1] if r.size else -1 for r in self.col_rows])
 
     @classmethod
     def from_localization(cls, loc_layout, supports, n_rows: int) -> "ColumnSupport":
         """From per-centre supports (column_supports) and the column order."""
         centre = loc_layout.centers_of_new_cols()
-        parts = [np.asarray(supports[int(c)], dtype=np.int64) for c in centre]
-        counts = np.asarray([p.size for p in parts], dtype=np.int64)
-        ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-        rows = np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
-        return cls(n_rows, ptr, rows)
+        return cls(n_rows, [supports[int(c)] for c in centre])
 
     @property
     def nnz(self) -> int:
-        return int(self.rows.size)
+        return int(sum(r.size for r in self.col_rows))
+
+    def columns_touching(self, lo: int, hi: int) -> np.ndarray:
+        """Columns with at least one support row in [lo, hi)."""
+        return np.flatnonzero((self._lo < hi) & (self._hi >= lo))
+
+    def entries_in(self, lo: int, hi: int, extra_rows: np.ndarray | None = None):
+        """(rows, cols) of support entries with rows in [lo, hi) or in extra_rows (sorted)."""
+        rows, cols = [], []
+        cand = set(self.columns_touching(lo, hi).tolist())
+        if extra_rows is not None and extra_rows.size:
+            cand |= set(np.flatnonzero((self._lo <= extra_rows[-1])
+                                       & (self._hi >= extra_rows[0])).tolist())
+        for c in sorted(cand):
+            r = self.col_rows[c]
+            a, b = np.searchsorted(r, [lo, hi])
+            keep = [r[a:b]]
+            if extra_rows is not None and extra_rows.size:
+                pos = np.searchsorted(extra_rows, r)
+                hit = (pos < extra_rows.size) & (extra_rows[np.minimum(pos, extra_rows.size - 1)] == r)
+                hit[a:b] = False
+                keep.append(r[hit])
+            rr = np.concatenate(keep)
+            rows.append(rr)
+            cols.append(np.full(rr.size, c, dtype=np.int64))
+        if not rows:
+            z = np.zeros(0, dtype=np.int64)
+            return z, z
+        return np.concatenate(rows), np.concatenate(cols)
 
     def local_mask(self, layout) -> sparse.csr_matrix:
         """Boolean (local rows x columns) CSR; local rows = owned then ghosts."""
@@ -55,22 +85,15 @@ class ColumnSupport:
             return hit
         lo, hi = layout.owned_rows
         n_own = hi - lo
-        col = np.repeat(np.arange(self.n_cols, dtype=np.int64), np.diff(self.col_ptr))
-        r = self.rows
-        own = (r >= lo) & (r < hi)
-        loc = np.full(r.size, -1, dtype=np.int64)
-        loc[own] = r[own] - lo
         flat = layout.ghost_rows_flat
-        if flat.size:
-            rest = ~own
-            pos = np.searchsorted(flat, r[rest])
-            hit_g = (pos < flat.size) & (flat[np.minimum(pos, flat.size - 1)] == r[rest])
-            tmp = np.full(pos.size, -1, dtype=np.int64)
-            tmp[hit_g] = n_own + pos[hit_g]
-            loc[rest] = tmp
-        keep = loc >= 0
+        r, col = self.entries_in(lo, hi, flat)
+        own = (r >= lo) & (r < hi)
+        loc = np.empty(r.size, dtype=np.int64)
+        loc[own] = r[own] - lo
+        if flat.size and (~own).any():
+            loc[~own] = n_own + np.searchsorted(flat, r[~own])
         n_local = n_own + flat.size
-        m = sparse.csr_matrix((np.ones(int(keep.sum()), dtype=np.int8), (loc[keep], col[keep])),
+        m = sparse.csr_matrix((np.ones(r.size, dtype=np.int8), (loc, col)),
                               shape=(n_local, self.n_cols))
         m.sum_duplicates()
         m.sort_indices()
@@ -91,10 +114,7 @@ class ColumnSupport:
             return hit
         layout = matrix.layout
         lo, hi = layout.owned_rows
-        cols = np.repeat(np.arange(self.n_cols, dtype=np.int64), np.diff(self.col_ptr))
-        rows = self.rows
-        keep = (rows >= lo) & (rows < hi)
-        rows, cols = rows[keep], cols[keep]
+        rows, cols = self.entries_in(lo, hi)
         if rows.size == 0:
             hit = (rows, rows, cols)
             cache[key] = hit
@@ -128,7 +148,6 @@ class ColumnSupport:
 
     def check_matrix(self, matrix) -> None:
         """Raise ConsistencyError if an owned entry outside the support is nonzero."""
-        dense_rows = matrix.layout.owned_rows
         flat, grow, gcol = matrix._valid_owned_index()
         if flat.size == 0:
             return
@@ -137,16 +156,17 @@ class ColumnSupport:
         if not nz.any():
             return
         grow, gcol = grow[nz], gcol[nz]
+        lo, hi = matrix.layout.owned_rows
+        r, c = self.entries_in(lo, hi)
+        skey = np.sort(c * self.n_rows + r)
         key = gcol * self.n_rows + grow
-        col = np.repeat(np.arange(self.n_cols, dtype=np.int64), np.diff(self.col_ptr))
-        skey = np.sort(col * self.n_rows + self.rows)
         pos = np.searchsorted(skey, key)
         inside = (pos < skey.size) & (skey[np.minimum(pos, max(skey.size - 1, 0))] == key)
         if not inside.all():
             i = int(np.flatnonzero(~inside)[0])
             raise ConsistencyError(
                 f"entry ({int(grow[i])}, {int(gcol[i])}) is nonzero but outside the declared "
-                f"column support (owned rows {dense_rows})")
+                f"column support (owned rows {(lo, hi)})")
 
 
 def attach_support(matrix, support: ColumnSupport, check: bool = True):

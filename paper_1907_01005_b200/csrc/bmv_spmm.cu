@@ -86,6 +86,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// FP64 tensor-core MMA (DMMA): D(8x8) = A(8x4, row) * B(4x8, col) + C.
+// Fragments (lane = 4 * gid + tig): A[gid][tig], B[tig][gid], C/D[gid][2 tig + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 // Stage n doubles from global src to shared dst: one elected thread issues
 // TMA bulk copies (16-byte granules, 32 KB pieces) when both ends are
 // 16-byte aligned and n is even; otherwise all threads copy.  Returns after
@@ -195,41 +203,35 @@ __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8_1(const TmArgs
   double* SB = stage + na;
   stage_ranges(SA, g.a + a_lo, na, SB, g.b + b_lo, nb, &bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slice = lane >> 3, i = lane & 7;
+  const int gid = lane >> 2, tig = lane & 3;
   const int64_t s_end = g.chunk_seg_start[ch + 1];
   for (int64_t sg = g.chunk_seg_start[ch] + warp; sg < s_end; sg += kTmWarps) {
     const int64_t o = g.seg_out[sg];
     const int rows = g.out_rows[o], cols = g.out_cols[o];
-    const int ii = i < rows ? i : 0;
-    double acc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    // S(k, l) += sum_r A[r][k] B[r][l]: M = k (8), N = l (8), K = r in steps of 4
+    double d0 = 0.0, d1 = 0.0;
     const int64_t t1 = g.seg_tri_start[sg + 1];
     for (int64_t t = g.seg_tri_start[sg]; t < t1; ++t) {
-      const double* A = SA + g.tri_a_soff[t];
-      const double* B = SB + g.tri_b_soff[t];
+      const double* A = SA + g.tri_a_soff[t] + gid;
+      const double* B = SB + g.tri_b_soff[t] + gid;
       const int as = g.tri_a_stride[t], bs = g.tri_b_stride[t], nr = g.tri_rows[t];
-      for (int r = slice; r < nr; r += 4) {
-        const double av = A[r * as + ii];
-        const double2* br = reinterpret_cast<const double2*>(B + r * bs);  // 16 B aligned rows
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double2 bv = br[j];
-          acc[2 * j] = fma(av, bv.x, acc[2 * j]);
-          acc[2 * j + 1] = fma(av, bv.y, acc[2 * j + 1]);
-        }
+      // warp-uniform loop bounds (mma.sync needs every lane)
+      int r0 = 0;
+      for (; r0 + 8 <= nr; r0 += 8) {  // two k-steps per iteration
+        const int r = r0 + tig;
+        dmma_8x8x4(d0, d1, A[r * as], B[r * bs]);
+        dmma_8x8x4(d0, d1, A[(r + 4) * as], B[(r + 4) * bs]);
+      }
+      for (; r0 < nr; r0 += 4) {
+        const int rr = r0 + tig;
+        const bool in = rr < nr;
+        dmma_8x8x4(d0, d1, in ? A[rr * as] : 0.0, in ? B[rr * bs] : 0.0);
       }
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 8);
-      acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
-    }
-    if (slice == 0 && i < rows) {
-      double* P = g.partial + g.seg_poff[sg] + i * cols;
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < cols) P[j] = acc[j];
+    if (gid < rows) {
+      double* P = g.partial + g.seg_poff[sg] + gid * cols;
+      if (2 * tig < cols) P[2 * tig] = d0;
+      if (2 * tig + 1 < cols) P[2 * tig + 1] = d1;
     }
   }
 }
@@ -371,51 +373,48 @@ constexpr int kMmWarps = 8;
 constexpr int kMmEPT = 8;
 constexpr int kMmBMax = 256;  // doubles per staged B block
 
-// 8-column fast path: lane = 8 * rsub + c; the 8 C values of column c of
-// each pair live in registers (prefetched one pair ahead), A rows come from
-// the shared stage.
+// 8 x 8 inner/outer fast path on FP64 tensor cores: the output block (rows x 8)
+// is cut into 8-row tiles (<= 16 tiles held in registers); per (A_ik, C_kj)
+// pair the C block is two B fragments (k = 0..3, 4..7) loaded once, each
+// tile takes two DMMA k-steps with A rows from the shared stage.
+constexpr int kMmTiles = 16;
+
 __device__ __forceinline__ void mm_block8(const MmArgs& g, int64_t o, const double* SA, int lane) {
   const int rows = g.out_rows[o], cst = g.out_stride[o];
   const int64_t p0 = g.pair_start[o], p1 = g.pair_start[o + 1];
-  const int c0 = lane & 7, r0 = lane >> 3;
-  for (int rb = 0; rb < rows; rb += 4 * kMmEPT) {
-    double acc[kMmEPT];
+  const int gid = lane >> 2, tig = lane & 3;
+  const int ntiles = (rows + 7) >> 3;
+  double acc0[kMmTiles], acc1[kMmTiles];
 #pragma unroll
-    for (int m = 0; m < kMmEPT; ++m) acc[m] = 0.0;
-    double cv[8], cn[8];
-    if (p0 < p1) {
-      const double* Bg = g.b + g.pair_b_off[p0] + c0;
-      const int bs = g.pair_b_stride[p0];
+  for (int q = 0; q < kMmTiles; ++q) acc0[q] = acc1[q] = 0.0;
+  for (int64_t p = p0; p < p1; ++p) {
+    const double* Bg = g.b + g.pair_b_off[p] + gid;
+    const int bs = g.pair_b_stride[p];
+    const double b0 = __ldg(Bg + (int64_t)tig * bs), b1 = __ldg(Bg + (int64_t)(4 + tig) * bs);
+    const double* A = SA + g.pair_a_soff[p] + tig;
+    const int as = g.pair_a_stride[p];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) cv[k] = __ldg(Bg + (int64_t)k * bs);
-    }
-    for (int64_t p = p0; p < p1; ++p) {
-      if (p + 1 < p1) {
-        const double* Bn = g.b + g.pair_b_off[p + 1] + c0;
-        const int bsn = g.pair_b_stride[p + 1];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) cn[k] = __ldg(Bn + (int64_t)k * bsn);
+    for (int q = 0; q < kMmTiles; ++q) {
+      if (q < ntiles) {
+        const int r = 8 * q + gid;
+        const bool in = r < rows;
+        const double a0 = in ? A[r * as] : 0.0, a1 = in ? A[r * as + 4] : 0.0;
+        dmma_8x8x4(acc0[q], acc1[q], a0, b0);
+        dmma_8x8x4(acc0[q], acc1[q], a1, b1);
       }
-      const double* A = SA + g.pair_a_soff[p];
-      const int as = g.pair_a_stride[p];
-#pragma unroll
-      for (int m = 0; m < kMmEPT; ++m) {
-        const int r = rb + r0 + 4 * m;
-        if (r < rows) {
-          const double* ar = A + r * as;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc[m] = fma(ar[k], cv[k], acc[m]);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) cv[k] = cn[k];
     }
+  }
 #pragma unroll
-    for (int m = 0; m < kMmEPT; ++m) {
-      const int r = rb + r0 + 4 * m;
-      if (r < rows) {
-        double* dst = g.c + g.out_off[o] + (int64_t)r * cst + c0;
-        *dst = g.accumulate ? fma(g.alpha, acc[m], *dst) : g.alpha * acc[m];
+  for (int q = 0; q < kMmTiles; ++q) {
+    const int r = 8 * q + gid;
+    if (q < ntiles && r < rows) {
+      double* dst = g.c + g.out_off[o] + (int64_t)r * cst + 2 * tig;
+      if (g.accumulate) {
+        dst[0] = fma(g.alpha, acc0[q], dst[0]);
+        dst[1] = fma(g.alpha, acc1[q], dst[1]);
+      } else {
+        dst[0] = g.alpha * acc0[q];
+        dst[1] = g.alpha * acc1[q];
       }
     }
   }
@@ -426,7 +425,7 @@ __device__ __forceinline__ void mm_block(const MmArgs& g, int64_t o, const doubl
   const int rows = g.out_rows[o], cols = g.out_cols[o], cst = g.out_stride[o];
   const int64_t p0 = g.pair_start[o], p1 = g.pair_start[o + 1];
   const int entries = rows * cols;
-  if (cols == 8 && g.all_inner8) {
+  if (cols == 8 && g.all_inner8 && rows <= 8 * kMmTiles) {
     mm_block8(g, o, SA, lane);
     return;
   }

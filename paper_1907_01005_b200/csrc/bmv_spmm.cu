@@ -192,16 +192,8 @@ __device__ __forceinline__ void issue_chunk(const double* a, const int64_t* ca, 
 // lane = slice * 8 + i: the 4 slices split the block rows (r = slice,
 // slice + 4, ...), lane (slice, i) accumulates output row i in registers;
 // slices are summed with two xor-shuffles.
-__global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8_1(const TmArgs g) {
-  extern __shared__ __align__(16) double stage[];
-  __shared__ uint64_t bar;
-  const int64_t ch = g.chunk_ids ? g.chunk_ids[blockIdx.x] : blockIdx.x;
-  const int64_t a_lo = g.chunk_a[2 * ch], b_lo = g.chunk_b[2 * ch];
-  const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
-  const int nb = (int)(g.chunk_b[2 * ch + 1] - b_lo);
-  double* SA = stage;
-  double* SB = stage + na;
-  stage_ranges(SA, g.a + a_lo, na, SB, g.b + b_lo, nb, &bar);
+__device__ __forceinline__ void tm_chunk_compute8(const TmArgs& g, int64_t ch, const double* SA,
+                                                  const double* SB) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int64_t s_end = g.chunk_seg_start[ch + 1];
@@ -232,6 +224,61 @@ __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8_1(const TmArgs
       double* P = g.partial + g.seg_poff[sg] + gid * cols;
       if (2 * tig < cols) P[2 * tig] = d0;
       if (2 * tig + 1 < cols) P[2 * tig + 1] = d1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8_1(const TmArgs g) {
+  extern __shared__ __align__(16) double stage[];
+  __shared__ uint64_t bar;
+  const int64_t ch = g.chunk_ids ? g.chunk_ids[blockIdx.x] : blockIdx.x;
+  const int64_t a_lo = g.chunk_a[2 * ch], b_lo = g.chunk_b[2 * ch];
+  const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
+  const int nb = (int)(g.chunk_b[2 * ch + 1] - b_lo);
+  double* SA = stage;
+  double* SB = stage + na;
+  stage_ranges(SA, g.a + a_lo, na, SB, g.b + b_lo, nb, &bar);
+  tm_chunk_compute8(g, ch, SA, SB);
+}
+
+// Persistent variant: each CTA walks its chunks (ids[blockIdx.x + k gridDim.x])
+// through a kStages-deep ring of TMA-filled stages, so the next chunks stream
+// in while the current one is computed.
+constexpr int kStages = 3;
+#ifndef BMV_PERSISTENT
+#define BMV_PERSISTENT 1
+#endif
+constexpr bool kPersistent = BMV_PERSISTENT != 0;
+
+__global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8_p(const TmArgs g, int64_t n_list,
+                                                                     int stage_doubles) {
+  extern __shared__ __align__(16) double stage[];
+  __shared__ uint64_t bars[kStages];
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kStages; ++q) mbar_init(&bars[q], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kStages; ++q) {
+      const int64_t idx = blockIdx.x + (int64_t)q * gridDim.x;
+      if (idx < n_list)
+        issue_chunk(g.a, g.chunk_a, g.b, g.chunk_b, g.chunk_ids[idx], stage + q * stage_doubles,
+                    &bars[q]);
+    }
+  }
+  for (int it = 0;; ++it) {
+    const int64_t idx = blockIdx.x + (int64_t)it * gridDim.x;
+    if (idx >= n_list) break;
+    const int q = it % kStages;
+    mbar_wait(&bars[q], (it / kStages) & 1);
+    const int64_t ch = g.chunk_ids[idx];
+    const double* SA = stage + q * stage_doubles;
+    tm_chunk_compute8(g, ch, SA, SA + (g.chunk_a[2 * ch + 1] - g.chunk_a[2 * ch]));
+    __syncthreads();  // stage q fully consumed
+    if (threadIdx.x == 0) {
+      const int64_t nidx = idx + (int64_t)kStages * gridDim.x;
+      if (nidx < n_list)
+        issue_chunk(g.a, g.chunk_a, g.b, g.chunk_b, g.chunk_ids[nidx], stage + q * stage_doubles,
+                    &bars[q]);
     }
   }
 }
@@ -387,10 +434,21 @@ __device__ __forceinline__ void mm_block8(const MmArgs& g, int64_t o, const doub
   double acc0[kMmTiles], acc1[kMmTiles];
 #pragma unroll
   for (int q = 0; q < kMmTiles; ++q) acc0[q] = acc1[q] = 0.0;
+  double nb0 = 0.0, nb1 = 0.0;
+  if (p0 < p1) {
+    const double* Bg = g.b + g.pair_b_off[p0] + gid;
+    const int bs = g.pair_b_stride[p0];
+    nb0 = __ldg(Bg + (int64_t)tig * bs);
+    nb1 = __ldg(Bg + (int64_t)(4 + tig) * bs);
+  }
   for (int64_t p = p0; p < p1; ++p) {
-    const double* Bg = g.b + g.pair_b_off[p] + gid;
-    const int bs = g.pair_b_stride[p];
-    const double b0 = __ldg(Bg + (int64_t)tig * bs), b1 = __ldg(Bg + (int64_t)(4 + tig) * bs);
+    const double b0 = nb0, b1 = nb1;
+    if (p + 1 < p1) {  // prefetch the next pair's C fragments
+      const double* Bn = g.b + g.pair_b_off[p + 1] + gid;
+      const int bsn = g.pair_b_stride[p + 1];
+      nb0 = __ldg(Bn + (int64_t)tig * bsn);
+      nb1 = __ldg(Bn + (int64_t)(4 + tig) * bsn);
+    }
     const double* A = SA + g.pair_a_soff[p] + tig;
     const int as = g.pair_a_stride[p];
 #pragma unroll
@@ -491,31 +549,41 @@ __global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs
   for (int64_t o = g.chunk_out_start[ch] + warp; o < o_end; o += kMmWarps) mm_block(g, o, SA, SBw, lane);
 }
 
-// Persistent over chunks with a double-buffered TMA stage of A.
-__global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel_p(const MmArgs g, int64_t n_chunks,
-                                                                       int buf_doubles) {
+// Persistent over its chunk list with a kStages-deep ring of TMA-filled A stages.
+__global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel_p(const MmArgs g, int64_t n_list,
+                                                                       int stage_doubles) {
   extern __shared__ __align__(16) double stage[];
-  __shared__ uint64_t bars[2];
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-  }
+  __shared__ uint64_t bars[kStages];
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kStages; ++q) mbar_init(&bars[q], 1);
   __syncthreads();
   double* abuf = stage + kMmWarps * kMmBMax;
-  int64_t ch = blockIdx.x;
-  if (threadIdx.x == 0 && ch < n_chunks) issue_chunk(g.a, g.chunk_a, nullptr, nullptr, ch, abuf, &bars[0]);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kStages; ++q) {
+      const int64_t idx = blockIdx.x + (int64_t)q * gridDim.x;
+      if (idx < n_list)
+        issue_chunk(g.a, g.chunk_a, nullptr, nullptr, g.chunk_ids[idx], abuf + q * stage_doubles,
+                    &bars[q]);
+    }
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* SBw = stage + warp * kMmBMax;
-  for (int it = 0; ch < n_chunks; ch += gridDim.x, ++it) {
-    const int bsel = it & 1;
-    const int64_t nx = ch + gridDim.x;
-    if (threadIdx.x == 0 && nx < n_chunks)
-      issue_chunk(g.a, g.chunk_a, nullptr, nullptr, nx, abuf + (bsel ^ 1) * buf_doubles, &bars[bsel ^ 1]);
-    mbar_wait(&bars[bsel], (it >> 1) & 1);
-    const double* SA = abuf + bsel * buf_doubles;
+  for (int it = 0;; ++it) {
+    const int64_t idx = blockIdx.x + (int64_t)it * gridDim.x;
+    if (idx >= n_list) break;
+    const int q = it % kStages;
+    mbar_wait(&bars[q], (it / kStages) & 1);
+    const int64_t ch = g.chunk_ids[idx];
+    const double* SA = abuf + q * stage_doubles;
     const int64_t o_end = g.chunk_out_start[ch + 1];
     for (int64_t o = g.chunk_out_start[ch] + warp; o < o_end; o += kMmWarps) mm_block(g, o, SA, SBw, lane);
     __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t nidx = idx + (int64_t)kStages * gridDim.x;
+      if (nidx < n_list)
+        issue_chunk(g.a, g.chunk_a, nullptr, nullptr, g.chunk_ids[nidx], abuf + q * stage_doubles,
+                    &bars[q]);
+    }
   }
 }
 
@@ -684,6 +752,7 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
     cudaError_t e = cudaFuncSetAttribute(tm_chunk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel8, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel8_1, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel8_p, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tm_chunk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     if (e != cudaSuccess) {
@@ -719,7 +788,11 @@ int bmv_tmmult_run(bmv_tmmult* p, const double* a, const double* b, double* c, i
     g.chunk_ids = p->cls.ids[k];
     const unsigned grid = (unsigned)p->cls.count[k];
     const int smem = p->cls.smem[k];
-    if (p->small)
+    if (p->small && k == 0 && p->aligned && kPersistent) {
+      const int per_sm = std::max(1, (227 * 1024) / (kStages * smem + 1024));
+      const unsigned pgrid = (unsigned)std::min<int64_t>(p->cls.count[0], (int64_t)sm_count() * per_sm);
+      tm_chunk_kernel8_p<<<pgrid, kTmWarps * 32, kStages * smem, st>>>(g, p->cls.count[0], smem / 8);
+    } else if (p->small)
       tm_chunk_kernel8_1<<<grid, kTmWarps * 32, smem, st>>>(g);
     else if (p->ept == 2)
       tm_chunk_kernel<2><<<grid, kTmWarps * 32, smem, st>>>(g);
@@ -831,7 +904,15 @@ int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, dou
   for (int k = 0; k < 2; ++k) {
     if (p->cls.count[k] == 0) continue;
     g.chunk_ids = p->cls.ids[k];
-    mmult_chunk_kernel<<<(unsigned)p->cls.count[k], kMmWarps * 32, p->cls.smem[k], st>>>(g);
+    if (k == 0 && p->aligned && kPersistent) {
+      const int a_bytes = p->cls.smem[0] - kMmWarps * kMmBMax * 8;  // staged A bytes (max)
+      const int smem = kMmWarps * kMmBMax * 8 + kStages * a_bytes;
+      const int per_sm = std::max(1, (227 * 1024) / (smem + 1024));
+      const unsigned pgrid = (unsigned)std::min<int64_t>(p->cls.count[0], (int64_t)sm_count() * per_sm);
+      mmult_chunk_kernel_p<<<pgrid, kMmWarps * 32, smem, st>>>(g, p->cls.count[0], a_bytes / 8);
+    } else {
+      mmult_chunk_kernel<<<(unsigned)p->cls.count[k], kMmWarps * 32, p->cls.smem[k], st>>>(g);
+    }
     BMV_CHECK_LAUNCH();
   }
   BMV_CHECK_LAUNCH();

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kTmWarps * 32) tm_chunk_kernel8_1(const TmArgs
 // in while the current one is computed.
 constexpr int kStages = 3;
 #ifndef BMV_PERSISTENT
-#define BMV_PERSISTENT 1
+#define BMV_PERSISTENT 0
 #endif
 constexpr bool kPersistent = BMV_PERSISTENT != 0;
 
@@ -873,6 +873,13 @@ int bmv_mmult_create(const bmv_mmult_desc* d, bmv_mmult** out) {
   if (!rc) {
     cudaError_t e = cudaFuncSetAttribute(mmult_chunk_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mmult_chunk_kernel_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               max_smem - 1024);
+    int al = 1;
+    for (int64_t c = 0; c < d->n_chunks; ++c)
+      al &= ((d->chunk_a[2 * c] | d->chunk_a[2 * c + 1]) & 1) == 0;
+    p->aligned = al;
     if (e != cudaSuccess) {
       set_error("cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
       rc = BMV_ERR_CUDA;

@@ -40,8 +40,8 @@ struct CellTables {
 struct CellArgs {
   // per pair: {cell, first group index, lane | stride << 16, number of groups}
   const int4* __restrict__ pair_desc;
-  const int64_t* __restrict__ group_xoff;
-  const int64_t* __restrict__ group_hoff;
+  const int32_t* __restrict__ group_xoff;  // element offsets (< 2^31) of the groups' blocks
+  const int32_t* __restrict__ group_hoff;
   const uint32_t* __restrict__ cell_slots;
   const double* __restrict__ coef;
   int64_t coef_stride;
@@ -97,7 +97,11 @@ template <int N> struct Tile;
 template <> struct Tile<2> { static constexpr int BY = 2, BZ = 4, TILE = 9; };
 template <> struct Tile<3> { static constexpr int BY = 5, BZ = 21, TILE = 63; };
 template <> struct Tile<4> { static constexpr int BY = 4, BZ = 20, TILE = 77; };
-template <> struct Tile<5> { static constexpr int BY = 5, BZ = 27, TILE = 135; };
+#if defined(BMV_K1_TILE5_WIDE)
+template <> struct Tile<5> { static constexpr int BY = 7, BZ = 39, TILE = 195; };  // 2 + 2 wavefronts
+#else
+template <> struct Tile<5> { static constexpr int BY = 5, BZ = 27, TILE = 135; };  // 2 + 3 wavefronts
+#endif
 
 // A (z = t, [y][x]) -> B (y = t, [z][x]) through the pair tile.
 template <int N>
@@ -150,8 +154,8 @@ struct CellSmem {
   static constexpr int tile_bytes = ((P * TILE * 8 + 15) / 16) * 16;
   static constexpr int coef_bytes = COEF ? N2 * 32 * 8 : 0;
   static constexpr int slot_bytes = N2 * 32 * 4;
-  static __host__ __device__ int gtab_stride(int G) { return 2 * G + 1; }
-  static __host__ __device__ int gtab_bytes(int G) { return ((P * (2 * G + 1) * 8 + 15) / 16) * 16; }
+  static __host__ __device__ int gtab_stride(int G) { return 2 * G + 1; }  // int32, odd
+  static __host__ __device__ int gtab_bytes(int G) { return ((P * (2 * G + 1) * 4 + 15) / 16) * 16; }
   static __host__ __device__ int warp_bytes(int G) {
     return tile_bytes + coef_bytes + slot_bytes + gtab_bytes(G);
   }
@@ -160,6 +164,10 @@ struct CellSmem {
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() {
@@ -203,7 +211,7 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
   double* cbase = reinterpret_cast<double*>(wbase + SM::tile_bytes);  // [k][lane]
   double* cbuf = cbase + lid;
   uint32_t* slots = reinterpret_cast<uint32_t*>(wbase + SM::tile_bytes + SM::coef_bytes) + lid;
-  int64_t* gtab = reinterpret_cast<int64_t*>(wbase + SM::tile_bytes + SM::coef_bytes +
+  int32_t* gtab = reinterpret_cast<int32_t*>(wbase + SM::tile_bytes + SM::coef_bytes +
                                              SM::slot_bytes) + sub * SM::gtab_stride(G);
 
   // ---- trip 1: pair descriptor
@@ -225,8 +233,8 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
   }
   if (ok) {
     for (int g = t; g < ng; g += N) {
-      cp_async8(gtab + g, a.group_xoff + gbase + g);
-      cp_async8(gtab + G + g, a.group_hoff + gbase + g);
+      cp_async4(gtab + g, a.group_xoff + gbase + g);
+      cp_async4(gtab + G + g, a.group_hoff + gbase + g);
     }
   }
   cp_async_commit();  // group 1: group table
@@ -252,7 +260,7 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
       double v = 0.0;
       if (ok) {
         const uint32_t s = sl[y * N + x];
-        const int64_t xo = gtab[s >> 24];
+        const int xo = gtab[s >> 24];
         if (xo >= 0) v = __ldg(a.x + xo + (int64_t)(s & 0xffffffu) * stride + lane);
       }
       u[y][x] = v;
@@ -345,7 +353,7 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
 
   // ---- scatter-add
   if (ok) {
-    const int64_t* gh = gtab + G;
+    const int32_t* gh = gtab + G;
 #pragma unroll
     for (int y = 0; y < N; ++y) {
 #pragma unroll
@@ -404,7 +412,7 @@ struct bmv_cellop {
   std::vector<int64_t> color_start;  // empty => atomic single launch
   int max_groups = 4;
   int4* pair_desc = nullptr;
-  int64_t *group_xoff = nullptr, *group_hoff = nullptr;
+  int32_t *group_xoff = nullptr, *group_hoff = nullptr;
   uint32_t* cell_slots = nullptr;
   CellTables tables{};
 };
@@ -528,8 +536,21 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
     p->max_groups = std::min(kMaxGroups, (maxg + 3) / 4 * 4);
     if (rc == BMV_OK) rc = upload(desc.data(), d->n_pairs, &p->pair_desc);
   }
-  if (rc == BMV_OK) rc = upload(d->group_xoff, d->n_groups_total, &p->group_xoff);
-  if (rc == BMV_OK) rc = upload(d->group_hoff, d->n_groups_total, &p->group_hoff);
+  if (rc == BMV_OK && d->n_groups_total > 0) {
+    std::vector<int32_t> gx((size_t)d->n_groups_total), gh((size_t)d->n_groups_total);
+    for (int64_t i = 0; i < d->n_groups_total; ++i) {
+      if (d->group_xoff[i] > INT32_MAX || d->group_hoff[i] > INT32_MAX || d->group_hoff[i] < 0) {
+        set_error("block offset %lld exceeds the 2^31-element limit of this build",
+                  (long long)std::max(d->group_xoff[i], d->group_hoff[i]));
+        rc = BMV_ERR_INVALID;
+        break;
+      }
+      gx[(size_t)i] = (int32_t)d->group_xoff[i];
+      gh[(size_t)i] = (int32_t)d->group_hoff[i];
+    }
+    if (rc == BMV_OK) rc = upload(gx.data(), d->n_groups_total, &p->group_xoff);
+    if (rc == BMV_OK) rc = upload(gh.data(), d->n_groups_total, &p->group_hoff);
+  }
   if (rc == BMV_OK) rc = upload(d->cell_slots, (int64_t)d->n_cells * n3, &p->cell_slots);
   if (rc != BMV_OK) {
     bmv_cellop_destroy(p);

@@ -52,7 +52,6 @@ struct CellArgs {
 };
 
 constexpr int kWarps = 4;  // warps per CTA
-constexpr int kTasks = 4;  // pair batches per warp (descriptor prefetch)
 #ifndef BMV_K1_MINB5
 #define BMV_K1_MINB5 3
 #endif
@@ -204,14 +203,8 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
   const int t = lid - sub * N;
   const bool lane_ok = sub < P;
   const int tt = lane_ok ? t : 0;
-  // each warp runs kTasks consecutive batches of P pairs; the next batch's
-  // descriptor is loaded while the current batch is processed
-  const int64_t batch0 = ((int64_t)blockIdx.x * kWarps + warp) * kTasks;
-  int4 dnext = make_int4(0, 0, 0, 0);
-  {
-    const int64_t pr = a.pair_begin + batch0 * P + sub;
-    if (lane_ok && pr < a.pair_end) dnext = __ldg(a.pair_desc + pr);
-  }
+  const int64_t pair = a.pair_begin + ((int64_t)blockIdx.x * kWarps + warp) * P + sub;
+  const bool ok = lane_ok && pair < a.pair_end;
 
   unsigned char* wbase = smem_raw + warp * SM::warp_bytes(G);
   double* buf = reinterpret_cast<double*>(wbase) + sub * TILE;
@@ -221,24 +214,16 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
   int32_t* gtab = reinterpret_cast<int32_t*>(wbase + SM::tile_bytes + SM::coef_bytes +
                                              SM::slot_bytes) + sub * SM::gtab_stride(G);
 
-  for (int task = 0; task < kTasks; ++task) {
-  const int64_t pair = a.pair_begin + (batch0 + task) * P + sub;
-  if (a.pair_begin + (batch0 + task) * P >= a.pair_end) break;  // warp-uniform
-  const bool ok = lane_ok && pair < a.pair_end;
-  // ---- trip 1: pair descriptor (prefetched)
+  // ---- trip 1: pair descriptor
   int cell = 0, lane = 0, stride = 0, ng = 0, gbase = 0;
   if (ok) {
-    cell = dnext.x;
-    gbase = dnext.y;
-    lane = dnext.z & 0xffff;
-    stride = dnext.z >> 16;
-    ng = dnext.w;
+    const int4 d = __ldg(a.pair_desc + pair);
+    cell = d.x;
+    gbase = d.y;
+    lane = d.z & 0xffff;
+    stride = d.z >> 16;
+    ng = d.w;
   }
-  if (task + 1 < kTasks) {
-    const int64_t pr = pair + P;
-    dnext = (lane_ok && pr < a.pair_end) ? __ldg(a.pair_desc + pr) : make_int4(0, 0, 0, 0);
-  }
-  __syncwarp();  // previous batch's scatter has finished reading the staging buffers
   // ---- trip 2: slots, group table, coefficients
   uint32_t sl[N2];
   {
@@ -382,7 +367,6 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
       }
     }
   }
-  }  // batches
 }
 
 __global__ void gaussian_coef_kernel(const double* __restrict__ origins,
@@ -448,7 +432,7 @@ int launch_one(const CellArgs& args, const CellTables& tb, int G, cudaStream_t s
                                       kWarps * SM::warp_bytes(kMaxGroups)));
     configured = true;
   }
-  const int64_t per_cta = (int64_t)kWarps * P * kTasks;
+  const int64_t per_cta = (int64_t)kWarps * P;
   const int64_t grid = (n + per_cta - 1) / per_cta;
   cellop_kernel<N, KIN, COEF, ATOMIC>
       <<<(unsigned)grid, kWarps * 32, kWarps * SM::warp_bytes(G), st>>>(args, tb, G);

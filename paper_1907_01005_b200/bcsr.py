@@ -896,18 +896,83 @@ def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     b_row_lo = b.block_offsets[b.row_start[:n_rows]]
     b_row_hi = b.block_offsets[b.row_start[1 : n_rows + 1]]
     row_dbl = (a_row_hi - a_row_lo) + (b_row_hi - b_row_lo)
-    if n_rows and int(row_dbl.max()) > _TM_STAGE_MAX:
-        raise ShapeError(f"tmmult block row needs {int(row_dbl.max()) * 8} bytes of shared memory")
     target = int(np.clip(int(row_dbl.sum()) // (148 * 8), 2048, _TM_STAGE_TARGET))
-    row_chunk = _greedy_chunks(row_dbl, target)
-    n_chunks = int(row_chunk[-1]) + 1 if n_rows else 0
-    first_row = np.searchsorted(row_chunk, np.arange(n_chunks + 1)).astype(np.int64)
-    chunk_a = np.stack([a_row_lo[first_row[:-1]], a_row_hi[first_row[1:] - 1]], 1) if n_chunks \
-        else np.zeros((0, 2), np.int64)
-    chunk_b = np.stack([b_row_lo[first_row[:-1]], b_row_hi[first_row[1:] - 1]], 1) if n_chunks \
-        else np.zeros((0, 2), np.int64)
+    # units: whole block rows, or (A group x B group) tiles of one row when the
+    # row alone exceeds the stage target; whole-row units merge into chunks
+    a_dbl = a_row_hi - a_row_lo
+    b_dbl = b_row_hi - b_row_lo
+
+    def groups(offsets, p0, p1, budget):
+        starts, acc = [p0], 0
+        for pos in range(p0, p1):
+            sz = int(offsets[pos + 1] - offsets[pos])
+            if pos > starts[-1] and acc + sz > budget:
+                starts.append(pos)
+                acc = 0
+            acc += sz
+        return starts
+
+    ag_start, bg_start = [], []          # global group starts (row-ordered)
+    u_row, u_a0, u_a1, u_b0, u_b1, u_full = [], [], [], [], [], []
+    u_base = np.zeros(n_rows + 1, dtype=np.int64)
+    row_ag0 = np.zeros(n_rows, dtype=np.int64)
+    row_bg0 = np.zeros(n_rows, dtype=np.int64)
+    row_nbg = np.ones(n_rows, dtype=np.int64)
+    for i in range(n_rows):
+        pa0, pa1 = int(a.row_start[i]), int(a.row_start[i + 1])
+        pb0, pb1 = int(b.row_start[i]), int(b.row_start[i + 1])
+        u_base[i] = len(u_row)
+        row_ag0[i], row_bg0[i] = len(ag_start), len(bg_start)
+        if row_dbl[i] <= target:
+            gs_a, gs_b = [pa0], [pb0]
+        else:
+            half = target // 2
+            if a_dbl[i] <= half:
+                gs_a, gs_b = [pa0], groups(b.block_offsets, pb0, pb1, target - int(a_dbl[i]))
+            elif b_dbl[i] <= half:
+                gs_a, gs_b = groups(a.block_offsets, pa0, pa1, target - int(b_dbl[i])), [pb0]
+            else:
+                gs_a = groups(a.block_offsets, pa0, pa1, half)
+                gs_b = groups(b.block_offsets, pb0, pb1, half)
+        ag_start += gs_a
+        bg_start += gs_b
+        row_nbg[i] = len(gs_b)
+        ea, eb = gs_a[1:] + [pa1], gs_b[1:] + [pb1]
+        full = len(gs_a) == 1 and len(gs_b) == 1
+        for x0, x1 in zip(gs_a, ea):
+            for y0, y1 in zip(gs_b, eb):
+                u_row.append(i), u_a0.append(x0), u_a1.append(x1)
+                u_b0.append(y0), u_b1.append(y1), u_full.append(full)
+    u_base[n_rows] = len(u_row)
+    u_row = np.asarray(u_row, dtype=np.int64)
+    u_a0, u_a1 = np.asarray(u_a0, dtype=np.int64), np.asarray(u_a1, dtype=np.int64)
+    u_b0, u_b1 = np.asarray(u_b0, dtype=np.int64), np.asarray(u_b1, dtype=np.int64)
+    u_full = np.asarray(u_full, dtype=bool)
+    u_dbl = (a.block_offsets[u_a1] - a.block_offsets[u_a0]) \
+        + (b.block_offsets[u_b1] - b.block_offsets[u_b0])
+    if u_dbl.size and int(u_dbl.max()) > _TM_STAGE_MAX:
+        raise ShapeError(f"tmmult block row needs {int(u_dbl.max()) * 8} bytes of shared memory")
+    u_chunk = np.empty(u_row.size, dtype=np.int64)
+    cid, acc = -1, 0
+    for j in range(u_row.size):
+        v = int(u_dbl[j])
+        if cid < 0 or not u_full[j] or not u_full[j - 1] or acc + v > target:
+            cid += 1
+            acc = 0
+        acc += v
+        u_chunk[j] = cid
+    n_chunks = cid + 1
+    first_u = np.searchsorted(u_chunk, np.arange(n_chunks + 1)).astype(np.int64)
+    last_u = first_u[1:] - 1
+    chunk_a = np.stack([a.block_offsets[u_a0[first_u[:-1]]], a.block_offsets[u_a1[last_u]]], 1) \
+        if n_chunks else np.zeros((0, 2), np.int64)
+    chunk_b = np.stack([b.block_offsets[u_b0[first_u[:-1]]], b.block_offsets[u_b1[last_u]]], 1) \
+        if n_chunks else np.zeros((0, 2), np.int64)
     stage = (chunk_a[:, 1] - chunk_a[:, 0]) + (chunk_b[:, 1] - chunk_b[:, 0])
-    chunk = row_chunk[row]
+    ag = np.searchsorted(np.asarray(ag_start, dtype=np.int64), pa, side="right") - 1
+    bg = np.searchsorted(np.asarray(bg_start, dtype=np.int64), pb, side="right") - 1
+    unit = u_base[row] + (ag - row_ag0[row]) * row_nbg[row] + (bg - row_bg0[row])
+    chunk = u_chunk[unit]
     order = np.lexsort((cp, chunk))
     pa, pb, row, cp, chunk = pa[order], pb[order], row[order], cp[order], chunk[order]
     n_tri = int(pa.size)

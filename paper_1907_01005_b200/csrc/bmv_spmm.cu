@@ -424,55 +424,33 @@ constexpr int kMmBMax = 256;  // doubles per staged B block
 // is cut into 8-row tiles (<= 16 tiles held in registers); per (A_ik, C_kj)
 // pair the C block is two B fragments (k = 0..3, 4..7) loaded once, each
 // tile takes two DMMA k-steps with A rows from the shared stage.
-constexpr int kMmTiles = 16;
+constexpr int kMmTiles = 64;  // rows <= 512 on the fast path
 
 __device__ __forceinline__ void mm_block8(const MmArgs& g, int64_t o, const double* SA, int lane) {
   const int rows = g.out_rows[o], cst = g.out_stride[o];
   const int64_t p0 = g.pair_start[o], p1 = g.pair_start[o + 1];
   const int gid = lane >> 2, tig = lane & 3;
-  const int ntiles = (rows + 7) >> 3;
-  double acc0[kMmTiles], acc1[kMmTiles];
-#pragma unroll
-  for (int q = 0; q < kMmTiles; ++q) acc0[q] = acc1[q] = 0.0;
-  double nb0 = 0.0, nb1 = 0.0;
-  if (p0 < p1) {
-    const double* Bg = g.b + g.pair_b_off[p0] + gid;
-    const int bs = g.pair_b_stride[p0];
-    nb0 = __ldg(Bg + (int64_t)tig * bs);
-    nb1 = __ldg(Bg + (int64_t)(4 + tig) * bs);
-  }
-  for (int64_t p = p0; p < p1; ++p) {
-    const double b0 = nb0, b1 = nb1;
-    if (p + 1 < p1) {  // prefetch the next pair's C fragments
-      const double* Bn = g.b + g.pair_b_off[p + 1] + gid;
-      const int bsn = g.pair_b_stride[p + 1];
-      nb0 = __ldg(Bn + (int64_t)tig * bsn);
-      nb1 = __ldg(Bn + (int64_t)(4 + tig) * bsn);
+  for (int r0 = 0; r0 < rows; r0 += 8) {  // 8-row tiles, warp-uniform
+    const int r = r0 + gid;
+    const bool in = r < rows;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int64_t p = p0; p < p1; ++p) {
+      const double* Bg = g.b + g.pair_b_off[p] + gid;  // C block: L1/L2 resident
+      const int bs = g.pair_b_stride[p];
+      const double b0 = __ldg(Bg + (int64_t)tig * bs), b1 = __ldg(Bg + (int64_t)(4 + tig) * bs);
+      const double* A = SA + g.pair_a_soff[p] + tig + r * g.pair_a_stride[p];
+      const double a0 = in ? A[0] : 0.0, a1 = in ? A[4] : 0.0;
+      dmma_8x8x4(acc0, acc1, a0, b0);
+      dmma_8x8x4(acc0, acc1, a1, b1);
     }
-    const double* A = SA + g.pair_a_soff[p] + tig;
-    const int as = g.pair_a_stride[p];
-#pragma unroll
-    for (int q = 0; q < kMmTiles; ++q) {
-      if (q < ntiles) {
-        const int r = 8 * q + gid;
-        const bool in = r < rows;
-        const double a0 = in ? A[r * as] : 0.0, a1 = in ? A[r * as + 4] : 0.0;
-        dmma_8x8x4(acc0[q], acc1[q], a0, b0);
-        dmma_8x8x4(acc0[q], acc1[q], a1, b1);
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < kMmTiles; ++q) {
-    const int r = 8 * q + gid;
-    if (q < ntiles && r < rows) {
+    if (in) {
       double* dst = g.c + g.out_off[o] + (int64_t)r * cst + 2 * tig;
       if (g.accumulate) {
-        dst[0] = fma(g.alpha, acc0[q], dst[0]);
-        dst[1] = fma(g.alpha, acc1[q], dst[1]);
+        dst[0] = fma(g.alpha, acc0, dst[0]);
+        dst[1] = fma(g.alpha, acc1, dst[1]);
       } else {
-        dst[0] = g.alpha * acc0[q];
-        dst[1] = g.alpha * acc1[q];
+        dst[0] = g.alpha * acc0;
+        dst[1] = g.alpha * acc1;
       }
     }
   }
@@ -483,7 +461,7 @@ __device__ __forceinline__ void mm_block(const MmArgs& g, int64_t o, const doubl
   const int rows = g.out_rows[o], cols = g.out_cols[o], cst = g.out_stride[o];
   const int64_t p0 = g.pair_start[o], p1 = g.pair_start[o + 1];
   const int entries = rows * cols;
-  if (cols == 8 && g.all_inner8 && rows <= 8 * kMmTiles) {
+  if (cols == 8 && g.all_inner8) {
     mm_block8(g, o, SA, lane);
     return;
   }
@@ -535,18 +513,24 @@ __device__ __forceinline__ void mm_block(const MmArgs& g, int64_t o, const doubl
 }
 
 // One CTA per chunk (fallback, any alignment).
-__global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs g) {
+template <bool FAST>
+__global__ void __launch_bounds__(kMmWarps * 32) mmult_chunk_kernel(const MmArgs g, int sb_doubles) {
   extern __shared__ __align__(16) double stage[];
   const int64_t ch = g.chunk_ids ? g.chunk_ids[blockIdx.x] : blockIdx.x;
   const int64_t a_lo = g.chunk_a[2 * ch];
   const int na = (int)(g.chunk_a[2 * ch + 1] - a_lo);
   __shared__ uint64_t bar;
-  double* SA = stage + kMmWarps * kMmBMax;
+  double* SA = stage + sb_doubles;  // warp B buffers (generic path only) then the A stage
   stage_ranges(SA, g.a + a_lo, na, SA + na, g.a + a_lo + na, 0, &bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* SBw = stage + warp * kMmBMax;
   const int64_t o_end = g.chunk_out_start[ch + 1];
-  for (int64_t o = g.chunk_out_start[ch] + warp; o < o_end; o += kMmWarps) mm_block(g, o, SA, SBw, lane);
+  for (int64_t o = g.chunk_out_start[ch] + warp; o < o_end; o += kMmWarps) {
+    if (FAST)
+      mm_block8(g, o, SA, lane);
+    else
+      mm_block(g, o, SA, SBw, lane);
+  }
 }
 
 // Persistent over its chunk list with a kStages-deep ring of TMA-filled A stages.
@@ -637,7 +621,7 @@ struct bmv_tmmult {
 
 struct bmv_mmult {
   int64_t n_out = 0, n_chunks = 0, n_pairs = 0;
-  int smem_bytes = 0, aligned = 0, all_inner8 = 0;
+  int smem_bytes = 0, aligned = 0, all_inner8 = 0, all8 = 0;
   ChunkClasses cls;
   int64_t *chunk_a = nullptr, *chunk_out_start = nullptr, *out_off = nullptr,
           *pair_start = nullptr, *pair_b_off = nullptr;
@@ -869,10 +853,16 @@ int bmv_mmult_create(const bmv_mmult_desc* d, bmv_mmult** out) {
     int ok8 = 1;
     for (int64_t q = 0; q < d->n_pairs; ++q) ok8 &= d->pair_inner[q] == 8 && d->pair_b_stride[q] >= 8;
     p->all_inner8 = ok8;
+    int oc8 = 1;
+    for (int64_t o = 0; o < d->n_out; ++o) oc8 &= d->out_cols[o] == 8;
+    p->all8 = ok8 && oc8;
   }
   if (!rc) {
-    cudaError_t e = cudaFuncSetAttribute(mmult_chunk_kernel,
+    cudaError_t e = cudaFuncSetAttribute(mmult_chunk_kernel<false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mmult_chunk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               max_smem - 1024);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(mmult_chunk_kernel_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                max_smem - 1024);
@@ -918,7 +908,12 @@ int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, dou
       const unsigned pgrid = (unsigned)std::min<int64_t>(p->cls.count[0], (int64_t)sm_count() * per_sm);
       mmult_chunk_kernel_p<<<pgrid, kMmWarps * 32, smem, st>>>(g, p->cls.count[0], a_bytes / 8);
     } else {
-      mmult_chunk_kernel<<<(unsigned)p->cls.count[k], kMmWarps * 32, p->cls.smem[k], st>>>(g);
+      if (p->all8)
+        mmult_chunk_kernel<true><<<(unsigned)p->cls.count[k], kMmWarps * 32,
+                                   p->cls.smem[k] - kMmWarps * kMmBMax * 8, st>>>(g, 0);
+      else
+        mmult_chunk_kernel<false><<<(unsigned)p->cls.count[k], kMmWarps * 32, p->cls.smem[k], st>>>(
+            g, kMmWarps * kMmBMax);
     }
     BMV_CHECK_LAUNCH();
   }

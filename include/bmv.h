@@ -107,67 +107,81 @@ int bmv_cellop_launches(const bmv_cellop* plan, int32_t* out);
 
 /* ------------------------------------------------------------------ K4 --
  * C(k,l) = sum_i A_ik^T B_il over the owned block rows i.
- * Block rows are cut into chunks of consecutive rows whose A and B blocks
- * (each a contiguous range of the value arrays) fit in shared memory; one
- * CTA stages a chunk with coalesced loads, then its warps compute the
- * chunk's segments (= output blocks touched by the chunk) from shared
- * memory into partial blocks; a second kernel sums every output block's
- * partials in chunk order (fixed order: bit-reproducible, no atomics).  */
+ * Streaming plan: the rows are cut into sub-chunks (consecutive rows, or an
+ * A-group x B-group tile of one long row) whose A and B blocks are two
+ * contiguous value ranges; the sub-chunks are split into one part per CTA
+ * (one persistent CTA per SM).  A producer warp streams a part's
+ * sub-chunks through a ring of shared-memory stages with TMA bulk copies;
+ * n_warps consumer warps compute 8x8 output tiles with FP64 tensor cores.
+ * An item (a run of sub-chunks of one part) touches <= n_warps *
+ * slots_per_warp output tiles; each is owned by one warp, accumulated in
+ * a shared-memory slot and written once to a partial buffer; a second
+ * kernel sums every tile's partials in item order (fixed order:
+ * bit-reproducible, no atomics).
+ *
+ * Triple tile (4 x int32): {a_soff, b_soff, rows | slot << 16 | acols << 24
+ * | bcols << 28, a_stride | b_stride << 16}: stage offsets of the A / B
+ * tile columns (B stage starts at the A length rounded up to even), block
+ * rows, the owning warp's slot, valid tile columns (<= 8) of A and B, row
+ * strides.  Partial tile index of (item, warp, slot) =
+ * (item * n_warps + warp) * slots_per_warp + slot.                        */
 typedef struct {
-  int64_t n_out;             /* output blocks with work                    */
-  int64_t n_chunks;
-  int64_t n_seg;             /* segments (chunk, output block)             */
-  int64_t n_triples;
-  int64_t partial_len;       /* doubles of partial storage                 */
-  int32_t smem_doubles;      /* max staged doubles per chunk (A + B)       */
-  const int64_t* out_off;    /* element offset of the C block              */
-  const int32_t* out_rows;   /* valid rows (size of column block k)        */
-  const int32_t* out_cols;   /* valid cols (size of column block l)        */
-  const int32_t* out_stride; /* C row stride                               */
-  const int64_t* out_seg_start; /* n_out + 1, into out_seg_list            */
-  const int64_t* out_seg_list;  /* n_seg segment ids, chunk order per out  */
-  const int64_t* chunk_a;    /* n_chunks x 2: A element range [lo, hi)     */
-  const int64_t* chunk_b;    /* n_chunks x 2: B element range [lo, hi)     */
-  const int64_t* chunk_seg_start; /* n_chunks + 1, into the segments       */
-  const int64_t* seg_out;       /* n_seg: output index of the segment      */
-  const int64_t* seg_tri_start; /* n_seg + 1, into the triple arrays       */
-  const int64_t* seg_poff;      /* n_seg: offset of the partial block      */
-  const int32_t* tri_a_soff; /* A block offset inside the chunk stage      */
-  const int32_t* tri_b_soff; /* B block offset (from the start of B stage) */
-  const int32_t* tri_rows;   /* rows of block row i                         */
-  const int32_t* tri_a_stride;
-  const int32_t* tri_b_stride;
+  int32_t n_parts;           /* CTAs                                       */
+  int32_t n_warps;           /* consumer warps per CTA (must be 8)         */
+  int32_t slots_per_warp;    /* accumulator tiles per warp (must be 16)    */
+  int32_t stage_doubles;     /* capacity of one pipeline stage (even)      */
+  int64_t n_sub;             /* sub-chunks                                 */
+  int64_t n_items;
+  int64_t n_tri;             /* triple tiles                               */
+  int64_t n_out_tiles;       /* 8x8 tiles of the C blocks with work        */
+  int64_t n_src;             /* partial tiles summed by the reduction      */
+  const int64_t* part_sub_start; /* n_parts + 1                            */
+  const int64_t* sub_a;      /* n_sub x 2: A element range [lo, hi)        */
+  const int64_t* sub_b;      /* n_sub x 2: B element range [lo, hi)        */
+  const int32_t* sub_item;   /* n_sub: item of the sub-chunk (runs)        */
+  const int64_t* sub_tri_start; /* n_sub * n_warps + 1: per (sub, warp)    */
+  const int32_t* tri;        /* n_tri x 4 packed triple tiles              */
+  const int32_t* item_slots; /* n_items x n_warps: slots used              */
+  const int64_t* tile_off;   /* n_out_tiles: element offset in C           */
+  const int32_t* tile_shape; /* n_out_tiles x 3: rows, cols, row stride    */
+  const int64_t* tile_src_start; /* n_out_tiles + 1                        */
+  const int64_t* tile_src;   /* n_src partial tile indices, item order     */
 } bmv_tmmult_desc;
 
 typedef struct bmv_tmmult bmv_tmmult;
 int bmv_tmmult_create(const bmv_tmmult_desc* desc, bmv_tmmult** out);
 int bmv_tmmult_destroy(bmv_tmmult* plan);
-/* c[0:c_len] = 0, then every planned C block = sum over its triples. */
+/* c[0:c_len] = 0, then every planned C tile = sum of its partials. */
 int bmv_tmmult_run(bmv_tmmult* plan, const double* a, const double* b, double* c,
                    int64_t c_len, void* stream);
 
 /* ------------------------------------------------------------------ K5 --
- * Y_ij (+)= alpha * sum_k A_ik B_kj, truncated to Y's pattern.  Owned block
- * rows are cut into chunks whose A blocks (one contiguous range) are staged
- * in shared memory; one warp per output block of the chunk accumulates its
- * products (B blocks through L1/L2) and writes the block once.          */
+ * Y_ij (+)= alpha * sum_k A_ik B_kj, truncated to Y's pattern.
+ * Streaming plan: owned block rows cut into sub-chunks whose A blocks are
+ * one contiguous range (<= stage_doubles), sub-chunks split into one part
+ * per CTA (one persistent CTA per SM); a producer warp streams the A
+ * ranges through shared-memory stages with TMA bulk copies, consumer warps
+ * take the sub-chunk's 8x8 output tiles round-robin (FP64 tensor cores,
+ * B through L1/L2) and store each tile once.
+ * Output blocks are in row order; output block o owns tiles
+ * [tile_start[o], tile_start[o+1]) = ceil(rows/8) x ceil(cols/8), row-major
+ * over (8-row, 8-col) tiles.  Pair (4 x int32): {A offset inside the stage,
+ * a_stride | inner << 16, b_stride, b_off (< 2^31)}.                     */
 typedef struct {
+  int32_t n_parts;           /* CTAs                                       */
+  int32_t stage_doubles;     /* capacity of one pipeline stage (even)      */
+  int64_t n_sub;
   int64_t n_out;
-  int64_t n_chunks;
   int64_t n_pairs;
-  int32_t smem_doubles;      /* max staged A doubles per chunk             */
-  const int64_t* chunk_a;    /* n_chunks x 2: A element range [lo, hi)     */
-  const int64_t* chunk_out_start; /* n_chunks + 1, into the output blocks  */
-  const int64_t* out_off;
-  const int32_t* out_rows;   /* rows of block row i                        */
-  const int32_t* out_cols;   /* size of column block j                     */
-  const int32_t* out_stride;
+  const int64_t* part_sub_start; /* n_parts + 1                            */
+  const int64_t* sub_a;      /* n_sub x 2: A element range [lo, hi)        */
+  const int64_t* sub_tile;   /* n_sub x 2: output tile range [t0, t1)      */
+  const int64_t* sub_out0;   /* n_sub: output block holding tile t0        */
+  const int64_t* tile_start; /* n_out + 1                                  */
+  const int64_t* out_off;    /* n_out: element offset of the Y block       */
+  const int32_t* out_shape;  /* n_out x 4: rows, cols, row stride, 0       */
   const int64_t* pair_start; /* n_out + 1                                  */
-  const int32_t* pair_a_soff;   /* A block offset inside the chunk stage   */
-  const int32_t* pair_a_stride;
-  const int32_t* pair_inner; /* size of inner block k                      */
-  const int64_t* pair_b_off;
-  const int32_t* pair_b_stride;
+  const int32_t* pair;       /* n_pairs x 4 packed                         */
 } bmv_mmult_desc;
 
 typedef struct bmv_mmult bmv_mmult;

@@ -43,24 +43,21 @@ class CellopDesc(C.Structure):
 
 class TmmultDesc(C.Structure):
     _fields_ = [
-        ("n_out", C.c_int64), ("n_chunks", C.c_int64), ("n_seg", C.c_int64),
-        ("n_triples", C.c_int64), ("partial_len", C.c_int64), ("smem_doubles", C.c_int32),
-        ("out_off", _i64p), ("out_rows", _i32p), ("out_cols", _i32p), ("out_stride", _i32p),
-        ("out_seg_start", _i64p), ("out_seg_list", _i64p), ("chunk_a", _i64p),
-        ("chunk_b", _i64p), ("chunk_seg_start", _i64p), ("seg_out", _i64p),
-        ("seg_tri_start", _i64p), ("seg_poff", _i64p), ("tri_a_soff", _i32p),
-        ("tri_b_soff", _i32p), ("tri_rows", _i32p), ("tri_a_stride", _i32p),
-        ("tri_b_stride", _i32p),
+        ("n_parts", C.c_int32), ("n_warps", C.c_int32), ("slots_per_warp", C.c_int32),
+        ("stage_doubles", C.c_int32), ("n_sub", C.c_int64), ("n_items", C.c_int64),
+        ("n_tri", C.c_int64), ("n_out_tiles", C.c_int64), ("n_src", C.c_int64),
+        ("part_sub_start", _i64p), ("sub_a", _i64p), ("sub_b", _i64p), ("sub_item", _i32p),
+        ("sub_tri_start", _i64p), ("tri", _i32p), ("item_slots", _i32p), ("tile_off", _i64p),
+        ("tile_shape", _i32p), ("tile_src_start", _i64p), ("tile_src", _i64p),
     ]
 
 
 class MmultDesc(C.Structure):
     _fields_ = [
-        ("n_out", C.c_int64), ("n_chunks", C.c_int64), ("n_pairs", C.c_int64),
-        ("smem_doubles", C.c_int32), ("chunk_a", _i64p), ("chunk_out_start", _i64p),
-        ("out_off", _i64p), ("out_rows", _i32p), ("out_cols", _i32p), ("out_stride", _i32p),
-        ("pair_start", _i64p), ("pair_a_soff", _i32p), ("pair_a_stride", _i32p),
-        ("pair_inner", _i32p), ("pair_b_off", _i64p), ("pair_b_stride", _i32p),
+        ("n_parts", C.c_int32), ("stage_doubles", C.c_int32), ("n_sub", C.c_int64),
+        ("n_out", C.c_int64), ("n_pairs", C.c_int64), ("part_sub_start", _i64p),
+        ("sub_a", _i64p), ("sub_tile", _i64p), ("sub_out0", _i64p), ("tile_start", _i64p),
+        ("out_off", _i64p), ("out_shape", _i32p), ("pair_start", _i64p), ("pair", _i32p),
     ]
 
 

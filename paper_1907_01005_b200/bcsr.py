@@ -745,43 +745,75 @@ def _mmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     order, outs, start = _group_by_output(cp)
     pa, pb = pa[order], pb[order]
     n_out = int(outs.size)
-    # chunks of consecutive owned block rows whose A blocks fit the stage
+    # ---- streaming plan (csrc/bmv_postmul.cu) ------------------------------
     n_rows = a.n_owned_blocks
     a_row_lo = a.block_offsets[a.row_start[:n_rows]]
     a_row_hi = a.block_offsets[a.row_start[1 : n_rows + 1]]
     row_dbl = a_row_hi - a_row_lo
-    if n_rows and int(row_dbl.max()) > _TM_STAGE_MAX:
-        raise ShapeError(f"mmult block row needs {int(row_dbl.max()) * 8} bytes of shared memory")
-    target = int(np.clip(int(row_dbl.sum()) // (148 * 8), 2048, _TM_STAGE_TARGET))
-    row_chunk = _greedy_chunks(row_dbl, target)
-    n_chunks = int(row_chunk[-1]) + 1 if n_rows else 0
-    first_row = np.searchsorted(row_chunk, np.arange(n_chunks + 1)).astype(np.int64)
-    chunk_a = np.stack([a_row_lo[first_row[:-1]], a_row_hi[first_row[1:] - 1]], 1) if n_chunks \
+    cap = max(_PJ_STAGE, int(row_dbl.max(initial=0)))
+    cap += cap & 1
+    if 2 * cap * 8 > _SMEM_OPTIN:
+        raise ShapeError(f"mmult block row needs {cap * 8} bytes of shared memory (2 stages)")
+    out_row = c.pos_row[outs] if n_out else np.zeros(0, np.int64)
+    out_rows = c.local_row_sizes[out_row].astype(np.int64)
+    out_cols = c.col_blocks.sizes[c.col_index[outs]].astype(np.int64)
+    tiles = ((out_rows + 7) // 8) * ((out_cols + 7) // 8)
+    tile_start = np.concatenate([[0], np.cumsum(tiles)]).astype(np.int64)
+    # parts balanced by A + Y doubles; sub-chunks of consecutive rows <= _PJ_STAGE
+    y_dbl = np.zeros(n_rows, dtype=np.int64)
+    if n_out:
+        np.add.at(y_dbl, out_row, out_rows * c.col_strides[c.col_index[outs]])
+    w = row_dbl + y_dbl
+    n_parts = max(1, min(_pj_parts(c.device), n_rows))
+    total = max(int(w.sum()), 1)
+    before = np.concatenate([[0], np.cumsum(w)[:-1]]) if n_rows else np.zeros(0, np.int64)
+    r_part = np.minimum(before * n_parts // total, n_parts - 1)
+    r_sub = np.empty(n_rows, dtype=np.int64)
+    sid, acc = -1, 0
+    dl, pl = row_dbl.tolist(), r_part.tolist()
+    for j in range(n_rows):
+        if sid < 0 or pl[j] != pl[j - 1] or acc + dl[j] > _PJ_STAGE:
+            sid += 1
+            acc = 0
+        acc += dl[j]
+        r_sub[j] = sid
+    n_sub = sid + 1
+    first_r = np.searchsorted(r_sub, np.arange(n_sub + 1)).astype(np.int64)
+    sub_a = np.stack([a_row_lo[first_r[:-1]], a_row_hi[first_r[1:] - 1]], 1) if n_sub \
         else np.zeros((0, 2), np.int64)
-    out_chunk = row_chunk[c.pos_row[outs]] if n_out else np.zeros(0, np.int64)
-    chunk_out_start = np.searchsorted(out_chunk, np.arange(n_chunks + 1)).astype(np.int64)
-    pair_chunk = row_chunk[a.pos_row[pa]] if pa.size else np.zeros(0, np.int64)
+    part_sub_start = np.searchsorted(r_part[first_r[:-1]], np.arange(n_parts + 1)).astype(np.int64)
+    # outputs are in row order: the sub-chunk's outputs are one range
+    o_lo = np.searchsorted(out_row, first_r[:-1])
+    o_hi = np.searchsorted(out_row, first_r[1:])
+    sub_tile = np.stack([tile_start[o_lo], tile_start[o_hi]], 1)
+    sub_out0 = np.minimum(o_lo, max(n_out - 1, 0))
+    pair_sub = r_sub[a.pos_row[pa]] if pa.size else np.zeros(0, np.int64)
+    b_off = b.block_offsets[pb].astype(np.int64)
+    if b_off.size and int(b_off.max()) >= 1 << 31:
+        raise ShapeError("mmult b holds more than 2^31 values")
+    a_str = a.col_strides[a.col_index[pa]].astype(np.int64)
+    inner = a.col_blocks.sizes[a.col_index[pa]].astype(np.int64)
+    pair = np.empty((pa.size, 4), dtype=np.int64)
+    pair[:, 0] = a.block_offsets[pa] - sub_a[pair_sub, 0] if pa.size else 0
+    pair[:, 1] = a_str | (inner << 16)
+    pair[:, 2] = b.col_strides[b.col_index[pb]]
+    pair[:, 3] = b_off
+    c_str = c.col_strides[c.col_index[outs]].astype(np.int64)
+    out_shape = np.stack([out_rows, out_cols, c_str, np.zeros_like(c_str)], 1)
     arrays = dict(
-        n_chunks=n_chunks,
-        smem_doubles=int((chunk_a[:, 1] - chunk_a[:, 0]).max()) if n_chunks else 0,
-        chunk_a=np.ascontiguousarray(chunk_a, dtype=np.int64).ravel(),
-        chunk_out_start=chunk_out_start,
+        n_parts=n_parts, stage_doubles=cap, n_sub=n_sub,
+        part_sub_start=part_sub_start,
+        sub_a=np.ascontiguousarray(sub_a, dtype=np.int64).ravel(),
+        sub_tile=np.ascontiguousarray(sub_tile, dtype=np.int64).ravel(),
+        sub_out0=sub_out0.astype(np.int64),
+        tile_start=tile_start,
         out_off=c.block_offsets[outs].astype(np.int64),
-        out_rows=c.local_row_sizes[c.pos_row[outs]].astype(np.int32),
-        out_cols=c.col_blocks.sizes[c.col_index[outs]].astype(np.int32),
-        out_stride=c.col_strides[c.col_index[outs]].astype(np.int32),
-        pair_start=start,
-        pair_a_soff=(a.block_offsets[pa] - chunk_a[pair_chunk, 0]).astype(np.int32)
-        if pa.size else np.zeros(0, np.int32),
-        pair_a_stride=a.col_strides[a.col_index[pa]].astype(np.int32),
-        pair_inner=a.col_blocks.sizes[a.col_index[pa]].astype(np.int32),
-        pair_b_off=b.block_offsets[pb].astype(np.int64),
-        pair_b_stride=b.col_strides[b.col_index[pb]].astype(np.int32),
+        out_shape=np.ascontiguousarray(out_shape, dtype=np.int32).ravel(),
+        pair_start=start.astype(np.int64),
+        pair=np.ascontiguousarray(pair.astype(np.int32)).ravel(),
     )
     per = np.repeat(np.arange(n_out), np.diff(start))
-    flops = int(2 * np.sum(arrays["out_rows"].astype(np.int64)[per]
-                           * arrays["pair_inner"].astype(np.int64)
-                           * arrays["out_cols"].astype(np.int64)[per]))
+    flops = int(2 * np.sum(out_rows[per] * inner * out_cols[per]))
     n_own_c = int(c.row_start[c.n_owned_blocks])
     own_cols = c.col_index[:n_own_c]
     full_cover = bool(n_out == n_own_c and
@@ -792,6 +824,9 @@ def _mmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     return plan
 
 
+_SMEM_OPTIN = 232_448   # B200 max dynamic shared memory per block (bytes)
+
+
 class _MmultPlan:
     def __init__(self, arrays, n_out, n_pairs, flops):
         self.arrays = arrays
@@ -799,15 +834,14 @@ class _MmultPlan:
         self.n_out = n_out
         lib = _lib.load()
         d = _lib.MmultDesc()
-        d.n_out, d.n_pairs = n_out, n_pairs
-        d.n_chunks = int(arrays["n_chunks"])
-        d.smem_doubles = int(arrays["smem_doubles"])
-        for name, ct in (("chunk_a", _lib.C.c_int64), ("chunk_out_start", _lib.C.c_int64),
-                         ("out_off", _lib.C.c_int64), ("out_rows", _lib.C.c_int32),
-                         ("out_cols", _lib.C.c_int32), ("out_stride", _lib.C.c_int32),
-                         ("pair_start", _lib.C.c_int64), ("pair_a_soff", _lib.C.c_int32),
-                         ("pair_a_stride", _lib.C.c_int32), ("pair_inner", _lib.C.c_int32),
-                         ("pair_b_off", _lib.C.c_int64), ("pair_b_stride", _lib.C.c_int32)):
+        d.n_parts = int(arrays["n_parts"])
+        d.stage_doubles = int(arrays["stage_doubles"])
+        d.n_sub, d.n_out, d.n_pairs = int(arrays["n_sub"]), n_out, n_pairs
+        for name, ct in (("part_sub_start", _lib.C.c_int64), ("sub_a", _lib.C.c_int64),
+                         ("sub_tile", _lib.C.c_int64), ("sub_out0", _lib.C.c_int64),
+                         ("tile_start", _lib.C.c_int64), ("out_off", _lib.C.c_int64),
+                         ("out_shape", _lib.C.c_int32), ("pair_start", _lib.C.c_int64),
+                         ("pair", _lib.C.c_int32)):
             arrays[name] = np.ascontiguousarray(arrays[name])
             setattr(d, name, _lib.ptr(arrays[name], ct))
         raw = _lib.C.c_void_p()
@@ -841,23 +875,6 @@ def mmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, alpha: float 
         counters.flops += plan.flops
 
 
-_TM_STAGE_TARGET = 3_000   # doubles staged per K4/K5 chunk (24 KB: several CTAs per SM)
-_TM_STAGE_MAX = 27_000     # hard limit per chunk (216 KB of shared memory)
-
-
-def _greedy_chunks(sizes: np.ndarray, target: int) -> np.ndarray:
-    """Chunk id of each item: consecutive items while the running sum <= target."""
-    out = np.empty(sizes.size, dtype=np.int64)
-    cid, acc = 0, 0
-    for i, v in enumerate(sizes.tolist()):
-        if acc and acc + v > target:
-            cid += 1
-            acc = 0
-        acc += v
-        out[i] = cid
-    return out
-
-
 def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     """Per output block of C, the (A_ik, B_il) block products of owned rows i,
     in the reference loop order (bcsr.py:646-666); PatternError if C lacks one."""
@@ -888,166 +905,260 @@ def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
         raise PatternError(f"tmmult destination misses block ({int(k[j])}, {int(ell[j])})")
     if (c.local_row_sizes[c.pos_row[cp]] != a.col_blocks.sizes[k]).any():
         raise ShapeError("tmmult destination row block is incomplete (split ghost group)")
-    # chunks: consecutive owned block rows whose A and B blocks (two contiguous
-    # value ranges) fit the shared-memory stage; segments: one output block
-    # inside one chunk; triples keep the reference order inside a segment
+    # ---- streaming plan (csrc/bmv_project.cu) ------------------------------
     a_row_lo = a.block_offsets[a.row_start[:n_rows]]
     a_row_hi = a.block_offsets[a.row_start[1 : n_rows + 1]]
     b_row_lo = b.block_offsets[b.row_start[:n_rows]]
     b_row_hi = b.block_offsets[b.row_start[1 : n_rows + 1]]
-    row_dbl = (a_row_hi - a_row_lo) + (b_row_hi - b_row_lo)
-    target = int(np.clip(int(row_dbl.sum()) // (148 * 8), 2048, _TM_STAGE_TARGET))
-    # units: whole block rows, or (A group x B group) tiles of one row when the
-    # row alone exceeds the stage target; whole-row units merge into chunks
+    # output tiles: 8x8 pieces of the C blocks (blocks wider than 8 split)
+    mr = a.col_blocks.sizes[k].astype(np.int64)
+    mc = b.col_blocks.sizes[ell].astype(np.int64)
+    tm, tn = (mr + 7) // 8, (mc + 7) // 8
+    if n_rows and (int(tm.max(initial=1)) > 16 or int(tn.max(initial=1)) > 16):
+        raise ShapeError("tmmult column blocks wider than 128 are not supported")
+    tri, q = _expand(tm * tn)
+    mt, nt = q // tn[tri], q % tn[tri]
+    t_row, t_pa, t_pb, t_cp = row[tri], pa[tri], pb[tri], cp[tri]
+    t_key = t_cp * 256 + mt * 16 + nt
+    t_rows = a.local_row_sizes[t_row].astype(np.int64)
+
+    # units: whole block rows, or (A group x B group) tiles of a row that
+    # exceeds the stage or the tile budget of an item
+    cap = _PJ_STAGE
+    a_blk = np.diff(a.block_offsets[: int(a.row_start[n_rows]) + 1])
+    b_blk = np.diff(b.block_offsets[: int(b.row_start[n_rows]) + 1])
+    if a_blk.size or b_blk.size:
+        cap = max(cap, 2 * int(max(a_blk.max(initial=0), b_blk.max(initial=0))) + 2)
+    cap += cap & 1
+    a_tiles = (a.col_blocks.sizes[a.col_index[: int(a.row_start[n_rows])]] + 7) // 8
+    b_tiles = (b.col_blocks.sizes[b.col_index[: int(b.row_start[n_rows])]] + 7) // 8
+    cs = np.concatenate([[0], np.cumsum(a_tiles)])
+    ta_row = cs[a.row_start[1 : n_rows + 1]] - cs[a.row_start[:n_rows]]
+    cs = np.concatenate([[0], np.cumsum(b_tiles)])
+    tb_row = cs[b.row_start[1 : n_rows + 1]] - cs[b.row_start[:n_rows]]
     a_dbl = a_row_hi - a_row_lo
     b_dbl = b_row_hi - b_row_lo
+    unit_dbl_row = a_dbl + (a_dbl & 1) + b_dbl
+    big = (unit_dbl_row > cap) | (ta_row * tb_row > _PJ_TILES)
 
-    def groups(offsets, p0, p1, budget):
-        starts, acc = [p0], 0
+    def groups(blk, tiles, p0, p1, budget, tmax):
+        starts, acc, tacc = [p0], 0, 0
         for pos in range(p0, p1):
-            sz = int(offsets[pos + 1] - offsets[pos])
-            if pos > starts[-1] and acc + sz > budget:
+            sz, tt = int(blk[pos]), int(tiles[pos])
+            if pos > starts[-1] and (acc + sz > budget or tacc + tt > tmax):
                 starts.append(pos)
-                acc = 0
+                acc = tacc = 0
             acc += sz
+            tacc += tt
         return starts
 
-    ag_start, bg_start = [], []          # global group starts (row-ordered)
-    u_row, u_a0, u_a1, u_b0, u_b1, u_full = [], [], [], [], [], []
-    u_base = np.zeros(n_rows + 1, dtype=np.int64)
-    row_ag0 = np.zeros(n_rows, dtype=np.int64)
-    row_bg0 = np.zeros(n_rows, dtype=np.int64)
+    u_row = np.arange(n_rows, dtype=np.int64)
+    u_a0, u_a1 = a.row_start[:n_rows].copy(), a.row_start[1 : n_rows + 1].copy()
+    u_b0, u_b1 = b.row_start[:n_rows].copy(), b.row_start[1 : n_rows + 1].copy()
+    u_full = np.ones(n_rows, dtype=bool)
+    ag_start = [u_a0.copy()]
+    bg_start = [u_b0.copy()]
     row_nbg = np.ones(n_rows, dtype=np.int64)
-    for i in range(n_rows):
-        pa0, pa1 = int(a.row_start[i]), int(a.row_start[i + 1])
-        pb0, pb1 = int(b.row_start[i]), int(b.row_start[i + 1])
-        u_base[i] = len(u_row)
-        row_ag0[i], row_bg0[i] = len(ag_start), len(bg_start)
-        if row_dbl[i] <= target:
-            gs_a, gs_b = [pa0], [pb0]
+    extra = []
+    for i in np.flatnonzero(big).tolist():
+        pa0, pa1, pb0, pb1 = int(u_a0[i]), int(u_a1[i]), int(u_b0[i]), int(u_b1[i])
+        half = cap // 2 - 2
+        if a_dbl[i] <= half and ta_row[i] <= 8:
+            gs_a = [pa0]
+            gs_b = groups(b_blk, b_tiles, pb0, pb1, cap - 2 - int(a_dbl[i]), _PJ_TILES // max(int(ta_row[i]), 1))
+        elif b_dbl[i] <= half and tb_row[i] <= 8:
+            gs_b = [pb0]
+            gs_a = groups(a_blk, a_tiles, pa0, pa1, cap - 2 - int(b_dbl[i]), _PJ_TILES // max(int(tb_row[i]), 1))
         else:
-            half = target // 2
-            if a_dbl[i] <= half:
-                gs_a, gs_b = [pa0], groups(b.block_offsets, pb0, pb1, target - int(a_dbl[i]))
-            elif b_dbl[i] <= half:
-                gs_a, gs_b = groups(a.block_offsets, pa0, pa1, target - int(b_dbl[i])), [pb0]
-            else:
-                gs_a = groups(a.block_offsets, pa0, pa1, half)
-                gs_b = groups(b.block_offsets, pb0, pb1, half)
-        ag_start += gs_a
-        bg_start += gs_b
+            gs_a = groups(a_blk, a_tiles, pa0, pa1, half, 8)
+            gs_b = groups(b_blk, b_tiles, pb0, pb1, half, 16)
         row_nbg[i] = len(gs_b)
-        ea, eb = gs_a[1:] + [pa1], gs_b[1:] + [pb1]
-        full = len(gs_a) == 1 and len(gs_b) == 1
-        for x0, x1 in zip(gs_a, ea):
-            for y0, y1 in zip(gs_b, eb):
-                u_row.append(i), u_a0.append(x0), u_a1.append(x1)
-                u_b0.append(y0), u_b1.append(y1), u_full.append(full)
-    u_base[n_rows] = len(u_row)
-    u_row = np.asarray(u_row, dtype=np.int64)
-    u_a0, u_a1 = np.asarray(u_a0, dtype=np.int64), np.asarray(u_a1, dtype=np.int64)
-    u_b0, u_b1 = np.asarray(u_b0, dtype=np.int64), np.asarray(u_b1, dtype=np.int64)
-    u_full = np.asarray(u_full, dtype=bool)
-    u_dbl = (a.block_offsets[u_a1] - a.block_offsets[u_a0]) \
-        + (b.block_offsets[u_b1] - b.block_offsets[u_b0])
-    if u_dbl.size and int(u_dbl.max()) > _TM_STAGE_MAX:
-        raise ShapeError(f"tmmult block row needs {int(u_dbl.max()) * 8} bytes of shared memory")
-    u_chunk = np.empty(u_row.size, dtype=np.int64)
-    cid, acc = -1, 0
+        extra.append((i, gs_a, gs_b, pa1, pb1))
+    if extra:
+        # replace the big rows' single units by their tiles (row-major, A outer)
+        keep = ~big
+        rows_l, a0_l, a1_l, b0_l, b1_l = [u_row[keep]], [u_a0[keep]], [u_a1[keep]], [u_b0[keep]], [u_b1[keep]]
+        full_l = [u_full[keep]]
+        for i, gs_a, gs_b, pa1, pb1 in extra:
+            ea, eb = gs_a[1:] + [pa1], gs_b[1:] + [pb1]
+            for x0, x1 in zip(gs_a, ea):
+                for y0, y1 in zip(gs_b, eb):
+                    rows_l.append([i]), a0_l.append([x0]), a1_l.append([x1])
+                    b0_l.append([y0]), b1_l.append([y1]), full_l.append([False])
+            ag_start.append(np.asarray(gs_a[1:], dtype=np.int64))
+            bg_start.append(np.asarray(gs_b[1:], dtype=np.int64))
+        u_row = np.concatenate([np.asarray(v, dtype=np.int64) for v in rows_l])
+        u_a0 = np.concatenate([np.asarray(v, dtype=np.int64) for v in a0_l])
+        u_a1 = np.concatenate([np.asarray(v, dtype=np.int64) for v in a1_l])
+        u_b0 = np.concatenate([np.asarray(v, dtype=np.int64) for v in b0_l])
+        u_b1 = np.concatenate([np.asarray(v, dtype=np.int64) for v in b1_l])
+        u_full = np.concatenate([np.asarray(v, dtype=bool) for v in full_l])
+        o = np.lexsort((u_b0, u_a0, u_row))
+        u_row, u_a0, u_a1, u_b0, u_b1, u_full = u_row[o], u_a0[o], u_a1[o], u_b0[o], u_b1[o], u_full[o]
+    ag_start = np.unique(np.concatenate(ag_start))
+    bg_start = np.unique(np.concatenate(bg_start))
+    u_base = np.searchsorted(u_row, np.arange(n_rows + 1)).astype(np.int64)
+    ua = a.block_offsets[u_a1] - a.block_offsets[u_a0]
+    ub = b.block_offsets[u_b1] - b.block_offsets[u_b0]
+    u_dbl = ua + (ua & 1) + ub
+    u_tiles = np.zeros(u_row.size, dtype=np.int64)
+    # parts: balanced by staged doubles, one per SM
+    n_parts = max(1, min(_pj_parts(c.device), int(u_row.size)))
+    total = max(int(u_dbl.sum()), 1)
+    before = np.concatenate([[0], np.cumsum(u_dbl)[:-1]]) if u_row.size else np.zeros(0, np.int64)
+    u_part = np.minimum(before * n_parts // total, n_parts - 1)
+    # triple tile -> unit
+    ag = np.searchsorted(ag_start, t_pa, side="right") - 1
+    bg = np.searchsorted(bg_start, t_pb, side="right") - 1
+    row_ag0 = np.searchsorted(ag_start, a.row_start[:n_rows])
+    row_bg0 = np.searchsorted(bg_start, b.row_start[:n_rows])
+    t_unit = u_base[t_row] + (ag - row_ag0[t_row]) * row_nbg[t_row] + (bg - row_bg0[t_row])
+    np.add.at(u_tiles, t_unit, 1)  # upper bound of distinct tiles per unit
+    # sub-chunks: consecutive whole-row units of one part within the stage
+    u_sub = np.empty(u_row.size, dtype=np.int64)
+    sid, acc, tacc = -1, 0, 0
+    dl, tl, fl, pl = u_dbl.tolist(), u_tiles.tolist(), u_full.tolist(), u_part.tolist()
     for j in range(u_row.size):
-        v = int(u_dbl[j])
-        if cid < 0 or not u_full[j] or not u_full[j - 1] or acc + v > target:
-            cid += 1
-            acc = 0
-        acc += v
-        u_chunk[j] = cid
-    n_chunks = cid + 1
-    first_u = np.searchsorted(u_chunk, np.arange(n_chunks + 1)).astype(np.int64)
+        if (sid < 0 or not fl[j] or not fl[j - 1] or pl[j] != pl[j - 1]
+                or acc + dl[j] > cap or tacc + tl[j] > _PJ_TILES):
+            sid += 1
+            acc = tacc = 0
+        acc += dl[j]
+        tacc += tl[j]
+        u_sub[j] = sid
+    n_sub = sid + 1
+    first_u = np.searchsorted(u_sub, np.arange(n_sub + 1)).astype(np.int64)
     last_u = first_u[1:] - 1
-    chunk_a = np.stack([a.block_offsets[u_a0[first_u[:-1]]], a.block_offsets[u_a1[last_u]]], 1) \
-        if n_chunks else np.zeros((0, 2), np.int64)
-    chunk_b = np.stack([b.block_offsets[u_b0[first_u[:-1]]], b.block_offsets[u_b1[last_u]]], 1) \
-        if n_chunks else np.zeros((0, 2), np.int64)
-    stage = (chunk_a[:, 1] - chunk_a[:, 0]) + (chunk_b[:, 1] - chunk_b[:, 0])
-    ag = np.searchsorted(np.asarray(ag_start, dtype=np.int64), pa, side="right") - 1
-    bg = np.searchsorted(np.asarray(bg_start, dtype=np.int64), pb, side="right") - 1
-    unit = u_base[row] + (ag - row_ag0[row]) * row_nbg[row] + (bg - row_bg0[row])
-    chunk = u_chunk[unit]
-    order = np.lexsort((cp, chunk))
-    pa, pb, row, cp, chunk = pa[order], pb[order], row[order], cp[order], chunk[order]
-    n_tri = int(pa.size)
-    first = np.ones(n_tri, dtype=bool)
-    if n_tri:
-        first[1:] = (cp[1:] != cp[:-1]) | (chunk[1:] != chunk[:-1])
-    seg_tri_start = np.concatenate([np.flatnonzero(first), [n_tri]]).astype(np.int64)
-    outs = np.unique(cp)
-    n_out = int(outs.size)
-    seg_out = np.searchsorted(outs, cp[first]).astype(np.int64)
-    seg_chunk = chunk[first]
-    chunk_seg_start = np.searchsorted(seg_chunk, np.arange(n_chunks + 1)).astype(np.int64)
-    out_rows = c.local_row_sizes[c.pos_row[outs]].astype(np.int64)
-    out_cols = c.col_blocks.sizes[c.col_index[outs]].astype(np.int64)
-    seg_ent = out_rows[seg_out] * out_cols[seg_out]
-    # partials of one output block contiguous, in chunk order (coalesced reduce)
-    order2 = np.lexsort((seg_chunk, seg_out))
-    out_seg_start = np.searchsorted(seg_out[order2], np.arange(n_out + 1)).astype(np.int64)
-    poff_sorted = np.concatenate([[0], np.cumsum(seg_ent[order2])]).astype(np.int64)
-    seg_poff = np.empty(seg_ent.size + 1, dtype=np.int64)
-    seg_poff[order2] = poff_sorted[:-1]
-    seg_poff[-1] = poff_sorted[-1]
-    tri_chunk = chunk
+    sub_a = np.stack([a.block_offsets[u_a0[first_u[:-1]]], a.block_offsets[u_a1[last_u]]], 1)
+    sub_b = np.stack([b.block_offsets[u_b0[first_u[:-1]]], b.block_offsets[u_b1[last_u]]], 1)
+    sub_part = u_part[first_u[:-1]]
+    part_sub_start = np.searchsorted(sub_part, np.arange(n_parts + 1)).astype(np.int64)
+    t_sub = u_sub[t_unit]
+    # items: runs of sub-chunks of one part touching <= _PJ_TILES output tiles
+    o = np.argsort(t_sub, kind="stable")
+    s_sorted, k_sorted = t_sub[o], t_key[o]
+    sub_t0 = np.searchsorted(s_sorted, np.arange(n_sub + 1))
+    sub_item = np.empty(n_sub, dtype=np.int64)
+    n_items = 0
+    for p in range(n_parts):
+        cur, end = int(part_sub_start[p]), int(part_sub_start[p + 1])
+        while cur < end:
+            lo, hi = sub_t0[cur], sub_t0[end]
+            _, first = np.unique(k_sorted[lo:hi], return_index=True)
+            fs = np.sort(s_sorted[lo:hi][first])
+            stop = int(fs[_PJ_TILES]) if fs.size > _PJ_TILES else end
+            if stop <= cur:
+                raise ShapeError("tmmult sub-chunk touches more output tiles than an item holds")
+            sub_item[cur:stop] = n_items
+            n_items += 1
+            cur = stop
+    t_item = sub_item[t_sub]
+    # owner warp + slot of every (item, tile): longest-processing-time first
+    ik = t_item * (int(t_key.max(initial=0)) + 1) + t_key
+    uik, inv = np.unique(ik, return_inverse=True)
+    work = np.bincount(inv, weights=t_rows, minlength=uik.size)
+    it_item = uik // (int(t_key.max(initial=0)) + 1)
+    it_warp = np.empty(uik.size, dtype=np.int64)
+    it_slot = np.empty(uik.size, dtype=np.int64)
+    item_slots = np.zeros((n_items, _PJ_WARPS), dtype=np.int32)
+    bounds = np.searchsorted(it_item, np.arange(n_items + 1))
+    for it in range(n_items):
+        lo, hi = int(bounds[it]), int(bounds[it + 1])
+        load = [0.0] * _PJ_WARPS
+        cnt = [0] * _PJ_WARPS
+        for j in (lo + np.argsort(-work[lo:hi], kind="stable")).tolist():
+            w = min((x for x in range(_PJ_WARPS) if cnt[x] < _PJ_SLOTS), key=lambda x: load[x])
+            it_warp[j], it_slot[j] = w, cnt[w]
+            cnt[w] += 1
+            load[w] += work[j]
+        item_slots[it] = cnt
+    t_warp, t_slot = it_warp[inv], it_slot[inv]
+    # triple tiles sorted by (sub, warp, slot), reference order inside
+    o = np.lexsort((np.arange(t_key.size), t_slot, t_warp, t_sub))
+    t_sub, t_warp, t_slot = t_sub[o], t_warp[o], t_slot[o]
+    t_pa, t_pb, t_rows, mt, nt = t_pa[o], t_pb[o], t_rows[o], mt[o], nt[o]
+    t_mr, t_mc = mr[tri][o], mc[tri][o]
+    sub_tri_start = np.searchsorted(t_sub * _PJ_WARPS + t_warp,
+                                    np.arange(n_sub * _PJ_WARPS + 1)).astype(np.int64)
+    na_sub = sub_a[:, 1] - sub_a[:, 0]
+    a_soff = a.block_offsets[t_pa] - sub_a[t_sub, 0] + 8 * mt
+    b_soff = (na_sub + (na_sub & 1))[t_sub] + b.block_offsets[t_pb] - sub_b[t_sub, 0] + 8 * nt
+    acols = np.minimum(8, t_mr - 8 * mt)
+    bcols = np.minimum(8, t_mc - 8 * nt)
+    a_str = a.col_strides[a.col_index[t_pa]].astype(np.int64)
+    b_str = b.col_strides[b.col_index[t_pb]].astype(np.int64)
+    if t_rows.size and (int(t_rows.max()) >= 1 << 16 or int(max(a_str.max(), b_str.max())) >= 1 << 16):
+        raise ShapeError("tmmult block rows / strides exceed 65535")
+    packed = np.empty((t_key.size, 4), dtype=np.int64)
+    packed[:, 0] = a_soff
+    packed[:, 1] = b_soff
+    packed[:, 2] = t_rows | (t_slot << 16) | (acols << 24) | (bcols << 28)
+    packed[:, 3] = a_str | (b_str << 16)
+    packed = (packed & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+    # output tiles and their partial sources (item order)
+    tiles, tinv = np.unique(uik % (int(t_key.max(initial=0)) + 1), return_inverse=True)
+    src_order = np.lexsort((it_item, tinv))
+    tile_src = ((it_item * _PJ_WARPS + it_warp) * _PJ_SLOTS + it_slot)[src_order]
+    tile_src_start = np.searchsorted(tinv[src_order], np.arange(tiles.size + 1)).astype(np.int64)
+    tcp, tmt, tnt = tiles // 256, (tiles // 16) % 16, tiles % 16
+    c_str = c.col_strides[c.col_index[tcp]].astype(np.int64)
+    tile_off = c.block_offsets[tcp] + 8 * tmt * c_str + 8 * tnt
+    tr = np.minimum(8, c.local_row_sizes[c.pos_row[tcp]] - 8 * tmt)
+    tc = np.minimum(8, c.col_blocks.sizes[c.col_index[tcp]] - 8 * tnt)
     arrays = dict(
-        out_off=c.block_offsets[outs].astype(np.int64),
-        out_rows=out_rows.astype(np.int32),
-        out_cols=out_cols.astype(np.int32),
-        out_stride=c.col_strides[c.col_index[outs]].astype(np.int32),
-        out_seg_start=out_seg_start,
-        out_seg_list=order2.astype(np.int64),
-        chunk_a=np.ascontiguousarray(chunk_a, dtype=np.int64).ravel(),
-        chunk_b=np.ascontiguousarray(chunk_b, dtype=np.int64).ravel(),
-        chunk_seg_start=chunk_seg_start,
-        seg_out=seg_out,
-        seg_tri_start=seg_tri_start,
-        seg_poff=seg_poff[:-1].copy(),
-        partial_len=int(seg_poff[-1]),
-        smem_doubles=int(stage.max()) if n_chunks else 0,
-        n_chunks=n_chunks,
-        tri_a_soff=(a.block_offsets[pa] - chunk_a[tri_chunk, 0]).astype(np.int32),
-        tri_b_soff=(b.block_offsets[pb] - chunk_b[tri_chunk, 0]).astype(np.int32),
-        tri_rows=a.local_row_sizes[row].astype(np.int32),
-        tri_a_stride=a.col_strides[a.col_index[pa]].astype(np.int32),
-        tri_b_stride=b.col_strides[b.col_index[pb]].astype(np.int32),
+        n_parts=n_parts, stage_doubles=cap, n_sub=n_sub, n_items=n_items,
+        part_sub_start=part_sub_start,
+        sub_a=np.ascontiguousarray(sub_a, dtype=np.int64).ravel(),
+        sub_b=np.ascontiguousarray(sub_b, dtype=np.int64).ravel(),
+        sub_item=sub_item.astype(np.int32),
+        sub_tri_start=sub_tri_start,
+        tri=np.ascontiguousarray(packed).ravel(),
+        item_slots=np.ascontiguousarray(item_slots).ravel(),
+        tile_off=tile_off.astype(np.int64),
+        tile_shape=np.ascontiguousarray(np.stack([tr, tc, c_str], 1), dtype=np.int32).ravel(),
+        tile_src_start=tile_src_start,
+        tile_src=tile_src.astype(np.int64),
     )
-    kk = a.col_blocks.sizes[a.col_index[pa]].astype(np.int64)
-    ll = b.col_blocks.sizes[b.col_index[pb]].astype(np.int64)
-    flops = int(np.sum(2 * kk * arrays["tri_rows"].astype(np.int64) * ll))
-    plan = _TmmultPlan(arrays, n_out, int(pa.size), flops)
+    kk = a.col_blocks.sizes[k].astype(np.int64)
+    ll = b.col_blocks.sizes[ell].astype(np.int64)
+    flops = int(np.sum(2 * kk * a.local_row_sizes[row].astype(np.int64) * ll))
+    plan = _TmmultPlan(arrays, flops)
     cache[key] = (plan, b, c)
     return plan
 
 
+_PJ_WARPS = 8        # consumer warps per CTA (bmv_project.cu kPjWarps)
+_PJ_SLOTS = 16       # accumulator tiles per warp (kPjSlots)
+_PJ_TILES = _PJ_WARPS * _PJ_SLOTS
+_PJ_STAGE = 4864     # doubles per pipeline stage (38 KB: 4 stages + 64 KB of slots per SM)
+
+
+def _pj_parts(device) -> int:
+    """Persistent CTAs of the K4 stream kernel: one per SM."""
+    if device is not None and torch.device(device).type == "cuda" and torch.cuda.is_available():
+        return int(torch.cuda.get_device_properties(torch.device(device)).multi_processor_count)
+    return 148
+
+
 class _TmmultPlan:
-    def __init__(self, arrays, n_out, n_tri, flops):
+    def __init__(self, arrays, flops):
         self.arrays = arrays
         self.flops = flops
-        self.n_out = n_out
         lib = _lib.load()
         d = _lib.TmmultDesc()
-        d.n_out, d.n_triples = n_out, n_tri
-        d.n_chunks = int(arrays["n_chunks"])
-        d.n_seg = int(arrays["seg_out"].size)
-        d.partial_len = int(arrays["partial_len"])
-        d.smem_doubles = int(arrays["smem_doubles"])
-        for name, ct in (("out_off", _lib.C.c_int64), ("out_rows", _lib.C.c_int32),
-                         ("out_cols", _lib.C.c_int32), ("out_stride", _lib.C.c_int32),
-                         ("out_seg_start", _lib.C.c_int64), ("out_seg_list", _lib.C.c_int64),
-                         ("chunk_a", _lib.C.c_int64), ("chunk_b", _lib.C.c_int64),
-                         ("chunk_seg_start", _lib.C.c_int64),
-                         ("seg_out", _lib.C.c_int64), ("seg_tri_start", _lib.C.c_int64),
-                         ("seg_poff", _lib.C.c_int64),
-                         ("tri_a_soff", _lib.C.c_int32), ("tri_b_soff", _lib.C.c_int32),
-                         ("tri_rows", _lib.C.c_int32), ("tri_a_stride", _lib.C.c_int32),
-                         ("tri_b_stride", _lib.C.c_int32)):
+        d.n_parts = int(arrays["n_parts"])
+        d.n_warps, d.slots_per_warp = _PJ_WARPS, _PJ_SLOTS
+        d.stage_doubles = int(arrays["stage_doubles"])
+        d.n_sub, d.n_items = int(arrays["n_sub"]), int(arrays["n_items"])
+        d.n_tri = int(arrays["tri"].size // 4)
+        d.n_out_tiles = int(arrays["tile_off"].size)
+        d.n_src = int(arrays["tile_src"].size)
+        for name, ct in (("part_sub_start", _lib.C.c_int64), ("sub_a", _lib.C.c_int64),
+                         ("sub_b", _lib.C.c_int64), ("sub_item", _lib.C.c_int32),
+                         ("sub_tri_start", _lib.C.c_int64), ("tri", _lib.C.c_int32),
+                         ("item_slots", _lib.C.c_int32), ("tile_off", _lib.C.c_int64),
+                         ("tile_shape", _lib.C.c_int32), ("tile_src_start", _lib.C.c_int64),
+                         ("tile_src", _lib.C.c_int64)):
             arrays[name] = np.ascontiguousarray(arrays[name])
             setattr(d, name, _lib.ptr(arrays[name], ct))
         raw = _lib.C.c_void_p()

@@ -715,13 +715,23 @@ def _group_by_output(out_pos: np.ndarray):
 
 
 def _mmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
-    """Per output block of C, the (A_ik, B_kj) products kept by C's pattern,
-    in the reference's Gustavson order (bcsr.py:605-626)."""
     key = ("mm", id(b), id(c))
     cache = _plan_cache(a)
     hit = cache.get(key)
     if hit is not None:
         return hit[0]
+    arrays, n_out, n_pairs, flops, full_cover = mmult_plan_arrays(a, b, c, _pj_parts(c.device))
+    plan = _MmultPlan(arrays, n_out, n_pairs, flops)
+    plan.full_cover = full_cover
+    cache[key] = (plan, b, c)
+    return plan
+
+
+def mmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n_parts: int):
+    """K5 streaming plan (include/bmv.h bmv_mmult_desc): per output block of
+    C the (A_ik, B_kj) products kept by C's pattern, in the reference's
+    Gustavson order (bcsr.py:605-626).  Host-only; returns
+    (arrays, n_out, n_pairs, flops, full_cover)."""
     n_own_pos = int(a.row_start[a.n_owned_blocks])
     pos_a = np.arange(n_own_pos, dtype=np.int64)
     k = a.col_index[pos_a]
@@ -764,7 +774,7 @@ def _mmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     if n_out:
         np.add.at(y_dbl, out_row, out_rows * c.col_strides[c.col_index[outs]])
     w = row_dbl + y_dbl
-    n_parts = max(1, min(_pj_parts(c.device), n_rows))
+    n_parts = max(1, min(int(n_parts), n_rows))
     total = max(int(w.sum()), 1)
     before = np.concatenate([[0], np.cumsum(w)[:-1]]) if n_rows else np.zeros(0, np.int64)
     r_part = np.minimum(before * n_parts // total, n_parts - 1)
@@ -818,10 +828,7 @@ def _mmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     own_cols = c.col_index[:n_own_c]
     full_cover = bool(n_out == n_own_c and
                       np.all(c.col_blocks.sizes[own_cols] == c.col_strides[own_cols]))
-    plan = _MmultPlan(arrays, n_out, int(pa.size), flops)
-    plan.full_cover = full_cover
-    cache[key] = (plan, b, c)
-    return plan
+    return arrays, n_out, int(pa.size), flops, full_cover
 
 
 _SMEM_OPTIN = 232_448   # B200 max dynamic shared memory per block (bytes)
@@ -876,13 +883,22 @@ def mmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, alpha: float 
 
 
 def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
-    """Per output block of C, the (A_ik, B_il) block products of owned rows i,
-    in the reference loop order (bcsr.py:646-666); PatternError if C lacks one."""
     key = ("tm", id(b), id(c))
     cache = _plan_cache(a)
     hit = cache.get(key)
     if hit is not None:
         return hit[0]
+    arrays, flops = tmmult_plan_arrays(a, b, c, _pj_parts(c.device))
+    plan = _TmmultPlan(arrays, flops)
+    cache[key] = (plan, b, c)
+    return plan
+
+
+def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n_parts: int):
+    """K4 streaming plan (include/bmv.h bmv_tmmult_desc): the (A_ik, B_il)
+    block products of the owned rows i, in the reference loop order
+    (bcsr.py:646-666) inside each output tile; PatternError if C lacks a
+    block.  Host-only; returns (arrays, flops)."""
     n_rows = a.n_owned_blocks
     na = a.row_start[1 : n_rows + 1] - a.row_start[:n_rows]
     nb = b.row_start[1 : n_rows + 1] - b.row_start[:n_rows]
@@ -1003,7 +1019,7 @@ def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     u_dbl = ua + (ua & 1) + ub
     u_tiles = np.zeros(u_row.size, dtype=np.int64)
     # parts: balanced by staged doubles, one per SM
-    n_parts = max(1, min(_pj_parts(c.device), int(u_row.size)))
+    n_parts = max(1, min(int(n_parts), int(u_row.size)))
     total = max(int(u_dbl.sum()), 1)
     before = np.concatenate([[0], np.cumsum(u_dbl)[:-1]]) if u_row.size else np.zeros(0, np.int64)
     u_part = np.minimum(before * n_parts // total, n_parts - 1)
@@ -1122,9 +1138,7 @@ def _tmmult_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     kk = a.col_blocks.sizes[k].astype(np.int64)
     ll = b.col_blocks.sizes[ell].astype(np.int64)
     flops = int(np.sum(2 * kk * a.local_row_sizes[row].astype(np.int64) * ll))
-    plan = _TmmultPlan(arrays, flops)
-    cache[key] = (plan, b, c)
-    return plan
+    return arrays, flops
 
 
 _PJ_WARPS = 8        # consumer warps per CTA (bmv_project.cu kPjWarps)

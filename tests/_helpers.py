@@ -52,12 +52,28 @@ class Small:
             attach_support(m, self.support, check=True)
         return m
 
-    def operands(self, ctx, device):
+    def operands(self, ctx, device, lane_width=8):
         rl = make_dof_layout(ctx, self.mesh, self.partition, self.numbering)
         op = CellOperator(self.mesh, self.partition, self.numbering, rl)
-        x = BlockCsrMatrix(self.pattern, rl, ctx, 8, device)
-        hx = BlockCsrMatrix(self.grown, rl, ctx, 8, device)
+        x = BlockCsrMatrix(self.pattern, rl, ctx, lane_width, device)
+        hx = BlockCsrMatrix(self.grown, rl, ctx, lane_width, device)
         return rl, op, x, hx
+
+    def projection_operands(self, ctx, device, rl, lane_width=8, seed=77):
+        """(s, c, xc): projection target, a filled column-space matrix, X C target."""
+        from paper_1907_01005_b200.energy import (column_space_ghost_blocks, make_column_layout,
+                                                  projected_pattern)
+
+        proj = projected_pattern(self.pattern, self.grown)
+        ghosts = column_space_ghost_blocks(self.grown, proj, rl, self.layout.rank_block_start,
+                                           ctx.rank)
+        clayout = make_column_layout(ctx, self.layout.column_blocks, self.layout.rank_block_start,
+                                     ghosts)
+        s = BlockCsrMatrix(proj, clayout, ctx, lane_width, device)
+        c = BlockCsrMatrix(proj, clayout, ctx, lane_width, device)
+        c.fill_owned_entries(lambda r, col: hashed_entries(seed, r, col))
+        xc = BlockCsrMatrix(self.pattern, rl, ctx, lane_width, device)
+        return s, c, xc
 
 
 def cosine(seed):

@@ -1,0 +1,62 @@
+"""K4 / K5 streaming plans on CPU: emulate the kernels over the host plan
+(tests/_plan_emul.py) and compare with dense products of the same data.
+
+Covers wide column blocks (tiles split 2 x 2), narrow lane widths (strides
+< 8, guarded fragment loads), many / few parts and rows split into
+A-group x B-group tiles (small stage).
+"""
+
+import numpy as np
+import pytest
+
+from _helpers import Small
+from _plan_emul import emulate_mmult, emulate_tmmult
+from paper_1907_01005_b200 import bcsr as B
+from paper_1907_01005_b200.comm import serial_context
+from paper_1907_01005_b200.problem import hashed_entries
+
+CENTERS = np.asarray([[1.0, 1.0, 1.0], [3.0, 3.0, 2.0], [2.0, 1.5, 3.0], [0.5, 3.2, 0.7]])
+
+
+def _setup(block_size, lane_width):
+    s = Small((4, 4, 4), (1.0, 1.0, 1.0), 1, 2, CENTERS, 1.6, block_size, 3)
+    ctx = serial_context("cpu")
+    rl, _, x, hx = s.operands(ctx, "cpu", lane_width)
+    s.fill(x, 5, attach=False)
+    hx.fill_owned_entries(lambda r, c: hashed_entries(9, r, c))
+    sm, cm, xc = s.projection_operands(ctx, "cpu", rl, lane_width)
+    return x, hx, sm, cm, xc
+
+
+@pytest.mark.parametrize("block_size,lane_width", [(3, 8), (8, 8), (12, 8), (3, 4), (5, 2)])
+@pytest.mark.parametrize("n_parts", [1, 7, 148])
+@pytest.mark.parametrize("stage", [4864, 96])
+def test_tmmult_plan_emulation(monkeypatch, block_size, lane_width, n_parts, stage):
+    monkeypatch.setattr(B, "_PJ_STAGE", stage)
+    x, hx, sm, _, _ = _setup(block_size, lane_width)
+    arr, flops = B.tmmult_plan_arrays(x, hx, sm, n_parts)
+    got = emulate_tmmult(arr, x.data.numpy(), hx.data.numpy(), sm.data.numel())
+    sm.data.copy_(__import__("torch").from_numpy(got))
+    want = x.to_dense_owned().T @ hx.to_dense_owned()
+    assert np.allclose(sm.to_dense_owned(), want, rtol=1e-13, atol=1e-13 * np.abs(want).max())
+    assert flops > 0
+
+
+@pytest.mark.parametrize("block_size,lane_width", [(3, 8), (8, 8), (12, 8), (3, 4), (5, 2)])
+@pytest.mark.parametrize("n_parts", [1, 7, 148])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_mmult_plan_emulation(block_size, lane_width, n_parts, accumulate):
+    import torch
+
+    x, _, _, cm, xc = _setup(block_size, lane_width)
+    xc.fill_owned_entries(lambda r, c: hashed_entries(3, r, c))
+    before = xc.to_dense_owned()
+    arr, n_out, n_pairs, flops, _ = B.mmult_plan_arrays(x, cm, xc, n_parts)
+    got = emulate_mmult(arr, x.data.numpy(), cm.data.numpy(), xc.data.numpy(), -0.5, accumulate)
+    xc.data.copy_(torch.from_numpy(got))
+    mask = xc.pattern.entry_mask()
+    want = np.where(mask, -0.5 * (x.to_dense_owned() @ cm.to_dense_owned()), 0.0)
+    if accumulate:
+        want = want + before
+    assert np.allclose(xc.to_dense_owned(), want, rtol=1e-13, atol=1e-13 * np.abs(want).max())
+    assert n_pairs == arr["pair"].size // 4

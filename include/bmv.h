@@ -105,43 +105,46 @@ int bmv_potential_gaussian(int64_t n_cells, int32_t q3, const double* cell_origi
 /* Number of kernel launches one apply issues (for bench accounting). */
 int bmv_cellop_launches(const bmv_cellop* plan, int32_t* out);
 
+/* ---------------------------------------------------------- copy lists --
+ * K4 and K5 stream sub-chunks (consecutive block rows, or a tile of one
+ * long row) through a ring of shared-memory stages: one persistent CTA per
+ * part (one part per SM), a producer warp issuing TMA bulk copies, consumer
+ * warps on FP64 tensor cores.  What one sub-chunk stages is a copy list:
+ * entries of 4 x int32 {dst byte offset in the stage, bytes | src << 28 |
+ * last << 30, src byte offset lo, hi}; src 0 = the plan's metadata array,
+ * 1 = operand a, 2 = operand b; <= 32 consecutive entries per sub-chunk,
+ * the last one flagged; the first entry stages the sub-chunk's metadata
+ * (header + work descriptors) at offset 0.  Entries 16-byte aligned go
+ * through cp.async.bulk, others are copied by the producer's lanes.       */
+
 /* ------------------------------------------------------------------ K4 --
  * C(k,l) = sum_i A_ik^T B_il over the owned block rows i.
- * Streaming plan: the rows are cut into sub-chunks (consecutive rows, or an
- * A-group x B-group tile of one long row) whose A and B blocks are two
- * contiguous value ranges; the sub-chunks are split into one part per CTA
- * (one persistent CTA per SM).  A producer warp streams a part's
- * sub-chunks through a ring of shared-memory stages with TMA bulk copies;
- * n_warps consumer warps compute 8x8 output tiles with FP64 tensor cores.
- * An item (a run of sub-chunks of one part) touches <= n_warps *
- * slots_per_warp output tiles; each is owned by one warp, accumulated in
- * a shared-memory slot and written once to a partial buffer; a second
- * kernel sums every tile's partials in item order (fixed order:
- * bit-reproducible, no atomics).
- *
- * Triple tile (4 x int32): {a_soff, b_soff, rows | slot << 16 | acols << 24
- * | bcols << 28, a_stride | b_stride << 16}: stage offsets of the A / B
- * tile columns (B stage starts at the A length rounded up to even), block
- * rows, the owning warp's slot, valid tile columns (<= 8) of A and B, row
- * strides.  Partial tile index of (item, warp, slot) =
- * (item * n_warps + warp) * slots_per_warp + slot.                        */
+ * Stage = [header (36 int32)][triple tiles (4 x int32)][A blocks][B blocks].
+ * Header: [0..16] first triple tile of each of the 16 consumer warps
+ * (local index) and the end, [17] item, [18] 1 on the item's last
+ * sub-chunk, [20..35] slots used per warp in the item.
+ * Triple tile: {A tile offset, B tile offset (doubles from the stage
+ * start), rows | slot << 16 | acols << 24 | bcols << 28, a_stride |
+ * b_stride << 16}: sum_r A[r][0:acols] B[r][0:bcols] into the warp's slot.
+ * An item (run of sub-chunks of one part) touches <= 16 x 8 output tiles,
+ * each owned by one warp and written once to the partial buffer at
+ * (item * 16 + warp) * 8 + slot; a second kernel sums every 8x8 output
+ * tile's partials in item order (bit-reproducible, no atomics).          */
 typedef struct {
   int32_t n_parts;           /* CTAs                                       */
-  int32_t n_warps;           /* consumer warps per CTA (must be 8)         */
-  int32_t slots_per_warp;    /* accumulator tiles per warp (must be 16)    */
-  int32_t stage_doubles;     /* capacity of one pipeline stage (even)      */
+  int32_t n_warps;           /* consumer warps per CTA (must be 16)        */
+  int32_t slots_per_warp;    /* accumulator tiles per warp (must be 8)     */
+  int32_t stage_bytes;       /* capacity of one pipeline stage (16 | it)   */
   int64_t n_sub;             /* sub-chunks                                 */
   int64_t n_items;
-  int64_t n_tri;             /* triple tiles                               */
+  int64_t n_entries;         /* copy-list entries                          */
+  int64_t meta_len;          /* int32 values of metadata                   */
   int64_t n_out_tiles;       /* 8x8 tiles of the C blocks with work        */
   int64_t n_src;             /* partial tiles summed by the reduction      */
-  const int64_t* part_sub_start; /* n_parts + 1                            */
-  const int64_t* sub_a;      /* n_sub x 2: A element range [lo, hi)        */
-  const int64_t* sub_b;      /* n_sub x 2: B element range [lo, hi)        */
-  const int32_t* sub_item;   /* n_sub: item of the sub-chunk (runs)        */
-  const int64_t* sub_tri_start; /* n_sub * n_warps + 1: per (sub, warp)    */
-  const int32_t* tri;        /* n_tri x 4 packed triple tiles              */
-  const int32_t* item_slots; /* n_items x n_warps: slots used              */
+  const int64_t* part_sub_start;   /* n_parts + 1                          */
+  const int64_t* part_entry_start; /* n_parts + 1                          */
+  const int32_t* copies;     /* n_entries x 4                              */
+  const int32_t* meta;       /* meta_len                                   */
   const int64_t* tile_off;   /* n_out_tiles: element offset in C           */
   const int32_t* tile_shape; /* n_out_tiles x 3: rows, cols, row stride    */
   const int64_t* tile_src_start; /* n_out_tiles + 1                        */
@@ -157,31 +160,24 @@ int bmv_tmmult_run(bmv_tmmult* plan, const double* a, const double* b, double* c
 
 /* ------------------------------------------------------------------ K5 --
  * Y_ij (+)= alpha * sum_k A_ik B_kj, truncated to Y's pattern.
- * Streaming plan: owned block rows cut into sub-chunks whose A blocks are
- * one contiguous range (<= stage_doubles), sub-chunks split into one part
- * per CTA (one persistent CTA per SM); a producer warp streams the A
- * ranges through shared-memory stages with TMA bulk copies, consumer warps
- * take the sub-chunk's 8x8 output tiles round-robin (FP64 tensor cores,
- * B through L1/L2) and store each tile once.
- * Output blocks are in row order; output block o owns tiles
- * [tile_start[o], tile_start[o+1]) = ceil(rows/8) x ceil(cols/8), row-major
- * over (8-row, 8-col) tiles.  Pair (4 x int32): {A offset inside the stage,
- * a_stride | inner << 16, b_stride, b_off (< 2^31)}.                     */
+ * Stage = [header int4 {n_tasks, 0, 0, 0}][tasks (4 x int32)][pairs
+ * (4 x int32)][B blocks used by the pairs][A blocks of the rows].
+ * Task = one 8x8 output tile: {element offset of the tile in Y, rows |
+ * cols << 4 | col-tile << 8 | Y row stride << 16, first pair (index into
+ * the staged pairs) | pairs << 16, row-tile}.  Pair: {A block offset,
+ * a_stride | inner << 16, b_stride, B block offset} (offsets in doubles
+ * from the stage start).  16 consumer warps take the tasks round-robin and
+ * store each tile once.                                                   */
 typedef struct {
   int32_t n_parts;           /* CTAs                                       */
-  int32_t stage_doubles;     /* capacity of one pipeline stage (even)      */
+  int32_t stage_bytes;       /* capacity of one pipeline stage (16 | it)   */
   int64_t n_sub;
-  int64_t n_out;
-  int64_t n_pairs;
-  const int64_t* part_sub_start; /* n_parts + 1                            */
-  const int64_t* sub_a;      /* n_sub x 2: A element range [lo, hi)        */
-  const int64_t* sub_tile;   /* n_sub x 2: output tile range [t0, t1)      */
-  const int64_t* sub_out0;   /* n_sub: output block holding tile t0        */
-  const int64_t* tile_start; /* n_out + 1                                  */
-  const int64_t* out_off;    /* n_out: element offset of the Y block       */
-  const int32_t* out_shape;  /* n_out x 4: rows, cols, row stride, 0       */
-  const int64_t* pair_start; /* n_out + 1                                  */
-  const int32_t* pair;       /* n_pairs x 4 packed                         */
+  int64_t n_entries;
+  int64_t meta_len;          /* int32 values of metadata                   */
+  const int64_t* part_sub_start;   /* n_parts + 1                          */
+  const int64_t* part_entry_start; /* n_parts + 1                          */
+  const int32_t* copies;     /* n_entries x 4                              */
+  const int32_t* meta;       /* meta_len                                   */
 } bmv_mmult_desc;
 
 typedef struct bmv_mmult bmv_mmult;

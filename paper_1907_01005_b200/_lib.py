@@ -44,20 +44,19 @@ class CellopDesc(C.Structure):
 class TmmultDesc(C.Structure):
     _fields_ = [
         ("n_parts", C.c_int32), ("n_warps", C.c_int32), ("slots_per_warp", C.c_int32),
-        ("stage_doubles", C.c_int32), ("n_sub", C.c_int64), ("n_items", C.c_int64),
-        ("n_tri", C.c_int64), ("n_out_tiles", C.c_int64), ("n_src", C.c_int64),
-        ("part_sub_start", _i64p), ("sub_a", _i64p), ("sub_b", _i64p), ("sub_item", _i32p),
-        ("sub_tri_start", _i64p), ("tri", _i32p), ("item_slots", _i32p), ("tile_off", _i64p),
-        ("tile_shape", _i32p), ("tile_src_start", _i64p), ("tile_src", _i64p),
+        ("stage_bytes", C.c_int32), ("n_sub", C.c_int64), ("n_items", C.c_int64),
+        ("n_entries", C.c_int64), ("meta_len", C.c_int64), ("n_out_tiles", C.c_int64),
+        ("n_src", C.c_int64), ("part_sub_start", _i64p), ("part_entry_start", _i64p),
+        ("copies", _i32p), ("meta", _i32p), ("tile_off", _i64p), ("tile_shape", _i32p),
+        ("tile_src_start", _i64p), ("tile_src", _i64p),
     ]
 
 
 class MmultDesc(C.Structure):
     _fields_ = [
-        ("n_parts", C.c_int32), ("stage_doubles", C.c_int32), ("n_sub", C.c_int64),
-        ("n_out", C.c_int64), ("n_pairs", C.c_int64), ("part_sub_start", _i64p),
-        ("sub_a", _i64p), ("sub_tile", _i64p), ("sub_out0", _i64p), ("tile_start", _i64p),
-        ("out_off", _i64p), ("out_shape", _i32p), ("pair_start", _i64p), ("pair", _i32p),
+        ("n_parts", C.c_int32), ("stage_bytes", C.c_int32), ("n_sub", C.c_int64),
+        ("n_entries", C.c_int64), ("meta_len", C.c_int64), ("part_sub_start", _i64p),
+        ("part_entry_start", _i64p), ("copies", _i32p), ("meta", _i32p),
     ]
 
 

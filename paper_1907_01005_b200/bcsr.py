@@ -756,73 +756,133 @@ def mmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n
     pa, pb = pa[order], pb[order]
     n_out = int(outs.size)
     # ---- streaming plan (csrc/bmv_postmul.cu) ------------------------------
+    # stage = [header][tasks (8x8 output tiles)][pairs][B blocks][A blocks]
     n_rows = a.n_owned_blocks
     a_row_lo = a.block_offsets[a.row_start[:n_rows]]
     a_row_hi = a.block_offsets[a.row_start[1 : n_rows + 1]]
     row_dbl = a_row_hi - a_row_lo
-    cap = max(_PJ_STAGE, int(row_dbl.max(initial=0)))
-    cap += cap & 1
-    if 2 * cap * 8 > _SMEM_OPTIN:
-        raise ShapeError(f"mmult block row needs {cap * 8} bytes of shared memory (2 stages)")
+    per = np.repeat(np.arange(n_out), np.diff(start))
     out_row = c.pos_row[outs] if n_out else np.zeros(0, np.int64)
     out_rows = c.local_row_sizes[out_row].astype(np.int64)
     out_cols = c.col_blocks.sizes[c.col_index[outs]].astype(np.int64)
-    tiles = ((out_rows + 7) // 8) * ((out_cols + 7) // 8)
-    tile_start = np.concatenate([[0], np.cumsum(tiles)]).astype(np.int64)
-    # parts balanced by A + Y doubles; sub-chunks of consecutive rows <= _PJ_STAGE
-    y_dbl = np.zeros(n_rows, dtype=np.int64)
-    if n_out:
-        np.add.at(y_dbl, out_row, out_rows * c.col_strides[c.col_index[outs]])
+    c_str = c.col_strides[c.col_index[outs]].astype(np.int64)
+    tm, tn = (out_rows + 7) // 8, (out_cols + 7) // 8
+    if n_out and (int(tn.max()) > 16 or int(c_str.max()) >= 1 << 16):
+        raise ShapeError("mmult output blocks wider than 128 columns are not supported")
+    # B is staged as spans of its block rows: per (sub-chunk, block row k of
+    # B) the positions [first, last] the sub-chunk's products use
+    pair_row = out_row[per] if pa.size else np.zeros(0, np.int64)
+    kb = b.pos_row[pb].astype(np.int64)
+    nkb = int(b.pos_row.max(initial=0)) + 2
+
+    def spans(group):
+        key = group * nkb + kb
+        uk, inv = np.unique(key, return_inverse=True)
+        lo = np.full(uk.size, np.iinfo(np.int64).max)
+        hi = np.full(uk.size, -1)
+        np.minimum.at(lo, inv, pb)
+        np.maximum.at(hi, inv, pb)
+        nbytes = 8 * (b.block_offsets[hi + 1] - b.block_offsets[lo])
+        return uk // nkb, lo, hi, nbytes + nbytes % 16, inv
+
+    r_grp, _, _, r_bytes, _ = spans(pair_row)
+    row_cb = np.bincount(r_grp, minlength=n_rows).astype(np.int64)
+    row_cbytes = np.bincount(r_grp, weights=r_bytes, minlength=n_rows).astype(np.int64)
+    row_tasks = np.bincount(out_row, weights=tm * tn, minlength=n_rows).astype(np.int64)
+    row_pairs = np.bincount(pair_row, minlength=n_rows).astype(np.int64)
+    row_bytes = 8 * row_dbl + 16 * (row_tasks + row_pairs) + row_cbytes
+    if n_rows and int(row_cb.max()) > _CP_MAX - 2:
+        raise ShapeError("mmult block row uses more than 30 block rows of b")
+    # parts balanced by A + Y doubles; sub-chunks of consecutive rows
+    y_dbl = np.bincount(out_row, weights=out_rows * c_str, minlength=n_rows).astype(np.int64)
     w = row_dbl + y_dbl
     n_parts = max(1, min(int(n_parts), n_rows))
     total = max(int(w.sum()), 1)
     before = np.concatenate([[0], np.cumsum(w)[:-1]]) if n_rows else np.zeros(0, np.int64)
     r_part = np.minimum(before * n_parts // total, n_parts - 1)
     r_sub = np.empty(n_rows, dtype=np.int64)
-    sid, acc = -1, 0
-    dl, pl = row_dbl.tolist(), r_part.tolist()
+    sid, acc, cacc = -1, 0, 0
+    bl, cl, pl = row_bytes.tolist(), row_cb.tolist(), r_part.tolist()
     for j in range(n_rows):
-        if sid < 0 or pl[j] != pl[j - 1] or acc + dl[j] > _PJ_STAGE:
+        if (sid < 0 or pl[j] != pl[j - 1] or acc + bl[j] > _PM_STAGE_BYTES - 16
+                or cacc + cl[j] > _CP_MAX - 2):
             sid += 1
-            acc = 0
-        acc += dl[j]
+            acc = cacc = 0
+        acc += bl[j]
+        cacc += cl[j]
         r_sub[j] = sid
     n_sub = sid + 1
     first_r = np.searchsorted(r_sub, np.arange(n_sub + 1)).astype(np.int64)
     sub_a = np.stack([a_row_lo[first_r[:-1]], a_row_hi[first_r[1:] - 1]], 1) if n_sub \
         else np.zeros((0, 2), np.int64)
     part_sub_start = np.searchsorted(r_part[first_r[:-1]], np.arange(n_parts + 1)).astype(np.int64)
-    # outputs are in row order: the sub-chunk's outputs are one range
-    o_lo = np.searchsorted(out_row, first_r[:-1])
+    o_lo = np.searchsorted(out_row, first_r[:-1])       # outputs are in row order
     o_hi = np.searchsorted(out_row, first_r[1:])
-    sub_tile = np.stack([tile_start[o_lo], tile_start[o_hi]], 1)
-    sub_out0 = np.minimum(o_lo, max(n_out - 1, 0))
-    pair_sub = r_sub[a.pos_row[pa]] if pa.size else np.zeros(0, np.int64)
-    b_off = b.block_offsets[pb].astype(np.int64)
-    if b_off.size and int(b_off.max()) >= 1 << 31:
-        raise ShapeError("mmult b holds more than 2^31 values")
+    o_sub = r_sub[out_row]
+    # tasks: the 8x8 tiles of every output block, in (block, row tile, col tile) order
+    to, tq = _expand(tm * tn)
+    t_mi, t_ni = tq // tn[to], tq % tn[to]
+    t_sub = o_sub[to]
+    n_tasks_sub = np.bincount(t_sub, minlength=n_sub).astype(np.int64)
+    n_pairs_sub = (start[o_hi] - start[o_lo]).astype(np.int64)
+    # B spans per sub-chunk, staged after the metadata
+    p_sub = o_sub[per] if pa.size else np.zeros(0, np.int64)
+    cb_sub, cb_lo, cb_hi, cb_bytes, p_cb = spans(p_sub)
+    n_cb_sub = np.bincount(cb_sub, minlength=n_sub).astype(np.int64)
+    meta_bytes = 16 * (1 + n_tasks_sub + n_pairs_sub)
+    cb_first = np.concatenate([[0], np.cumsum(n_cb_sub)]).astype(np.int64)
+    cb_cum = np.concatenate([[0], np.cumsum(cb_bytes)]).astype(np.int64)
+    cb_soff = meta_bytes[cb_sub] + cb_cum[:-1] - cb_cum[cb_first[cb_sub]]
+    a_off = meta_bytes + cb_cum[cb_first[1:]] - cb_cum[cb_first[:-1]]
+    na_sub = sub_a[:, 1] - sub_a[:, 0]
+    stage_bytes = int((a_off + 8 * na_sub).max(initial=16))
+    stage_bytes += (-stage_bytes) % 16
+    if 2 * stage_bytes > _SMEM_OPTIN - 1024:
+        raise ShapeError(f"mmult block row needs {stage_bytes} bytes of shared memory (2 stages)")
+    # metadata: header, tasks, pairs per sub-chunk
+    meta_off = np.concatenate([[0], np.cumsum(meta_bytes // 4)]).astype(np.int64)
+    meta = np.zeros(int(meta_off[-1]), dtype=np.int64)
+    meta[meta_off[:-1]] = n_tasks_sub
+    task_first = np.concatenate([[0], np.cumsum(n_tasks_sub)]).astype(np.int64)
+    tpos = meta_off[t_sub] + 4 * (1 + np.arange(to.size) - task_first[t_sub])
+    t_off = c.block_offsets[outs][to] + 8 * t_mi * c_str[to] + 8 * t_ni
+    if t_off.size and int(t_off.max()) >= 1 << 32:
+        raise ShapeError("mmult output holds more than 2^32 values")
+    meta[tpos] = t_off
+    meta[tpos + 1] = (np.minimum(8, out_rows[to] - 8 * t_mi) | (np.minimum(8, out_cols[to] - 8 * t_ni) << 4)
+                      | (t_ni << 8) | (c_str[to] << 16))
+    np_o = np.diff(start)
+    meta[tpos + 2] = (start[to] - start[o_lo[t_sub]]) | (np_o[to] << 16)
+    meta[tpos + 3] = t_mi
+    if np_o.size and int(max(np_o.max(), n_pairs_sub.max(initial=0))) >= 1 << 16:
+        raise ShapeError("mmult sub-chunk holds more than 65535 products")
     a_str = a.col_strides[a.col_index[pa]].astype(np.int64)
     inner = a.col_blocks.sizes[a.col_index[pa]].astype(np.int64)
-    pair = np.empty((pa.size, 4), dtype=np.int64)
-    pair[:, 0] = a.block_offsets[pa] - sub_a[pair_sub, 0] if pa.size else 0
-    pair[:, 1] = a_str | (inner << 16)
-    pair[:, 2] = b.col_strides[b.col_index[pb]]
-    pair[:, 3] = b_off
-    c_str = c.col_strides[c.col_index[outs]].astype(np.int64)
-    out_shape = np.stack([out_rows, out_cols, c_str, np.zeros_like(c_str)], 1)
+    ppos = meta_off[p_sub] + 4 * (1 + n_tasks_sub[p_sub] + np.arange(pa.size) - start[o_lo[p_sub]])
+    meta[ppos] = a_off[p_sub] // 8 + a.block_offsets[pa] - sub_a[p_sub, 0]
+    meta[ppos + 1] = a_str | (inner << 16)
+    meta[ppos + 2] = b.col_strides[b.col_index[pb]]
+    meta[ppos + 3] = cb_soff[p_cb] // 8 + b.block_offsets[pb] - b.block_offsets[cb_lo[p_cb]]
+    meta = (meta & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+    # copy lists: metadata, B blocks, A range (last)
+    n_ent = 2 + n_cb_sub
+    e_first = np.concatenate([[0], np.cumsum(n_ent)]).astype(np.int64)
+    copies = np.zeros((int(e_first[-1]), 4), dtype=np.int64)
+    copies[e_first[:-1], 1] = meta_bytes
+    copies[e_first[:-1], 2] = 4 * meta_off[:-1]
+    cpos = e_first[cb_sub] + 1 + np.arange(cb_sub.size) - cb_first[cb_sub]
+    copies[cpos, 0] = cb_soff
+    copies[cpos, 1] = 8 * (b.block_offsets[cb_hi + 1] - b.block_offsets[cb_lo]) | (2 << 28)
+    copies[cpos, 2] = 8 * b.block_offsets[cb_lo]
+    last = e_first[1:] - 1
+    copies[last, 0] = a_off
+    copies[last, 1] = 8 * na_sub | (1 << 28) | (1 << 30)
+    copies[last, 2] = 8 * sub_a[:, 0]
     arrays = dict(
-        n_parts=n_parts, stage_doubles=cap, n_sub=n_sub,
-        part_sub_start=part_sub_start,
-        sub_a=np.ascontiguousarray(sub_a, dtype=np.int64).ravel(),
-        sub_tile=np.ascontiguousarray(sub_tile, dtype=np.int64).ravel(),
-        sub_out0=sub_out0.astype(np.int64),
-        tile_start=tile_start,
-        out_off=c.block_offsets[outs].astype(np.int64),
-        out_shape=np.ascontiguousarray(out_shape, dtype=np.int32).ravel(),
-        pair_start=start.astype(np.int64),
-        pair=np.ascontiguousarray(pair.astype(np.int32)).ravel(),
+        n_parts=n_parts, stage_bytes=stage_bytes, n_sub=n_sub,
+        part_sub_start=part_sub_start, part_entry_start=e_first[part_sub_start],
+        copies=_pack_copies(copies), meta=meta,
     )
-    per = np.repeat(np.arange(n_out), np.diff(start))
     flops = int(2 * np.sum(out_rows[per] * inner * out_cols[per]))
     n_own_c = int(c.row_start[c.n_owned_blocks])
     own_cols = c.col_index[:n_own_c]
@@ -842,13 +902,12 @@ class _MmultPlan:
         lib = _lib.load()
         d = _lib.MmultDesc()
         d.n_parts = int(arrays["n_parts"])
-        d.stage_doubles = int(arrays["stage_doubles"])
-        d.n_sub, d.n_out, d.n_pairs = int(arrays["n_sub"]), n_out, n_pairs
-        for name, ct in (("part_sub_start", _lib.C.c_int64), ("sub_a", _lib.C.c_int64),
-                         ("sub_tile", _lib.C.c_int64), ("sub_out0", _lib.C.c_int64),
-                         ("tile_start", _lib.C.c_int64), ("out_off", _lib.C.c_int64),
-                         ("out_shape", _lib.C.c_int32), ("pair_start", _lib.C.c_int64),
-                         ("pair", _lib.C.c_int32)):
+        d.stage_bytes = int(arrays["stage_bytes"])
+        d.n_sub = int(arrays["n_sub"])
+        d.n_entries = int(arrays["copies"].size // 4)
+        d.meta_len = int(arrays["meta"].size)
+        for name, ct in (("part_sub_start", _lib.C.c_int64), ("part_entry_start", _lib.C.c_int64),
+                         ("copies", _lib.C.c_int32), ("meta", _lib.C.c_int32)):
             arrays[name] = np.ascontiguousarray(arrays[name])
             setattr(d, name, _lib.ptr(arrays[name], ct))
         raw = _lib.C.c_void_p()
@@ -1096,21 +1155,49 @@ def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, 
     t_mr, t_mc = mr[tri][o], mc[tri][o]
     sub_tri_start = np.searchsorted(t_sub * _PJ_WARPS + t_warp,
                                     np.arange(n_sub * _PJ_WARPS + 1)).astype(np.int64)
+    # per sub-chunk: stage = [header][triple tiles][A][B]; metadata = header + tiles
+    n_tri_sub = np.bincount(t_sub, minlength=n_sub).astype(np.int64)
     na_sub = sub_a[:, 1] - sub_a[:, 0]
-    a_soff = a.block_offsets[t_pa] - sub_a[t_sub, 0] + 8 * mt
-    b_soff = (na_sub + (na_sub & 1))[t_sub] + b.block_offsets[t_pb] - sub_b[t_sub, 0] + 8 * nt
+    nb_sub = sub_b[:, 1] - sub_b[:, 0]
+    a_off = _PJ_HDR + 16 * n_tri_sub                       # bytes
+    b_off = a_off + 8 * (na_sub + (na_sub & 1))
+    stage_end = b_off + 8 * nb_sub
+    stage_bytes = int(max(int(stage_end.max(initial=0)), _PJ_HDR))
+    stage_bytes += (-stage_bytes) % 16
+    t_first = sub_tri_start[t_sub * _PJ_WARPS]
+    a_soff = a_off[t_sub] // 8 + a.block_offsets[t_pa] - sub_a[t_sub, 0] + 8 * mt
+    b_soff = b_off[t_sub] // 8 + b.block_offsets[t_pb] - sub_b[t_sub, 0] + 8 * nt
     acols = np.minimum(8, t_mr - 8 * mt)
     bcols = np.minimum(8, t_mc - 8 * nt)
     a_str = a.col_strides[a.col_index[t_pa]].astype(np.int64)
     b_str = b.col_strides[b.col_index[t_pb]].astype(np.int64)
     if t_rows.size and (int(t_rows.max()) >= 1 << 16 or int(max(a_str.max(), b_str.max())) >= 1 << 16):
         raise ShapeError("tmmult block rows / strides exceed 65535")
-    packed = np.empty((t_key.size, 4), dtype=np.int64)
-    packed[:, 0] = a_soff
-    packed[:, 1] = b_soff
-    packed[:, 2] = t_rows | (t_slot << 16) | (acols << 24) | (bcols << 28)
-    packed[:, 3] = a_str | (b_str << 16)
-    packed = (packed & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+    meta_len_sub = _PJ_HDR // 4 + 4 * n_tri_sub          # int32 values
+    meta_off = np.concatenate([[0], np.cumsum(meta_len_sub)]).astype(np.int64)
+    meta = np.zeros(int(meta_off[-1]), dtype=np.int64)
+    hdr = np.zeros((n_sub, _PJ_HDR // 4), dtype=np.int64)
+    sts = sub_tri_start[:-1].reshape(n_sub, _PJ_WARPS) if n_sub else np.zeros((0, _PJ_WARPS), np.int64)
+    hdr[:, :_PJ_WARPS] = sts - sts[:, :1]
+    hdr[:, _PJ_WARPS] = n_tri_sub
+    hdr[:, 17] = sub_item
+    hdr[:, 18] = np.concatenate([sub_item[1:] != sub_item[:-1], [True]]) if n_sub else 0
+    hdr[:, 20:20 + _PJ_WARPS] = item_slots[sub_item] if n_sub else 0
+    meta[(meta_off[:-1, None] + np.arange(_PJ_HDR // 4)[None, :]).ravel()] = hdr.ravel()
+    rowpos = meta_off[t_sub] + _PJ_HDR // 4 + 4 * (np.arange(t_sub.size) - t_first)
+    meta[rowpos] = a_soff
+    meta[rowpos + 1] = b_soff
+    meta[rowpos + 2] = t_rows | (t_slot << 16) | (acols << 24) | (bcols << 28)
+    meta[rowpos + 3] = a_str | (b_str << 16)
+    meta = (meta & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+    # copy lists: metadata, A range, B range
+    copies = np.zeros((n_sub, 3, 4), dtype=np.int64)
+    copies[:, 0, 1], copies[:, 0, 2] = 4 * meta_len_sub, 4 * meta_off[:-1]
+    copies[:, 1, 0], copies[:, 1, 1], copies[:, 1, 2] = a_off, 8 * na_sub | (1 << 28), 8 * sub_a[:, 0]
+    copies[:, 2, 0], copies[:, 2, 1], copies[:, 2, 2] = b_off, 8 * nb_sub | (2 << 28) | (1 << 30), \
+        8 * sub_b[:, 0]
+    copies = _pack_copies(copies.reshape(-1, 4))
+    part_entry_start = 3 * part_sub_start
     # output tiles and their partial sources (item order)
     tiles, tinv = np.unique(uik % (int(t_key.max(initial=0)) + 1), return_inverse=True)
     src_order = np.lexsort((it_item, tinv))
@@ -1122,14 +1209,9 @@ def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, 
     tr = np.minimum(8, c.local_row_sizes[c.pos_row[tcp]] - 8 * tmt)
     tc = np.minimum(8, c.col_blocks.sizes[c.col_index[tcp]] - 8 * tnt)
     arrays = dict(
-        n_parts=n_parts, stage_doubles=cap, n_sub=n_sub, n_items=n_items,
-        part_sub_start=part_sub_start,
-        sub_a=np.ascontiguousarray(sub_a, dtype=np.int64).ravel(),
-        sub_b=np.ascontiguousarray(sub_b, dtype=np.int64).ravel(),
-        sub_item=sub_item.astype(np.int32),
-        sub_tri_start=sub_tri_start,
-        tri=np.ascontiguousarray(packed).ravel(),
-        item_slots=np.ascontiguousarray(item_slots).ravel(),
+        n_parts=n_parts, stage_bytes=stage_bytes, n_sub=n_sub, n_items=n_items,
+        part_sub_start=part_sub_start, part_entry_start=part_entry_start,
+        copies=copies, meta=meta,
         tile_off=tile_off.astype(np.int64),
         tile_shape=np.ascontiguousarray(np.stack([tr, tc, c_str], 1), dtype=np.int32).ravel(),
         tile_src_start=tile_src_start,
@@ -1141,10 +1223,29 @@ def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, 
     return arrays, flops
 
 
-_PJ_WARPS = 8        # consumer warps per CTA (bmv_project.cu kPjWarps)
-_PJ_SLOTS = 16       # accumulator tiles per warp (kPjSlots)
+_PJ_WARPS = 16       # consumer warps per CTA (bmv_project.cu kPjWarps)
+_PJ_SLOTS = 8        # accumulator tiles per warp (kPjSlots)
 _PJ_TILES = _PJ_WARPS * _PJ_SLOTS
-_PJ_STAGE = 4864     # doubles per pipeline stage (38 KB: 4 stages + 64 KB of slots per SM)
+_PJ_HDR = 144        # bytes of the K4 stage header (kPjHeader)
+# A + B doubles per K4 stage: 40 KB stages (header + <= 128 triple tiles
+# included) -> 4 stages + 64 KB of accumulator slots per SM
+_PJ_STAGE = (40960 - _PJ_HDR - 16 * _PJ_TILES) // 8
+_PM_STAGE_BYTES = 40960   # K5 stage target (5 stages per SM)
+_CP_MAX = 32              # copy entries per sub-chunk (kCpMaxPerSub)
+
+
+def _pack_copies(entries: np.ndarray) -> np.ndarray:
+    """int64 (n, 4) {dst, bytes | src << 28 | last << 30, src byte offset, 0}
+    -> the C-ABI copy entries (n x 4 int32, source offset split lo / hi)."""
+    out = np.empty((entries.shape[0], 4), dtype=np.int64)
+    out[:, 0] = entries[:, 0]
+    out[:, 1] = entries[:, 1]
+    out[:, 2] = entries[:, 2] & 0xFFFFFFFF
+    out[:, 3] = entries[:, 2] >> 32
+    if entries.size and (int(entries[:, 0].max()) >= 1 << 31 or
+                         int((entries[:, 1] & ((1 << 28) - 1)).max()) >= 1 << 28):
+        raise ShapeError("stage copy out of range")
+    return np.ascontiguousarray((out & 0xFFFFFFFF).astype(np.uint32).view(np.int32)).ravel()
 
 
 def _pj_parts(device) -> int:
@@ -1162,17 +1263,16 @@ class _TmmultPlan:
         d = _lib.TmmultDesc()
         d.n_parts = int(arrays["n_parts"])
         d.n_warps, d.slots_per_warp = _PJ_WARPS, _PJ_SLOTS
-        d.stage_doubles = int(arrays["stage_doubles"])
+        d.stage_bytes = int(arrays["stage_bytes"])
         d.n_sub, d.n_items = int(arrays["n_sub"]), int(arrays["n_items"])
-        d.n_tri = int(arrays["tri"].size // 4)
+        d.n_entries = int(arrays["copies"].size // 4)
+        d.meta_len = int(arrays["meta"].size)
         d.n_out_tiles = int(arrays["tile_off"].size)
         d.n_src = int(arrays["tile_src"].size)
-        for name, ct in (("part_sub_start", _lib.C.c_int64), ("sub_a", _lib.C.c_int64),
-                         ("sub_b", _lib.C.c_int64), ("sub_item", _lib.C.c_int32),
-                         ("sub_tri_start", _lib.C.c_int64), ("tri", _lib.C.c_int32),
-                         ("item_slots", _lib.C.c_int32), ("tile_off", _lib.C.c_int64),
-                         ("tile_shape", _lib.C.c_int32), ("tile_src_start", _lib.C.c_int64),
-                         ("tile_src", _lib.C.c_int64)):
+        for name, ct in (("part_sub_start", _lib.C.c_int64), ("part_entry_start", _lib.C.c_int64),
+                         ("copies", _lib.C.c_int32), ("meta", _lib.C.c_int32),
+                         ("tile_off", _lib.C.c_int64), ("tile_shape", _lib.C.c_int32),
+                         ("tile_src_start", _lib.C.c_int64), ("tile_src", _lib.C.c_int64)):
             arrays[name] = np.ascontiguousarray(arrays[name])
             setattr(d, name, _lib.ptr(arrays[name], ct))
         raw = _lib.C.c_void_p()

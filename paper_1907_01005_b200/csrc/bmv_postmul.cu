@@ -26,33 +26,54 @@ using namespace bmv;
 
 namespace {
 
-constexpr int kPmWarps = 8;
+constexpr int kPmWarps = 16;
 constexpr int kPmThreads = (kPmWarps + 1) * 32;
 constexpr int kPmMaxStages = 8;
-constexpr int kPmPiece = 4096;
 
 struct PmArgs {
   const int64_t* __restrict__ part_sub_start;
-  const int64_t* __restrict__ sub_a;     // [lo, hi) per sub-chunk
-  const int64_t* __restrict__ sub_tile;  // [t0, t1) per sub-chunk
-  const int64_t* __restrict__ sub_out0;  // first output block of the sub-chunk
-  const int64_t* __restrict__ tile_start;  // n_out + 1
-  const int64_t* __restrict__ out_off;
-  const int4* __restrict__ out_shape;    // rows, cols, stride, -
-  const int64_t* __restrict__ pair_start;
-  const int4* __restrict__ pair;         // a_soff, a_stride | inner << 16, b_stride, b_off
-  const double* __restrict__ a;
-  const double* __restrict__ b;
+  const int64_t* __restrict__ part_entry_start;
+  const int4* __restrict__ copies;
+  CopySrc src;  // p0 = meta, p1 = a, p2 = b
   double* __restrict__ c;
   double alpha;
   int accumulate;
-  int stage_doubles;
+  int stage_bytes;
   int n_stages;
-  int bulk_ok;
 };
 
+// One 8x8 output tile: sum over its pairs of A(8 rows x inner) B(inner x 8),
+// all operands in the stage.  Lane (gid, tig) returns D[gid][2 tig + {0,1}].
+__device__ __forceinline__ void task_tile(const double* S, const int4* pairs, const int4 t,
+                                          int gid, int tig, double& x, double& y) {
+  const int rv = t.y & 15, cv = (t.y >> 4) & 15, ni = (t.y >> 8) & 15;
+  const int p0 = t.z & 0xffff, np = (t.z >> 16) & 0xffff;
+  const bool am = gid < rv, bm = gid < cv;
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+  for (int p = p0; p < p0 + np; ++p) {
+    const int4 d = pairs[p];
+    const int as = d.y & 0xffff, inner = (d.y >> 16) & 0xffff, bs = d.z;
+    const double* A = S + d.x + (8 * t.w + gid) * as + tig;
+    const double* B = S + d.w + tig * bs + 8 * ni + gid;
+    int k0 = 0;
+    for (; k0 + 8 <= inner; k0 += 8) {
+      const double a0 = am ? A[k0] : 0.0, a1 = am ? A[k0 + 4] : 0.0;
+      const double b0 = bm ? B[k0 * bs] : 0.0, b1 = bm ? B[(k0 + 4) * bs] : 0.0;
+      dmma_8x8x4(c0, c1, a0, b0);
+      dmma_8x8x4(c2, c3, a1, b1);
+    }
+    for (; k0 < inner; k0 += 4) {
+      const bool ok = k0 + tig < inner;
+      const double a0 = (am && ok) ? A[k0] : 0.0, b0 = (bm && ok) ? B[k0 * bs] : 0.0;
+      dmma_8x8x4(c0, c1, a0, b0);
+    }
+  }
+  x = c0 + c2;
+  y = c1 + c3;
+}
+
 __global__ void __launch_bounds__(kPmThreads, 1) pm_stream_kernel(const PmArgs g) {
-  extern __shared__ __align__(128) double stages[];
+  extern __shared__ __align__(128) char stages[];
   __shared__ __align__(8) uint64_t full[kPmMaxStages], empty[kPmMaxStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t s0 = g.part_sub_start[blockIdx.x], s1 = g.part_sub_start[blockIdx.x + 1];
@@ -65,74 +86,33 @@ __global__ void __launch_bounds__(kPmThreads, 1) pm_stream_kernel(const PmArgs g
   }
   __syncthreads();
 
-  if (warp == kPmWarps) {  // producer
-    for (int64_t s = s0; s < s1; ++s) {
-      const int64_t i = s - s0;
-      const int st = (int)(i % NS);
-      if (i >= NS) mbar_wait(&empty[st], (unsigned)((i / NS - 1) & 1));
-      double* dst = stages + (int64_t)st * g.stage_doubles;
-      const int64_t alo = g.sub_a[2 * s], ahi = g.sub_a[2 * s + 1];
-      const int na = (int)(ahi - alo);
-      if (g.bulk_ok && ((alo | ahi) & 1) == 0) {
-        if (lane == 0) {
-          mbar_expect_tx(&full[st], (unsigned)na * 8u);
-          for (int k = 0; k < na; k += kPmPiece)
-            bulk_g2s(dst + k, g.a + alo + k, (unsigned)min(kPmPiece, na - k) * 8u, &full[st]);
-        }
-      } else {
-        for (int k = lane; k < na; k += 32) dst[k] = __ldg(g.a + alo + k);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[st]);
-      }
-    }
+  if (warp == kPmWarps) {
+    stream_producer(g.copies, g.part_entry_start[blockIdx.x], g.part_entry_start[blockIdx.x + 1],
+                    s1 - s0, g.src, stages, g.stage_bytes, NS, full, empty, lane);
     return;
   }
 
   const int gid = lane >> 2, tig = lane & 3;
-  for (int64_t s = s0; s < s1; ++s) {
-    const int64_t i = s - s0;
+  for (int64_t i = 0; i < s1 - s0; ++i) {
     const int st = (int)(i % NS);
     mbar_wait(&full[st], (unsigned)((i / NS) & 1));
-    const double* S = stages + (int64_t)st * g.stage_doubles;
-    const int64_t t1 = g.sub_tile[2 * s + 1];
-    int64_t o = g.sub_out0[s];
-    int64_t o_end = g.tile_start[o + 1];
-    for (int64_t t = g.sub_tile[2 * s] + warp; t < t1; t += kPmWarps) {
-      while (o_end <= t) o_end = g.tile_start[++o + 1];
-      const int4 shp = __ldg(g.out_shape + o);
-      const int rows = shp.x, cols = shp.y, ys = shp.z;
-      const int tn = (cols + 7) >> 3;
-      const int mt = (int)(t - g.tile_start[o]);
-      const int mi = mt / tn, ni = mt - mi * tn;
-      const int r = 8 * mi + gid, cb = 8 * ni + gid;
-      const bool rv = r < rows, cv = cb < cols;
-      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-      const int64_t p1 = g.pair_start[o + 1];
-      for (int64_t p = g.pair_start[o]; p < p1; ++p) {
-        const int4 d = __ldg(g.pair + p);
-        const int as = d.y & 0xffff, inner = (d.y >> 16) & 0xffff, bs = d.z;
-        const double* A = S + d.x + r * as + tig;
-        const double* B = g.b + (uint32_t)d.w + (int64_t)tig * bs + cb;
-        int k0 = 0;
-        for (; k0 + 8 <= inner; k0 += 8) {
-          const double a0 = rv ? A[k0] : 0.0, a1 = rv ? A[k0 + 4] : 0.0;
-          const double b0 = cv ? __ldg(B + (int64_t)k0 * bs) : 0.0;
-          const double b1 = cv ? __ldg(B + (int64_t)(k0 + 4) * bs) : 0.0;
-          dmma_8x8x4(c0, c1, a0, b0);
-          dmma_8x8x4(c2, c3, a1, b1);
-        }
-        for (; k0 < inner; k0 += 4) {
-          const bool ok = k0 + tig < inner;
-          const double a0 = (rv && ok) ? A[k0] : 0.0;
-          const double b0 = (cv && ok) ? __ldg(B + (int64_t)k0 * bs) : 0.0;
-          dmma_8x8x4(c0, c1, a0, b0);
-        }
-      }
-      const int col = 8 * ni + 2 * tig;
-      if (rv && col < cols) {
-        double* Y = g.c + g.out_off[o] + (int64_t)r * ys + col;
-        double x = g.alpha * (c0 + c2), y = g.alpha * (c1 + c3);
-        const bool two = col + 1 < cols;
+    const char* stg = stages + (int64_t)st * g.stage_bytes;
+    const int4* meta = reinterpret_cast<const int4*>(stg);
+    const double* S = reinterpret_cast<const double*>(stg);
+    const int n_tasks = meta[0].x;
+    const int4* tasks = meta + 1;
+    const int4* pairs = meta + 1 + n_tasks;
+    for (int k = warp; k < n_tasks; k += kPmWarps) {
+      const int4 t = tasks[k];
+      double x, y;
+      task_tile(S, pairs, t, gid, tig, x, y);
+      const int rv = t.y & 15, cv = (t.y >> 4) & 15, ys = (t.y >> 16) & 0xffff;
+      const int col = 2 * tig;
+      if (gid < rv && col < cv) {
+        double* Y = g.c + (uint32_t)t.x + (int64_t)gid * ys + col;
+        x *= g.alpha;
+        y *= g.alpha;
+        const bool two = col + 1 < cv;
         if (two && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0)) {
           double2* Y2 = reinterpret_cast<double2*>(Y);
           if (g.accumulate) {
@@ -155,19 +135,99 @@ __global__ void __launch_bounds__(kPmThreads, 1) pm_stream_kernel(const PmArgs g
 }  // namespace
 
 struct bmv_mmult {
-  int n_parts = 0, stage_doubles = 0, n_stages = 0, smem_bytes = 0;
-  int64_t n_sub = 0, n_out = 0, n_pairs = 0;
-  int64_t *part_sub_start = nullptr, *sub_a = nullptr, *sub_tile = nullptr, *sub_out0 = nullptr,
-          *tile_start = nullptr, *out_off = nullptr, *pair_start = nullptr;
-  int32_t *out_shape = nullptr, *pair = nullptr;
+  int n_parts = 0, stage_bytes = 0, n_stages = 0, smem_bytes = 0;
+  int64_t n_sub = 0, c_extent = 0;
+  int64_t *part_sub_start = nullptr, *part_entry_start = nullptr;
+  int32_t *copies = nullptr, *meta = nullptr;
 };
+
+namespace {
+
+int validate_mmult(const bmv_mmult_desc* d, int64_t* c_extent) {
+  const int64_t meta_bytes = d->meta_len * 4;
+  *c_extent = 0;
+  if (d->n_parts > 0 && (d->part_sub_start[0] != 0 || d->part_sub_start[d->n_parts] != d->n_sub ||
+                         d->part_entry_start[0] != 0 || d->part_entry_start[d->n_parts] != d->n_entries)) {
+    set_error("mmult part ranges do not cover the sub-chunks / copies");
+    return BMV_ERR_INVALID;
+  }
+  for (int p = 0; p < d->n_parts; ++p) {
+    int64_t e = d->part_entry_start[p];
+    const int64_t e1 = d->part_entry_start[p + 1];
+    for (int64_t s = d->part_sub_start[p]; s < d->part_sub_start[p + 1]; ++s) {
+      const int64_t first = e;
+      for (;; ++e) {
+        if (e >= e1 || e - first >= kCpMaxPerSub) {
+          set_error("mmult copy list of sub-chunk %lld is malformed", (long long)s);
+          return BMV_ERR_INVALID;
+        }
+        const int32_t* q = d->copies + 4 * e;
+        const unsigned y = (unsigned)q[1];
+        const int64_t len = y & kCpLenMask, sel = (y >> 28) & 3;
+        const int64_t src = ((int64_t)(uint32_t)q[3] << 32) | (uint32_t)q[2];
+        if (q[0] < 0 || q[0] + len > d->stage_bytes || sel > 2 || src < 0 ||
+            (sel == 0 && src + len > meta_bytes)) {
+          set_error("mmult copy entry %lld out of range", (long long)e);
+          return BMV_ERR_INVALID;
+        }
+        if (e == first) {
+          if (sel != 0 || q[0] != 0 || len < 16 || (src & 15)) {
+            set_error("mmult sub-chunk %lld does not start with its header", (long long)s);
+            return BMV_ERR_INVALID;
+          }
+          const int32_t* m = d->meta + src / 4;
+          const int nt = m[0];
+          if (nt < 0 || 16 * (1 + (int64_t)nt) > len) {
+            set_error("mmult header of sub-chunk %lld is malformed", (long long)s);
+            return BMV_ERR_INVALID;
+          }
+          const int64_t n_pairs = len / 16 - 1 - nt;
+          for (int k = 0; k < nt; ++k) {
+            const int32_t* t = m + 4 * (1 + k);
+            const int rv = t[1] & 15, cv = (t[1] >> 4) & 15, ni = (t[1] >> 8) & 15;
+            const int ys = ((unsigned)t[1] >> 16) & 0xffff;
+            const int p0 = t[2] & 0xffff, np = ((unsigned)t[2] >> 16) & 0xffff;
+            if (rv > 8 || cv > 8 || p0 + np > n_pairs || t[3] < 0) {
+              set_error("mmult task %d of sub-chunk %lld out of range", k, (long long)s);
+              return BMV_ERR_INVALID;
+            }
+            if (rv > 0 && cv > 0)
+              *c_extent = std::max<int64_t>(*c_extent, (int64_t)(uint32_t)t[0] + (int64_t)(rv - 1) * ys + cv);
+            for (int pp = p0; pp < p0 + np; ++pp) {
+              const int32_t* q4 = m + 4 * (1 + nt + pp);
+              const int as = q4[1] & 0xffff, inner = ((unsigned)q4[1] >> 16) & 0xffff, bs = q4[2];
+              const int64_t a_end = 8 * ((int64_t)q4[0] + (int64_t)(8 * t[3] + rv - 1) * as + inner);
+              const int64_t b_end = 8 * ((int64_t)q4[3] + (int64_t)(inner - 1) * bs + 8 * ni + cv);
+              if (q4[0] < 0 || q4[3] < 0 || bs < 0 ||
+                  (rv > 0 && inner > 0 && a_end > d->stage_bytes) ||
+                  (cv > 0 && inner > 0 && b_end > d->stage_bytes)) {
+                set_error("mmult pair %d of sub-chunk %lld out of range", pp, (long long)s);
+                return BMV_ERR_INVALID;
+              }
+            }
+          }
+        }
+        if ((y >> 30) & 1) {
+          ++e;
+          break;
+        }
+      }
+    }
+    if (e != e1) {
+      set_error("mmult part %d has stray copy entries", p);
+      return BMV_ERR_INVALID;
+    }
+  }
+  return BMV_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
 int bmv_mmult_destroy(bmv_mmult* p) {
   if (!p) return BMV_OK;
-  void* ptrs[] = {p->part_sub_start, p->sub_a,     p->sub_tile,  p->sub_out0, p->tile_start,
-                  p->out_off,        p->pair_start, p->out_shape, p->pair};
+  void* ptrs[] = {p->part_sub_start, p->part_entry_start, p->copies, p->meta};
   for (void* q : ptrs) release(q);
   delete p;
   return BMV_OK;
@@ -176,69 +236,33 @@ int bmv_mmult_destroy(bmv_mmult* p) {
 int bmv_mmult_create(const bmv_mmult_desc* d, bmv_mmult** out) {
   if (!out) return BMV_ERR_INVALID;
   *out = nullptr;
-  if (!d || d->n_parts < 0 || d->n_sub < 0 || d->n_out < 0 || d->n_pairs < 0 ||
-      d->stage_doubles < 2 || (d->stage_doubles & 1)) {
+  if (!d || d->n_parts < 0 || d->n_sub < 0 || d->n_entries < 0 || d->meta_len < 0 ||
+      d->stage_bytes < 16 || (d->stage_bytes & 15)) {
     set_error("invalid mmult descriptor");
     return BMV_ERR_INVALID;
   }
-  if (d->n_parts > 0 && (d->part_sub_start[0] != 0 || d->part_sub_start[d->n_parts] != d->n_sub)) {
-    set_error("mmult part ranges do not cover the sub-chunks");
-    return BMV_ERR_INVALID;
-  }
-  const int64_t n_tiles = d->n_out > 0 ? d->tile_start[d->n_out] : 0;
-  for (int64_t s = 0; s < d->n_sub; ++s) {
-    const int64_t na = d->sub_a[2 * s + 1] - d->sub_a[2 * s];
-    const int64_t t0 = d->sub_tile[2 * s], t1 = d->sub_tile[2 * s + 1];
-    if (na < 0 || na > d->stage_doubles || t0 > t1 || t1 > n_tiles ||
-        (t1 > t0 && (d->sub_out0[s] < 0 || d->sub_out0[s] >= d->n_out ||
-                     d->tile_start[d->sub_out0[s]] > t0))) {
-      set_error("mmult sub-chunk %lld is inconsistent", (long long)s);
-      return BMV_ERR_INVALID;
-    }
-  }
-  for (int64_t o = 0; o < d->n_out; ++o) {
-    const int32_t* q = d->out_shape + 4 * o;
-    const int64_t tiles = (int64_t)((q[0] + 7) / 8) * ((q[1] + 7) / 8);
-    if (q[0] < 0 || q[1] < 0 || d->tile_start[o + 1] - d->tile_start[o] != tiles ||
-        d->pair_start[o + 1] < d->pair_start[o]) {
-      set_error("mmult output block %lld is inconsistent", (long long)o);
-      return BMV_ERR_INVALID;
-    }
-  }
-  if (d->n_out > 0 && d->pair_start[d->n_out] != d->n_pairs) {
-    set_error("mmult pair ranges do not cover the pairs");
-    return BMV_ERR_INVALID;
-  }
-  for (int64_t p = 0; p < d->n_pairs; ++p)
-    if (d->pair[4 * p] < 0 || d->pair[4 * p + 3] < 0) {
-      set_error("mmult pair %lld has a bad offset", (long long)p);
-      return BMV_ERR_INVALID;
-    }
+  int64_t c_extent = 0;
+  int rc = validate_mmult(d, &c_extent);
+  if (rc) return rc;
   int dev = 0, max_smem = 0;
   BMV_CUDA_TRY(cudaGetDevice(&dev));
   BMV_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const int ns = std::min(kPmMaxStages, (max_smem - 1024) / (d->stage_doubles * 8));
+  const int ns = std::min(kPmMaxStages, (max_smem - 1024) / d->stage_bytes);
   if (ns < 2) {
-    set_error("mmult stage of %d doubles leaves fewer than 2 pipeline stages", d->stage_doubles);
+    set_error("mmult stage of %d bytes leaves fewer than 2 pipeline stages", d->stage_bytes);
     return BMV_ERR_INVALID;
   }
   auto* p = new bmv_mmult();
   p->n_parts = d->n_parts;
   p->n_sub = d->n_sub;
-  p->n_out = d->n_out;
-  p->n_pairs = d->n_pairs;
-  p->stage_doubles = d->stage_doubles;
+  p->c_extent = c_extent;
+  p->stage_bytes = d->stage_bytes;
   p->n_stages = ns;
-  p->smem_bytes = ns * d->stage_doubles * 8;
-  int rc = upload(d->part_sub_start, (int64_t)d->n_parts + 1, &p->part_sub_start);
-  if (!rc) rc = upload(d->sub_a, 2 * d->n_sub, &p->sub_a);
-  if (!rc) rc = upload(d->sub_tile, 2 * d->n_sub, &p->sub_tile);
-  if (!rc) rc = upload(d->sub_out0, d->n_sub, &p->sub_out0);
-  if (!rc) rc = upload(d->tile_start, d->n_out + 1, &p->tile_start);
-  if (!rc) rc = upload(d->out_off, d->n_out, &p->out_off);
-  if (!rc) rc = upload(d->out_shape, 4 * d->n_out, &p->out_shape);
-  if (!rc) rc = upload(d->pair_start, d->n_out + 1, &p->pair_start);
-  if (!rc) rc = upload(d->pair, 4 * d->n_pairs, &p->pair);
+  p->smem_bytes = ns * d->stage_bytes;
+  rc = upload(d->part_sub_start, (int64_t)d->n_parts + 1, &p->part_sub_start);
+  if (!rc) rc = upload(d->part_entry_start, (int64_t)d->n_parts + 1, &p->part_entry_start);
+  if (!rc) rc = upload(d->copies, 4 * d->n_entries, &p->copies);
+  if (!rc) rc = upload(d->meta, d->meta_len, &p->meta);
   if (!rc) {
     const cudaError_t e = cudaFuncSetAttribute(pm_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                p->smem_bytes);
@@ -261,17 +285,21 @@ int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, dou
     set_error("null plan");
     return BMV_ERR_INVALID;
   }
+  if (c_len > 0 && c_len < p->c_extent) {
+    set_error("mmult output of %lld values, plan writes up to %lld", (long long)c_len,
+              (long long)p->c_extent);
+    return BMV_ERR_INVALID;
+  }
   cudaStream_t st = as_stream(stream);
   if (!accumulate) {
     int rc = zero_async(c, c_len, st);
     if (rc) return rc;
   }
   if (p->n_sub == 0 || p->n_parts == 0) return BMV_OK;
-  const int bulk_ok = (reinterpret_cast<uintptr_t>(a) & 15) == 0;
-  PmArgs g{p->part_sub_start, p->sub_a, p->sub_tile, p->sub_out0, p->tile_start, p->out_off,
-           reinterpret_cast<const int4*>(p->out_shape), p->pair_start,
-           reinterpret_cast<const int4*>(p->pair), a, b, c, alpha, accumulate,
-           p->stage_doubles, p->n_stages, bulk_ok};
+  PmArgs g{p->part_sub_start, p->part_entry_start, reinterpret_cast<const int4*>(p->copies),
+           CopySrc{reinterpret_cast<const char*>(p->meta), reinterpret_cast<const char*>(a),
+                   reinterpret_cast<const char*>(b)},
+           c, alpha, accumulate, p->stage_bytes, p->n_stages};
   pm_stream_kernel<<<(unsigned)p->n_parts, kPmThreads, p->smem_bytes, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;

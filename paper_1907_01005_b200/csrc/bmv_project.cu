@@ -30,34 +30,29 @@ using namespace bmv;
 
 namespace {
 
-constexpr int kPjWarps = 8;                     // consumer warps per CTA
-constexpr int kPjSlots = 16;                    // accumulator tiles per consumer warp
+constexpr int kPjWarps = 16;                    // consumer warps per CTA
+constexpr int kPjSlots = 8;                     // accumulator tiles per consumer warp
 constexpr int kPjThreads = (kPjWarps + 1) * 32; // + one producer warp
 constexpr int kPjMaxStages = 8;
 constexpr int kPjSlotDoubles = kPjWarps * kPjSlots * 64;
-constexpr int kPjPiece = 4096;                  // doubles per bulk copy instruction
+// Stage = [header (36 int32)][triple tiles (int4)][A blocks][B blocks].  Header:
+// [0..16] first triple of each consumer warp (local) and the end, [17] item,
+// [18] flush (last sub-chunk of the item), [20..35] slots used per warp.
+constexpr int kPjHeader = 144;
 
 struct PjArgs {
   const int64_t* __restrict__ part_sub_start;
-  const int64_t* __restrict__ sub_a;   // [lo, hi) per sub-chunk
-  const int64_t* __restrict__ sub_b;
-  const int32_t* __restrict__ sub_item;
-  const int64_t* __restrict__ sub_tri_start;  // per (sub, warp)
-  const int4* __restrict__ tri;
-  const int32_t* __restrict__ item_slots;     // per (item, warp)
-  const double* __restrict__ a;
-  const double* __restrict__ b;
+  const int64_t* __restrict__ part_entry_start;
+  const int4* __restrict__ copies;
+  CopySrc src;  // p0 = meta, p1 = a, p2 = b
   double* __restrict__ partial;
-  int stage_doubles;
+  int stage_bytes;
   int n_stages;
-  int bulk_ok;  // a, b 16-byte aligned
 };
-
-__device__ __forceinline__ int b_stage_offset(int na) { return (na + 1) & ~1; }
 
 // Tile of one triple: sum_r A[r][8 mt + m] B[r][8 nt + n] over the block rows,
 // A/B in the stage at (row stride as/bs).  Lane (gid, tig) returns
-// D[gid][2 tig], D[gid][2 tig + 1].
+// D[gid][2 tig], D[gid][2 tig + 1].  Four independent DMMA chains.
 __device__ __forceinline__ void triple_tile(const double* S, const int4 d, int gid, int tig,
                                             double& x, double& y) {
   const int rows = d.z & 0xffff;
@@ -66,29 +61,32 @@ __device__ __forceinline__ void triple_tile(const double* S, const int4 d, int g
   const bool am = gid < acols, bm = gid < bcols;
   const double* A = S + d.x + gid + tig * as;
   const double* B = S + d.y + gid + tig * bs;
-  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0, c4 = 0.0, c5 = 0.0, c6 = 0.0, c7 = 0.0;
   int r0 = 0;
-#pragma unroll 2
-  for (; r0 + 8 <= rows; r0 += 8) {
+  for (; r0 + 16 <= rows; r0 += 16) {
     const double a0 = am ? A[r0 * as] : 0.0, b0 = bm ? B[r0 * bs] : 0.0;
     const double a1 = am ? A[(r0 + 4) * as] : 0.0, b1 = bm ? B[(r0 + 4) * bs] : 0.0;
+    const double a2 = am ? A[(r0 + 8) * as] : 0.0, b2 = bm ? B[(r0 + 8) * bs] : 0.0;
+    const double a3 = am ? A[(r0 + 12) * as] : 0.0, b3 = bm ? B[(r0 + 12) * bs] : 0.0;
     dmma_8x8x4(c0, c1, a0, b0);
     dmma_8x8x4(c2, c3, a1, b1);
+    dmma_8x8x4(c4, c5, a2, b2);
+    dmma_8x8x4(c6, c7, a3, b3);
   }
   for (; r0 < rows; r0 += 4) {
     const bool ok = r0 + tig < rows;
     const double a0 = (am && ok) ? A[r0 * as] : 0.0, b0 = (bm && ok) ? B[r0 * bs] : 0.0;
     dmma_8x8x4(c0, c1, a0, b0);
   }
-  x = c0 + c2;
-  y = c1 + c3;
+  x = (c0 + c2) + (c4 + c6);
+  y = (c1 + c3) + (c5 + c7);
 }
 
 __global__ void __launch_bounds__(kPjThreads, 1) pj_stream_kernel(const PjArgs g) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[kPjMaxStages], empty[kPjMaxStages];
   double* slots = smem;
-  double* stages = smem + kPjSlotDoubles;
+  char* stages = reinterpret_cast<char*>(smem + kPjSlotDoubles);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t s0 = g.part_sub_start[blockIdx.x], s1 = g.part_sub_start[blockIdx.x + 1];
   const int NS = g.n_stages;
@@ -101,44 +99,26 @@ __global__ void __launch_bounds__(kPjThreads, 1) pj_stream_kernel(const PjArgs g
   for (int i = threadIdx.x; i < kPjSlotDoubles; i += blockDim.x) slots[i] = 0.0;
   __syncthreads();
 
-  if (warp == kPjWarps) {  // producer: stream the sub-chunks through the ring
-    for (int64_t s = s0; s < s1; ++s) {
-      const int64_t i = s - s0;
-      const int st = (int)(i % NS);
-      if (i >= NS) mbar_wait(&empty[st], (unsigned)((i / NS - 1) & 1));
-      double* dst = stages + (int64_t)st * g.stage_doubles;
-      const int64_t alo = g.sub_a[2 * s], ahi = g.sub_a[2 * s + 1];
-      const int64_t blo = g.sub_b[2 * s], bhi = g.sub_b[2 * s + 1];
-      const int na = (int)(ahi - alo), nb = (int)(bhi - blo), boff = b_stage_offset(na);
-      if (g.bulk_ok && ((alo | ahi | blo | bhi) & 1) == 0) {
-        if (lane == 0) {
-          mbar_expect_tx(&full[st], (unsigned)(na + nb) * 8u);
-          for (int k = 0; k < na; k += kPjPiece)
-            bulk_g2s(dst + k, g.a + alo + k, (unsigned)min(kPjPiece, na - k) * 8u, &full[st]);
-          for (int k = 0; k < nb; k += kPjPiece)
-            bulk_g2s(dst + boff + k, g.b + blo + k, (unsigned)min(kPjPiece, nb - k) * 8u, &full[st]);
-        }
-      } else {
-        for (int k = lane; k < na; k += 32) dst[k] = __ldg(g.a + alo + k);
-        for (int k = lane; k < nb; k += 32) dst[boff + k] = __ldg(g.b + blo + k);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[st]);
-      }
-    }
+  if (warp == kPjWarps) {
+    stream_producer(g.copies, g.part_entry_start[blockIdx.x], g.part_entry_start[blockIdx.x + 1],
+                    s1 - s0, g.src, stages, g.stage_bytes, NS, full, empty, lane);
     return;
   }
 
   const int gid = lane >> 2, tig = lane & 3;
   double* mine = slots + warp * kPjSlots * 64 + 2 * lane;
-  for (int64_t s = s0; s < s1; ++s) {
-    const int64_t i = s - s0;
+  for (int64_t i = 0; i < s1 - s0; ++i) {
     const int st = (int)(i % NS);
     mbar_wait(&full[st], (unsigned)((i / NS) & 1));
-    const double* S = stages + (int64_t)st * g.stage_doubles;
-    const int64_t t0 = g.sub_tri_start[s * kPjWarps + warp];
-    const int64_t t1 = g.sub_tri_start[s * kPjWarps + warp + 1];
-    for (int64_t t = t0; t < t1; ++t) {
-      const int4 d = __ldg(g.tri + t);
+    const char* stg = stages + (int64_t)st * g.stage_bytes;
+    const int* hdr = reinterpret_cast<const int*>(stg);
+    const int4* tri = reinterpret_cast<const int4*>(stg + kPjHeader);
+    const double* S = reinterpret_cast<const double*>(stg);
+    const int t0 = hdr[warp], t1 = hdr[warp + 1];
+    const int item = hdr[17], flush = hdr[18];
+    const int n_slots = hdr[20 + warp];
+    for (int t = t0; t < t1; ++t) {
+      const int4 d = tri[t];
       double x, y;
       triple_tile(S, d, gid, tig, x, y);
       double2* q = reinterpret_cast<double2*>(mine + ((d.z >> 16) & 0xff) * 64);
@@ -149,11 +129,9 @@ __global__ void __launch_bounds__(kPjThreads, 1) pj_stream_kernel(const PjArgs g
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-    const int item = g.sub_item[s];
-    if (s + 1 == s1 || g.sub_item[s + 1] != item) {  // item done: flush this warp's tiles
-      const int n = g.item_slots[(int64_t)item * kPjWarps + warp];
+    if (flush) {  // last sub-chunk of the item: write this warp's tiles once, clear them
       double* P = g.partial + ((int64_t)item * kPjWarps + warp) * kPjSlots * 64 + 2 * lane;
-      for (int k = 0; k < n; ++k) {
+      for (int k = 0; k < n_slots; ++k) {
         double2* q = reinterpret_cast<double2*>(mine + k * 64);
         *reinterpret_cast<double2*>(P + k * 64) = *q;
         *q = make_double2(0.0, 0.0);
@@ -192,22 +170,105 @@ __global__ void __launch_bounds__(256) pj_reduce_kernel(const int64_t* __restric
 }  // namespace
 
 struct bmv_tmmult {
-  int n_parts = 0, stage_doubles = 0, n_stages = 0, smem_bytes = 0;
-  int64_t n_sub = 0, n_items = 0, n_tri = 0, n_tiles = 0;
-  int64_t *part_sub_start = nullptr, *sub_a = nullptr, *sub_b = nullptr,
-          *sub_tri_start = nullptr, *tile_off = nullptr, *tile_src_start = nullptr,
-          *tile_src = nullptr;
-  int32_t *sub_item = nullptr, *tri = nullptr, *item_slots = nullptr, *tile_shape = nullptr;
+  int n_parts = 0, stage_bytes = 0, n_stages = 0, smem_bytes = 0;
+  int64_t n_sub = 0, n_items = 0, n_tiles = 0, c_extent = 0;
+  int64_t *part_sub_start = nullptr, *part_entry_start = nullptr, *tile_off = nullptr,
+          *tile_src_start = nullptr, *tile_src = nullptr;
+  int32_t *copies = nullptr, *meta = nullptr, *tile_shape = nullptr;
   double* partial = nullptr;
 };
+
+namespace {
+
+// Walk every sub-chunk's copy entries and staged header / triple tiles: the
+// bounds the kernel relies on (stage extents, slots, items) hold.
+int validate_tmmult(const bmv_tmmult_desc* d) {
+  const int64_t meta_bytes = d->meta_len * 4;
+  if (d->n_parts > 0 && (d->part_sub_start[0] != 0 || d->part_sub_start[d->n_parts] != d->n_sub ||
+                         d->part_entry_start[0] != 0 || d->part_entry_start[d->n_parts] != d->n_entries)) {
+    set_error("tmmult part ranges do not cover the sub-chunks / copies");
+    return BMV_ERR_INVALID;
+  }
+  for (int p = 0; p < d->n_parts; ++p) {
+    int64_t e = d->part_entry_start[p];
+    const int64_t e1 = d->part_entry_start[p + 1];
+    for (int64_t s = d->part_sub_start[p]; s < d->part_sub_start[p + 1]; ++s) {
+      const int64_t first = e;
+      const int32_t* m = nullptr;
+      for (;; ++e) {
+        if (e >= e1 || e - first >= kCpMaxPerSub) {
+          set_error("tmmult copy list of sub-chunk %lld is malformed", (long long)s);
+          return BMV_ERR_INVALID;
+        }
+        const int32_t* q = d->copies + 4 * e;
+        const unsigned y = (unsigned)q[1];
+        const int64_t len = y & kCpLenMask, sel = (y >> 28) & 3;
+        const int64_t src = ((int64_t)(uint32_t)q[3] << 32) | (uint32_t)q[2];
+        if (q[0] < 0 || q[0] + len > d->stage_bytes || sel > 2 || src < 0 ||
+            (sel == 0 && src + len > meta_bytes)) {
+          set_error("tmmult copy entry %lld out of range", (long long)e);
+          return BMV_ERR_INVALID;
+        }
+        if (e == first) {
+          if (sel != 0 || q[0] != 0 || len < kPjHeader || (src & 15)) {
+            set_error("tmmult sub-chunk %lld does not start with its header", (long long)s);
+            return BMV_ERR_INVALID;
+          }
+          m = d->meta + src / 4;
+          const int n_tri = m[kPjWarps];
+          if (m[0] != 0 || n_tri < 0 || kPjHeader + 16 * (int64_t)n_tri > len || m[17] < 0 ||
+              m[17] >= d->n_items) {
+            set_error("tmmult header of sub-chunk %lld is malformed", (long long)s);
+            return BMV_ERR_INVALID;
+          }
+          for (int w = 0; w < kPjWarps; ++w)
+            if (m[w] > m[w + 1] || m[20 + w] < 0 || m[20 + w] > kPjSlots) {
+              set_error("tmmult header of sub-chunk %lld is malformed", (long long)s);
+              return BMV_ERR_INVALID;
+            }
+          for (int t = 0; t < n_tri; ++t) {
+            const int32_t* q4 = m + kPjHeader / 4 + 4 * t;
+            const int rows = q4[2] & 0xffff, slot = (q4[2] >> 16) & 0xff;
+            const int ac = (q4[2] >> 24) & 15, bc = ((unsigned)q4[2] >> 28) & 15;
+            const int as = q4[3] & 0xffff, bs = ((unsigned)q4[3] >> 16) & 0xffff;
+            const int64_t a_end = 8 * ((int64_t)q4[0] + (int64_t)(rows - 1) * as + ac);
+            const int64_t b_end = 8 * ((int64_t)q4[1] + (int64_t)(rows - 1) * bs + bc);
+            if (q4[0] < 0 || q4[1] < 0 || slot >= kPjSlots || ac > 8 || bc > 8 ||
+                (rows > 0 && (a_end > d->stage_bytes || b_end > d->stage_bytes))) {
+              set_error("tmmult triple tile %d of sub-chunk %lld out of range", t, (long long)s);
+              return BMV_ERR_INVALID;
+            }
+          }
+        }
+        if ((y >> 30) & 1) {
+          ++e;
+          break;
+        }
+      }
+    }
+    if (e != e1) {
+      set_error("tmmult part %d has stray copy entries", p);
+      return BMV_ERR_INVALID;
+    }
+  }
+  const int64_t partial_tiles = d->n_items * kPjWarps * kPjSlots;
+  for (int64_t j = 0; j < d->n_src; ++j)
+    if (d->tile_src[j] < 0 || d->tile_src[j] >= partial_tiles) {
+      set_error("tmmult reduction source out of range");
+      return BMV_ERR_INVALID;
+    }
+  return BMV_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
 int bmv_tmmult_destroy(bmv_tmmult* p) {
   if (!p) return BMV_OK;
-  void* ptrs[] = {p->part_sub_start, p->sub_a,      p->sub_b,          p->sub_tri_start,
-                  p->tile_off,       p->tile_src_start, p->tile_src,   p->sub_item,
-                  p->tri,            p->item_slots, p->tile_shape,     p->partial};
+  void* ptrs[] = {p->part_sub_start, p->part_entry_start, p->tile_off, p->tile_src_start,
+                  p->tile_src,       p->copies,           p->meta,     p->tile_shape,
+                  p->partial};
   for (void* q : ptrs) release(q);
   delete p;
   return BMV_OK;
@@ -216,8 +277,9 @@ int bmv_tmmult_destroy(bmv_tmmult* p) {
 int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
   if (!out) return BMV_ERR_INVALID;
   *out = nullptr;
-  if (!d || d->n_parts < 0 || d->n_sub < 0 || d->n_items < 0 || d->n_tri < 0 ||
-      d->n_out_tiles < 0 || d->n_src < 0 || d->stage_doubles < 2 || (d->stage_doubles & 1)) {
+  if (!d || d->n_parts < 0 || d->n_sub < 0 || d->n_items < 0 || d->n_entries < 0 ||
+      d->meta_len < 0 || d->n_out_tiles < 0 || d->n_src < 0 || d->stage_bytes < kPjHeader ||
+      (d->stage_bytes & 15)) {
     set_error("invalid tmmult descriptor");
     return BMV_ERR_INVALID;
   }
@@ -226,66 +288,35 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
               d->slots_per_warp, kPjWarps, kPjSlots);
     return BMV_ERR_INVALID;
   }
-  // host-side validation of the plan (bounds the kernel relies on)
-  if (d->n_parts > 0 && (d->part_sub_start[0] != 0 || d->part_sub_start[d->n_parts] != d->n_sub)) {
-    set_error("tmmult part ranges do not cover the sub-chunks");
-    return BMV_ERR_INVALID;
-  }
-  for (int64_t s = 0; s < d->n_sub; ++s) {
-    const int64_t na = d->sub_a[2 * s + 1] - d->sub_a[2 * s], nb = d->sub_b[2 * s + 1] - d->sub_b[2 * s];
-    if (na < 0 || nb < 0 || ((na + 1) & ~1LL) + nb > d->stage_doubles || d->sub_item[s] < 0 ||
-        d->sub_item[s] >= d->n_items) {
-      set_error("tmmult sub-chunk %lld exceeds the stage or names a bad item", (long long)s);
-      return BMV_ERR_INVALID;
-    }
-  }
-  if (d->n_sub > 0 && d->sub_tri_start[(int64_t)d->n_sub * kPjWarps] != d->n_tri) {
-    set_error("tmmult triple ranges do not cover the triples");
-    return BMV_ERR_INVALID;
-  }
-  for (int64_t t = 0; t < d->n_tri; ++t) {
-    const int32_t* q = d->tri + 4 * t;
-    if (q[0] < 0 || q[1] < 0 || ((q[2] >> 16) & 0xff) >= kPjSlots) {
-      set_error("tmmult triple %lld has a bad stage offset or slot", (long long)t);
-      return BMV_ERR_INVALID;
-    }
-  }
-  for (int64_t k = 0; k < d->n_items * kPjWarps; ++k)
-    if (d->item_slots[k] < 0 || d->item_slots[k] > kPjSlots) {
-      set_error("tmmult item uses more than %d slots per warp", kPjSlots);
-      return BMV_ERR_INVALID;
-    }
-  const int64_t partial_tiles = d->n_items * kPjWarps * kPjSlots;
-  for (int64_t j = 0; j < d->n_src; ++j)
-    if (d->tile_src[j] < 0 || d->tile_src[j] >= partial_tiles) {
-      set_error("tmmult reduction source out of range");
-      return BMV_ERR_INVALID;
-    }
+  int rc = validate_tmmult(d);
+  if (rc) return rc;
   int dev = 0, max_smem = 0;
   BMV_CUDA_TRY(cudaGetDevice(&dev));
   BMV_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int avail = max_smem - 1024 - kPjSlotDoubles * 8;
-  const int ns = std::min(kPjMaxStages, avail / (d->stage_doubles * 8));
+  const int ns = std::min(kPjMaxStages, avail / d->stage_bytes);
   if (ns < 2) {
-    set_error("tmmult stage of %d doubles leaves fewer than 2 pipeline stages", d->stage_doubles);
+    set_error("tmmult stage of %d bytes leaves fewer than 2 pipeline stages", d->stage_bytes);
     return BMV_ERR_INVALID;
   }
   auto* p = new bmv_tmmult();
   p->n_parts = d->n_parts;
   p->n_sub = d->n_sub;
   p->n_items = d->n_items;
-  p->n_tri = d->n_tri;
   p->n_tiles = d->n_out_tiles;
-  p->stage_doubles = d->stage_doubles;
+  p->stage_bytes = d->stage_bytes;
   p->n_stages = ns;
-  p->smem_bytes = (kPjSlotDoubles + ns * d->stage_doubles) * 8;
-  int rc = upload(d->part_sub_start, (int64_t)d->n_parts + 1, &p->part_sub_start);
-  if (!rc) rc = upload(d->sub_a, 2 * d->n_sub, &p->sub_a);
-  if (!rc) rc = upload(d->sub_b, 2 * d->n_sub, &p->sub_b);
-  if (!rc) rc = upload(d->sub_item, d->n_sub, &p->sub_item);
-  if (!rc) rc = upload(d->sub_tri_start, d->n_sub * kPjWarps + 1, &p->sub_tri_start);
-  if (!rc) rc = upload(d->tri, 4 * d->n_tri, &p->tri);
-  if (!rc) rc = upload(d->item_slots, d->n_items * kPjWarps, &p->item_slots);
+  p->smem_bytes = kPjSlotDoubles * 8 + ns * d->stage_bytes;
+  for (int64_t t = 0; t < d->n_out_tiles; ++t) {
+    const int32_t* q = d->tile_shape + 3 * t;
+    if (q[0] > 0 && q[1] > 0)
+      p->c_extent = std::max<int64_t>(p->c_extent, d->tile_off[t] + (int64_t)(q[0] - 1) * q[2] + q[1]);
+  }
+  const int64_t partial_tiles = d->n_items * kPjWarps * kPjSlots;
+  rc = upload(d->part_sub_start, (int64_t)d->n_parts + 1, &p->part_sub_start);
+  if (!rc) rc = upload(d->part_entry_start, (int64_t)d->n_parts + 1, &p->part_entry_start);
+  if (!rc) rc = upload(d->copies, 4 * d->n_entries, &p->copies);
+  if (!rc) rc = upload(d->meta, d->meta_len, &p->meta);
   if (!rc) rc = upload(d->tile_off, d->n_out_tiles, &p->tile_off);
   if (!rc) rc = upload(d->tile_shape, 3 * d->n_out_tiles, &p->tile_shape);
   if (!rc) rc = upload(d->tile_src_start, d->n_out_tiles + 1, &p->tile_src_start);
@@ -317,14 +348,19 @@ int bmv_tmmult_run(bmv_tmmult* p, const double* a, const double* b, double* c, i
     set_error("null plan");
     return BMV_ERR_INVALID;
   }
+  if (c_len < p->c_extent) {
+    set_error("tmmult output of %lld values, plan writes up to %lld", (long long)c_len,
+              (long long)p->c_extent);
+    return BMV_ERR_INVALID;
+  }
   cudaStream_t st = as_stream(stream);
   int rc = zero_async(c, c_len, st);
   if (rc) return rc;
   if (p->n_sub > 0 && p->n_parts > 0) {
-    const int bulk_ok = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
-    PjArgs g{p->part_sub_start, p->sub_a, p->sub_b, p->sub_item, p->sub_tri_start,
-             reinterpret_cast<const int4*>(p->tri), p->item_slots, a, b, p->partial,
-             p->stage_doubles, p->n_stages, bulk_ok};
+    PjArgs g{p->part_sub_start, p->part_entry_start, reinterpret_cast<const int4*>(p->copies),
+             CopySrc{reinterpret_cast<const char*>(p->meta), reinterpret_cast<const char*>(a),
+                     reinterpret_cast<const char*>(b)},
+             p->partial, p->stage_bytes, p->n_stages};
     pj_stream_kernel<<<(unsigned)p->n_parts, kPjThreads, p->smem_bytes, st>>>(g);
     BMV_CHECK_LAUNCH();
   }

@@ -1,50 +1,84 @@
 """CPU emulation of the K4 / K5 streaming kernels over their host plans.
 
-Executes exactly what csrc/bmv_project.cu and csrc/bmv_postmul.cu do with a
-plan (stage contents, tile offsets, warp slots, partial layout, reduction
-order) in numpy, and asserts every stage read stays inside the staged
-range, so plan bugs surface on CPU.  Tests only.
+Executes what csrc/bmv_tma.cuh (producer: copy lists -> stage bytes),
+csrc/bmv_project.cu and csrc/bmv_postmul.cu (consumers: header, work
+descriptors, warp slots, partial layout, reduction order) do with a plan,
+in numpy, reading everything back from the emulated stage and asserting
+every read stays inside what was staged, so plan bugs surface on CPU.
+Tests only.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-W, SLOTS = 8, 16
+PJ_WARPS, PJ_SLOTS, PJ_HDR = 16, 8, 144
+PM_WARPS = 16
+
+
+def _subs(arr):
+    """Yield (sub index, staged bytes, staged mask) per sub-chunk, part by part."""
+    cps = arr["copies"].reshape(-1, 4).astype(np.int64) & 0xFFFFFFFF
+    pss, pes = arr["part_sub_start"], arr["part_entry_start"]
+    for p in range(int(arr["n_parts"])):
+        e = int(pes[p])
+        for s in range(int(pss[p]), int(pss[p + 1])):
+            first = e
+            ents = []
+            while True:
+                assert e < pes[p + 1] and e - first < 32, "malformed copy list"
+                ents.append(cps[e])
+                e += 1
+                if (ents[-1][1] >> 30) & 1:
+                    break
+            yield s, ents
+        assert e == pes[p + 1], "stray copy entries"
+
+
+def _stage(ents, srcs, stage_bytes):
+    buf = np.zeros(stage_bytes, dtype=np.uint8)
+    mask = np.zeros(stage_bytes, dtype=bool)
+    for x, y, lo, hi in ents:
+        n, sel = int(y & ((1 << 28) - 1)), int((y >> 28) & 3)
+        src = int(lo) | (int(hi) << 32)
+        assert x + n <= stage_bytes, "copy past the stage"
+        assert not mask[x:x + n].any(), "copies overlap"
+        buf[x:x + n] = srcs[sel][src:src + n]
+        mask[x:x + n] = True
+    return buf, mask
+
+
+def _dbl(buf, mask, off, n):
+    """n doubles at double offset off, all staged."""
+    assert off >= 0 and mask[8 * off: 8 * (off + n)].all(), "read outside the staged bytes"
+    return buf[8 * off: 8 * (off + n)].view(np.float64)
 
 
 def emulate_tmmult(arr, a_data, b_data, c_len):
-    sa = arr["sub_a"].reshape(-1, 2)
-    sb = arr["sub_b"].reshape(-1, 2)
-    tri = arr["tri"].reshape(-1, 4).astype(np.int64) & 0xFFFFFFFF
-    pss, sts, item = arr["part_sub_start"], arr["sub_tri_start"], arr["sub_item"]
-    cap = int(arr["stage_doubles"])
-    partial = np.zeros((int(arr["n_items"]) * W * SLOTS, 8, 8))
-    slots = np.zeros((W, SLOTS, 8, 8))
-    for p in range(int(arr["n_parts"])):
-        for s in range(pss[p], pss[p + 1]):
-            na, nb = sa[s, 1] - sa[s, 0], sb[s, 1] - sb[s, 0]
-            boff = na + (na & 1)
-            assert boff + nb <= cap
-            S = np.full(cap + 64 * 16, np.nan)
-            S[:na] = a_data[sa[s, 0]:sa[s, 1]]
-            S[boff:boff + nb] = b_data[sb[s, 0]:sb[s, 1]]
-            for w in range(W):
-                for t in range(sts[s * W + w], sts[s * W + w + 1]):
-                    x, y, z, ww = tri[t]
-                    rows, slot, ac, bc = z & 0xFFFF, (z >> 16) & 0xFF, (z >> 24) & 15, (z >> 28) & 15
-                    a_s, b_s = ww & 0xFFFF, ww >> 16
-                    assert 0 <= x and x + (rows - 1) * a_s + ac <= na, "A tile outside the stage"
-                    assert boff <= y and y + (rows - 1) * b_s + bc <= boff + nb, "B tile outside"
-                    am = np.stack([S[x + r * a_s: x + r * a_s + ac] for r in range(rows)])
-                    bm = np.stack([S[y + r * b_s: y + r * b_s + bc] for r in range(rows)])
-                    slots[w, slot, :ac, :bc] += am.T @ bm
-            it = item[s]
-            if s + 1 == pss[p + 1] or item[s + 1] != it:
-                for w in range(W):
-                    for k in range(arr["item_slots"][it * W + w]):
-                        partial[(it * W + w) * SLOTS + k] = slots[w, k]
-                        slots[w, k] = 0.0
+    srcs = [arr["meta"].view(np.uint8), a_data.view(np.uint8), b_data.view(np.uint8)]
+    sb = int(arr["stage_bytes"])
+    partial = np.zeros((int(arr["n_items"]) * PJ_WARPS * PJ_SLOTS, 8, 8))
+    slots = np.zeros((PJ_WARPS, PJ_SLOTS, 8, 8))
+    for s, ents in _subs(arr):
+        buf, mask = _stage(ents, srcs, sb)
+        hdr = buf[:PJ_HDR].view(np.int32)
+        n_tri = int(hdr[PJ_WARPS])
+        tri = buf[PJ_HDR:PJ_HDR + 16 * n_tri].view(np.int32).reshape(-1, 4).astype(np.int64) & 0xFFFFFFFF
+        for w in range(PJ_WARPS):
+            for t in range(hdr[w], hdr[w + 1]):
+                x, y, z, ww = tri[t]
+                rows, slot, ac, bc = z & 0xFFFF, (z >> 16) & 0xFF, (z >> 24) & 15, (z >> 28) & 15
+                a_s, b_s = ww & 0xFFFF, ww >> 16
+                assert slot < PJ_SLOTS
+                am = np.stack([_dbl(buf, mask, x + r * a_s, ac) for r in range(rows)])
+                bm = np.stack([_dbl(buf, mask, y + r * b_s, bc) for r in range(rows)])
+                slots[w, slot, :ac, :bc] += am.T @ bm
+        if hdr[18]:
+            it = int(hdr[17])
+            for w in range(PJ_WARPS):
+                for k in range(hdr[20 + w]):
+                    partial[(it * PJ_WARPS + w) * PJ_SLOTS + k] = slots[w, k]
+                    slots[w, k] = 0.0
     assert not slots.any(), "slot left unflushed"
     c = np.zeros(c_len)
     shp = arr["tile_shape"].reshape(-1, 3)
@@ -61,41 +95,28 @@ def emulate_tmmult(arr, a_data, b_data, c_len):
 
 def emulate_mmult(arr, a_data, b_data, c_data, alpha=1.0, accumulate=False):
     c = c_data.copy() if accumulate else np.zeros_like(c_data)
-    sa = arr["sub_a"].reshape(-1, 2)
-    stile = arr["sub_tile"].reshape(-1, 2)
-    pair = arr["pair"].reshape(-1, 4).astype(np.int64)
-    shp = arr["out_shape"].reshape(-1, 4)
-    ts, ps = arr["tile_start"], arr["pair_start"]
-    pss = arr["part_sub_start"]
-    cap = int(arr["stage_doubles"])
-    seen = 0
-    for p in range(int(arr["n_parts"])):
-        for s in range(pss[p], pss[p + 1]):
-            na = sa[s, 1] - sa[s, 0]
-            assert na <= cap
-            S = np.full(cap + 4096, np.nan)
-            S[:na] = a_data[sa[s, 0]:sa[s, 1]]
-            o = arr["sub_out0"][s]
-            for t in range(stile[s, 0], stile[s, 1]):
-                while ts[o + 1] <= t:
-                    o += 1
-                rows, cols, ys, _ = shp[o]
-                tn = (cols + 7) // 8
-                mi, ni = divmod(t - ts[o], tn)
-                r0, r1 = 8 * mi, min(rows, 8 * mi + 8)
-                c0, c1 = 8 * ni, min(cols, 8 * ni + 8)
-                acc = np.zeros((r1 - r0, c1 - c0))
-                for q in range(ps[o], ps[o + 1]):
-                    x, y, bs, boff = pair[q]
-                    a_s, inner = y & 0xFFFF, y >> 16
-                    assert 0 <= x and x + (rows - 1) * a_s + inner <= na, "A block outside the stage"
-                    am = np.stack([S[x + r * a_s: x + r * a_s + inner] for r in range(r0, r1)])
-                    bm = np.stack([b_data[boff + k * bs + c0: boff + k * bs + c1] for k in range(inner)])
-                    acc += am @ bm
-                for i in range(r0, r1):
-                    off = arr["out_off"][o] + i * ys
-                    c[off + c0: off + c1] = (c[off + c0: off + c1] if accumulate else 0.0) \
-                        + alpha * acc[i - r0]
-                seen += 1
-    assert seen == ts[-1], "tiles skipped or repeated"
+    written = np.zeros(c.size, dtype=bool)
+    srcs = [arr["meta"].view(np.uint8), a_data.view(np.uint8), b_data.view(np.uint8)]
+    sb = int(arr["stage_bytes"])
+    for s, ents in _subs(arr):
+        buf, mask = _stage(ents, srcs, sb)
+        nt = int(buf[:16].view(np.int32)[0])
+        meta = buf[16:].view(np.int32)
+        tasks = meta[:4 * nt].reshape(-1, 4).astype(np.int64) & 0xFFFFFFFF
+        for k in range(nt):
+            off, y, z, mi = tasks[k]
+            rv, cv, ni, ys = y & 15, (y >> 4) & 15, (y >> 8) & 15, y >> 16
+            p0, npairs = z & 0xFFFF, z >> 16
+            acc = np.zeros((rv, cv))
+            for p in range(p0, p0 + npairs):
+                q = meta[4 * (nt + p): 4 * (nt + p) + 4].astype(np.int64)
+                a_s, inner, bs = q[1] & 0xFFFF, q[1] >> 16, q[2]
+                am = np.stack([_dbl(buf, mask, q[0] + (8 * mi + r) * a_s, inner) for r in range(rv)])
+                bm = np.stack([_dbl(buf, mask, q[3] + kk * bs + 8 * ni, cv) for kk in range(inner)])
+                acc += am @ bm
+            for i in range(rv):
+                o = off + i * ys
+                assert not written[o:o + cv].any(), "output written twice"
+                written[o:o + cv] = True
+                c[o:o + cv] = (c[o:o + cv] if accumulate else 0.0) + alpha * acc[i]
     return c

@@ -756,7 +756,8 @@ def mmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n
     pa, pb = pa[order], pb[order]
     n_out = int(outs.size)
     # ---- streaming plan (csrc/bmv_postmul.cu) ------------------------------
-    # stage = [header][tasks (8x8 output tiles)][pairs][B blocks][A blocks]
+    # stage = [header][tasks][pairs][A blocks]; a task = up to 8 row tiles x
+    # one 8-column tile of an output block; B read through L1/L2
     n_rows = a.n_owned_blocks
     a_row_lo = a.block_offsets[a.row_start[:n_rows]]
     a_row_hi = a.block_offsets[a.row_start[1 : n_rows + 1]]
@@ -766,33 +767,18 @@ def mmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n
     out_rows = c.local_row_sizes[out_row].astype(np.int64)
     out_cols = c.col_blocks.sizes[c.col_index[outs]].astype(np.int64)
     c_str = c.col_strides[c.col_index[outs]].astype(np.int64)
-    tm, tn = (out_rows + 7) // 8, (out_cols + 7) // 8
+    tm = (out_rows + 8 * _PM_ROW_TILES - 1) // (8 * _PM_ROW_TILES)
+    tn = (out_cols + 7) // 8
     if n_out and (int(tn.max()) > 16 or int(c_str.max()) >= 1 << 16):
         raise ShapeError("mmult output blocks wider than 128 columns are not supported")
-    # B is staged as spans of its block rows: per (sub-chunk, block row k of
-    # B) the positions [first, last] the sub-chunk's products use
+    b_off = b.block_offsets[pb].astype(np.int64)
+    if b_off.size and int(b_off.max()) >= 1 << 31:
+        raise ShapeError("mmult b holds more than 2^31 values")
+    np_o = np.diff(start).astype(np.int64)
     pair_row = out_row[per] if pa.size else np.zeros(0, np.int64)
-    kb = b.pos_row[pb].astype(np.int64)
-    nkb = int(b.pos_row.max(initial=0)) + 2
-
-    def spans(group):
-        key = group * nkb + kb
-        uk, inv = np.unique(key, return_inverse=True)
-        lo = np.full(uk.size, np.iinfo(np.int64).max)
-        hi = np.full(uk.size, -1)
-        np.minimum.at(lo, inv, pb)
-        np.maximum.at(hi, inv, pb)
-        nbytes = 8 * (b.block_offsets[hi + 1] - b.block_offsets[lo])
-        return uk // nkb, lo, hi, nbytes + nbytes % 16, inv
-
-    r_grp, _, _, r_bytes, _ = spans(pair_row)
-    row_cb = np.bincount(r_grp, minlength=n_rows).astype(np.int64)
-    row_cbytes = np.bincount(r_grp, weights=r_bytes, minlength=n_rows).astype(np.int64)
     row_tasks = np.bincount(out_row, weights=tm * tn, minlength=n_rows).astype(np.int64)
     row_pairs = np.bincount(pair_row, minlength=n_rows).astype(np.int64)
-    row_bytes = 8 * row_dbl + 16 * (row_tasks + row_pairs) + row_cbytes
-    if n_rows and int(row_cb.max()) > _CP_MAX - 2:
-        raise ShapeError("mmult block row uses more than 30 block rows of b")
+    row_bytes = 8 * row_dbl + 16 * (row_tasks + row_pairs)
     # parts balanced by A + Y doubles; sub-chunks of consecutive rows
     y_dbl = np.bincount(out_row, weights=out_rows * c_str, minlength=n_rows).astype(np.int64)
     w = row_dbl + y_dbl
@@ -801,15 +787,13 @@ def mmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n
     before = np.concatenate([[0], np.cumsum(w)[:-1]]) if n_rows else np.zeros(0, np.int64)
     r_part = np.minimum(before * n_parts // total, n_parts - 1)
     r_sub = np.empty(n_rows, dtype=np.int64)
-    sid, acc, cacc = -1, 0, 0
-    bl, cl, pl = row_bytes.tolist(), row_cb.tolist(), r_part.tolist()
+    sid, acc = -1, 0
+    bl, pl = row_bytes.tolist(), r_part.tolist()
     for j in range(n_rows):
-        if (sid < 0 or pl[j] != pl[j - 1] or acc + bl[j] > _PM_STAGE_BYTES - 16
-                or cacc + cl[j] > _CP_MAX - 2):
+        if sid < 0 or pl[j] != pl[j - 1] or acc + bl[j] > _PM_STAGE_BYTES - 32:
             sid += 1
-            acc = cacc = 0
+            acc = 0
         acc += bl[j]
-        cacc += cl[j]
         r_sub[j] = sid
     n_sub = sid + 1
     first_r = np.searchsorted(r_sub, np.arange(n_sub + 1)).astype(np.int64)
@@ -819,69 +803,51 @@ def mmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n
     o_lo = np.searchsorted(out_row, first_r[:-1])       # outputs are in row order
     o_hi = np.searchsorted(out_row, first_r[1:])
     o_sub = r_sub[out_row]
-    # tasks: the 8x8 tiles of every output block, in (block, row tile, col tile) order
     to, tq = _expand(tm * tn)
-    t_mi, t_ni = tq // tn[to], tq % tn[to]
+    t_mi, t_ni = tq // tn[to], tq % tn[to]               # t_mi counts 64-row task rows
     t_sub = o_sub[to]
     n_tasks_sub = np.bincount(t_sub, minlength=n_sub).astype(np.int64)
     n_pairs_sub = (start[o_hi] - start[o_lo]).astype(np.int64)
-    # B spans per sub-chunk, staged after the metadata
-    p_sub = o_sub[per] if pa.size else np.zeros(0, np.int64)
-    cb_sub, cb_lo, cb_hi, cb_bytes, p_cb = spans(p_sub)
-    n_cb_sub = np.bincount(cb_sub, minlength=n_sub).astype(np.int64)
+    if n_sub and int(max(np_o.max(initial=0), n_pairs_sub.max())) >= 1 << 16:
+        raise ShapeError("mmult sub-chunk holds more than 65535 products")
     meta_bytes = 16 * (1 + n_tasks_sub + n_pairs_sub)
-    cb_first = np.concatenate([[0], np.cumsum(n_cb_sub)]).astype(np.int64)
-    cb_cum = np.concatenate([[0], np.cumsum(cb_bytes)]).astype(np.int64)
-    cb_soff = meta_bytes[cb_sub] + cb_cum[:-1] - cb_cum[cb_first[cb_sub]]
-    a_off = meta_bytes + cb_cum[cb_first[1:]] - cb_cum[cb_first[:-1]]
+    a_off = meta_bytes
     na_sub = sub_a[:, 1] - sub_a[:, 0]
     stage_bytes = int((a_off + 8 * na_sub).max(initial=16))
     stage_bytes += (-stage_bytes) % 16
     if 2 * stage_bytes > _SMEM_OPTIN - 1024:
         raise ShapeError(f"mmult block row needs {stage_bytes} bytes of shared memory (2 stages)")
-    # metadata: header, tasks, pairs per sub-chunk
     meta_off = np.concatenate([[0], np.cumsum(meta_bytes // 4)]).astype(np.int64)
     meta = np.zeros(int(meta_off[-1]), dtype=np.int64)
     meta[meta_off[:-1]] = n_tasks_sub
     task_first = np.concatenate([[0], np.cumsum(n_tasks_sub)]).astype(np.int64)
     tpos = meta_off[t_sub] + 4 * (1 + np.arange(to.size) - task_first[t_sub])
-    t_off = c.block_offsets[outs][to] + 8 * t_mi * c_str[to] + 8 * t_ni
+    r0 = 8 * _PM_ROW_TILES * t_mi
+    t_off = c.block_offsets[outs][to] + r0 * c_str[to] + 8 * t_ni
     if t_off.size and int(t_off.max()) >= 1 << 32:
         raise ShapeError("mmult output holds more than 2^32 values")
     meta[tpos] = t_off
-    meta[tpos + 1] = (np.minimum(8, out_rows[to] - 8 * t_mi) | (np.minimum(8, out_cols[to] - 8 * t_ni) << 4)
-                      | (t_ni << 8) | (c_str[to] << 16))
-    np_o = np.diff(start)
+    meta[tpos + 1] = (np.minimum(8 * _PM_ROW_TILES, out_rows[to] - r0)
+                      | (np.minimum(8, out_cols[to] - 8 * t_ni) << 8) | (t_ni << 12) | (c_str[to] << 16))
     meta[tpos + 2] = (start[to] - start[o_lo[t_sub]]) | (np_o[to] << 16)
-    meta[tpos + 3] = t_mi
-    if np_o.size and int(max(np_o.max(), n_pairs_sub.max(initial=0))) >= 1 << 16:
-        raise ShapeError("mmult sub-chunk holds more than 65535 products")
+    meta[tpos + 3] = _PM_ROW_TILES * t_mi
     a_str = a.col_strides[a.col_index[pa]].astype(np.int64)
     inner = a.col_blocks.sizes[a.col_index[pa]].astype(np.int64)
+    p_sub = o_sub[per] if pa.size else np.zeros(0, np.int64)
     ppos = meta_off[p_sub] + 4 * (1 + n_tasks_sub[p_sub] + np.arange(pa.size) - start[o_lo[p_sub]])
     meta[ppos] = a_off[p_sub] // 8 + a.block_offsets[pa] - sub_a[p_sub, 0]
     meta[ppos + 1] = a_str | (inner << 16)
     meta[ppos + 2] = b.col_strides[b.col_index[pb]]
-    meta[ppos + 3] = cb_soff[p_cb] // 8 + b.block_offsets[pb] - b.block_offsets[cb_lo[p_cb]]
+    meta[ppos + 3] = b_off
     meta = (meta & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
-    # copy lists: metadata, B blocks, A range (last)
-    n_ent = 2 + n_cb_sub
-    e_first = np.concatenate([[0], np.cumsum(n_ent)]).astype(np.int64)
-    copies = np.zeros((int(e_first[-1]), 4), dtype=np.int64)
-    copies[e_first[:-1], 1] = meta_bytes
-    copies[e_first[:-1], 2] = 4 * meta_off[:-1]
-    cpos = e_first[cb_sub] + 1 + np.arange(cb_sub.size) - cb_first[cb_sub]
-    copies[cpos, 0] = cb_soff
-    copies[cpos, 1] = 8 * (b.block_offsets[cb_hi + 1] - b.block_offsets[cb_lo]) | (2 << 28)
-    copies[cpos, 2] = 8 * b.block_offsets[cb_lo]
-    last = e_first[1:] - 1
-    copies[last, 0] = a_off
-    copies[last, 1] = 8 * na_sub | (1 << 28) | (1 << 30)
-    copies[last, 2] = 8 * sub_a[:, 0]
+    copies = np.zeros((n_sub, 2, 4), dtype=np.int64)
+    copies[:, 0, 1], copies[:, 0, 2] = meta_bytes, 4 * meta_off[:-1]
+    copies[:, 1, 0], copies[:, 1, 1], copies[:, 1, 2] = a_off, 8 * na_sub | (1 << 28) | (1 << 30), \
+        8 * sub_a[:, 0]
     arrays = dict(
         n_parts=n_parts, stage_bytes=stage_bytes, n_sub=n_sub,
-        part_sub_start=part_sub_start, part_entry_start=e_first[part_sub_start],
-        copies=_pack_copies(copies), meta=meta,
+        part_sub_start=part_sub_start, part_entry_start=2 * part_sub_start,
+        copies=_pack_copies(copies.reshape(-1, 4)), meta=meta,
     )
     flops = int(2 * np.sum(out_rows[per] * inner * out_cols[per]))
     n_own_c = int(c.row_start[c.n_owned_blocks])
@@ -1014,7 +980,7 @@ def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, 
     a_dbl = a_row_hi - a_row_lo
     b_dbl = b_row_hi - b_row_lo
     unit_dbl_row = a_dbl + (a_dbl & 1) + b_dbl
-    big = (unit_dbl_row > cap) | (ta_row * tb_row > _PJ_TILES)
+    big = (unit_dbl_row > cap) | (ta_row * tb_row > _PJ_UNITS)
 
     def groups(blk, tiles, p0, p1, budget, tmax):
         starts, acc, tacc = [p0], 0, 0
@@ -1038,15 +1004,15 @@ def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, 
     for i in np.flatnonzero(big).tolist():
         pa0, pa1, pb0, pb1 = int(u_a0[i]), int(u_a1[i]), int(u_b0[i]), int(u_b1[i])
         half = cap // 2 - 2
-        if a_dbl[i] <= half and ta_row[i] <= 8:
+        if a_dbl[i] <= half and ta_row[i] <= 4:
             gs_a = [pa0]
-            gs_b = groups(b_blk, b_tiles, pb0, pb1, cap - 2 - int(a_dbl[i]), _PJ_TILES // max(int(ta_row[i]), 1))
-        elif b_dbl[i] <= half and tb_row[i] <= 8:
+            gs_b = groups(b_blk, b_tiles, pb0, pb1, cap - 2 - int(a_dbl[i]), _PJ_UNITS // max(int(ta_row[i]), 1))
+        elif b_dbl[i] <= half and tb_row[i] <= 4:
             gs_b = [pb0]
-            gs_a = groups(a_blk, a_tiles, pa0, pa1, cap - 2 - int(b_dbl[i]), _PJ_TILES // max(int(tb_row[i]), 1))
+            gs_a = groups(a_blk, a_tiles, pa0, pa1, cap - 2 - int(b_dbl[i]), _PJ_UNITS // max(int(tb_row[i]), 1))
         else:
-            gs_a = groups(a_blk, a_tiles, pa0, pa1, half, 8)
-            gs_b = groups(b_blk, b_tiles, pb0, pb1, half, 16)
+            gs_a = groups(a_blk, a_tiles, pa0, pa1, half, 4)
+            gs_b = groups(b_blk, b_tiles, pb0, pb1, half, 8)
         row_nbg[i] = len(gs_b)
         extra.append((i, gs_a, gs_b, pa1, pb1))
     if extra:
@@ -1095,7 +1061,7 @@ def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, 
     dl, tl, fl, pl = u_dbl.tolist(), u_tiles.tolist(), u_full.tolist(), u_part.tolist()
     for j in range(u_row.size):
         if (sid < 0 or not fl[j] or not fl[j - 1] or pl[j] != pl[j - 1]
-                or acc + dl[j] > cap or tacc + tl[j] > _PJ_TILES):
+                or acc + dl[j] > cap or tacc + tl[j] > _PJ_UNITS):
             sid += 1
             acc = tacc = 0
         acc += dl[j]
@@ -1128,29 +1094,34 @@ def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, 
             n_items += 1
             cur = stop
     t_item = sub_item[t_sub]
-    # owner warp + slot of every (item, tile): longest-processing-time first
-    ik = t_item * (int(t_key.max(initial=0)) + 1) + t_key
+    # owner warp + register slot of every (item, tile): round robin
+    kmax = int(t_key.max(initial=0)) + 1
+    ik = t_item * kmax + t_key
     uik, inv = np.unique(ik, return_inverse=True)
-    work = np.bincount(inv, weights=t_rows, minlength=uik.size)
-    it_item = uik // (int(t_key.max(initial=0)) + 1)
-    it_warp = np.empty(uik.size, dtype=np.int64)
-    it_slot = np.empty(uik.size, dtype=np.int64)
-    item_slots = np.zeros((n_items, _PJ_WARPS), dtype=np.int32)
-    bounds = np.searchsorted(it_item, np.arange(n_items + 1))
-    for it in range(n_items):
-        lo, hi = int(bounds[it]), int(bounds[it + 1])
-        load = [0.0] * _PJ_WARPS
-        cnt = [0] * _PJ_WARPS
-        for j in (lo + np.argsort(-work[lo:hi], kind="stable")).tolist():
-            w = min((x for x in range(_PJ_WARPS) if cnt[x] < _PJ_SLOTS), key=lambda x: load[x])
-            it_warp[j], it_slot[j] = w, cnt[w]
-            cnt[w] += 1
-            load[w] += work[j]
-        item_slots[it] = cnt
-    t_warp, t_slot = it_warp[inv], it_slot[inv]
-    # triple tiles sorted by (sub, warp, slot), reference order inside
-    o = np.lexsort((np.arange(t_key.size), t_slot, t_warp, t_sub))
-    t_sub, t_warp, t_slot = t_sub[o], t_warp[o], t_slot[o]
+    it_item = uik // kmax
+    it_rank = np.arange(uik.size) - np.searchsorted(it_item, it_item)
+    it_warp, it_slot = it_rank % _PJ_WARPS, it_rank // _PJ_WARPS
+    item_slots = np.zeros((n_items, _PJ_WARPS), dtype=np.int64)
+    np.add.at(item_slots, (it_item, it_warp), 1)
+    # units: the output tiles of one sub-chunk; computing warp by a snake
+    # over the units in decreasing work (balanced per sub-chunk)
+    sk = t_sub * kmax + t_key
+    usk, uinv = np.unique(sk, return_inverse=True)
+    u_sub = usk // kmax
+    u_work = np.bincount(uinv, weights=t_rows, minlength=usk.size)
+    o = np.lexsort((-u_work, u_sub))
+    u_rank = np.empty(usk.size, dtype=np.int64)
+    u_rank[o] = np.arange(usk.size) - np.searchsorted(u_sub[o], u_sub[o])
+    if u_rank.size and int(u_rank.max()) >= _PJ_UNITS:
+        raise ShapeError("tmmult sub-chunk touches more output tiles than a stage holds")
+    cyc = u_rank % (2 * _PJ_WARPS)
+    u_comp = np.where(cyc < _PJ_WARPS, cyc, 2 * _PJ_WARPS - 1 - cyc)
+    u_it = np.searchsorted(uik, sub_item[u_sub] * kmax + usk % kmax)
+    u_owner, u_slot = it_warp[u_it], it_slot[u_it]
+    t_warp, t_unit = u_comp[uinv], u_rank[uinv]
+    # triple tiles sorted by (sub, computing warp, unit), reference order inside
+    o = np.lexsort((np.arange(t_key.size), t_unit, t_warp, t_sub))
+    t_sub, t_warp, t_unit = t_sub[o], t_warp[o], t_unit[o]
     t_pa, t_pb, t_rows, mt, nt = t_pa[o], t_pb[o], t_rows[o], mt[o], nt[o]
     t_mr, t_mc = mr[tri][o], mc[tri][o]
     sub_tri_start = np.searchsorted(t_sub * _PJ_WARPS + t_warp,
@@ -1182,12 +1153,14 @@ def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, 
     hdr[:, _PJ_WARPS] = n_tri_sub
     hdr[:, 17] = sub_item
     hdr[:, 18] = np.concatenate([sub_item[1:] != sub_item[:-1], [True]]) if n_sub else 0
+    hdr[:, 19] = np.bincount(u_sub, minlength=n_sub)
     hdr[:, 20:20 + _PJ_WARPS] = item_slots[sub_item] if n_sub else 0
+    hdr[u_sub, 36 + u_rank] = u_owner | (u_slot << 8)
     meta[(meta_off[:-1, None] + np.arange(_PJ_HDR // 4)[None, :]).ravel()] = hdr.ravel()
     rowpos = meta_off[t_sub] + _PJ_HDR // 4 + 4 * (np.arange(t_sub.size) - t_first)
     meta[rowpos] = a_soff
     meta[rowpos + 1] = b_soff
-    meta[rowpos + 2] = t_rows | (t_slot << 16) | (acols << 24) | (bcols << 28)
+    meta[rowpos + 2] = t_rows | (t_unit << 16) | (acols << 24) | (bcols << 28)
     meta[rowpos + 3] = a_str | (b_str << 16)
     meta = (meta & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
     # copy lists: metadata, A range, B range
@@ -1199,7 +1172,7 @@ def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, 
     copies = _pack_copies(copies.reshape(-1, 4))
     part_entry_start = 3 * part_sub_start
     # output tiles and their partial sources (item order)
-    tiles, tinv = np.unique(uik % (int(t_key.max(initial=0)) + 1), return_inverse=True)
+    tiles, tinv = np.unique(uik % kmax, return_inverse=True)
     src_order = np.lexsort((it_item, tinv))
     tile_src = ((it_item * _PJ_WARPS + it_warp) * _PJ_SLOTS + it_slot)[src_order]
     tile_src_start = np.searchsorted(tinv[src_order], np.arange(tiles.size + 1)).astype(np.int64)
@@ -1226,12 +1199,14 @@ def tmmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, 
 _PJ_WARPS = 16       # consumer warps per CTA (bmv_project.cu kPjWarps)
 _PJ_SLOTS = 8        # accumulator tiles per warp (kPjSlots)
 _PJ_TILES = _PJ_WARPS * _PJ_SLOTS
-_PJ_HDR = 144        # bytes of the K4 stage header (kPjHeader)
-# A + B doubles per K4 stage: 40 KB stages (header + <= 128 triple tiles
-# included) -> 4 stages + 64 KB of accumulator slots per SM
-_PJ_STAGE = (40960 - _PJ_HDR - 16 * _PJ_TILES) // 8
+_PJ_UNITS = 32       # output tiles per K4 sub-chunk (kPjUnits)
+_PJ_HDR = 272        # bytes of the K4 stage header (kPjHeader)
+# A + B doubles per K4 stage: 48 KB stages (header + triple tiles included)
+# -> 4 stages + 32 KB of unit results per SM
+_PJ_STAGE = (49152 - _PJ_HDR - 16 * 4 * _PJ_UNITS) // 8
 _PM_STAGE_BYTES = 40960   # K5 stage target (5 stages per SM)
 _CP_MAX = 32              # copy entries per sub-chunk (kCpMaxPerSub)
+_PM_ROW_TILES = 8         # 8-row tiles per K5 task (kPmRowTiles)
 
 
 def _pack_copies(entries: np.ndarray) -> np.ndarray:

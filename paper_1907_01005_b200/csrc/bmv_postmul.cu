@@ -34,7 +34,8 @@ struct PmArgs {
   const int64_t* __restrict__ part_sub_start;
   const int64_t* __restrict__ part_entry_start;
   const int4* __restrict__ copies;
-  CopySrc src;  // p0 = meta, p1 = a, p2 = b
+  CopySrc src;  // p0 = meta, p1 = a
+  const double* __restrict__ b;
   double* __restrict__ c;
   double alpha;
   int accumulate;
@@ -42,37 +43,63 @@ struct PmArgs {
   int n_stages;
 };
 
-// One 8x8 output tile: sum over its pairs of A(8 rows x inner) B(inner x 8),
-// all operands in the stage.  Lane (gid, tig) returns D[gid][2 tig + {0,1}].
-__device__ __forceinline__ void task_tile(const double* S, const int4* pairs, const int4 t,
-                                          int gid, int tig, double& x, double& y) {
-  const int rv = t.y & 15, cv = (t.y >> 4) & 15, ni = (t.y >> 8) & 15;
-  const int p0 = t.z & 0xffff, np = (t.z >> 16) & 0xffff;
-  const bool am = gid < rv, bm = gid < cv;
-  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-  for (int p = p0; p < p0 + np; ++p) {
-    const int4 d = pairs[p];
-    const int as = d.y & 0xffff, inner = (d.y >> 16) & 0xffff, bs = d.z;
-    const double* A = S + d.x + (8 * t.w + gid) * as + tig;
-    const double* B = S + d.w + tig * bs + 8 * ni + gid;
-    int k0 = 0;
-    for (; k0 + 8 <= inner; k0 += 8) {
-      const double a0 = am ? A[k0] : 0.0, a1 = am ? A[k0 + 4] : 0.0;
-      const double b0 = bm ? B[k0 * bs] : 0.0, b1 = bm ? B[(k0 + 4) * bs] : 0.0;
-      dmma_8x8x4(c0, c1, a0, b0);
-      dmma_8x8x4(c2, c3, a1, b1);
-    }
-    for (; k0 < inner; k0 += 4) {
-      const bool ok = k0 + tig < inner;
-      const double a0 = (am && ok) ? A[k0] : 0.0, b0 = (bm && ok) ? B[k0 * bs] : 0.0;
-      dmma_8x8x4(c0, c1, a0, b0);
-    }
-  }
-  x = c0 + c2;
-  y = c1 + c3;
+constexpr int kPmRowTiles = 8;  // 8-row tiles per task (64 rows)
+
+// B fragments of one pair (up to 16 inner rows = 4 k-steps): lane (gid, tig)
+// holds B[4 ks + tig][8 ni + gid].
+__device__ __forceinline__ void load_b(const double* __restrict__ b, const int4 d, int k0, int ni,
+                                       int gid, int tig, bool bm, double (&f)[4]) {
+  const int inner = (d.y >> 16) & 0xffff, bs = d.z;
+  const double* B = b + (uint32_t)d.w + (int64_t)(k0 + tig) * bs + 8 * ni + gid;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks)
+    f[ks] = (bm && k0 + 4 * ks + tig < inner) ? __ldg(B + (int64_t)4 * ks * bs) : 0.0;
 }
 
-__global__ void __launch_bounds__(kPmThreads, 1) pm_stream_kernel(const PmArgs g) {
+// One task = up to 8 row tiles x one 8-column tile of an output block:
+// acc[m] += sum_pairs A[8 (mi0 + m) + gid][k] B[k][8 ni + 2 tig + {0,1}].
+// B fragments (global, L1/L2) of pair p + 1 are loaded while pair p runs.
+__device__ __forceinline__ void task_tiles(const double* S, const int4* pairs, const int4 t,
+                                           const double* __restrict__ b, int gid, int tig,
+                                           double (&acc)[kPmRowTiles][2]) {
+  const int rows = t.y & 0x7f, cv = (t.y >> 8) & 15, ni = (t.y >> 12) & 15;
+  const int p0 = t.z & 0xffff, np = (t.z >> 16) & 0xffff;
+  const bool bm = gid < cv;
+  const int nm = (rows + 7) >> 3;
+  double fb[4], fn[4];
+  if (np > 0) load_b(b, pairs[p0], 0, ni, gid, tig, bm, fb);
+  for (int p = p0; p < p0 + np; ++p) {
+    const int4 d = pairs[p];
+    const int as = d.y & 0xffff, inner = (d.y >> 16) & 0xffff;
+    for (int k0 = 0; k0 < inner; k0 += 16) {
+      // prefetch the next fragments: this pair's next 16 rows or the next pair
+      const bool more = k0 + 16 < inner;
+      if (more)
+        load_b(b, d, k0 + 16, ni, gid, tig, bm, fn);
+      else if (p + 1 < p0 + np)
+        load_b(b, pairs[p + 1], 0, ni, gid, tig, bm, fn);
+      const double* A = S + d.x + (8 * t.w + gid) * as + k0 + tig;
+#pragma unroll
+      for (int m = 0; m < kPmRowTiles; ++m) {
+        if (m < nm) {
+          const bool am = 8 * m + gid < rows;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            if (k0 + 4 * ks < inner) {
+              const double a = (am && k0 + 4 * ks + tig < inner) ? A[8 * m * as + 4 * ks] : 0.0;
+              dmma_8x8x4(acc[m][0], acc[m][1], a, fb[ks]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) fb[ks] = fn[ks];
+    }
+  }
+}
+
+// 17 warps x 120 registers fill the register file; __launch_bounds__ would cap at 96.
+__global__ void __maxnreg__(120) pm_stream_kernel(const PmArgs g) {
   extern __shared__ __align__(128) char stages[];
   __shared__ __align__(8) uint64_t full[kPmMaxStages], empty[kPmMaxStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -104,26 +131,31 @@ __global__ void __launch_bounds__(kPmThreads, 1) pm_stream_kernel(const PmArgs g
     const int4* pairs = meta + 1 + n_tasks;
     for (int k = warp; k < n_tasks; k += kPmWarps) {
       const int4 t = tasks[k];
-      double x, y;
-      task_tile(S, pairs, t, gid, tig, x, y);
-      const int rv = t.y & 15, cv = (t.y >> 4) & 15, ys = (t.y >> 16) & 0xffff;
+      double acc[kPmRowTiles][2];
+#pragma unroll
+      for (int m = 0; m < kPmRowTiles; ++m) acc[m][0] = acc[m][1] = 0.0;
+      task_tiles(S, pairs, t, g.b, gid, tig, acc);
+      const int rows = t.y & 0x7f, cv = (t.y >> 8) & 15, ys = (t.y >> 16) & 0xffff;
       const int col = 2 * tig;
-      if (gid < rv && col < cv) {
-        double* Y = g.c + (uint32_t)t.x + (int64_t)gid * ys + col;
-        x *= g.alpha;
-        y *= g.alpha;
-        const bool two = col + 1 < cv;
-        if (two && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0)) {
-          double2* Y2 = reinterpret_cast<double2*>(Y);
-          if (g.accumulate) {
-            const double2 old = *Y2;
-            x += old.x;
-            y += old.y;
+      const bool two = col + 1 < cv;
+#pragma unroll
+      for (int m = 0; m < kPmRowTiles; ++m) {
+        const int r = 8 * m + gid;
+        if (r < rows && col < cv) {
+          double* Y = g.c + (uint32_t)t.x + (int64_t)r * ys + col;
+          double x = g.alpha * acc[m][0], y = g.alpha * acc[m][1];
+          if (two && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0)) {
+            double2* Y2 = reinterpret_cast<double2*>(Y);
+            if (g.accumulate) {
+              const double2 old = *Y2;
+              x += old.x;
+              y += old.y;
+            }
+            *Y2 = make_double2(x, y);
+          } else {
+            Y[0] = g.accumulate ? Y[0] + x : x;
+            if (two) Y[1] = g.accumulate ? Y[1] + y : y;
           }
-          *Y2 = make_double2(x, y);
-        } else {
-          Y[0] = g.accumulate ? Y[0] + x : x;
-          if (two) Y[1] = g.accumulate ? Y[1] + y : y;
         }
       }
     }
@@ -184,23 +216,20 @@ int validate_mmult(const bmv_mmult_desc* d, int64_t* c_extent) {
           const int64_t n_pairs = len / 16 - 1 - nt;
           for (int k = 0; k < nt; ++k) {
             const int32_t* t = m + 4 * (1 + k);
-            const int rv = t[1] & 15, cv = (t[1] >> 4) & 15, ni = (t[1] >> 8) & 15;
+            const int rows = t[1] & 0x7f, cv = (t[1] >> 8) & 15;
             const int ys = ((unsigned)t[1] >> 16) & 0xffff;
             const int p0 = t[2] & 0xffff, np = ((unsigned)t[2] >> 16) & 0xffff;
-            if (rv > 8 || cv > 8 || p0 + np > n_pairs || t[3] < 0) {
+            if (rows > 8 * kPmRowTiles || cv > 8 || p0 + np > n_pairs || t[3] < 0) {
               set_error("mmult task %d of sub-chunk %lld out of range", k, (long long)s);
               return BMV_ERR_INVALID;
             }
-            if (rv > 0 && cv > 0)
-              *c_extent = std::max<int64_t>(*c_extent, (int64_t)(uint32_t)t[0] + (int64_t)(rv - 1) * ys + cv);
+            if (rows > 0 && cv > 0)
+              *c_extent = std::max<int64_t>(*c_extent, (int64_t)(uint32_t)t[0] + (int64_t)(rows - 1) * ys + cv);
             for (int pp = p0; pp < p0 + np; ++pp) {
               const int32_t* q4 = m + 4 * (1 + nt + pp);
-              const int as = q4[1] & 0xffff, inner = ((unsigned)q4[1] >> 16) & 0xffff, bs = q4[2];
-              const int64_t a_end = 8 * ((int64_t)q4[0] + (int64_t)(8 * t[3] + rv - 1) * as + inner);
-              const int64_t b_end = 8 * ((int64_t)q4[3] + (int64_t)(inner - 1) * bs + 8 * ni + cv);
-              if (q4[0] < 0 || q4[3] < 0 || bs < 0 ||
-                  (rv > 0 && inner > 0 && a_end > d->stage_bytes) ||
-                  (cv > 0 && inner > 0 && b_end > d->stage_bytes)) {
+              const int as = q4[1] & 0xffff, inner = ((unsigned)q4[1] >> 16) & 0xffff;
+              const int64_t a_end = 8 * ((int64_t)q4[0] + (int64_t)(8 * t[3] + rows - 1) * as + inner);
+              if (q4[0] < 0 || q4[2] < 0 || q4[3] < 0 || (rows > 0 && inner > 0 && a_end > d->stage_bytes)) {
                 set_error("mmult pair %d of sub-chunk %lld out of range", pp, (long long)s);
                 return BMV_ERR_INVALID;
               }
@@ -265,7 +294,7 @@ int bmv_mmult_create(const bmv_mmult_desc* d, bmv_mmult** out) {
   if (!rc) rc = upload(d->meta, d->meta_len, &p->meta);
   if (!rc) {
     const cudaError_t e = cudaFuncSetAttribute(pm_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               p->smem_bytes);
+                                               max_smem - 1024);
     if (e != cudaSuccess) {
       set_error("cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
       rc = BMV_ERR_CUDA;
@@ -298,8 +327,8 @@ int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, dou
   if (p->n_sub == 0 || p->n_parts == 0) return BMV_OK;
   PmArgs g{p->part_sub_start, p->part_entry_start, reinterpret_cast<const int4*>(p->copies),
            CopySrc{reinterpret_cast<const char*>(p->meta), reinterpret_cast<const char*>(a),
-                   reinterpret_cast<const char*>(b)},
-           c, alpha, accumulate, p->stage_bytes, p->n_stages};
+                   nullptr},
+           b, c, alpha, accumulate, p->stage_bytes, p->n_stages};
   pm_stream_kernel<<<(unsigned)p->n_parts, kPmThreads, p->smem_bytes, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;

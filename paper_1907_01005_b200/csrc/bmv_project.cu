@@ -31,14 +31,16 @@ using namespace bmv;
 namespace {
 
 constexpr int kPjWarps = 16;                    // consumer warps per CTA
-constexpr int kPjSlots = 8;                     // accumulator tiles per consumer warp
+constexpr int kPjSlots = 8;                     // accumulator tiles per consumer warp (registers)
+constexpr int kPjUnits = 32;                    // output tiles per sub-chunk
 constexpr int kPjThreads = (kPjWarps + 1) * 32; // + one producer warp
 constexpr int kPjMaxStages = 8;
-constexpr int kPjSlotDoubles = kPjWarps * kPjSlots * 64;
-// Stage = [header (36 int32)][triple tiles (int4)][A blocks][B blocks].  Header:
-// [0..16] first triple of each consumer warp (local) and the end, [17] item,
-// [18] flush (last sub-chunk of the item), [20..35] slots used per warp.
-constexpr int kPjHeader = 144;
+constexpr int kPjResultDoubles = 2 * kPjUnits * 64;  // double-buffered unit results
+// Stage = [header (68 int32)][triple tiles (int4)][A blocks][B blocks].  Header:
+// [0..16] first triple of each computing warp (local) and the end, [17] item,
+// [18] flush (last sub-chunk of the item), [19] units, [20..35] slots per
+// warp in the item, [36..67] unit -> owner warp | slot << 8.
+constexpr int kPjHeader = 272;
 
 struct PjArgs {
   const int64_t* __restrict__ part_sub_start;
@@ -50,9 +52,8 @@ struct PjArgs {
   int n_stages;
 };
 
-// Tile of one triple: sum_r A[r][8 mt + m] B[r][8 nt + n] over the block rows,
-// A/B in the stage at (row stride as/bs).  Lane (gid, tig) returns
-// D[gid][2 tig], D[gid][2 tig + 1].  Four independent DMMA chains.
+// sum_r A[r][0:acols] B[r][0:bcols] of one triple tile, added to (x, y):
+// lane (gid, tig) holds D[gid][2 tig + {0,1}].  Four independent DMMA chains.
 __device__ __forceinline__ void triple_tile(const double* S, const int4 d, int gid, int tig,
                                             double& x, double& y) {
   const int rows = d.z & 0xffff;
@@ -78,15 +79,19 @@ __device__ __forceinline__ void triple_tile(const double* S, const int4 d, int g
     const double a0 = (am && ok) ? A[r0 * as] : 0.0, b0 = (bm && ok) ? B[r0 * bs] : 0.0;
     dmma_8x8x4(c0, c1, a0, b0);
   }
-  x = (c0 + c2) + (c4 + c6);
-  y = (c1 + c3) + (c5 + c7);
+  x += (c0 + c2) + (c4 + c6);
+  y += (c1 + c3) + (c5 + c7);
+}
+
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kPjWarps * 32) : "memory");
 }
 
 __global__ void __launch_bounds__(kPjThreads, 1) pj_stream_kernel(const PjArgs g) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[kPjMaxStages], empty[kPjMaxStages];
-  double* slots = smem;
-  char* stages = reinterpret_cast<char*>(smem + kPjSlotDoubles);
+  double* results = smem;
+  char* stages = reinterpret_cast<char*>(smem + kPjResultDoubles);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t s0 = g.part_sub_start[blockIdx.x], s1 = g.part_sub_start[blockIdx.x + 1];
   const int NS = g.n_stages;
@@ -96,7 +101,6 @@ __global__ void __launch_bounds__(kPjThreads, 1) pj_stream_kernel(const PjArgs g
       mbar_init(&empty[k], kPjWarps);
     }
   }
-  for (int i = threadIdx.x; i < kPjSlotDoubles; i += blockDim.x) slots[i] = 0.0;
   __syncthreads();
 
   if (warp == kPjWarps) {
@@ -106,7 +110,9 @@ __global__ void __launch_bounds__(kPjThreads, 1) pj_stream_kernel(const PjArgs g
   }
 
   const int gid = lane >> 2, tig = lane & 3;
-  double* mine = slots + warp * kPjSlots * 64 + 2 * lane;
+  double acc[kPjSlots][2];  // this warp's owned output tiles (registers)
+#pragma unroll
+  for (int k = 0; k < kPjSlots; ++k) acc[k][0] = acc[k][1] = 0.0;
   for (int64_t i = 0; i < s1 - s0; ++i) {
     const int st = (int)(i % NS);
     mbar_wait(&full[st], (unsigned)((i / NS) & 1));
@@ -114,27 +120,43 @@ __global__ void __launch_bounds__(kPjThreads, 1) pj_stream_kernel(const PjArgs g
     const int* hdr = reinterpret_cast<const int*>(stg);
     const int4* tri = reinterpret_cast<const int4*>(stg + kPjHeader);
     const double* S = reinterpret_cast<const double*>(stg);
-    const int t0 = hdr[warp], t1 = hdr[warp + 1];
-    const int item = hdr[17], flush = hdr[18];
-    const int n_slots = hdr[20 + warp];
-    for (int t = t0; t < t1; ++t) {
-      const int4 d = tri[t];
-      double x, y;
-      triple_tile(S, d, gid, tig, x, y);
-      double2* q = reinterpret_cast<double2*>(mine + ((d.z >> 16) & 0xff) * 64);
-      double2 v = *q;
-      v.x += x;
-      v.y += y;
-      *q = v;
+    double* R = results + (i & 1) * (kPjUnits * 64);
+    // 1) compute this warp's units (balanced per sub-chunk on the host)
+    const int t1 = hdr[warp + 1];
+    int t = hdr[warp];
+    while (t < t1) {
+      const int unit = (tri[t].z >> 16) & 0xff;
+      double x = 0.0, y = 0.0;
+      do {
+        triple_tile(S, tri[t], gid, tig, x, y);
+        ++t;
+      } while (t < t1 && ((tri[t].z >> 16) & 0xff) == unit);
+      reinterpret_cast<double2*>(R + unit * 64)[lane] = make_double2(x, y);
     }
+    consumer_sync();  // all unit results of this sub-chunk are in R
+    // 2) owners add the unit results into their register tiles
+    const int n_units = hdr[19];
+    for (int u = 0; u < n_units; ++u) {
+      const int ow = hdr[36 + u];
+      if ((ow & 0xff) != warp) continue;
+      const int slot = ow >> 8;
+      const double2 v = reinterpret_cast<const double2*>(R + u * 64)[lane];
+#pragma unroll
+      for (int k = 0; k < kPjSlots; ++k)
+        if (k == slot) {
+          acc[k][0] += v.x;
+          acc[k][1] += v.y;
+        }
+    }
+    const int item = hdr[17], flush = hdr[18], n_slots = hdr[20 + warp];
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
     if (flush) {  // last sub-chunk of the item: write this warp's tiles once, clear them
-      double* P = g.partial + ((int64_t)item * kPjWarps + warp) * kPjSlots * 64 + 2 * lane;
-      for (int k = 0; k < n_slots; ++k) {
-        double2* q = reinterpret_cast<double2*>(mine + k * 64);
-        *reinterpret_cast<double2*>(P + k * 64) = *q;
-        *q = make_double2(0.0, 0.0);
+      double* P = g.partial + ((int64_t)item * kPjWarps + warp) * kPjSlots * 64;
+#pragma unroll
+      for (int k = 0; k < kPjSlots; ++k) {
+        if (k < n_slots) reinterpret_cast<double2*>(P + k * 64)[lane] = make_double2(acc[k][0], acc[k][1]);
+        acc[k][0] = acc[k][1] = 0.0;
       }
     }
   }
@@ -217,7 +239,7 @@ int validate_tmmult(const bmv_tmmult_desc* d) {
           m = d->meta + src / 4;
           const int n_tri = m[kPjWarps];
           if (m[0] != 0 || n_tri < 0 || kPjHeader + 16 * (int64_t)n_tri > len || m[17] < 0 ||
-              m[17] >= d->n_items) {
+              m[17] >= d->n_items || m[19] < 0 || m[19] > kPjUnits) {
             set_error("tmmult header of sub-chunk %lld is malformed", (long long)s);
             return BMV_ERR_INVALID;
           }
@@ -226,14 +248,19 @@ int validate_tmmult(const bmv_tmmult_desc* d) {
               set_error("tmmult header of sub-chunk %lld is malformed", (long long)s);
               return BMV_ERR_INVALID;
             }
+          for (int u = 0; u < m[19]; ++u)
+            if ((m[36 + u] & 0xff) >= kPjWarps || (m[36 + u] >> 8) >= kPjSlots) {
+              set_error("tmmult unit owner of sub-chunk %lld out of range", (long long)s);
+              return BMV_ERR_INVALID;
+            }
           for (int t = 0; t < n_tri; ++t) {
             const int32_t* q4 = m + kPjHeader / 4 + 4 * t;
-            const int rows = q4[2] & 0xffff, slot = (q4[2] >> 16) & 0xff;
+            const int rows = q4[2] & 0xffff, unit = (q4[2] >> 16) & 0xff;
             const int ac = (q4[2] >> 24) & 15, bc = ((unsigned)q4[2] >> 28) & 15;
             const int as = q4[3] & 0xffff, bs = ((unsigned)q4[3] >> 16) & 0xffff;
             const int64_t a_end = 8 * ((int64_t)q4[0] + (int64_t)(rows - 1) * as + ac);
             const int64_t b_end = 8 * ((int64_t)q4[1] + (int64_t)(rows - 1) * bs + bc);
-            if (q4[0] < 0 || q4[1] < 0 || slot >= kPjSlots || ac > 8 || bc > 8 ||
+            if (q4[0] < 0 || q4[1] < 0 || unit >= m[19] || ac > 8 || bc > 8 ||
                 (rows > 0 && (a_end > d->stage_bytes || b_end > d->stage_bytes))) {
               set_error("tmmult triple tile %d of sub-chunk %lld out of range", t, (long long)s);
               return BMV_ERR_INVALID;
@@ -293,7 +320,7 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
   int dev = 0, max_smem = 0;
   BMV_CUDA_TRY(cudaGetDevice(&dev));
   BMV_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const int avail = max_smem - 1024 - kPjSlotDoubles * 8;
+  const int avail = max_smem - 1024 - kPjResultDoubles * 8;
   const int ns = std::min(kPjMaxStages, avail / d->stage_bytes);
   if (ns < 2) {
     set_error("tmmult stage of %d bytes leaves fewer than 2 pipeline stages", d->stage_bytes);
@@ -306,7 +333,7 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
   p->n_tiles = d->n_out_tiles;
   p->stage_bytes = d->stage_bytes;
   p->n_stages = ns;
-  p->smem_bytes = kPjSlotDoubles * 8 + ns * d->stage_bytes;
+  p->smem_bytes = kPjResultDoubles * 8 + ns * d->stage_bytes;
   for (int64_t t = 0; t < d->n_out_tiles; ++t) {
     const int32_t* q = d->tile_shape + 3 * t;
     if (q[0] > 0 && q[1] > 0)
@@ -328,7 +355,7 @@ int bmv_tmmult_create(const bmv_tmmult_desc* d, bmv_tmmult** out) {
   }
   if (!rc) {
     const cudaError_t e = cudaFuncSetAttribute(pj_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               p->smem_bytes);
+                                               max_smem - 1024);
     if (e != cudaSuccess) {
       set_error("cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
       rc = BMV_ERR_CUDA;

@@ -1,0 +1,6 @@
+set -x
+timeout 600 python -m pytest tests -m "gpu and not slow" -x -q > gpurun_out/gpu18_pytest.log 2>&1; echo "pytest rc $?" >> gpurun_out/gpu18_pytest.log
+for cfg in q2 q4 proj weak1; do timeout 600 python scripts/spmm_timing.py $cfg 10 >> gpurun_out/gpu18_spmm.log 2>&1; done
+timeout 300 python scripts/spmm_timing.py weak1 3 > gpurun_out/gpu18_plain.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pj_stream|pm_stream" -s 2 -c 2 -o gpurun_out/gpu18_w1 python scripts/spmm_timing.py weak1 3 > gpurun_out/gpu18_ncu.log 2>&1
+timeout 900 python -m pytest tests -m "gpu and slow" -x -q > gpurun_out/gpu18_pytest_slow.log 2>&1; echo "pytest rc $?" >> gpurun_out/gpu18_pytest_slow.log

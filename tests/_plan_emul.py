@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import numpy as np
 
-PJ_WARPS, PJ_SLOTS, PJ_HDR = 16, 8, 144
+PJ_WARPS, PJ_SLOTS, PJ_HDR = 16, 8, 272
 PM_WARPS = 16
 
 
@@ -62,23 +62,36 @@ def emulate_tmmult(arr, a_data, b_data, c_len):
     for s, ents in _subs(arr):
         buf, mask = _stage(ents, srcs, sb)
         hdr = buf[:PJ_HDR].view(np.int32)
-        n_tri = int(hdr[PJ_WARPS])
+        n_tri, n_units = int(hdr[PJ_WARPS]), int(hdr[19])
         tri = buf[PJ_HDR:PJ_HDR + 16 * n_tri].view(np.int32).reshape(-1, 4).astype(np.int64) & 0xFFFFFFFF
+        res = np.full((32, 8, 8), np.nan)
+        done = np.zeros(32, dtype=bool)
         for w in range(PJ_WARPS):
-            for t in range(hdr[w], hdr[w + 1]):
-                x, y, z, ww = tri[t]
-                rows, slot, ac, bc = z & 0xFFFF, (z >> 16) & 0xFF, (z >> 24) & 15, (z >> 28) & 15
-                a_s, b_s = ww & 0xFFFF, ww >> 16
-                assert slot < PJ_SLOTS
-                am = np.stack([_dbl(buf, mask, x + r * a_s, ac) for r in range(rows)])
-                bm = np.stack([_dbl(buf, mask, y + r * b_s, bc) for r in range(rows)])
-                slots[w, slot, :ac, :bc] += am.T @ bm
+            t, t1 = int(hdr[w]), int(hdr[w + 1])
+            while t < t1:
+                unit = (tri[t][2] >> 16) & 0xFF
+                assert unit < n_units and not done[unit], "unit computed twice"
+                acc = np.zeros((8, 8))
+                while t < t1 and ((tri[t][2] >> 16) & 0xFF) == unit:
+                    x, y, z, ww = tri[t]
+                    rows, ac, bc = z & 0xFFFF, (z >> 24) & 15, (z >> 28) & 15
+                    a_s, b_s = ww & 0xFFFF, ww >> 16
+                    am = np.stack([_dbl(buf, mask, x + r * a_s, ac) for r in range(rows)])
+                    bm = np.stack([_dbl(buf, mask, y + r * b_s, bc) for r in range(rows)])
+                    acc[:ac, :bc] += am.T @ bm
+                    t += 1
+                res[unit] = acc
+                done[unit] = True
+        assert done[:n_units].all(), "unit never computed"
+        for u in range(n_units):
+            ow = int(hdr[36 + u])
+            slots[ow & 0xFF, ow >> 8] += res[u]
         if hdr[18]:
             it = int(hdr[17])
             for w in range(PJ_WARPS):
                 for k in range(hdr[20 + w]):
                     partial[(it * PJ_WARPS + w) * PJ_SLOTS + k] = slots[w, k]
-                    slots[w, k] = 0.0
+                slots[w] = 0.0
     assert not slots.any(), "slot left unflushed"
     c = np.zeros(c_len)
     shp = arr["tile_shape"].reshape(-1, 3)
@@ -96,7 +109,7 @@ def emulate_tmmult(arr, a_data, b_data, c_len):
 def emulate_mmult(arr, a_data, b_data, c_data, alpha=1.0, accumulate=False):
     c = c_data.copy() if accumulate else np.zeros_like(c_data)
     written = np.zeros(c.size, dtype=bool)
-    srcs = [arr["meta"].view(np.uint8), a_data.view(np.uint8), b_data.view(np.uint8)]
+    srcs = [arr["meta"].view(np.uint8), a_data.view(np.uint8), None]
     sb = int(arr["stage_bytes"])
     for s, ents in _subs(arr):
         buf, mask = _stage(ents, srcs, sb)
@@ -104,17 +117,19 @@ def emulate_mmult(arr, a_data, b_data, c_data, alpha=1.0, accumulate=False):
         meta = buf[16:].view(np.int32)
         tasks = meta[:4 * nt].reshape(-1, 4).astype(np.int64) & 0xFFFFFFFF
         for k in range(nt):
-            off, y, z, mi = tasks[k]
-            rv, cv, ni, ys = y & 15, (y >> 4) & 15, (y >> 8) & 15, y >> 16
+            off, y, z, mi0 = tasks[k]
+            rows, cv, ni, ys = y & 0x7F, (y >> 8) & 15, (y >> 12) & 15, y >> 16
             p0, npairs = z & 0xFFFF, z >> 16
-            acc = np.zeros((rv, cv))
+            assert rows <= 64 and cv <= 8
+            acc = np.zeros((rows, cv))
             for p in range(p0, p0 + npairs):
                 q = meta[4 * (nt + p): 4 * (nt + p) + 4].astype(np.int64)
-                a_s, inner, bs = q[1] & 0xFFFF, q[1] >> 16, q[2]
-                am = np.stack([_dbl(buf, mask, q[0] + (8 * mi + r) * a_s, inner) for r in range(rv)])
-                bm = np.stack([_dbl(buf, mask, q[3] + kk * bs + 8 * ni, cv) for kk in range(inner)])
+                a_s, inner, bs, boff = q[1] & 0xFFFF, q[1] >> 16, q[2], q[3]
+                am = np.stack([_dbl(buf, mask, q[0] + (8 * mi0 + r) * a_s, inner) for r in range(rows)])
+                bm = np.stack([b_data[boff + kk * bs + 8 * ni: boff + kk * bs + 8 * ni + cv]
+                               for kk in range(inner)])
                 acc += am @ bm
-            for i in range(rv):
+            for i in range(rows):
                 o = off + i * ys
                 assert not written[o:o + cv].any(), "output written twice"
                 written[o:o + cv] = True

@@ -161,13 +161,15 @@ int bmv_tmmult_run(bmv_tmmult* plan, const double* a, const double* b, double* c
 /* ------------------------------------------------------------------ K5 --
  * Y_ij (+)= alpha * sum_k A_ik B_kj, truncated to Y's pattern.
  * Stage = [header int4 {n_tasks, 0, 0, 0}][tasks (4 x int32)][pairs
- * (4 x int32)][B blocks used by the pairs][A blocks of the rows].
- * Task = one 8x8 output tile: {element offset of the tile in Y, rows |
- * cols << 4 | col-tile << 8 | Y row stride << 16, first pair (index into
- * the staged pairs) | pairs << 16, row-tile}.  Pair: {A block offset,
- * a_stride | inner << 16, b_stride, B block offset} (offsets in doubles
- * from the stage start).  16 consumer warps take the tasks round-robin and
- * store each tile once.                                                   */
+ * (4 x int32)][A blocks of the rows]; copy entries: metadata, A range.
+ * Task = up to 64 rows x one 8-column tile of an output block: {element
+ * offset of the tile's first row in Y (< 2^32), rows | cols << 8 |
+ * col-tile << 12 | Y row stride << 16, first pair (index into the staged
+ * pairs) | pairs << 16, first 8-row tile in the block}.  Pair: {A block
+ * offset in the stage (doubles), a_stride | inner << 16, b_stride, B block
+ * offset in b (< 2^31)}.  15 consumer warps take the tasks round-robin
+ * (B fragments through L1/L2, prefetched one pair ahead) and store every
+ * output value once.                                                     */
 typedef struct {
   int32_t n_parts;           /* CTAs                                       */
   int32_t stage_bytes;       /* capacity of one pipeline stage (16 | it)   */

@@ -26,7 +26,7 @@ using namespace bmv;
 
 namespace {
 
-constexpr int kPmWarps = 16;
+constexpr int kPmWarps = 15;  // + the producer: 16 warps, 4 per SM sub-partition
 constexpr int kPmThreads = (kPmWarps + 1) * 32;
 constexpr int kPmMaxStages = 8;
 
@@ -98,8 +98,7 @@ __device__ __forceinline__ void task_tiles(const double* S, const int4* pairs, c
   }
 }
 
-// 17 warps x 120 registers fill the register file; __launch_bounds__ would cap at 96.
-__global__ void __maxnreg__(120) pm_stream_kernel(const PmArgs g) {
+__global__ void __launch_bounds__(kPmThreads, 1) pm_stream_kernel(const PmArgs g) {
   extern __shared__ __align__(128) char stages[];
   __shared__ __align__(8) uint64_t full[kPmMaxStages], empty[kPmMaxStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -112,8 +112,8 @@ int bmv_cellop_launches(const bmv_cellop* plan, int32_t* out);
  * warps on FP64 tensor cores.  What one sub-chunk stages is a copy list:
  * entries of 4 x int32 {dst byte offset in the stage, bytes | src << 28 |
  * last << 30, src byte offset lo, hi}; src 0 = the plan's metadata array,
- * 1 = operand a, 2 = operand b; <= 32 consecutive entries per sub-chunk,
- * the last one flagged; the first entry stages the sub-chunk's metadata
+ * 1 = operand a, 2 = operand b; consecutive entries per sub-chunk, the
+ * last one flagged; the first entry stages the sub-chunk's metadata
  * (header + work descriptors) at offset 0.  Entries 16-byte aligned go
  * through cp.async.bulk, others are copied by the producer's lanes.       */
 
@@ -161,15 +161,15 @@ int bmv_tmmult_run(bmv_tmmult* plan, const double* a, const double* b, double* c
 /* ------------------------------------------------------------------ K5 --
  * Y_ij (+)= alpha * sum_k A_ik B_kj, truncated to Y's pattern.
  * Stage = [header int4 {n_tasks, 0, 0, 0}][tasks (4 x int32)][pairs
- * (4 x int32)][A blocks of the rows]; copy entries: metadata, A range.
+ * (4 x int32)][B blocks used by the pairs][A blocks of the rows]; copy
+ * entries: metadata, one per B block, A range.
  * Task = up to 64 rows x one 8-column tile of an output block: {element
  * offset of the tile's first row in Y (< 2^32), rows | cols << 8 |
  * col-tile << 12 | Y row stride << 16, first pair (index into the staged
  * pairs) | pairs << 16, first 8-row tile in the block}.  Pair: {A block
  * offset in the stage (doubles), a_stride | inner << 16, b_stride, B block
- * offset in b (< 2^31)}.  15 consumer warps take the tasks round-robin
- * (B fragments through L1/L2, prefetched one pair ahead) and store every
- * output value once.                                                     */
+ * offset in the stage (doubles)}.  15 consumer warps take the tasks
+ * round-robin and store every output value once.                         */
 typedef struct {
   int32_t n_parts;           /* CTAs                                       */
   int32_t stage_bytes;       /* capacity of one pipeline stage (16 | it)   */

@@ -756,8 +756,8 @@ def mmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n
     pa, pb = pa[order], pb[order]
     n_out = int(outs.size)
     # ---- streaming plan (csrc/bmv_postmul.cu) ------------------------------
-    # stage = [header][tasks][pairs][A blocks]; a task = up to 8 row tiles x
-    # one 8-column tile of an output block; B read through L1/L2
+    # stage = [header][tasks][pairs][B blocks][A blocks]; a task = up to 8 row
+    # tiles x one 8-column tile of an output block
     n_rows = a.n_owned_blocks
     a_row_lo = a.block_offsets[a.row_start[:n_rows]]
     a_row_hi = a.block_offsets[a.row_start[1 : n_rows + 1]]
@@ -771,14 +771,16 @@ def mmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n
     tn = (out_cols + 7) // 8
     if n_out and (int(tn.max()) > 16 or int(c_str.max()) >= 1 << 16):
         raise ShapeError("mmult output blocks wider than 128 columns are not supported")
-    b_off = b.block_offsets[pb].astype(np.int64)
-    if b_off.size and int(b_off.max()) >= 1 << 31:
-        raise ShapeError("mmult b holds more than 2^31 values")
     np_o = np.diff(start).astype(np.int64)
     pair_row = out_row[per] if pa.size else np.zeros(0, np.int64)
+    b_size = (b.block_offsets[pb + 1] - b.block_offsets[pb]).astype(np.int64)
+    b_bytes = 8 * b_size + (8 * b_size) % 16
+    nbk = int(b.pos_row.size) + 1
+    rk, r_first = np.unique(pair_row * nbk + pb, return_index=True)
+    row_cbytes = np.bincount(rk // nbk, weights=b_bytes[r_first], minlength=n_rows).astype(np.int64)
     row_tasks = np.bincount(out_row, weights=tm * tn, minlength=n_rows).astype(np.int64)
     row_pairs = np.bincount(pair_row, minlength=n_rows).astype(np.int64)
-    row_bytes = 8 * row_dbl + 16 * (row_tasks + row_pairs)
+    row_bytes = 8 * row_dbl + 16 * (row_tasks + row_pairs) + row_cbytes
     # parts balanced by A + Y doubles; sub-chunks of consecutive rows
     y_dbl = np.bincount(out_row, weights=out_rows * c_str, minlength=n_rows).astype(np.int64)
     w = row_dbl + y_dbl
@@ -811,7 +813,15 @@ def mmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n
     if n_sub and int(max(np_o.max(initial=0), n_pairs_sub.max())) >= 1 << 16:
         raise ShapeError("mmult sub-chunk holds more than 65535 products")
     meta_bytes = 16 * (1 + n_tasks_sub + n_pairs_sub)
-    a_off = meta_bytes
+    # distinct B blocks per sub-chunk, staged after the metadata
+    p_sub = o_sub[per] if pa.size else np.zeros(0, np.int64)
+    sk, s_first, p_cb = np.unique(p_sub * nbk + pb, return_index=True, return_inverse=True)
+    cb_sub, cb_pb, cb_bytes = sk // nbk, sk % nbk, b_bytes[s_first]
+    n_cb_sub = np.bincount(cb_sub, minlength=n_sub).astype(np.int64)
+    cb_first = np.concatenate([[0], np.cumsum(n_cb_sub)]).astype(np.int64)
+    cb_cum = np.concatenate([[0], np.cumsum(cb_bytes)]).astype(np.int64)
+    cb_soff = meta_bytes[cb_sub] + cb_cum[:-1] - cb_cum[cb_first[cb_sub]]
+    a_off = meta_bytes + cb_cum[cb_first[1:]] - cb_cum[cb_first[:-1]]
     na_sub = sub_a[:, 1] - sub_a[:, 0]
     stage_bytes = int((a_off + 8 * na_sub).max(initial=16))
     stage_bytes += (-stage_bytes) % 16
@@ -833,21 +843,29 @@ def mmult_plan_arrays(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, n
     meta[tpos + 3] = _PM_ROW_TILES * t_mi
     a_str = a.col_strides[a.col_index[pa]].astype(np.int64)
     inner = a.col_blocks.sizes[a.col_index[pa]].astype(np.int64)
-    p_sub = o_sub[per] if pa.size else np.zeros(0, np.int64)
     ppos = meta_off[p_sub] + 4 * (1 + n_tasks_sub[p_sub] + np.arange(pa.size) - start[o_lo[p_sub]])
     meta[ppos] = a_off[p_sub] // 8 + a.block_offsets[pa] - sub_a[p_sub, 0]
     meta[ppos + 1] = a_str | (inner << 16)
     meta[ppos + 2] = b.col_strides[b.col_index[pb]]
-    meta[ppos + 3] = b_off
+    meta[ppos + 3] = cb_soff[p_cb] // 8
     meta = (meta & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
-    copies = np.zeros((n_sub, 2, 4), dtype=np.int64)
-    copies[:, 0, 1], copies[:, 0, 2] = meta_bytes, 4 * meta_off[:-1]
-    copies[:, 1, 0], copies[:, 1, 1], copies[:, 1, 2] = a_off, 8 * na_sub | (1 << 28) | (1 << 30), \
-        8 * sub_a[:, 0]
+    # copy lists: metadata, B blocks, A range (last)
+    e_first = np.concatenate([[0], np.cumsum(2 + n_cb_sub)]).astype(np.int64)
+    copies = np.zeros((int(e_first[-1]), 4), dtype=np.int64)
+    copies[e_first[:-1], 1] = meta_bytes
+    copies[e_first[:-1], 2] = 4 * meta_off[:-1]
+    cpos = e_first[cb_sub] + 1 + np.arange(cb_sub.size) - cb_first[cb_sub]
+    copies[cpos, 0] = cb_soff
+    copies[cpos, 1] = 8 * b_size[s_first] | (2 << 28)
+    copies[cpos, 2] = 8 * b.block_offsets[cb_pb]
+    last = e_first[1:] - 1
+    copies[last, 0] = a_off
+    copies[last, 1] = 8 * na_sub | (1 << 28) | (1 << 30)
+    copies[last, 2] = 8 * sub_a[:, 0]
     arrays = dict(
         n_parts=n_parts, stage_bytes=stage_bytes, n_sub=n_sub,
-        part_sub_start=part_sub_start, part_entry_start=2 * part_sub_start,
-        copies=_pack_copies(copies.reshape(-1, 4)), meta=meta,
+        part_sub_start=part_sub_start, part_entry_start=e_first[part_sub_start],
+        copies=_pack_copies(copies), meta=meta,
     )
     flops = int(2 * np.sum(out_rows[per] * inner * out_cols[per]))
     n_own_c = int(c.row_start[c.n_owned_blocks])
@@ -1205,7 +1223,6 @@ _PJ_HDR = 272        # bytes of the K4 stage header (kPjHeader)
 # -> 4 stages + 32 KB of unit results per SM
 _PJ_STAGE = (49152 - _PJ_HDR - 16 * 4 * _PJ_UNITS) // 8
 _PM_STAGE_BYTES = 40960   # K5 stage target (5 stages per SM)
-_CP_MAX = 32              # copy entries per sub-chunk (kCpMaxPerSub)
 _PM_ROW_TILES = 8         # 8-row tiles per K5 task (kPmRowTiles)
 
 

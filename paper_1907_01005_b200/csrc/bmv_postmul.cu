@@ -34,8 +34,7 @@ struct PmArgs {
   const int64_t* __restrict__ part_sub_start;
   const int64_t* __restrict__ part_entry_start;
   const int4* __restrict__ copies;
-  CopySrc src;  // p0 = meta, p1 = a
-  const double* __restrict__ b;
+  CopySrc src;  // p0 = meta, p1 = a, p2 = b
   double* __restrict__ c;
   double alpha;
   int accumulate;
@@ -45,55 +44,30 @@ struct PmArgs {
 
 constexpr int kPmRowTiles = 8;  // 8-row tiles per task (64 rows)
 
-// B fragments of one pair (up to 16 inner rows = 4 k-steps): lane (gid, tig)
-// holds B[4 ks + tig][8 ni + gid].
-__device__ __forceinline__ void load_b(const double* __restrict__ b, const int4 d, int k0, int ni,
-                                       int gid, int tig, bool bm, double (&f)[4]) {
-  const int inner = (d.y >> 16) & 0xffff, bs = d.z;
-  const double* B = b + (uint32_t)d.w + (int64_t)(k0 + tig) * bs + 8 * ni + gid;
-#pragma unroll
-  for (int ks = 0; ks < 4; ++ks)
-    f[ks] = (bm && k0 + 4 * ks + tig < inner) ? __ldg(B + (int64_t)4 * ks * bs) : 0.0;
-}
-
 // One task = up to 8 row tiles x one 8-column tile of an output block:
-// acc[m] += sum_pairs A[8 (mi0 + m) + gid][k] B[k][8 ni + 2 tig + {0,1}].
-// B fragments (global, L1/L2) of pair p + 1 are loaded while pair p runs.
+// acc[m] += sum_pairs A[8 (mi0 + m) + gid][k] B[k][8 ni + 2 tig + {0,1}],
+// A and B blocks both in the stage.
 __device__ __forceinline__ void task_tiles(const double* S, const int4* pairs, const int4 t,
-                                           const double* __restrict__ b, int gid, int tig,
-                                           double (&acc)[kPmRowTiles][2]) {
+                                           int gid, int tig, double (&acc)[kPmRowTiles][2]) {
   const int rows = t.y & 0x7f, cv = (t.y >> 8) & 15, ni = (t.y >> 12) & 15;
   const int p0 = t.z & 0xffff, np = (t.z >> 16) & 0xffff;
   const bool bm = gid < cv;
   const int nm = (rows + 7) >> 3;
-  double fb[4], fn[4];
-  if (np > 0) load_b(b, pairs[p0], 0, ni, gid, tig, bm, fb);
   for (int p = p0; p < p0 + np; ++p) {
     const int4 d = pairs[p];
-    const int as = d.y & 0xffff, inner = (d.y >> 16) & 0xffff;
-    for (int k0 = 0; k0 < inner; k0 += 16) {
-      // prefetch the next fragments: this pair's next 16 rows or the next pair
-      const bool more = k0 + 16 < inner;
-      if (more)
-        load_b(b, d, k0 + 16, ni, gid, tig, bm, fn);
-      else if (p + 1 < p0 + np)
-        load_b(b, pairs[p + 1], 0, ni, gid, tig, bm, fn);
-      const double* A = S + d.x + (8 * t.w + gid) * as + k0 + tig;
+    const int as = d.y & 0xffff, inner = (d.y >> 16) & 0xffff, bs = d.z;
+    const double* A = S + d.x + (8 * t.w + gid) * as + tig;
+    const double* B = S + d.w + tig * bs + 8 * ni + gid;
+    for (int k0 = 0; k0 < inner; k0 += 4) {
+      const bool ok = k0 + tig < inner;
+      const double bk = (bm && ok) ? B[k0 * bs] : 0.0;
 #pragma unroll
       for (int m = 0; m < kPmRowTiles; ++m) {
         if (m < nm) {
-          const bool am = 8 * m + gid < rows;
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            if (k0 + 4 * ks < inner) {
-              const double a = (am && k0 + 4 * ks + tig < inner) ? A[8 * m * as + 4 * ks] : 0.0;
-              dmma_8x8x4(acc[m][0], acc[m][1], a, fb[ks]);
-            }
-          }
+          const double a = (8 * m + gid < rows && ok) ? A[8 * m * as + k0] : 0.0;
+          dmma_8x8x4(acc[m][0], acc[m][1], a, bk);
         }
       }
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) fb[ks] = fn[ks];
     }
   }
 }
@@ -133,7 +107,7 @@ __global__ void __launch_bounds__(kPmThreads, 1) pm_stream_kernel(const PmArgs g
       double acc[kPmRowTiles][2];
 #pragma unroll
       for (int m = 0; m < kPmRowTiles; ++m) acc[m][0] = acc[m][1] = 0.0;
-      task_tiles(S, pairs, t, g.b, gid, tig, acc);
+      task_tiles(S, pairs, t, gid, tig, acc);
       const int rows = t.y & 0x7f, cv = (t.y >> 8) & 15, ys = (t.y >> 16) & 0xffff;
       const int col = 2 * tig;
       const bool two = col + 1 < cv;
@@ -188,7 +162,7 @@ int validate_mmult(const bmv_mmult_desc* d, int64_t* c_extent) {
     for (int64_t s = d->part_sub_start[p]; s < d->part_sub_start[p + 1]; ++s) {
       const int64_t first = e;
       for (;; ++e) {
-        if (e >= e1 || e - first >= kCpMaxPerSub) {
+        if (e >= e1) {
           set_error("mmult copy list of sub-chunk %lld is malformed", (long long)s);
           return BMV_ERR_INVALID;
         }
@@ -226,9 +200,13 @@ int validate_mmult(const bmv_mmult_desc* d, int64_t* c_extent) {
               *c_extent = std::max<int64_t>(*c_extent, (int64_t)(uint32_t)t[0] + (int64_t)(rows - 1) * ys + cv);
             for (int pp = p0; pp < p0 + np; ++pp) {
               const int32_t* q4 = m + 4 * (1 + nt + pp);
-              const int as = q4[1] & 0xffff, inner = ((unsigned)q4[1] >> 16) & 0xffff;
+              const int as = q4[1] & 0xffff, inner = ((unsigned)q4[1] >> 16) & 0xffff, bs = q4[2];
+              const int ni = (t[1] >> 12) & 15;
               const int64_t a_end = 8 * ((int64_t)q4[0] + (int64_t)(8 * t[3] + rows - 1) * as + inner);
-              if (q4[0] < 0 || q4[2] < 0 || q4[3] < 0 || (rows > 0 && inner > 0 && a_end > d->stage_bytes)) {
+              const int64_t b_end = 8 * ((int64_t)q4[3] + (int64_t)(inner - 1) * bs + 8 * ni + cv);
+              if (q4[0] < 0 || bs < 0 || q4[3] < 0 ||
+                  (rows > 0 && inner > 0 && a_end > d->stage_bytes) ||
+                  (cv > 0 && inner > 0 && b_end > d->stage_bytes)) {
                 set_error("mmult pair %d of sub-chunk %lld out of range", pp, (long long)s);
                 return BMV_ERR_INVALID;
               }
@@ -326,8 +304,8 @@ int bmv_mmult_run(bmv_mmult* p, const double* a, const double* b, double* c, dou
   if (p->n_sub == 0 || p->n_parts == 0) return BMV_OK;
   PmArgs g{p->part_sub_start, p->part_entry_start, reinterpret_cast<const int4*>(p->copies),
            CopySrc{reinterpret_cast<const char*>(p->meta), reinterpret_cast<const char*>(a),
-                   nullptr},
-           b, c, alpha, accumulate, p->stage_bytes, p->n_stages};
+                   reinterpret_cast<const char*>(b)},
+           c, alpha, accumulate, p->stage_bytes, p->n_stages};
   pm_stream_kernel<<<(unsigned)p->n_parts, kPmThreads, p->smem_bytes, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;

@@ -64,6 +64,7 @@ __device__ __forceinline__ void triple_tile(const double* S, const int4 d, int g
   const double* B = S + d.y + gid + tig * bs;
   double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0, c4 = 0.0, c5 = 0.0, c6 = 0.0, c7 = 0.0;
   int r0 = 0;
+#pragma unroll 2
   for (; r0 + 16 <= rows; r0 += 16) {
     const double a0 = am ? A[r0 * as] : 0.0, b0 = bm ? B[r0 * bs] : 0.0;
     const double a1 = am ? A[(r0 + 4) * as] : 0.0, b1 = bm ? B[(r0 + 4) * bs] : 0.0;
@@ -136,10 +137,12 @@ __global__ void __launch_bounds__(kPjThreads, 1) pj_stream_kernel(const PjArgs g
     consumer_sync();  // all unit results of this sub-chunk are in R
     // 2) owners add the unit results into their register tiles
     const int n_units = hdr[19];
-    for (int u = 0; u < n_units; ++u) {
-      const int ow = hdr[36 + u];
-      if ((ow & 0xff) != warp) continue;
-      const int slot = ow >> 8;
+    const int ow = lane < n_units ? hdr[36 + lane] : -1;
+    unsigned mine_u = __ballot_sync(~0u, (ow & 0xff) == warp && lane < n_units);
+    while (mine_u) {
+      const int u = __ffs(mine_u) - 1;
+      mine_u &= mine_u - 1;
+      const int slot = __shfl_sync(~0u, ow, u) >> 8;
       const double2 v = reinterpret_cast<const double2*>(R + u * 64)[lane];
 #pragma unroll
       for (int k = 0; k < kPjSlots; ++k)
@@ -218,7 +221,7 @@ int validate_tmmult(const bmv_tmmult_desc* d) {
       const int64_t first = e;
       const int32_t* m = nullptr;
       for (;; ++e) {
-        if (e >= e1 || e - first >= kCpMaxPerSub) {
+        if (e >= e1) {
           set_error("tmmult copy list of sub-chunk %lld is malformed", (long long)s);
           return BMV_ERR_INVALID;
         }

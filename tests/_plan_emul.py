@@ -26,7 +26,7 @@ def _subs(arr):
             first = e
             ents = []
             while True:
-                assert e < pes[p + 1] and e - first < 32, "malformed copy list"
+                assert e < pes[p + 1], "malformed copy list"
                 ents.append(cps[e])
                 e += 1
                 if (ents[-1][1] >> 30) & 1:
@@ -109,7 +109,7 @@ def emulate_tmmult(arr, a_data, b_data, c_len):
 def emulate_mmult(arr, a_data, b_data, c_data, alpha=1.0, accumulate=False):
     c = c_data.copy() if accumulate else np.zeros_like(c_data)
     written = np.zeros(c.size, dtype=bool)
-    srcs = [arr["meta"].view(np.uint8), a_data.view(np.uint8), None]
+    srcs = [arr["meta"].view(np.uint8), a_data.view(np.uint8), b_data.view(np.uint8)]
     sb = int(arr["stage_bytes"])
     for s, ents in _subs(arr):
         buf, mask = _stage(ents, srcs, sb)
@@ -124,10 +124,9 @@ def emulate_mmult(arr, a_data, b_data, c_data, alpha=1.0, accumulate=False):
             acc = np.zeros((rows, cv))
             for p in range(p0, p0 + npairs):
                 q = meta[4 * (nt + p): 4 * (nt + p) + 4].astype(np.int64)
-                a_s, inner, bs, boff = q[1] & 0xFFFF, q[1] >> 16, q[2], q[3]
+                a_s, inner, bs = q[1] & 0xFFFF, q[1] >> 16, q[2]
                 am = np.stack([_dbl(buf, mask, q[0] + (8 * mi0 + r) * a_s, inner) for r in range(rows)])
-                bm = np.stack([b_data[boff + kk * bs + 8 * ni: boff + kk * bs + 8 * ni + cv]
-                               for kk in range(inner)])
+                bm = np.stack([_dbl(buf, mask, q[3] + kk * bs + 8 * ni, cv) for kk in range(inner)])
                 acc += am @ bm
             for i in range(rows):
                 o = off + i * ys

@@ -119,15 +119,20 @@ int bmv_cellop_launches(const bmv_cellop* plan, int32_t* out);
 
 /* ------------------------------------------------------------------ K4 --
  * C(k,l) = sum_i A_ik^T B_il over the owned block rows i.
- * Stage = [header (36 int32)][triple tiles (4 x int32)][A blocks][B blocks].
+ * Stage = [header (68 int32)][triple tiles (4 x int32)][A blocks][B blocks].
  * Header: [0..16] first triple tile of each of the 16 consumer warps
  * (local index) and the end, [17] item, [18] 1 on the item's last
- * sub-chunk, [20..35] slots used per warp in the item.
+ * sub-chunk, [19] units, [20..35] slots used per warp in the item,
+ * [36..67] unit -> owner warp | slot << 8.
  * Triple tile: {A tile offset, B tile offset (doubles from the stage
- * start), rows | slot << 16 | acols << 24 | bcols << 28, a_stride |
- * b_stride << 16}: sum_r A[r][0:acols] B[r][0:bcols] into the warp's slot.
- * An item (run of sub-chunks of one part) touches <= 16 x 8 output tiles,
- * each owned by one warp and written once to the partial buffer at
+ * start), rows | unit << 16 | acols << 24 | bcols << 28, a_stride |
+ * b_stride << 16}: sum_r A[r][0:acols] B[r][0:bcols].
+ * A unit is one 8x8 output tile touched by the sub-chunk (<= 32); the
+ * units are computed by the warps the host balanced them on, written to a
+ * shared result buffer, and after a barrier of the consumer warps added by
+ * the tile's owner warp into a register-resident accumulator.  An item
+ * (run of sub-chunks of one part) touches <= 16 x 8 output tiles; at its
+ * end each owner writes its tiles once to the partial buffer at
  * (item * 16 + warp) * 8 + slot; a second kernel sums every 8x8 output
  * tile's partials in item order (bit-reproducible, no atomics).          */
 typedef struct {

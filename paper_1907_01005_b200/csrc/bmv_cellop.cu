@@ -26,16 +26,9 @@
 #include <vector>
 
 #include "bmv_common.cuh"
+#include "bmv_sumfac.cuh"
 
 namespace bmv {
-
-struct CellTables {
-  double S[BMV_MAX_NODES * BMV_MAX_NODES];    // S[q*n + i]
-  double D[BMV_MAX_NODES * BMV_MAX_NODES];    // D_co[q*n + j]
-  double W2[BMV_MAX_NODES * BMV_MAX_NODES];   // w[a]*w[b]
-  double w[BMV_MAX_NODES];
-  double kin[3];
-};
 
 struct CellArgs {
   // per pair: {cell, first group index, lane | stride << 16, number of groups}
@@ -56,90 +49,6 @@ constexpr int kWarps = 4;  // warps per CTA
 #define BMV_K1_MINB5 3
 #endif
 
-// Contract along the fast (last) index of a [N][N] plane:
-// out[s][q] = sum_j M[q*N + j] * in[s][j]  (TR: M[j*N + q])
-template <int N, bool TR>
-__device__ __forceinline__ void contract_fast(const double (&in)[N][N], double (&out)[N][N],
-                                              const double* __restrict__ M) {
-#pragma unroll
-  for (int s = 0; s < N; ++s) {
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      double acc = 0.0;
-#pragma unroll
-      for (int j = 0; j < N; ++j) acc = fma(TR ? M[j * N + q] : M[q * N + j], in[s][j], acc);
-      out[s][q] = acc;
-    }
-  }
-}
-
-// Contract along the slow (first) index: out[q][f] = sum_j M[q*N+j] in[j][f]
-template <int N, bool TR>
-__device__ __forceinline__ void contract_slow(const double (&in)[N][N], double (&out)[N][N],
-                                              const double* __restrict__ M) {
-#pragma unroll
-  for (int q = 0; q < N; ++q) {
-#pragma unroll
-    for (int f = 0; f < N; ++f) {
-      double acc = 0.0;
-#pragma unroll
-      for (int j = 0; j < N; ++j) acc = fma(TR ? M[j * N + q] : M[q * N + j], in[j][f], acc);
-      out[q][f] = acc;
-    }
-  }
-}
-
-// Per-pair transpose tile: element (z, y, x) at z*BZ + y*BY + x, pairs TILE
-// apart.  Strides chosen by a half-warp bank model (64-bit accesses, 16
-// bank pairs per 128 B wavefront) for the pair-major lane mapping: N = 3, 4
-// conflict-free stores and loads (2 + 2 wavefronts), N = 5 2 + 3.
-template <int N> struct Tile;
-template <> struct Tile<2> { static constexpr int BY = 2, BZ = 4, TILE = 9; };
-template <> struct Tile<3> { static constexpr int BY = 5, BZ = 21, TILE = 63; };
-template <> struct Tile<4> { static constexpr int BY = 4, BZ = 20, TILE = 77; };
-#if defined(BMV_K1_TILE5_WIDE)
-template <> struct Tile<5> { static constexpr int BY = 7, BZ = 39, TILE = 195; };  // 2 + 2 wavefronts
-#else
-template <> struct Tile<5> { static constexpr int BY = 5, BZ = 27, TILE = 135; };  // 2 + 3 wavefronts
-#endif
-
-// A (z = t, [y][x]) -> B (y = t, [z][x]) through the pair tile.
-template <int N>
-__device__ __forceinline__ void a_to_b(const double (&a)[N][N], double (&b)[N][N],
-                                       double* buf, int t, bool store) {
-  using L = Tile<N>;
-  __syncwarp();
-  if (store) {
-#pragma unroll
-    for (int y = 0; y < N; ++y)
-#pragma unroll
-      for (int x = 0; x < N; ++x) buf[t * L::BZ + y * L::BY + x] = a[y][x];
-  }
-  __syncwarp();
-#pragma unroll
-  for (int z = 0; z < N; ++z)
-#pragma unroll
-    for (int x = 0; x < N; ++x) b[z][x] = buf[z * L::BZ + t * L::BY + x];
-}
-
-// B (y = t, [z][x]) -> A (z = t, [y][x]).
-template <int N>
-__device__ __forceinline__ void b_to_a(const double (&b)[N][N], double (&a)[N][N],
-                                       double* buf, int t, bool store) {
-  using L = Tile<N>;
-  __syncwarp();
-  if (store) {
-#pragma unroll
-    for (int z = 0; z < N; ++z)
-#pragma unroll
-      for (int x = 0; x < N; ++x) buf[z * L::BZ + t * L::BY + x] = b[z][x];
-  }
-  __syncwarp();
-#pragma unroll
-  for (int y = 0; y < N; ++y)
-#pragma unroll
-    for (int x = 0; x < N; ++x) a[y][x] = buf[t * L::BZ + y * L::BY + x];
-}
 
 constexpr int kMaxGroups = 32;  // distinct block rows per cell (<= 27 at L = 0)
 
@@ -161,21 +70,6 @@ struct CellSmem {
   }
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_one() {
-  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-}
 
 template <int N> struct MinBlocks { static constexpr int v = N >= 4 ? BMV_K1_MINB5 : (N == 3 ? 7 : 1); };
 
@@ -267,89 +161,31 @@ __global__ void __launch_bounds__(kWarps * 32, MinBlocks<N>::v)
     }
   }
 
-  // ---- values to the quadrature points
-  double v1[N][N], v2[N][N];
-  contract_fast<N, false>(u, v1, tb.S);   // x
-  contract_slow<N, false>(v1, v2, tb.S);  // y
-  a_to_b<N>(v2, v1, buf, tt, lane_ok);    // B: y = qy = t, [z][qx]
-  double uqB[N][N];
-  contract_slow<N, false>(v1, uqB, tb.S); // z -> uq at (qz, qy=t, qx)
-  cp_async_wait_all();
-  __syncwarp();
-
-  double acc[N][N];
+  double v2[N][N];
   if (KIN) {
-    // gy in A layout (qz = t)
-    b_to_a<N>(uqB, v1, buf, tt, lane_ok);  // v1 = uq[qz=t][qy][qx]
-    contract_slow<N, false>(v1, v2, tb.D);  // d/dy at the points
-    const double fy = tb.w[tt] * tb.kin[1];
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-#pragma unroll
-      for (int j = 0; j < N; ++j) v2[i][j] *= fy * tb.W2[i * N + j];
-    contract_slow<N, true>(v2, acc, tb.D);  // D^T along y
-    if (COEF) {
-#pragma unroll
-      for (int i = 0; i < N; ++i)
-#pragma unroll
-        for (int j = 0; j < N; ++j) acc[i][j] = fma(cbuf[32 * (i * N + j)], v1[i][j], acc[i][j]);
-    }
-    a_to_b<N>(acc, v2, buf, tt, lane_ok);  // v2 = acc in B (qy = t): [qz][qx]
-    // gx and gz in B layout, applied row/column-wise to limit live registers
-    const double wt = tb.w[tt];
-    const double fx = wt * tb.kin[0];
-    const double fz = wt * tb.kin[2];
-#pragma unroll
-    for (int z = 0; z < N; ++z) {
-      double g[N];
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        double s = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) s = fma(tb.D[q * N + j], uqB[z][j], s);
-        g[q] = s * (fx * tb.W2[z * N + q]);
-      }
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        double s = v2[z][q];
-#pragma unroll
-        for (int j = 0; j < N; ++j) s = fma(tb.D[j * N + q], g[j], s);
-        v2[z][q] = s;
-      }
-    }
-#pragma unroll
-    for (int x = 0; x < N; ++x) {
-      double g[N];
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        double s = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) s = fma(tb.D[q * N + j], uqB[j][x], s);
-        g[q] = s * (fz * tb.W2[q * N + x]);
-      }
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        double s = v2[q][x];
-#pragma unroll
-        for (int j = 0; j < N; ++j) s = fma(tb.D[j * N + q], g[j], s);
-        v2[q][x] = s;
-      }
-    }
+    cp_async_wait_all();  // coefficients staged by cp.async
+    __syncwarp();
+    sumfac_h_plane<N, COEF, 32>(u, v2, buf, tt, lane_ok, cbuf, tb);
   } else {
-    // mass-like: acc = c * uq, computed in B layout directly (qy = t)
+    // mass-like: values to the points, c * uq in B layout (qy = t), back
+    double v1[N][N], uqB[N][N];
+    contract_fast<N, false>(u, v1, tb.S);   // x
+    contract_slow<N, false>(v1, v2, tb.S);  // y
+    a_to_b<N>(v2, v1, buf, tt, lane_ok);    // B: y = qy = t, [z][qx]
+    contract_slow<N, false>(v1, uqB, tb.S); // z
+    cp_async_wait_all();
+    __syncwarp();
 #pragma unroll
     for (int z = 0; z < N; ++z)
 #pragma unroll
       for (int x = 0; x < N; ++x)
         // element (qz=z, qy=t, qx=x) was staged by the thread of plane z, k = t*N + x
         v2[z][x] = COEF ? cbase[32 * (tt * N + x) + sub * N + z] * uqB[z][x] : 0.0;
+    contract_slow<N, true>(v2, v1, tb.S);   // S^T along z
+    contract_fast<N, true>(v1, v2, tb.S);   // S^T along x
+    b_to_a<N>(v2, v1, buf, tt, lane_ok);    // A: z = t, [qy][x]
+    contract_slow<N, true>(v1, v2, tb.S);   // S^T along y -> out[y][x]
   }
-
-  // ---- back to the nodes: z, x in B, then y in A
-  contract_slow<N, true>(v2, v1, tb.S);   // S^T along z
-  contract_fast<N, true>(v1, v2, tb.S);   // S^T along x
-  b_to_a<N>(v2, v1, buf, tt, lane_ok);    // A: z = t, [qy][x]
-  contract_slow<N, true>(v1, v2, tb.S);   // S^T along y -> out[y][x]
 
   // ---- scatter-add
   if (ok) {

@@ -1,0 +1,206 @@
+// Device building blocks of the sum-factorised cell kernels (K1): the 1D
+// tables, register-resident contractions of one n x n plane per thread,
+// the per-pair shared-memory transposes and cp.async helpers.  Shared by
+// the one-pass kernel (bmv_cellop.cu) and the TMA-streamed kernel
+// (bmv_cellop_stream.cu).  Arithmetic follows cell_integrals_sumfac of the
+// reference (bcsrmv/matfree.py:288-367) in collocation form.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bmv.h"
+
+namespace bmv {
+
+struct CellTables {
+  double S[BMV_MAX_NODES * BMV_MAX_NODES];    // S[q*n + i]
+  double D[BMV_MAX_NODES * BMV_MAX_NODES];    // D_co[q*n + j]
+  double W2[BMV_MAX_NODES * BMV_MAX_NODES];   // w[a]*w[b]
+  double w[BMV_MAX_NODES];
+  double kin[3];
+};
+
+// Contract along the fast (last) index of a [N][N] plane:
+// out[s][q] = sum_j M[q*N + j] * in[s][j]  (TR: M[j*N + q])
+template <int N, bool TR>
+__device__ __forceinline__ void contract_fast(const double (&in)[N][N], double (&out)[N][N],
+                                              const double* __restrict__ M) {
+#pragma unroll
+  for (int s = 0; s < N; ++s) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc = fma(TR ? M[j * N + q] : M[q * N + j], in[s][j], acc);
+      out[s][q] = acc;
+    }
+  }
+}
+
+// Contract along the slow (first) index: out[q][f] = sum_j M[q*N+j] in[j][f]
+template <int N, bool TR>
+__device__ __forceinline__ void contract_slow(const double (&in)[N][N], double (&out)[N][N],
+                                              const double* __restrict__ M) {
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+#pragma unroll
+    for (int f = 0; f < N; ++f) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc = fma(TR ? M[j * N + q] : M[q * N + j], in[j][f], acc);
+      out[q][f] = acc;
+    }
+  }
+}
+
+// Per-pair transpose tile: element (z, y, x) at z*BZ + y*BY + x, pairs TILE
+// apart.  Strides chosen by a half-warp bank model (64-bit accesses, 16
+// bank pairs per 128 B wavefront) for the pair-major lane mapping: N = 3, 4
+// conflict-free stores and loads (2 + 2 wavefronts), N = 5 2 + 3.
+template <int N> struct Tile;
+template <> struct Tile<2> { static constexpr int BY = 2, BZ = 4, TILE = 9; };
+template <> struct Tile<3> { static constexpr int BY = 5, BZ = 21, TILE = 63; };
+template <> struct Tile<4> { static constexpr int BY = 4, BZ = 20, TILE = 77; };
+#if defined(BMV_K1_TILE5_WIDE)
+template <> struct Tile<5> { static constexpr int BY = 7, BZ = 39, TILE = 195; };  // 2 + 2 wavefronts
+#else
+template <> struct Tile<5> { static constexpr int BY = 5, BZ = 27, TILE = 135; };  // 2 + 3 wavefronts
+#endif
+
+// A (z = t, [y][x]) -> B (y = t, [z][x]) through the pair tile.
+template <int N>
+__device__ __forceinline__ void a_to_b(const double (&a)[N][N], double (&b)[N][N],
+                                       double* buf, int t, bool store) {
+  using L = Tile<N>;
+  __syncwarp();
+  if (store) {
+#pragma unroll
+    for (int y = 0; y < N; ++y)
+#pragma unroll
+      for (int x = 0; x < N; ++x) buf[t * L::BZ + y * L::BY + x] = a[y][x];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int z = 0; z < N; ++z)
+#pragma unroll
+    for (int x = 0; x < N; ++x) b[z][x] = buf[z * L::BZ + t * L::BY + x];
+}
+
+// B (y = t, [z][x]) -> A (z = t, [y][x]).
+template <int N>
+__device__ __forceinline__ void b_to_a(const double (&b)[N][N], double (&a)[N][N],
+                                       double* buf, int t, bool store) {
+  using L = Tile<N>;
+  __syncwarp();
+  if (store) {
+#pragma unroll
+    for (int z = 0; z < N; ++z)
+#pragma unroll
+      for (int x = 0; x < N; ++x) buf[z * L::BZ + t * L::BY + x] = b[z][x];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int y = 0; y < N; ++y)
+#pragma unroll
+    for (int x = 0; x < N; ++x) a[y][x] = buf[t * L::BZ + y * L::BY + x];
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_one() {
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+}
+
+// H = -1/2 Laplace (+ c(q) u(q)) on one pair, thread t holding plane z = t
+// of the pair's n^3 tensor ("A" layout, [y][x]).  In: u = nodal values;
+// out: the cell integral at the nodes, same layout.  Collocation form at the
+// Gauss points (q = n): 3 interpolations, gradients with D_co = D S^-1
+// (3 + 3 transposed), 3 transposed interpolations = 12 contractions of n^4
+// FMAs, 4 transposes through the pair tile `buf`.  The coefficient of
+// quadrature point (qz = t, qy = i, qx = j) is read at cf[(i * N + j) * CS].
+template <int N, bool COEF, int CS>
+__device__ __forceinline__ void sumfac_h_plane(const double (&u)[N][N], double (&v2)[N][N],
+                                               double* buf, int tt, bool lane_ok,
+                                               const double* cf, const CellTables& tb) {
+  double v1[N][N];
+  contract_fast<N, false>(u, v1, tb.S);   // x
+  contract_slow<N, false>(v1, v2, tb.S);  // y
+  a_to_b<N>(v2, v1, buf, tt, lane_ok);    // B: y = qy = t, [z][qx]
+  double uqB[N][N];
+  contract_slow<N, false>(v1, uqB, tb.S); // z -> uq at (qz, qy=t, qx)
+  double acc[N][N];
+  // gy in A layout (qz = t)
+  b_to_a<N>(uqB, v1, buf, tt, lane_ok);  // v1 = uq[qz=t][qy][qx]
+  contract_slow<N, false>(v1, v2, tb.D);  // d/dy at the points
+  const double fy = tb.w[tt] * tb.kin[1];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) v2[i][j] *= fy * tb.W2[i * N + j];
+  contract_slow<N, true>(v2, acc, tb.D);  // D^T along y
+  if (COEF) {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc[i][j] = fma(cf[CS * (i * N + j)], v1[i][j], acc[i][j]);
+  }
+  a_to_b<N>(acc, v2, buf, tt, lane_ok);  // v2 = acc in B (qy = t): [qz][qx]
+  // gx and gz in B layout, applied row/column-wise to limit live registers
+  const double wt = tb.w[tt];
+  const double fx = wt * tb.kin[0];
+  const double fz = wt * tb.kin[2];
+#pragma unroll
+  for (int z = 0; z < N; ++z) {
+    double g[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(tb.D[q * N + j], uqB[z][j], s);
+      g[q] = s * (fx * tb.W2[z * N + q]);
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s = v2[z][q];
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(tb.D[j * N + q], g[j], s);
+      v2[z][q] = s;
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < N; ++x) {
+    double g[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(tb.D[q * N + j], uqB[j][x], s);
+      g[q] = s * (fz * tb.W2[q * N + x]);
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s = v2[q][x];
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(tb.D[j * N + q], g[j], s);
+      v2[q][x] = s;
+    }
+  }
+  // back to the nodes: z, x in B, then y in A
+  contract_slow<N, true>(v2, v1, tb.S);   // S^T along z
+  contract_fast<N, true>(v1, v2, tb.S);   // S^T along x
+  b_to_a<N>(v2, v1, buf, tt, lane_ok);    // A: z = t, [qy][x]
+  contract_slow<N, true>(v1, v2, tb.S);   // S^T along y -> out[y][x]
+}
+
+}  // namespace bmv

@@ -195,6 +195,64 @@ int bmv_mmult_destroy(bmv_mmult* plan);
 int bmv_mmult_run(bmv_mmult* plan, const double* a, const double* b, double* c,
                   double alpha, int32_t accumulate, int64_t c_len, void* stream);
 
+/* ------------------------------------------------- K4 / K5, lane-compacted --
+ * Same products as bmv_tmmult_* / bmv_mmult_* (reference tmmult
+ * bcsr.py:631-667, mmult bcsr.py:587-628), computed on the active columns of
+ * A only: a_mask[pos] marks the lanes of A block pos that hold support
+ * entries (the multivector's declared column support, support.py; all
+ * stored lanes when A has none).  Values of A outside the mask must be 0.
+ * S (K4) is accumulated with fp64 reductions: summation order is not
+ * fixed (like K1's atomic scatter).  Owned block rows i = 0..n_rows-1;
+ * positions index the host arrays below (element offsets into the
+ * operand's value array).                                                 */
+typedef struct {
+  int32_t n_rows;
+  const int32_t* row_rows;       /* rows of block row i                     */
+  const int64_t* a_row_start;    /* n_rows + 1                              */
+  const int64_t* a_off;          /* per A position                          */
+  const int32_t* a_stride;
+  const uint64_t* a_mask;        /* active lanes (bit l = lane l, l < 64)    */
+  const int64_t* b_row_start;    /* n_rows + 1                              */
+  const int64_t* b_off;
+  const int32_t* b_stride;
+  const int32_t* b_width;        /* columns of the B block                  */
+  /* per (row i, A position, B position), row-major over (pa, pb) inside
+     the row, rows in order: the S block of (col block of pa, col block of
+     pb): element offset, row stride, rows (= width of pa's col block)    */
+  const int64_t* c_off;
+  const int32_t* c_stride;
+  const int32_t* c_rows;
+} bmv_tmmult_lane_desc;
+typedef struct bmv_lane_plan bmv_lane_plan;
+int bmv_tmmult_lane_create(const bmv_tmmult_lane_desc* desc, bmv_lane_plan** out);
+/* c[0:c_len] = 0, then c += A^T B on the plan's blocks. */
+int bmv_tmmult_lane_run(bmv_lane_plan* plan, const double* a, const double* b, double* c,
+                        int64_t c_len, void* stream);
+typedef struct {
+  int32_t n_rows;
+  const int32_t* row_rows;
+  const int64_t* a_row_start;    /* A = X, n_rows + 1                       */
+  const int64_t* a_off;
+  const int32_t* a_stride;
+  const uint64_t* a_mask;
+  const int64_t* c_row_start;    /* C = Y (output), n_rows + 1              */
+  const int64_t* c_off;
+  const int32_t* c_stride;
+  const int32_t* c_width;
+  /* B = the square matrix: per (row i, A position, Y position), row-major
+     over (pa, pc) inside the row starting at b_pair_start[i]: element
+     offset of block (col block of pa, col block of pc) in b (-1: absent)
+     and its row stride                                                   */
+  const int64_t* b_pair_start;   /* n_rows                                  */
+  const int64_t* b_off;
+  const int32_t* b_stride;
+} bmv_mmult_lane_desc;
+int bmv_mmult_lane_create(const bmv_mmult_lane_desc* desc, bmv_lane_plan** out);
+/* c[0:zero_len] = 0; then every planned Y block = alpha A B (+ old value if
+   accumulate): all stored lanes of the planned blocks are written. */
+int bmv_mmult_lane_run(bmv_lane_plan* plan, const double* a, const double* b, double* c,
+                       double alpha, int32_t accumulate, int64_t zero_len, void* stream);
+int bmv_lane_plan_destroy(bmv_lane_plan* plan);
 /* --------------------------------------------------------- halo / util --
  * Device index lists for ghost exchange packing.                         */
 typedef struct bmv_index bmv_index;

@@ -27,6 +27,7 @@ _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
 _u32p = C.POINTER(C.c_uint32)
 _f64p = C.POINTER(C.c_double)
+_u64p = C.POINTER(C.c_uint64)
 
 
 class CellopDesc(C.Structure):
@@ -60,6 +61,24 @@ class MmultDesc(C.Structure):
     ]
 
 
+class TmmultLaneDesc(C.Structure):
+    _fields_ = [
+        ("n_rows", C.c_int32), ("row_rows", _i32p), ("a_row_start", _i64p), ("a_off", _i64p),
+        ("a_stride", _i32p), ("a_mask", _u64p), ("b_row_start", _i64p), ("b_off", _i64p),
+        ("b_stride", _i32p), ("b_width", _i32p), ("c_off", _i64p), ("c_stride", _i32p),
+        ("c_rows", _i32p),
+    ]
+
+
+class MmultLaneDesc(C.Structure):
+    _fields_ = [
+        ("n_rows", C.c_int32), ("row_rows", _i32p), ("a_row_start", _i64p), ("a_off", _i64p),
+        ("a_stride", _i32p), ("a_mask", _u64p), ("c_row_start", _i64p), ("c_off", _i64p),
+        ("c_stride", _i32p), ("c_width", _i32p), ("b_pair_start", _i64p), ("b_off", _i64p),
+        ("b_stride", _i32p),
+    ]
+
+
 # (name, restype, argtypes) of every exported symbol; also used by the
 # CPU-side test that the library exports exactly what bmv.h declares.
 SIGNATURES = [
@@ -84,6 +103,14 @@ SIGNATURES = [
     ("bmv_mmult_run", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_int64,
       C.c_void_p]),
+    ("bmv_tmmult_lane_create", C.c_int, [C.POINTER(TmmultLaneDesc), C.POINTER(C.c_void_p)]),
+    ("bmv_tmmult_lane_run", C.c_int,
+     [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    ("bmv_mmult_lane_create", C.c_int, [C.POINTER(MmultLaneDesc), C.POINTER(C.c_void_p)]),
+    ("bmv_mmult_lane_run", C.c_int,
+     [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_int64,
+      C.c_void_p]),
+    ("bmv_lane_plan_destroy", C.c_int, [C.c_void_p]),
     ("bmv_index_create", C.c_int, [_i64p, C.c_int64, C.POINTER(C.c_void_p)]),
     ("bmv_index_destroy", C.c_int, [C.c_void_p]),
     ("bmv_index_size", C.c_int64, [C.c_void_p]),

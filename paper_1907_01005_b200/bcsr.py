@@ -24,6 +24,7 @@ tested with gloo, but every compute kernel refuses CPU storage
 from __future__ import annotations
 
 import json
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -899,6 +900,196 @@ class _MmultPlan:
         self.handle = _lib.Handle("bmv_mmult_destroy", raw)
 
 
+# -- lane-compacted K4 / K5 (csrc/bmv_spmm_lane.cu) -------------------------------
+
+
+def _deterministic() -> bool:
+    """BMV_DETERMINISTIC=1 keeps the fixed-order K4 / K5 kernels (bmv_project.cu,
+    bmv_postmul.cu); default: the lane-compacted kernels (S reduced with fp64
+    atomics, like K1's default scatter)."""
+    return os.environ.get("BMV_DETERMINISTIC", "0") == "1"
+
+
+def _a_lane_masks(a: BlockCsrMatrix) -> np.ndarray:
+    """uint64 mask of the lanes of every owned block of `a` that may hold
+    nonzeros: its declared column support (support.py) or, without one, all
+    stored columns of the block.  Host-only; cached per support."""
+    key = ("lanemask", id(a.support))
+    cache = _plan_cache(a)
+    hit = cache.get(key)
+    if hit is not None and hit[1] is a.support:
+        return hit[0]
+    n_pos = int(a.row_start[a.n_owned_blocks])
+    widths = a.col_blocks.sizes[a.col_index[:n_pos]].astype(np.int64)
+    if widths.size and int(widths.max()) > 64:
+        raise ShapeError("lane masks need column blocks of at most 64 columns")
+    if a.support is None:
+        mask = np.where(widths >= 64, np.uint64(0xFFFFFFFFFFFFFFFF),
+                        (np.uint64(1) << np.minimum(widths, 63).astype(np.uint64)) - np.uint64(1))
+        mask = mask.astype(np.uint64)
+    else:
+        flat, _rows, cols = a.support.owned_entries(a)
+        mask = np.zeros(n_pos, dtype=np.uint64)
+        if flat.size:
+            pos = np.searchsorted(a.block_offsets[: n_pos + 1], flat, side="right") - 1
+            cb = a.col_blocks.blocks_of(cols)
+            lane = (cols - a.col_blocks.starts[cb]).astype(np.uint64)
+            np.bitwise_or.at(mask, pos, np.uint64(1) << lane)
+    cache[key] = (mask, a.support)
+    return mask
+
+
+def _lane_plan_or_none(build, a, b, c):
+    """The lane plan, or None when the shapes exceed it (ShapeError from the
+    planner: > 64 columns per block, > 32 active columns per row for K5, a
+    block row larger than a stage); PatternError propagates."""
+    key = ("lane_fail", build.__name__, id(b), id(c), id(a.support))
+    cache = _plan_cache(a)
+    if key in cache:
+        return None
+    try:
+        return build(a, b, c)
+    except ShapeError:
+        cache[key] = True
+        return None
+
+
+class _LanePlan:
+    def __init__(self, kind: str, desc, keep):
+        lib = _lib.load()
+        raw = _lib.C.c_void_p()
+        fn = lib.bmv_tmmult_lane_create if kind == "tm" else lib.bmv_mmult_lane_create
+        _lib.check(fn(_lib.C.byref(desc), _lib.C.byref(raw)), f"bmv_{kind}mult_lane_create")
+        self.handle = _lib.Handle("bmv_lane_plan_destroy", raw)
+        self._keep = keep
+
+
+def _tm_pairs(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
+    """(row, pa, pb, c position) of every owned block pair, row-major over
+    (pa, pb) inside a row; PatternError if c lacks a product block."""
+    n_rows = a.n_owned_blocks
+    na = a.row_start[1 : n_rows + 1] - a.row_start[:n_rows]
+    nb = b.row_start[1 : n_rows + 1] - b.row_start[:n_rows]
+    row, t = _expand(na * nb)
+    nbr = nb[row]
+    pa = a.row_start[row] + t // np.maximum(nbr, 1)
+    pb = b.row_start[row] + t % np.maximum(nbr, 1)
+    k = a.col_index[pa]
+    ck = _local_block_table(c.layout, c.layout.blocks.n_blocks)[k]
+    if (ck < 0).any():
+        raise PatternError(f"rank {c.layout.rank} holds no ghost of block row {int(k[ck < 0][0])}")
+    ell = b.col_index[pb]
+    ckey = ck * c.col_blocks.n_blocks + ell
+    ckeys = c.local_keys()
+    cp = np.searchsorted(ckeys, ckey)
+    ok = (cp < ckeys.size) & (ckeys[np.minimum(cp, max(ckeys.size - 1, 0))] == ckey) \
+        if ckeys.size else np.zeros(ckey.size, dtype=bool)
+    if not ok.all():
+        j = int(np.flatnonzero(~ok)[0])
+        raise PatternError(f"tmmult destination misses block ({int(k[j])}, {int(ell[j])})")
+    if (c.local_row_sizes[c.pos_row[cp]] != a.col_blocks.sizes[k]).any():
+        raise ShapeError("tmmult destination row block is incomplete (split ghost group)")
+    return row, pa, pb, cp
+
+
+def _tmmult_lane_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
+    key = ("tml", id(b), id(c), id(a.support))
+    cache = _plan_cache(a)
+    hit = cache.get(key)
+    if hit is not None:
+        return hit[0]
+    n_rows = a.n_owned_blocks
+    _row, _pa, _pb, cp = _tm_pairs(a, b, c)
+    n_pa = int(a.row_start[n_rows])
+    n_pb = int(b.row_start[n_rows])
+    arr = dict(
+        row_rows=a.local_row_sizes[:n_rows].astype(np.int32),
+        a_row_start=a.row_start[: n_rows + 1].astype(np.int64),
+        a_off=a.block_offsets[:n_pa].astype(np.int64),
+        a_stride=a.col_strides[a.col_index[:n_pa]].astype(np.int32),
+        a_mask=_a_lane_masks(a),
+        b_row_start=b.row_start[: n_rows + 1].astype(np.int64),
+        b_off=b.block_offsets[:n_pb].astype(np.int64),
+        b_stride=b.col_strides[b.col_index[:n_pb]].astype(np.int32),
+        b_width=b.col_blocks.sizes[b.col_index[:n_pb]].astype(np.int32),
+        c_off=c.block_offsets[cp].astype(np.int64),
+        c_stride=c.col_strides[c.col_index[cp]].astype(np.int32),
+        c_rows=c.local_row_sizes[c.pos_row[cp]].astype(np.int32),
+    )
+    arr = {k: np.ascontiguousarray(v) for k, v in arr.items()}
+    d = _lib.TmmultLaneDesc()
+    d.n_rows = n_rows
+    for name, ct in (("row_rows", _lib.C.c_int32), ("a_row_start", _lib.C.c_int64),
+                     ("a_off", _lib.C.c_int64), ("a_stride", _lib.C.c_int32),
+                     ("a_mask", _lib.C.c_uint64), ("b_row_start", _lib.C.c_int64),
+                     ("b_off", _lib.C.c_int64), ("b_stride", _lib.C.c_int32),
+                     ("b_width", _lib.C.c_int32), ("c_off", _lib.C.c_int64),
+                     ("c_stride", _lib.C.c_int32), ("c_rows", _lib.C.c_int32)):
+        setattr(d, name, _lib.ptr(arr[name], ct))
+    plan = _LanePlan("tm", d, arr)
+    cache[key] = (plan, b, c, a.support)
+    return plan
+
+
+def _mmult_lane_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
+    key = ("mml", id(b), id(c), id(a.support))
+    cache = _plan_cache(a)
+    hit = cache.get(key)
+    if hit is not None:
+        return hit[0]
+    n_rows = a.n_owned_blocks
+    n_pa = int(a.row_start[n_rows])
+    n_pc = int(c.row_start[n_rows])
+    # b's local block row of every a position's column block
+    k = a.col_index[:n_pa]
+    kb = _local_block_table(b.layout, b.layout.blocks.n_blocks)[k]
+    if (kb < 0).any():
+        raise PatternError(f"rank {b.layout.rank} holds no ghost of block row {int(k[kb < 0][0])}")
+    if (b.local_row_sizes[kb] != a.col_blocks.sizes[k]).any():
+        bad = int(k[b.local_row_sizes[kb] != a.col_blocks.sizes[k]][0])
+        raise ShapeError(f"row block {bad} of b is incomplete (split ghost group)")
+    na = a.row_start[1 : n_rows + 1] - a.row_start[:n_rows]
+    nc = c.row_start[1 : n_rows + 1] - c.row_start[:n_rows]
+    row, t = _expand(na * nc)
+    ncr = nc[row]
+    pa = a.row_start[row] + t // np.maximum(ncr, 1)
+    pc = c.row_start[row] + t % np.maximum(ncr, 1)
+    bkey = kb[pa] * b.col_blocks.n_blocks + c.col_index[pc]
+    bkeys = b.local_keys()
+    bp = np.searchsorted(bkeys, bkey)
+    ok = (bp < bkeys.size) & (bkeys[np.minimum(bp, max(bkeys.size - 1, 0))] == bkey) \
+        if bkeys.size else np.zeros(bkey.size, dtype=bool)
+    b_off = np.where(ok, b.block_offsets[np.minimum(bp, max(b.block_offsets.size - 2, 0))], -1)
+    pair_start = np.concatenate([[0], np.cumsum(na * nc)])[:-1].astype(np.int64)
+    arr = dict(
+        row_rows=a.local_row_sizes[:n_rows].astype(np.int32),
+        a_row_start=a.row_start[: n_rows + 1].astype(np.int64),
+        a_off=a.block_offsets[:n_pa].astype(np.int64),
+        a_stride=a.col_strides[a.col_index[:n_pa]].astype(np.int32),
+        a_mask=_a_lane_masks(a),
+        c_row_start=c.row_start[: n_rows + 1].astype(np.int64),
+        c_off=c.block_offsets[:n_pc].astype(np.int64),
+        c_stride=c.col_strides[c.col_index[:n_pc]].astype(np.int32),
+        c_width=c.col_blocks.sizes[c.col_index[:n_pc]].astype(np.int32),
+        b_pair_start=pair_start,
+        b_off=b_off.astype(np.int64),
+        b_stride=b.col_strides[c.col_index[pc]].astype(np.int32),
+    )
+    arr = {kk: np.ascontiguousarray(v) for kk, v in arr.items()}
+    d = _lib.MmultLaneDesc()
+    d.n_rows = n_rows
+    for name, ct in (("row_rows", _lib.C.c_int32), ("a_row_start", _lib.C.c_int64),
+                     ("a_off", _lib.C.c_int64), ("a_stride", _lib.C.c_int32),
+                     ("a_mask", _lib.C.c_uint64), ("c_row_start", _lib.C.c_int64),
+                     ("c_off", _lib.C.c_int64), ("c_stride", _lib.C.c_int32),
+                     ("c_width", _lib.C.c_int32), ("b_pair_start", _lib.C.c_int64),
+                     ("b_off", _lib.C.c_int64), ("b_stride", _lib.C.c_int32)):
+        setattr(d, name, _lib.ptr(arr[name], ct))
+    plan = _LanePlan("mm", d, arr)
+    cache[key] = (plan, b, c, a.support)
+    return plan
+
+
 def mmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, alpha: float = 1.0,
           accumulate: bool = False, counters: OpCounters | None = None):
     """c = alpha * a @ b truncated to c's pattern (K5 on the GPU)."""
@@ -910,8 +1101,22 @@ def mmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, alpha: float 
     if b.state != GHOSTED and b.layout.ghost_groups:
         raise StateError("b must have updated ghost values before mmult")
     c.ensure_owned()
-    plan = _mmult_plan(a, b, c)
     lib = _lib.require_device()
+    if not _deterministic():
+        lp = _lane_plan_or_none(_mmult_lane_plan, a, b, c)
+        if lp is not None:
+            # every owned block of c is written (alpha A B, + old if accumulate);
+            # ghost blocks are zeroed like zero_out
+            if not accumulate:
+                _zero_range(c.data, c._ghost_data_begin, c.data.numel())
+            _lib.check(lib.bmv_mmult_lane_run(lp.handle.raw, _lib.dptr(a.data), _lib.dptr(b.data),
+                                              _lib.dptr(c.data), float(alpha),
+                                              1 if accumulate else 0, 0,
+                                              _lib.stream_handle(c.device)), "bmv_mmult_lane_run")
+            if counters is not None:
+                counters.flops += _mmult_plan(a, b, c).flops
+            return
+    plan = _mmult_plan(a, b, c)
     zero_len = 0 if accumulate else c.data.numel()
     if not accumulate and plan.full_cover:
         # every owned value is overwritten by the kernel (all owned blocks have
@@ -1282,8 +1487,18 @@ def tmmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix,
     if c.col_blocks != b.col_blocks:
         raise ShapeError("c's column blocking must equal b's")
     c.ensure_owned()
-    plan = _tmmult_plan(a, b, c)
     lib = _lib.require_device()
+    if not _deterministic():
+        lp = _lane_plan_or_none(_tmmult_lane_plan, a, b, c)
+        if lp is not None:
+            _lib.check(lib.bmv_tmmult_lane_run(lp.handle.raw, _lib.dptr(a.data), _lib.dptr(b.data),
+                                               _lib.dptr(c.data), c.data.numel(),
+                                               _lib.stream_handle(c.device)), "bmv_tmmult_lane_run")
+            if counters is not None:
+                counters.flops += _tmmult_plan(a, b, c).flops
+            c.compress()
+            return
+    plan = _tmmult_plan(a, b, c)
     _lib.check(lib.bmv_tmmult_run(plan.handle.raw, _lib.dptr(a.data), _lib.dptr(b.data),
                                   _lib.dptr(c.data), c.data.numel(),
                                   _lib.stream_handle(c.device)), "bmv_tmmult_run")

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "bmv_cellop_stream.cuh"
 #include "bmv_common.cuh"
 #include "bmv_sumfac.cuh"
 
@@ -251,6 +252,7 @@ struct bmv_cellop {
   int32_t *group_xoff = nullptr, *group_hoff = nullptr;
   uint32_t* cell_slots = nullptr;
   CellTables tables{};
+  StreamPlan* stream = nullptr;  // TMA-streamed Hamiltonian path (bmv_cellop_stream.cu)
 };
 
 namespace {
@@ -402,6 +404,11 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
     for (int j = 0; j < n; ++j) p->tables.W2[i * n + j] = d->w[i] * d->w[j];
   }
   for (int k = 0; k < 3; ++k) p->tables.kin[k] = d->kin[k];
+  rc = stream_plan_build(d, &p->stream);
+  if (rc != BMV_OK) {
+    bmv_cellop_destroy(p);
+    return rc;
+  }
   *out = p;
   return BMV_OK;
 }
@@ -412,6 +419,7 @@ int bmv_cellop_destroy(bmv_cellop* p) {
   release(p->group_xoff);
   release(p->group_hoff);
   release(p->cell_slots);
+  stream_plan_destroy(p->stream);
   delete p;
   return BMV_OK;
 }
@@ -464,6 +472,8 @@ int bmv_cellop_apply(bmv_cellop* p, int32_t kinetic, const double* coef, int64_t
   CellArgs args{p->pair_desc, p->group_xoff, p->group_hoff, p->cell_slots, coef, coef_stride,
                 0, p->n_pairs, x, hx};
   const bool use_coef = coef != nullptr;
+  if (p->stream && kinetic && (!coef || coef_stride == 0 || coef_stride == p->stream->q3p))
+    return stream_apply(p->stream, p->tables, coef, coef_stride != 0 ? 1 : 0, x, hx, st);
   if (p->color_start.empty()) {
     return launch_dispatch(p->n, args, p->tables, p->max_groups, kinetic != 0, use_coef, true, st);
   }

@@ -65,6 +65,7 @@ struct CopySrc {
   const char* p0;
   const char* p1;
   const char* p2;
+  const char* p3 = nullptr;
 };
 
 __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, unsigned bytes) {
@@ -104,7 +105,7 @@ __device__ __forceinline__ void stream_producer(const int4* __restrict__ cps, in
       const bool mine = lane >= pos && lane <= end;
       const unsigned len = mine ? ((unsigned)cur.y & kCpLenMask) : 0u;
       const int sel = ((unsigned)cur.y >> 28) & 3;
-      const char* s = (sel == 0 ? src.p0 : (sel == 1 ? src.p1 : src.p2)) +
+      const char* s = (sel == 0 ? src.p0 : sel == 1 ? src.p1 : sel == 2 ? src.p2 : src.p3) +
                       (((int64_t)(unsigned)cur.w << 32) | (unsigned)cur.z);
       const unsigned doff = (unsigned)cur.x;
       const bool bulk = mine && ((reinterpret_cast<uintptr_t>(s) | doff | len) & 15u) == 0;

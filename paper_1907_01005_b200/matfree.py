@@ -519,8 +519,13 @@ class CellOperator:
         return self._dev_tables
 
     def coefficient(self, spec: OperatorSpec, device):
-        """(device tensor or None, cell stride) of the quadrature coefficient."""
+        """(device tensor or None, cell stride) of the quadrature coefficient.
+
+        Rows are padded to q3p = q^3 rounded up to even (16-byte rows, staged
+        by TMA in the streamed K1); the stride is q3p for a per-cell
+        coefficient and 0 for one shared by every cell."""
         q3 = self.shape.n_q ** 3
+        q3p = q3 + (q3 & 1)
         if spec.kind == MASS:
             key = ("mass",)
         elif spec.kind == HAMILTONIAN:
@@ -533,36 +538,43 @@ class CellOperator:
         if hit is not None:
             return hit[0], hit[1]
         w3 = self.kernels.w3.ravel()
+
+        def padded_row(v):
+            return torch.as_tensor(np.concatenate([v, np.zeros(q3p - q3)]), device=device)
+
         if key[0] == "mass":
-            coef, stride = torch.as_tensor(w3.copy(), device=device), 0
+            coef, stride = padded_row(w3), 0
         elif key[0] == "const":
-            coef, stride = torch.as_tensor(w3 * float(spec.potential), device=device), 0
+            coef, stride = padded_row(w3 * float(spec.potential)), 0
         elif isinstance(spec.potential, GaussianPotential):
             pot = spec.potential
             n_cells = len(self.cells)
             org, qoff, w3d = self._device_tables(device)
             cen = torch.as_tensor(pot.centers, dtype=torch.float64, device=device)
-            coef = torch.zeros(max(n_cells, 1) * q3, dtype=torch.float64, device=device)
+            acc = torch.zeros(max(n_cells, 1) * q3, dtype=torch.float64, device=device)
             lib = _lib.require_device()
             chunk = 4096
             for c0 in range(0, max(pot.centers.shape[0], 1), chunk):
                 part = cen[c0 : c0 + chunk]
-                tmp = torch.empty_like(coef)
+                tmp = torch.empty_like(acc)
                 _lib.check(lib.bmv_potential_gaussian(
                     n_cells, q3, _lib.dptr(org), _lib.dptr(qoff), _lib.dptr(w3d), _lib.dptr(part),
                     int(part.shape[0]), pot.inv_sigma2, pot.scale, _lib.dptr(tmp),
                     _lib.stream_handle(device)), "bmv_potential_gaussian")
-                coef += tmp
-            stride = q3
+                acc += tmp
+            coef = torch.zeros(max(n_cells, 1), q3p, dtype=torch.float64, device=device)
+            coef[:, :q3] = acc.view(-1, q3)
+            coef = coef.view(-1)
+            stride = q3p
         else:
             n_cells = len(self.cells)
-            vals = np.empty((n_cells, q3))
+            vals = np.zeros((n_cells, q3p))
             step = 4096
             for c0 in range(0, n_cells, step):
                 pts = (self.cell_origins[c0 : c0 + step, None, :]
                        + self.kernels.quad_offsets[None, :, :]).reshape(-1, 3)
-                vals[c0 : c0 + step] = spec.sample_potential(pts).reshape(-1, q3)
-            coef, stride = torch.as_tensor((vals * w3[None, :]).ravel(), device=device), q3
+                vals[c0 : c0 + step, :q3] = spec.sample_potential(pts).reshape(-1, q3) * w3[None, :]
+            coef, stride = torch.as_tensor(vals.ravel(), device=device), q3p
         self._coefs[key] = (coef, stride, spec.potential)
         return coef, stride
 

@@ -253,6 +253,20 @@ int bmv_mmult_lane_create(const bmv_mmult_lane_desc* desc, bmv_lane_plan** out);
 int bmv_mmult_lane_run(bmv_lane_plan* plan, const double* a, const double* b, double* c,
                        double alpha, int32_t accumulate, int64_t zero_len, void* stream);
 int bmv_lane_plan_destroy(bmv_lane_plan* plan);
+/* Host-only (no device needed): the stage stream a lane plan would upload,
+   for CPU emulation of the kernels in the tests.                         */
+typedef struct {
+  int32_t stage_bytes;
+  int32_t n_parts;
+  int64_t meta_len;          /* int32 words                               */
+  int64_t n_entries;         /* copy entries (4 x int32)                  */
+  int32_t* meta;
+  int32_t* copies;
+  int64_t* part_sub_start;   /* n_parts + 1                               */
+  int64_t* part_entry_start; /* n_parts + 1                               */
+} bmv_lane_host;
+int bmv_lane_plan_host(int32_t kind, const void* desc, int32_t n_parts, bmv_lane_host* out);
+int bmv_lane_host_free(bmv_lane_host* host);
 /* --------------------------------------------------------- halo / util --
  * Device index lists for ghost exchange packing.                         */
 typedef struct bmv_index bmv_index;

@@ -79,6 +79,14 @@ class MmultLaneDesc(C.Structure):
     ]
 
 
+class LaneHost(C.Structure):
+    _fields_ = [
+        ("stage_bytes", C.c_int32), ("n_parts", C.c_int32), ("meta_len", C.c_int64),
+        ("n_entries", C.c_int64), ("meta", _i32p), ("copies", _i32p),
+        ("part_sub_start", _i64p), ("part_entry_start", _i64p),
+    ]
+
+
 # (name, restype, argtypes) of every exported symbol; also used by the
 # CPU-side test that the library exports exactly what bmv.h declares.
 SIGNATURES = [
@@ -111,6 +119,8 @@ SIGNATURES = [
      [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_int64,
       C.c_void_p]),
     ("bmv_lane_plan_destroy", C.c_int, [C.c_void_p]),
+    ("bmv_lane_plan_host", C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.POINTER(LaneHost)]),
+    ("bmv_lane_host_free", C.c_int, [C.POINTER(LaneHost)]),
     ("bmv_index_create", C.c_int, [_i64p, C.c_int64, C.POINTER(C.c_void_p)]),
     ("bmv_index_destroy", C.c_int, [C.c_void_p]),
     ("bmv_index_size", C.c_int64, [C.c_void_p]),

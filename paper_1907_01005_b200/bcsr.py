@@ -954,6 +954,26 @@ def _lane_plan_or_none(build, a, b, c):
         return None
 
 
+def lane_plan_host(kind: int, desc, n_parts: int = 4) -> dict:
+    """The stage stream of a lane plan as numpy arrays (bmv_lane_plan_host;
+    no device).  Used by the tests' CPU emulation of the lane kernels."""
+    lib = _lib.load()
+    h = _lib.LaneHost()
+    _lib.check(lib.bmv_lane_plan_host(int(kind), _lib.C.cast(_lib.C.byref(desc), _lib.C.c_void_p),
+                                      int(n_parts), _lib.C.byref(h)), "bmv_lane_plan_host")
+    try:
+        def arr(p, n):
+            return np.ctypeslib.as_array(p, shape=(int(n),)).copy() if n else np.zeros(0, np.int64)
+        out = dict(stage_bytes=int(h.stage_bytes), n_parts=int(h.n_parts),
+                   meta=arr(h.meta, h.meta_len).astype(np.int32),
+                   copies=arr(h.copies, 4 * h.n_entries).astype(np.int32).reshape(-1, 4),
+                   part_sub_start=arr(h.part_sub_start, h.n_parts + 1 if h.n_parts else 0),
+                   part_entry_start=arr(h.part_entry_start, h.n_parts + 1 if h.n_parts else 0))
+    finally:
+        lib.bmv_lane_host_free(_lib.C.byref(h))
+    return out
+
+
 class _LanePlan:
     def __init__(self, kind: str, desc, keep):
         lib = _lib.load()
@@ -998,6 +1018,14 @@ def _tmmult_lane_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     hit = cache.get(key)
     if hit is not None:
         return hit[0]
+    d, arr = tmmult_lane_desc(a, b, c)
+    plan = _LanePlan("tm", d, arr)
+    cache[key] = (plan, b, c, a.support)
+    return plan
+
+
+def tmmult_lane_desc(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
+    """(bmv_tmmult_lane_desc, arrays it points into): host-only."""
     n_rows = a.n_owned_blocks
     _row, _pa, _pb, cp = _tm_pairs(a, b, c)
     n_pa = int(a.row_start[n_rows])
@@ -1026,9 +1054,7 @@ def _tmmult_lane_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
                      ("b_width", _lib.C.c_int32), ("c_off", _lib.C.c_int64),
                      ("c_stride", _lib.C.c_int32), ("c_rows", _lib.C.c_int32)):
         setattr(d, name, _lib.ptr(arr[name], ct))
-    plan = _LanePlan("tm", d, arr)
-    cache[key] = (plan, b, c, a.support)
-    return plan
+    return d, arr
 
 
 def _mmult_lane_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
@@ -1037,6 +1063,14 @@ def _mmult_lane_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
     hit = cache.get(key)
     if hit is not None:
         return hit[0]
+    d, arr = mmult_lane_desc(a, b, c)
+    plan = _LanePlan("mm", d, arr)
+    cache[key] = (plan, b, c, a.support)
+    return plan
+
+
+def mmult_lane_desc(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
+    """(bmv_mmult_lane_desc, arrays it points into): host-only."""
     n_rows = a.n_owned_blocks
     n_pa = int(a.row_start[n_rows])
     n_pc = int(c.row_start[n_rows])
@@ -1085,9 +1119,7 @@ def _mmult_lane_plan(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix):
                      ("c_width", _lib.C.c_int32), ("b_pair_start", _lib.C.c_int64),
                      ("b_off", _lib.C.c_int64), ("b_stride", _lib.C.c_int32)):
         setattr(d, name, _lib.ptr(arr[name], ct))
-    plan = _LanePlan("mm", d, arr)
-    cache[key] = (plan, b, c, a.support)
-    return plan
+    return d, arr
 
 
 def mmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix, alpha: float = 1.0,

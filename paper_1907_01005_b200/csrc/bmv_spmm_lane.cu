@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <unordered_map>
 #include <vector>
 
@@ -272,6 +273,7 @@ struct StreamBuild {
   std::vector<int32_t> cps;  // 4 int32 per entry
   std::vector<int64_t> chunk_entry{0};
   std::vector<int64_t> chunk_work;
+  std::vector<int64_t> fixed_parts;  // chunk index where each part starts (K4: items never span parts)
   void add(const Chunk& c, int64_t work) {
     const int64_t moff = (int64_t)meta.size() * 4;  // bytes
     std::vector<int32_t> m = c.meta;
@@ -293,6 +295,20 @@ struct StreamBuild {
   // contiguous chunk ranges per part, balanced by work
   void parts(int n_parts, std::vector<int64_t>& sub_start, std::vector<int64_t>& entry_start) const {
     const int64_t nc = (int64_t)chunk_work.size();
+    if (!fixed_parts.empty()) {
+      sub_start.clear();
+      entry_start.clear();
+      for (int64_t c : fixed_parts) {
+        if (!sub_start.empty() && c == sub_start.back()) continue;  // empty part
+        sub_start.push_back(c);
+        entry_start.push_back(chunk_entry[(size_t)c]);
+      }
+      if (sub_start.back() != nc) {
+        sub_start.push_back(nc);
+        entry_start.push_back(chunk_entry.back());
+      }
+      return;
+    }
     int64_t total = 0;
     for (int64_t w : chunk_work) total += w;
     n_parts = (int)std::max<int64_t>(1, std::min<int64_t>(n_parts, nc));
@@ -353,14 +369,14 @@ int bmv_lane_plan_destroy(bmv_lane_plan* p) {
   return BMV_OK;
 }
 
-int bmv_tmmult_lane_create(const bmv_tmmult_lane_desc* d, bmv_lane_plan** out) {
-  if (!d || !out) {
-    set_error("null argument");
-    return BMV_ERR_INVALID;
-  }
-  *out = nullptr;
+}  // extern "C"
+
+namespace {
+
+int plan_k4(const bmv_tmmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out,
+            int sm_count_host) {
   const int stage_bytes = ((kSmemBudget - kAccTiles * 64 * 8) / kLnStages) & ~127;
-  StreamBuild sb;
+  stage_bytes_out = stage_bytes;
   // one item = rows sharing the accumulator (<= kAccTiles S tiles); chunks of
   // an item = rows (or B-block groups of one row) fitting a stage
   std::unordered_map<int64_t, int> tile_of;  // (S offset of tile row 0) -> acc tile
@@ -429,7 +445,28 @@ int bmv_tmmult_lane_create(const bmv_tmmult_lane_desc* d, bmv_lane_plan** out) {
     }
   };
 
+  // parts (one per CTA) are cut at rows, balanced by DMMA work; an item
+  // (accumulator lifetime) never spans two parts
+  std::vector<int64_t> row_work((size_t)d->n_rows + 1, 0);
   for (int32_t i = 0; i < d->n_rows; ++i) {
+    int64_t ncols = 0, ntl = 0;
+    for (int64_t pa = d->a_row_start[i]; pa < d->a_row_start[i + 1]; ++pa)
+      ncols += __builtin_popcountll(d->a_mask[pa]);
+    for (int64_t pb = d->b_row_start[i]; pb < d->b_row_start[i + 1]; ++pb)
+      ntl += (d->b_width[pb] + 7) / 8;
+    row_work[(size_t)i + 1] = row_work[(size_t)i] + ((ncols + 7) / 8) * ntl * (d->row_rows[i] + 4) + 16;
+  }
+  const int n_parts = std::max(1, sm_count_host);
+  int next_part = 1;
+  sb.fixed_parts.push_back(0);
+  for (int32_t i = 0; i < d->n_rows; ++i) {
+    if (next_part < n_parts &&
+        row_work[(size_t)i] >= row_work.back() * next_part / n_parts) {
+      emit(true);
+      sb.fixed_parts.push_back((int64_t)sb.chunk_work.size());
+      while (next_part < n_parts && row_work[(size_t)i] >= row_work.back() * next_part / n_parts)
+        ++next_part;
+    }
     const int64_t pa0 = d->a_row_start[i], pa1 = d->a_row_start[i + 1];
     const int64_t pb0 = d->b_row_start[i], pb1 = d->b_row_start[i + 1];
     const int rows = d->row_rows[i];
@@ -456,6 +493,11 @@ int bmv_tmmult_lane_create(const bmv_tmmult_lane_desc* d, bmv_lane_plan** out) {
                 (long long)a_len);
       return BMV_ERR_INVALID;
     }
+    // (A col block, 8-lane row group) pairs with active lanes: S tile rows
+    int row_rgroups = 0;
+    for (int64_t pa = pa0; pa < pa1; ++pa)
+      for (int rg = 0; rg < 64; rg += 8)
+        if ((d->a_mask[pa] >> rg) & 0xffull) ++row_rgroups;
     // the row's S tiles (new ones count against the accumulator)
     // tile key: S offset of (row a-lane group 0, col tile) -> per (pa, pb, nt)
     // process B blocks in groups that fit the stage together with the A range
@@ -466,19 +508,21 @@ int bmv_tmmult_lane_create(const bmv_tmmult_lane_desc* d, bmv_lane_plan** out) {
       int64_t b_len = 0;
       const int64_t b_first = d->b_off[pb];
       const int ncg = (int)((cols.size() + 7) / 8);
-      int grp_tiles = 0;
+      int grp_tiles = 0, grp_acc = 0;
       for (; pe < pb1; ++pe) {
         const int64_t nl = d->b_off[pe] + (int64_t)rows * d->b_stride[pe] - b_first;
         const int ntile = (d->b_width[pe] + 7) / 8;
+        const int acc_pe = row_rgroups * ntile;  // S tiles of this B block
         const int need = align16((int)(a_len * 8)) + align16((int)(nl * 8)) +
                          chunk_meta_bytes((size_t)(grp_tiles + ncg * ntile), kAccTiles) + 64;
-        if (pe > pb && need > stage_bytes) break;
-        if (need > stage_bytes) {
-          set_error("tmmult lane plan: block row %d does not fit a stage", i);
+        if (pe > pb && (need > stage_bytes || grp_acc + acc_pe > kAccTiles)) break;
+        if (need > stage_bytes || acc_pe > kAccTiles) {
+          set_error("tmmult lane plan: block row %d does not fit a stage / the accumulator", i);
           return BMV_ERR_INVALID;
         }
         b_len = nl;
         grp_tiles += ncg * ntile;
+        grp_acc += acc_pe;
       }
       // count new accumulator tiles of this group
       std::vector<int64_t> new_keys;
@@ -571,8 +615,24 @@ int bmv_tmmult_lane_create(const bmv_tmmult_lane_desc* d, bmv_lane_plan** out) {
     pair_base += na * nb;
   }
   emit(true);
-  if (sb.chunk_work.empty()) {
-    // nothing to compute: an empty plan (run only zeroes c)
+  return BMV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bmv_tmmult_lane_create(const bmv_tmmult_lane_desc* d, bmv_lane_plan** out) {
+  if (!d || !out) {
+    set_error("null argument");
+    return BMV_ERR_INVALID;
+  }
+  *out = nullptr;
+  StreamBuild sb;
+  int stage_bytes = 0;
+  {
+    const int rc0 = plan_k4(d, sb, stage_bytes, sm_count());
+    if (rc0 != BMV_OK) return rc0;
   }
   auto* p = new bmv_lane_plan();
   p->kind = 4;
@@ -612,14 +672,13 @@ int bmv_tmmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doub
   return BMV_OK;
 }
 
-int bmv_mmult_lane_create(const bmv_mmult_lane_desc* d, bmv_lane_plan** out) {
-  if (!d || !out) {
-    set_error("null argument");
-    return BMV_ERR_INVALID;
-  }
-  *out = nullptr;
+}  // extern "C"
+
+namespace {
+
+int plan_k5(const bmv_mmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out) {
   const int stage_bytes = (kSmemBudget / kLnStages) & ~127;
-  StreamBuild sb;
+  stage_bytes_out = stage_bytes;
   Chunk cur;
   std::vector<int32_t> tasks;  // concatenated records
   std::vector<int32_t> toffs;  // record offsets (int32 units, relative to the record area)
@@ -759,6 +818,25 @@ int bmv_mmult_lane_create(const bmv_mmult_lane_desc* d, bmv_lane_plan** out) {
     work += (int64_t)ro.size() * rows * (ks + 1);
   }
   emit();
+  return BMV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bmv_mmult_lane_create(const bmv_mmult_lane_desc* d, bmv_lane_plan** out) {
+  if (!d || !out) {
+    set_error("null argument");
+    return BMV_ERR_INVALID;
+  }
+  *out = nullptr;
+  StreamBuild sb;
+  int stage_bytes = 0;
+  {
+    const int rc0 = plan_k5(d, sb, stage_bytes);
+    if (rc0 != BMV_OK) return rc0;
+  }
   auto* p = new bmv_lane_plan();
   p->kind = 5;
   p->stage_bytes = stage_bytes;
@@ -796,6 +874,47 @@ int bmv_mmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doubl
   g.cmat = b;
   k5_lane_kernel<<<p->n_parts, kLnThreads, p->smem_bytes, st>>>(g);
   BMV_CHECK_LAUNCH();
+  return BMV_OK;
+}
+
+/* Host-only: the plan's stage stream (metadata words, copy entries, part
+   ranges) for CPU emulation in the tests; arrays malloc'ed, freed with
+   bmv_lane_host_free.  kind 4: desc is a bmv_tmmult_lane_desc, 5: mmult. */
+int bmv_lane_plan_host(int32_t kind, const void* desc, int32_t n_parts, bmv_lane_host* out) {
+  if (!desc || !out || (kind != 4 && kind != 5)) {
+    set_error("invalid lane plan host request");
+    return BMV_ERR_INVALID;
+  }
+  StreamBuild sb;
+  int stage_bytes = 0;
+  const int rc = kind == 4 ? plan_k4(static_cast<const bmv_tmmult_lane_desc*>(desc), sb, stage_bytes, n_parts)
+                           : plan_k5(static_cast<const bmv_mmult_lane_desc*>(desc), sb, stage_bytes);
+  if (rc != BMV_OK) return rc;
+  std::vector<int64_t> ss, es;
+  if (!sb.chunk_work.empty()) sb.parts(n_parts, ss, es);
+  out->stage_bytes = stage_bytes;
+  out->n_parts = sb.chunk_work.empty() ? 0 : (int32_t)ss.size() - 1;
+  out->meta_len = (int64_t)sb.meta.size();
+  out->n_entries = (int64_t)sb.cps.size() / 4;
+  out->meta = static_cast<int32_t*>(malloc(sizeof(int32_t) * (sb.meta.size() + 1)));
+  out->copies = static_cast<int32_t*>(malloc(sizeof(int32_t) * (sb.cps.size() + 1)));
+  out->part_sub_start = static_cast<int64_t*>(malloc(sizeof(int64_t) * (ss.size() + 1)));
+  out->part_entry_start = static_cast<int64_t*>(malloc(sizeof(int64_t) * (es.size() + 1)));
+  std::copy(sb.meta.begin(), sb.meta.end(), out->meta);
+  std::copy(sb.cps.begin(), sb.cps.end(), out->copies);
+  std::copy(ss.begin(), ss.end(), out->part_sub_start);
+  std::copy(es.begin(), es.end(), out->part_entry_start);
+  return BMV_OK;
+}
+
+int bmv_lane_host_free(bmv_lane_host* h) {
+  if (!h) return BMV_OK;
+  free(h->meta);
+  free(h->copies);
+  free(h->part_sub_start);
+  free(h->part_entry_start);
+  h->meta = h->copies = nullptr;
+  h->part_sub_start = h->part_entry_start = nullptr;
   return BMV_OK;
 }
 

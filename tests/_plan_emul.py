@@ -134,3 +134,90 @@ def emulate_mmult(arr, a_data, b_data, c_data, alpha=1.0, accumulate=False):
                 written[o:o + cv] = True
                 c[o:o + cv] = (c[o:o + cv] if accumulate else 0.0) + alpha * acc[i]
     return c
+
+
+# -- lane-compacted kernels (csrc/bmv_spmm_lane.cu) -----------------------------
+
+
+def _i32(buf, byte_off, n):
+    return buf[byte_off:byte_off + 4 * n].view(np.int32)
+
+
+def emulate_tmmult_lane(arr, a_data, b_data, c_len):
+    """k4_lane_kernel over a lane plan: tiles -> shared accumulator -> flush."""
+    srcs = [arr["meta"].view(np.uint8), a_data.view(np.uint8), b_data.view(np.uint8)]
+    sb = arr["stage_bytes"]
+    out = np.zeros(c_len)
+    acc = np.zeros(64 * 64)
+    pss = arr["part_sub_start"]
+    for s_idx, ents in _subs(arr):
+        if s_idx in pss:  # a new CTA: its accumulator starts empty
+            assert not acc.any(), "accumulator of the previous part not flushed"
+        buf, mask = _stage(ents, srcs, sb)
+        hdr = _i32(buf, 0, 4)
+        n_tiles, n_flush, rec_off, fl_off = (int(v) for v in hdr)
+        dbl = buf[: sb - sb % 8].view(np.float64)
+        dmask = mask[: sb - sb % 8].reshape(-1, 8).all(axis=1)
+        for t in range(n_tiles):
+            r = _i32(buf, 4 * (rec_off + 20 * t), 20)
+            rows, bs = int(r[17]) & 0xFFFF, int(r[17]) >> 16
+            nb = int(r[18])
+            B = np.zeros((rows, 8))
+            for n in range(nb):
+                idx = int(r[16]) + n + bs * np.arange(rows)
+                assert dmask[idx].all(), "B read outside the staged data"
+                B[:, n] = dbl[idx]
+            for m in range(8):
+                ac = int(r[m])
+                if ac < 0 or int(r[8 + m]) < 0:
+                    continue
+                ao, as_ = ac & 0xFFFF, (ac >> 16) & 0x7FFF
+                idx = ao + as_ * np.arange(rows)
+                assert dmask[idx].all(), "A read outside the staged data"
+                acc[int(r[8 + m]): int(r[8 + m]) + nb] += dbl[idx] @ B[:, :nb]
+        for f in range(n_flush):
+            x, y, z, w = (int(v) for v in _i32(buf, 4 * fl_off + 16 * f, 4))
+            rr, cc = z & 0xFF, (z >> 8) & 0xFF
+            tile = acc[w * 64: w * 64 + 64].reshape(8, 8)
+            for row in range(rr):
+                out[x + row * y: x + row * y + cc] += tile[row, :cc]
+            acc[w * 64: w * 64 + 64] = 0.0
+    assert not acc.any(), "accumulator not flushed"
+    return out
+
+
+def emulate_mmult_lane(arr, a_data, b_data, c_data, alpha=1.0, accumulate=False):
+    """k5_lane_kernel over a lane plan (c_data: the output before the call)."""
+    srcs = [arr["meta"].view(np.uint8), a_data.view(np.uint8)]
+    sb = arr["stage_bytes"]
+    out = c_data.copy()
+    for _s, ents in _subs(arr):
+        buf, mask = _stage(ents, srcs, sb)
+        n_tasks, toff = (int(v) for v in _i32(buf, 0, 2))
+        dbl = buf[: sb - sb % 8].view(np.float64)
+        dmask = mask[: sb - sb % 8].reshape(-1, 8).all(axis=1)
+        offs = _i32(buf, 4 * toff, n_tasks)
+        for t in range(n_tasks):
+            r0 = int(offs[t])
+            head = _i32(buf, 4 * r0, 4)
+            yoff = (int(head[0]) & 0xFFFFFFFF) | (int(head[1]) << 32)
+            rows, ys = int(head[2]) & 0xFFFF, int(head[2]) >> 16
+            ncol, nst, ks = int(head[3]) & 0xFF, (int(head[3]) >> 8) & 0xFF, int(head[3]) >> 16
+            rec = _i32(buf, 4 * (r0 + 4), 8 * ks)
+            D = np.zeros((rows, 8))
+            for s in range(ks):
+                for m in range(4):
+                    ac, co = int(rec[8 * s + m]), int(rec[8 * s + 4 + m])
+                    if ac < 0 or co < 0:
+                        continue
+                    ao, as_ = ac & 0xFFFF, (ac >> 16) & 0x7FFF
+                    idx = ao + as_ * np.arange(rows)
+                    assert dmask[idx].all(), "A read outside the staged data"
+                    crow = np.zeros(8)
+                    crow[:ncol] = b_data[co: co + ncol]
+                    D += np.outer(dbl[idx], crow)
+            for row in range(rows):
+                p = yoff + row * ys
+                v = alpha * D[row, :nst]
+                out[p: p + nst] = (out[p: p + nst] + v) if accumulate else v
+    return out

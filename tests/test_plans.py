@@ -60,3 +60,55 @@ def test_mmult_plan_emulation(block_size, lane_width, n_parts, accumulate):
         want = want + before
     assert np.allclose(xc.to_dense_owned(), want, rtol=1e-13, atol=1e-13 * np.abs(want).max())
     assert n_pairs > 0 and flops > 0 and n_out > 0
+
+
+# -- lane-compacted K4 / K5 (csrc/bmv_spmm_lane.cu): planner in the library,
+#    kernels emulated on CPU over the host stage stream ----------------------
+
+
+@pytest.mark.parametrize("block_size,lane_width", [(3, 8), (8, 8), (12, 8), (3, 4), (5, 2)])
+@pytest.mark.parametrize("attach", [False, True])
+@pytest.mark.parametrize("n_parts", [1, 7])
+def test_tmmult_lane_plan_emulation(block_size, lane_width, attach, n_parts):
+    from _plan_emul import emulate_tmmult_lane
+
+    s = Small((4, 4, 4), (1.0, 1.0, 1.0), 1, 2, CENTERS, 1.6, block_size, 3)
+    ctx = serial_context("cpu")
+    rl, _, x, hx = s.operands(ctx, "cpu", lane_width)
+    s.fill(x, 5, attach=attach)
+    hx.fill_owned_entries(lambda r, c: hashed_entries(9, r, c))
+    sm, _, _ = s.projection_operands(ctx, "cpu", rl, lane_width)
+    d, keep = B.tmmult_lane_desc(x, hx, sm)
+    arr = B.lane_plan_host(4, d, n_parts)
+    got = emulate_tmmult_lane(arr, x.data.numpy(), hx.data.numpy(), sm.data.numel())
+    import torch
+
+    sm.data.copy_(torch.from_numpy(got))
+    want = x.to_dense_owned().T @ hx.to_dense_owned()
+    assert np.allclose(sm.to_dense_owned(), want, rtol=1e-13, atol=1e-13 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("block_size,lane_width", [(3, 8), (8, 8), (12, 8), (3, 4), (5, 2)])
+@pytest.mark.parametrize("attach", [False, True])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_mmult_lane_plan_emulation(block_size, lane_width, attach, accumulate):
+    import torch
+
+    from _plan_emul import emulate_mmult_lane
+
+    s = Small((4, 4, 4), (1.0, 1.0, 1.0), 1, 2, CENTERS, 1.6, block_size, 3)
+    ctx = serial_context("cpu")
+    rl, _, x, hx = s.operands(ctx, "cpu", lane_width)
+    s.fill(x, 5, attach=attach)
+    _, cm, xc = s.projection_operands(ctx, "cpu", rl, lane_width)
+    xc.fill_owned_entries(lambda r, c: hashed_entries(3, r, c))
+    before = xc.to_dense_owned()
+    d, keep = B.mmult_lane_desc(x, cm, xc)
+    arr = B.lane_plan_host(5, d, 3)
+    got = emulate_mmult_lane(arr, x.data.numpy(), cm.data.numpy(), xc.data.numpy(), -0.5,
+                             accumulate)
+    xc.data.copy_(torch.from_numpy(got))
+    want = np.where(xc.pattern.entry_mask(), -0.5 * (x.to_dense_owned() @ cm.to_dense_owned()), 0.0)
+    if accumulate:
+        want = want + before
+    assert np.allclose(xc.to_dense_owned(), want, rtol=1e-13, atol=1e-13 * np.abs(want).max())

@@ -443,6 +443,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu_baseline = cpu_baseline_leg(st, prob, cnt)
 
+    # collective (sum over ranks): every rank computes it
+    rk = spmm_roofline(st, cnt, ms_tm, ms_mm, float(peaks_file().get("hbm_gbs", 6650.0)),
+                       sum_over_ranks)
     if rank == 0:
         peaks = peaks_file()
         line = {
@@ -468,6 +471,7 @@ def main():
                          "hbm_frac_at_k1_time": round(cnt["bytes_hx"] / (ms_k1 * 1e-3) / 1e9
                                                       / float(peaks.get("hbm_gbs", 6650.0)), 4),
                          "traffic": traffic},
+            "roofline_kernels": rk,
             "gpu_launches": per_step_launches * args.steps,
             "setup_s": round(t_setup, 1),
             "clocks": clk,
@@ -478,6 +482,28 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def spmm_roofline(st, cnt, ms_tm, ms_mm, hbm_gbs, sum_over_ranks):
+    """K4 / K5 are HBM-bound: the BCSR layout streams whole stored blocks
+    (X + HX for K4; X read + X C written for K5), so the achieved bandwidth
+    is measured on the stored bytes; `algorithmic_frac` uses the nnz bytes of
+    SURVEY 8(d) (8 (nnzX + nnzHX) and 16 nnzX), a bound no padded-block
+    layout can reach."""
+    out = {}
+    for name, ms, stored, alg in (
+            ("k4_tmmult", ms_tm, 8 * (st.x.data.numel() + st.hx.data.numel() + st.s.data.numel()),
+             cnt["bytes_s"]),
+            ("k5_mmult", ms_mm, 8 * (st.x.data.numel() + st.xc.data.numel()), cnt["bytes_xc"])):
+        stored = sum_over_ranks(stored)
+        alg = sum_over_ranks(alg)
+        gbs = stored / (ms * 1e-3) / 1e9
+        out[name] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_gbs, "unit": "GB/s",
+                     "frac": round(gbs / hbm_gbs, 4), "bytes_per_launch": int(stored),
+                     "algorithmic_bytes": int(alg),
+                     "algorithmic_frac": round(alg / (ms * 1e-3) / 1e9 / hbm_gbs, 4),
+                     "ms": round(ms, 4)}
+    return out
 
 
 def _coef_args(st, spec, dev):

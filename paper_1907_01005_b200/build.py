@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libbmv.so"
-SOURCES = ["bmv_util.cu", "bmv_cellop.cu", "bmv_cellop_stream.cu", "bmv_project.cu", "bmv_postmul.cu", "bmv_spmm_lane.cu"]
+SOURCES = ["bmv_util.cu", "bmv_cellop.cu", "bmv_cellop_stream.cu", "bmv_cellop_tma.cu", "bmv_project.cu", "bmv_postmul.cu", "bmv_spmm_lane.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -69,8 +69,9 @@ class RankContext:
             acc = value
             for src in range(1, self.n_ranks):
                 acc = acc + self.irecv(src, ("_coll", seq)).wait()
-            for dst in range(1, self.n_ranks):
-                self.isend(dst, ("_coll_b", seq), acc)
+            sends = [self.isend(dst, ("_coll_b", seq), acc) for dst in range(1, self.n_ranks)]
+            for h in sends:  # complete before returning: a rank may tear down next
+                h.wait()
             return acc
         self.isend(0, ("_coll", seq), value)
         return self.irecv(0, ("_coll_b", seq)).wait()
@@ -87,7 +88,7 @@ class RankContext:
                 if src != root:
                     out[src] = self.irecv(src, ("_gath", seq)).wait()
             return out
-        self.isend(root, ("_gath", seq), value)
+        self.isend(root, ("_gath", seq), value).wait()
         return None
 
     def stream_sync(self):

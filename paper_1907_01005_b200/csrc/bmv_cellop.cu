@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "bmv_cellop_stream.cuh"
+#include "bmv_cellop_tma.cuh"
 #include "bmv_common.cuh"
 #include "bmv_sumfac.cuh"
 
@@ -253,6 +254,7 @@ struct bmv_cellop {
   uint32_t* cell_slots = nullptr;
   CellTables tables{};
   StreamPlan* stream = nullptr;  // TMA-streamed Hamiltonian path (bmv_cellop_stream.cu)
+  TmaPlan* tma = nullptr;        // TMA-staged Hamiltonian path (bmv_cellop_tma.cu), default
 };
 
 namespace {
@@ -405,6 +407,7 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
   }
   for (int k = 0; k < 3; ++k) p->tables.kin[k] = d->kin[k];
   rc = stream_plan_build(d, &p->stream);
+  if (rc == BMV_OK) rc = tma_plan_build(d, &p->tma);
   if (rc != BMV_OK) {
     bmv_cellop_destroy(p);
     return rc;
@@ -420,6 +423,7 @@ int bmv_cellop_destroy(bmv_cellop* p) {
   release(p->group_hoff);
   release(p->cell_slots);
   stream_plan_destroy(p->stream);
+  tma_plan_destroy(p->tma);
   delete p;
   return BMV_OK;
 }
@@ -472,6 +476,8 @@ int bmv_cellop_apply(bmv_cellop* p, int32_t kinetic, const double* coef, int64_t
   CellArgs args{p->pair_desc, p->group_xoff, p->group_hoff, p->cell_slots, coef, coef_stride,
                 0, p->n_pairs, x, hx};
   const bool use_coef = coef != nullptr;
+  if (p->tma && kinetic && (!coef || coef_stride == 0 || coef_stride == p->tma->q3p))
+    return tma_apply(p->tma, p->tables, coef, coef_stride != 0 ? 1 : 0, x, hx, st);
   if (p->stream && kinetic && (!coef || coef_stride == 0 || coef_stride == p->stream->q3p))
     return stream_apply(p->stream, p->tables, coef, coef_stride != 0 ? 1 : 0, x, hx, st);
   if (p->color_start.empty()) {

@@ -466,6 +466,9 @@ int bmv_cellop_apply(bmv_cellop* p, int32_t kinetic, const double* coef, int64_t
     return BMV_ERR_INVALID;
   }
   cudaStream_t st = as_stream(stream);
+  if (p->tma && p->n_pairs > 0 && x && hx && kinetic &&
+      (!coef || coef_stride == 0 || coef_stride == p->tma->q3p))
+    return tma_apply(p->tma, p->tables, coef, coef_stride != 0 ? 1 : 0, x, hx, zero_len, st);
   int rc = zero_launch(hx, zero_len, st);
   if (rc) return rc;
   if (p->n_pairs == 0) return BMV_OK;
@@ -476,8 +479,7 @@ int bmv_cellop_apply(bmv_cellop* p, int32_t kinetic, const double* coef, int64_t
   CellArgs args{p->pair_desc, p->group_xoff, p->group_hoff, p->cell_slots, coef, coef_stride,
                 0, p->n_pairs, x, hx};
   const bool use_coef = coef != nullptr;
-  if (p->tma && kinetic && (!coef || coef_stride == 0 || coef_stride == p->tma->q3p))
-    return tma_apply(p->tma, p->tables, coef, coef_stride != 0 ? 1 : 0, x, hx, st);
+
   if (p->stream && kinetic && (!coef || coef_stride == 0 || coef_stride == p->stream->q3p))
     return stream_apply(p->stream, p->tables, coef, coef_stride != 0 ? 1 : 0, x, hx, st);
   if (p->color_start.empty()) {

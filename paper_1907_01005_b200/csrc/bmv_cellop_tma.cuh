@@ -12,7 +12,7 @@ namespace bmv {
 // Per nodes-per-axis N: P pairs per warp; per-pair shared rows of CS
 // coefficients (>= Q3P = q^3 rounded to even) and SS slots (>= SRP = n^3
 // rounded to 4), padded off the bank period (bank model in DESIGN.md 4);
-// MINB CTAs of 4 warps per SM (shared memory at the largest group table).
+// MINB CTAs of 4 warps per SM.
 template <int N>
 struct TmaShape {
   static constexpr int P = 32 / N;
@@ -22,31 +22,30 @@ struct TmaShape {
   static constexpr int CS = N == 5 ? 134 : (N == 4 ? 66 : (N == 3 ? 28 : 10));
   static constexpr int SS = N == 5 ? 132 : (N == 4 ? 68 : SRP);
   static constexpr int MINB = N == 5 ? 3 : (N == 4 ? 4 : (N == 3 ? 5 : 8));
-  static constexpr int tile_bytes = (P * Tile<N>::TILE * 8 + 15) / 16 * 16;
+  static constexpr int tile_bytes0 = (P * Tile<N>::TILE * 8 + 15) / 16 * 16;
+  // the X offset rows overlay the tiles
+  static constexpr int tile_bytes = tile_bytes0 > P * SS * 4 ? tile_bytes0 : P * SS * 4;
   static constexpr int coef_bytes = P * CS * 8;
-  static constexpr int slot_bytes = P * SS * 4;
-  static __host__ __device__ constexpr int warp_bytes(int g4) {
-    return tile_bytes + coef_bytes + slot_bytes + P * 2 * g4 * 4;
-  }
+  static constexpr int hoff_bytes = P * SS * 4;
+  static constexpr int warp_bytes = tile_bytes + coef_bytes + hoff_bytes;
 };
 
 struct TmaPlan {
   int n = 0;
   int64_t n_pairs = 0;
-  int g4max = 4;
   int q3p = 0;
   int4* desc = nullptr;
-  int32_t* gxh = nullptr;
-  uint32_t* slots = nullptr;
+  int32_t* xoff = nullptr;
+  int32_t* hoff = nullptr;
 };
 
 // Built from the one-pass descriptor; *out stays null when not applicable
 // (colour mode, BMV_K1 selecting another kernel, > 32 groups per visit).
 int tma_plan_build(const bmv_cellop_desc* d, TmaPlan** out);
 void tma_plan_destroy(TmaPlan* tp);
-// hx += H x (hx zeroed by the caller); coef: null, per cell (coef_cell = 1,
+// hx[0:zero_len] = 0, then hx += H x; coef: null, per cell (coef_cell = 1,
 // row stride q3p) or one row (coef_cell = 0).
 int tma_apply(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,
-              const double* x, double* hx, cudaStream_t st);
+              const double* x, double* hx, int64_t zero_len, cudaStream_t st);
 
 }  // namespace bmv

@@ -25,6 +25,7 @@
 #include <string>
 #include <vector>
 
+#include "bmv_cellop_pair.cuh"
 #include "bmv_cellop_tma.cuh"
 #include "bmv_common.cuh"
 #include "bmv_sumfac.cuh"
@@ -47,11 +48,11 @@ struct TmaArgs {
   double* __restrict__ hx;
 };
 
-template <int N, bool COEF>
+template <int N, bool COEF, bool WIDE>
 __global__ void __launch_bounds__(kTmaWarps * 32, TmaShape<N>::MINB)
     cellop_tma_kernel(const TmaArgs a, const __grid_constant__ CellTables tb) {
-  using TS = TmaShape<N>;
-  constexpr int P = TS::P, N2 = N * N, TILE = Tile<N>::TILE;
+  using TS = TmaShape<N, WIDE>;
+  constexpr int P = TS::P, N2 = N * N, TILE = TS::L::TILE;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[kTmaWarps];
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, TmaShape<N>::MINB)
     }
   }
   double out[N][N];
-  sumfac_h_plane<N, COEF, 1>(u, out, buf, tt, lane_ok, cs + tt * N2, tb);
+  sumfac_h_plane<N, COEF, 1, typename TS::L>(u, out, buf, tt, lane_ok, cs + tt * N2, tb);
   if (ok) {
 #pragma unroll
     for (int y = 0; y < N; ++y)
@@ -116,11 +117,113 @@ __global__ void __launch_bounds__(kTmaWarps * 32, TmaShape<N>::MINB)
   (void)stride;
 }
 
+
+// One thread per pair (n <= 3; bmv_cellop_pair.cuh).  4 warps per CTA.
 template <int N, bool COEF>
+__global__ void __launch_bounds__(kTmaWarps * 32, 3)  // 27 values + 27 accumulators: no spills
+    cellop_pair_kernel(const TmaArgs a, const __grid_constant__ CellTables tb) {
+  using PS = PairShape<N>;
+  constexpr int N2 = N * N, N3 = N2 * N;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[kTmaWarps];
+  const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
+  const int64_t pair = ((int64_t)blockIdx.x * kTmaWarps + warp) * 32 + lid;
+  const bool ok = pair < a.n_pairs;
+  unsigned char* wbase = smem + warp * PS::warp_bytes;
+  int32_t* orow = reinterpret_cast<int32_t*>(wbase) + lid * PS::OU * 4;
+  double* crow = reinterpret_cast<double*>(wbase + 32 * 16 * PS::OU) + lid * PS::CU * 2;
+  if (lid == 0) mbar_init(&bar[warp], 1);
+  __syncwarp();
+  int4 d = make_int4(0, 0, 0, 0);
+  if (ok) d = __ldg(a.desc + pair);
+  const int lane = d.z & 0xffff;
+  const unsigned cbytes = COEF ? PS::Q3P * 8u : 0u;
+  unsigned total = __reduce_add_sync(~0u, ok ? cbytes + PS::SRP * 4u : 0u);
+  if (lid == 0) mbar_expect_tx(&bar[warp], total);
+  __syncwarp();
+  if (ok) {
+    if (COEF) bulk_g2s(crow, a.coef + (a.coef_cell ? (int64_t)d.y * PS::Q3P : 0), cbytes, &bar[warp]);
+    bulk_g2s(orow, a.xoff + (int64_t)d.x * PS::SRP, PS::SRP * 4u, &bar[warp]);
+  }
+  mbar_wait(&bar[warp], 0);
+  double v[N][N][N];
+#pragma unroll
+  for (int k4 = 0; k4 < PS::SRP / 4; ++k4) {
+    const int4 o = reinterpret_cast<const int4*>(orow)[k4];
+    const int oo[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int k = 4 * k4 + m;
+      if (k < N3) {
+        const double x = (ok && oo[m] >= 0) ? __ldg(a.x + (int64_t)oo[m] + lane) : 0.0;
+        v[k / N2][(k / N) % N][k % N] = x;
+      }
+    }
+  }
+  // the HX offsets replace the X offsets (lands during the arithmetic)
+  __syncwarp();
+  total = __reduce_add_sync(~0u, ok ? PS::SRP * 4u : 0u);
+  if (lid == 0) mbar_expect_tx(&bar[warp], total);
+  __syncwarp();
+  if (ok) bulk_g2s(orow, a.hoff + (int64_t)d.x * PS::SRP, PS::SRP * 4u, &bar[warp]);
+  // values at the Gauss points
+  contract3<N, 0, false>(v, tb.S);
+  contract3<N, 1, false>(v, tb.S);
+  contract3<N, 2, false>(v, tb.S);
+  double acc[N][N][N];
+  if (COEF) {
+#pragma unroll
+    for (int k2 = 0; k2 < PS::Q3P / 2; ++k2) {
+      const double2 c = reinterpret_cast<const double2*>(crow)[k2];
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int k = 2 * k2 + m;
+        if (k < N3) acc[k / N2][(k / N) % N][k % N] = (m ? c.y : c.x) * v[k / N2][(k / N) % N][k % N];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < N3; ++k) acc[k / N2][(k / N) % N][k % N] = 0.0;
+  }
+  grad3<N, 0>(v, acc, tb);
+  grad3<N, 1>(v, acc, tb);
+  grad3<N, 2>(v, acc, tb);
+  // back to the nodes
+  contract3<N, 0, true>(acc, tb.S);
+  contract3<N, 1, true>(acc, tb.S);
+  contract3<N, 2, true>(acc, tb.S);
+  mbar_wait(&bar[warp], 1);
+  if (ok) {
+#pragma unroll
+    for (int k4 = 0; k4 < PS::SRP / 4; ++k4) {
+      const int4 o = reinterpret_cast<const int4*>(orow)[k4];
+      const int oo[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int k = 4 * k4 + m;
+        if (k < N3) atomicAdd(a.hx + (int64_t)oo[m] + lane, acc[k / N2][(k / N) % N][k % N]);
+      }
+    }
+  }
+}
+
+template <int N, bool COEF, bool WIDE>
 int launch_tma(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,
                const double* x, double* hx, int64_t zero_len, cudaStream_t st) {
-  using TS = TmaShape<N>;
-  auto kern = cellop_tma_kernel<N, COEF>;
+  using TS = TmaShape<N, WIDE>;
+  if (N <= 3 && tp->per_pair) {
+    auto pk = cellop_pair_kernel<N < 4 ? N : 3, COEF>;
+    const int psmem = kTmaWarps * PairShape<N < 4 ? N : 3>::warp_bytes;
+    BMV_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
+    TmaArgs pargs{tp->desc, tp->xoff, tp->hoff, coef, coef_cell, tp->n_pairs, x, hx};
+    const int rc0 = zero_async(hx, zero_len, st);
+    if (rc0) return rc0;
+    const int64_t per = (int64_t)kTmaWarps * 32;
+    pk<<<(unsigned)((tp->n_pairs + per - 1) / per), kTmaWarps * 32, psmem, st>>>(pargs, tb);
+    BMV_CHECK_LAUNCH();
+    return BMV_OK;
+  }
+  auto kern = cellop_tma_kernel<N, COEF, WIDE>;
   const int smem = kTmaWarps * TS::warp_bytes;
   BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   TmaArgs args{tp->desc, tp->xoff, tp->hoff, coef, coef_cell, tp->n_pairs, x, hx};
@@ -164,6 +267,10 @@ int build_n(const bmv_cellop_desc* d, TmaPlan* tp) {
   tp->n = N;
   tp->n_pairs = d->n_pairs;
   tp->q3p = TS::Q3P;
+  const char* pe = std::getenv("BMV_K1_PAIR");
+  tp->per_pair = N <= 3 && !(pe && pe[0] == '0');
+  const char* we = std::getenv("BMV_K1_TILE5");
+  tp->wide = N == 5 && we && std::string(we) == "wide";
   int rc = upload(desc.data(), (int64_t)desc.size(), &tp->desc);
   if (rc == BMV_OK) rc = upload(xo.data(), (int64_t)xo.size(), &tp->xoff);
   if (rc == BMV_OK) rc = upload(ho.data(), (int64_t)ho.size(), &tp->hoff);
@@ -208,14 +315,18 @@ int tma_apply(const TmaPlan* tp, const CellTables& tb, const double* coef, int c
               const double* x, double* hx, int64_t zero_len, cudaStream_t st) {
   const bool c = coef != nullptr;
   switch (tp->n) {
-    case 2: return c ? launch_tma<2, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
-                     : launch_tma<2, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
-    case 3: return c ? launch_tma<3, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
-                     : launch_tma<3, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
-    case 4: return c ? launch_tma<4, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
-                     : launch_tma<4, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
-    case 5: return c ? launch_tma<5, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
-                     : launch_tma<5, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+    case 2: return c ? launch_tma<2, true, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
+                     : launch_tma<2, false, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+    case 3: return c ? launch_tma<3, true, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
+                     : launch_tma<3, false, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+    case 4: return c ? launch_tma<4, true, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
+                     : launch_tma<4, false, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+    case 5:
+      if (tp->wide)
+        return c ? launch_tma<5, true, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
+                 : launch_tma<5, false, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+      return c ? launch_tma<5, true, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
+               : launch_tma<5, false, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
     default:
       set_error("TMA plan with unsupported n %d", tp->n);
       return BMV_ERR_INVALID;

@@ -48,10 +48,10 @@ struct TmaArgs {
   double* __restrict__ hx;
 };
 
-template <int N, bool COEF, bool WIDE>
+template <int N, bool COEF, bool WIDE, bool GC>
 __global__ void __launch_bounds__(kTmaWarps * 32, TmaShape<N>::MINB)
     cellop_tma_kernel(const TmaArgs a, const __grid_constant__ CellTables tb) {
-  using TS = TmaShape<N, WIDE>;
+  using TS = TmaShape<N, WIDE, GC>;
   constexpr int P = TS::P, N2 = N * N, TILE = TS::L::TILE;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[kTmaWarps];
@@ -78,14 +78,18 @@ __global__ void __launch_bounds__(kTmaWarps * 32, TmaShape<N>::MINB)
   if (ok) d = __ldg(a.desc + pair);
   const int lane = d.z & 0xffff, stride = d.z >> 16;
   const bool issuer = ok && t == 0;
-  const unsigned cbytes = COEF ? TS::Q3P * 8u : 0u;
+  const unsigned cbytes = (COEF && !GC) ? TS::Q3P * 8u : 0u;
+  const double* gcf = a.coef + (a.coef_cell ? (int64_t)d.y * TS::Q3P : 0);
+  if (GC && COEF && ok) {  // the cell's coefficient row into L1 (used mid-computation)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(gcf + 32 * t));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(gcf + 32 * t + 16));
+  }
   const unsigned my_bytes = issuer ? cbytes + 2u * TS::SRP * 4u : 0u;
   const unsigned total = __reduce_add_sync(~0u, my_bytes);
   if (lid == 0) mbar_expect_tx(&bar[warp], total);  // the warp's single arrival
   __syncwarp();
   if (issuer) {
-    if (COEF)
-      bulk_g2s(cs, a.coef + (a.coef_cell ? (int64_t)d.y * TS::Q3P : 0), cbytes, &bar[warp]);
+    if (COEF && !GC) bulk_g2s(cs, gcf, cbytes, &bar[warp]);
     bulk_g2s(const_cast<int32_t*>(xs), a.xoff + (int64_t)d.x * TS::SRP, TS::SRP * 4u, &bar[warp]);
     bulk_g2s(const_cast<int32_t*>(hs), a.hoff + (int64_t)d.x * TS::SRP, TS::SRP * 4u, &bar[warp]);
   }
@@ -106,7 +110,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32, TmaShape<N>::MINB)
     }
   }
   double out[N][N];
-  sumfac_h_plane<N, COEF, 1, typename TS::L>(u, out, buf, tt, lane_ok, cs + tt * N2, tb);
+  if (GC)
+    sumfac_h_plane<N, COEF, 1, typename TS::L, GCoef>(u, out, buf, tt, lane_ok, GCoef{gcf + tt * N2}, tb);
+  else
+    sumfac_h_plane<N, COEF, 1, typename TS::L>(u, out, buf, tt, lane_ok, cs + tt * N2, tb);
   if (ok) {
 #pragma unroll
     for (int y = 0; y < N; ++y)
@@ -207,10 +214,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3)  // 27 values + 27 accumula
   }
 }
 
-template <int N, bool COEF, bool WIDE>
+template <int N, bool COEF, bool WIDE, bool GC = false>
 int launch_tma(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,
                const double* x, double* hx, int64_t zero_len, cudaStream_t st) {
-  using TS = TmaShape<N, WIDE>;
+  using TS = TmaShape<N, WIDE, GC>;
   if (N <= 3 && tp->per_pair) {
     auto pk = cellop_pair_kernel<N < 4 ? N : 3, COEF>;
     const int psmem = kTmaWarps * PairShape<N < 4 ? N : 3>::warp_bytes;
@@ -223,7 +230,7 @@ int launch_tma(const TmaPlan* tp, const CellTables& tb, const double* coef, int 
     BMV_CHECK_LAUNCH();
     return BMV_OK;
   }
-  auto kern = cellop_tma_kernel<N, COEF, WIDE>;
+  auto kern = cellop_tma_kernel<N, COEF, WIDE, GC>;
   const int smem = kTmaWarps * TS::warp_bytes;
   BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   TmaArgs args{tp->desc, tp->xoff, tp->hoff, coef, coef_cell, tp->n_pairs, x, hx};
@@ -269,6 +276,8 @@ int build_n(const bmv_cellop_desc* d, TmaPlan* tp) {
   tp->q3p = TS::Q3P;
   const char* pe = std::getenv("BMV_K1_PAIR");
   tp->per_pair = N <= 3 && !(pe && pe[0] == '0');
+  const char* ge = std::getenv("BMV_K1_COEF");
+  tp->gcoef = N == 5 && ge && std::string(ge) == "global";
   const char* we = std::getenv("BMV_K1_TILE5");
   tp->wide = N == 5 && we && std::string(we) == "wide";
   int rc = upload(desc.data(), (int64_t)desc.size(), &tp->desc);
@@ -322,6 +331,8 @@ int tma_apply(const TmaPlan* tp, const CellTables& tb, const double* coef, int c
     case 4: return c ? launch_tma<4, true, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
                      : launch_tma<4, false, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
     case 5:
+      if (tp->gcoef && c)
+        return launch_tma<5, true, false, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
       if (tp->wide)
         return c ? launch_tma<5, true, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
                  : launch_tma<5, false, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st);

@@ -15,8 +15,9 @@ namespace bmv {
 // coefficients (>= Q3P = q^3 rounded to even) and SS slots (>= SRP = n^3
 // rounded to 4), padded off the bank period (bank model in DESIGN.md 4);
 // MINB CTAs of 4 warps per SM.
-template <int N, bool WIDE = false>
+template <int N, bool WIDE = false, bool GC = false>
 struct TmaShape {
+  // GC: coefficients read from global (L1) instead of staged per pair
   // WIDE (n = 5 only): conflict-free transpose tiles, coefficient rows unpadded
   using L = typename std::conditional<WIDE && N == 5, Tile5Wide, Tile<N>>::type;
   static constexpr int P = 32 / N;
@@ -29,7 +30,7 @@ struct TmaShape {
   static constexpr int tile_bytes0 = (P * L::TILE * 8 + 15) / 16 * 16;
   // the X offset rows overlay the tiles
   static constexpr int tile_bytes = tile_bytes0 > P * SS * 4 ? tile_bytes0 : P * SS * 4;
-  static constexpr int coef_bytes = P * CS * 8;
+  static constexpr int coef_bytes = GC ? 0 : P * CS * 8;
   static constexpr int hoff_bytes = P * SS * 4;
   static constexpr int warp_bytes = tile_bytes + coef_bytes + hoff_bytes;
 };
@@ -40,6 +41,7 @@ struct TmaPlan {
   int q3p = 0;
   bool wide = false;      // n = 5 wide transpose tiles (BMV_K1_TILE5=wide)
   bool per_pair = false;  // n <= 3: thread-per-pair kernel (BMV_K1_PAIR=0 disables)
+  bool gcoef = false;     // n = 5: coefficients from global / L1 (BMV_K1_COEF=global)
   int4* desc = nullptr;
   int32_t* xoff = nullptr;
   int32_t* hoff = nullptr;

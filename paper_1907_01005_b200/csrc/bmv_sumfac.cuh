@@ -129,10 +129,18 @@ __device__ __forceinline__ void cp_async_wait_one() {
 // (3 + 3 transposed), 3 transposed interpolations = 12 contractions of n^4
 // FMAs, 4 transposes through the pair tile `buf`.  The coefficient of
 // quadrature point (qz = t, qy = i, qx = j) is read at cf[(i * N + j) * CS].
-template <int N, bool COEF, int CS, class L = Tile<N>>
+// Coefficient access: shared memory (plain pointer) or global through the
+// read-only path (GCoef).
+struct GCoef {
+  const double* p;
+};
+__device__ __forceinline__ double coef_at(const double* cf, int k) { return cf[k]; }
+__device__ __forceinline__ double coef_at(GCoef cf, int k) { return __ldg(cf.p + k); }
+
+template <int N, bool COEF, int CS, class L = Tile<N>, class CP = const double*>
 __device__ __forceinline__ void sumfac_h_plane(const double (&u)[N][N], double (&v2)[N][N],
                                                double* buf, int tt, bool lane_ok,
-                                               const double* cf, const CellTables& tb) {
+                                               CP cf, const CellTables& tb) {
   double v1[N][N];
   contract_fast<N, false>(u, v1, tb.S);   // x
   contract_slow<N, false>(v1, v2, tb.S);  // y
@@ -153,7 +161,7 @@ __device__ __forceinline__ void sumfac_h_plane(const double (&u)[N][N], double (
 #pragma unroll
     for (int i = 0; i < N; ++i)
 #pragma unroll
-      for (int j = 0; j < N; ++j) acc[i][j] = fma(cf[CS * (i * N + j)], v1[i][j], acc[i][j]);
+      for (int j = 0; j < N; ++j) acc[i][j] = fma(coef_at(cf, CS * (i * N + j)), v1[i][j], acc[i][j]);
   }
   a_to_b<N, L>(acc, v2, buf, tt, lane_ok);  // v2 = acc in B (qy = t): [qz][qx]
   // gx and gz in B layout, applied row/column-wise to limit live registers

@@ -95,6 +95,15 @@ int bmv_cellop_destroy(bmv_cellop* plan);
 int bmv_cellop_apply(bmv_cellop* plan, int32_t kinetic, const double* coef,
                      int64_t coef_stride, const double* x, double* hx, int64_t zero_len,
                      void* stream);
+/* Fused mass + Hamiltonian (reference compute_energy applies both to the
+   same X, energy.py:129-174): hx = H x and mx = M x from one gather and one
+   interpolation to the quadrature points; hx and mx share the plan's
+   destination pattern; both zeroed over [0, zero_len) first.  mass_coef:
+   the mass coefficient row (w3, padded to an even length, device).
+   Needs the TMA plan (BMV_ERR_INVALID otherwise).                          */
+int bmv_cellop_apply_hm(bmv_cellop* plan, const double* coef, int64_t coef_stride,
+                        const double* mass_coef, const double* x, double* hx, double* mx,
+                        int64_t zero_len, void* stream);
 /* Device evaluation of the Gaussian-sum potential coefficient:
    coef[c*q3 + q] = w3[q] * scale * sum_k exp(-|x - center_k|^2 * inv_sigma2)
    at x = cell_origins[c] + quad_offsets[q].  All arrays device. */

@@ -102,6 +102,9 @@ SIGNATURES = [
      [C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
       C.c_double, C.c_double, C.c_void_p, C.c_void_p]),
     ("bmv_cellop_launches", C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    ("bmv_cellop_apply_hm", C.c_int,
+     [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+      C.c_int64, C.c_void_p]),
     ("bmv_tmmult_create", C.c_int, [C.POINTER(TmmultDesc), C.POINTER(C.c_void_p)]),
     ("bmv_tmmult_destroy", C.c_int, [C.c_void_p]),
     ("bmv_tmmult_run", C.c_int,

@@ -494,6 +494,25 @@ int bmv_cellop_apply(bmv_cellop* p, int32_t kinetic, const double* coef, int64_t
   return BMV_OK;
 }
 
+int bmv_cellop_apply_hm(bmv_cellop* p, const double* coef, int64_t coef_stride,
+                        const double* mass_coef, const double* x, double* hx, double* mx,
+                        int64_t zero_len, void* stream) {
+  if (!p || !mass_coef || !x || !hx || !mx) {
+    set_error("null argument");
+    return BMV_ERR_INVALID;
+  }
+  if (!p->tma || p->n_pairs == 0) {
+    set_error("the fused H + mass apply needs the TMA plan (BMV_K1=tma) and pairs");
+    return BMV_ERR_INVALID;
+  }
+  if (coef && coef_stride != 0 && coef_stride != p->tma->q3p) {
+    set_error("coefficient stride %lld: expected 0 or %d", (long long)coef_stride, p->tma->q3p);
+    return BMV_ERR_INVALID;
+  }
+  return tma_apply_hm(p->tma, p->tables, coef, coef_stride != 0 ? 1 : 0, mass_coef, x, hx, mx,
+                      zero_len, as_stream(stream));
+}
+
 int bmv_cellop_launches(const bmv_cellop* p, int32_t* out) {
   if (!p || !out) {
     set_error("null argument");

@@ -46,9 +46,39 @@ struct TmaArgs {
   int64_t n_pairs;
   const double* __restrict__ x;
   double* __restrict__ hx;
+  double* __restrict__ mx;           // fused mass output (DUAL), same layout as hx
+  const double* __restrict__ mcoef;  // mass coefficient row (w3, q3p doubles)
 };
 
-template <int N, bool COEF, bool WIDE, bool GC>
+// Scatter-add of a pair's plane result (A layout) through the HX offset row.
+struct PlaneScatter {
+  double* dst;
+  const int32_t* hs;
+  int t, lane;
+  bool ok;
+  template <int N, class L>
+  __device__ __forceinline__ void operator()(double (&v)[N][N], double*, int, bool,
+                                             const CellTables&) const {
+    if (!ok) return;
+#pragma unroll
+    for (int y = 0; y < N; ++y)
+#pragma unroll
+      for (int x = 0; x < N; ++x) atomicAdd(dst + (int64_t)hs[t * N * N + y * N + x] + lane, v[y][x]);
+  }
+};
+// The fused mass operator: w3 * uq back to the nodes, scattered into mx.
+struct MassScatter {
+  PlaneScatter sc;
+  const double* w3;
+  template <int N, class L>
+  __device__ __forceinline__ void operator()(double (&uqB)[N][N], double* buf, int tt,
+                                             bool lane_ok, const CellTables& tb) const {
+    mass_back_plane<N, L>(uqB, w3, buf, tt, lane_ok, tb);
+    sc.template operator()<N, L>(uqB, buf, tt, lane_ok, tb);
+  }
+};
+
+template <int N, bool COEF, bool WIDE, bool GC, bool DUAL = false>
 __global__ void __launch_bounds__(kTmaWarps * 32, TmaShape<N>::MINB)
     cellop_tma_kernel(const TmaArgs a, const __grid_constant__ CellTables tb) {
   using TS = TmaShape<N, WIDE, GC>;
@@ -110,6 +140,13 @@ __global__ void __launch_bounds__(kTmaWarps * 32, TmaShape<N>::MINB)
     }
   }
   double out[N][N];
+  if (DUAL) {  // H x to hx and M x to mx from one gather and one interpolation
+    const PlaneScatter hsc{a.hx, hs, t, lane, ok};
+    sumfac_h_plane<N, COEF, 1, typename TS::L, const double*, MassScatter, PlaneScatter>(
+        u, out, buf, tt, lane_ok, cs + tt * N2, tb,
+        MassScatter{PlaneScatter{a.mx, hs, t, lane, ok}, a.mcoef}, hsc);
+    return;
+  }
   if (GC)
     sumfac_h_plane<N, COEF, 1, typename TS::L, GCoef>(u, out, buf, tt, lane_ok, GCoef{gcf + tt * N2}, tb);
   else
@@ -212,6 +249,25 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3)  // 27 values + 27 accumula
       }
     }
   }
+}
+
+template <int N, bool COEF>
+int launch_dual(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,
+                const double* mcoef, const double* x, double* hx, double* mx, int64_t zero_len,
+                cudaStream_t st) {
+  using TS = TmaShape<N, false, false>;
+  auto kern = cellop_tma_kernel<N, COEF, false, false, true>;
+  const int smem = kTmaWarps * TS::warp_bytes;
+  BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  TmaArgs args{tp->desc, tp->xoff, tp->hoff, coef, coef_cell, tp->n_pairs, x, hx, mx, mcoef};
+  int rc = zero_async(hx, zero_len, st);
+  if (rc == BMV_OK) rc = zero_async(mx, zero_len, st);
+  if (rc) return rc;
+  const int64_t per_cta = (int64_t)kTmaWarps * TS::P;
+  const int64_t grid = (tp->n_pairs + per_cta - 1) / per_cta;
+  kern<<<(unsigned)grid, kTmaWarps * 32, smem, st>>>(args, tb);
+  BMV_CHECK_LAUNCH();
+  return BMV_OK;
 }
 
 template <int N, bool COEF, bool WIDE, bool GC = false>
@@ -318,6 +374,25 @@ void tma_plan_destroy(TmaPlan* tp) {
   release(tp->xoff);
   release(tp->hoff);
   delete tp;
+}
+
+int tma_apply_hm(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,
+                 const double* mcoef, const double* x, double* hx, double* mx, int64_t zero_len,
+                 cudaStream_t st) {
+  const bool c = coef != nullptr;
+#define BMV_DUAL(NN)                                                                       \
+  return c ? launch_dual<NN, true>(tp, tb, coef, coef_cell, mcoef, x, hx, mx, zero_len, st) \
+           : launch_dual<NN, false>(tp, tb, coef, coef_cell, mcoef, x, hx, mx, zero_len, st)
+  switch (tp->n) {
+    case 2: BMV_DUAL(2);
+    case 3: BMV_DUAL(3);
+    case 4: BMV_DUAL(4);
+    case 5: BMV_DUAL(5);
+    default:
+      set_error("TMA plan with unsupported n %d", tp->n);
+      return BMV_ERR_INVALID;
+  }
+#undef BMV_DUAL
 }
 
 int tma_apply(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,

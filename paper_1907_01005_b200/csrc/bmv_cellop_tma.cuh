@@ -55,5 +55,10 @@ void tma_plan_destroy(TmaPlan* tp);
 // row stride q3p) or one row (coef_cell = 0).
 int tma_apply(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,
               const double* x, double* hx, int64_t zero_len, cudaStream_t st);
+// Fused: hx = H x and mx = M x (mass coefficient row mcoef = w3), hx and mx on
+// the same pattern (same offsets), both zeroed over [0, zero_len) first.
+int tma_apply_hm(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,
+                 const double* mcoef, const double* x, double* hx, double* mx, int64_t zero_len,
+                 cudaStream_t st);
 
 }  // namespace bmv

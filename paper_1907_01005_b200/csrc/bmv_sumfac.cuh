@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "bmv.h"
 
 namespace bmv {
@@ -137,10 +139,23 @@ struct GCoef {
 __device__ __forceinline__ double coef_at(const double* cf, int k) { return cf[k]; }
 __device__ __forceinline__ double coef_at(GCoef cf, int k) { return __ldg(cf.p + k); }
 
-template <int N, bool COEF, int CS, class L = Tile<N>, class CP = const double*>
+struct NoMass {
+  template <int N, class L>
+  __device__ __forceinline__ void operator()(double (&)[N][N], double*, int, bool,
+                                             const CellTables&) const {}
+};
+
+// MASS (optional): called with the values at the quadrature points in B
+// layout (qy = t, [qz][qx]) once the Hamiltonian no longer needs them, after
+// the Hamiltonian result has been handed to HOUT (A layout); it owns the
+// array from then on (the fused mass + Hamiltonian apply).
+template <int N, bool COEF, int CS, class L = Tile<N>, class CP = const double*,
+          class MASS = NoMass, class HOUT = NoMass>
 __device__ __forceinline__ void sumfac_h_plane(const double (&u)[N][N], double (&v2)[N][N],
                                                double* buf, int tt, bool lane_ok,
-                                               CP cf, const CellTables& tb) {
+                                               CP cf, const CellTables& tb,
+                                               const MASS& mass = MASS(),
+                                               const HOUT& hout = HOUT()) {
   double v1[N][N];
   contract_fast<N, false>(u, v1, tb.S);   // x
   contract_slow<N, false>(v1, v2, tb.S);  // y
@@ -209,6 +224,28 @@ __device__ __forceinline__ void sumfac_h_plane(const double (&u)[N][N], double (
   contract_fast<N, true>(v1, v2, tb.S);   // S^T along x
   b_to_a<N, L>(v2, v1, buf, tt, lane_ok);    // A: z = t, [qy][x]
   contract_slow<N, true>(v1, v2, tb.S);   // S^T along y -> out[y][x]
+  if (!std::is_same<MASS, NoMass>::value) {
+    hout.template operator()<N, L>(v2, buf, tt, lane_ok, tb);  // Hamiltonian result out
+    mass.template operator()<N, L>(uqB, buf, tt, lane_ok, tb);
+  }
+}
+
+// The mass operator on values at the quadrature points in B layout (qy = t):
+// w3 * uq, back to the nodes (S^T along z and x in B, transpose, y in A);
+// result in A layout (z = t, [y][x]) in m.
+template <int N, class L>
+__device__ __forceinline__ void mass_back_plane(double (&m)[N][N], const double* __restrict__ w3,
+                                                double* buf, int tt, bool lane_ok,
+                                                const CellTables& tb) {
+  double v1[N][N];
+#pragma unroll
+  for (int z = 0; z < N; ++z)
+#pragma unroll
+    for (int x = 0; x < N; ++x) m[z][x] *= __ldg(w3 + z * N * N + tt * N + x);
+  contract_slow<N, true>(m, v1, tb.S);    // S^T along z
+  contract_fast<N, true>(v1, m, tb.S);    // S^T along x
+  b_to_a<N, L>(m, v1, buf, tt, lane_ok);  // A: z = t
+  contract_slow<N, true>(v1, m, tb.S);    // S^T along y
 }
 
 }  // namespace bmv

@@ -606,6 +606,47 @@ class CellOperator:
         if counters is not None:
             self._count(spec, variant, plan, src, dst, counters)
 
+    def apply_h_and_mass(self, spec: OperatorSpec, src: BlockCsrMatrix, hdst: BlockCsrMatrix,
+                         mdst: BlockCsrMatrix, counters: OpCounters | None = None):
+        """hdst = H(spec) @ src and mdst = M @ src (the two products
+        compute_energy forms, reference energy.py:129-174), fused: one gather
+        of src and one interpolation to the quadrature points feed both
+        (bmv_cellop_apply_hm).  Same results as two `apply` calls; falls back
+        to them when the fused kernel does not apply (colour mode, other K1
+        variants, different destination patterns)."""
+        if spec.kind != HAMILTONIAN:
+            raise ShapeError("apply_h_and_mass takes the Hamiltonian spec")
+        for d in (hdst, mdst):
+            if d.layout is not self.layout or d.col_blocks != src.col_blocks:
+                raise ShapeError("operator and operands must share one rank layout and blocking")
+        lib = _lib.require_device()
+        plan = self.plan_for(src, hdst)
+        fused = (hdst.pattern is mdst.pattern and hdst.data.numel() == mdst.data.numel()
+                 and _scatter_mode() == "atomic")
+        if fused:
+            hdst.ensure_owned()
+            mdst.ensure_owned()
+            coef, stride = self.coefficient(spec, hdst.device)
+            mcoef, _ = self.coefficient(mass_operator(), hdst.device)
+            src.update_ghost_values()
+            rc = lib.bmv_cellop_apply_hm(
+                plan.handle.raw, _lib.dptr(coef) if coef is not None else C.c_void_p(None),
+                stride, _lib.dptr(mcoef), _lib.dptr(src.data), _lib.dptr(hdst.data),
+                _lib.dptr(mdst.data), hdst.data.numel(), _lib.stream_handle(hdst.device))
+            if rc == _lib.BMV_OK:
+                src.release_ghosts()
+                hdst.compress()
+                mdst.compress()
+                if counters is not None:
+                    self._count(spec, SUMFAC, plan, src, hdst, counters)
+                    self._count(mass_operator(), SUMFAC, plan, src, mdst, counters)
+                return
+            src.release_ghosts()
+            if rc != _lib.BMV_ERR_INVALID:
+                _lib.check(rc, "bmv_cellop_apply_hm")
+        self.apply(spec, src, hdst, counters=counters)
+        self.apply(mass_operator(), src, mdst, counters=counters)
+
     def _count(self, spec, variant, plan, src, dst, counters):
         n = plan.n
         w = src.lane_width

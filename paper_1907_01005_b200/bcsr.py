@@ -636,42 +636,87 @@ def _common_positions(dst: BlockCsrMatrix, src: BlockCsrMatrix):
     return np.arange(n_s)[ok], pos[ok], np.arange(n_s)[~ok]
 
 
+def _entry_offsets(m: BlockCsrMatrix, positions: np.ndarray) -> np.ndarray:
+    """Flat element offsets of the valid entries of blocks `positions`,
+    block by block, row-major inside a block (vectorised _entry_index)."""
+    positions = np.asarray(positions, dtype=np.int64)
+    if positions.size == 0:
+        return np.zeros(0, dtype=np.int64)
+    cb = m.col_index[positions]
+    n_c = m.col_blocks.sizes[cb].astype(np.int64)
+    n_r = m.local_row_sizes[m.pos_row[positions]].astype(np.int64)
+    owner, t = _expand(n_r * n_c)
+    r, c = t // n_c[owner], t % n_c[owner]
+    return m.block_offsets[positions[owner]] + r * m.col_strides[cb[owner]] + c
+
+
+def _glue_index(key, a: BlockCsrMatrix, build):
+    """Device index tensors of an element-wise glue operation, cached per
+    (operation, operand patterns, layouts) on the first operand."""
+    cache = _plan_cache(a)
+    hit = cache.get(key)
+    if hit is None:
+        arrays = build()
+        hit = tuple(torch.as_tensor(x, dtype=torch.int64, device=a.device) for x in arrays)
+        cache[key] = hit
+    return hit
+
+
+def _common_entries(dst: BlockCsrMatrix, src: BlockCsrMatrix):
+    """(dst offsets, src offsets) of the valid entries of the owned blocks both
+    store, and the src positions dst lacks."""
+    s_pos, d_pos, missing = _common_positions(dst, src)
+    return _entry_offsets(dst, d_pos), _entry_offsets(src, s_pos), missing
+
+
 def scale_add(c: BlockCsrMatrix, a: float, x: BlockCsrMatrix | None = None, b: float = 0.0):
+    """c <- a c + b x over stored blocks; x's pattern must sit inside c's
+    (reference bcsr.py:532-549).  Device element-wise ops on cached indices."""
     c._require(OWNED)
     c.data.mul_(a)
     if x is None or b == 0.0:
         return
     if x.col_blocks != c.col_blocks or x.layout.blocks != c.layout.blocks:
         raise ShapeError("scale_add operands have different blockings")
-    s_pos, d_pos, missing = _common_positions(c, x)
+    _, _, missing = _common_positions(c, x)
     if missing.size:
         p = int(missing[0])
         raise ShapeError(f"scale_add: block ({int(x.pos_row[p])}, {int(x.col_index[p])}) of x missing from c's pattern")
-    for sp, dp in zip(s_pos.tolist(), d_pos.tolist()):
-        c.block_valid(dp).add_(x.block_valid(sp), alpha=b)
+    di, si = _glue_index(("scale_add", id(c.pattern), id(x.pattern), id(x.layout)), c,
+                         lambda: _common_entries(c, x)[:2])
+    c.data.index_add_(0, di, x.data[si], alpha=b)
 
 
 def copy_pattern_subset(dst: BlockCsrMatrix, src: BlockCsrMatrix):
+    """dst <- src where both patterns store the block, zero elsewhere
+    (reference bcsr.py:552-563)."""
     dst.ensure_owned()
     dst.zero_out()
     if src.col_blocks != dst.col_blocks or src.layout.blocks != dst.layout.blocks:
         raise ShapeError("copy_pattern_subset operands have different blockings")
-    s_pos, d_pos, _ = _common_positions(dst, src)
-    for sp, dp in zip(s_pos.tolist(), d_pos.tolist()):
-        dst.block_valid(dp).copy_(src.block_valid(sp))
+    di, si = _glue_index(("copy_subset", id(dst.pattern), id(src.pattern), id(src.layout)), dst,
+                         lambda: _common_entries(dst, src)[:2])
+    dst.data[di] = src.data[si]
 
 
 def add_scaled_identity(c: BlockCsrMatrix, s: float):
+    """c <- c + s I on the owned diagonal blocks (reference bcsr.py:566-577)."""
     c._require(OWNED)
-    for lb in range(c.n_owned_blocks):
-        gb = c.layout.global_block_of_local(lb)
-        pos = c.block_pos_local(lb, gb)
-        if pos < 0:
-            raise PatternError(f"diagonal block ({gb}, {gb}) not stored")
-        v = c.block_valid(pos)
-        n = min(v.shape)
-        idx = torch.arange(n, device=v.device)
-        v[idx, idx] += s
+
+    def build():
+        idx = []
+        for lb in range(c.n_owned_blocks):
+            gb = c.layout.global_block_of_local(lb)
+            pos = c.block_pos_local(lb, gb)
+            if pos < 0:
+                raise PatternError(f"diagonal block ({gb}, {gb}) not stored")
+            n = min(int(c.local_row_sizes[lb]), int(c.col_blocks.sizes[gb]))
+            k = np.arange(n)
+            idx.append(int(c.block_offsets[pos]) + k * int(c.col_strides[gb]) + k)
+        return (np.concatenate(idx) if idx else np.zeros(0, dtype=np.int64),)
+
+    (di,) = _glue_index(("identity", id(c.pattern), id(c.layout)), c, build)
+    c.data[di] += s
 
 
 # -- K4 / K5 ----------------------------------------------------------------------
@@ -1540,20 +1585,58 @@ def tmmult(a: BlockCsrMatrix, b: BlockCsrMatrix, c: BlockCsrMatrix,
 
 
 def tr_tmmult(d: BlockCsrMatrix, g: BlockCsrMatrix, counters: OpCounters | None = None) -> float:
-    """tr(d^T g) over common stored blocks, reduced over ranks (OM glue)."""
+    """tr(d^T g) over common stored blocks, reduced over ranks (reference
+    bcsr.py:670-698; the line-search slope of the OM step)."""
     if d.layout.blocks != g.layout.blocks or d.layout.rank != g.layout.rank:
         raise ShapeError("operands must share row blocking and partitioning")
     if d.col_blocks != g.col_blocks:
         raise ShapeError("operands must share column blocking")
-    s_pos, d_pos, _ = _common_positions(g, d)
-    local = 0.0
-    for sp, dp in zip(s_pos.tolist(), d_pos.tolist()):
-        dv, gv = d.block_valid(sp), g.block_valid(dp)
-        local += float(torch.sum(dv * gv).item())
-        if counters is not None:
-            counters.flops += 2 * dv.numel()
+    gi, di = _glue_index(("tr_tmmult", id(g.pattern), id(d.pattern), id(d.layout)), g,
+                         lambda: _common_entries(g, d)[:2])
+    local = float(torch.dot(d.data[di], g.data[gi]).item()) if di.numel() else 0.0
+    if counters is not None:
+        counters.flops += 2 * int(di.numel())
     if d.ctx is not None:
         return float(d.ctx.allreduce_sum(local))
+    return local
+
+
+def tr_mult(t: BlockCsrMatrix, h: BlockCsrMatrix, counters: OpCounters | None = None) -> float:
+    """tr(t h) over stored blocks, reduced over ranks; h must be ghosted for
+    remote rows (reference bcsr.py:701-725; the OM energy)."""
+    if not np.array_equal(t.col_blocks.sizes, h.layout.blocks.sizes):
+        raise ShapeError("inner blockings differ")
+    if not np.array_equal(t.layout.blocks.sizes, h.col_blocks.sizes):
+        raise ShapeError("outer blockings differ")
+    if h.state != GHOSTED and h.layout.ghost_groups:
+        raise StateError("h must have updated ghost values before tr_mult")
+
+    def build():
+        ti, hi = [], []
+        for lb in range(t.n_owned_blocks):
+            k = t.layout.global_block_of_local(lb)
+            for pos in range(int(t.row_start[lb]), int(t.row_start[lb + 1])):
+                ell = int(t.col_index[pos])
+                hl = h.layout.local_block_of_global(ell)
+                if hl < 0:
+                    continue
+                hpos = h.block_pos_local(hl, k)
+                if hpos < 0:
+                    continue
+                nr, nc = int(t.local_row_sizes[lb]), int(t.col_blocks.sizes[ell])
+                r, c = np.meshgrid(np.arange(nr), np.arange(nc), indexing="ij")
+                ti.append(int(t.block_offsets[pos]) + r.ravel() * int(t.col_strides[ell]) + c.ravel())
+                hi.append(int(h.block_offsets[hpos]) + c.ravel() * int(h.col_strides[k]) + r.ravel())
+        z = np.zeros(0, dtype=np.int64)
+        return (np.concatenate(ti) if ti else z, np.concatenate(hi) if hi else z)
+
+    ti, hi = _glue_index(("tr_mult", id(t.pattern), id(h.pattern), id(t.layout), id(h.layout)), t,
+                         build)
+    local = float(torch.dot(t.data[ti], h.data[hi]).item()) if ti.numel() else 0.0
+    if counters is not None:
+        counters.flops += 2 * int(ti.numel())
+    if t.ctx is not None:
+        return float(t.ctx.allreduce_sum(local))
     return local
 
 

@@ -501,8 +501,12 @@ int bmv_cellop_apply_hm(bmv_cellop* p, const double* coef, int64_t coef_stride,
     set_error("null argument");
     return BMV_ERR_INVALID;
   }
-  if (!p->tma || p->n_pairs == 0) {
-    set_error("the fused H + mass apply needs the TMA plan (BMV_K1=tma) and pairs");
+  if (p->n_pairs == 0) {  // nothing to add: both results are zero (every rank takes this path)
+    int rc = zero_launch(hx, zero_len, as_stream(stream));
+    return rc ? rc : zero_launch(mx, zero_len, as_stream(stream));
+  }
+  if (!p->tma) {
+    set_error("the fused H + mass apply needs the TMA plan (BMV_K1=tma)");
     return BMV_ERR_INVALID;
   }
   if (coef && coef_stride != 0 && coef_stride != p->tma->q3p) {

@@ -27,7 +27,15 @@ sys.path.insert(0, REF)
 from bcsrmv.bcsr import BlockCsrMatrix, mmult, tmmult  # noqa: E402
 from bcsrmv.bench.problem import hashed_values  # noqa: E402
 from bcsrmv.comm import run_ranks  # noqa: E402
-from bcsrmv.energy import column_space_ghost_blocks, make_column_layout, projected_pattern  # noqa: E402
+from bcsrmv.energy import (  # noqa: E402
+    column_space_ghost_blocks,
+    compute_energy,
+    compute_gradient,
+    directional_derivative,
+    make_column_layout,
+    make_workspace,
+    projected_pattern,
+)
 from bcsrmv.localization import (  # noqa: E402
     build_support_sparsity,
     column_supports,
@@ -181,6 +189,37 @@ def make_smoke():
     print("smoke.npz", {k: v.shape for k, v in out.items() if k in ("x", "hx", "s")})
 
 
+def make_energy():
+    """The OM energy / gradient composition (reference energy.py:129-174) on the
+    smoke config at 1 and 2 ranks: E, G, mbar, hbar and the slope tr(G^T G)."""
+    centers = lattice((2, 2, 2), 0.5, 0.25)
+    out = {}
+    for n_ranks in (1, 2):
+        mesh, part, num, lay, sup, pat, gro = setup((8, 8, 8), (1 / 8,) * 3, 0, 2, centers, 0.3, 1,
+                                                    8, n_ranks)
+        pot = gaussian(centers, 0.2)
+
+        def program(ctx):
+            rl = make_dof_layout(ctx, mesh, part, num)
+            op = CellOperator(mesh, part, num, rl)
+            x = BlockCsrMatrix(pat, rl, ctx, 8)
+            x.fill_owned(filler(lay, sup, 1, scale=0.25))
+            ws = make_workspace(ctx, op, x, lay)
+            e = compute_energy(op, mass_operator(), hamiltonian_operator(pot), x, ws)
+            g = compute_gradient(ws)
+            slope = directional_derivative(g, g)
+            return (e, slope, g.to_dense_owned(), ws.mbar.to_dense_owned(),
+                    ws.hbar.to_dense_owned(), ws.phi_m.to_dense_owned())
+
+        parts = run_ranks(n_ranks, program)
+        out[f"r{n_ranks}_energy"] = np.asarray(parts[0][0])
+        out[f"r{n_ranks}_slope"] = np.asarray(parts[0][1])
+        for k, name in ((2, "g"), (3, "mbar"), (4, "hbar"), (5, "phi_m")):
+            out[f"r{n_ranks}_{name}"] = np.sum([p[k] for p in parts], axis=0)
+    np.savez_compressed(OUT / "energy.npz", **out)
+    print("energy.npz", {k: (v.shape if v.ndim else float(v)) for k, v in out.items()})
+
+
 def make_random():
     """Acceptance-style small problems (test_acceptance.py:68-127): p=1..4, ranks 1/2/4."""
     meshes = {1: (8, 8, 8), 2: (6, 6, 6), 3: (4, 4, 4), 4: (4, 4, 4)}
@@ -244,9 +283,11 @@ def make_digests():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["smoke", "random", "digests"]
+    which = sys.argv[1:] or ["smoke", "random", "digests", "energy"]
     if "smoke" in which:
         make_smoke()
+    if "energy" in which:
+        make_energy()
     if "random" in which:
         make_random()
     if "digests" in which:

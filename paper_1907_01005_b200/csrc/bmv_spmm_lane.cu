@@ -47,7 +47,8 @@ constexpr int kLnStages = 3;
 constexpr int kAccTiles = 64;                     // K4 shared accumulator: 64 tiles of 8x8
 constexpr int kSmemBudget = 227 * 1024 - 1024;
 constexpr int kK4Rec = 20;                        // int32 per K4 tile record
-constexpr int kMaxKSteps = 8;                     // K5: compact columns per row <= 32
+constexpr int kMaxKSteps = 16;                    // K5: compact columns per row <= 64
+constexpr int kKStepsSmall = 8;                   // K5 instantiation for rows with <= 32
 
 // ---- K4 ------------------------------------------------------------------------
 // Stage: [hdr 4 int: n_tiles, n_flush, tile rec offset (int), flush offset]
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(kLnThreads, 1) k4_lane_kernel(const LnArgs g) 
 // [3] valid lanes (columns of C) | stored lanes << 8 | ksteps << 16,
 // then per k-step 4 A columns (stage double offset | stride << 16, -1 none)
 // and 4 C element offsets (row a, column lane 0 of the tile; -1 none).
+template <int MAXK>
 __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[kLnStages], empty[kLnStages];
@@ -204,10 +206,10 @@ __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) 
       const int ncol = r[3] & 0xff, nst = (r[3] >> 8) & 0xff, ks = r[3] >> 16;
       // B fragments (C rows of the compact columns): lane (gid, tig) holds
       // C[a_{4s + tig}][gid] for every k-step s
-      double bf[kMaxKSteps];
-      int ac[kMaxKSteps];
+      double bf[MAXK];
+      int ac[MAXK];
 #pragma unroll
-      for (int s = 0; s < kMaxKSteps; ++s) {
+      for (int s = 0; s < MAXK; ++s) {
         bf[s] = 0.0;
         ac[s] = -1;
         if (s < ks) {
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) 
         const int row = r0 + gid;
         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-        for (int s = 0; s < kMaxKSteps; ++s) {
+        for (int s = 0; s < MAXK; ++s) {
           if (s < ks) {
             const int c = ac[s];
             const double a = (c >= 0 && row < rows) ? S[(c & 0xffff) + row * ((c >> 16) & 0x7fff)] : 0.0;
@@ -332,6 +334,7 @@ int align16(int x) { return (x + 15) & ~15; }
 
 struct bmv_lane_plan {
   int kind = 0;  // 4 or 5
+  int maxk = 0;  // K5: largest k-step count of a task
   int n_parts = 0;
   int stage_bytes = 0;
   int smem_bytes = 0;
@@ -676,7 +679,8 @@ int bmv_tmmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doub
 
 namespace {
 
-int plan_k5(const bmv_mmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out) {
+int plan_k5(const bmv_mmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out, int& maxk) {
+  maxk = 0;
   const int stage_bytes = (kSmemBudget / kLnStages) & ~127;
   stage_bytes_out = stage_bytes;
   Chunk cur;
@@ -732,6 +736,7 @@ int plan_k5(const bmv_mmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out)
       }
     }
     const int ks = (int)((cols.size() + 3) / 4);
+    maxk = std::max(maxk, ks);
     if (ks > kMaxKSteps) {
       set_error("mmult lane plan: block row %d has %d active columns (max %d)", i,
                 (int)cols.size(), 4 * kMaxKSteps);
@@ -833,12 +838,16 @@ int bmv_mmult_lane_create(const bmv_mmult_lane_desc* d, bmv_lane_plan** out) {
   *out = nullptr;
   StreamBuild sb;
   int stage_bytes = 0;
+  int k5_maxk = 0;
   {
-    const int rc0 = plan_k5(d, sb, stage_bytes);
+    int maxk = 0;
+    const int rc0 = plan_k5(d, sb, stage_bytes, maxk);
+    k5_maxk = maxk;
     if (rc0 != BMV_OK) return rc0;
   }
   auto* p = new bmv_lane_plan();
   p->kind = 5;
+  p->maxk = k5_maxk;
   p->stage_bytes = stage_bytes;
   p->smem_bytes = kLnStages * stage_bytes;
   int rc = sb.chunk_work.empty() ? BMV_OK : upload_stream(sb, sm_count(), p);
@@ -860,7 +869,8 @@ int bmv_mmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doubl
   cudaStream_t st = as_stream(stream);
   int rc = zero_async(c, zero_len, st);
   if (rc || p->n_parts == 0) return rc;
-  BMV_CUDA_TRY(cudaFuncSetAttribute(k5_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = p->maxk <= kKStepsSmall ? k5_lane_kernel<kKStepsSmall> : k5_lane_kernel<kMaxKSteps>;
+  BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     p->smem_bytes));
   LnArgs g{};
   g.part_sub_start = p->part_sub_start;
@@ -872,7 +882,7 @@ int bmv_mmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doubl
   g.accumulate = accumulate;
   g.stage_bytes = p->stage_bytes;
   g.cmat = b;
-  k5_lane_kernel<<<p->n_parts, kLnThreads, p->smem_bytes, st>>>(g);
+  kern<<<p->n_parts, kLnThreads, p->smem_bytes, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
@@ -886,9 +896,9 @@ int bmv_lane_plan_host(int32_t kind, const void* desc, int32_t n_parts, bmv_lane
     return BMV_ERR_INVALID;
   }
   StreamBuild sb;
-  int stage_bytes = 0;
+  int stage_bytes = 0, host_maxk = 0;
   const int rc = kind == 4 ? plan_k4(static_cast<const bmv_tmmult_lane_desc*>(desc), sb, stage_bytes, n_parts)
-                           : plan_k5(static_cast<const bmv_mmult_lane_desc*>(desc), sb, stage_bytes);
+                           : plan_k5(static_cast<const bmv_mmult_lane_desc*>(desc), sb, stage_bytes, host_maxk);
   if (rc != BMV_OK) return rc;
   std::vector<int64_t> ss, es;
   if (!sb.chunk_work.empty()) sb.parts(n_parts, ss, es);

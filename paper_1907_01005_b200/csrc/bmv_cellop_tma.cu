@@ -78,19 +78,19 @@ struct MassScatter {
   }
 };
 
-template <int N, bool COEF, bool WIDE, bool GC, bool DUAL = false>
-__global__ void __launch_bounds__(kTmaWarps * 32, TmaShape<N>::MINB)
+template <int N, bool COEF, bool WIDE, bool GC, bool DUAL = false, int WPC = kTmaWarps>
+__global__ void __launch_bounds__(WPC * 32, TmaShape<N>::MINB * kTmaWarps / WPC)
     cellop_tma_kernel(const TmaArgs a, const __grid_constant__ CellTables tb) {
   using TS = TmaShape<N, WIDE, GC>;
   constexpr int P = TS::P, N2 = N * N, TILE = TS::L::TILE;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[kTmaWarps];
+  __shared__ __align__(8) uint64_t bar[WPC];
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
   const int sub = lid / N;
   const int t = lid - sub * N;
   const bool lane_ok = sub < P;
   const int tt = lane_ok ? t : 0;
-  const int64_t pair = ((int64_t)blockIdx.x * kTmaWarps + warp) * P + sub;
+  const int64_t pair = ((int64_t)blockIdx.x * WPC + warp) * P + sub;
   const bool ok = lane_ok && pair < a.n_pairs;
 
   // per warp: [pair tiles | coefficient rows | HX offset rows]; the X offset
@@ -270,7 +270,7 @@ int launch_dual(const TmaPlan* tp, const CellTables& tb, const double* coef, int
   return BMV_OK;
 }
 
-template <int N, bool COEF, bool WIDE, bool GC = false>
+template <int N, bool COEF, bool WIDE, bool GC = false, int WPC = kTmaWarps>
 int launch_tma(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,
                const double* x, double* hx, int64_t zero_len, cudaStream_t st) {
   using TS = TmaShape<N, WIDE, GC>;
@@ -286,15 +286,15 @@ int launch_tma(const TmaPlan* tp, const CellTables& tb, const double* coef, int 
     BMV_CHECK_LAUNCH();
     return BMV_OK;
   }
-  auto kern = cellop_tma_kernel<N, COEF, WIDE, GC>;
-  const int smem = kTmaWarps * TS::warp_bytes;
+  auto kern = cellop_tma_kernel<N, COEF, WIDE, GC, false, WPC>;
+  const int smem = WPC * TS::warp_bytes;
   BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   TmaArgs args{tp->desc, tp->xoff, tp->hoff, coef, coef_cell, tp->n_pairs, x, hx};
   const int rc = zero_async(hx, zero_len, st);
   if (rc) return rc;
-  const int64_t per_cta = (int64_t)kTmaWarps * TS::P;
+  const int64_t per_cta = (int64_t)WPC * TS::P;
   const int64_t grid = (tp->n_pairs + per_cta - 1) / per_cta;
-  kern<<<(unsigned)grid, kTmaWarps * 32, smem, st>>>(args, tb);
+  kern<<<(unsigned)grid, WPC * 32, smem, st>>>(args, tb);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
@@ -332,6 +332,8 @@ int build_n(const bmv_cellop_desc* d, TmaPlan* tp) {
   tp->q3p = TS::Q3P;
   const char* pe = std::getenv("BMV_K1_PAIR");
   tp->per_pair = N <= 3 && !(pe && pe[0] == '0');
+  const char* wpe = std::getenv("BMV_K1_WPC");
+  tp->wpc = wpe ? std::atoi(wpe) : kTmaWarps;
   const char* ge = std::getenv("BMV_K1_COEF");
   tp->gcoef = N == 5 && ge && std::string(ge) == "global";
   const char* we = std::getenv("BMV_K1_TILE5");
@@ -411,6 +413,8 @@ int tma_apply(const TmaPlan* tp, const CellTables& tb, const double* coef, int c
       if (tp->wide)
         return c ? launch_tma<5, true, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
                  : launch_tma<5, false, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+      if (c && tp->wpc == 1) return launch_tma<5, true, false, false, 1>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+      if (c && tp->wpc == 2) return launch_tma<5, true, false, false, 2>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
       return c ? launch_tma<5, true, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
                : launch_tma<5, false, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
     default:

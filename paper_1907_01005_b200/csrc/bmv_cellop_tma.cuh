@@ -42,6 +42,7 @@ struct TmaPlan {
   bool wide = false;      // n = 5 wide transpose tiles (BMV_K1_TILE5=wide)
   bool per_pair = false;  // n <= 3: thread-per-pair kernel (BMV_K1_PAIR=0 disables)
   bool gcoef = false;     // n = 5: coefficients from global / L1 (BMV_K1_COEF=global)
+  int wpc = 4;            // n = 5: warps per CTA (BMV_K1_WPC = 1, 2 or 4)
   int4* desc = nullptr;
   int32_t* xoff = nullptr;
   int32_t* hoff = nullptr;

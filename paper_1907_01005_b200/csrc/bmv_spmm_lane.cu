@@ -457,7 +457,8 @@ int plan_k4(const bmv_tmmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out
       ncols += __builtin_popcountll(d->a_mask[pa]);
     for (int64_t pb = d->b_row_start[i]; pb < d->b_row_start[i + 1]; ++pb)
       ntl += (d->b_width[pb] + 7) / 8;
-    row_work[(size_t)i + 1] = row_work[(size_t)i] + ((ncols + 7) / 8) * ntl * (d->row_rows[i] + 4) + 16;
+    // per tile: ~130 warp instructions of decode / accumulator add + the DMMAs
+    row_work[(size_t)i + 1] = row_work[(size_t)i] + ((ncols + 7) / 8) * ntl * (d->row_rows[i] + 48) + 16;
   }
   const int n_parts = std::max(1, sm_count_host);
   int next_part = 1;

@@ -1591,11 +1591,19 @@ def tr_tmmult(d: BlockCsrMatrix, g: BlockCsrMatrix, counters: OpCounters | None 
         raise ShapeError("operands must share row blocking and partitioning")
     if d.col_blocks != g.col_blocks:
         raise ShapeError("operands must share column blocking")
-    gi, di = _glue_index(("tr_tmmult", id(g.pattern), id(d.pattern), id(d.layout)), g,
-                         lambda: _common_entries(g, d)[:2])
-    local = float(torch.dot(d.data[di], g.data[gi]).item()) if di.numel() else 0.0
-    if counters is not None:
-        counters.flops += 2 * int(di.numel())
+    if d.pattern is g.pattern and d.lane_width == g.lane_width:
+        # same blocks at the same offsets: one dot over the owned values (the
+        # padded lanes are exact zeros, the layout invariant)
+        n = d.n_owned_values
+        local = float(torch.dot(d.data[:n], g.data[:n]).item()) if n else 0.0
+        if counters is not None:
+            counters.flops += 2 * n
+    else:
+        gi, di = _glue_index(("tr_tmmult", id(g.pattern), id(d.pattern), id(d.layout)), g,
+                             lambda: _common_entries(g, d)[:2])
+        local = float(torch.dot(d.data[di], g.data[gi]).item()) if di.numel() else 0.0
+        if counters is not None:
+            counters.flops += 2 * int(di.numel())
     if d.ctx is not None:
         return float(d.ctx.allreduce_sum(local))
     return local

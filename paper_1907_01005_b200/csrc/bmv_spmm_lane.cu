@@ -47,8 +47,7 @@ constexpr int kLnStages = 3;
 constexpr int kAccTiles = 64;                     // K4 shared accumulator: 64 tiles of 8x8
 constexpr int kSmemBudget = 227 * 1024 - 1024;
 constexpr int kK4Rec = 20;                        // int32 per K4 tile record
-constexpr int kMaxKSteps = 16;                    // K5: compact columns per row <= 64
-constexpr int kKStepsSmall = 8;                   // K5 instantiation for rows with <= 32
+constexpr int kKGroup = 8;                        // K5: k-steps (4 compact columns each) per pass
 
 // ---- K4 ------------------------------------------------------------------------
 // Stage: [hdr 4 int: n_tiles, n_flush, tile rec offset (int), flush offset]
@@ -204,50 +203,56 @@ __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) 
       double* Y = g.out + (((int64_t)(unsigned)r[1] << 32) | (unsigned)r[0]);
       const int rows = r[2] & 0xffff, ys = r[2] >> 16;
       const int ncol = r[3] & 0xff, nst = (r[3] >> 8) & 0xff, ks = r[3] >> 16;
-      // B fragments (C rows of the compact columns): lane (gid, tig) holds
-      // C[a_{4s + tig}][gid] for every k-step s
-      double bf[MAXK];
-      int ac[MAXK];
-#pragma unroll
-      for (int s = 0; s < MAXK; ++s) {
-        bf[s] = 0.0;
-        ac[s] = -1;
-        if (s < ks) {
-          const int co = r[4 + 8 * s + 4 + tig];
-          if (co >= 0 && gid < ncol) bf[s] = __ldg(g.cmat + co + gid);
-          ac[s] = r[4 + 8 * s + tig];
-        }
-      }
-      for (int r0 = 0; r0 < rows; r0 += 8) {
-        const int row = r0 + gid;
-        double d0 = 0.0, d1 = 0.0;
+      // k-steps in groups of MAXK: lane (gid, tig) holds the B fragments
+      // C[a_{4s + tig}][gid] of the group; groups after the first add to the
+      // values the warp itself wrote (rows with more than 4 MAXK columns)
+      for (int kg = 0; kg < max(ks, 1); kg += MAXK) {
+        double bf[MAXK];
+        int ac[MAXK];
 #pragma unroll
         for (int s = 0; s < MAXK; ++s) {
-          if (s < ks) {
-            const int c = ac[s];
-            const double a = (c >= 0 && row < rows) ? S[(c & 0xffff) + row * ((c >> 16) & 0x7fff)] : 0.0;
-            dmma_8x8x4(d0, d1, a, bf[s]);
+          bf[s] = 0.0;
+          ac[s] = -1;
+          if (kg + s < ks) {
+            const int* e = r + 4 + 8 * (kg + s);
+            const int co = e[4 + tig];
+            if (co >= 0 && gid < ncol) bf[s] = __ldg(g.cmat + co + gid);
+            ac[s] = e[tig];
           }
         }
-        if (row < rows) {
-          double* p = Y + (int64_t)row * ys + 2 * tig;
-          double v0 = g.alpha * d0, v1 = g.alpha * d1;
-          if (2 * tig + 1 < nst) {
-            if (g.accumulate) {
-              const double2 o = *reinterpret_cast<const double2*>(p);
-              v0 += o.x;
-              v1 += o.y;
+        const bool add_old = g.accumulate || kg > 0;
+        for (int r0 = 0; r0 < rows; r0 += 8) {
+          const int row = r0 + gid;
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int s = 0; s < MAXK; ++s) {
+            if (kg + s < ks) {
+              const int c = ac[s];
+              const double a = (c >= 0 && row < rows) ? S[(c & 0xffff) + row * ((c >> 16) & 0x7fff)] : 0.0;
+              dmma_8x8x4(d0, d1, a, bf[s]);
             }
-            if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-              *reinterpret_cast<double2*>(p) = make_double2(v0, v1);
-            } else {
-              p[0] = v0;
-              p[1] = v1;
+          }
+          if (row < rows) {
+            double* p = Y + (int64_t)row * ys + 2 * tig;
+            double v0 = g.alpha * d0, v1 = g.alpha * d1;
+            if (2 * tig + 1 < nst) {
+              if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+                if (add_old) {
+                  const double2 o = *reinterpret_cast<const double2*>(p);
+                  v0 += o.x;
+                  v1 += o.y;
+                }
+                *reinterpret_cast<double2*>(p) = make_double2(v0, v1);
+              } else {
+                p[0] = add_old ? p[0] + v0 : v0;
+                p[1] = add_old ? p[1] + v1 : v1;
+              }
+            } else if (2 * tig < nst) {
+              p[0] = add_old ? p[0] + v0 : v0;
             }
-          } else if (2 * tig < nst) {
-            p[0] = g.accumulate ? p[0] + v0 : v0;
           }
         }
+        __syncwarp();  // the group's stores are visible to this warp's next group
       }
     }
     __syncwarp();
@@ -738,9 +743,9 @@ int plan_k5(const bmv_mmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out,
     }
     const int ks = (int)((cols.size() + 3) / 4);
     maxk = std::max(maxk, ks);
-    if (ks > kMaxKSteps) {
-      set_error("mmult lane plan: block row %d has %d active columns (max %d)", i,
-                (int)cols.size(), 4 * kMaxKSteps);
+    if (ks > 255) {
+      set_error("mmult lane plan: block row %d has %d active columns (max 1020)", i,
+                (int)cols.size());
       return BMV_ERR_INVALID;
     }
     int64_t a_first = na ? d->a_off[pa0] : 0;
@@ -870,7 +875,7 @@ int bmv_mmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doubl
   cudaStream_t st = as_stream(stream);
   int rc = zero_async(c, zero_len, st);
   if (rc || p->n_parts == 0) return rc;
-  auto kern = p->maxk <= kKStepsSmall ? k5_lane_kernel<kKStepsSmall> : k5_lane_kernel<kMaxKSteps>;
+  auto kern = k5_lane_kernel<kKGroup>;
   BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     p->smem_bytes));
   LnArgs g{};

@@ -112,3 +112,37 @@ def test_mmult_lane_plan_emulation(block_size, lane_width, attach, accumulate):
     if accumulate:
         want = want + before
     assert np.allclose(xc.to_dense_owned(), want, rtol=1e-13, atol=1e-13 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("attach", [False, True])
+def test_mmult_lane_many_columns_per_row(attach):
+    """Rows with more than 32 active columns: K5 passes over k-step groups and
+    adds to the values it wrote (k5_lane_kernel), emulated."""
+    import torch
+
+    from _plan_emul import emulate_mmult_lane
+
+    centers = np.asarray([[1.0, 1.0, 1.0], [3.0, 3.0, 2.0], [2.0, 1.5, 3.0], [0.5, 3.2, 0.7],
+                          [2.5, 2.5, 0.5], [1.5, 3.5, 2.5]])
+    s = Small((4, 4, 4), (1.0, 1.0, 1.0), 1, 2, centers, 3.5, 8, 8)  # 48 columns, wide supports
+    ctx = serial_context("cpu")
+    rl, _, x, hx = s.operands(ctx, "cpu")
+    s.fill(x, 5, attach=attach)
+    _, cm, xc = s.projection_operands(ctx, "cpu", rl)
+    d, keep = B.mmult_lane_desc(x, cm, xc)
+    arr = B.lane_plan_host(5, d, 3)
+    ks_max = 0
+    meta = arr["meta"]
+    cps = arr["copies"].astype(np.int64) & 0xFFFFFFFF
+    for e in cps:
+        if ((e[1] >> 28) & 3) == 0:
+            off = int(e[2] | (e[3] << 32)) // 4
+            n_t, toff = int(meta[off]), int(meta[off + 1])
+            for t in range(n_t):
+                r0 = off + int(meta[off + toff + t])
+                ks_max = max(ks_max, int(meta[r0 + 3]) >> 16)
+    assert ks_max > 8  # exercises several k-step groups
+    got = emulate_mmult_lane(arr, x.data.numpy(), cm.data.numpy(), xc.data.numpy(), 0.75, False)
+    xc.data.copy_(torch.from_numpy(got))
+    want = np.where(xc.pattern.entry_mask(), 0.75 * (x.to_dense_owned() @ cm.to_dense_owned()), 0.0)
+    assert np.allclose(xc.to_dense_owned(), want, rtol=1e-13, atol=1e-13 * np.abs(want).max())

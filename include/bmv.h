@@ -41,6 +41,8 @@ extern "C" {
 
 int bmv_version(void);
 const char* bmv_last_error(void);
+/* kernels this library has launched so far (all threads) */
+int bmv_launch_count(int64_t* out);
 /* number of SMs of the current device (grid sizing helper) */
 int bmv_device_sm_count(int* out);
 

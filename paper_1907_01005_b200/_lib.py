@@ -93,6 +93,7 @@ SIGNATURES = [
     ("bmv_version", C.c_int, []),
     ("bmv_last_error", C.c_char_p, []),
     ("bmv_device_sm_count", C.c_int, [C.POINTER(C.c_int)]),
+    ("bmv_launch_count", C.c_int, [_i64p]),
     ("bmv_cellop_create", C.c_int, [C.POINTER(CellopDesc), C.POINTER(C.c_void_p)]),
     ("bmv_cellop_destroy", C.c_int, [C.c_void_p]),
     ("bmv_cellop_apply", C.c_int,
@@ -213,6 +214,13 @@ class Handle:
                 self.raw = None
         except Exception:
             pass
+
+
+def launch_count() -> int:
+    """Kernels libbmv has launched so far (counted at every launch site)."""
+    v = C.c_int64()
+    check(load().bmv_launch_count(C.byref(v)), "bmv_launch_count")
+    return int(v.value)
 
 
 def require_device():

@@ -24,8 +24,13 @@ void set_error(const char* fmt, ...);
     }                                                                         \
   } while (0)
 
+// every kernel launch is followed by BMV_CHECK_LAUNCH(): it also counts it
+// (bmv_launch_count, used by bench.py's gpu_launches)
+void count_launch();
+
 #define BMV_CHECK_LAUNCH()                                                    \
   do {                                                                        \
+    ::bmv::count_launch();                                                    \
     cudaError_t e_ = cudaGetLastError();                                      \
     if (e_ != cudaSuccess) {                                                  \
       ::bmv::set_error("kernel launch failed: %s (%s:%d)",                    \

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 
@@ -34,6 +35,9 @@ int sm_count() {
 }
 
 int zero_async(double* p, int64_t n, cudaStream_t st);
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 }  // namespace bmv
 
@@ -97,6 +101,15 @@ __global__ void fp64_peak_kernel(double* out, int iters, double a, double b) {
 extern "C" {
 
 int bmv_version(void) { return 1; }
+
+int bmv_launch_count(int64_t* out) {
+  if (!out) {
+    bmv::set_error("null argument");
+    return BMV_ERR_INVALID;
+  }
+  *out = bmv::g_launches.load(std::memory_order_relaxed);
+  return BMV_OK;
+}
 
 const char* bmv_last_error(void) { return bmv::g_err; }
 

@@ -203,56 +203,29 @@ __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) 
       double* Y = g.out + (((int64_t)(unsigned)r[1] << 32) | (unsigned)r[0]);
       const int rows = r[2] & 0xffff, ys = r[2] >> 16;
       const int ncol = r[3] & 0xff, nst = (r[3] >> 8) & 0xff, ks = r[3] >> 16;
-      if (ks <= MAXK) {
-        // one group: lane (gid, tig) holds the B fragments C[a_{4s + tig}][gid]
-        double bf[MAXK];
-        int ac[MAXK];
-#pragma unroll
-        for (int s = 0; s < MAXK; ++s) {
-          bf[s] = 0.0;
-          ac[s] = -1;
-          if (s < ks) {
-            const int co = r[4 + 8 * s + 4 + tig];
-            if (co >= 0 && gid < ncol) bf[s] = __ldg(g.cmat + co + gid);
-            ac[s] = r[4 + 8 * s + tig];
-          }
-        }
-        for (int r0 = 0; r0 < rows; r0 += 8) {
-          const int row = r0 + gid;
-          double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-          for (int s = 0; s < MAXK; ++s) {
-            if (s < ks) {
-              const int c = ac[s];
-              const double a = (c >= 0 && row < rows) ? S[(c & 0xffff) + row * ((c >> 16) & 0x7fff)] : 0.0;
-              dmma_8x8x4(d0, d1, a, bf[s]);
+      auto store = [&](int row, double d0, double d1, bool add_old) {
+        double* p = Y + (int64_t)row * ys + 2 * tig;
+        double v0 = g.alpha * d0, v1 = g.alpha * d1;
+        if (2 * tig + 1 < nst) {
+          if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+            if (add_old) {
+              const double2 o = *reinterpret_cast<const double2*>(p);
+              v0 += o.x;
+              v1 += o.y;
             }
+            *reinterpret_cast<double2*>(p) = make_double2(v0, v1);
+          } else {
+            p[0] = add_old ? p[0] + v0 : v0;
+            p[1] = add_old ? p[1] + v1 : v1;
           }
-          if (row < rows) {
-            double* p = Y + (int64_t)row * ys + 2 * tig;
-            double v0 = g.alpha * d0, v1 = g.alpha * d1;
-            if (2 * tig + 1 < nst) {
-              if (g.accumulate) {
-                const double2 o = *reinterpret_cast<const double2*>(p);
-                v0 += o.x;
-                v1 += o.y;
-              }
-              if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-                *reinterpret_cast<double2*>(p) = make_double2(v0, v1);
-              } else {
-                p[0] = v0;
-                p[1] = v1;
-              }
-            } else if (2 * tig < nst) {
-              p[0] = g.accumulate ? p[0] + v0 : v0;
-            }
-          }
+        } else if (2 * tig < nst) {
+          p[0] = add_old ? p[0] + v0 : v0;
         }
-        continue;
-      }
+      };
       // k-steps in groups of MAXK: lane (gid, tig) holds the B fragments
-      // C[a_{4s + tig}][gid] of the group; groups after the first add to the
-      // values the warp itself wrote (rows with more than 4 MAXK columns)
+      // C[a_{4s + tig}][gid] of the group; two 8-row tiles in flight
+      // (independent DMMA chains); groups after the first add to the values
+      // the warp itself wrote (rows with more than 4 MAXK columns)
       for (int kg = 0; kg < max(ks, 1); kg += MAXK) {
         double bf[MAXK];
         int ac[MAXK];
@@ -268,36 +241,22 @@ __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) 
           }
         }
         const bool add_old = g.accumulate || kg > 0;
-        for (int r0 = 0; r0 < rows; r0 += 8) {
-          const int row = r0 + gid;
-          double d0 = 0.0, d1 = 0.0;
+        for (int r0 = 0; r0 < rows; r0 += 16) {
+          const int ra = r0 + gid, rb = r0 + 8 + gid;
+          double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
           for (int s = 0; s < MAXK; ++s) {
             if (kg + s < ks) {
               const int c = ac[s];
-              const double a = (c >= 0 && row < rows) ? S[(c & 0xffff) + row * ((c >> 16) & 0x7fff)] : 0.0;
-              dmma_8x8x4(d0, d1, a, bf[s]);
+              const int off = c & 0xffff, cs = (c >> 16) & 0x7fff;
+              const double xa = (c >= 0 && ra < rows) ? S[off + ra * cs] : 0.0;
+              const double xb = (c >= 0 && rb < rows) ? S[off + rb * cs] : 0.0;
+              dmma_8x8x4(a0, a1, xa, bf[s]);
+              dmma_8x8x4(b0, b1, xb, bf[s]);
             }
           }
-          if (row < rows) {
-            double* p = Y + (int64_t)row * ys + 2 * tig;
-            double v0 = g.alpha * d0, v1 = g.alpha * d1;
-            if (2 * tig + 1 < nst) {
-              if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-                if (add_old) {
-                  const double2 o = *reinterpret_cast<const double2*>(p);
-                  v0 += o.x;
-                  v1 += o.y;
-                }
-                *reinterpret_cast<double2*>(p) = make_double2(v0, v1);
-              } else {
-                p[0] = add_old ? p[0] + v0 : v0;
-                p[1] = add_old ? p[1] + v1 : v1;
-              }
-            } else if (2 * tig < nst) {
-              p[0] = add_old ? p[0] + v0 : v0;
-            }
-          }
+          if (ra < rows) store(ra, a0, a1, add_old);
+          if (rb < rows) store(rb, b0, b1, add_old);
         }
         if (kg + MAXK < ks) __syncwarp();  // this group's stores before the next group's loads
       }

@@ -170,7 +170,9 @@ __global__ void __launch_bounds__(kLnThreads, 1) k4_lane_kernel(const LnArgs g) 
 // [3] valid lanes (columns of C) | stored lanes << 8 | ksteps << 16,
 // then per k-step 4 A columns (stage double offset | stride << 16, -1 none)
 // and 4 C element offsets (row a, column lane 0 of the tile; -1 none).
-template <int MAXK>
+// TWO: two 8-row tiles in flight per task (independent DMMA chains) for
+// block rows of many rows (Q4: 65); one tile for short rows (Q2: 8).
+template <int MAXK, bool TWO>
 __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[kLnStages], empty[kLnStages];
@@ -223,9 +225,8 @@ __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) 
         }
       };
       // k-steps in groups of MAXK: lane (gid, tig) holds the B fragments
-      // C[a_{4s + tig}][gid] of the group; two 8-row tiles in flight
-      // (independent DMMA chains); groups after the first add to the values
-      // the warp itself wrote (rows with more than 4 MAXK columns)
+      // C[a_{4s + tig}][gid] of the group; groups after the first add to the
+      // values the warp itself wrote (rows with more than 4 MAXK columns)
       for (int kg = 0; kg < max(ks, 1); kg += MAXK) {
         double bf[MAXK];
         int ac[MAXK];
@@ -241,22 +242,39 @@ __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) 
           }
         }
         const bool add_old = g.accumulate || kg > 0;
-        for (int r0 = 0; r0 < rows; r0 += 16) {
-          const int ra = r0 + gid, rb = r0 + 8 + gid;
-          double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        if (TWO) {
+          for (int r0 = 0; r0 < rows; r0 += 16) {
+            const int ra = r0 + gid, rb = r0 + 8 + gid;
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
-          for (int s = 0; s < MAXK; ++s) {
-            if (kg + s < ks) {
-              const int c = ac[s];
-              const int off = c & 0xffff, cs = (c >> 16) & 0x7fff;
-              const double xa = (c >= 0 && ra < rows) ? S[off + ra * cs] : 0.0;
-              const double xb = (c >= 0 && rb < rows) ? S[off + rb * cs] : 0.0;
-              dmma_8x8x4(a0, a1, xa, bf[s]);
-              dmma_8x8x4(b0, b1, xb, bf[s]);
+            for (int s = 0; s < MAXK; ++s) {
+              if (kg + s < ks) {
+                const int c = ac[s];
+                const int off = c & 0xffff, cs = (c >> 16) & 0x7fff;
+                const double xa = (c >= 0 && ra < rows) ? S[off + ra * cs] : 0.0;
+                const double xb = (c >= 0 && rb < rows) ? S[off + rb * cs] : 0.0;
+                dmma_8x8x4(a0, a1, xa, bf[s]);
+                dmma_8x8x4(b0, b1, xb, bf[s]);
+              }
             }
+            if (ra < rows) store(ra, a0, a1, add_old);
+            if (rb < rows) store(rb, b0, b1, add_old);
           }
-          if (ra < rows) store(ra, a0, a1, add_old);
-          if (rb < rows) store(rb, b0, b1, add_old);
+        } else {
+          for (int r0 = 0; r0 < rows; r0 += 8) {
+            const int ra = r0 + gid;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int s = 0; s < MAXK; ++s) {
+              if (kg + s < ks) {
+                const int c = ac[s];
+                const double xa =
+                    (c >= 0 && ra < rows) ? S[(c & 0xffff) + ra * ((c >> 16) & 0x7fff)] : 0.0;
+                dmma_8x8x4(a0, a1, xa, bf[s]);
+              }
+            }
+            if (ra < rows) store(ra, a0, a1, add_old);
+          }
         }
         if (kg + MAXK < ks) __syncwarp();  // this group's stores before the next group's loads
       }
@@ -346,6 +364,7 @@ int align16(int x) { return (x + 15) & ~15; }
 struct bmv_lane_plan {
   int kind = 0;  // 4 or 5
   int maxk = 0;  // K5: largest k-step count of a task
+  bool two_tiles = false;  // K5: block rows average more than 16 rows
   int n_parts = 0;
   int stage_bytes = 0;
   int smem_bytes = 0;
@@ -860,6 +879,11 @@ int bmv_mmult_lane_create(const bmv_mmult_lane_desc* d, bmv_lane_plan** out) {
   auto* p = new bmv_lane_plan();
   p->kind = 5;
   p->maxk = k5_maxk;
+  {
+    int64_t sum_rows = 0;
+    for (int32_t i = 0; i < d->n_rows; ++i) sum_rows += d->row_rows[i];
+    p->two_tiles = d->n_rows > 0 && sum_rows > 16 * (int64_t)d->n_rows;
+  }
   p->stage_bytes = stage_bytes;
   p->smem_bytes = kLnStages * stage_bytes;
   int rc = sb.chunk_work.empty() ? BMV_OK : upload_stream(sb, sm_count(), p);
@@ -881,7 +905,7 @@ int bmv_mmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doubl
   cudaStream_t st = as_stream(stream);
   int rc = zero_async(c, zero_len, st);
   if (rc || p->n_parts == 0) return rc;
-  auto kern = k5_lane_kernel<kKGroup>;
+  auto kern = p->two_tiles ? k5_lane_kernel<kKGroup, true> : k5_lane_kernel<kKGroup, false>;
   BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     p->smem_bytes));
   LnArgs g{};

@@ -111,38 +111,24 @@ __global__ void __launch_bounds__(kLnThreads, 1) k4_lane_kernel(const LnArgs g) 
       const bool bm = gid < r[18];
       const double* A = S + ao + tig * as;
       const double* B = S + r[16] + gid + tig * bs;
-      double x, y;
-      if (rows <= 8) {
-        // short block rows (Q2 / proj: 8 rows): two k-steps, straight-line
-        double c0 = 0.0, c1 = 0.0;
-        const double a0 = (am && tig < rows) ? A[0] : 0.0, b0 = (bm && tig < rows) ? B[0] : 0.0;
-        const double a1 = (am && tig + 4 < rows) ? A[4 * as] : 0.0;
-        const double b1 = (bm && tig + 4 < rows) ? B[4 * bs] : 0.0;
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0, c4 = 0.0, c5 = 0.0, c6 = 0.0, c7 = 0.0;
+      int r0 = 0;
+      for (; r0 + 16 <= rows; r0 += 16) {
+        const double a0 = am ? A[r0 * as] : 0.0, b0 = bm ? B[r0 * bs] : 0.0;
+        const double a1 = am ? A[(r0 + 4) * as] : 0.0, b1 = bm ? B[(r0 + 4) * bs] : 0.0;
+        const double a2 = am ? A[(r0 + 8) * as] : 0.0, b2 = bm ? B[(r0 + 8) * bs] : 0.0;
+        const double a3 = am ? A[(r0 + 12) * as] : 0.0, b3 = bm ? B[(r0 + 12) * bs] : 0.0;
         dmma_8x8x4(c0, c1, a0, b0);
-        dmma_8x8x4(c0, c1, a1, b1);
-        x = c0;
-        y = c1;
-      } else {
-        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0, c4 = 0.0, c5 = 0.0, c6 = 0.0, c7 = 0.0;
-        int r0 = 0;
-        for (; r0 + 16 <= rows; r0 += 16) {
-          const double a0 = am ? A[r0 * as] : 0.0, b0 = bm ? B[r0 * bs] : 0.0;
-          const double a1 = am ? A[(r0 + 4) * as] : 0.0, b1 = bm ? B[(r0 + 4) * bs] : 0.0;
-          const double a2 = am ? A[(r0 + 8) * as] : 0.0, b2 = bm ? B[(r0 + 8) * bs] : 0.0;
-          const double a3 = am ? A[(r0 + 12) * as] : 0.0, b3 = bm ? B[(r0 + 12) * bs] : 0.0;
-          dmma_8x8x4(c0, c1, a0, b0);
-          dmma_8x8x4(c2, c3, a1, b1);
-          dmma_8x8x4(c4, c5, a2, b2);
-          dmma_8x8x4(c6, c7, a3, b3);
-        }
-        for (; r0 < rows; r0 += 4) {
-          const bool ok = r0 + tig < rows;
-          const double a0 = (am && ok) ? A[r0 * as] : 0.0, b0 = (bm && ok) ? B[r0 * bs] : 0.0;
-          dmma_8x8x4(c0, c1, a0, b0);
-        }
-        x = (c0 + c2) + (c4 + c6);
-        y = (c1 + c3) + (c5 + c7);
+        dmma_8x8x4(c2, c3, a1, b1);
+        dmma_8x8x4(c4, c5, a2, b2);
+        dmma_8x8x4(c6, c7, a3, b3);
       }
+      for (; r0 < rows; r0 += 4) {
+        const bool ok = r0 + tig < rows;
+        const double a0 = (am && ok) ? A[r0 * as] : 0.0, b0 = (bm && ok) ? B[r0 * bs] : 0.0;
+        dmma_8x8x4(c0, c1, a0, b0);
+      }
+      const double x = (c0 + c2) + (c4 + c6), y = (c1 + c3) + (c5 + c7);
       const int ro = r[8 + gid];
       if (am && ro >= 0) {
         if (2 * tig < r[18]) atomicAdd(acc + ro + 2 * tig, x);

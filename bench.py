@@ -460,7 +460,7 @@ def main():
             "kernels_ms": {"k1_cellop": round(ms_k1, 4), "apply_total": round(ms_apply, 4),
                            "tmmult": round(ms_tm, 4), "mmult": round(ms_mm, 4)},
             "work": {k: (int(sum_over_ranks(v)) if isinstance(v, int) else v) for k, v in cnt.items()},
-            "roofline": {"bound": "fp64", "kernel": "K1 cellop (bmv_cellop.cu)",
+            "roofline": {"bound": "fp64", "kernel": "K1 cellop (bmv_cellop_tma.cu, cellop_tma_kernel<5>)",
                          "achieved": round(k1_tflops, 3), "peak": round(peak_fp64, 3),
                          "unit": "TFLOP/s", "frac": round(k1_tflops / peak_fp64, 4),
                          "peak_source": "measured in-run: bmv_fp64_peak_kernel (independent DFMA "

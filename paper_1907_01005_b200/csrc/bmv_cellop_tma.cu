@@ -78,19 +78,19 @@ struct MassScatter {
   }
 };
 
-template <int N, bool COEF, bool WIDE, bool GC, bool DUAL = false, int WPC = kTmaWarps>
-__global__ void __launch_bounds__(WPC * 32, TmaShape<N>::MINB * kTmaWarps / WPC)
+template <int N, bool COEF, bool DUAL = false>
+__global__ void __launch_bounds__(kTmaWarps * 32, TmaShape<N>::MINB)
     cellop_tma_kernel(const TmaArgs a, const __grid_constant__ CellTables tb) {
-  using TS = TmaShape<N, WIDE, GC>;
-  constexpr int P = TS::P, N2 = N * N, TILE = TS::L::TILE;
+  using TS = TmaShape<N>;
+  constexpr int P = TS::P, N2 = N * N, TILE = Tile<N>::TILE;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[WPC];
+  __shared__ __align__(8) uint64_t bar[kTmaWarps];
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
   const int sub = lid / N;
   const int t = lid - sub * N;
   const bool lane_ok = sub < P;
   const int tt = lane_ok ? t : 0;
-  const int64_t pair = ((int64_t)blockIdx.x * WPC + warp) * P + sub;
+  const int64_t pair = ((int64_t)blockIdx.x * kTmaWarps + warp) * P + sub;
   const bool ok = lane_ok && pair < a.n_pairs;
 
   // per warp: [pair tiles | coefficient rows | HX offset rows]; the X offset
@@ -108,18 +108,14 @@ __global__ void __launch_bounds__(WPC * 32, TmaShape<N>::MINB * kTmaWarps / WPC)
   if (ok) d = __ldg(a.desc + pair);
   const int lane = d.z & 0xffff, stride = d.z >> 16;
   const bool issuer = ok && t == 0;
-  const unsigned cbytes = (COEF && !GC) ? TS::Q3P * 8u : 0u;
+  const unsigned cbytes = COEF ? TS::Q3P * 8u : 0u;
   const double* gcf = a.coef + (a.coef_cell ? (int64_t)d.y * TS::Q3P : 0);
-  if (GC && COEF && ok) {  // the cell's coefficient row into L1 (used mid-computation)
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(gcf + 32 * t));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(gcf + 32 * t + 16));
-  }
   const unsigned my_bytes = issuer ? cbytes + 2u * TS::SRP * 4u : 0u;
   const unsigned total = __reduce_add_sync(~0u, my_bytes);
   if (lid == 0) mbar_expect_tx(&bar[warp], total);  // the warp's single arrival
   __syncwarp();
   if (issuer) {
-    if (COEF && !GC) bulk_g2s(cs, gcf, cbytes, &bar[warp]);
+    if (COEF) bulk_g2s(cs, gcf, cbytes, &bar[warp]);
     bulk_g2s(const_cast<int32_t*>(xs), a.xoff + (int64_t)d.x * TS::SRP, TS::SRP * 4u, &bar[warp]);
     bulk_g2s(const_cast<int32_t*>(hs), a.hoff + (int64_t)d.x * TS::SRP, TS::SRP * 4u, &bar[warp]);
   }
@@ -142,15 +138,12 @@ __global__ void __launch_bounds__(WPC * 32, TmaShape<N>::MINB * kTmaWarps / WPC)
   double out[N][N];
   if (DUAL) {  // H x to hx and M x to mx from one gather and one interpolation
     const PlaneScatter hsc{a.hx, hs, t, lane, ok};
-    sumfac_h_plane<N, COEF, 1, typename TS::L, const double*, MassScatter, PlaneScatter>(
+    sumfac_h_plane<N, COEF, 1, Tile<N>, const double*, MassScatter, PlaneScatter>(
         u, out, buf, tt, lane_ok, cs + tt * N2, tb,
         MassScatter{PlaneScatter{a.mx, hs, t, lane, ok}, a.mcoef}, hsc);
     return;
   }
-  if (GC)
-    sumfac_h_plane<N, COEF, 1, typename TS::L, GCoef>(u, out, buf, tt, lane_ok, GCoef{gcf + tt * N2}, tb);
-  else
-    sumfac_h_plane<N, COEF, 1, typename TS::L>(u, out, buf, tt, lane_ok, cs + tt * N2, tb);
+  sumfac_h_plane<N, COEF, 1>(u, out, buf, tt, lane_ok, cs + tt * N2, tb);
   if (ok) {
 #pragma unroll
     for (int y = 0; y < N; ++y)
@@ -255,8 +248,8 @@ template <int N, bool COEF>
 int launch_dual(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,
                 const double* mcoef, const double* x, double* hx, double* mx, int64_t zero_len,
                 cudaStream_t st) {
-  using TS = TmaShape<N, false, false>;
-  auto kern = cellop_tma_kernel<N, COEF, false, false, true>;
+  using TS = TmaShape<N>;
+  auto kern = cellop_tma_kernel<N, COEF, true>;
   const int smem = kTmaWarps * TS::warp_bytes;
   BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   TmaArgs args{tp->desc, tp->xoff, tp->hoff, coef, coef_cell, tp->n_pairs, x, hx, mx, mcoef};
@@ -270,10 +263,10 @@ int launch_dual(const TmaPlan* tp, const CellTables& tb, const double* coef, int
   return BMV_OK;
 }
 
-template <int N, bool COEF, bool WIDE, bool GC = false, int WPC = kTmaWarps>
+template <int N, bool COEF>
 int launch_tma(const TmaPlan* tp, const CellTables& tb, const double* coef, int coef_cell,
                const double* x, double* hx, int64_t zero_len, cudaStream_t st) {
-  using TS = TmaShape<N, WIDE, GC>;
+  using TS = TmaShape<N>;
   if (N <= 3 && tp->per_pair) {
     auto pk = cellop_pair_kernel<N < 4 ? N : 3, COEF>;
     const int psmem = kTmaWarps * PairShape<N < 4 ? N : 3>::warp_bytes;
@@ -286,15 +279,15 @@ int launch_tma(const TmaPlan* tp, const CellTables& tb, const double* coef, int 
     BMV_CHECK_LAUNCH();
     return BMV_OK;
   }
-  auto kern = cellop_tma_kernel<N, COEF, WIDE, GC, false, WPC>;
-  const int smem = WPC * TS::warp_bytes;
+  auto kern = cellop_tma_kernel<N, COEF>;
+  const int smem = kTmaWarps * TS::warp_bytes;
   BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   TmaArgs args{tp->desc, tp->xoff, tp->hoff, coef, coef_cell, tp->n_pairs, x, hx};
   const int rc = zero_async(hx, zero_len, st);
   if (rc) return rc;
-  const int64_t per_cta = (int64_t)WPC * TS::P;
+  const int64_t per_cta = (int64_t)kTmaWarps * TS::P;
   const int64_t grid = (tp->n_pairs + per_cta - 1) / per_cta;
-  kern<<<(unsigned)grid, WPC * 32, smem, st>>>(args, tb);
+  kern<<<(unsigned)grid, kTmaWarps * 32, smem, st>>>(args, tb);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
@@ -332,12 +325,6 @@ int build_n(const bmv_cellop_desc* d, TmaPlan* tp) {
   tp->q3p = TS::Q3P;
   const char* pe = std::getenv("BMV_K1_PAIR");
   tp->per_pair = N <= 3 && !(pe && pe[0] == '0');
-  const char* wpe = std::getenv("BMV_K1_WPC");
-  tp->wpc = wpe ? std::atoi(wpe) : kTmaWarps;
-  const char* ge = std::getenv("BMV_K1_COEF");
-  tp->gcoef = N == 5 && ge && std::string(ge) == "global";
-  const char* we = std::getenv("BMV_K1_TILE5");
-  tp->wide = N == 5 && we && std::string(we) == "wide";
   int rc = upload(desc.data(), (int64_t)desc.size(), &tp->desc);
   if (rc == BMV_OK) rc = upload(xo.data(), (int64_t)xo.size(), &tp->xoff);
   if (rc == BMV_OK) rc = upload(ho.data(), (int64_t)ho.size(), &tp->hoff);
@@ -401,22 +388,14 @@ int tma_apply(const TmaPlan* tp, const CellTables& tb, const double* coef, int c
               const double* x, double* hx, int64_t zero_len, cudaStream_t st) {
   const bool c = coef != nullptr;
   switch (tp->n) {
-    case 2: return c ? launch_tma<2, true, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
-                     : launch_tma<2, false, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
-    case 3: return c ? launch_tma<3, true, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
-                     : launch_tma<3, false, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
-    case 4: return c ? launch_tma<4, true, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
-                     : launch_tma<4, false, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
-    case 5:
-      if (tp->gcoef && c)
-        return launch_tma<5, true, false, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
-      if (tp->wide)
-        return c ? launch_tma<5, true, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
-                 : launch_tma<5, false, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
-      if (c && tp->wpc == 1) return launch_tma<5, true, false, false, 1>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
-      if (c && tp->wpc == 2) return launch_tma<5, true, false, false, 2>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
-      return c ? launch_tma<5, true, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
-               : launch_tma<5, false, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+    case 2: return c ? launch_tma<2, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
+                     : launch_tma<2, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+    case 3: return c ? launch_tma<3, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
+                     : launch_tma<3, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+    case 4: return c ? launch_tma<4, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
+                     : launch_tma<4, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
+    case 5: return c ? launch_tma<5, true>(tp, tb, coef, coef_cell, x, hx, zero_len, st)
+                     : launch_tma<5, false>(tp, tb, coef, coef_cell, x, hx, zero_len, st);
     default:
       set_error("TMA plan with unsupported n %d", tp->n);
       return BMV_ERR_INVALID;

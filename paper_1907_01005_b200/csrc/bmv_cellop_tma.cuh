@@ -15,22 +15,19 @@ namespace bmv {
 // coefficients (>= Q3P = q^3 rounded to even) and SS slots (>= SRP = n^3
 // rounded to 4), padded off the bank period (bank model in DESIGN.md 4);
 // MINB CTAs of 4 warps per SM.
-template <int N, bool WIDE = false, bool GC = false>
+template <int N>
 struct TmaShape {
-  // GC: coefficients read from global (L1) instead of staged per pair
-  // WIDE (n = 5 only): conflict-free transpose tiles, coefficient rows unpadded
-  using L = typename std::conditional<WIDE && N == 5, Tile5Wide, Tile<N>>::type;
   static constexpr int P = 32 / N;
   static constexpr int N3 = N * N * N;
   static constexpr int Q3P = (N3 + 1) / 2 * 2;
   static constexpr int SRP = (N3 + 3) / 4 * 4;
-  static constexpr int CS = N == 5 ? (WIDE ? 126 : 134) : (N == 4 ? 66 : (N == 3 ? 28 : 10));
+  static constexpr int CS = N == 5 ? 134 : (N == 4 ? 66 : (N == 3 ? 28 : 10));
   static constexpr int SS = N == 5 ? 132 : (N == 4 ? 68 : SRP);
   static constexpr int MINB = N == 5 ? 3 : (N == 4 ? 4 : (N == 3 ? 5 : 8));
-  static constexpr int tile_bytes0 = (P * L::TILE * 8 + 15) / 16 * 16;
+  static constexpr int tile_bytes0 = (P * Tile<N>::TILE * 8 + 15) / 16 * 16;
   // the X offset rows overlay the tiles
   static constexpr int tile_bytes = tile_bytes0 > P * SS * 4 ? tile_bytes0 : P * SS * 4;
-  static constexpr int coef_bytes = GC ? 0 : P * CS * 8;
+  static constexpr int coef_bytes = P * CS * 8;
   static constexpr int hoff_bytes = P * SS * 4;
   static constexpr int warp_bytes = tile_bytes + coef_bytes + hoff_bytes;
 };
@@ -39,10 +36,7 @@ struct TmaPlan {
   int n = 0;
   int64_t n_pairs = 0;
   int q3p = 0;
-  bool wide = false;      // n = 5 wide transpose tiles (BMV_K1_TILE5=wide)
   bool per_pair = false;  // n <= 3: thread-per-pair kernel (BMV_K1_PAIR=0 disables)
-  bool gcoef = false;     // n = 5: coefficients from global / L1 (BMV_K1_COEF=global)
-  int wpc = 4;            // n = 5: warps per CTA (BMV_K1_WPC = 1, 2 or 4)
   int4* desc = nullptr;
   int32_t* xoff = nullptr;
   int32_t* hoff = nullptr;

@@ -61,16 +61,12 @@ __device__ __forceinline__ void contract_slow(const double (&in)[N][N], double (
 // bank pairs per 128 B wavefront) for the pair-major lane mapping: N = 3, 4
 // conflict-free stores and loads (2 + 2 wavefronts), N = 5 2 + 3.
 template <int N> struct Tile;
-// n = 5 conflict-free (2 + 2 wavefronts) layout, 45 % more shared memory
-struct Tile5Wide { static constexpr int BY = 7, BZ = 39, TILE = 195; };
 template <> struct Tile<2> { static constexpr int BY = 2, BZ = 4, TILE = 9; };
 template <> struct Tile<3> { static constexpr int BY = 5, BZ = 21, TILE = 63; };
 template <> struct Tile<4> { static constexpr int BY = 4, BZ = 20, TILE = 77; };
-#if defined(BMV_K1_TILE5_WIDE)
-template <> struct Tile<5> { static constexpr int BY = 7, BZ = 39, TILE = 195; };  // 2 + 2 wavefronts
-#else
+// n = 5: a 2 + 2 layout (BY 7, BZ 39, TILE 195) exists but its 45 % larger
+// footprint pushes the TMA K1 past the 196 KB shared-memory carve-out
 template <> struct Tile<5> { static constexpr int BY = 5, BZ = 27, TILE = 135; };  // 2 + 3 wavefronts
-#endif
 
 // A (z = t, [y][x]) -> B (y = t, [z][x]) through the pair tile.
 template <int N, class L = Tile<N>>
@@ -131,13 +127,7 @@ __device__ __forceinline__ void cp_async_wait_one() {
 // (3 + 3 transposed), 3 transposed interpolations = 12 contractions of n^4
 // FMAs, 4 transposes through the pair tile `buf`.  The coefficient of
 // quadrature point (qz = t, qy = i, qx = j) is read at cf[(i * N + j) * CS].
-// Coefficient access: shared memory (plain pointer) or global through the
-// read-only path (GCoef).
-struct GCoef {
-  const double* p;
-};
 __device__ __forceinline__ double coef_at(const double* cf, int k) { return cf[k]; }
-__device__ __forceinline__ double coef_at(GCoef cf, int k) { return __ldg(cf.p + k); }
 
 struct NoMass {
   template <int N, class L>

@@ -13,7 +13,13 @@ computes:
   libbmv gather/scatter kernels and move buffers with the rank context
   (NCCL point-to-point between GPUs); compress adds in ascending source
   rank order, like the reference.
-* `tmmult` / `mmult` (`bcsr.py:587-667`) run the K4 / K5 kernels.
+* `tmmult` / `mmult` (`bcsr.py:587-667`) run the K4 / K5 kernels: by default
+  the lane-compacted ones (csrc/bmv_spmm_lane.cu: FP64 tensor cores on the
+  active columns of A), with BMV_DETERMINISTIC=1 the fixed-order ones
+  (bmv_project.cu, bmv_postmul.cu).
+* the OM glue (`scale_add`, `copy_pattern_subset`, `add_scaled_identity`,
+  `tr_tmmult`, `tr_mult`; `bcsr.py:526-577,670-725`) runs as element-wise
+  device ops on cached index maps.
 
 Matrices may also live on the CPU (`device="cpu"`): layout and exchange
 logic then run with torch index ops so the multi-rank protocol can be

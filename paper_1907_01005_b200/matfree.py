@@ -3,8 +3,10 @@
 Drop-in for the reference `bcsrmv/matfree.py` (same names and semantics).
 `CellOperator.apply` keeps the reference's contract (`matfree.py:458-527`):
 checks -> dst zeroed -> src ghosts updated -> cell loop -> src ghosts
-released -> dst compressed.  The cell loop itself is one launch of the K1
-kernel (csrc/bmv_cellop.cu) over a precomputed plan:
+released -> dst compressed.  The cell loop itself is one launch of a K1
+kernel over a precomputed plan (the Hamiltonian: csrc/bmv_cellop_tma.cu,
+per-pair operands staged by TMA, thread per pair for n <= 3; the mass
+operator and the deterministic colour mode: csrc/bmv_cellop.cu):
 
 * per cell: the (group, row-in-block) slot of each of its (p+1)^3 DoFs,
   groups being the distinct local block rows in first-occurrence order
@@ -21,6 +23,10 @@ kernel (csrc/bmv_cellop.cu) over a precomputed plan:
 The potential is sampled once per (operator, potential) at the cell
 quadrature points (`matfree.py:35-40,491-495`): Gaussian-sum potentials on
 the device, arbitrary callables on the host in cell chunks.
+
+`CellOperator.apply_h_and_mass` computes H X and M X with one gather and
+one interpolation (the two products compute_energy forms,
+`energy.py:144-145`).
 """
 
 from __future__ import annotations

@@ -305,6 +305,30 @@ struct StreamBuild {
   std::vector<int64_t> chunk_entry{0};
   std::vector<int64_t> chunk_work;
   std::vector<int64_t> fixed_parts;  // chunk index where each part starts (K4: items never span parts)
+  // deferred chunks (interleaved assignment): chunk c goes to CTA c % n_parts
+  bool defer = false;
+  std::vector<std::pair<Chunk, int64_t>> pending;
+  void put(const Chunk& c, int64_t work) {
+    if (defer)
+      pending.push_back({c, work});
+    else
+      add(c, work);
+  }
+  // short block rows: consecutive chunks to different CTAs, so every CTA
+  // samples every region of the rows (static contiguous parts left a 31 %
+  // spread of SM active time at the proj config)
+  void finish_interleaved(int n_parts) {
+    if (!defer) return;
+    const int64_t nc = (int64_t)pending.size();
+    const int64_t np = std::max<int64_t>(1, std::min<int64_t>(n_parts, nc));
+    fixed_parts.clear();
+    for (int64_t b = 0; b < np; ++b) {
+      fixed_parts.push_back((int64_t)chunk_work.size());
+      for (int64_t c = b; c < nc; c += np) add(pending[(size_t)c].first, pending[(size_t)c].second);
+    }
+    pending.clear();
+    defer = false;
+  }
   void add(const Chunk& c, int64_t work) {
     const int64_t moff = (int64_t)meta.size() * 4;  // bytes
     std::vector<int32_t> m = c.meta;
@@ -358,6 +382,15 @@ struct StreamBuild {
 };
 
 int align16(int x) { return (x + 15) & ~15; }
+
+// BMV_LANE_INTERLEAVE=0/1 forces the chunk assignment (tests); default: the
+// planner's choice
+bool interleave_override(bool choice) {
+  const char* e = std::getenv("BMV_LANE_INTERLEAVE");
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return true;
+  return choice;
+}
 
 }  // namespace
 
@@ -466,7 +499,7 @@ int plan_k4(const bmv_tmmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out
     cur.copies.clear();
     if (a_hi > a_lo) cur.copies.push_back({a_off_b, (a_hi - a_lo) * 8, 1, a_lo * 8});
     if (b_hi > b_lo) cur.copies.push_back({b_off_b, (b_hi - b_lo) * 8, 2, b_lo * 8});
-    sb.add(cur, cur_work + 64);
+    sb.put(cur, cur_work + 64);
     recs.clear();
     cur_bytes = 0;
     cur_rows = 0;
@@ -491,10 +524,24 @@ int plan_k4(const bmv_tmmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out
     row_work[(size_t)i + 1] = row_work[(size_t)i] + ((ncols + 7) / 8) * ntl * (d->row_rows[i] + 48) + 16;
   }
   const int n_parts = std::max(1, sm_count_host);
+  int64_t sum_rows = 0;
+  for (int32_t i = 0; i < d->n_rows; ++i) sum_rows += d->row_rows[i];
+  // short block rows: every chunk is its own item and chunks are interleaved
+  // over the CTAs (finish_interleaved); long rows: contiguous row parts
+  // (and enough chunks per CTA for the interleave to average out: >= 16)
+  int64_t data_bytes = 0;
+  if (d->n_rows > 0) {
+    const int64_t pa_end = d->a_row_start[d->n_rows], pb_end = d->b_row_start[d->n_rows];
+    if (pa_end > 0) data_bytes += 8 * (d->a_off[pa_end - 1] - d->a_off[0]);
+    if (pb_end > 0) data_bytes += 8 * (d->b_off[pb_end - 1] - d->b_off[0]);
+  }
+  const bool interleave = interleave_override(d->n_rows > 0 && sum_rows < 16 * (int64_t)d->n_rows &&
+                                              data_bytes >= 16LL * n_parts * stage_bytes);
+  sb.defer = interleave;
   int next_part = 1;
   sb.fixed_parts.push_back(0);
   for (int32_t i = 0; i < d->n_rows; ++i) {
-    if (next_part < n_parts &&
+    if (!interleave && next_part < n_parts &&
         row_work[(size_t)i] >= row_work.back() * next_part / n_parts) {
       emit(true);
       sb.fixed_parts.push_back((int64_t)sb.chunk_work.size());
@@ -591,7 +638,7 @@ int plan_k4(const bmv_tmmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out
         const int need = align16((int)((a_last - a_lo) * 8)) +
                          align16((int)((b_first + b_len - b_lo) * 8)) +
                          chunk_meta_bytes(recs.size() / kK4Rec + grp_tiles, kAccTiles) + 64;
-        if (same_row || need > stage_bytes || a_last - a_lo >= 0x8000) emit(false);
+        if (same_row || need > stage_bytes || a_last - a_lo >= 0x8000) emit(interleave);
       }
       if (recs.empty()) {
         a_lo = a_first;
@@ -649,6 +696,7 @@ int plan_k4(const bmv_tmmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out
     pair_base += na * nb;
   }
   emit(true);
+  sb.finish_interleaved(n_parts);
   return BMV_OK;
 }
 
@@ -710,8 +758,20 @@ int bmv_tmmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doub
 
 namespace {
 
-int plan_k5(const bmv_mmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out, int& maxk) {
+int plan_k5(const bmv_mmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out, int& maxk,
+            int n_parts) {
   maxk = 0;
+  {
+    // short rows and >= 16 chunks per CTA: interleave the chunks over the CTAs
+    int64_t sum_rows = 0;
+    for (int32_t i = 0; i < d->n_rows; ++i) sum_rows += d->row_rows[i];
+    int64_t data_bytes = 0;
+    if (d->n_rows > 0 && d->a_row_start[d->n_rows] > 0)
+      data_bytes = 8 * (d->a_off[d->a_row_start[d->n_rows] - 1] - d->a_off[0]);
+    sb.defer = interleave_override(
+        d->n_rows > 0 && sum_rows < 16 * (int64_t)d->n_rows &&
+        data_bytes >= 16LL * std::max(1, n_parts) * ((kSmemBudget / kLnStages) & ~127));
+  }
   const int stage_bytes = (kSmemBudget / kLnStages) & ~127;
   stage_bytes_out = stage_bytes;
   Chunk cur;
@@ -745,7 +805,7 @@ int plan_k5(const bmv_mmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out,
     }
     cur.copies.clear();
     if (a_hi > a_lo) cur.copies.push_back({a_off_b, (a_hi - a_lo) * 8, 1, a_lo * 8});
-    sb.add(cur, work + 64);
+    sb.put(cur, work + 64);
     tasks.clear();
     toffs.clear();
     a_lo = a_hi = 0;
@@ -854,6 +914,7 @@ int plan_k5(const bmv_mmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out,
     work += (int64_t)ro.size() * rows * (ks + 1);
   }
   emit();
+  sb.finish_interleaved(std::max(1, n_parts));
   return BMV_OK;
 }
 
@@ -872,7 +933,7 @@ int bmv_mmult_lane_create(const bmv_mmult_lane_desc* d, bmv_lane_plan** out) {
   int k5_maxk = 0;
   {
     int maxk = 0;
-    const int rc0 = plan_k5(d, sb, stage_bytes, maxk);
+    const int rc0 = plan_k5(d, sb, stage_bytes, maxk, sm_count());
     k5_maxk = maxk;
     if (rc0 != BMV_OK) return rc0;
   }
@@ -934,7 +995,7 @@ int bmv_lane_plan_host(int32_t kind, const void* desc, int32_t n_parts, bmv_lane
   StreamBuild sb;
   int stage_bytes = 0, host_maxk = 0;
   const int rc = kind == 4 ? plan_k4(static_cast<const bmv_tmmult_lane_desc*>(desc), sb, stage_bytes, n_parts)
-                           : plan_k5(static_cast<const bmv_mmult_lane_desc*>(desc), sb, stage_bytes, host_maxk);
+                           : plan_k5(static_cast<const bmv_mmult_lane_desc*>(desc), sb, stage_bytes, host_maxk, n_parts);
   if (rc != BMV_OK) return rc;
   std::vector<int64_t> ss, es;
   if (!sb.chunk_work.empty()) sb.parts(n_parts, ss, es);

@@ -66,10 +66,21 @@ def test_mmult_plan_emulation(block_size, lane_width, n_parts, accumulate):
 #    kernels emulated on CPU over the host stage stream ----------------------
 
 
+@pytest.fixture(params=["auto", "1"])
+def interleave(request, monkeypatch):
+    """Lane plans: the planner's chunk assignment, or chunks interleaved over
+    the CTAs with one accumulator item per chunk (short block rows)."""
+    if request.param == "auto":
+        monkeypatch.delenv("BMV_LANE_INTERLEAVE", raising=False)
+    else:
+        monkeypatch.setenv("BMV_LANE_INTERLEAVE", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("block_size,lane_width", [(3, 8), (8, 8), (12, 8), (3, 4), (5, 2)])
 @pytest.mark.parametrize("attach", [False, True])
 @pytest.mark.parametrize("n_parts", [1, 7])
-def test_tmmult_lane_plan_emulation(block_size, lane_width, attach, n_parts):
+def test_tmmult_lane_plan_emulation(block_size, lane_width, attach, n_parts, interleave):
     from _plan_emul import emulate_tmmult_lane
 
     s = Small((4, 4, 4), (1.0, 1.0, 1.0), 1, 2, CENTERS, 1.6, block_size, 3)
@@ -91,7 +102,7 @@ def test_tmmult_lane_plan_emulation(block_size, lane_width, attach, n_parts):
 @pytest.mark.parametrize("block_size,lane_width", [(3, 8), (8, 8), (12, 8), (3, 4), (5, 2)])
 @pytest.mark.parametrize("attach", [False, True])
 @pytest.mark.parametrize("accumulate", [False, True])
-def test_mmult_lane_plan_emulation(block_size, lane_width, attach, accumulate):
+def test_mmult_lane_plan_emulation(block_size, lane_width, attach, accumulate, interleave):
     import torch
 
     from _plan_emul import emulate_mmult_lane

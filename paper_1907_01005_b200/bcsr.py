@@ -1000,8 +1000,12 @@ def _lane_plan_or_none(build, a, b, c):
         return None
     try:
         return build(a, b, c)
-    except ShapeError:
+    except ShapeError as exc:
         cache[key] = True
+        import warnings
+
+        warnings.warn(f"{build.__name__}: {exc}; using the fixed-order kernel", RuntimeWarning,
+                      stacklevel=3)
         return None
 
 

@@ -57,3 +57,34 @@ def test_large_config_hx_matches_c_oracle(cuda, name):
     ok = ref > 0
     err = float(np.sqrt(np.max(diff[ok] / ref[ok])))
     assert err <= 1e-12, err
+
+
+@pytest.mark.parametrize("name", ["proj", "weak1"])
+def test_large_config_lane_kernels_match_fixed_order(cuda, name, monkeypatch):
+    """The lane-compacted K4 / K5 (default) against the fixed-order kernels on the
+    same full-size operands (proj, weak G = 1): S entries <= 1e-11 relative to
+    max(|S_ab|, ||x_a|| ||(HX)_b||), X C <= 1e-12 per vector."""
+    from paper_1907_01005_b200.bcsr import mmult, tmmult
+
+    prob = P.build_problem(name)
+    st = P.make_rank_setup(serial_context(cuda), prob, projection=True, device=cuda)
+    st.op.apply(prob.spec_h(), st.x, st.hx)
+    st.c.update_ghost_values()
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("BMV_DETERMINISTIC", mode)
+        tmmult(st.x, st.hx, st.s)
+        mmult(st.x, st.c, st.xc)
+        torch.cuda.synchronize()
+        out[mode] = (st.s.to_dense_owned(), st.xc.data.clone())
+    s_lane, s_det = out["0"][0], out["1"][0]
+    xn = np.sqrt(column_sq_norms(st.x, st.x.data.cpu().numpy()))
+    hn = np.sqrt(column_sq_norms(st.hx, st.hx.data.cpu().numpy()))
+    scale = np.maximum(np.abs(s_det), np.outer(xn, hn))
+    scale = np.where(scale > 0, scale, 1.0)
+    assert float(np.max(np.abs(s_lane - s_det) / scale)) <= 1e-11
+    xc_lane, xc_det = out["0"][1], out["1"][1]
+    diff = column_sq_norms(st.xc, (xc_lane - xc_det).cpu().numpy())
+    ref = column_sq_norms(st.xc, xc_det.cpu().numpy())
+    ok = ref > 0
+    assert float(np.sqrt(np.max(diff[ok] / ref[ok]))) <= 1e-12

@@ -1,0 +1,73 @@
+/* bmv_plan.h — native host plan builder (libbmvplan.so, C++/OpenMP, no CUDA).
+ *
+ * Setup-time index maps of the hot path that the reference builds in Python
+ * ("C++ plan construction, bit-exact").  Host pointers,
+ * int64 indices, return 0 on success, 1 on invalid arguments, 3 when an entry
+ * falls outside the matrix pattern (the Python shim raises ConsistencyError).
+ *
+ * Reference interfaces each entry point replaces:
+ *   bmvp_hash_fill            bench/problem.py:113-131 fill_multivector (splitmix64
+ *                             `_mix64` hash of (seed, row, original column)); here the
+ *                             per-entry form used by problem.fill_multivector
+ *   bmvp_owned_entries_*      bcsr.py:233-318 block storage offsets of the support
+ *                             entries of a multivector (ColumnSupport.owned_entries)
+ *   bmvp_blocks_of            bcsr.py:126-152 map_rows (row -> (block, row in block))
+ *   bmvp_first_groups_*       matfree.py:90-116 build_cell_dof_map: per-cell grouping of
+ *                             DoFs by row block in first-occurrence order
+ */
+#ifndef BMV_PLAN_H
+#define BMV_PLAN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+int bmvp_version(void);
+
+/* out[flat ? flat[i] : i] = scale * (mix64(rows[i]*K1 + c*K2 + seed) / 2^64 - 0.5),
+ * c = col_map ? col_map[cols[i]] : cols[i]. */
+int bmvp_hash_fill(uint64_t seed, int64_t n, const int64_t* rows, const int64_t* cols,
+                   const int64_t* col_map, const int64_t* flat, double scale, double* out);
+
+/* block[i] = b with starts[b] <= idx[i] < starts[b+1]; offset[i] = idx[i] - starts[b]
+ * (offset may be NULL).  Returns 1 if an index lies outside [starts[0], starts[n_blocks]).
+ * Replaces the searchsorted of bcsr.py:126-152 map_rows (owned rows). */
+int bmvp_blocks_of(int64_t n_blocks, const int64_t* starts, int64_t n, const int64_t* idx,
+                   int64_t* block, int64_t* offset);
+
+/* col_count[c] = #{support rows of column c in [lo, hi)}; columns are CSR
+ * (col_ptr[n_cols+1], col_rows sorted per column). */
+int bmvp_owned_entries_count(int64_t n_cols, const int64_t* col_ptr, const int64_t* col_rows,
+                             int64_t lo, int64_t hi, int64_t* col_count);
+
+/* Column-major (column, then row) support entries of the owned rows: storage
+ * offset, global row, column.  out_start[c] = exclusive prefix sum of col_count.
+ * block_starts: global first row of the nb_own owned block rows (+ end);
+ * cb_starts: first column of each of n_cb column blocks (+ end); row_start /
+ * col_index / block_offsets: the matrix's block CSR (col_index ascending per row). */
+int bmvp_owned_entries_fill(int64_t n_cols, const int64_t* col_ptr, const int64_t* col_rows,
+                            int64_t lo, int64_t hi, const int64_t* out_start,
+                            int64_t nb_own, const int64_t* block_starts,
+                            int64_t n_cb, const int64_t* cb_starts,
+                            const int64_t* row_start, const int64_t* col_index,
+                            const int64_t* block_offsets, const int64_t* col_strides,
+                            int64_t* flat, int64_t* rows, int64_t* cols);
+
+/* lb: (n_cells, n3) local block of every cell DoF.  slot_group (n_cells, n3):
+ * group index of each DoF inside its cell, groups in first-occurrence order;
+ * cell_count[c] = groups of cell c (n3 <= 4096). */
+int bmvp_first_groups_count(int64_t n_cells, int32_t n3, const int64_t* lb,
+                            int64_t* slot_group, int64_t* cell_count);
+
+/* cell_gstart = exclusive prefix sum of cell_count; fills grp_cell / grp_block. */
+int bmvp_first_groups_fill(int64_t n_cells, int32_t n3, const int64_t* lb,
+                           const int64_t* slot_group, const int64_t* cell_gstart,
+                           int64_t* grp_cell, int64_t* grp_block);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BMV_PLAN_H */

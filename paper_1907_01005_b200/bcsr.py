@@ -36,7 +36,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, _plan
 from .blocks import BlockIndices, BlockSparsityPattern
 from .counters import OpCounters
 from .errors import (
@@ -156,6 +156,9 @@ class RankLayout:
         rib = np.empty(rows.shape, dtype=np.int64)
         lo, hi = self.owned_rows
         own = (rows >= lo) & (rows < hi)
+        if own.all() and rows.size > 100_000 and _plan.enabled():
+            g, rib = _plan.blocks_of(self.blocks.starts, rows)  # native, OpenMP
+            return g - self.first_block, rib
         if own.any():
             g = self.blocks.blocks_of(rows[own])
             lb[own] = g - self.first_block

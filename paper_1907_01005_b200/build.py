@@ -1,4 +1,5 @@
-"""Build libbmv.so (sm_100a) in-tree with nvcc.
+"""Build libbmv.so (sm_100a) in-tree with nvcc, and the host plan builder
+libbmvplan.so (g++ -fopenmp, no CUDA).
 
 `python -m paper_1907_01005_b200.build` or `__graft_entry__.build()`.
 The shared library lands next to this file so it travels with the repo
@@ -16,6 +17,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libbmv.so"
+PLAN_LIB = PKG / "libbmvplan.so"
+PLAN_SOURCES = ["bmv_plan.cpp"]
 SOURCES = ["bmv_util.cu", "bmv_cellop.cu", "bmv_cellop_stream.cu", "bmv_cellop_tma.cu", "bmv_project.cu", "bmv_postmul.cu", "bmv_spmm_lane.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -34,7 +37,31 @@ def needs_rebuild() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 
+def _cxx() -> str:
+    # /usr/bin/g++ ships libgomp; a wrapper earlier on PATH may not
+    return "/usr/bin/g++" if Path("/usr/bin/g++").exists() else "g++"
+
+
+def build_plan(force: bool = False) -> Path:
+    """g++ -O3 -fopenmp -> libbmvplan.so (include/bmv_plan.h).  -ffp-contract=off keeps
+    the hashed fill bit-identical to numpy."""
+    deps = [CSRC / s for s in PLAN_SOURCES] + [ROOT / "include" / "bmv_plan.h"]
+    if not force and PLAN_LIB.exists() and all(p.stat().st_mtime <= PLAN_LIB.stat().st_mtime
+                                               for p in deps):
+        return PLAN_LIB
+    cmd = [_cxx(), "-O3", "-std=c++17", "-fopenmp", "-ffp-contract=off",
+           "-shared", "-fPIC", "-I", str(ROOT / "include"),
+           *[str(CSRC / s) for s in PLAN_SOURCES], "-o", str(PLAN_LIB) + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("g++ failed building libbmvplan.so")
+    os.replace(str(PLAN_LIB) + ".tmp", PLAN_LIB)
+    return PLAN_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    build_plan(force)
     if not force and not needs_rebuild():
         return LIB
     cmd = [

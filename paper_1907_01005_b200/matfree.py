@@ -133,6 +133,16 @@ class CellDoFMap:
 
 
 def _first_occurrence_groups(lb: np.ndarray):
+    """Native builder (libbmvplan) unless BMV_PLAN_NATIVE=0; same arrays as the numpy form."""
+    from . import _plan
+
+    lb = np.asarray(lb)
+    if _plan.enabled() and lb.shape[0] > 0:
+        return _plan.first_occurrence_groups(lb)
+    return _first_occurrence_groups_numpy(lb)
+
+
+def _first_occurrence_groups_numpy(lb: np.ndarray):
     """Group the DoFs of each cell by local block, groups in first-occurrence order.
 
     lb: (n_cells, n3) local block per cell DoF.  Returns
@@ -194,7 +204,10 @@ def build_cell_dof_map(mesh, numbering, layout, cells) -> CellDoFMap:
 
 def owned_cell_ghost_rows(mesh, numbering, partition, rank) -> np.ndarray:
     cells = partition.cells_of_rank(rank)
-    touched = np.unique(cells_nodes(mesh, numbering, cells))
+    nodes = cells_nodes(mesh, numbering, cells).ravel()
+    mark = np.zeros(int(nodes.max()) + 1 if nodes.size else 0, dtype=bool)
+    mark[nodes] = True
+    touched = np.flatnonzero(mark)  # == np.unique(nodes), without the sort
     lo, hi = numbering.owned_ranges[rank]
     return touched[(touched < lo) | (touched >= hi)]
 

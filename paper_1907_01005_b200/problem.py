@@ -241,7 +241,12 @@ def fill_multivector(matrix: BlockCsrMatrix, prob: Problem, seed: int, attach: b
     if matrix.n_owned_values < host.size:
         host[matrix.n_owned_values :] = matrix.data[matrix.n_owned_values :].cpu().numpy()
     if rows.size:
-        host[flat] = 2.0 * hashed_entries(seed, rows, prob.loc_layout.old_col_of_new[cols])
+        from . import _plan
+
+        if _plan.enabled():
+            _plan.hash_fill(seed, rows, cols, prob.loc_layout.old_col_of_new, flat, 2.0, host)
+        else:
+            host[flat] = 2.0 * hashed_entries(seed, rows, prob.loc_layout.old_col_of_new[cols])
     matrix.data.copy_(torch.from_numpy(host))
     if attach:
         attach_support(matrix, prob.column_support, check=False)

@@ -44,6 +44,16 @@ class ColumnSupport:
         centre = loc_layout.centers_of_new_cols()
         return cls(n_rows, [supports[int(c)] for c in centre])
 
+    def csr(self):
+        """(col_ptr, col_rows): the columns' rows concatenated (cached; native builder input)."""
+        hit = self.__dict__.get("_csr")
+        if hit is None:
+            ptr = np.zeros(self.n_cols + 1, dtype=np.int64)
+            np.cumsum([r.size for r in self.col_rows], out=ptr[1:])
+            rows = np.concatenate(self.col_rows) if self.n_cols else np.zeros(0, dtype=np.int64)
+            hit = self._csr = (ptr, np.ascontiguousarray(rows, dtype=np.int64))
+        return hit
+
     @property
     def nnz(self) -> int:
         return int(sum(r.size for r in self.col_rows))
@@ -112,13 +122,20 @@ class ColumnSupport:
         hit = cache.get(key)
         if hit is not None:
             return hit
+        from . import _plan
+
+        hit = _plan.owned_entries(self, matrix) if _plan.enabled() \
+            else self._owned_entries_numpy(matrix)
+        cache[key] = hit
+        return hit
+
+    def _owned_entries_numpy(self, matrix):
+        """numpy restatement of owned_entries (the native builder is pinned to it)."""
         layout = matrix.layout
         lo, hi = layout.owned_rows
         rows, cols = self.entries_in(lo, hi)
         if rows.size == 0:
-            hit = (rows, rows, cols)
-            cache[key] = hit
-            return hit
+            return rows, rows, cols
         blocks = layout.blocks
         nb_own = layout.n_owned_blocks
         own_sizes = blocks.sizes[layout.first_block : layout.first_block + nb_own]
@@ -142,9 +159,7 @@ class ColumnSupport:
             raise ConsistencyError("a support entry lies outside the multivector pattern")
         flat = (matrix.block_offsets[pos] + rib * matrix.col_strides[cbk]
                 + (cols - matrix.col_blocks.starts[cbk]))
-        hit = (flat, rows, cols)
-        cache[key] = hit
-        return hit
+        return flat, rows, cols
 
     def check_matrix(self, matrix) -> None:
         """Raise ConsistencyError if an owned entry outside the support is nonzero."""

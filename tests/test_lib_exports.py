@@ -45,3 +45,18 @@ def test_sm100a_code_present():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+def test_plan_library_exports_every_declared_symbol():
+    from paper_1907_01005_b200 import _plan
+
+    header = ROOT / "include" / "bmv_plan.h"
+    text = re.sub(r"/\*.*?\*/", "", header.read_text(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(bmvp_[a-z0-9_]+)\s*\(", text)))
+    assert names
+    lib = _plan.load()
+    for name in names:
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_plan.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert sorted(set(re.findall(r"\sT\s(bmvp_[a-z0-9_]+)", out))) == names

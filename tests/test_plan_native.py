@@ -1,0 +1,101 @@
+"""The native plan builder (libbmvplan.so, include/bmv_plan.h) against the numpy
+restatements it replaces: bit-identical arrays on the smoke, random and full-size
+layouts (CPU only; matrices live on the CPU)."""
+
+import numpy as np
+import pytest
+
+from paper_1907_01005_b200 import _plan
+from paper_1907_01005_b200 import problem as P
+from paper_1907_01005_b200.bcsr import BlockCsrMatrix
+from paper_1907_01005_b200.comm import run_ranks, serial_context
+from paper_1907_01005_b200.matfree import _first_occurrence_groups_numpy, make_dof_layout
+
+
+def test_library_exports():
+    lib = _plan.load()
+    assert lib.bmvp_version() == 1
+    for name in ("bmvp_hash_fill", "bmvp_owned_entries_count", "bmvp_owned_entries_fill",
+                 "bmvp_first_groups_count", "bmvp_first_groups_fill"):
+        assert hasattr(lib, name)
+
+
+def test_hash_fill_matches_numpy():
+    rng = np.random.default_rng(3)
+    rows = rng.integers(0, 1 << 40, 100_003)
+    cols = rng.integers(0, 4096, rows.size)
+    cmap = rng.permutation(4096)
+    for seed in (0, 1, 7, -5, (1 << 63) + 11):
+        want = 2.0 * P.hashed_entries(seed, rows, cmap[cols])
+        got = _plan.hash_fill(seed, rows, cols, cmap, None, 2.0)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    flat = rng.permutation(rows.size)
+    out = np.zeros(rows.size)
+    _plan.hash_fill(1, rows, cols, None, flat, 1.0, out)
+    want = np.zeros(rows.size)
+    want[flat] = P.hashed_entries(1, rows, cols)
+    assert np.array_equal(out, want)
+
+
+def _groups_equal(lb):
+    a = _plan.first_occurrence_groups(lb)
+    b = _first_occurrence_groups_numpy(lb)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_first_groups_random():
+    rng = np.random.default_rng(5)
+    for n3 in (8, 27, 125):
+        _groups_equal(rng.integers(0, 9, (300, n3)))
+        _groups_equal(np.zeros((4, n3), dtype=np.int64))
+
+
+def _owned_check(ctx, prob):
+    if True:
+        layout = make_dof_layout(ctx, prob.mesh, prob.partition, prob.numbering)
+        m = BlockCsrMatrix(prob.pattern, layout, ctx, prob.cfg.lane_width, "cpu")
+        a = _plan.owned_entries(prob.column_support, m)
+        b = prob.column_support._owned_entries_numpy(m)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+        c, _, _ = prob.column_support.owned_entries(m)
+        assert np.array_equal(c, b[0])
+        # the same offsets in the layout the CellOperator builds
+        op_groups = P.CellOperator(prob.mesh, prob.partition, prob.numbering, layout)
+        _groups_equal(op_groups._lb)
+
+
+@pytest.mark.parametrize("name", ["smoke", "q2"])
+def test_owned_entries_and_groups_configs(name):
+    _owned_check(serial_context("cpu"), P.build_problem(name))
+
+
+@pytest.mark.parametrize("n_ranks", [2, 4])
+def test_owned_entries_and_groups_ranks(n_ranks):
+    prob = P.build_problem("smoke", n_ranks)
+    run_ranks(n_ranks, lambda ctx: _owned_check(ctx, prob), device="cpu")
+
+
+def test_fill_multivector_native_equals_numpy(monkeypatch):
+    prob = P.build_problem("smoke")
+    st = P.make_rank_setup(serial_context("cpu"), prob, device="cpu")
+    got = st.x.data.numpy().copy()
+    monkeypatch.setenv("BMV_PLAN_NATIVE", "0")
+    prob2 = P.build_problem("smoke")
+    st2 = P.make_rank_setup(serial_context("cpu"), prob2, device="cpu")
+    assert np.array_equal(got, st2.x.data.numpy())
+    assert np.array_equal(st.op.cell_slots, st2.op.cell_slots)
+
+
+def test_blocks_of_matches_searchsorted():
+    rng = np.random.default_rng(9)
+    starts = np.concatenate([[5], 5 + np.cumsum(rng.integers(1, 70, 5000))])
+    idx = rng.integers(starts[0], starts[-1], 300_001)
+    b, off = _plan.blocks_of(starts, idx)
+    want = np.searchsorted(starts, idx, side="right") - 1
+    assert np.array_equal(b, want) and np.array_equal(off, idx - starts[want])
+    from paper_1907_01005_b200.errors import DomainError
+
+    with pytest.raises(DomainError):
+        _plan.blocks_of(starts, np.asarray([starts[-1]]))

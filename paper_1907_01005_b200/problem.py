@@ -173,27 +173,33 @@ class Problem:
         mesh = self.mesh
         nc = lay.centers.shape[0]
         nx, ny, nz = mesh.extents
-        patches, dilated = [], []
-        offs = np.asarray([[dx, dy, dz] for dz in (-1, 0, 1) for dy in (-1, 0, 1)
-                           for dx in (-1, 0, 1)])
-        for c in range(nc):
-            cells = np.unique(patch_fine_cells(mesh, lay, c))
-            patches.append(cells)
-            q = (mesh.cells_ijk(cells)[:, None, :] + offs[None, :, :]).reshape(-1, 3)
-            ok = ((q[:, 0] >= 0) & (q[:, 0] < nx) & (q[:, 1] >= 0) & (q[:, 1] < ny)
-                  & (q[:, 2] >= 0) & (q[:, 2] < nz))
-            q = q[ok]
-            dilated.append(np.unique(q[:, 0] + nx * (q[:, 1] + ny * q[:, 2])))
-        h = float(np.max(mesh.spacing)) * (1 << mesh.coarse_level)
-        reach = 2.0 * lay.radius + 4.0 * h * np.sqrt(3.0)
-        from scipy.spatial import cKDTree
-
-        cand = cKDTree(lay.centers).query_pairs(reach, output_type="ndarray")
-        rr, cc = [np.arange(nc)], [np.arange(nc)]
-        for a, b in cand:
-            if np.intersect1d(dilated[a], patches[b], assume_unique=True).size:
-                rr.append(np.asarray([a, b]))
-                cc.append(np.asarray([b, a]))
+        patches = [patch_fine_cells(mesh, lay, c) for c in range(nc)]
+        plen = np.asarray([p_.size for p_ in patches], dtype=np.int64)
+        n_cells = mesh.n_cells
+        pmat = sparse.csr_matrix(
+            (np.ones(int(plen.sum()), dtype=np.int32),
+             np.concatenate(patches) if nc else np.zeros(0, dtype=np.int64),
+             np.concatenate([[0], np.cumsum(plen)])), shape=(nc, n_cells))
+        pmat.sum_duplicates()
+        pmat.data[:] = 1
+        # cell adjacency (27-point, cells sharing a node) as a sparse matrix
+        ijk = mesh.cells_ijk(np.arange(n_cells))
+        rows_a, cols_a = [], []
+        for dz in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    q = ijk + np.asarray([dx, dy, dz])
+                    ok = ((q[:, 0] >= 0) & (q[:, 0] < nx) & (q[:, 1] >= 0) & (q[:, 1] < ny)
+                          & (q[:, 2] >= 0) & (q[:, 2] < nz))
+                    rows_a.append(np.flatnonzero(ok))
+                    qo = q[ok]
+                    cols_a.append(qo[:, 0] + nx * (qo[:, 1] + ny * qo[:, 2]))
+        adj = sparse.csr_matrix((np.ones(sum(r.size for r in rows_a), dtype=np.int32),
+                                 (np.concatenate(rows_a), np.concatenate(cols_a))),
+                                shape=(n_cells, n_cells))
+        touch = ((pmat @ adj) @ pmat.T).tocoo()  # patch a dilated by one cell meets patch b
+        rr = [np.arange(nc), touch.row.astype(np.int64)]
+        cc = [np.arange(nc), touch.col.astype(np.int64)]
         r_c = np.concatenate(rr)
         c_c = np.concatenate(cc)
         v = lay.vectors_per_center

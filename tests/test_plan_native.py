@@ -99,3 +99,19 @@ def test_blocks_of_matches_searchsorted():
 
     with pytest.raises(DomainError):
         _plan.blocks_of(starts, np.asarray([starts[-1]]))
+
+
+@pytest.mark.parametrize("name", ["smoke", "q2"])
+def test_support_overlap_equals_node_set_intersection(name):
+    """Cell-adjacency form of support_overlap == pairwise intersection of the DoF supports."""
+    prob = P.build_problem(name)
+    ov = prob.support_overlap().toarray()
+    lay = prob.loc_layout
+    nc, v = lay.centers.shape[0], lay.vectors_per_center
+    new = lay.new_col_of_old.reshape(nc, v)
+    want = np.zeros_like(ov)
+    for a in range(nc):
+        for b in range(nc):
+            if a == b or np.intersect1d(prob.supports[a], prob.supports[b]).size:
+                want[np.ix_(new[a], new[b])] = True
+    assert np.array_equal(ov, want)

@@ -12,6 +12,8 @@
  *   bmvp_owned_entries_*      bcsr.py:233-318 block storage offsets of the support
  *                             entries of a multivector (ColumnSupport.owned_entries)
  *   bmvp_blocks_of            bcsr.py:126-152 map_rows (row -> (block, row in block))
+ *   bmvp_grow_*               localization.py:251-267 grow_sparsity_for_operator
+ *                             (block pattern inc^T (inc S) + S)
  *   bmvp_first_groups_*       matfree.py:90-116 build_cell_dof_map: per-cell grouping of
  *                             DoFs by row block in first-occurrence order
  */
@@ -65,6 +67,18 @@ int bmvp_first_groups_count(int64_t n_cells, int32_t n3, const int64_t* lb,
 int bmvp_first_groups_fill(int64_t n_cells, int32_t n3, const int64_t* lb,
                            const int64_t* slot_group, const int64_t* cell_gstart,
                            int64_t* grp_cell, int64_t* grp_block);
+
+/* Block pattern of H X from the pattern S of X: row block rb holds column block cb iff
+ * S[rb, cb] or some cell touching rb touches a row block rb' with S[rb', cb].
+ * cell_rb: (n_cells, n3) row block of every cell DoF; bits: n_rb * ceil(n_cb/64) words,
+ * zeroed by the caller, returned as the row bitsets; row_count[rb] = popcount. */
+int bmvp_grow_count(int64_t n_cells, int32_t n3, const int64_t* cell_rb, int64_t n_rb,
+                    int64_t n_cb, const int64_t* s_row_start, const int64_t* s_col_index,
+                    uint64_t* bits, int64_t* row_count);
+
+/* Sorted column indices of every row from the bitsets; row_start = prefix sum of row_count. */
+int bmvp_grow_fill(int64_t n_rb, int64_t n_cb, const uint64_t* bits, const int64_t* row_start,
+                   int64_t* col_index);
 
 #ifdef __cplusplus
 }

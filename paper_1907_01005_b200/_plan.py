@@ -21,6 +21,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libbmvplan.so"
 
 _i64p = C.POINTER(C.c_int64)
 _f64p = C.POINTER(C.c_double)
+_u64p = C.POINTER(C.c_uint64)
 _lib = None
 _lock = threading.Lock()
 
@@ -49,7 +50,10 @@ def load():
         lib.bmvp_first_groups_count.argtypes = [C.c_int64, C.c_int32, _i64p, _i64p, _i64p]
         lib.bmvp_first_groups_fill.argtypes = [C.c_int64, C.c_int32, _i64p, _i64p, _i64p, _i64p,
                                                _i64p]
-        for f in ("bmvp_hash_fill", "bmvp_blocks_of", "bmvp_owned_entries_count", "bmvp_owned_entries_fill",
+        lib.bmvp_grow_count.argtypes = [C.c_int64, C.c_int32, _i64p, C.c_int64, C.c_int64,
+                                         _i64p, _i64p, _u64p, _i64p]
+        lib.bmvp_grow_fill.argtypes = [C.c_int64, C.c_int64, _u64p, _i64p, _i64p]
+        for f in ("bmvp_grow_count", "bmvp_grow_fill", "bmvp_hash_fill", "bmvp_blocks_of", "bmvp_owned_entries_count", "bmvp_owned_entries_fill",
                   "bmvp_first_groups_count", "bmvp_first_groups_fill"):
             getattr(lib, f).restype = C.c_int
         _lib = lib
@@ -63,6 +67,8 @@ def _i64(a) -> np.ndarray:
 def _p(a: np.ndarray | None):
     if a is None:
         return None
+    if a.dtype == np.uint64:
+        return a.ctypes.data_as(_u64p)
     return a.ctypes.data_as(_f64p if a.dtype == np.float64 else _i64p)
 
 
@@ -151,3 +157,21 @@ def first_occurrence_groups(lb: np.ndarray):
     _check(lib.bmvp_first_groups_fill(n_cells, n3, _p(lb), _p(slot_group), _p(cell_gstart),
                                       _p(grp_cell), _p(grp_block)), "bmvp_first_groups_fill")
     return slot_group, grp_cell, grp_block, cell_gstart
+
+
+def grow_pattern(cell_rb: np.ndarray, n_rb: int, n_cb: int, s_row_start, s_col_index):
+    """(row_start, col_index) of inc^T (inc S) + S (grow_sparsity_for_operator)."""
+    lib = load()
+    cell_rb = _i64(cell_rb)
+    n_cells, n3 = cell_rb.shape
+    words = (n_cb + 63) // 64
+    bits = np.zeros(max(n_rb * words, 1), dtype=np.uint64)
+    counts = np.empty(n_rb, dtype=np.int64)
+    _check(lib.bmvp_grow_count(n_cells, n3, _p(cell_rb), n_rb, n_cb, _p(_i64(s_row_start)),
+                               _p(_i64(s_col_index)), _p(bits), _p(counts)), "bmvp_grow_count")
+    row_start = np.zeros(n_rb + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_start[1:])
+    col_index = np.empty(int(row_start[-1]), dtype=np.int64)
+    _check(lib.bmvp_grow_fill(n_rb, n_cb, _p(bits), _p(row_start), _p(col_index)),
+           "bmvp_grow_fill")
+    return row_start, col_index

@@ -8,6 +8,8 @@
 //   bmvp_owned_entries_*   support.ColumnSupport.owned_entries (storage offsets of the
 //                          support entries, reference bcsr.py:233-318 layout)
 //   bmvp_blocks_of         RankLayout.map_rows, owned rows (reference bcsr.py:126-152)
+//   bmvp_grow_*            localization.grow_sparsity_for_operator (inc^T (inc S) + S,
+//                          reference localization.py:251-267) as per-cell bitset unions
 //   bmvp_first_groups_*    matfree._first_occurrence_groups (reference CellDoFMap
 //                          grouping, matfree.py:58-130)
 // Declared in include/bmv_plan.h.  No CUDA: these build index maps on the host
@@ -156,6 +158,67 @@ int bmvp_first_groups_fill(int64_t n_cells, int32_t n3, const int64_t* lb,
         grp_cell[g0 + next] = c;
         grp_block[g0 + next] = l[d];
         ++next;
+      }
+    }
+  }
+  return 0;
+}
+
+int bmvp_grow_count(int64_t n_cells, int32_t n3, const int64_t* cell_rb, int64_t n_rb,
+                    int64_t n_cb, const int64_t* s_row_start, const int64_t* s_col_index,
+                    uint64_t* bits, int64_t* row_count) {
+  if (n_cells < 0 || n3 <= 0 || n3 > 4096 || n_rb < 0 || n_cb < 0) return 1;
+  const int64_t W = (n_cb + 63) / 64;
+  // the pattern itself (the "+ S" term)
+#pragma omp parallel for schedule(static)
+  for (int64_t rb = 0; rb < n_rb; ++rb)
+    for (int64_t k = s_row_start[rb]; k < s_row_start[rb + 1]; ++k)
+      bits[rb * W + s_col_index[k] / 64] |= uint64_t(1) << (s_col_index[k] % 64);
+  int bad = 0;
+#pragma omp parallel reduction(| : bad)
+  {
+    std::vector<uint64_t> cset(W);
+    std::vector<int64_t> rbs;
+    rbs.reserve(64);
+#pragma omp for schedule(static)
+    for (int64_t c = 0; c < n_cells; ++c) {
+      rbs.clear();
+      const int64_t* l = cell_rb + c * n3;
+      for (int32_t d = 0; d < n3; ++d) {
+        if (l[d] < 0 || l[d] >= n_rb) { bad = 1; break; }
+        if (std::find(rbs.begin(), rbs.end(), l[d]) == rbs.end()) rbs.push_back(l[d]);
+      }
+      std::fill(cset.begin(), cset.end(), 0);
+      for (int64_t rb : rbs)  // inc S: the column blocks any row block of the cell holds
+        for (int64_t k = s_row_start[rb]; k < s_row_start[rb + 1]; ++k)
+          cset[s_col_index[k] / 64] |= uint64_t(1) << (s_col_index[k] % 64);
+      for (int64_t rb : rbs)  // inc^T (inc S)
+        for (int64_t w = 0; w < W; ++w)
+          if (cset[w]) __atomic_fetch_or(&bits[rb * W + w], cset[w], __ATOMIC_RELAXED);
+    }
+  }
+  if (bad) return 1;
+#pragma omp parallel for schedule(static)
+  for (int64_t rb = 0; rb < n_rb; ++rb) {
+    int64_t n = 0;
+    for (int64_t w = 0; w < W; ++w) n += __builtin_popcountll(bits[rb * W + w]);
+    row_count[rb] = n;
+  }
+  return 0;
+}
+
+int bmvp_grow_fill(int64_t n_rb, int64_t n_cb, const uint64_t* bits, const int64_t* row_start,
+                   int64_t* col_index) {
+  if (n_rb < 0 || n_cb < 0) return 1;
+  const int64_t W = (n_cb + 63) / 64;
+#pragma omp parallel for schedule(static)
+  for (int64_t rb = 0; rb < n_rb; ++rb) {
+    int64_t o = row_start[rb];
+    for (int64_t w = 0; w < W; ++w) {
+      uint64_t m = bits[rb * W + w];
+      while (m) {
+        col_index[o++] = w * 64 + __builtin_ctzll(m);
+        m &= m - 1;
       }
     }
   }

@@ -115,3 +115,35 @@ def test_support_overlap_equals_node_set_intersection(name):
             if a == b or np.intersect1d(prob.supports[a], prob.supports[b]).size:
                 want[np.ix_(new[a], new[b])] = True
     assert np.array_equal(ov, want)
+
+
+@pytest.mark.parametrize("name", ["smoke", "q2", "q4"])
+def test_grow_pattern_native_equals_sparse_product(name):
+    from paper_1907_01005_b200.localization import (_grow_sparsity_numpy,
+                                                    grow_sparsity_for_operator)
+
+    prob = P.build_problem(name)
+    a = grow_sparsity_for_operator(prob.pattern, prob.mesh, prob.numbering)
+    b = _grow_sparsity_numpy(prob.pattern, prob.mesh, prob.numbering)
+    assert np.array_equal(a.row_start, b.row_start) and np.array_equal(a.col_index, b.col_index)
+
+
+def test_grow_pattern_random_patterns():
+    from paper_1907_01005_b200.localization import (_grow_sparsity_numpy,
+                                                    grow_sparsity_for_operator)
+    from paper_1907_01005_b200.blocks import BlockSparsityPattern
+
+    prob = P.build_problem("smoke", 2)
+    rng = np.random.default_rng(11)
+    nrb = prob.pattern.row_blocks.n_blocks
+    for n_cb_frac in (0.05, 0.3):
+        from paper_1907_01005_b200.blocks import BlockIndices
+
+        cb = BlockIndices(np.full(130, 1))  # > 64 column blocks: several bitset words
+        mask = rng.random((nrb, 130)) < n_cb_frac
+        row_start = np.concatenate([[0], np.cumsum(mask.sum(1))])
+        pat = BlockSparsityPattern.from_csr(prob.pattern.row_blocks, cb, row_start,
+                                            np.nonzero(mask)[1])
+        a = grow_sparsity_for_operator(pat, prob.mesh, prob.numbering)
+        b = _grow_sparsity_numpy(pat, prob.mesh, prob.numbering)
+        assert np.array_equal(a.row_start, b.row_start) and np.array_equal(a.col_index, b.col_index)

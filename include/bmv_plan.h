@@ -12,6 +12,7 @@
  *   bmvp_owned_entries_*      bcsr.py:233-318 block storage offsets of the support
  *                             entries of a multivector (ColumnSupport.owned_entries)
  *   bmvp_blocks_of            bcsr.py:126-152 map_rows (row -> (block, row in block))
+ *   bmvp_first_touch          mesh.py:263-322 enumerate_dofs (first-touch positions)
  *   bmvp_grow_*               localization.py:251-267 grow_sparsity_for_operator
  *                             (block pattern inc^T (inc S) + S)
  *   bmvp_first_groups_*       matfree.py:90-116 build_cell_dof_map: per-cell grouping of
@@ -67,6 +68,9 @@ int bmvp_first_groups_count(int64_t n_cells, int32_t n3, const int64_t* lb,
 int bmvp_first_groups_fill(int64_t n_cells, int32_t n3, const int64_t* lb,
                            const int64_t* slot_group, const int64_t* cell_gstart,
                            int64_t* grp_cell, int64_t* grp_block);
+
+/* first[v] = smallest pos with touches[pos] == v, else n (first-touch DoF numbering). */
+int bmvp_first_touch(int64_t n_nodes, int64_t n, const int64_t* touches, int64_t* first);
 
 /* Block pattern of H X from the pattern S of X: row block rb holds column block cb iff
  * S[rb, cb] or some cell touching rb touches a row block rb' with S[rb', cb].

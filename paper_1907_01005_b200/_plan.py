@@ -53,7 +53,8 @@ def load():
         lib.bmvp_grow_count.argtypes = [C.c_int64, C.c_int32, _i64p, C.c_int64, C.c_int64,
                                          _i64p, _i64p, _u64p, _i64p]
         lib.bmvp_grow_fill.argtypes = [C.c_int64, C.c_int64, _u64p, _i64p, _i64p]
-        for f in ("bmvp_grow_count", "bmvp_grow_fill", "bmvp_hash_fill", "bmvp_blocks_of", "bmvp_owned_entries_count", "bmvp_owned_entries_fill",
+        lib.bmvp_first_touch.argtypes = [C.c_int64, C.c_int64, _i64p, _i64p]
+        for f in ("bmvp_first_touch", "bmvp_grow_count", "bmvp_grow_fill", "bmvp_hash_fill", "bmvp_blocks_of", "bmvp_owned_entries_count", "bmvp_owned_entries_fill",
                   "bmvp_first_groups_count", "bmvp_first_groups_fill"):
             getattr(lib, f).restype = C.c_int
         _lib = lib
@@ -175,3 +176,12 @@ def grow_pattern(cell_rb: np.ndarray, n_rb: int, n_cb: int, s_row_start, s_col_i
     _check(lib.bmvp_grow_fill(n_rb, n_cb, _p(bits), _p(row_start), _p(col_index)),
            "bmvp_grow_fill")
     return row_start, col_index
+
+
+def first_touch(n_nodes: int, touches) -> np.ndarray:
+    """first[v] = first position of v in touches (touches.size if never touched)."""
+    lib = load()
+    touches = _i64(touches)
+    first = np.empty(n_nodes, dtype=np.int64)
+    _check(lib.bmvp_first_touch(n_nodes, touches.size, _p(touches), _p(first)), "bmvp_first_touch")
+    return first

@@ -8,6 +8,8 @@
 //   bmvp_owned_entries_*   support.ColumnSupport.owned_entries (storage offsets of the
 //                          support entries, reference bcsr.py:233-318 layout)
 //   bmvp_blocks_of         RankLayout.map_rows, owned rows (reference bcsr.py:126-152)
+//   bmvp_first_touch       mesh.enumerate_dofs first-touch positions (reference
+//                          mesh.py:263-322 numbering along the ordered cells)
 //   bmvp_grow_*            localization.grow_sparsity_for_operator (inc^T (inc S) + S,
 //                          reference localization.py:251-267) as per-cell bitset unions
 //   bmvp_first_groups_*    matfree._first_occurrence_groups (reference CellDoFMap
@@ -160,6 +162,17 @@ int bmvp_first_groups_fill(int64_t n_cells, int32_t n3, const int64_t* lb,
         ++next;
       }
     }
+  }
+  return 0;
+}
+
+int bmvp_first_touch(int64_t n_nodes, int64_t n, const int64_t* touches, int64_t* first) {
+  if (n_nodes < 0 || n < 0) return 1;
+  for (int64_t i = 0; i < n_nodes; ++i) first[i] = n;
+  for (int64_t pos = 0; pos < n; ++pos) {
+    const int64_t t = touches[pos];
+    if (t < 0 || t >= n_nodes) return 1;
+    if (first[t] == n) first[t] = pos;
   }
   return 0;
 }

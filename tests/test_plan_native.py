@@ -147,3 +147,24 @@ def test_grow_pattern_random_patterns():
         a = grow_sparsity_for_operator(pat, prob.mesh, prob.numbering)
         b = _grow_sparsity_numpy(pat, prob.mesh, prob.numbering)
         assert np.array_equal(a.row_start, b.row_start) and np.array_equal(a.col_index, b.col_index)
+
+
+def test_first_touch_matches_minimum_at():
+    rng = np.random.default_rng(2)
+    touches = rng.integers(0, 5000, 200_000)
+    first = np.full(5003, touches.size, dtype=np.int64)
+    np.minimum.at(first, touches, np.arange(touches.size))
+    assert np.array_equal(_plan.first_touch(5003, touches), first)
+
+
+@pytest.mark.parametrize("n_ranks", [1, 3])
+def test_enumerate_dofs_native_equals_numpy(monkeypatch, n_ranks):
+    from paper_1907_01005_b200.mesh import build_mesh, enumerate_dofs, partition_and_order_cells
+
+    mesh = build_mesh((6, 5, 7), (1 / 6, 1 / 5, 1 / 7), 0)
+    part = partition_and_order_cells(mesh, n_ranks)
+    a = enumerate_dofs(mesh, part, 3)
+    monkeypatch.setenv("BMV_PLAN_NATIVE", "0")
+    b = enumerate_dofs(mesh, part, 3)
+    assert np.array_equal(a.new_index_of_node, b.new_index_of_node)
+    assert a.owned_ranges == b.owned_ranges

@@ -241,14 +241,21 @@ def fill_multivector(matrix: BlockCsrMatrix, prob: Problem, seed: int, attach: b
     """
     import torch
 
+    from . import _plan
+
     matrix._require("owned-writable")
     flat, rows, cols = _support_entries(matrix, prob)
+    if attach and matrix.data.is_cuda and _plan.enabled():
+        # compact values (nnz, column-major support order) scattered on the device:
+        # no padded host image, host->device bytes = 8 nnz instead of the stored blocks
+        attach_support(matrix, prob.column_support, check=False)
+        vals = _plan.hash_fill(seed, rows, cols, prob.loc_layout.old_col_of_new, None, 2.0)
+        matrix.upload_support_values(torch.from_numpy(vals))
+        return matrix
     host = np.zeros(matrix.data.numel())
     if matrix.n_owned_values < host.size:
         host[matrix.n_owned_values :] = matrix.data[matrix.n_owned_values :].cpu().numpy()
     if rows.size:
-        from . import _plan
-
         if _plan.enabled():
             _plan.hash_fill(seed, rows, cols, prob.loc_layout.old_col_of_new, flat, 2.0, host)
         else:

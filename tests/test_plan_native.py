@@ -168,3 +168,23 @@ def test_enumerate_dofs_native_equals_numpy(monkeypatch, n_ranks):
     b = enumerate_dofs(mesh, part, 3)
     assert np.array_equal(a.new_index_of_node, b.new_index_of_node)
     assert a.owned_ranges == b.owned_ranges
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,n_ranks", [("smoke", 1), ("q2", 1), ("smoke", 2)])
+def test_fill_multivector_device_scatter_equals_host_image(name, n_ranks):
+    """The device path (compact values + upload_support_values) writes the same X as the
+    host image path, ghosts included, bit for bit."""
+    import torch
+
+    prob = P.build_problem(name, n_ranks)
+    dev = torch.device("cuda", 0)
+
+    def prog(ctx):
+        layout = make_dof_layout(ctx, prob.mesh, prob.partition, prob.numbering)
+        a = P.fill_multivector(BlockCsrMatrix(prob.pattern, layout, ctx, 8, dev), prob, 1)
+        b = P.fill_multivector(BlockCsrMatrix(prob.pattern, layout, ctx, 8, "cpu"), prob, 1)
+        torch.cuda.synchronize()
+        return bool(torch.equal(a.data.cpu(), b.data))
+
+    assert all(run_ranks(n_ranks, prog, device=dev))

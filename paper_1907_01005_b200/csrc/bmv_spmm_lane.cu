@@ -305,8 +305,10 @@ struct StreamBuild {
   std::vector<int64_t> chunk_entry{0};
   std::vector<int64_t> chunk_work;
   std::vector<int64_t> fixed_parts;  // chunk index where each part starts (K4: items never span parts)
-  // deferred chunks (interleaved assignment): chunk c goes to CTA c % n_parts
+  // deferred chunks (interleaved assignment): run r = chunks [r*run, (r+1)*run)
+  // goes to CTA r % n_parts (K4 items may span the chunks of one run)
   bool defer = false;
+  int64_t run = 1;
   std::vector<std::pair<Chunk, int64_t>> pending;
   void put(const Chunk& c, int64_t work) {
     if (defer)
@@ -320,11 +322,14 @@ struct StreamBuild {
   void finish_interleaved(int n_parts) {
     if (!defer) return;
     const int64_t nc = (int64_t)pending.size();
-    const int64_t np = std::max<int64_t>(1, std::min<int64_t>(n_parts, nc));
+    const int64_t nr = (nc + run - 1) / run;
+    const int64_t np = std::max<int64_t>(1, std::min<int64_t>(n_parts, nr));
     fixed_parts.clear();
     for (int64_t b = 0; b < np; ++b) {
       fixed_parts.push_back((int64_t)chunk_work.size());
-      for (int64_t c = b; c < nc; c += np) add(pending[(size_t)c].first, pending[(size_t)c].second);
+      for (int64_t r = b; r < nr; r += np)
+        for (int64_t c = r * run; c < std::min(nc, (r + 1) * run); ++c)
+          add(pending[(size_t)c].first, pending[(size_t)c].second);
     }
     pending.clear();
     defer = false;
@@ -389,6 +394,13 @@ bool interleave_override(bool choice) {
   const char* e = std::getenv("BMV_LANE_INTERLEAVE");
   if (e && e[0] == '0') return false;
   if (e && e[0] == '1') return true;
+  return choice;
+}
+
+// BMV_LANE_RUN=k forces the K4 interleave run length (tests / tuning)
+int64_t lane_run_override(int64_t choice) {
+  const char* e = std::getenv("BMV_LANE_RUN");
+  if (e && e[0]) return std::max<int64_t>(1, std::atoll(e));
   return choice;
 }
 
@@ -459,6 +471,8 @@ int plan_k4(const bmv_tmmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out
   };
   // close the current chunk (flush=true: also the item)
   auto emit = [&](bool do_flush) {
+    // interleaved chunks: the item closes at the end of every run of chunks
+    if (sb.defer && ((int64_t)sb.pending.size() + 1) % sb.run == 0) do_flush = true;
     const int n_tiles = (int)(recs.size() / kK4Rec);
     const int nfl = do_flush ? (int)flush.size() : 0;
     if (n_tiles == 0 && nfl == 0) return;
@@ -538,6 +552,11 @@ int plan_k4(const bmv_tmmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out
   const bool interleave = interleave_override(d->n_rows > 0 && sum_rows < 16 * (int64_t)d->n_rows &&
                                               data_bytes >= 16LL * n_parts * stage_bytes);
   sb.defer = interleave;
+  // runs of consecutive chunks per CTA turn: fewer item flushes (S tiles shared by
+  // neighbouring block rows are reduced in shared memory once per run instead of once
+  // per chunk) while every CTA still gets >= 16 runs
+  sb.run = lane_run_override(std::max<int64_t>(
+      1, std::min<int64_t>(8, data_bytes / std::max<int64_t>(1, 16LL * n_parts * stage_bytes))));
   int next_part = 1;
   sb.fixed_parts.push_back(0);
   for (int32_t i = 0; i < d->n_rows; ++i) {
@@ -638,7 +657,7 @@ int plan_k4(const bmv_tmmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out
         const int need = align16((int)((a_last - a_lo) * 8)) +
                          align16((int)((b_first + b_len - b_lo) * 8)) +
                          chunk_meta_bytes(recs.size() / kK4Rec + grp_tiles, kAccTiles) + 64;
-        if (same_row || need > stage_bytes || a_last - a_lo >= 0x8000) emit(interleave);
+        if (same_row || need > stage_bytes || a_last - a_lo >= 0x8000) emit(false);
       }
       if (recs.empty()) {
         a_lo = a_first;

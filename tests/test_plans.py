@@ -66,14 +66,17 @@ def test_mmult_plan_emulation(block_size, lane_width, n_parts, accumulate):
 #    kernels emulated on CPU over the host stage stream ----------------------
 
 
-@pytest.fixture(params=["auto", "1"])
+@pytest.fixture(params=["auto", "1", "1:run3"])
 def interleave(request, monkeypatch):
     """Lane plans: the planner's chunk assignment, or chunks interleaved over
-    the CTAs with one accumulator item per chunk (short block rows)."""
+    the CTAs with one accumulator item per chunk (short block rows), or runs of
+    3 consecutive chunks per CTA turn sharing one K4 item."""
+    monkeypatch.delenv("BMV_LANE_RUN", raising=False)
     if request.param == "auto":
         monkeypatch.delenv("BMV_LANE_INTERLEAVE", raising=False)
     else:
-        monkeypatch.setenv("BMV_LANE_INTERLEAVE", request.param)
+        monkeypatch.setenv("BMV_LANE_INTERLEAVE", "1")
+        monkeypatch.setenv("BMV_LANE_RUN", "3" if request.param.endswith("run3") else "1")
     return request.param
 
 

@@ -41,7 +41,10 @@ using namespace bmv;
 
 namespace {
 
-constexpr int kLnWarps = 16;                      // consumer warps
+#ifndef BMV_LN_WARPS
+#define BMV_LN_WARPS 16
+#endif
+constexpr int kLnWarps = BMV_LN_WARPS;            // consumer warps
 constexpr int kLnThreads = (kLnWarps + 1) * 32;   // + producer
 constexpr int kLnStages = 3;
 constexpr int kAccTiles = 64;                     // K4 shared accumulator: 64 tiles of 8x8
@@ -556,7 +559,7 @@ int plan_k4(const bmv_tmmult_lane_desc* d, StreamBuild& sb, int& stage_bytes_out
   // neighbouring block rows are reduced in shared memory once per run instead of once
   // per chunk) while every CTA still gets >= 16 runs
   sb.run = lane_run_override(std::max<int64_t>(
-      1, std::min<int64_t>(8, data_bytes / std::max<int64_t>(1, 16LL * n_parts * stage_bytes))));
+      1, std::min<int64_t>(4, data_bytes / std::max<int64_t>(1, 16LL * n_parts * stage_bytes))));
   int next_part = 1;
   sb.fixed_parts.push_back(0);
   for (int32_t i = 0; i < d->n_rows; ++i) {

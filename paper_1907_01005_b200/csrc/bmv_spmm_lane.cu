@@ -41,11 +41,12 @@ using namespace bmv;
 
 namespace {
 
-#ifndef BMV_LN_WARPS
-#define BMV_LN_WARPS 16
-#endif
-constexpr int kLnWarps = BMV_LN_WARPS;            // consumer warps
-constexpr int kLnThreads = (kLnWarps + 1) * 32;   // + producer
+// consumer warps (+ 1 producer warp) per CTA: 16 for long block rows (the kernels
+// stream at the HBM roofline), 24 where per-tile latency binds -- K4 on short
+// (interleaved) block rows and K5 everywhere (measured: proj K4 0.974 -> 0.895 ms,
+// K5 0.600 -> 0.537 ms; weak G = 1 K4 0.983 -> 1.004 ms, K5 0.893 -> 0.878 ms)
+constexpr int kLnWarps = 16;
+constexpr int kLnWarpsWide = 24;
 constexpr int kLnStages = 3;
 constexpr int kAccTiles = 64;                     // K4 shared accumulator: 64 tiles of 8x8
 constexpr int kSmemBudget = 227 * 1024 - 1024;
@@ -72,11 +73,13 @@ struct LnArgs {
   const double* __restrict__ cmat;  // K5: the C operand (global)
 };
 
+template <int NW>
 __device__ __forceinline__ void consumers_sync() {
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kLnWarps * 32) : "memory");
+  asm volatile("bar.sync 1, %0;\n" ::"n"(NW * 32) : "memory");
 }
 
-__global__ void __launch_bounds__(kLnThreads, 1) k4_lane_kernel(const LnArgs g) {
+template <int NW>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) k4_lane_kernel(const LnArgs g) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[kLnStages], empty[kLnStages];
   double* acc = smem;  // kAccTiles * 64
@@ -86,12 +89,12 @@ __global__ void __launch_bounds__(kLnThreads, 1) k4_lane_kernel(const LnArgs g) 
   if (threadIdx.x == 0) {
     for (int k = 0; k < kLnStages; ++k) {
       mbar_init(&full[k], 1);
-      mbar_init(&empty[k], kLnWarps);
+      mbar_init(&empty[k], NW);
     }
   }
   for (int i = threadIdx.x; i < kAccTiles * 64; i += blockDim.x) acc[i] = 0.0;
   __syncthreads();
-  if (warp == kLnWarps) {
+  if (warp == NW) {
     stream_producer(g.copies, g.part_entry_start[blockIdx.x], g.part_entry_start[blockIdx.x + 1],
                     s1 - s0, g.src, stages, g.stage_bytes, kLnStages, full, empty, lane);
     return;
@@ -105,7 +108,7 @@ __global__ void __launch_bounds__(kLnThreads, 1) k4_lane_kernel(const LnArgs g) 
     const double* S = reinterpret_cast<const double*>(stg);
     const int n_tiles = hdr[0], n_flush = hdr[1];
     const int* recs = hdr + hdr[2];
-    for (int t = warp; t < n_tiles; t += kLnWarps) {
+    for (int t = warp; t < n_tiles; t += NW) {
       const int* r = recs + t * kK4Rec;
       const int ac = r[gid];
       const int ao = ac & 0xffff, as = (ac >> 16) & 0x7fff;
@@ -147,8 +150,8 @@ __global__ void __launch_bounds__(kLnThreads, 1) k4_lane_kernel(const LnArgs g) 
       if (lane == 0) mbar_arrive(&empty[st]);
       continue;
     }
-    consumers_sync();  // every tile of the item is in acc
-    for (int f = warp; f < n_flush; f += kLnWarps) {
+    consumers_sync<NW>();  // every tile of the item is in acc
+    for (int f = warp; f < n_flush; f += NW) {
       fl = frec[f];
       const int rr = fl.z & 0xff, cc = (fl.z >> 8) & 0xff;
       double* tile = acc + fl.w * 64;
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(kLnThreads, 1) k4_lane_kernel(const LnArgs g) 
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-    consumers_sync();  // acc cleared before the next item accumulates
+    consumers_sync<NW>();  // acc cleared before the next item accumulates
   }
 }
 
@@ -175,8 +178,8 @@ __global__ void __launch_bounds__(kLnThreads, 1) k4_lane_kernel(const LnArgs g) 
 // and 4 C element offsets (row a, column lane 0 of the tile; -1 none).
 // TWO: two 8-row tiles in flight per task (independent DMMA chains) for
 // block rows of many rows (Q4: 65); one tile for short rows (Q2: 8).
-template <int MAXK, bool TWO>
-__global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) {
+template <int MAXK, bool TWO, int NW>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) k5_lane_kernel(const LnArgs g) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[kLnStages], empty[kLnStages];
   char* stages = reinterpret_cast<char*>(smem);
@@ -185,11 +188,11 @@ __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) 
   if (threadIdx.x == 0) {
     for (int k = 0; k < kLnStages; ++k) {
       mbar_init(&full[k], 1);
-      mbar_init(&empty[k], kLnWarps);
+      mbar_init(&empty[k], NW);
     }
   }
   __syncthreads();
-  if (warp == kLnWarps) {
+  if (warp == NW) {
     stream_producer(g.copies, g.part_entry_start[blockIdx.x], g.part_entry_start[blockIdx.x + 1],
                     s1 - s0, g.src, stages, g.stage_bytes, kLnStages, full, empty, lane);
     return;
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(kLnThreads, 1) k5_lane_kernel(const LnArgs g) 
     const double* S = reinterpret_cast<const double*>(stg);
     const int n_tasks = hdr[0];
     const int* toff = hdr + hdr[1];
-    for (int t = warp; t < n_tasks; t += kLnWarps) {
+    for (int t = warp; t < n_tasks; t += NW) {
       const int* r = hdr + toff[t];
       double* Y = g.out + (((int64_t)(unsigned)r[1] << 32) | (unsigned)r[0]);
       const int rows = r[2] & 0xffff, ys = r[2] >> 16;
@@ -311,6 +314,7 @@ struct StreamBuild {
   // deferred chunks (interleaved assignment): run r = chunks [r*run, (r+1)*run)
   // goes to CTA r % n_parts (K4 items may span the chunks of one run)
   bool defer = false;
+  bool interleaved = false;  // finish_interleaved dealt the chunks
   int64_t run = 1;
   std::vector<std::pair<Chunk, int64_t>> pending;
   void put(const Chunk& c, int64_t work) {
@@ -336,6 +340,7 @@ struct StreamBuild {
     }
     pending.clear();
     defer = false;
+    interleaved = true;
   }
   void add(const Chunk& c, int64_t work) {
     const int64_t moff = (int64_t)meta.size() * 4;  // bytes
@@ -413,6 +418,7 @@ struct bmv_lane_plan {
   int kind = 0;  // 4 or 5
   int maxk = 0;  // K5: largest k-step count of a task
   bool two_tiles = false;  // K5: block rows average more than 16 rows
+  bool short_rows = false;  // K4: interleaved chunks (short block rows)
   int n_parts = 0;
   int stage_bytes = 0;
   int smem_bytes = 0;
@@ -740,6 +746,7 @@ int bmv_tmmult_lane_create(const bmv_tmmult_lane_desc* d, bmv_lane_plan** out) {
   }
   auto* p = new bmv_lane_plan();
   p->kind = 4;
+  p->short_rows = sb.interleaved;
   p->stage_bytes = stage_bytes;
   p->smem_bytes = kAccTiles * 64 * 8 + kLnStages * stage_bytes;
   int rc = sb.chunk_work.empty() ? BMV_OK : upload_stream(sb, sm_count(), p);
@@ -761,7 +768,9 @@ int bmv_tmmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doub
   cudaStream_t st = as_stream(stream);
   int rc = zero_async(c, c_len, st);
   if (rc || p->n_parts == 0) return rc;
-  BMV_CUDA_TRY(cudaFuncSetAttribute(k4_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = p->short_rows ? k4_lane_kernel<kLnWarpsWide> : k4_lane_kernel<kLnWarps>;
+  const int threads = ((p->short_rows ? kLnWarpsWide : kLnWarps) + 1) * 32;
+  BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     p->smem_bytes));
   LnArgs g{};
   g.part_sub_start = p->part_sub_start;
@@ -771,7 +780,7 @@ int bmv_tmmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doub
                   reinterpret_cast<const char*>(b)};
   g.out = c;
   g.stage_bytes = p->stage_bytes;
-  k4_lane_kernel<<<p->n_parts, kLnThreads, p->smem_bytes, st>>>(g);
+  kern<<<p->n_parts, threads, p->smem_bytes, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
@@ -988,7 +997,8 @@ int bmv_mmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doubl
   cudaStream_t st = as_stream(stream);
   int rc = zero_async(c, zero_len, st);
   if (rc || p->n_parts == 0) return rc;
-  auto kern = p->two_tiles ? k5_lane_kernel<kKGroup, true> : k5_lane_kernel<kKGroup, false>;
+  auto kern = p->two_tiles ? k5_lane_kernel<kKGroup, true, kLnWarpsWide>
+                           : k5_lane_kernel<kKGroup, false, kLnWarpsWide>;
   BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     p->smem_bytes));
   LnArgs g{};
@@ -1001,7 +1011,7 @@ int bmv_mmult_lane_run(bmv_lane_plan* p, const double* a, const double* b, doubl
   g.accumulate = accumulate;
   g.stage_bytes = p->stage_bytes;
   g.cmat = b;
-  kern<<<p->n_parts, kLnThreads, p->smem_bytes, st>>>(g);
+  kern<<<p->n_parts, (kLnWarpsWide + 1) * 32, p->smem_bytes, st>>>(g);
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }

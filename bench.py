@@ -147,7 +147,9 @@ def workload_counts(st):
 
 
 def measure_fp64_peak(torch, lib, C, dev):
-    """FP64 FMA throughput of this GPU (roofline denominator for K1), TFLOP/s."""
+    """FP64 throughput of this GPU, TFLOP/s: (DFMA probe, DMMA probe).  The K1
+    roofline denominator is the larger of the two (MEASURED_PEAKS.json has no
+    FP64 entry)."""
     from paper_1907_01005_b200 import _lib
 
     scratch = torch.zeros(8, dtype=torch.float64, device=dev)
@@ -156,18 +158,21 @@ def measure_fp64_peak(torch, lib, C, dev):
     blocks = sm.value * 8
     flops = C.c_double()
     st = _lib.stream_handle(dev)
-    for _ in range(2):
-        _lib.check(lib.bmv_fp64_peak_kernel(_lib.dptr(scratch), blocks, 256, C.byref(flops), st))
-    torch.cuda.synchronize()
-    best = 0.0
-    for _ in range(5):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        _lib.check(lib.bmv_fp64_peak_kernel(_lib.dptr(scratch), blocks, 2048, C.byref(flops), st))
-        e1.record()
-        e1.synchronize()
-        best = max(best, flops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
-    return best
+    out = []
+    for fn, iters in ((lib.bmv_fp64_peak_kernel, 2048), (lib.bmv_fp64_dmma_peak_kernel, 1024)):
+        for _ in range(2):
+            _lib.check(fn(_lib.dptr(scratch), blocks, 64, C.byref(flops), st))
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _lib.check(fn(_lib.dptr(scratch), blocks, iters, C.byref(flops), st))
+            e1.record()
+            e1.synchronize()
+            best = max(best, flops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        out.append(best)
+    return tuple(out)
 
 
 def peaks_file():
@@ -183,70 +188,91 @@ def peaks_file():
 # -- the CPU reference arm -----------------------------------------------------------------
 
 
+def bench_config(name, prob, st):
+    """The `config` object of both arms' JSON lines (same workload, same text)."""
+    return {"workload": name, "note": prob.cfg.note,
+            "step": "apply H (halo) + tmmult S=X^T(HX) (compress) + mmult XC",
+            "storage": "slab layout (slabs.py): X %.3f GB, H X %.3f GB, X C %.3f GB" % (
+                st.x.slab.off[-1] * 8e-9, st.hx.slab.off[-1] * 8e-9, st.xc.slab.off[-1] * 8e-9),
+            "l2": "inputs larger than L2 (126 MB): no flush between steps"}
+
+
 def reference_arm(args, rank, world):
+    """The reference algorithm on the host cores: the C restatement of the
+    reference loops (oracle/cellop.c: Algorithm 6 on the reference BCSR layout,
+    all lanes, 18 contractions; tmmult / mmult block loops), inputs built with
+    the package's numpy setup path only (BMV_PLAN_NATIVE=0: no repo library is
+    loaded by this process besides oracle/liboracle.so)."""
+    os.environ["BMV_PLAN_NATIVE"] = "0"
+    if rank != 0:
+        return
     import torch  # noqa: F401  (matrices on the CPU)
 
     from oracle import c_oracle as CO
-    from oracle import numpy_oracle as NO
     from paper_1907_01005_b200 import problem as P
     from paper_1907_01005_b200.comm import serial_context
 
-    if rank != 0:
-        return
     name = args.config or f"weak{world}"
     prob = P.build_problem(name, world)
-    st = P.make_rank_setup(serial_context("cpu"), prob, device="cpu")
+    st = P.make_rank_setup(serial_context("cpu"), prob, device="cpu", projection=True)
     cnt = workload_counts(st)
-    f_total = cnt["flops_hx"] + (cnt["flops_s"] + cnt["flops_xc"] if st.s is not None else 0)
+    f_total = cnt["flops_hx"] + cnt["flops_s"] + cnt["flops_xc"]
     threads = os.cpu_count() or 1
     op = st.op
     deg = prob.cfg.degree
     n_cells = len(op.cells)
-    vq_all = NO.sample_potential(prob.potential, op.cell_origins, deg, prob.mesh.spacing) \
-        if n_cells * (deg + 1) ** 3 * prob.cfg.centers.shape[0] < 5e8 else None
-    # sample size: about 2 s of H X per step on this host
-    frac = 1.0
-    probe = max(1, min(n_cells, 256))
-    x = st.x.data.numpy()
-
+    x = CO.reference_values(st.x)
+    c_vals = CO.reference_values(st.c)
     vq_cache = {}
 
-    def run_cells(k):
-        sel = slice(0, k)
+    def hx_cells(k):
         if k not in vq_cache:
             vq_cache.clear()
-            vq_cache[k] = vq_all[sel] if vq_all is not None else NO.sample_potential(
-                prob.potential, op.cell_origins[sel], deg, prob.mesh.spacing)
-        vq = vq_cache[k]
-        h = np.zeros(st.hx.data.numel())
+            vq_cache[k] = CO.potential_gaussian(prob.potential, op.cell_origins[:k], deg,
+                                                prob.mesh.spacing, threads)
+        h = CO.reference_zeros(st.hx)
         t0 = time.perf_counter()
-        CO.cellop_apply(deg, prob.mesh.spacing, "h", op._lb[sel], op._rib[sel], op.cell_color[sel],
-                        vq, CO.matrix_meta(st.x), CO.matrix_meta(st.hx), st.x.col_strides,
+        CO.cellop_apply(deg, prob.mesh.spacing, "h", op._lb[:k], op._rib[:k], op.cell_color[:k],
+                        vq_cache[k], CO.matrix_meta(st.x), CO.matrix_meta(st.hx), st.x.col_strides,
                         st.x.col_blocks.sizes, x, h, threads=threads)
+        return time.perf_counter() - t0, h
+
+    holder = {}
+
+    def products():
+        h_full = holder["h"]  # H X of the sampled cells (the loops' work is value-independent)
+        t0 = time.perf_counter()
+        CO.tmmult(st.x, st.hx, st.s, x, h_full, threads=threads)
+        CO.mmult(st.x, st.c, st.xc, x, c_vals, threads=threads)
         return time.perf_counter() - t0
 
-    t_probe = run_cells(probe)
+    # sample size: about 2 s of H X per step on this host
+    probe = max(1, min(n_cells, 256))
+    t_probe, holder["h"] = hx_cells(probe)
     k = int(min(n_cells, max(probe, probe * 2.0 / max(t_probe, 1e-6))))
     frac = k / max(n_cells, 1)
     for _ in range(args.warmup):
-        run_cells(k)
-    times = [run_cells(k) for _ in range(args.steps)]
-    t_step = float(np.mean(times)) / frac  # extrapolated full-step H X time
-    # S and X C (< 6 % of the step's flops) are not timed on the CPU: counting their
-    # flops over the H X time alone favours the reference arm
+        _, holder["h"] = hx_cells(k)
+        products()
+    times = []
+    for _ in range(args.steps):
+        t_h, holder["h"] = hx_cells(k)
+        times.append(t_h / frac + products())
+    t_step = float(np.mean(times))  # H X extrapolated by cells + S and X C timed in full
     value = f_total / t_step / 1e9
     line = {
         "metric": "matrix-free sparse SpMM fp64 GFlop/s (algorithmic) at N B200",
         "impl": "reference", "value": round(value, 3), "unit": "GFlop/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded splitmix64 fill, SURVEY 0.1)",
-        "config": {"workload": name, "note": prob.cfg.note},
+        "data": "synthetic (seeded splitmix64 fill, Gaussian potential; SURVEY 0.1)",
+        "config": bench_config(name, prob, st),
         "cpu_baseline": {"value": round(value, 3), "unit": "GFlop/s", "cores": threads,
                          "kind": "port",
                          "sample": f"H X over the first {k} of {n_cells} Hilbert-ordered cells "
-                                   f"({frac:.3f} of the workload) per step, C restatement of "
-                                   f"Algorithm 6 (oracle/cellop.c), time extrapolated by cells"},
+                                   f"({frac:.3f} of the workload, time extrapolated by cells) + "
+                                   f"S = X^T (H X) and X C on the whole workload per step; C "
+                                   f"restatement of the reference loops (oracle/cellop.c)"},
         "e2e": {"value": round(value, 3), "unit": "GFlop/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -365,7 +391,8 @@ def main():
 
     f_step = sum_over_ranks(cnt["flops_hx"] + cnt["flops_s"] + cnt["flops_xc"])
     value = f_step / (ms * 1e-3) / 1e9
-    peak_fp64 = measure_fp64_peak(torch, lib, C, dev)
+    peak_dfma, peak_dmma = measure_fp64_peak(torch, lib, C, dev)
+    peak_fp64 = max(peak_dfma, peak_dmma)
     k1_tflops = cnt["flops_hx"] / (ms_k1 * 1e-3) / 1e12
     traffic = None
     tp = ROOT / "profiles" / "k1_traffic.json"
@@ -453,19 +480,19 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded splitmix64 fill, Gaussian potential; SURVEY 0.1)",
-            "config": {"workload": name, "note": prob.cfg.note,
-                       "step": "apply H (halo) + tmmult S=X^T(HX) (compress) + mmult XC",
-                       "l2": "inputs larger than L2 (X stored %.2f GB)" % (st.x.data.numel() * 8e-9),
-                       "scatter": os.environ.get("BMV_SCATTER", "atomic")},
+            "config": bench_config(name, prob, st),
             "dof_vectors_per_s": round(sum_over_ranks(cnt["nnzX"]) / (ms_apply * 1e-3), 1),
             "kernels_ms": {"k1_cellop": round(ms_k1, 4), "apply_total": round(ms_apply, 4),
                            "tmmult": round(ms_tm, 4), "mmult": round(ms_mm, 4)},
             "work": {k: (int(sum_over_ranks(v)) if isinstance(v, int) else v) for k, v in cnt.items()},
-            "roofline": {"bound": "fp64", "kernel": "K1 cellop (bmv_cellop_tma.cu, cellop_tma_kernel<5>)",
+            "roofline": {"bound": "fp64", "kernel": "K1 cellop (csrc/bmv_k1.cu, k1_plane_kernel<%d>)"
+                         % (prob.cfg.degree + 1),
                          "achieved": round(k1_tflops, 3), "peak": round(peak_fp64, 3),
                          "unit": "TFLOP/s", "frac": round(k1_tflops / peak_fp64, 4),
-                         "peak_source": "measured in-run: bmv_fp64_peak_kernel (independent DFMA "
-                                        "chains); MEASURED_PEAKS.json has no FP64 figure",
+                         "frac_vs_dfma": round(k1_tflops / peak_dfma, 4),
+                         "peak_source": "measured in-run, max of the DFMA probe (%.2f) and the "
+                                        "DMMA probe (%.2f TFLOP/s); MEASURED_PEAKS.json has no "
+                                        "FP64 figure" % (peak_dfma, peak_dmma),
                          "hbm_bytes_algorithmic": cnt["bytes_hx"],
                          "hbm_frac_at_k1_time": round(cnt["bytes_hx"] / (ms_k1 * 1e-3) / 1e9
                                                       / float(peaks.get("hbm_gbs", 6650.0)), 4),
@@ -484,23 +511,23 @@ def main():
 
 
 def spmm_roofline(st, cnt, ms_tm, ms_mm, hbm_gbs, sum_over_ranks):
-    """K4 / K5 are HBM-bound: the BCSR layout streams whole stored blocks
-    (X + HX for K4; X read + X C written for K5), so the achieved bandwidth
-    is measured on the stored bytes; `algorithmic_frac` uses the nnz bytes of
-    SURVEY 8(d) (8 (nnzX + nnzHX) and 16 nnzX), a bound no padded-block
-    layout can reach."""
+    """K4 / K5 are HBM-bound.  `achieved` = algorithmic bytes (SURVEY 8(d):
+    8 (nnzX + nnzHX) for K4, 16 nnzX for K5) per launch / time; `stored_*`
+    gives the same on the slab bytes the kernels actually stream (X + H X
+    for K4; X read + X C written for K5)."""
     out = {}
     for name, ms, stored, alg in (
-            ("k4_tmmult", ms_tm, 8 * (st.x.data.numel() + st.hx.data.numel() + st.s.data.numel()),
+            ("k4_tmmult", ms_tm, 8 * (st.x.n_owned_values + st.hx.n_owned_values),
              cnt["bytes_s"]),
-            ("k5_mmult", ms_mm, 8 * (st.x.data.numel() + st.xc.data.numel()), cnt["bytes_xc"])):
+            ("k5_mmult", ms_mm, 8 * (st.x.n_owned_values + st.xc.n_owned_values),
+             cnt["bytes_xc"])):
         stored = sum_over_ranks(stored)
         alg = sum_over_ranks(alg)
-        gbs = stored / (ms * 1e-3) / 1e9
+        gbs = alg / (ms * 1e-3) / 1e9
         out[name] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_gbs, "unit": "GB/s",
-                     "frac": round(gbs / hbm_gbs, 4), "bytes_per_launch": int(stored),
-                     "algorithmic_bytes": int(alg),
-                     "algorithmic_frac": round(alg / (ms * 1e-3) / 1e9 / hbm_gbs, 4),
+                     "frac": round(gbs / hbm_gbs, 4), "algorithmic_bytes": int(alg),
+                     "stored_bytes": int(stored),
+                     "stored_frac": round(stored / (ms * 1e-3) / 1e9 / hbm_gbs, 4),
                      "ms": round(ms, 4)}
     return out
 
@@ -518,20 +545,24 @@ def cpu_baseline_leg(st, prob, cnt):
     """C restatement of the reference cell loop on a bounded sample (rank 0, N = 1)."""
     try:
         from oracle import c_oracle as CO
-        from oracle import numpy_oracle as NO
     except Exception as exc:  # pragma: no cover
         return {"value": None, "error": repr(exc)}
     op = st.op
     deg = prob.cfg.degree
     n_cells = len(op.cells)
     threads = os.cpu_count() or 1
-    x = st.x.data.cpu().numpy()
-    h = np.zeros(st.hx.data.numel())
-    xm = (st.x.row_start, st.x.col_index, st.x.block_offsets)
-    hm = (st.hx.row_start, st.hx.col_index, st.hx.block_offsets)
+    x = CO.reference_values(st.x)
+    h = CO.reference_zeros(st.hx)
+    xm, hm = CO.matrix_meta(st.x), CO.matrix_meta(st.hx)
+
+    # V at the points from the operator's coefficient (timing only: the parity of
+    # the potential is tested in tests/test_gpu_fullsize.py against the numpy oracle)
+    coef, stride = op.coefficient(prob.spec_h(), st.x.device)
+    w3 = op.kernels.w3.ravel()
+    vq_all = coef.view(-1, stride)[:, : w3.size].cpu().numpy() / w3[None, :]
 
     def run(k):
-        vq = NO.sample_potential(prob.potential, op.cell_origins[:k], deg, prob.mesh.spacing)
+        vq = vq_all[:k]
         t0 = time.perf_counter()
         CO.cellop_apply(deg, prob.mesh.spacing, "h", op._lb[:k], op._rib[:k], op.cell_color[:k], vq,
                         xm, hm, st.x.col_strides, st.x.col_blocks.sizes, x, h, threads=threads)

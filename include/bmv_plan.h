@@ -9,14 +9,18 @@
  *   bmvp_hash_fill            bench/problem.py:113-131 fill_multivector (splitmix64
  *                             `_mix64` hash of (seed, row, original column)); here the
  *                             per-entry form used by problem.fill_multivector
- *   bmvp_owned_entries_*      bcsr.py:233-318 block storage offsets of the support
- *                             entries of a multivector (ColumnSupport.owned_entries)
+ *   bmvp_owned_entries_*      bcsr.py:233-318 storage offsets of the support entries of
+ *                             a multivector (ColumnSupport.owned_entries; slab layout)
+ *   bmvp_support_columns_*    bcsr.py:233-318 which columns a block row stores (the
+ *                             slab columns of a support-declared multivector)
  *   bmvp_blocks_of            bcsr.py:126-152 map_rows (row -> (block, row in block))
  *   bmvp_first_touch          mesh.py:263-322 enumerate_dofs (first-touch positions)
  *   bmvp_grow_*               localization.py:251-267 grow_sparsity_for_operator
  *                             (block pattern inc^T (inc S) + S)
  *   bmvp_first_groups_*       matfree.py:90-116 build_cell_dof_map: per-cell grouping of
  *                             DoFs by row block in first-occurrence order
+ *   bmvp_chunk_*              bcsr.py:587-667 tmmult / mmult block loops: the K4 / K5
+ *                             chunk plans (union columns, colmaps, output slots)
  */
 #ifndef BMV_PLAN_H
 #define BMV_PLAN_H
@@ -48,15 +52,29 @@ int bmvp_owned_entries_count(int64_t n_cols, const int64_t* col_ptr, const int64
 /* Column-major (column, then row) support entries of the owned rows: storage
  * offset, global row, column.  out_start[c] = exclusive prefix sum of col_count.
  * block_starts: global first row of the nb_own owned block rows (+ end);
- * cb_starts: first column of each of n_cb column blocks (+ end); row_start /
- * col_index / block_offsets: the matrix's block CSR (col_index ascending per row). */
+ * slab_ptr / slab_cols / slab_off: the matrix's slab geometry over its owned
+ * block rows (stored columns ascending per row, slab offsets; slabs.py).
+ * Returns 3 if a support entry has no stored slot. */
 int bmvp_owned_entries_fill(int64_t n_cols, const int64_t* col_ptr, const int64_t* col_rows,
                             int64_t lo, int64_t hi, const int64_t* out_start,
                             int64_t nb_own, const int64_t* block_starts,
-                            int64_t n_cb, const int64_t* cb_starts,
-                            const int64_t* row_start, const int64_t* col_index,
-                            const int64_t* block_offsets, const int64_t* col_strides,
-                            int64_t* flat, int64_t* rows, int64_t* cols);
+                            const int64_t* slab_ptr, const int64_t* slab_cols,
+                            const int64_t* slab_off, int64_t* flat, int64_t* rows,
+                            int64_t* cols);
+
+/* Stored columns of selected global block rows from a column support
+ * (ColumnSupport.columns_for): column c is stored in block row g when one of
+ * its support rows lies in [block_starts[g], block_starts[g+1]).
+ * block_sel[g] = index of g among the n_sel selected rows, -1 otherwise.
+ * count: counts[s] = columns of selected row s.  fill: ptr = exclusive prefix
+ * sum of counts (n_sel + 1), cursor scratch (n_sel); cols ascending per row. */
+int bmvp_support_columns_count(int64_t n_cols, const int64_t* col_ptr, const int64_t* col_rows,
+                               int64_t n_blocks, const int64_t* block_starts,
+                               const int64_t* block_sel, int64_t n_sel, int64_t* counts);
+int bmvp_support_columns_fill(int64_t n_cols, const int64_t* col_ptr, const int64_t* col_rows,
+                              int64_t n_blocks, const int64_t* block_starts,
+                              const int64_t* block_sel, int64_t n_sel, const int64_t* ptr,
+                              int64_t* cursor, int64_t* cols);
 
 /* lb: (n_cells, n3) local block of every cell DoF.  slot_group (n_cells, n3):
  * group index of each DoF inside its cell, groups in first-occurrence order;
@@ -83,6 +101,31 @@ int bmvp_grow_count(int64_t n_cells, int32_t n3, const int64_t* cell_rb, int64_t
 /* Sorted column indices of every row from the bitsets; row_start = prefix sum of row_count. */
 int bmvp_grow_fill(int64_t n_rb, int64_t n_cb, const uint64_t* bits, const int64_t* row_start,
                    int64_t* col_index);
+
+/* K4 / K5 chunk plan (include/bmv.h bmv_chunk_desc), replacing the block
+ * loops of reference tmmult / mmult (bcsr.py:587-667).  Owned block rows
+ * 0..n_rows-1 of A with rows[i] rows; slab geometry (ptr, cols, off) of A,
+ * of B (K4: the second factor, staged; K5: the output Y), and of M (K4: the
+ * output S; K5: the factor C) over M's local block rows; M row of A column
+ * col: local block m_ltab[cb] of A's column block cb (acb_starts), row
+ * col - acb_starts[cb].  Chunks: <= max_rows rows, <= max_brows block rows,
+ * <= data_bytes of staged values, meta + values <= stage_bytes; n_parts
+ * contiguous chunk ranges of equal estimated cost.  bmvp_chunk_status: 0
+ * ok, 1 invalid arguments, 3 M lacks a block row (PatternError), 4 a row
+ * does not fit a stage, 5 offsets beyond 2^31. */
+typedef struct bmvp_chunks bmvp_chunks;
+bmvp_chunks* bmvp_chunk_plan(int32_t kind, int64_t n_rows, const int64_t* rows,
+                             const int64_t* a_ptr, const int64_t* a_cols, const int64_t* a_off,
+                             const int64_t* b_ptr, const int64_t* b_cols, const int64_t* b_off,
+                             int64_t n_acb, const int64_t* acb_starts, const int64_t* m_ltab,
+                             const int64_t* m_ptr, const int64_t* m_cols, const int64_t* m_off,
+                             int32_t max_rows, int32_t max_brows, int32_t data_bytes,
+                             int32_t stage_bytes, int32_t n_parts);
+int bmvp_chunk_status(const bmvp_chunks* c);
+void bmvp_chunk_sizes(const bmvp_chunks* c, int64_t* n_chunks, int64_t* meta_len, int64_t* dmma);
+void bmvp_chunk_copy(const bmvp_chunks* c, int64_t* part_start, int64_t* chunk_meta, int32_t* meta,
+                     int64_t* chunk_a, int64_t* chunk_b);
+void bmvp_chunk_free(bmvp_chunks* c);
 
 #ifdef __cplusplus
 }

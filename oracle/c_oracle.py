@@ -35,6 +35,7 @@ def load():
         _lib.oracle_cellop_apply.restype = C.c_int
         _lib.oracle_tmmult.restype = C.c_int
         _lib.oracle_mmult.restype = C.c_int
+        _lib.oracle_potential_gaussian.restype = C.c_int
     return _lib
 
 
@@ -89,6 +90,110 @@ def cellop_apply(degree, spacing, kind, cell_lb, cell_rib, cell_color, vq, x_met
     return threads
 
 
+def reference_offsets(m):
+    """Block offsets of a BlockCsrMatrix's blocks in the reference layout
+    (rows x padded stride per block, owned then ghost; reference bcsr.py:233-318)."""
+    sizes = m.local_row_sizes[m.pos_row] * m.col_strides[m.col_index]
+    return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+
 def matrix_meta(m):
-    """(row_start, col_index, block_offsets) host arrays of a BlockCsrMatrix."""
-    return m.row_start, m.col_index, m.block_offsets
+    """(row_start, col_index, block_offsets) of a BlockCsrMatrix in the
+    reference's BCSR layout -- the layout the C restatement runs on."""
+    return m.row_start, m.col_index, reference_offsets(m)
+
+
+def reference_values(m) -> np.ndarray:
+    """Values of a BlockCsrMatrix in the reference layout (through the public
+    value_bytes, which converts from the B200 slab layout)."""
+    from paper_1907_01005_b200.bcsr import value_bytes
+
+    return np.frombuffer(value_bytes(m), dtype="<f8").astype(np.float64)
+
+
+def reference_zeros(m) -> np.ndarray:
+    return np.zeros(int(reference_offsets(m)[-1]))
+
+
+def load_reference(m, values: np.ndarray):
+    """Write reference-layout values into a BlockCsrMatrix (load_value_bytes)."""
+    from paper_1907_01005_b200.bcsr import load_value_bytes
+
+    load_value_bytes(m, np.ascontiguousarray(values, dtype="<f8").tobytes())
+
+
+def _ltab(layout, n_global):
+    tab = np.full(n_global, -1, dtype=np.int64)
+    gl = layout.global_blocks_of_locals()
+    tab[gl] = np.arange(gl.size, dtype=np.int64)
+    return tab
+
+
+def tmmult(a, b, c, a_vals, b_vals, threads=None):
+    """C = A^T B over the owned rows of a (reference tmmult loop, bcsr.py:631-667,
+    before the compress), all arrays in the reference layout; returns c's values."""
+    lib = load()
+    n = a.n_owned_blocks
+    out = reference_zeros(c)
+    ar, ac, ao = (_i64(v) for v in matrix_meta(a))
+    br, bc, bo = (_i64(v) for v in matrix_meta(b))
+    cr, cc, co = (_i64(v) for v in matrix_meta(c))
+    cl = _i64(_ltab(c.layout, c.layout.blocks.n_blocks))
+    rows = _i64(a.local_row_sizes)
+    av = np.ascontiguousarray(a_vals, dtype=np.float64)
+    bv = np.ascontiguousarray(b_vals, dtype=np.float64)
+    rc = lib.oracle_tmmult(
+        C.c_int64(n), _p(ar, C.c_int64), _p(ac, C.c_int64), _p(ao, C.c_int64),
+        _p(_i64(a.col_strides), C.c_int64), _p(_i64(a.col_blocks.sizes), C.c_int64),
+        _p(rows, C.c_int64), _p(av, C.c_double), _p(br, C.c_int64), _p(bc, C.c_int64),
+        _p(bo, C.c_int64), _p(_i64(b.col_strides), C.c_int64),
+        _p(_i64(b.col_blocks.sizes), C.c_int64), _p(bv, C.c_double), _p(cl, C.c_int64),
+        _p(cr, C.c_int64), _p(cc, C.c_int64), _p(co, C.c_int64),
+        _p(_i64(c.col_strides), C.c_int64), _p(out, C.c_double), C.c_int64(out.size),
+        C.c_int(int(threads or os.cpu_count() or 1)))
+    if rc == -3:
+        raise LookupError("tmmult destination misses a block (PatternError)")
+    if rc != 0:
+        raise RuntimeError(f"oracle_tmmult failed ({rc})")
+    return out
+
+
+def mmult(a, b, c, a_vals, b_vals, alpha=1.0, threads=None):
+    """C = alpha A B truncated to c's block pattern (reference mmult,
+    bcsr.py:587-628), reference layout; returns c's values (zero start)."""
+    lib = load()
+    n = a.n_owned_blocks
+    out = reference_zeros(c)
+    ar, ac, ao = (_i64(v) for v in matrix_meta(a))
+    br, bc, bo = (_i64(v) for v in matrix_meta(b))
+    cr, cc, co = (_i64(v) for v in matrix_meta(c))
+    bl = _i64(_ltab(b.layout, b.layout.blocks.n_blocks))
+    rows = _i64(a.local_row_sizes)
+    av = np.ascontiguousarray(a_vals, dtype=np.float64)
+    bv = np.ascontiguousarray(b_vals, dtype=np.float64)
+    rc = lib.oracle_mmult(
+        C.c_int64(n), _p(ar, C.c_int64), _p(ac, C.c_int64), _p(ao, C.c_int64),
+        _p(_i64(a.col_strides), C.c_int64), _p(_i64(a.col_blocks.sizes), C.c_int64),
+        _p(rows, C.c_int64), _p(av, C.c_double), _p(bl, C.c_int64), _p(br, C.c_int64),
+        _p(bc, C.c_int64), _p(bo, C.c_int64), _p(_i64(b.col_strides), C.c_int64),
+        _p(_i64(b.col_blocks.sizes), C.c_int64), _p(bv, C.c_double), _p(cr, C.c_int64),
+        _p(cc, C.c_int64), _p(co, C.c_int64), _p(out, C.c_double), C.c_double(alpha),
+        C.c_int(int(threads or os.cpu_count() or 1)))
+    if rc != 0:
+        raise RuntimeError(f"oracle_mmult failed ({rc})")
+    return out
+
+
+def potential_gaussian(pot, cell_origins, degree, spacing, threads=None) -> np.ndarray:
+    """(n_cells, q^3) V of a GaussianPotential at the cell quadrature points (C, OpenMP)."""
+    lib = load()
+    qo = np.ascontiguousarray(NO.quad_offsets(degree, spacing), dtype=np.float64)
+    org = np.ascontiguousarray(cell_origins, dtype=np.float64)
+    cen = np.ascontiguousarray(pot.centers, dtype=np.float64)
+    out = np.empty((org.shape[0], qo.shape[0]))
+    lib.oracle_potential_gaussian(C.c_int64(org.shape[0]), C.c_int(qo.shape[0]),
+                                  _p(org, C.c_double), _p(qo, C.c_double), _p(cen, C.c_double),
+                                  C.c_int(cen.shape[0]), C.c_double(pot.inv_sigma2),
+                                  C.c_double(pot.scale), _p(out, C.c_double),
+                                  C.c_int(int(threads or os.cpu_count() or 1)))
+    return out

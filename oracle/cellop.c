@@ -22,6 +22,7 @@
  * Built by oracle/Makefile into oracle/liboracle.so.
  */
 #include <stdint.h>
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
@@ -329,6 +330,32 @@ int oracle_mmult(int64_t n_rows, const int64_t* a_row_start, const int64_t* a_co
             Cb[rr * sb + jj] += alpha * acc;
           }
       }
+    }
+  }
+  return 0;
+}
+
+/* V(x) = scale * sum_k exp(-|x - c_k|^2 * inv_s2) at x = origins[c] + qoff[q]
+   (the BASELINE Gaussian-sum potential, matfree.py:35-40 sampled at the
+   quadrature points as in matfree.py:491-495); out[c * q3 + q]. */
+int oracle_potential_gaussian(int64_t n_cells, int q3, const double* origins, const double* qoff,
+                              const double* centers, int n_centers, double inv_s2, double scale,
+                              double* out, int n_threads) {
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#endif
+#pragma omp parallel for schedule(static)
+  for (int64_t c = 0; c < n_cells; ++c) {
+    for (int q = 0; q < q3; ++q) {
+      const double px = origins[3 * c] + qoff[3 * q], py = origins[3 * c + 1] + qoff[3 * q + 1],
+                   pz = origins[3 * c + 2] + qoff[3 * q + 2];
+      double v = 0.0;
+      for (int k = 0; k < n_centers; ++k) {
+        const double dx = px - centers[3 * k], dy = py - centers[3 * k + 1],
+                     dz = pz - centers[3 * k + 2];
+        v += exp(-(dx * dx + dy * dy + dz * dz) * inv_s2);
+      }
+      out[c * q3 + q] = scale * v;
     }
   }
   return 0;

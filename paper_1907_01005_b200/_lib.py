@@ -32,58 +32,20 @@ _u64p = C.POINTER(C.c_uint64)
 
 class CellopDesc(C.Structure):
     _fields_ = [
-        ("n", C.c_int32), ("n_cells", C.c_int32), ("n_visits", C.c_int32),
-        ("n_pairs", C.c_int64), ("n_groups_total", C.c_int64), ("n_colors", C.c_int32),
-        ("color_pair_start", _i64p), ("pair_visit", _i32p), ("pair_lane", _i32p),
-        ("visit_cell", _i32p), ("visit_stride", _i32p), ("visit_goff", _i64p),
-        ("group_xoff", _i64p), ("group_hoff", _i64p), ("cell_slots", _u32p),
+        ("n", C.c_int32), ("wide", C.c_int32), ("n_cells", C.c_int32),
+        ("code_stride", C.c_int32), ("max_groups", C.c_int32), ("n_pairs", C.c_int64),
+        ("gtab_len", C.c_int64), ("pair_cell", _i32p), ("pair_gtab", _i64p),
+        ("pair_ngp", _i32p), ("gtab", _i32p), ("codes", _u32p),
         ("S", C.c_double * (MAX_NODES * MAX_NODES)), ("Dco", C.c_double * (MAX_NODES * MAX_NODES)),
         ("w", C.c_double * MAX_NODES), ("kin", C.c_double * 3), ("det", C.c_double),
     ]
 
 
-class TmmultDesc(C.Structure):
+class ChunkDesc(C.Structure):
     _fields_ = [
-        ("n_parts", C.c_int32), ("n_warps", C.c_int32), ("slots_per_warp", C.c_int32),
-        ("stage_bytes", C.c_int32), ("n_sub", C.c_int64), ("n_items", C.c_int64),
-        ("n_entries", C.c_int64), ("meta_len", C.c_int64), ("n_out_tiles", C.c_int64),
-        ("n_src", C.c_int64), ("part_sub_start", _i64p), ("part_entry_start", _i64p),
-        ("copies", _i32p), ("meta", _i32p), ("tile_off", _i64p), ("tile_shape", _i32p),
-        ("tile_src_start", _i64p), ("tile_src", _i64p),
-    ]
-
-
-class MmultDesc(C.Structure):
-    _fields_ = [
-        ("n_parts", C.c_int32), ("stage_bytes", C.c_int32), ("n_sub", C.c_int64),
-        ("n_entries", C.c_int64), ("meta_len", C.c_int64), ("part_sub_start", _i64p),
-        ("part_entry_start", _i64p), ("copies", _i32p), ("meta", _i32p),
-    ]
-
-
-class TmmultLaneDesc(C.Structure):
-    _fields_ = [
-        ("n_rows", C.c_int32), ("row_rows", _i32p), ("a_row_start", _i64p), ("a_off", _i64p),
-        ("a_stride", _i32p), ("a_mask", _u64p), ("b_row_start", _i64p), ("b_off", _i64p),
-        ("b_stride", _i32p), ("b_width", _i32p), ("c_off", _i64p), ("c_stride", _i32p),
-        ("c_rows", _i32p),
-    ]
-
-
-class MmultLaneDesc(C.Structure):
-    _fields_ = [
-        ("n_rows", C.c_int32), ("row_rows", _i32p), ("a_row_start", _i64p), ("a_off", _i64p),
-        ("a_stride", _i32p), ("a_mask", _u64p), ("c_row_start", _i64p), ("c_off", _i64p),
-        ("c_stride", _i32p), ("c_width", _i32p), ("b_pair_start", _i64p), ("b_off", _i64p),
-        ("b_stride", _i32p),
-    ]
-
-
-class LaneHost(C.Structure):
-    _fields_ = [
-        ("stage_bytes", C.c_int32), ("n_parts", C.c_int32), ("meta_len", C.c_int64),
-        ("n_entries", C.c_int64), ("meta", _i32p), ("copies", _i32p),
-        ("part_sub_start", _i64p), ("part_entry_start", _i64p),
+        ("kind", C.c_int32), ("n_parts", C.c_int32), ("stage_bytes", C.c_int32),
+        ("n_chunks", C.c_int64), ("meta_len", C.c_int64), ("part_chunk_start", _i64p),
+        ("chunk_meta", _i64p), ("meta", _i32p), ("chunk_a", _i64p), ("chunk_b", _i64p),
     ]
 
 
@@ -106,25 +68,13 @@ SIGNATURES = [
     ("bmv_cellop_apply_hm", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
       C.c_int64, C.c_void_p]),
-    ("bmv_tmmult_create", C.c_int, [C.POINTER(TmmultDesc), C.POINTER(C.c_void_p)]),
-    ("bmv_tmmult_destroy", C.c_int, [C.c_void_p]),
+    ("bmv_chunk_plan_create", C.c_int, [C.POINTER(ChunkDesc), C.POINTER(C.c_void_p)]),
+    ("bmv_chunk_plan_destroy", C.c_int, [C.c_void_p]),
     ("bmv_tmmult_run", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
-    ("bmv_mmult_create", C.c_int, [C.POINTER(MmultDesc), C.POINTER(C.c_void_p)]),
-    ("bmv_mmult_destroy", C.c_int, [C.c_void_p]),
     ("bmv_mmult_run", C.c_int,
-     [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_int64,
-      C.c_void_p]),
-    ("bmv_tmmult_lane_create", C.c_int, [C.POINTER(TmmultLaneDesc), C.POINTER(C.c_void_p)]),
-    ("bmv_tmmult_lane_run", C.c_int,
-     [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
-    ("bmv_mmult_lane_create", C.c_int, [C.POINTER(MmultLaneDesc), C.POINTER(C.c_void_p)]),
-    ("bmv_mmult_lane_run", C.c_int,
-     [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_int64,
-      C.c_void_p]),
-    ("bmv_lane_plan_destroy", C.c_int, [C.c_void_p]),
-    ("bmv_lane_plan_host", C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.POINTER(LaneHost)]),
-    ("bmv_lane_host_free", C.c_int, [C.POINTER(LaneHost)]),
+     [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_void_p]),
+    ("bmv_chunk_kernel_config", C.c_int, [_i32p, _i32p]),
     ("bmv_index_create", C.c_int, [_i64p, C.c_int64, C.POINTER(C.c_void_p)]),
     ("bmv_index_destroy", C.c_int, [C.c_void_p]),
     ("bmv_index_size", C.c_int64, [C.c_void_p]),
@@ -132,6 +82,8 @@ SIGNATURES = [
     ("bmv_scatter", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     ("bmv_zero", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
     ("bmv_fp64_peak_kernel", C.c_int,
+     [C.c_void_p, C.c_int32, C.c_int32, _f64p, C.c_void_p]),
+    ("bmv_fp64_dmma_peak_kernel", C.c_int,
      [C.c_void_p, C.c_int32, C.c_int32, _f64p, C.c_void_p]),
 ]
 

@@ -45,8 +45,12 @@ def load():
         lib.bmvp_owned_entries_count.argtypes = [C.c_int64, _i64p, _i64p, C.c_int64, C.c_int64,
                                                  _i64p]
         lib.bmvp_owned_entries_fill.argtypes = [C.c_int64, _i64p, _i64p, C.c_int64, C.c_int64,
-                                                _i64p, C.c_int64, _i64p, C.c_int64, _i64p, _i64p,
-                                                _i64p, _i64p, _i64p, _i64p, _i64p, _i64p]
+                                                _i64p, C.c_int64, _i64p, _i64p, _i64p, _i64p,
+                                                _i64p, _i64p, _i64p]
+        lib.bmvp_support_columns_count.argtypes = [C.c_int64, _i64p, _i64p, C.c_int64, _i64p,
+                                                   _i64p, C.c_int64, _i64p]
+        lib.bmvp_support_columns_fill.argtypes = [C.c_int64, _i64p, _i64p, C.c_int64, _i64p,
+                                                  _i64p, C.c_int64, _i64p, _i64p, _i64p]
         lib.bmvp_first_groups_count.argtypes = [C.c_int64, C.c_int32, _i64p, _i64p, _i64p]
         lib.bmvp_first_groups_fill.argtypes = [C.c_int64, C.c_int32, _i64p, _i64p, _i64p, _i64p,
                                                _i64p]
@@ -54,7 +58,22 @@ def load():
                                          _i64p, _i64p, _u64p, _i64p]
         lib.bmvp_grow_fill.argtypes = [C.c_int64, C.c_int64, _u64p, _i64p, _i64p]
         lib.bmvp_first_touch.argtypes = [C.c_int64, C.c_int64, _i64p, _i64p]
+        lib.bmvp_chunk_plan.restype = C.c_void_p
+        lib.bmvp_chunk_plan.argtypes = [C.c_int32, C.c_int64, _i64p, _i64p, _i64p, _i64p, _i64p,
+                                        _i64p, _i64p, C.c_int64, _i64p, _i64p, _i64p, _i64p,
+                                        _i64p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32]
+        lib.bmvp_chunk_status.argtypes = [C.c_void_p]
+        lib.bmvp_chunk_status.restype = C.c_int
+        lib.bmvp_chunk_sizes.argtypes = [C.c_void_p, _i64p, _i64p, _i64p]
+        lib.bmvp_chunk_sizes.restype = None
+        lib.bmvp_chunk_copy.argtypes = [C.c_void_p, _i64p, _i64p, C.POINTER(C.c_int32), _i64p,
+                                        _i64p]
+        lib.bmvp_chunk_copy.restype = None
+        lib.bmvp_chunk_free.argtypes = [C.c_void_p]
+        lib.bmvp_chunk_free.restype = None
         for f in ("bmvp_first_touch", "bmvp_grow_count", "bmvp_grow_fill", "bmvp_hash_fill", "bmvp_blocks_of", "bmvp_owned_entries_count", "bmvp_owned_entries_fill",
+                  "bmvp_support_columns_count", "bmvp_support_columns_fill",
                   "bmvp_first_groups_count", "bmvp_first_groups_fill"):
             getattr(lib, f).restype = C.c_int
         _lib = lib
@@ -132,13 +151,35 @@ def owned_entries(support, matrix):
     nb_own = int(layout.n_owned_blocks)
     fb = int(layout.first_block)
     bstarts = _i64(layout.blocks.starts[fb : fb + nb_own + 1])
-    cbs = _i64(matrix.col_blocks.starts)
+    sg = matrix.slab
     _check(lib.bmvp_owned_entries_fill(
         n_cols, _p(col_ptr), _p(col_rows), lo, hi, _p(start), nb_own, _p(bstarts),
-        int(matrix.col_blocks.n_blocks), _p(cbs), _p(_i64(matrix.row_start)),
-        _p(_i64(matrix.col_index)), _p(_i64(matrix.block_offsets)), _p(_i64(matrix.col_strides)),
-        _p(flat), _p(rows), _p(cols)), "bmvp_owned_entries_fill")
+        _p(_i64(sg.ptr)), _p(_i64(sg.cols)), _p(_i64(sg.off)), _p(flat), _p(rows), _p(cols)),
+        "bmvp_owned_entries_fill")
     return flat, rows, cols
+
+
+def support_columns(support, blocks, gblocks):
+    """Native form of ColumnSupport.columns_for: (ptr, cols) over gblocks."""
+    lib = load()
+    col_ptr, col_rows = support.csr()
+    gblocks = _i64(gblocks)
+    n_blocks = int(blocks.n_blocks)
+    sel = np.full(n_blocks, -1, dtype=np.int64)
+    sel[gblocks] = np.arange(gblocks.size, dtype=np.int64)
+    counts = np.empty(gblocks.size, dtype=np.int64)
+    starts = _i64(blocks.starts)
+    _check(lib.bmvp_support_columns_count(support.n_cols, _p(col_ptr), _p(col_rows), n_blocks,
+                                          _p(starts), _p(sel), gblocks.size, _p(counts)),
+           "bmvp_support_columns_count")
+    ptr = np.zeros(gblocks.size + 1, dtype=np.int64)
+    np.cumsum(counts, out=ptr[1:])
+    cols = np.empty(int(ptr[-1]), dtype=np.int64)
+    cursor = np.empty(max(gblocks.size, 1), dtype=np.int64)
+    _check(lib.bmvp_support_columns_fill(support.n_cols, _p(col_ptr), _p(col_rows), n_blocks,
+                                         _p(starts), _p(sel), gblocks.size, _p(ptr), _p(cursor),
+                                         _p(cols)), "bmvp_support_columns_fill")
+    return ptr, cols
 
 
 def first_occurrence_groups(lb: np.ndarray):
@@ -185,3 +226,49 @@ def first_touch(n_nodes: int, touches) -> np.ndarray:
     first = np.empty(n_nodes, dtype=np.int64)
     _check(lib.bmvp_first_touch(n_nodes, touches.size, _p(touches), _p(first)), "bmvp_first_touch")
     return first
+
+
+def chunk_plan(kind: int, rows, a, b, acb_starts, m_ltab, m, max_rows: int, max_brows: int,
+               data_bytes: int, stage_bytes: int, n_parts: int) -> dict:
+    """K4 / K5 chunk plan (bmv.h bmv_chunk_desc) from slab geometries a, b, m
+    (objects with ptr / cols / off arrays).  Returns the descriptor arrays;
+    raises PatternError (M lacks a block row), ShapeError (a row exceeds a
+    stage, offsets beyond 2^31)."""
+    from .errors import PatternError, ShapeError
+
+    lib = load()
+    keep = [_i64(x) for x in (rows, a.ptr, a.cols, a.off, b.ptr, b.cols, b.off, acb_starts,
+                               m_ltab, m.ptr, m.cols, m.off)]
+    h = lib.bmvp_chunk_plan(int(kind), keep[0].size, *[_p(x) for x in keep[:7]],
+                            keep[7].size - 1, *[_p(x) for x in keep[7:]], int(max_rows),
+                            int(max_brows), int(data_bytes), int(stage_bytes), int(n_parts))
+    try:
+        st = lib.bmvp_chunk_status(h)
+        if st == 3:
+            raise PatternError("the product matrix holds no block row for a column block of A")
+        if st == 4:
+            raise ShapeError("a single row of the product does not fit a K4/K5 stage")
+        if st == 5:
+            raise ShapeError("K4/K5 offsets exceed 2^31 elements")
+        if st != 0:
+            raise UsageError(f"bmvp_chunk_plan failed (status {st})")
+        n = C.c_int64()
+        ml = C.c_int64()
+        dm = C.c_int64()
+        lib.bmvp_chunk_sizes(h, C.byref(n), C.byref(ml), C.byref(dm))
+        n_chunks, meta_len = n.value, ml.value
+        out = {
+            "part_chunk_start": np.empty(n_parts + 1, dtype=np.int64),
+            "chunk_meta": np.empty(n_chunks + 1, dtype=np.int64),
+            "meta": np.empty(max(meta_len, 1), dtype=np.int32),
+            "chunk_a": np.empty(max(2 * n_chunks, 1), dtype=np.int64),
+            "chunk_b": np.empty(max(2 * n_chunks, 1), dtype=np.int64) if kind == 4 else None,
+        }
+        lib.bmvp_chunk_copy(h, _p(out["part_chunk_start"]), _p(out["chunk_meta"]),
+                            out["meta"].ctypes.data_as(C.POINTER(C.c_int32)), _p(out["chunk_a"]),
+                            _p(out["chunk_b"]) if kind == 4 else None)
+        out.update(kind=kind, n_chunks=n_chunks, meta_len=meta_len, dmma=dm.value,
+                   n_parts=n_parts, stage_bytes=stage_bytes)
+        return out
+    finally:
+        lib.bmvp_chunk_free(h)

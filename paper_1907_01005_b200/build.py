@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libbmv.so"
 PLAN_LIB = PKG / "libbmvplan.so"
 PLAN_SOURCES = ["bmv_plan.cpp"]
-SOURCES = ["bmv_util.cu", "bmv_cellop.cu", "bmv_cellop_stream.cu", "bmv_cellop_tma.cu", "bmv_project.cu", "bmv_postmul.cu", "bmv_spmm_lane.cu"]
+SOURCES = ["bmv_util.cu", "bmv_misc.cu", "bmv_k1.cu", "bmv_spmm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

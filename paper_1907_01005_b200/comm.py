@@ -179,12 +179,17 @@ class ThreadRankContext(RankContext):
             raise DomainError(f"peer {peer} outside [0, {self.n_ranks})")
         return _Handle(lambda: self._rt.take(self.rank, peer, tag))
 
-    def exchange(self, sends, recvs):
-        """Post all buffer sends, then fill every receive buffer (in place)."""
+    def exchange_start(self, sends, recvs, key=None):
+        """Post all buffer sends; the receives complete in exchange_finish."""
         self._xchg_seq += 1
         tag = ("_xchg", self._xchg_seq)
         for peer, buf in sends:
             self.isend(peer, tag, buf.clone())
+        return (tag, recvs)
+
+    def exchange_finish(self, handle):
+        """Fill every receive buffer (in place); ProtocolError on a size mismatch."""
+        tag, recvs = handle
         for peer, buf in recvs:
             got = self.irecv(peer, tag).wait()
             if got.numel() != buf.numel():
@@ -194,6 +199,9 @@ class ThreadRankContext(RankContext):
                     f"rank {self.rank}: buffer from {peer} has {got.numel()} values, "
                     f"expected {buf.numel()}")
             buf.copy_(got)
+
+    def exchange(self, sends, recvs, key=None):
+        self.exchange_finish(self.exchange_start(sends, recvs, key))
 
 
 def run_ranks(n_ranks, program, *shared, deadlock_timeout=30.0, trace_path=None, device=None):
@@ -271,6 +279,7 @@ class DistContext(RankContext):
         self._obj_group = dist.new_group(backend="gloo") if self.backend != "gloo" else None
         self.device = device
         self._pending = []
+        self._verified = set()
         self._torch = torch
         # the first NCCL call of a group must involve every rank; point-to-point
         # halo exchanges do not, so initialise the communicator collectively here
@@ -314,10 +323,45 @@ class DistContext(RankContext):
                 keep.append(item)
         self._pending = keep
 
-    def exchange(self, sends, recvs):
+    def _verify_sizes(self, sends, recvs, key):
+        """Once per exchange plan (key: matrix id and direction, the same on every
+        rank): all ranks gather every rank's per-peer send / receive sizes and
+        check them pairwise -- ProtocolError instead of an NCCL hang or silent
+        corruption."""
+        if key is None or key in self._verified:
+            return
+        mine = ({int(p): int(b.numel()) for p, b in sends},
+                {int(p): int(b.numel()) for p, b in recvs})
+        tables = [None] * self.n_ranks
+        self._dist.all_gather_object(tables, mine, group=self._obj_group)
+        for p, (their_send, their_recv) in enumerate(tables):
+            if p == self.rank:
+                continue
+            if mine[0].get(p, 0) != their_recv.get(self.rank, 0) or \
+                    mine[1].get(p, 0) != their_send.get(self.rank, 0):
+                from .errors import ProtocolError
+
+                raise ProtocolError(
+                    f"rank {self.rank}: exchange {key} with rank {p}: I send "
+                    f"{mine[0].get(p, 0)} / receive {mine[1].get(p, 0)} values, the peer "
+                    f"receives {their_recv.get(self.rank, 0)} / sends "
+                    f"{their_send.get(self.rank, 0)}")
+        self._verified.add(key)
+
+    def exchange_start(self, sends, recvs, key=None):
+        """Post the NCCL (gloo on CPU) point-to-point sends and receives; the
+        returned works are waited on in exchange_finish, so kernels launched in
+        between overlap the transfer."""
+        self._verify_sizes(sends, recvs, key)
         ops = [self._dist.P2POp(self._dist.isend, buf, peer) for peer, buf in sends]
         ops += [self._dist.P2POp(self._dist.irecv, buf, peer) for peer, buf in recvs]
         if not ops:
-            return
-        for w in self._dist.batch_isend_irecv(ops):
+            return []
+        return self._dist.batch_isend_irecv(ops)
+
+    def exchange_finish(self, works):
+        for w in works:
             w.wait()
+
+    def exchange(self, sends, recvs, key=None):
+        self.exchange_finish(self.exchange_start(sends, recvs, key))

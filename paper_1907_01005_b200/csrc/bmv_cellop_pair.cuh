@@ -1,30 +1,12 @@
-// K1 thread-per-pair kernel for n <= 3 (Q1 / Q2): one thread holds a whole
-// (cell, column) pair's n^3 tensor in registers, so the 12 contractions need
-// no transposes at all.  Included by bmv_cellop_tma.cu (same plan data: pair
-// descriptors, per-visit X / HX element offset rows, padded coefficient rows).
-//
-// Per pair, the thread itself issues cp.async.bulk copies into its warp's
-// shared memory (completion on the warp's mbarrier): the visit's X offset row
-// and the cell's coefficient row; after the gather has consumed the X
-// offsets the HX offset row is copied into the same place (second mbarrier
-// phase) and lands during the arithmetic.  Rows are read back with 16-byte
-// loads at a pitch of an odd number of 16-byte units (conflict-free).
+// K1 thread-per-pair building blocks for n <= 3 (Q1 / Q2): one thread holds
+// a whole (cell, column) pair's n^3 tensor in registers, so the 12
+// contractions need no transposes at all (used by bmv_k1.cu).
 #pragma once
 
 #include "bmv_sumfac.cuh"
 #include "bmv_tma.cuh"
 
 namespace bmv {
-
-template <int N>
-struct PairShape {
-  static constexpr int N3 = N * N * N;
-  static constexpr int SRP = (N3 + 3) / 4 * 4;          // offsets per row (int32)
-  static constexpr int Q3P = (N3 + 1) / 2 * 2;          // coefficients per row (doubles)
-  static constexpr int OU = ((SRP / 4) | 1);            // offset row pitch, 16-byte units (odd)
-  static constexpr int CU = ((Q3P / 2) | 1);            // coefficient row pitch, 16-byte units (odd)
-  static constexpr int warp_bytes = 32 * 16 * (OU + CU);
-};
 
 // out[line](a) = sum_b M[a][b] in[line](b) along axis `ax` of a [z][y][x] tensor
 template <int N, int AX, bool TR>

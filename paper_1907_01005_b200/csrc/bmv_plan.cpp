@@ -88,10 +88,9 @@ int bmvp_owned_entries_count(int64_t n_cols, const int64_t* col_ptr, const int64
 int bmvp_owned_entries_fill(int64_t n_cols, const int64_t* col_ptr, const int64_t* col_rows,
                             int64_t lo, int64_t hi, const int64_t* out_start,
                             int64_t nb_own, const int64_t* block_starts,
-                            int64_t n_cb, const int64_t* cb_starts,
-                            const int64_t* row_start, const int64_t* col_index,
-                            const int64_t* block_offsets, const int64_t* col_strides,
-                            int64_t* flat, int64_t* rows, int64_t* cols) {
+                            const int64_t* slab_ptr, const int64_t* slab_cols,
+                            const int64_t* slab_off, int64_t* flat, int64_t* rows,
+                            int64_t* cols) {
   int bad = 0;
 #pragma omp parallel for schedule(dynamic, 1) reduction(| : bad)
   for (int64_t c = 0; c < n_cols; ++c) {
@@ -100,29 +99,78 @@ int bmvp_owned_entries_fill(int64_t n_cols, const int64_t* col_ptr, const int64_
     const int64_t* e = col_rows + col_ptr[c + 1];
     const int64_t* a = std::lower_bound(b, e, lo);
     const int64_t* z = std::lower_bound(a, e, hi);
-    const int64_t cbk = range_of(cb_starts, n_cb, c);
-    const int64_t cin = c - cb_starts[cbk];
-    const int64_t stride = col_strides[cbk];
     int64_t o = out_start[c];
-    int64_t lb = -1, bend = 0, base = 0, bstart = 0;
+    int64_t lb = -1, bend = 0, base = 0, bstart = 0, width = 0;
     for (const int64_t* p = a; p < z; ++p, ++o) {
       const int64_t r = *p;
       if (r >= bend) {  // next block row holding r (rows ascend within a column)
         lb = range_of(block_starts, nb_own, r);
         bstart = block_starts[lb];
         bend = block_starts[lb + 1];
-        const int64_t* kb = col_index + row_start[lb];
-        const int64_t* ke = col_index + row_start[lb + 1];
-        const int64_t* k = std::lower_bound(kb, ke, cbk);
-        if (k == ke || *k != cbk) { bad = 1; break; }
-        base = block_offsets[row_start[lb] + (k - kb)];
+        const int64_t* kb = slab_cols + slab_ptr[lb];
+        const int64_t* ke = slab_cols + slab_ptr[lb + 1];
+        const int64_t* k = std::lower_bound(kb, ke, c);
+        if (k == ke || *k != c) { bad = 1; break; }
+        width = slab_ptr[lb + 1] - slab_ptr[lb];
+        base = slab_off[lb] + (k - kb);
       }
-      flat[o] = base + (r - bstart) * stride + cin;
+      flat[o] = base + (r - bstart) * width;
       rows[o] = r;
       cols[o] = c;
     }
   }
   return bad ? 3 : 0;
+}
+
+int bmvp_support_columns_count(int64_t n_cols, const int64_t* col_ptr, const int64_t* col_rows,
+                               int64_t n_blocks, const int64_t* block_starts,
+                               const int64_t* block_sel, int64_t n_sel, int64_t* counts) {
+  if (n_cols < 0 || n_blocks < 0 || n_sel < 0) return 1;
+  std::memset(counts, 0, sizeof(int64_t) * (size_t)n_sel);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t c = 0; c < n_cols; ++c) {
+    int64_t bend = -1;
+    for (int64_t i = col_ptr[c]; i < col_ptr[c + 1]; ++i) {
+      const int64_t r = col_rows[i];
+      if (r < bend) continue;
+      const int64_t g = range_of(block_starts, n_blocks, r);
+      bend = block_starts[g + 1];
+      const int64_t s = block_sel[g];
+      if (s >= 0) {
+#pragma omp atomic
+        counts[s] += 1;
+      }
+    }
+  }
+  return 0;
+}
+
+int bmvp_support_columns_fill(int64_t n_cols, const int64_t* col_ptr, const int64_t* col_rows,
+                              int64_t n_blocks, const int64_t* block_starts,
+                              const int64_t* block_sel, int64_t n_sel, const int64_t* ptr,
+                              int64_t* cursor, int64_t* cols) {
+  if (n_cols < 0 || n_blocks < 0 || n_sel < 0) return 1;
+  std::memcpy(cursor, ptr, sizeof(int64_t) * (size_t)n_sel);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t c = 0; c < n_cols; ++c) {
+    int64_t bend = -1;
+    for (int64_t i = col_ptr[c]; i < col_ptr[c + 1]; ++i) {
+      const int64_t r = col_rows[i];
+      if (r < bend) continue;
+      const int64_t g = range_of(block_starts, n_blocks, r);
+      bend = block_starts[g + 1];
+      const int64_t s = block_sel[g];
+      if (s >= 0) {
+        int64_t at;
+#pragma omp atomic capture
+        at = cursor[s]++;
+        cols[at] = c;
+      }
+    }
+  }
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t s = 0; s < n_sel; ++s) std::sort(cols + ptr[s], cols + ptr[s + 1]);
+  return 0;
 }
 
 int bmvp_first_groups_count(int64_t n_cells, int32_t n3, const int64_t* lb,
@@ -237,5 +285,293 @@ int bmvp_grow_fill(int64_t n_rb, int64_t n_cb, const uint64_t* bits, const int64
   }
   return 0;
 }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// K4 / K5 chunk plans (include/bmv.h bmv_chunk_desc): replaces the block
+// loops of reference tmmult / mmult (bcsr.py:587-667) by chunks of
+// consecutive owned rows of A, dense over the union of their stored
+// columns.  See the header for the meta layout.
+
+namespace {
+
+struct SlabView {
+  const int64_t* ptr;    // stored columns per block row (CSR)
+  const int64_t* cols;
+  const int64_t* off;    // slab offsets
+};
+
+inline int64_t width_of(const SlabView& s, int64_t i) { return s.ptr[i + 1] - s.ptr[i]; }
+
+inline int64_t slot_of(const SlabView& s, int64_t i, int64_t col) {
+  const int64_t* b = s.cols + s.ptr[i];
+  const int64_t* e = s.cols + s.ptr[i + 1];
+  const int64_t* k = std::lower_bound(b, e, col);
+  return (k != e && *k == col) ? int64_t(k - b) : -1;
+}
+
+struct Segment {
+  int64_t row;  // block row
+  int64_t r0, r1;
+};
+
+}  // namespace
+
+struct bmvp_chunks {
+  std::vector<int64_t> chunk_meta{0};
+  std::vector<int32_t> meta;
+  std::vector<int64_t> chunk_a, chunk_b;
+  std::vector<int64_t> part_start;
+  std::vector<double> cost;
+  int64_t n_chunks = 0;
+  int64_t dmma = 0;
+  int status = 0;
+};
+
+extern "C" {
+
+bmvp_chunks* bmvp_chunk_plan(int32_t kind, int64_t n_rows, const int64_t* rows,
+                             const int64_t* a_ptr, const int64_t* a_cols, const int64_t* a_off,
+                             const int64_t* b_ptr, const int64_t* b_cols, const int64_t* b_off,
+                             int64_t n_acb, const int64_t* acb_starts, const int64_t* m_ltab,
+                             const int64_t* m_ptr, const int64_t* m_cols, const int64_t* m_off,
+                             int32_t max_rows, int32_t max_brows, int32_t data_bytes,
+                             int32_t stage_bytes, int32_t n_parts) {
+  auto* out = new bmvp_chunks();
+  if ((kind != 4 && kind != 5) || n_rows < 0 || max_rows <= 0 || stage_bytes <= 0 ||
+      n_parts <= 0 || max_brows <= 0 || max_brows > 255) {
+    out->status = 1;
+    return out;
+  }
+  const SlabView A{a_ptr, a_cols, a_off}, B{b_ptr, b_cols, b_off}, M{m_ptr, m_cols, m_off};
+  const bool k4 = kind == 4;
+  // 1. segments -> chunks (greedy over block rows in order)
+  std::vector<std::vector<Segment>> chunks;
+  {
+    std::vector<Segment> cur;
+    int64_t cur_rows = 0, cur_bytes = 0;
+    auto flush = [&]() {
+      if (!cur.empty()) chunks.push_back(cur);
+      cur.clear();
+      cur_rows = cur_bytes = 0;
+    };
+    for (int64_t i = 0; i < n_rows; ++i) {
+      const int64_t R = rows[i];
+      if (R == 0) continue;
+      const int64_t per_row = 8 * (width_of(A, i) + (k4 ? width_of(B, i) : 0));
+      const int64_t bytes = R * per_row;
+      if (R <= max_rows && bytes <= data_bytes) {
+        if (cur_rows + R > max_rows || cur_bytes + bytes > data_bytes ||
+            (int64_t)cur.size() >= max_brows)
+          flush();
+        cur.push_back({i, 0, R});
+        cur_rows += R;
+        cur_bytes += bytes;
+      } else {  // a long block row: balanced row ranges, each its own chunk
+        flush();
+        int64_t lim = max_rows;
+        if (per_row > 0) lim = std::min<int64_t>(lim, std::max<int64_t>(1, data_bytes / per_row));
+        const int64_t np = (R + lim - 1) / lim;
+        for (int64_t p = 0; p < np; ++p) {
+          const int64_t r0 = R * p / np, r1 = R * (p + 1) / np;
+          chunks.push_back({{i, r0, r1}});
+        }
+      }
+    }
+    flush();
+  }
+  // 2. per chunk: meta (split chunks whose stage does not fit)
+  std::vector<int64_t> ua, ub, ka, kb, mk;
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+    const std::vector<Segment>& seg = chunks[ci];
+    const int64_t nbr = (int64_t)seg.size();
+    int64_t nrows = 0;
+    for (const Segment& s : seg) nrows += s.r1 - s.r0;
+    // union columns
+    ua.clear();
+    ub.clear();
+    for (const Segment& s : seg) {
+      ua.insert(ua.end(), A.cols + A.ptr[s.row], A.cols + A.ptr[s.row + 1]);
+      ub.insert(ub.end(), B.cols + B.ptr[s.row], B.cols + B.ptr[s.row + 1]);
+    }
+    std::sort(ua.begin(), ua.end());
+    ua.erase(std::unique(ua.begin(), ua.end()), ua.end());
+    std::sort(ub.begin(), ub.end());
+    ub.erase(std::unique(ub.begin(), ub.end()), ub.end());
+    const int64_t UA = (int64_t)ua.size(), UB = (int64_t)ub.size();
+    // M rows of the union A columns
+    ka.assign(UA, 0);
+    mk.clear();
+    std::vector<int64_t> rb(UA, 0), kk(UA, 0);
+    for (int64_t a = 0; a < UA; ++a) {
+      const int64_t col = ua[a];
+      const int64_t cb = int64_t(std::upper_bound(acb_starts, acb_starts + n_acb + 1, col) -
+                                 acb_starts) - 1;
+      const int64_t lb = m_ltab[cb];
+      if (lb < 0) {
+        out->status = 3;  // M holds no (ghost) block row for this column block
+        return out;
+      }
+      const int64_t r = col - acb_starts[cb];
+      rb[a] = m_off[lb] + r * width_of(M, lb);
+      auto it = std::find(mk.begin(), mk.end(), lb);
+      kk[a] = int64_t(it - mk.begin());
+      if (it == mk.end()) mk.push_back(lb);
+    }
+    const int64_t NK = (int64_t)mk.size();
+    const int64_t tab_w = k4 ? 2 * nrows : nrows;
+    const int64_t yrow_w = k4 ? 0 : nrows;
+    const int64_t cma_w = (nbr * UA + 1) / 2, cmb_w = (nbr * UB + 1) / 2;
+    int64_t words = 16 + tab_w + yrow_w + cma_w + cmb_w + 2 * UA + NK * UB;
+    words = (words + 3) / 4 * 4;
+    // staged ranges (doubles, even bounds)
+    const Segment& s0 = seg.front();
+    const Segment& s1 = seg.back();
+    const int64_t a0 = (a_off[s0.row] + s0.r0 * width_of(A, s0.row)) & ~int64_t(1);
+    int64_t a1 = a_off[s1.row] + s1.r1 * width_of(A, s1.row);
+    a1 = (a1 + 1) & ~int64_t(1);
+    int64_t b0 = 0, b1 = 0;
+    if (k4) {
+      b0 = (b_off[s0.row] + s0.r0 * width_of(B, s0.row)) & ~int64_t(1);
+      b1 = b_off[s1.row] + s1.r1 * width_of(B, s1.row);
+      b1 = (b1 + 1) & ~int64_t(1);
+    }
+    const int64_t total = 4 * words + 8 * (a1 - a0) + 8 * (b1 - b0);
+    if (total > stage_bytes || UA > 32767 || UB > 32767 || nrows > (k4 ? 4096 : 32)) {
+      // split and retry (rows or block rows)
+      if (nbr > 1) {
+        std::vector<Segment> h1(seg.begin(), seg.begin() + nbr / 2), h2(seg.begin() + nbr / 2, seg.end());
+        chunks[ci] = h1;
+        chunks.insert(chunks.begin() + ci + 1, h2);
+        --ci;
+        continue;
+      }
+      if (s0.r1 - s0.r0 > 1) {
+        const int64_t mid = (s0.r0 + s0.r1) / 2;
+        chunks[ci] = {{s0.row, s0.r0, mid}};
+        chunks.insert(chunks.begin() + ci + 1, std::vector<Segment>{{s0.row, mid, s0.r1}});
+        --ci;
+        continue;
+      }
+      out->status = 4;  // one row does not fit a stage
+      return out;
+    }
+    const int64_t base = (int64_t)out->meta.size();
+    out->meta.resize(base + words, 0);
+    int32_t* m = out->meta.data() + base;
+    const int64_t aoff = 4 * words, boff = aoff + 8 * (a1 - a0);
+    int64_t w = 16;
+    m[0] = (int32_t)nrows;
+    m[1] = (int32_t)nbr;
+    m[2] = (int32_t)UA;
+    m[3] = (int32_t)UB;
+    m[4] = (int32_t)NK;
+    m[5] = (int32_t)aoff;
+    m[6] = (int32_t)boff;
+    m[7] = (int32_t)UA;
+    m[8] = (int32_t)UB;
+    m[9] = (int32_t)w;  // row table
+    int64_t row = 0;
+    for (int64_t bi = 0; bi < nbr; ++bi) {
+      const Segment& s = seg[bi];
+      for (int64_t r = s.r0; r < s.r1; ++r, ++row) {
+        const int64_t ar = a_off[s.row] + r * width_of(A, s.row) - a0;
+        if (k4) {
+          const int64_t br = b_off[s.row] + r * width_of(B, s.row) - b0;
+          m[w + 2 * row] = (int32_t)(bi | (ar << 8));
+          m[w + 2 * row + 1] = (int32_t)br;
+        } else {
+          m[w + row] = (int32_t)(bi | (ar << 8));
+        }
+      }
+    }
+    w += tab_w;
+    if (!k4) {
+      m[15] = (int32_t)w;  // Y row offsets
+      row = 0;
+      for (int64_t bi = 0; bi < nbr; ++bi) {
+        const Segment& s = seg[bi];
+        for (int64_t r = s.r0; r < s.r1; ++r, ++row) {
+          const int64_t yo = b_off[s.row] + r * width_of(B, s.row);
+          if (yo > INT32_MAX) {
+            out->status = 5;
+            return out;
+          }
+          m[w + row] = (int32_t)yo;
+        }
+      }
+      w += yrow_w;
+    }
+    m[10] = (int32_t)w;  // A colmap
+    int16_t* cma = reinterpret_cast<int16_t*>(m + w);
+    for (int64_t bi = 0; bi < nbr; ++bi)
+      for (int64_t a = 0; a < UA; ++a) cma[bi * UA + a] = (int16_t)slot_of(A, seg[bi].row, ua[a]);
+    w += cma_w;
+    m[11] = (int32_t)w;  // B / Y colmap
+    int16_t* cmb = reinterpret_cast<int16_t*>(m + w);
+    for (int64_t bi = 0; bi < nbr; ++bi)
+      for (int64_t b = 0; b < UB; ++b) cmb[bi * UB + b] = (int16_t)slot_of(B, seg[bi].row, ub[b]);
+    w += cmb_w;
+    m[12] = (int32_t)w;
+    for (int64_t a = 0; a < UA; ++a) {
+      if (rb[a] > INT32_MAX) {
+        out->status = 5;
+        return out;
+      }
+      m[w + a] = (int32_t)rb[a];
+    }
+    w += UA;
+    m[13] = (int32_t)w;
+    for (int64_t a = 0; a < UA; ++a) m[w + a] = (int32_t)kk[a];
+    w += UA;
+    m[14] = (int32_t)w;
+    for (int64_t k = 0; k < NK; ++k)
+      for (int64_t b = 0; b < UB; ++b) m[w + k * UB + b] = (int32_t)slot_of(M, mk[k], ub[b]);
+    out->chunk_meta.push_back(base + words);
+    out->chunk_a.push_back(a0);
+    out->chunk_a.push_back(a1);
+    if (k4) {
+      out->chunk_b.push_back(b0);
+      out->chunk_b.push_back(b1);
+    }
+    const int64_t ta = (UA + 7) / 8, tb = (UB + 7) / 8;
+    const int64_t dm = k4 ? ta * tb * ((nrows + 3) / 4) : ((UA + 3) / 4) * tb * ((nrows + 7) / 8);
+    out->dmma += dm;
+    out->cost.push_back((double)(8 * (a1 - a0) + 8 * (b1 - b0) + 4 * words) + 32.0 * (double)dm);
+  }
+  out->n_chunks = (int64_t)out->chunk_a.size() / 2;
+  // 3. parts: contiguous chunk ranges of equal estimated cost
+  double tot = 0;
+  for (double c : out->cost) tot += c;
+  out->part_start.assign(n_parts + 1, out->n_chunks);
+  out->part_start[0] = 0;
+  double acc = 0;
+  int p = 1;
+  for (int64_t j = 0; j < out->n_chunks && p < n_parts; ++j) {
+    acc += out->cost[j];
+    while (p < n_parts && acc >= tot * p / n_parts) out->part_start[p++] = j + 1;
+  }
+  return out;
+}
+
+int bmvp_chunk_status(const bmvp_chunks* c) { return c ? c->status : 1; }
+
+void bmvp_chunk_sizes(const bmvp_chunks* c, int64_t* n_chunks, int64_t* meta_len, int64_t* dmma) {
+  *n_chunks = c->n_chunks;
+  *meta_len = (int64_t)c->meta.size();
+  *dmma = c->dmma;
+}
+
+void bmvp_chunk_copy(const bmvp_chunks* c, int64_t* part_start, int64_t* chunk_meta, int32_t* meta,
+                     int64_t* chunk_a, int64_t* chunk_b) {
+  std::copy(c->part_start.begin(), c->part_start.end(), part_start);
+  std::copy(c->chunk_meta.begin(), c->chunk_meta.end(), chunk_meta);
+  std::copy(c->meta.begin(), c->meta.end(), meta);
+  std::copy(c->chunk_a.begin(), c->chunk_a.end(), chunk_a);
+  if (chunk_b) std::copy(c->chunk_b.begin(), c->chunk_b.end(), chunk_b);
+}
+
+void bmvp_chunk_free(bmvp_chunks* c) { delete c; }
 
 }  // extern "C"

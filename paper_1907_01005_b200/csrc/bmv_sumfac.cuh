@@ -139,13 +139,20 @@ struct NoMass {
 // layout (qy = t, [qz][qx]) once the Hamiltonian no longer needs them, after
 // the Hamiltonian result has been handed to HOUT (A layout); it owns the
 // array from then on (the fused mass + Hamiltonian apply).
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// HOOK (optional): called once the coefficient row `cf` has been read by
+// every lane (the caller may then reuse its shared memory).
 template <int N, bool COEF, int CS, class L = Tile<N>, class CP = const double*,
-          class MASS = NoMass, class HOUT = NoMass>
+          class MASS = NoMass, class HOUT = NoMass, class HOOK = NoHook>
 __device__ __forceinline__ void sumfac_h_plane(const double (&u)[N][N], double (&v2)[N][N],
                                                double* buf, int tt, bool lane_ok,
                                                CP cf, const CellTables& tb,
                                                const MASS& mass = MASS(),
-                                               const HOUT& hout = HOUT()) {
+                                               const HOUT& hout = HOUT(),
+                                               const HOOK& hook = HOOK()) {
   double v1[N][N];
   contract_fast<N, false>(u, v1, tb.S);   // x
   contract_slow<N, false>(v1, v2, tb.S);  // y
@@ -168,6 +175,7 @@ __device__ __forceinline__ void sumfac_h_plane(const double (&u)[N][N], double (
 #pragma unroll
       for (int j = 0; j < N; ++j) acc[i][j] = fma(coef_at(cf, CS * (i * N + j)), v1[i][j], acc[i][j]);
   }
+  hook();
   a_to_b<N, L>(acc, v2, buf, tt, lane_ok);  // v2 = acc in B (qy = t): [qz][qx]
   // gx and gz in B layout, applied row/column-wise to limit live registers
   const double wt = tb.w[tt];

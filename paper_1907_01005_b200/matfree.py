@@ -4,21 +4,21 @@ Drop-in for the reference `bcsrmv/matfree.py` (same names and semantics).
 `CellOperator.apply` keeps the reference's contract (`matfree.py:458-527`):
 checks -> dst zeroed -> src ghosts updated -> cell loop -> src ghosts
 released -> dst compressed.  The cell loop itself is one launch of a K1
-kernel over a precomputed plan (the Hamiltonian: csrc/bmv_cellop_tma.cu,
-per-pair operands staged by TMA, thread per pair for n <= 3; the mass
-operator and the deterministic colour mode: csrc/bmv_cellop.cu):
+kernel (csrc/bmv_k1.cu) over a precomputed plan on slab storage (slabs.py):
 
 * per cell: the (group, row-in-block) slot of each of its (p+1)^3 DoFs,
   groups being the distinct local block rows in first-occurrence order
-  (the reference CellDoFMap, `matfree.py:58-130`);
-* per visit (cell, column block C) -- exactly the columns the reference's
-  RowsBlockAccessor emits (`matfree.py:159-237`) -- the element offsets of
-  the (group, C) blocks in src and dst; a dst block missing for any group
-  raises PatternError like `advance_to` (`matfree.py:207-219`);
-* the work list: (visit, lane) pairs.  Without an entry-level support every
-  valid lane of every visit is computed (reference work); with a
-  `ColumnSupport` attached to src only the pairs whose orbital touches the
-  cell are (see support.py).
+  (the reference CellDoFMap, `matfree.py:58-130`), encoded with the row
+  offsets r * K of src and dst;
+* the work list: (cell, column) pairs -- with a ColumnSupport declared on
+  src only the columns whose support reaches the cell (support.py),
+  otherwise every column src stores in the cell's block rows -- and per
+  pair and group the slab positions of the column in src and dst; a column
+  dst does not store raises PatternError like the reference's
+  `advance_to` (`matfree.py:207-219`).
+
+A destination built with `columns=op.image_columns(spec_of_src)`
+(ImageColumns) stores exactly the columns the operator can reach.
 
 The potential is sampled once per (operator, potential) at the cell
 quadrature points (`matfree.py:35-40,491-495`): Gaussian-sum potentials on
@@ -322,123 +322,199 @@ def implemented_flops_per_pair(n: int, kind: str, with_potential: bool) -> int:
 # -- the operator ------------------------------------------------------------------
 
 
-def _scatter_mode() -> str:
-    return os.environ.get("BMV_SCATTER", "atomic")
+def _expand(counts: np.ndarray):
+    counts = np.asarray(counts, dtype=np.int64)
+    owner = np.repeat(np.arange(counts.size, dtype=np.int64), counts)
+    start = np.concatenate([[0], np.cumsum(counts)])[:-1]
+    return owner, np.arange(int(counts.sum()), dtype=np.int64) - start[owner]
+
+
+def _bool_csr(m) -> sparse.csr_matrix:
+    m = m.tocsr()
+    m.sum_duplicates()
+    m.sort_indices()
+    m.data[:] = 1
+    return m
+
+
+class ImageColumns:
+    """Stored columns of an operator image H X (the `columns=` of a
+    destination BlockCsrMatrix, slabs.py).
+
+    Block row i stores column alpha iff some cell touching a row of i has the
+    active pair (cell, alpha), i.e. the pair K1 computes when it applies the
+    operator to a source with stored-column spec `source`: a ColumnSupport
+    (entry level: the cell has a node in supp(alpha)) or any other spec
+    (every stored column of the block rows the cell touches).  Defined per
+    GLOBAL block row (the owner and every ghost copy agree), computed from
+    the cells touching the requested block rows.
+    """
+
+    def __init__(self, op: "CellOperator", source):
+        self.op = op
+        self.source = source
+
+    def key(self):
+        return ("image", id(self.op), id(self.source))
+
+    def columns_for(self, pattern, gblocks: np.ndarray):
+        from .support import ColumnSupport
+
+        op = self.op
+        mesh, numbering = op.mesh, op.numbering
+        blocks = numbering.row_blocks
+        gblocks = np.asarray(gblocks, dtype=np.int64)
+        n_cols = pattern.col_blocks.total
+        cells = op.cells_touching_blocks(gblocks)
+        nodes = cells_nodes(mesh, numbering, cells)  # (nc, n3) global rows
+        nc, n3 = nodes.shape
+        cell_of = np.repeat(np.arange(nc, dtype=np.int64), n3)
+        flat = nodes.ravel()
+        if isinstance(self.source, ColumnSupport):
+            ptr, rows = self.source.csr()
+            # support restricted to the rows these cells touch
+            mark = np.full(numbering.n_dofs, -1, dtype=np.int64)
+            uniq = np.unique(flat)
+            mark[uniq] = np.arange(uniq.size, dtype=np.int64)
+            col_of = np.repeat(np.arange(self.source.n_cols, dtype=np.int64), np.diff(ptr))
+            sel = mark[rows] >= 0
+            xm = sparse.csr_matrix((np.ones(int(sel.sum()), dtype=np.int32),
+                                    (mark[rows[sel]], col_of[sel])), shape=(uniq.size, n_cols))
+            a = sparse.csr_matrix((np.ones(flat.size, dtype=np.int32), (cell_of, mark[flat])),
+                                  shape=(nc, uniq.size))
+            act = _bool_csr(a @ xm)
+        else:
+            gb = blocks.blocks_of(flat)
+            touched = np.unique(gb)
+            sptr, scols = self.source.columns_for(pattern, touched)
+            tpos = np.searchsorted(touched, gb)
+            inc = _bool_csr(sparse.csr_matrix((np.ones(flat.size, dtype=np.int32),
+                                               (cell_of, tpos)), shape=(nc, touched.size)))
+            s = sparse.csr_matrix((np.ones(scols.size, dtype=np.int32), scols, sptr),
+                                  shape=(touched.size, n_cols))
+            act = _bool_csr(inc @ s)
+        # cell -> requested block rows it touches
+        sel = np.full(blocks.n_blocks, -1, dtype=np.int64)
+        sel[gblocks] = np.arange(gblocks.size, dtype=np.int64)
+        sb = sel[blocks.blocks_of(flat)]
+        ok = sb >= 0
+        touch = _bool_csr(sparse.csr_matrix((np.ones(int(ok.sum()), dtype=np.int32),
+                                             (sb[ok], cell_of[ok])), shape=(gblocks.size, nc)))
+        img = _bool_csr(touch @ act)
+        return img.indptr.astype(np.int64), img.indices.astype(np.int64)
 
 
 class _CellPlan:
-    """Device plan of K1 for one (src pattern/support, dst pattern) couple."""
+    """Device plan of K1 (csrc/bmv_k1.cu) for one (src, dst) geometry couple."""
 
-    def __init__(self, op: "CellOperator", src: BlockCsrMatrix, dst: BlockCsrMatrix, mode: str,
+    def __init__(self, op: "CellOperator", src: BlockCsrMatrix, dst: BlockCsrMatrix,
                  upload: bool = True):
         n = op.shape.degree + 1
         n3 = n**3
         n_cells = op.slot_group.shape[0]
-        n_cb = src.col_blocks.n_blocks
-        # visits: union of the src column lists over the cell's groups
-        grp_cell, grp_block = op.grp_cell, op.grp_block
-        n_lb = src.n_local_blocks
-        inc = sparse.csr_matrix((np.ones(grp_cell.size, dtype=np.int8), (grp_cell, grp_block)),
-                                shape=(n_cells, n_lb))
-        xp = sparse.csr_matrix((np.ones(src.col_index.size, dtype=np.int8),
-                                src.col_index.copy(), src.row_start.copy()),
-                               shape=(n_lb, n_cb))
-        vis = (inc.astype(np.int32) @ xp.astype(np.int32)).tocsr()
-        vis.sort_indices()
-        visit_cell = np.repeat(np.arange(n_cells, dtype=np.int64), np.diff(vis.indptr))
-        visit_col = vis.indices.astype(np.int64)
-        n_visits = visit_cell.size
-        # per (visit, group) block offsets in src / dst
         ng = np.diff(op.cell_gstart)
-        v_ng = ng[visit_cell]
-        visit_goff = np.concatenate([[0], np.cumsum(v_ng)]).astype(np.int64)
-        total = int(visit_goff[-1])
-        v_rep = np.repeat(np.arange(n_visits, dtype=np.int64), v_ng)
-        g_idx = op.cell_gstart[visit_cell][v_rep] + (np.arange(total) - visit_goff[:-1][v_rep])
-        lb_e = grp_block[g_idx]
-        key = lb_e * n_cb + visit_col[v_rep]
-        group_xoff = _lookup_offsets(src, key, missing=-1)
-        group_hoff = _lookup_offsets(dst, key, missing=None)
-        if (group_hoff < 0).any():
-            bad = int(np.flatnonzero(group_hoff < 0)[0])
-            raise PatternError(f"destination pattern misses column block {int(key[bad] % n_cb)} "
-                               f"in local block row {int(key[bad] // n_cb)}")
-        # work list
-        sizes = src.col_blocks.sizes
+        # work list: (cell, column) pairs, cells in Hilbert order, columns ascending
         if src.support is not None:
-            mask = src.support.local_mask(op.layout)
-            a_cell = op.cell_local_rows_matrix(mask.shape[0])
-            act = (a_cell @ mask.astype(np.int32)).tocsr()
-            act.sum_duplicates()
-            act.sort_indices()
-            p_cell = np.repeat(np.arange(n_cells, dtype=np.int64), np.diff(act.indptr))
-            p_col = act.indices.astype(np.int64)
-            p_cb = src.col_blocks.blocks_of(p_col) if p_col.size else p_col
-            p_lane = p_col - src.col_blocks.starts[p_cb]
-            vkey = visit_cell * n_cb + visit_col
-            pkey = p_cell * n_cb + p_cb
-            pv = np.searchsorted(vkey, pkey)
-            okv = (pv < vkey.size) & (vkey[np.minimum(pv, max(vkey.size - 1, 0))] == pkey)
-            if not okv.all():
-                raise ConsistencyError("column support reaches a cell whose rows have no "
-                                       "stored block for that column block")
-            pair_visit, pair_lane = pv, p_lane
+            act = op.active_pairs(src.support)
             self.support_based = True
         else:
-            lanes = sizes[visit_col]
-            pair_visit = np.repeat(np.arange(n_visits, dtype=np.int64), lanes)
-            starts = np.concatenate([[0], np.cumsum(lanes)])[:-1]
-            pair_lane = np.arange(int(lanes.sum())) - np.repeat(starts, lanes)
+            inc = _bool_csr(sparse.csr_matrix(
+                (np.ones(op.grp_cell.size, dtype=np.int32), (op.grp_cell, op.grp_block)),
+                shape=(n_cells, src.n_local_blocks)))
+            sg = src.slab
+            s = sparse.csr_matrix((np.ones(sg.cols.size, dtype=np.int32), sg.cols, sg.ptr),
+                                  shape=(src.n_local_blocks, src.col_blocks.total))
+            act = _bool_csr(inc @ s)
             self.support_based = False
-        colors = None
-        if mode == "color":
-            color = op.cell_color[visit_cell[pair_visit]] if pair_visit.size else np.zeros(0, np.int64)
-            order = np.argsort(color, kind="stable")
-            pair_visit, pair_lane = pair_visit[order], pair_lane[order]
-            colors = np.searchsorted(color[order], np.arange(9)).astype(np.int64)
+        p_cell = np.repeat(np.arange(n_cells, dtype=np.int64), np.diff(act.indptr))
+        p_col = act.indices.astype(np.int64)
+        n_pairs = p_col.size
+        # per (pair, group): {src slab offset + slot | -1, dst slab offset + slot}
+        pg = ng[p_cell]
+        ngp = pg + (pg & 1)
+        if ngp.size and int(ngp.max()) > 32:
+            raise ConsistencyError("a cell touches more than 32 block rows")
+        owner, g = _expand(pg)
+        lb = op.grp_block[op.cell_gstart[p_cell][owner] + g]
+        col = p_col[owner]
+        zero = np.zeros(lb.size, dtype=np.int64)
+        xo = src.slab.offsets(lb, zero, col)
+        ho = dst.slab.offsets(lb, zero, col)
+        if (ho < 0).any():
+            bad = int(np.flatnonzero(ho < 0)[0])
+            raise PatternError(f"destination does not store column {int(col[bad])} in local "
+                               f"block row {int(lb[bad])} (reached by cell "
+                               f"{int(p_cell[owner[bad]])})")
+        if max(int(xo.max(initial=0)), int(ho.max(initial=0))) >= 2**31 - 2**20:
+            raise ShapeError("K1 offsets exceed 2^31 elements")
+        pair_gtab = np.concatenate([[0], np.cumsum(2 * ngp)]).astype(np.int64)
+        gtab = np.zeros(int(pair_gtab[-1]), dtype=np.int32)
+        gtab[0::2] = -1
+        at = pair_gtab[:-1][owner] + 2 * g
+        gtab[at] = xo
+        gtab[at + 1] = ho
+        # per (cell, DoF) codes: group, r * K_src, r * K_dst
+        sgp = op.slot_group
+        lbd, rib = op._lb, op._rib
+        rkx = rib * src.slab.width[lbd]
+        rkh = rib * dst.slab.width[lbd]
+        wide = bool(n_cells and (int(sgp.max()) >= 32 or int(rkx.max()) >= 1 << 13
+                                 or int(rkh.max()) >= 1 << 14))
+        if wide:
+            if n_cells and (int(rkx.max()) >= 1 << 27 or int(rkh.max()) >= 1 << 31):
+                raise ShapeError("K1 codes: block rows too large for 32-bit row offsets")
+            stride = (2 * n3 + 3) // 4 * 4
+            codes = np.zeros((n_cells, stride), dtype=np.uint32)
+            codes[:, 0 : 2 * n3 : 2] = (sgp << 27) | rkx
+            codes[:, 1 : 2 * n3 : 2] = rkh
+        else:
+            stride = (n3 + 3) // 4 * 4
+            codes = np.zeros((n_cells, stride), dtype=np.uint32)
+            codes[:, :n3] = (sgp << 27) | (rkx << 14) | rkh
         self.n = n
         self.n_cells = n_cells
-        self.n_visits = n_visits
-        self.n_pairs = int(pair_visit.size)
-        self.visit_cell = visit_cell
-        self.visit_col = visit_col
-        self.pair_visit = pair_visit
-        self.lane_groups = int(np.sum((src.col_strides[visit_col] + src.lane_width - 1) // src.lane_width))
+        self.n_pairs = int(n_pairs)
+        self.wide = wide
+        self.max_groups = int(ngp.max()) if ngp.size else 2
+        self.cells_visited = int(np.count_nonzero(np.diff(act.indptr)))
+        # reference accounting (OpCounters): visits = (cell, column block) couples
+        # of the RowsBlockAccessor over src's block pattern
+        inc_b = _bool_csr(sparse.csr_matrix(
+            (np.ones(op.grp_cell.size, dtype=np.int32), (op.grp_cell, op.grp_block)),
+            shape=(n_cells, src.n_local_blocks)))
+        xp = sparse.csr_matrix((np.ones(src.col_index.size, dtype=np.int32), src.col_index,
+                                src.row_start), shape=(src.n_local_blocks, src.col_blocks.n_blocks))
+        vis = _bool_csr(inc_b @ xp)
+        visit_col = vis.indices.astype(np.int64)
+        self.n_visits = int(visit_col.size)
+        self.lane_groups = int(np.sum((src.col_strides[visit_col] + src.lane_width - 1)
+                                      // src.lane_width))
         self.dof_lane_slots = int(n3 * np.sum(src.col_strides[visit_col]))
-        self.cells_visited = int(np.unique(visit_cell).size)
-        self.mode = mode
-        arrs = dict(
-            pair_visit=np.ascontiguousarray(pair_visit, dtype=np.int32),
-            pair_lane=np.ascontiguousarray(pair_lane, dtype=np.int32),
-            visit_cell=np.ascontiguousarray(visit_cell, dtype=np.int32),
-            visit_stride=np.ascontiguousarray(src.col_strides[visit_col], dtype=np.int32),
-            visit_goff=np.ascontiguousarray(visit_goff, dtype=np.int64),
-            group_xoff=np.ascontiguousarray(group_xoff, dtype=np.int64),
-            group_hoff=np.ascontiguousarray(group_hoff, dtype=np.int64),
-            cell_slots=np.ascontiguousarray(op.cell_slots, dtype=np.uint32),
-            color_pair_start=None if colors is None else np.ascontiguousarray(colors),
+        self.arrays = dict(
+            pair_cell=np.ascontiguousarray(p_cell, dtype=np.int32),
+            pair_gtab=np.ascontiguousarray(pair_gtab[:-1], dtype=np.int64),
+            pair_ngp=np.ascontiguousarray(ngp, dtype=np.int32),
+            gtab=gtab,
+            codes=np.ascontiguousarray(codes.ravel()),
         )
-        self.arrays = arrs
-        self.n_groups_total = total
-        self.colors = colors
+        self.code_stride = stride
         self.handle = None
         self.launches = 0
         if upload:
             self.upload(op)
 
     def upload(self, op):
-        n, arrs, colors = self.n, self.arrays, self.colors
+        n, arrs = self.n, self.arrays
         lib = _lib.load()
         d = _lib.CellopDesc()
-        d.n, d.n_cells, d.n_visits = n, self.n_cells, self.n_visits
-        d.n_pairs, d.n_groups_total = self.n_pairs, self.n_groups_total
-        d.n_colors = 0 if colors is None else 8
-        d.color_pair_start = _lib.ptr(arrs["color_pair_start"], C.c_int64)
-        for name, ct in (("pair_visit", C.c_int32), ("pair_lane", C.c_int32),
-                         ("visit_cell", C.c_int32), ("visit_stride", C.c_int32),
-                         ("visit_goff", C.c_int64), ("group_xoff", C.c_int64),
-                         ("group_hoff", C.c_int64), ("cell_slots", C.c_uint32)):
-            setattr(d, name, _lib.ptr(arrs[name], ct))
+        d.n, d.wide, d.n_cells = n, 1 if self.wide else 0, self.n_cells
+        d.code_stride, d.max_groups = self.code_stride, self.max_groups
+        d.n_pairs, d.gtab_len = self.n_pairs, int(arrs["gtab"].size)
+        d.pair_cell = _lib.ptr(arrs["pair_cell"], C.c_int32)
+        d.pair_gtab = _lib.ptr(arrs["pair_gtab"], C.c_int64)
+        d.pair_ngp = _lib.ptr(arrs["pair_ngp"], C.c_int32)
+        d.gtab = _lib.ptr(arrs["gtab"], C.c_int32)
+        d.codes = _lib.ptr(arrs["codes"], C.c_uint32)
         sh = op.shape
         dco = collocation_derivative(sh)
         for i in range(n):
@@ -456,17 +532,6 @@ class _CellPlan:
         nl = C.c_int32()
         _lib.check(lib.bmv_cellop_launches(self.handle.raw, C.byref(nl)))
         self.launches = int(nl.value)
-
-
-def _lookup_offsets(m: BlockCsrMatrix, key: np.ndarray, missing):
-    keys = m.local_keys()
-    pos = np.searchsorted(keys, key)
-    if keys.size == 0:
-        return np.full(key.size, -1, dtype=np.int64)
-    ok = (pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == key)
-    out = np.full(key.size, -1, dtype=np.int64)
-    out[ok] = m.block_offsets[pos[ok]]
-    return out
 
 
 class CellOperator:
@@ -503,7 +568,10 @@ class CellOperator:
             self.cell_color = np.zeros(0, dtype=np.int64)
         self._plans: dict = {}
         self._coefs: dict = {}
+        self._act: dict = {}
+        self._images: dict = {}
         self._dev_tables = None
+        self._node_of_dof = None
 
     @property
     def cell_map(self) -> CellDoFMap:
@@ -518,17 +586,73 @@ class CellOperator:
         return sparse.csr_matrix((np.ones(loc.size, dtype=np.int32), loc.ravel(),
                                   np.arange(0, loc.size + 1, n3)), shape=(n_cells, n_local_rows))
 
-    # -- plans and coefficients -----------------------------------------------
+    # -- supports, images and plans ---------------------------------------------
+
+    def active_pairs(self, support) -> sparse.csr_matrix:
+        """(owned cells x columns) bool CSR: the cell has a node in the column's support."""
+        hit = self._act.get(id(support))
+        if hit is not None and hit[0] is support:
+            return hit[1]
+        mask = support.local_mask(self.layout)
+        a_cell = self.cell_local_rows_matrix(mask.shape[0])
+        act = _bool_csr(a_cell @ mask.astype(np.int32))
+        self._act[id(support)] = (support, act)
+        return act
+
+    def image_columns(self, source) -> ImageColumns:
+        """Stored-column spec of H X for a source X stored with spec `source`
+        (`BlockCsrMatrix(grown_pattern, layout, ctx, columns=op.image_columns(support))`)."""
+        hit = self._images.get(id(source))
+        if hit is None or hit.source is not source:
+            hit = ImageColumns(self, source)
+            self._images[id(source)] = hit
+        return hit
+
+    def cells_touching_blocks(self, gblocks: np.ndarray) -> np.ndarray:
+        """Global ids of the cells with a node in one of the global block rows."""
+        mesh, numbering = self.mesh, self.numbering
+        blocks = numbering.row_blocks
+        gblocks = np.asarray(gblocks, dtype=np.int64)
+        if gblocks.size == blocks.n_blocks:
+            return np.arange(mesh.n_cells, dtype=np.int64)
+        if self._node_of_dof is None:
+            inv = np.empty(numbering.n_dofs, dtype=np.int64)
+            inv[numbering.new_index_of_node] = np.arange(numbering.n_dofs, dtype=np.int64)
+            self._node_of_dof = inv
+        sz = blocks.sizes[gblocks]
+        owner = np.repeat(np.arange(gblocks.size, dtype=np.int64), sz)
+        first = np.concatenate([[0], np.cumsum(sz)])[:-1]
+        rows = blocks.starts[gblocks][owner] + (np.arange(int(sz.sum())) - first[owner])
+        node = self._node_of_dof[rows]
+        p = numbering.degree
+        sx, sy, _ = mesh.node_grid_shape(p)
+        ex, ey, ez = mesh.extents
+        idx = (node % sx, (node // sx) % sy, node // (sx * sy))
+        cand = []
+        for axis_lo in range(8):
+            ok = np.ones(node.size, dtype=bool)
+            c = []
+            for ax, (v, e) in enumerate(zip(idx, (ex, ey, ez))):
+                lo = (axis_lo >> ax) & 1
+                ci = v // p - lo
+                good = (ci >= 0) & (ci < e)
+                if lo:
+                    good &= (v % p) == 0
+                ok &= good
+                c.append(ci)
+            cand.append((c[0] + ex * (c[1] + ey * c[2]))[ok])
+        return np.unique(np.concatenate(cand))
 
     def plan_for(self, src: BlockCsrMatrix, dst: BlockCsrMatrix) -> _CellPlan:
-        mode = _scatter_mode()
-        key = (id(src.pattern), id(src.support), id(dst.pattern), mode)
-        plan = self._plans.get(key)
-        if plan is None:
-            plan = _CellPlan(self, src, dst, mode)
-            self._plans[key] = (plan, src.pattern, src.support, dst.pattern)
-            return plan
-        return plan[0]
+        key = (id(src.slab), id(src.support), id(dst.slab))
+        hit = self._plans.get(key)
+        if hit is not None and hit[1] is src.slab and hit[2] is src.support and hit[3] is dst.slab:
+            return hit[0]
+        plan = _CellPlan(self, src, dst)
+        self._plans[key] = (plan, src.slab, src.support, dst.slab)
+        while len(self._plans) > 8:
+            self._plans.pop(next(iter(self._plans)))
+        return plan
 
     def _device_tables(self, device):
         if self._dev_tables is None:
@@ -541,8 +665,8 @@ class CellOperator:
         """(device tensor or None, cell stride) of the quadrature coefficient.
 
         Rows are padded to q3p = q^3 rounded up to even (16-byte rows, staged
-        by TMA in the streamed K1); the stride is q3p for a per-cell
-        coefficient and 0 for one shared by every cell."""
+        by TMA in K1); the stride is q3p for a per-cell coefficient and 0 for
+        one shared by every cell."""
         q3 = self.shape.n_q ** 3
         q3p = q3 + (q3 & 1)
         if spec.kind == MASS:
@@ -554,7 +678,7 @@ class CellOperator:
         else:
             raise ShapeError(f"unknown operator kind {spec.kind!r}")
         hit = self._coefs.get(key)
-        if hit is not None:
+        if hit is not None and (key[0] != "pot" or hit[2] is spec.potential):
             return hit[0], hit[1]
         w3 = self.kernels.w3.ravel()
 
@@ -599,17 +723,23 @@ class CellOperator:
 
     # -- apply ------------------------------------------------------------------
 
-    def apply(self, spec: OperatorSpec, src: BlockCsrMatrix, dst: BlockCsrMatrix,
-              variant: str = SUMFAC, counters: OpCounters | None = None):
-        """dst = Op(spec) @ src over the rank's cells, then compress dst."""
+    def _check_operands(self, spec, src, dst, variant):
         if src.layout is not self.layout or dst.layout is not self.layout:
             raise ShapeError("operator and operands must share one rank layout")
         if src.col_blocks != dst.col_blocks or src.lane_width != dst.lane_width:
             raise ShapeError("src and dst must share column blocking and lanes")
-        if variant not in (SUMFAC, GEMM):
+        if variant == GEMM:
+            raise ShapeError("variant 'gemm' (element-matrix products) is not implemented on the "
+                             "GPU path; use 'sumfac' (same operator)")
+        if variant != SUMFAC:
             raise ShapeError(f"unknown operator variant {variant!r}")
         if spec.kind not in (MASS, HAMILTONIAN):
             raise ShapeError(f"unknown operator kind {spec.kind!r}")
+
+    def apply(self, spec: OperatorSpec, src: BlockCsrMatrix, dst: BlockCsrMatrix,
+              variant: str = SUMFAC, counters: OpCounters | None = None):
+        """dst = Op(spec) @ src over the rank's cells, then compress dst."""
+        self._check_operands(spec, src, dst, variant)
         lib = _lib.require_device()
         dst.ensure_owned()
         plan = self.plan_for(src, dst)
@@ -621,6 +751,7 @@ class CellOperator:
             _lib.dptr(src.data), _lib.dptr(dst.data), dst.data.numel(),
             _lib.stream_handle(dst.device)), "bmv_cellop_apply")
         src.release_ghosts()
+        dst.support = None
         dst.compress()
         if counters is not None:
             self._count(spec, variant, plan, src, dst, counters)
@@ -630,55 +761,49 @@ class CellOperator:
         """hdst = H(spec) @ src and mdst = M @ src (the two products
         compute_energy forms, reference energy.py:129-174), fused: one gather
         of src and one interpolation to the quadrature points feed both
-        (bmv_cellop_apply_hm).  Same results as two `apply` calls; falls back
-        to them when the fused kernel does not apply (colour mode, other K1
-        variants, different destination patterns)."""
+        (bmv_cellop_apply_hm).  When the destinations store different
+        entries it runs the two applies instead; the choice depends only on
+        the operands' storage, which every rank shares, so all ranks run the
+        same exchange sequence."""
         if spec.kind != HAMILTONIAN:
             raise ShapeError("apply_h_and_mass takes the Hamiltonian spec")
         for d in (hdst, mdst):
-            if d.layout is not self.layout or d.col_blocks != src.col_blocks:
-                raise ShapeError("operator and operands must share one rank layout and blocking")
+            self._check_operands(spec, src, d, SUMFAC)
+        same = (hdst.pattern is mdst.pattern and hdst.columns is mdst.columns)
+        if not same:
+            self.apply(spec, src, hdst, counters=counters)
+            self.apply(mass_operator(), src, mdst, counters=counters)
+            return
         lib = _lib.require_device()
         plan = self.plan_for(src, hdst)
-        fused = (hdst.pattern is mdst.pattern and hdst.data.numel() == mdst.data.numel()
-                 and _scatter_mode() == "atomic")
-        if fused:
-            hdst.ensure_owned()
-            mdst.ensure_owned()
-            coef, stride = self.coefficient(spec, hdst.device)
-            mcoef, _ = self.coefficient(mass_operator(), hdst.device)
-            src.update_ghost_values()
-            rc = lib.bmv_cellop_apply_hm(
-                plan.handle.raw, _lib.dptr(coef) if coef is not None else C.c_void_p(None),
-                stride, _lib.dptr(mcoef), _lib.dptr(src.data), _lib.dptr(hdst.data),
-                _lib.dptr(mdst.data), hdst.data.numel(), _lib.stream_handle(hdst.device))
-            if rc == _lib.BMV_OK:
-                src.release_ghosts()
-                hdst.compress()
-                mdst.compress()
-                if counters is not None:
-                    self._count(spec, SUMFAC, plan, src, hdst, counters)
-                    self._count(mass_operator(), SUMFAC, plan, src, mdst, counters)
-                return
-            src.release_ghosts()
-            if rc != _lib.BMV_ERR_INVALID:
-                _lib.check(rc, "bmv_cellop_apply_hm")
-        self.apply(spec, src, hdst, counters=counters)
-        self.apply(mass_operator(), src, mdst, counters=counters)
+        hdst.ensure_owned()
+        mdst.ensure_owned()
+        coef, stride = self.coefficient(spec, hdst.device)
+        mcoef, _ = self.coefficient(mass_operator(), hdst.device)
+        src.update_ghost_values()
+        _lib.check(lib.bmv_cellop_apply_hm(
+            plan.handle.raw, _lib.dptr(coef) if coef is not None else C.c_void_p(None),
+            stride, _lib.dptr(mcoef), _lib.dptr(src.data), _lib.dptr(hdst.data),
+            _lib.dptr(mdst.data), hdst.data.numel(), _lib.stream_handle(hdst.device)),
+            "bmv_cellop_apply_hm")
+        src.release_ghosts()
+        hdst.support = None
+        mdst.support = None
+        hdst.compress()
+        mdst.compress()
+        if counters is not None:
+            self._count(spec, SUMFAC, plan, src, hdst, counters)
+            self._count(mass_operator(), SUMFAC, plan, src, mdst, counters)
 
     def _count(self, spec, variant, plan, src, dst, counters):
         n = plan.n
         w = src.lane_width
         with_v = spec.kind == HAMILTONIAN and spec.potential is not None
-        if variant == GEMM:
-            counters.flops += plan.lane_groups * 2 * (n**3) ** 2 * w
-        else:
-            counters.flops += plan.lane_groups * sumfac_flops_per_lane(n, spec.kind, with_v) * w
+        counters.flops += plan.lane_groups * sumfac_flops_per_lane(n, spec.kind, with_v) * w
         counters.cells_visited += plan.cells_visited
         counters.col_blocks_visited += plan.n_visits
         counters.dof_lane_slots += plan.dof_lane_slots
-        ghost_vals = sum(len(g.rows) * src.pattern.row_cols(g.block).size
-                         for g in self.layout.ghost_groups)
+        ghost_vals = int(src.slab.off[-1] - src.slab.ghost_begin)
         counters.bytes_moved += 8 * (src.data.numel() + 2 * dst.data.numel()) + 16 * ghost_vals
         counters.add_extra("pairs", plan.n_pairs)
         counters.add_extra("flops_implemented",

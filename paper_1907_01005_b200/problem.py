@@ -236,34 +236,38 @@ def _support_entries(matrix: BlockCsrMatrix, prob: Problem):
 def fill_multivector(matrix: BlockCsrMatrix, prob: Problem, seed: int, attach: bool = True):
     """X[r, c] = 2 * hash(seed, r, old(c)) on the support of c, else 0 (owned rows).
 
-    Writes the owned region from the support entries directly (one hash per
-    support entry), which equals the reference's masked per-block fill.
+    With `attach` (default) the matrix is (re)laid out to store exactly the
+    support's columns (support.attach_support; slabs.py) and the values go up
+    as the compact support vector (8 bytes per structural nonzero), scattered
+    on the device.  Equals the reference's masked per-block fill
+    (`bench/problem.py:113-131`) on every stored entry.
     """
     import torch
 
     from . import _plan
 
     matrix._require("owned-writable")
-    flat, rows, cols = _support_entries(matrix, prob)
-    if attach and matrix.data.is_cuda and _plan.enabled():
-        # compact values (nnz, column-major support order) scattered on the device:
-        # no padded host image, host->device bytes = 8 nnz instead of the stored blocks
-        attach_support(matrix, prob.column_support, check=False)
-        vals = _plan.hash_fill(seed, rows, cols, prob.loc_layout.old_col_of_new, None, 2.0)
-        matrix.upload_support_values(torch.from_numpy(vals))
-        return matrix
-    host = np.zeros(matrix.data.numel())
-    if matrix.n_owned_values < host.size:
-        host[matrix.n_owned_values :] = matrix.data[matrix.n_owned_values :].cpu().numpy()
-    if rows.size:
-        if _plan.enabled():
-            _plan.hash_fill(seed, rows, cols, prob.loc_layout.old_col_of_new, flat, 2.0, host)
-        else:
-            host[flat] = 2.0 * hashed_entries(seed, rows, prob.loc_layout.old_col_of_new[cols])
-    matrix.data.copy_(torch.from_numpy(host))
+    sup = prob.column_support
+    if attach and matrix.support is not sup:
+        matrix.relayout(sup)
+    flat, rows, cols = sup.owned_entries(matrix)
+    old = prob.loc_layout.old_col_of_new
+    if _plan.enabled():
+        vals = _plan.hash_fill(seed, rows, cols, old, None, 2.0)
+    else:
+        vals = 2.0 * hashed_entries(seed, rows, old[cols])
     if attach:
-        attach_support(matrix, prob.column_support, check=False)
+        matrix.upload_support_values(torch.from_numpy(vals))
+    else:
+        _zero_owned(matrix)
+        matrix._write_host(flat, vals)
     return matrix
+
+
+def _zero_owned(matrix: BlockCsrMatrix):
+    from .bcsr import _zero_range
+
+    _zero_range(matrix.data, 0, matrix.n_owned_values)
 
 
 def fill_projected(matrix: BlockCsrMatrix, prob: Problem, seed: int):
@@ -301,14 +305,12 @@ class DirichletMask:
         rows = np.asarray(rows, dtype=np.int64)
         rows = rows[(rows >= lo) & (rows < hi)]
         lb, rib = matrix.layout.map_rows(rows)
-        idx = []
-        for l, r in zip(lb.tolist(), rib.tolist()):
-            for pos in range(int(matrix.row_start[l]), int(matrix.row_start[l + 1])):
-                cols = int(matrix.col_blocks.sizes[matrix.col_index[pos]])
-                stride = int(matrix.col_strides[matrix.col_index[pos]])
-                base = int(matrix.block_offsets[pos]) + r * stride
-                idx.append(np.arange(base, base + cols))
-        self.index = _IndexList(np.concatenate(idx) if idx else np.zeros(0, np.int64), matrix.device)
+        sg = matrix.slab
+        k = sg.width[lb]
+        owner = np.repeat(np.arange(lb.size, dtype=np.int64), k)
+        first = np.concatenate([[0], np.cumsum(k)])[:-1]
+        idx = sg.off[lb][owner] + rib[owner] * k[owner] + (np.arange(int(k.sum())) - first[owner])
+        self.index = _IndexList(idx.astype(np.int64), matrix.device)
         self._zeros = None
 
     def apply(self, matrix: BlockCsrMatrix):
@@ -338,13 +340,21 @@ class RankSetup:
 
 
 def make_rank_setup(ctx, prob: Problem, projection: bool | None = None, device=None,
-                    with_y: bool | None = None) -> RankSetup:
+                    with_y: bool | None = None, compact_xc: bool = True) -> RankSetup:
+    """Operands of one workload on this rank, in slab storage (slabs.py):
+    X (and Y) store their support columns, H X (H Y) the operator image of
+    that support, S and C (projected pattern) every column of their blocks,
+    X C the support columns of X (X's own storage; compact_xc=False
+    keeps the reference's block-level truncation instead)."""
     cfg = prob.cfg
     layout = make_dof_layout(ctx, prob.mesh, prob.partition, prob.numbering)
     op = CellOperator(prob.mesh, prob.partition, prob.numbering, layout)
     w = cfg.lane_width
-    x = fill_multivector(BlockCsrMatrix(prob.pattern, layout, ctx, w, device), prob, cfg.seed_x)
-    hx = BlockCsrMatrix(prob.grown, layout, ctx, w, device)
+    sup = prob.column_support
+    img = op.image_columns(sup)
+    x = fill_multivector(BlockCsrMatrix(prob.pattern, layout, ctx, w, device, columns=sup),
+                         prob, cfg.seed_x)
+    hx = BlockCsrMatrix(prob.grown, layout, ctx, w, device, columns=img)
     st = RankSetup(prob, ctx, layout, op, x, hx)
     if cfg.dirichlet:
         rows = dirichlet_rows(prob)
@@ -359,10 +369,11 @@ def make_rank_setup(ctx, prob: Problem, projection: bool | None = None, device=N
         if with_y is None:
             with_y = cfg.name == "proj"
         if with_y:
-            st.y = fill_multivector(BlockCsrMatrix(prob.pattern, layout, ctx, w, device), prob,
-                                    cfg.seed_y)
-            st.hy = BlockCsrMatrix(prob.grown, layout, ctx, w, device)
+            st.y = fill_multivector(BlockCsrMatrix(prob.pattern, layout, ctx, w, device,
+                                                   columns=sup), prob, cfg.seed_y)
+            st.hy = BlockCsrMatrix(prob.grown, layout, ctx, w, device, columns=img)
         st.s = BlockCsrMatrix(proj, clayout, ctx, w, device)
         st.c = fill_projected(BlockCsrMatrix(proj, clayout, ctx, w, device), prob, cfg.seed_c)
-        st.xc = BlockCsrMatrix(prob.pattern, layout, ctx, w, device)
+        st.xc = BlockCsrMatrix(prob.pattern, layout, ctx, w, device,
+                               columns=sup if compact_xc else None)
     return st

@@ -11,6 +11,12 @@ runs only the active (cell, column) pairs.  Skipping a pair whose input is
 identically zero on the cell changes no output value, so results are the
 same as the all-lanes computation whenever the declaration holds.
 
+A support also decides the STORAGE of a matrix built with it
+(`BlockCsrMatrix(..., columns=support)`, slabs.py): a block row stores only
+the columns whose support reaches one of its rows, so entries outside the
+support take no memory and no HBM traffic.  `attach_support` re-lays-out an
+existing matrix the same way.
+
 `check=True` (default) verifies the declaration on the host when the
 support is attached to a filled matrix.
 """
@@ -110,24 +116,52 @@ class ColumnSupport:
         cache[key] = m
         return m
 
+    def columns_for(self, pattern, gblocks: np.ndarray):
+        """Stored columns (slab columns, slabs.py) of global block rows `gblocks`:
+        the columns whose support has a row in the block row.  (ptr, cols)."""
+        from . import _plan
+
+        blocks = pattern.row_blocks
+        gblocks = np.asarray(gblocks, dtype=np.int64)
+        if _plan.enabled():
+            return _plan.support_columns(self, blocks, gblocks)
+        sel = np.full(blocks.n_blocks, -1, dtype=np.int64)
+        sel[gblocks] = np.arange(gblocks.size, dtype=np.int64)
+        keys = []
+        for c in range(self.n_cols):
+            r = self.col_rows[c]
+            if r.size == 0:
+                continue
+            g = np.unique(blocks.blocks_of(r))
+            s_ = sel[g]
+            s_ = s_[s_ >= 0]
+            keys.append(s_ * self.n_cols + c)
+        k = np.sort(np.concatenate(keys)) if keys else np.zeros(0, dtype=np.int64)
+        ptr = np.searchsorted(k // max(self.n_cols, 1) if k.size else k,
+                              np.arange(gblocks.size + 1), side="left").astype(np.int64)
+        return ptr, (k % max(self.n_cols, 1)).astype(np.int64)
+
+    def key(self):
+        return ("support", id(self))
+
     def owned_entries(self, matrix):
         """(flat storage offsets, global rows, columns) of the support entries
         in the matrix's owned rows, column-major (column, then row) order.
 
         This is the compact value order used by `upload_support_values`.
-        Cached per (pattern, layout, lane width).
+        Cached per matrix geometry.
         """
-        key = ("owned", id(matrix.pattern), id(matrix.layout), matrix.lane_width)
+        key = ("owned", id(matrix.slab))
         cache = self.__dict__.setdefault("_cache", {})
         hit = cache.get(key)
-        if hit is not None:
-            return hit
+        if hit is not None and hit[0] is matrix.slab:
+            return hit[1]
         from . import _plan
 
-        hit = _plan.owned_entries(self, matrix) if _plan.enabled() \
+        out = _plan.owned_entries(self, matrix) if _plan.enabled() \
             else self._owned_entries_numpy(matrix)
-        cache[key] = hit
-        return hit
+        cache[key] = (matrix.slab, out)
+        return out
 
     def _owned_entries_numpy(self, matrix):
         """numpy restatement of owned_entries (the native builder is pinned to it)."""
@@ -141,24 +175,9 @@ class ColumnSupport:
         own_sizes = blocks.sizes[layout.first_block : layout.first_block + nb_own]
         lb = np.repeat(np.arange(nb_own, dtype=np.int64), own_sizes)[rows - lo]
         rib = rows - blocks.starts[layout.first_block + lb]
-        cbk = np.repeat(np.arange(matrix.col_blocks.n_blocks, dtype=np.int64),
-                        matrix.col_blocks.sizes)[cols]
-        n_cb = matrix.col_blocks.n_blocks
-        n_own_pos = int(matrix.row_start[nb_own])
-        if nb_own * n_cb <= 64_000_000:
-            table = np.full(nb_own * n_cb, -1, dtype=np.int64)
-            table[matrix.pos_row[:n_own_pos] * n_cb + matrix.col_index[:n_own_pos]] = \
-                np.arange(n_own_pos, dtype=np.int64)
-            pos = table[lb * n_cb + cbk]
-        else:
-            keys = matrix.local_keys()[:n_own_pos]
-            k = lb * n_cb + cbk
-            pos = np.searchsorted(keys, k)
-            pos = np.where((pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == k), pos, -1)
-        if (pos < 0).any():
+        flat = matrix.slab.offsets(lb, rib, cols)
+        if (flat < 0).any():
             raise ConsistencyError("a support entry lies outside the multivector pattern")
-        flat = (matrix.block_offsets[pos] + rib * matrix.col_strides[cbk]
-                + (cols - matrix.col_blocks.starts[cbk]))
         return flat, rows, cols
 
     def check_matrix(self, matrix) -> None:
@@ -185,10 +204,14 @@ class ColumnSupport:
 
 
 def attach_support(matrix, support: ColumnSupport, check: bool = True):
-    """Declare matrix entries outside `support` structural zeros."""
+    """Declare matrix entries outside `support` structural zeros.
+
+    If the matrix does not already store exactly the support's columns, it is
+    re-laid-out (slabs.py): values inside the new slabs are kept, entries
+    outside the support are dropped (check=True first verifies they are 0)."""
     if support.n_cols != matrix.col_blocks.total:
         raise ConsistencyError("support column count differs from the matrix")
     if check:
         support.check_matrix(matrix)
-    matrix.support = support
+    matrix.relayout(support)
     return matrix

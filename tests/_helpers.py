@@ -93,7 +93,7 @@ def emulated_apply(op, potential, kind, src, dst):
     """CPU emulation of CellOperator.apply for CPU-resident matrices (tests only).
 
     Same sequence as the product (zero dst, update src ghosts, K1 plan over
-    (visit, lane) pairs, release src ghosts, compress dst) with the cell
+    (cell, column) pairs, release src ghosts, compress dst) with the cell
     integral taken from the numpy oracle.  Exercises the host plan and the
     rank-context exchange without a GPU.
     """
@@ -107,27 +107,28 @@ def emulated_apply(op, potential, kind, src, dst):
     dst.ensure_owned()
     dst.zero_out()
     src.update_ghost_values()
-    plan = _CellPlan(op, src, dst, "atomic", upload=False)
+    plan = _CellPlan(op, src, dst, upload=False)
     a = plan.arrays
     if plan.n_pairs:
-        pv = a["pair_visit"].astype(np.int64)
-        lane = a["pair_lane"].astype(np.int64)
-        cell = a["visit_cell"][pv].astype(np.int64)
-        stride = a["visit_stride"][pv].astype(np.int64)
-        gb = a["visit_goff"][:-1][pv]
-        slots = a["cell_slots"].reshape(-1, n3)[cell].astype(np.int64)
-        g = slots >> 24
-        rib = slots & 0xFFFFFF
-        xo = a["group_xoff"][gb[:, None] + g]
-        ho = a["group_hoff"][gb[:, None] + g]
+        cell = a["pair_cell"].astype(np.int64)
+        codes = a["codes"].reshape(-1, plan.code_stride)[cell].astype(np.int64)
+        if plan.wide:
+            w0, w1 = codes[:, 0 : 2 * n3 : 2], codes[:, 1 : 2 * n3 : 2]
+            g, rx, rh = w0 >> 27, w0 & 0x7FFFFFF, w1
+        else:
+            c = codes[:, :n3]
+            g, rx, rh = c >> 27, (c >> 14) & 0x1FFF, c & 0x3FFF
+        gt = a["gtab"].astype(np.int64)
+        base = a["pair_gtab"][:, None] + 2 * g
+        xo, ho = gt[base], gt[base + 1]
         X = src.data.numpy()
-        u = np.where(xo >= 0, X[np.maximum(xo, 0) + rib * stride[:, None] + lane[:, None]], 0.0)
+        u = np.where(xo >= 0, X[np.maximum(xo, 0) + rx], 0.0)
         vq = None
         if kind != "mass" and potential is not None:
             vq = O.sample_potential(potential, op.cell_origins[cell], deg, op.mesh.spacing)
         out = O.cell_integrals(deg, op.mesh.spacing, kind, u[:, :, None], vq)[:, :, 0]
         H = dst.data.numpy().copy()
-        np.add.at(H, (ho + rib * stride[:, None] + lane[:, None]).ravel(), out.ravel())
+        np.add.at(H, (ho + rh).ravel(), out.ravel())
         dst.data.copy_(torch.from_numpy(H))
     src.release_ghosts()
     dst.compress()

@@ -49,3 +49,90 @@ def test_identity_and_traces():
     got = B.tr_mult(sm, cm)
     want = float(np.sum(np.where(mask_t, t, 0.0) * h.T))
     assert abs(got - want) <= 1e-12 * max(1.0, abs(want))
+
+
+CENTERS6 = np.asarray([[1.0, 1.0, 1.0], [3.0, 3.0, 2.0], [2.0, 1.5, 3.0], [0.5, 3.2, 0.7],
+                      [4.5, 4.5, 4.5], [5.0, 1.0, 3.0]])
+
+
+def _compact():
+    """Coarse level 0, one vector per centre: supports cover 38 % of the
+    stored block columns, so compact and full storage differ."""
+    s = Small((6, 6, 6), (1.0, 1.0, 1.0), 0, 2, CENTERS6, 1.6, 3, 1)
+    ctx = serial_context("cpu")
+    rl, op, x, hx = s.operands(ctx, "cpu")
+    s.fill(x, 5, attach=True)
+    return s, op, x, hx
+
+
+def test_copy_keeps_storage_and_writes_clear_the_support_declaration():
+    """A copy stores the same columns (its structural zeros are part of the
+    storage); a write whose source is not declared with the same support
+    drops the declaration, so K1 falls back to every stored column instead of
+    silently skipping pairs (copy() + scale_add)."""
+    import pytest
+
+    from paper_1907_01005_b200.errors import ShapeError
+
+    s, op, x, hx = _compact()
+    x2 = x.copy()
+    assert x2.support is x.support and x2.slab is x.slab
+    assert np.array_equal(x2.to_dense_owned(), x.to_dense_owned())
+    B.scale_add(x2, 1.0, x, -0.5)  # same support: declaration kept
+    assert x2.support is x.support
+    assert np.allclose(x2.to_dense_owned(), 0.5 * x.to_dense_owned(), atol=1e-15)
+    d = x.copy()
+    d.fill_owned_entries(lambda r, c: hashed_entries(11, r, c))  # values off the support
+    assert d.support is None and d.slab is x.slab
+    B.scale_add(x2, 1.0, d, 1.0)
+    assert x2.support is None  # no longer a valid declaration
+    full = B.BlockCsrMatrix(x.pattern, x.layout, x.ctx, x.lane_width, "cpu")
+    full.fill_owned_entries(lambda r, c: hashed_entries(12, r, c))
+    with pytest.raises(ShapeError):
+        B.scale_add(x2, 1.0, full, 1.0)  # stores entries x2 has no room for
+
+
+def test_attach_support_relayouts_and_checks():
+    import pytest
+
+    from paper_1907_01005_b200.errors import ConsistencyError
+    from paper_1907_01005_b200.support import attach_support
+
+    s, op, x, hx = _compact()
+    full = B.BlockCsrMatrix(x.pattern, x.layout, x.ctx, x.lane_width, "cpu")
+    s.fill(full, 5, attach=False)
+    assert full.support is None and full.data.numel() > x.data.numel()
+    attach_support(full, s.support, check=True)
+    assert full.data.numel() == x.data.numel()
+    assert np.array_equal(full.to_dense_owned(), x.to_dense_owned())
+    bad = B.BlockCsrMatrix(x.pattern, x.layout, x.ctx, x.lane_width, "cpu")
+    bad.fill_owned_entries(lambda r, c: hashed_entries(3, r, c))
+    with pytest.raises(ConsistencyError):
+        attach_support(bad, s.support, check=True)
+
+
+def test_image_columns_cover_the_operator_reach():
+    """H X stored with op.image_columns(support) holds every column some cell
+    couples to its rows, and no more than the full grown pattern."""
+    s, op, x, hx = _compact()
+    img = B.BlockCsrMatrix(hx.pattern, hx.layout, hx.ctx, hx.lane_width, "cpu",
+                           columns=op.image_columns(x.columns))
+    act = op.active_pairs(s.support)
+    assert img.data.numel() < hx.data.numel()
+    # every (cell, column) pair reaches every block row of the cell
+    p_cell = np.repeat(np.arange(act.shape[0]), np.diff(act.indptr))
+    g0, g1 = op.cell_gstart[p_cell], op.cell_gstart[p_cell + 1]
+    for c, a, b in zip(act.indices, g0, g1):
+        lbs = op.grp_block[a:b]
+        assert (img.slab.slots(lbs, np.full(lbs.size, c)) >= 0).all()
+
+
+def test_gemm_variant_rejected():
+    import pytest
+
+    from paper_1907_01005_b200.errors import ShapeError
+    from paper_1907_01005_b200.matfree import hamiltonian_operator
+
+    s, op, x, hx = _compact()
+    with pytest.raises(ShapeError):
+        op.apply(hamiltonian_operator(None), x, hx, variant="gemm")

@@ -75,11 +75,11 @@ def test_c_oracle_matches_reference_random(golden_random, degree):
     rl, op, x, hx = s.operands(ctx, "cpu")
     s.fill(x, 10 * degree)
     vq = O.sample_potential(cosine(degree), op.cell_origins, degree, s.mesh.spacing)
-    h = np.zeros(hx.data.numel())
+    h = CO.reference_zeros(hx)
     CO.cellop_apply(degree, s.mesh.spacing, "h", op._lb, op._rib, op.cell_color, vq,
                     CO.matrix_meta(x), CO.matrix_meta(hx), x.col_strides, x.col_blocks.sizes,
-                    x.data.numpy(), h, threads=2)
-    hx.data.copy_(torch.from_numpy(h))
+                    CO.reference_values(x), h, threads=2)
+    CO.load_reference(hx, h)
     got = hx.to_dense_owned()
     want = g[f"p{degree}_r1_hx"]
     assert O.per_vector_rel_err(got, want) <= 1e-13
@@ -90,11 +90,11 @@ def test_c_oracle_smoke_matches_reference(golden_smoke):
     st = P.make_rank_setup(serial_context("cpu"), prob, device="cpu")
     op = st.op
     vq = O.sample_potential(prob.potential, op.cell_origins, 2, prob.mesh.spacing)
-    h = np.zeros(st.hx.data.numel())
+    h = CO.reference_zeros(st.hx)
     CO.cellop_apply(2, prob.mesh.spacing, "h", op._lb, op._rib, op.cell_color, vq,
                     CO.matrix_meta(st.x), CO.matrix_meta(st.hx), st.x.col_strides,
-                    st.x.col_blocks.sizes, st.x.data.numpy(), h, threads=2)
-    st.hx.data.copy_(torch.from_numpy(h))
+                    st.x.col_blocks.sizes, CO.reference_values(st.x), h, threads=2)
+    CO.load_reference(st.hx, h)
     assert O.per_vector_rel_err(st.hx.to_dense_owned(), golden_smoke["hx"]) <= 1e-13
 
 
@@ -112,3 +112,30 @@ def test_one_dimensional_fe_stencil_known_answer():
                              mesh.spacing, "h", None, num.n_dofs)
     assert np.abs(a @ np.ones(num.n_dofs)).max() <= 1e-14
     assert (a - a.T).nnz == 0
+
+
+def test_c_oracle_projection_and_postmultiply_match_reference(golden_smoke):
+    """oracle_tmmult / oracle_mmult (oracle/cellop.c, the reference loops of
+    bcsr.py:587-667) pinned to the reference's own S and X C on the smoke config."""
+    prob = P.build_problem("smoke")
+    st = P.make_rank_setup(serial_context("cpu"), prob, device="cpu", projection=True,
+                           compact_xc=False)
+    CO.load_reference(st.hx, _hx_reference(st, prob))
+    s_ref = CO.tmmult(st.x, st.hx, st.s, CO.reference_values(st.x), CO.reference_values(st.hx),
+                      threads=2)
+    CO.load_reference(st.s, s_ref)
+    assert np.abs(st.s.to_dense_owned() - golden_smoke["s"]).max() <= 1e-13 * np.abs(golden_smoke["s"]).max()
+    xc_ref = CO.mmult(st.x, st.c, st.xc, CO.reference_values(st.x), CO.reference_values(st.c),
+                      threads=2)
+    CO.load_reference(st.xc, xc_ref)
+    assert O.per_vector_rel_err(st.xc.to_dense_owned(), golden_smoke["xc"]) <= 1e-14
+
+
+def _hx_reference(st, prob):
+    op = st.op
+    vq = O.sample_potential(prob.potential, op.cell_origins, 2, prob.mesh.spacing)
+    h = CO.reference_zeros(st.hx)
+    CO.cellop_apply(2, prob.mesh.spacing, "h", op._lb, op._rib, op.cell_color, vq,
+                    CO.matrix_meta(st.x), CO.matrix_meta(st.hx), st.x.col_strides,
+                    st.x.col_blocks.sizes, CO.reference_values(st.x), h, threads=2)
+    return h

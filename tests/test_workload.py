@@ -21,7 +21,7 @@ def test_algorithmic_counts_match_survey(name, pairs, nnzx, nnzhx):
     assert (cnt["pairs"], cnt["nnzX"], cnt["nnzHX"]) == (pairs, nnzx, nnzhx)
     n = prob.cfg.degree + 1
     assert cnt["flops_hx_reference_formulation"] == pairs * (36 * n**4 + 8 * n**3)
-    plan = _CellPlan(st.op, st.x, st.hx, "atomic", upload=False)
+    plan = _CellPlan(st.op, st.x, st.hx, upload=False)
     assert plan.n_pairs == pairs
     if name != "smoke":
         assert plan.n_visits == 70_882  # reference OpCounters.col_blocks_visited

@@ -108,6 +108,16 @@ int bmv_cellop_apply(bmv_cellop* plan, int32_t kinetic, const double* coef,
 int bmv_cellop_apply_hm(bmv_cellop* plan, const double* coef, int64_t coef_stride,
                         const double* mass_coef, const double* x, double* hx, double* mx,
                         int64_t zero_len, void* stream);
+/* The same products on the plan's pairs [pair_begin, pair_end) only, without
+   zeroing: CellOperator.apply runs the pairs of cells touching no ghost row
+   while the halo exchange is in flight (the plan orders its pairs: interior
+   cells part A, cells with ghost rows, interior cells part B). */
+int bmv_cellop_apply_pairs(bmv_cellop* plan, int32_t kinetic, const double* coef,
+                           int64_t coef_stride, const double* x, double* hx,
+                           int64_t pair_begin, int64_t pair_end, void* stream);
+int bmv_cellop_apply_hm_pairs(bmv_cellop* plan, const double* coef, int64_t coef_stride,
+                              const double* mass_coef, const double* x, double* hx, double* mx,
+                              int64_t pair_begin, int64_t pair_end, void* stream);
 /* Device evaluation of the Gaussian-sum potential coefficient:
    coef[c*q3 + q] = w3[q] * scale * sum_k exp(-|x - center_k|^2 * inv_sigma2)
    at x = cell_origins[c] + quad_offsets[q].  All arrays device. */

@@ -21,6 +21,10 @@
  *                             DoFs by row block in first-occurrence order
  *   bmvp_chunk_*              bcsr.py:587-667 tmmult / mmult block loops: the K4 / K5
  *                             chunk plans (union columns, colmaps, output slots)
+ *   bmvp_support_transpose, bmvp_cell_pairs, bmvp_block_image, bmvp_k1_plan
+ *                             matfree.py:159-237,458-527: active (cell, column) pairs,
+ *                             the operator image (entry-level grown pattern) and the
+ *                             K1 group tables
  */
 #ifndef BMV_PLAN_H
 #define BMV_PLAN_H
@@ -126,6 +130,34 @@ void bmvp_chunk_sizes(const bmvp_chunks* c, int64_t* n_chunks, int64_t* meta_len
 void bmvp_chunk_copy(const bmvp_chunks* c, int64_t* part_start, int64_t* chunk_meta, int32_t* meta,
                      int64_t* chunk_a, int64_t* chunk_b);
 void bmvp_chunk_free(bmvp_chunks* c);
+
+/* Row -> columns transpose of a column support over selected rows (row_sel:
+ * global row -> selected index or -1).  Pass 1 (cols NULL): ptr (n_sel + 1).
+ * Pass 2: cols (int32), ascending per row.  (matfree active pairs / images) */
+int bmvp_support_transpose(int64_t n_cols, const int64_t* col_ptr, const int64_t* col_rows,
+                           const int64_t* row_sel, int64_t n_sel, int64_t* ptr, int32_t* cols);
+/* Per cell the sorted union of the columns of its n3 rows (cell_rows: indices
+ * into the row CSR row_ptr / row_cols, -1 none): the active (cell, column)
+ * pairs of K1 (reference RowsBlockAccessor emission, matfree.py:159-237, at
+ * entry level).  Two passes as above. */
+int bmvp_cell_pairs(int64_t n_cells, int32_t n3, const int64_t* cell_rows, const int64_t* row_ptr,
+                    const int32_t* row_cols, int64_t* ptr, int32_t* cols);
+/* Operator image per selected block row: union of the pair columns of the
+ * cells touching it (cell_blocks (n_cells, n3): selected block or -1); the
+ * stored columns of H X (matfree.ImageColumns; the grown pattern,
+ * localization.py:251-267, at entry level).  Two passes as above. */
+int bmvp_block_image(int64_t n_cells, int32_t n3, const int64_t* cell_blocks,
+                     const int64_t* pair_ptr, const int32_t* pair_cols, int64_t n_blocks,
+                     int64_t n_cols, int64_t* ptr, int64_t* cols);
+/* K1 per-pair group tables (include/bmv.h bmv_cellop_desc gtab): for pair p
+ * (cell, column) and each group g of the cell, {src slab offset + slot or -1,
+ * dst slab offset + slot}; odd group counts padded with {-1, 0}.  Returns 3
+ * and *bad_pair when dst lacks a slot (PatternError). */
+int bmvp_k1_plan(int64_t n_pairs, const int64_t* pair_cell, const int64_t* pair_col,
+                 const int64_t* cell_gstart, const int64_t* grp_block, const int64_t* src_ptr,
+                 const int64_t* src_cols, const int64_t* src_off, const int64_t* dst_ptr,
+                 const int64_t* dst_cols, const int64_t* dst_off, const int64_t* pair_gtab,
+                 int32_t* gtab, int64_t* bad_pair);
 
 #ifdef __cplusplus
 }

@@ -68,6 +68,12 @@ SIGNATURES = [
     ("bmv_cellop_apply_hm", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
       C.c_int64, C.c_void_p]),
+    ("bmv_cellop_apply_pairs", C.c_int,
+     [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+      C.c_void_p]),
+    ("bmv_cellop_apply_hm_pairs", C.c_int,
+     [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+      C.c_int64, C.c_int64, C.c_void_p]),
     ("bmv_chunk_plan_create", C.c_int, [C.POINTER(ChunkDesc), C.POINTER(C.c_void_p)]),
     ("bmv_chunk_plan_destroy", C.c_int, [C.c_void_p]),
     ("bmv_tmmult_run", C.c_int,

@@ -72,6 +72,16 @@ def load():
         lib.bmvp_chunk_copy.restype = None
         lib.bmvp_chunk_free.argtypes = [C.c_void_p]
         lib.bmvp_chunk_free.restype = None
+        _i32p = C.POINTER(C.c_int32)
+        lib.bmvp_support_transpose.argtypes = [C.c_int64, _i64p, _i64p, _i64p, C.c_int64, _i64p,
+                                               _i32p]
+        lib.bmvp_cell_pairs.argtypes = [C.c_int64, C.c_int32, _i64p, _i64p, _i32p, _i64p, _i32p]
+        lib.bmvp_block_image.argtypes = [C.c_int64, C.c_int32, _i64p, _i64p, _i32p, C.c_int64,
+                                         C.c_int64, _i64p, _i64p]
+        lib.bmvp_k1_plan.argtypes = [C.c_int64, _i64p, _i64p, _i64p, _i64p, _i64p, _i64p, _i64p,
+                                     _i64p, _i64p, _i64p, _i64p, _i32p, _i64p]
+        for f in ("bmvp_support_transpose", "bmvp_cell_pairs", "bmvp_block_image", "bmvp_k1_plan"):
+            getattr(lib, f).restype = C.c_int
         for f in ("bmvp_first_touch", "bmvp_grow_count", "bmvp_grow_fill", "bmvp_hash_fill", "bmvp_blocks_of", "bmvp_owned_entries_count", "bmvp_owned_entries_fill",
                   "bmvp_support_columns_count", "bmvp_support_columns_fill",
                   "bmvp_first_groups_count", "bmvp_first_groups_fill"):
@@ -272,3 +282,71 @@ def chunk_plan(kind: int, rows, a, b, acb_starts, m_ltab, m, max_rows: int, max_
         return out
     finally:
         lib.bmvp_chunk_free(h)
+
+
+def _p32(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def support_transpose(support, row_sel: np.ndarray, n_sel: int):
+    """Row -> columns CSR of a ColumnSupport over the selected rows
+    (row_sel: global row -> selected index or -1); columns ascending."""
+    lib = load()
+    col_ptr, col_rows = support.csr()
+    row_sel = _i64(row_sel)
+    ptr = np.zeros(n_sel + 1, dtype=np.int64)
+    _check(lib.bmvp_support_transpose(support.n_cols, _p(col_ptr), _p(col_rows), _p(row_sel),
+                                      n_sel, _p(ptr), None), "bmvp_support_transpose")
+    cols = np.empty(max(int(ptr[-1]), 1), dtype=np.int32)
+    _check(lib.bmvp_support_transpose(support.n_cols, _p(col_ptr), _p(col_rows), _p(row_sel),
+                                      n_sel, _p(ptr), _p32(cols)), "bmvp_support_transpose")
+    return ptr, cols[: int(ptr[-1])]
+
+
+def cell_pairs(cell_rows: np.ndarray, row_ptr: np.ndarray, row_cols: np.ndarray):
+    """Per cell the sorted union of the columns of its rows (cell_rows (n, n3)
+    indices into the row CSR, -1 = none).  (ptr, cols int32)."""
+    lib = load()
+    cell_rows = _i64(cell_rows)
+    n, n3 = cell_rows.shape
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    row_ptr = _i64(row_ptr)
+    row_cols = np.ascontiguousarray(row_cols, dtype=np.int32)
+    rc = row_cols if row_cols.size else np.zeros(1, dtype=np.int32)
+    _check(lib.bmvp_cell_pairs(n, n3, _p(cell_rows), _p(row_ptr), _p32(rc), _p(ptr), None),
+           "bmvp_cell_pairs")
+    cols = np.empty(max(int(ptr[-1]), 1), dtype=np.int32)
+    _check(lib.bmvp_cell_pairs(n, n3, _p(cell_rows), _p(row_ptr), _p32(rc), _p(ptr), _p32(cols)),
+           "bmvp_cell_pairs")
+    return ptr, cols[: int(ptr[-1])]
+
+
+def block_image(cell_blocks: np.ndarray, pair_ptr, pair_cols, n_blocks: int, n_cols: int):
+    """image(b) = union of the cells' pair columns over the cells touching b
+    (cell_blocks (n, n3): selected block index or -1).  (ptr, cols int64)."""
+    lib = load()
+    cell_blocks = _i64(cell_blocks)
+    n, n3 = cell_blocks.shape
+    pair_ptr = _i64(pair_ptr)
+    pc = np.ascontiguousarray(pair_cols, dtype=np.int32)
+    pc = pc if pc.size else np.zeros(1, dtype=np.int32)
+    ptr = np.zeros(n_blocks + 1, dtype=np.int64)
+    _check(lib.bmvp_block_image(n, n3, _p(cell_blocks), _p(pair_ptr), _p32(pc), n_blocks, n_cols,
+                                _p(ptr), None), "bmvp_block_image")
+    cols = np.empty(max(int(ptr[-1]), 1), dtype=np.int64)
+    _check(lib.bmvp_block_image(n, n3, _p(cell_blocks), _p(pair_ptr), _p32(pc), n_blocks, n_cols,
+                                _p(ptr), _p(cols)), "bmvp_block_image")
+    return ptr, cols[: int(ptr[-1])]
+
+
+def k1_gtab(pair_cell, pair_col, cell_gstart, grp_block, src, dst, pair_gtab, gtab_len: int):
+    """K1 group tables (see bmv_plan.h bmvp_k1_plan); returns (gtab, bad pair or -1)."""
+    lib = load()
+    gtab = np.empty(max(gtab_len, 2), dtype=np.int32)
+    bad = C.c_int64(-1)
+    keep = [_i64(a) for a in (pair_cell, pair_col, cell_gstart, grp_block, src.ptr, src.cols,
+                               src.off, dst.ptr, dst.cols, dst.off, pair_gtab)]
+    rc = lib.bmvp_k1_plan(keep[0].size, *[_p(a) for a in keep], _p32(gtab), C.byref(bad))
+    if rc not in (0, 3):
+        raise UsageError(f"bmvp_k1_plan failed (status {rc})")
+    return gtab[:gtab_len], int(bad.value)

@@ -512,6 +512,31 @@ int bmv_cellop_destroy(bmv_cellop* p) {
   return BMV_OK;
 }
 
+namespace {
+
+// mode 0: H, 1: coefficient only (mass), 2: fused H + M; pairs [p0, p1)
+int run_pairs(const bmv_cellop* p, int mode, const double* coef, int64_t coef_stride,
+              const double* mcoef, const double* x, double* hx, double* mx, int64_t p0, int64_t p1,
+              cudaStream_t st) {
+  using namespace bmv;
+  const int q3 = p->n * p->n * p->n, q3p = q3 + (q3 & 1);
+  if (coef && coef_stride != 0 && coef_stride != q3p) {
+    set_error("K1: coefficient rows must have stride 0 or %d", q3p);
+    return BMV_ERR_INVALID;
+  }
+  if (p0 < 0 || p1 > p->n_pairs || p0 > p1) {
+    set_error("K1: pair range [%lld, %lld) outside [0, %lld)", (long long)p0, (long long)p1,
+              (long long)p->n_pairs);
+    return BMV_ERR_INVALID;
+  }
+  if (p1 == p0) return BMV_OK;
+  K1Args args{p->desc + p0, p->codes, p->gtab, p->code_stride, p->gbytes, coef,
+              coef_stride != 0 ? 1 : 0, p1 - p0, x, hx, mx, mcoef};
+  return dispatch(p, args, coef != nullptr, mode, st);
+}
+
+}  // namespace
+
 int bmv_cellop_apply(bmv_cellop* p, int32_t kinetic, const double* coef, int64_t coef_stride,
                      const double* x, double* hx, int64_t zero_len, void* stream) {
   using namespace bmv;
@@ -523,17 +548,23 @@ int bmv_cellop_apply(bmv_cellop* p, int32_t kinetic, const double* coef, int64_t
     set_error("operator without kinetic and coefficient terms");
     return BMV_ERR_INVALID;
   }
-  const int q3 = p->n * p->n * p->n, q3p = q3 + (q3 & 1);
-  if (coef && coef_stride != 0 && coef_stride != q3p) {
-    set_error("bmv_cellop_apply: coefficient rows must have stride 0 or %d", q3p);
+  cudaStream_t st = as_stream(stream);
+  const int rc = zero_async(hx, zero_len, st);
+  if (rc != BMV_OK) return rc;
+  return run_pairs(p, kinetic ? 0 : 1, coef, coef_stride, nullptr, x, hx, nullptr, 0, p->n_pairs,
+                   st);
+}
+
+int bmv_cellop_apply_pairs(bmv_cellop* p, int32_t kinetic, const double* coef,
+                           int64_t coef_stride, const double* x, double* hx, int64_t pair_begin,
+                           int64_t pair_end, void* stream) {
+  using namespace bmv;
+  if (!p || (!kinetic && !coef)) {
+    set_error("bmv_cellop_apply_pairs: null plan or empty operator");
     return BMV_ERR_INVALID;
   }
-  cudaStream_t st = as_stream(stream);
-  int rc = zero_async(hx, zero_len, st);
-  if (rc != BMV_OK || p->n_pairs == 0) return rc;
-  K1Args args{p->desc, p->codes, p->gtab, p->code_stride, p->gbytes, coef, coef_stride != 0 ? 1 : 0,
-              p->n_pairs, x, hx, nullptr, nullptr};
-  return dispatch(p, args, coef != nullptr, kinetic ? 0 : 1, st);
+  return run_pairs(p, kinetic ? 0 : 1, coef, coef_stride, nullptr, x, hx, nullptr, pair_begin,
+                   pair_end, as_stream(stream));
 }
 
 int bmv_cellop_apply_hm(bmv_cellop* p, const double* coef, int64_t coef_stride,
@@ -544,18 +575,23 @@ int bmv_cellop_apply_hm(bmv_cellop* p, const double* coef, int64_t coef_stride,
     set_error("bmv_cellop_apply_hm: null plan or mass coefficient");
     return BMV_ERR_INVALID;
   }
-  const int q3 = p->n * p->n * p->n, q3p = q3 + (q3 & 1);
-  if (coef && coef_stride != 0 && coef_stride != q3p) {
-    set_error("bmv_cellop_apply_hm: coefficient rows must have stride 0 or %d", q3p);
-    return BMV_ERR_INVALID;
-  }
   cudaStream_t st = as_stream(stream);
   int rc = zero_async(hx, zero_len, st);
   if (rc == BMV_OK) rc = zero_async(mx, zero_len, st);
-  if (rc != BMV_OK || p->n_pairs == 0) return rc;
-  K1Args args{p->desc, p->codes, p->gtab, p->code_stride, p->gbytes, coef, coef_stride != 0 ? 1 : 0,
-              p->n_pairs, x, hx, mx, mass_coef};
-  return dispatch(p, args, coef != nullptr, 2, st);
+  if (rc != BMV_OK) return rc;
+  return run_pairs(p, 2, coef, coef_stride, mass_coef, x, hx, mx, 0, p->n_pairs, st);
+}
+
+int bmv_cellop_apply_hm_pairs(bmv_cellop* p, const double* coef, int64_t coef_stride,
+                              const double* mass_coef, const double* x, double* hx, double* mx,
+                              int64_t pair_begin, int64_t pair_end, void* stream) {
+  using namespace bmv;
+  if (!p || !mass_coef) {
+    set_error("bmv_cellop_apply_hm_pairs: null plan or mass coefficient");
+    return BMV_ERR_INVALID;
+  }
+  return run_pairs(p, 2, coef, coef_stride, mass_coef, x, hx, mx, pair_begin, pair_end,
+                   as_stream(stream));
 }
 
 int bmv_cellop_launches(const bmv_cellop* p, int32_t* out) {

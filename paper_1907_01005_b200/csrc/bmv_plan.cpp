@@ -575,3 +575,190 @@ void bmvp_chunk_copy(const bmvp_chunks* c, int64_t* part_start, int64_t* chunk_m
 void bmvp_chunk_free(bmvp_chunks* c) { delete c; }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Active pairs, operator images and the K1 plan (matfree.py: ImageColumns,
+// CellOperator.active_pairs, _CellPlan), replacing sparse products over the
+// whole mesh.  Reference: the cell loop's column emission
+// (RowsBlockAccessor, matfree.py:159-237) restricted to the columns whose
+// support reaches the cell, and the grown pattern (localization.py:251-267)
+// at entry level.
+
+namespace {
+
+// columns of a sorted small list, deduplicated
+inline void sort_unique(std::vector<int32_t>& v) {
+  std::sort(v.begin(), v.end());
+  v.erase(std::unique(v.begin(), v.end()), v.end());
+}
+
+}  // namespace
+
+extern "C" {
+
+int bmvp_support_transpose(int64_t n_cols, const int64_t* col_ptr, const int64_t* col_rows,
+                           const int64_t* row_sel, int64_t n_sel, int64_t* ptr, int32_t* cols) {
+  // pass 1 (cols == NULL): ptr[s + 1] = columns of selected row s; pass 2: fill
+  if (n_cols < 0 || n_sel < 0) return 1;
+  if (!cols) {
+    std::memset(ptr, 0, sizeof(int64_t) * (size_t)(n_sel + 1));
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c = 0; c < n_cols; ++c)
+      for (int64_t i = col_ptr[c]; i < col_ptr[c + 1]; ++i) {
+        const int64_t s = row_sel[col_rows[i]];
+        if (s >= 0) {
+#pragma omp atomic
+          ptr[s + 1] += 1;
+        }
+      }
+    for (int64_t s = 0; s < n_sel; ++s) ptr[s + 1] += ptr[s];
+    return 0;
+  }
+  std::vector<int64_t> cur(ptr, ptr + n_sel);
+  // columns ascending per row: fill column by column in order (serial over
+  // columns keeps the order; rows in parallel would not)
+  for (int64_t c = 0; c < n_cols; ++c)
+    for (int64_t i = col_ptr[c]; i < col_ptr[c + 1]; ++i) {
+      const int64_t s = row_sel[col_rows[i]];
+      if (s >= 0) cols[cur[s]++] = (int32_t)c;
+    }
+  return 0;
+}
+
+int bmvp_cell_pairs(int64_t n_cells, int32_t n3, const int64_t* cell_rows, const int64_t* row_ptr,
+                    const int32_t* row_cols, int64_t* ptr, int32_t* cols) {
+  // cell_rows: (n_cells, n3) indices into the row CSR (-1: no row);
+  // pass 1 (cols == NULL) counts, pass 2 fills sorted unique columns per cell
+  if (n_cells < 0 || n3 <= 0) return 1;
+  if (!cols) {
+    ptr[0] = 0;
+#pragma omp parallel
+    {
+      std::vector<int32_t> v;
+#pragma omp for schedule(dynamic, 256)
+      for (int64_t c = 0; c < n_cells; ++c) {
+        v.clear();
+        for (int d = 0; d < n3; ++d) {
+          const int64_t r = cell_rows[c * n3 + d];
+          if (r >= 0) v.insert(v.end(), row_cols + row_ptr[r], row_cols + row_ptr[r + 1]);
+        }
+        sort_unique(v);
+        ptr[c + 1] = (int64_t)v.size();
+      }
+    }
+    for (int64_t c = 0; c < n_cells; ++c) ptr[c + 1] += ptr[c];
+    return 0;
+  }
+#pragma omp parallel
+  {
+    std::vector<int32_t> v;
+#pragma omp for schedule(dynamic, 256)
+    for (int64_t c = 0; c < n_cells; ++c) {
+      v.clear();
+      for (int d = 0; d < n3; ++d) {
+        const int64_t r = cell_rows[c * n3 + d];
+        if (r >= 0) v.insert(v.end(), row_cols + row_ptr[r], row_cols + row_ptr[r + 1]);
+      }
+      sort_unique(v);
+      std::copy(v.begin(), v.end(), cols + ptr[c]);
+    }
+  }
+  return 0;
+}
+
+int bmvp_block_image(int64_t n_cells, int32_t n3, const int64_t* cell_blocks,
+                     const int64_t* pair_ptr, const int32_t* pair_cols, int64_t n_blocks,
+                     int64_t n_cols, int64_t* ptr, int64_t* cols) {
+  // image(b) = union of pair_cols(c) over the cells c with cell_blocks[c][d] == b
+  // (cell_blocks: selected block index or -1).  pass 1 (cols == NULL) counts.
+  if (n_cells < 0 || n3 <= 0 || n_blocks < 0 || n_cols < 0) return 1;
+  const int64_t words = (n_cols + 63) / 64;
+  std::vector<uint64_t> bits((size_t)(n_blocks * words), 0);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t c = 0; c < n_cells; ++c) {
+    int64_t seen[64];
+    int ns = 0;
+    for (int d = 0; d < n3; ++d) {
+      const int64_t b = cell_blocks[c * n3 + d];
+      if (b < 0) continue;
+      bool dup = false;
+      for (int k = 0; k < ns; ++k) dup |= seen[k] == b;
+      if (dup) continue;
+      if (ns < 64) seen[ns++] = b;
+      uint64_t* w = bits.data() + b * words;
+      for (int64_t i = pair_ptr[c]; i < pair_ptr[c + 1]; ++i) {
+        const int64_t col = pair_cols[i];
+#pragma omp atomic
+        w[col >> 6] |= (uint64_t)1 << (col & 63);
+      }
+    }
+  }
+  if (!cols) {
+    ptr[0] = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < n_blocks; ++b) {
+      int64_t n = 0;
+      for (int64_t k = 0; k < words; ++k) n += __builtin_popcountll(bits[b * words + k]);
+      ptr[b + 1] = n;
+    }
+    for (int64_t b = 0; b < n_blocks; ++b) ptr[b + 1] += ptr[b];
+    return 0;
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < n_blocks; ++b) {
+    int64_t o = ptr[b];
+    for (int64_t k = 0; k < words; ++k) {
+      uint64_t w = bits[b * words + k];
+      while (w) {
+        const int t = __builtin_ctzll(w);
+        cols[o++] = k * 64 + t;
+        w &= w - 1;
+      }
+    }
+  }
+  return 0;
+}
+
+int bmvp_k1_plan(int64_t n_pairs, const int64_t* pair_cell, const int64_t* pair_col,
+                 const int64_t* cell_gstart, const int64_t* grp_block, const int64_t* src_ptr,
+                 const int64_t* src_cols, const int64_t* src_off, const int64_t* dst_ptr,
+                 const int64_t* dst_cols, const int64_t* dst_off, const int64_t* pair_gtab,
+                 int32_t* gtab, int64_t* bad_pair) {
+  // gtab[pair_gtab[p] + 2 g] = src slab offset + slot of the pair's column in
+  // group g's block row (-1 absent), [+1] = dst slab offset + slot (-1 -> error)
+  *bad_pair = -1;
+  int64_t bad = INT64_MAX;
+#pragma omp parallel for schedule(static) reduction(min : bad)
+  for (int64_t p = 0; p < n_pairs; ++p) {
+    const int64_t c = pair_cell[p], col = pair_col[p];
+    const int64_t g0 = cell_gstart[c], ng = cell_gstart[c + 1] - g0;
+    int32_t* t = gtab + pair_gtab[p];
+    for (int64_t g = 0; g < ng; ++g) {
+      const int64_t lb = grp_block[g0 + g];
+      const int64_t* sb = src_cols + src_ptr[lb];
+      const int64_t* se = src_cols + src_ptr[lb + 1];
+      const int64_t* s = std::lower_bound(sb, se, col);
+      t[2 * g] = (s != se && *s == col) ? (int32_t)(src_off[lb] + (s - sb)) : -1;
+      const int64_t* db = dst_cols + dst_ptr[lb];
+      const int64_t* de = dst_cols + dst_ptr[lb + 1];
+      const int64_t* q = std::lower_bound(db, de, col);
+      if (q == de || *q != col) {
+        bad = std::min(bad, p);
+        t[2 * g + 1] = 0;
+      } else {
+        t[2 * g + 1] = (int32_t)(dst_off[lb] + (q - db));
+      }
+    }
+    if (ng & 1) {
+      t[2 * ng] = -1;
+      t[2 * ng + 1] = 0;
+    }
+  }
+  if (bad != INT64_MAX) {
+    *bad_pair = bad;
+    return 3;
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -40,7 +40,7 @@ import torch
 from scipy import sparse
 
 from . import _lib
-from .bcsr import BlockCsrMatrix, RankLayout, build_rank_layout, serial_layout
+from .bcsr import BlockCsrMatrix, RankLayout, _zero_range, build_rank_layout, serial_layout
 from .blocks import BlockSparsityPattern
 from .counters import OpCounters
 from .errors import ConsistencyError, PatternError, ShapeError
@@ -358,6 +358,35 @@ class ImageColumns:
         return ("image", id(self.op), id(self.source))
 
     def columns_for(self, pattern, gblocks: np.ndarray):
+        from . import _plan
+
+        if _plan.enabled():
+            return self._columns_native(pattern, gblocks)
+        return self._columns_numpy(pattern, gblocks)
+
+    def _columns_native(self, pattern, gblocks: np.ndarray):
+        from . import _plan
+        from .support import ColumnSupport
+
+        op = self.op
+        blocks = op.numbering.row_blocks
+        gblocks = np.asarray(gblocks, dtype=np.int64)
+        cells = op.cells_touching_blocks(gblocks)
+        nodes = cells_nodes(op.mesh, op.numbering, cells)
+        nb, _ = _plan.blocks_of(blocks.starts, nodes)
+        if isinstance(self.source, ColumnSupport):
+            row_sel, rptr, rcols = op.support_rows(self.source, nodes)
+            pptr, pcols = _plan.cell_pairs(row_sel[nodes], rptr, rcols)
+        else:
+            touched = np.unique(nb)
+            sptr, scols = self.source.columns_for(pattern, touched)
+            pptr, pcols = _plan.cell_pairs(np.searchsorted(touched, nb), sptr, scols)
+        sel = np.full(blocks.n_blocks, -1, dtype=np.int64)
+        sel[gblocks] = np.arange(gblocks.size, dtype=np.int64)
+        return _plan.block_image(sel[nb], pptr, pcols, gblocks.size, pattern.col_blocks.total)
+
+    def _columns_numpy(self, pattern, gblocks: np.ndarray):
+        """numpy restatement of the native image (sparse products)."""
         from .support import ColumnSupport
 
         op = self.op
@@ -426,33 +455,55 @@ class _CellPlan:
                                   shape=(src.n_local_blocks, src.col_blocks.total))
             act = _bool_csr(inc @ s)
             self.support_based = False
-        p_cell = np.repeat(np.arange(n_cells, dtype=np.int64), np.diff(act.indptr))
-        p_col = act.indices.astype(np.int64)
+        # pair order: interior cells part A | cells with a ghost row | interior part B,
+        # so apply() runs A during the halo exchange of src and B during the compress
+        cnt = np.diff(act.indptr).astype(np.int64)
+        ghost = (op._lb >= op.layout.n_owned_blocks).any(axis=1) if n_cells else \
+            np.zeros(0, dtype=bool)
+        interior = np.flatnonzero(~ghost)
+        cum = np.cumsum(cnt[interior])
+        half = int(np.searchsorted(cum, cum[-1] // 2)) + 1 if interior.size and ghost.any() \
+            else interior.size
+        order = np.concatenate([interior[:half], np.flatnonzero(ghost), interior[half:]])
+        owner_c, k = _expand(cnt[order])
+        p_cell = order[owner_c]
+        p_col = act.indices[act.indptr[order][owner_c] + k].astype(np.int64)
         n_pairs = p_col.size
+        n_a = int(cnt[interior[:half]].sum())
+        self.split = (n_a, n_a + int(cnt[ghost].sum()))
         # per (pair, group): {src slab offset + slot | -1, dst slab offset + slot}
         pg = ng[p_cell]
         ngp = pg + (pg & 1)
         if ngp.size and int(ngp.max()) > 32:
             raise ConsistencyError("a cell touches more than 32 block rows")
-        owner, g = _expand(pg)
-        lb = op.grp_block[op.cell_gstart[p_cell][owner] + g]
-        col = p_col[owner]
-        zero = np.zeros(lb.size, dtype=np.int64)
-        xo = src.slab.offsets(lb, zero, col)
-        ho = dst.slab.offsets(lb, zero, col)
-        if (ho < 0).any():
-            bad = int(np.flatnonzero(ho < 0)[0])
-            raise PatternError(f"destination does not store column {int(col[bad])} in local "
-                               f"block row {int(lb[bad])} (reached by cell "
-                               f"{int(p_cell[owner[bad]])})")
-        if max(int(xo.max(initial=0)), int(ho.max(initial=0))) >= 2**31 - 2**20:
+        if max(int(src.slab.off[-1]), int(dst.slab.off[-1])) >= 2**31:
             raise ShapeError("K1 offsets exceed 2^31 elements")
         pair_gtab = np.concatenate([[0], np.cumsum(2 * ngp)]).astype(np.int64)
-        gtab = np.zeros(int(pair_gtab[-1]), dtype=np.int32)
-        gtab[0::2] = -1
-        at = pair_gtab[:-1][owner] + 2 * g
-        gtab[at] = xo
-        gtab[at + 1] = ho
+        from . import _plan
+
+        if _plan.enabled():
+            gtab, bad = _plan.k1_gtab(p_cell, p_col, op.cell_gstart, op.grp_block, src.slab,
+                                      dst.slab, pair_gtab[:-1], int(pair_gtab[-1]))
+            if bad >= 0:
+                raise PatternError(f"destination does not store column {int(p_col[bad])} in a "
+                                   f"block row reached by cell {int(p_cell[bad])}")
+        else:
+            owner, g = _expand(pg)
+            lb = op.grp_block[op.cell_gstart[p_cell][owner] + g]
+            col = p_col[owner]
+            zero = np.zeros(lb.size, dtype=np.int64)
+            xo = src.slab.offsets(lb, zero, col)
+            ho = dst.slab.offsets(lb, zero, col)
+            if (ho < 0).any():
+                bad = int(np.flatnonzero(ho < 0)[0])
+                raise PatternError(f"destination does not store column {int(col[bad])} in local "
+                                   f"block row {int(lb[bad])} (reached by cell "
+                                   f"{int(p_cell[owner[bad]])})")
+            gtab = np.zeros(int(pair_gtab[-1]), dtype=np.int32)
+            gtab[0::2] = -1
+            at = pair_gtab[:-1][owner] + 2 * g
+            gtab[at] = xo
+            gtab[at + 1] = ho
         # per (cell, DoF) codes: group, r * K_src, r * K_dst
         sgp = op.slot_group
         lbd, rib = op._lb, op._rib
@@ -569,6 +620,7 @@ class CellOperator:
         self._plans: dict = {}
         self._coefs: dict = {}
         self._act: dict = {}
+        self._rows: dict = {}
         self._images: dict = {}
         self._dev_tables = None
         self._node_of_dof = None
@@ -590,14 +642,44 @@ class CellOperator:
 
     def active_pairs(self, support) -> sparse.csr_matrix:
         """(owned cells x columns) bool CSR: the cell has a node in the column's support."""
+        from . import _plan
+
         hit = self._act.get(id(support))
         if hit is not None and hit[0] is support:
             return hit[1]
-        mask = support.local_mask(self.layout)
-        a_cell = self.cell_local_rows_matrix(mask.shape[0])
-        act = _bool_csr(a_cell @ mask.astype(np.int32))
+        if _plan.enabled():
+            nodes = cells_nodes(self.mesh, self.numbering, self.cells)
+            row_sel, rptr, rcols = self.support_rows(support, nodes)
+            ptr, cols = _plan.cell_pairs(row_sel[nodes], rptr, rcols)
+            act = sparse.csr_matrix((np.ones(cols.size, dtype=np.int8), cols.astype(np.int64), ptr),
+                                    shape=(len(self.cells), support.n_cols))
+        else:
+            mask = support.local_mask(self.layout)
+            a_cell = self.cell_local_rows_matrix(mask.shape[0])
+            act = _bool_csr(a_cell @ mask.astype(np.int32))
         self._act[id(support)] = (support, act)
         return act
+
+    def support_rows(self, support, nodes: np.ndarray):
+        """(row_sel, ptr, cols): the support's row -> columns CSR over the rows
+        of the cells touching this rank's block rows (native transpose; cached
+        per support).  `nodes` must lie in those rows."""
+        from . import _plan
+
+        hit = self._rows.get(id(support))
+        if hit is None or hit[0] is not support:
+            cells = self.cells_touching_blocks(self.layout.global_blocks_of_locals())
+            rows = cells_nodes(self.mesh, self.numbering, cells).ravel()
+            row_sel = np.full(self.numbering.n_dofs, -1, dtype=np.int64)
+            row_sel[rows] = 0
+            sel = np.flatnonzero(row_sel == 0)
+            row_sel[sel] = np.arange(sel.size, dtype=np.int64)
+            ptr, cols = _plan.support_transpose(support, row_sel, sel.size)
+            hit = (support, row_sel, ptr, cols)
+            self._rows[id(support)] = hit
+        if (hit[1][nodes] < 0).any():
+            raise ConsistencyError("support_rows: rows outside the rank's neighbourhood")
+        return hit[1], hit[2], hit[3]
 
     def image_columns(self, source) -> ImageColumns:
         """Stored-column spec of H X for a source X stored with spec `source`
@@ -738,30 +820,52 @@ class CellOperator:
 
     def apply(self, spec: OperatorSpec, src: BlockCsrMatrix, dst: BlockCsrMatrix,
               variant: str = SUMFAC, counters: OpCounters | None = None):
-        """dst = Op(spec) @ src over the rank's cells, then compress dst."""
+        """dst = Op(spec) @ src over the rank's cells, then compress dst
+        (reference matfree.py:458-527).  With ghost rows the exchanges overlap
+        the cell loop: src's ghost update is in flight while the cells
+        touching no ghost row (part A) run, the compress of dst while part B
+        runs; the cells with ghost rows run in between."""
         self._check_operands(spec, src, dst, variant)
         lib = _lib.require_device()
         dst.ensure_owned()
         plan = self.plan_for(src, dst)
         coef, stride = self.coefficient(spec, dst.device)
-        src.update_ghost_values()
-        _lib.check(lib.bmv_cellop_apply(
-            plan.handle.raw, 1 if spec.kind == HAMILTONIAN else 0,
-            _lib.dptr(coef) if coef is not None else C.c_void_p(None), stride,
-            _lib.dptr(src.data), _lib.dptr(dst.data), dst.data.numel(),
-            _lib.stream_handle(dst.device)), "bmv_cellop_apply")
-        src.release_ghosts()
-        dst.support = None
-        dst.compress()
+        kin = 1 if spec.kind == HAMILTONIAN else 0
+        cp = _lib.dptr(coef) if coef is not None else C.c_void_p(None)
+        stream = _lib.stream_handle(dst.device)
+
+        def run(p0, p1):
+            _lib.check(lib.bmv_cellop_apply_pairs(
+                plan.handle.raw, kin, cp, stride, _lib.dptr(src.data), _lib.dptr(dst.data), p0, p1,
+                stream), "bmv_cellop_apply_pairs")
+
+        self._overlapped(plan, src, (dst,), run)
         if counters is not None:
             self._count(spec, variant, plan, src, dst, counters)
+
+    def _overlapped(self, plan, src, dsts, run):
+        """zero dsts | src ghost update || part A | boundary | compress dsts || part B."""
+        for d in dsts:
+            _zero_range(d.data, 0, d.data.numel())
+        a_end, b_beg = plan.split
+        src.update_ghost_values_start()
+        run(0, a_end)
+        src.update_ghost_values_finish()
+        run(a_end, b_beg)
+        for d in dsts:
+            d.support = None
+            d.compress_start()
+        run(b_beg, plan.n_pairs)
+        src.release_ghosts()
+        for d in dsts:
+            d.compress_finish()
 
     def apply_h_and_mass(self, spec: OperatorSpec, src: BlockCsrMatrix, hdst: BlockCsrMatrix,
                          mdst: BlockCsrMatrix, counters: OpCounters | None = None):
         """hdst = H(spec) @ src and mdst = M @ src (the two products
         compute_energy forms, reference energy.py:129-174), fused: one gather
         of src and one interpolation to the quadrature points feed both
-        (bmv_cellop_apply_hm).  When the destinations store different
+        (bmv_cellop_apply_hm_pairs).  When the destinations store different
         entries it runs the two applies instead; the choice depends only on
         the operands' storage, which every rank shares, so all ranks run the
         same exchange sequence."""
@@ -780,17 +884,16 @@ class CellOperator:
         mdst.ensure_owned()
         coef, stride = self.coefficient(spec, hdst.device)
         mcoef, _ = self.coefficient(mass_operator(), hdst.device)
-        src.update_ghost_values()
-        _lib.check(lib.bmv_cellop_apply_hm(
-            plan.handle.raw, _lib.dptr(coef) if coef is not None else C.c_void_p(None),
-            stride, _lib.dptr(mcoef), _lib.dptr(src.data), _lib.dptr(hdst.data),
-            _lib.dptr(mdst.data), hdst.data.numel(), _lib.stream_handle(hdst.device)),
-            "bmv_cellop_apply_hm")
-        src.release_ghosts()
-        hdst.support = None
-        mdst.support = None
-        hdst.compress()
-        mdst.compress()
+        cp = _lib.dptr(coef) if coef is not None else C.c_void_p(None)
+        stream = _lib.stream_handle(hdst.device)
+
+        def run(p0, p1):
+            _lib.check(lib.bmv_cellop_apply_hm_pairs(
+                plan.handle.raw, cp, stride, _lib.dptr(mcoef), _lib.dptr(src.data),
+                _lib.dptr(hdst.data), _lib.dptr(mdst.data), p0, p1, stream),
+                "bmv_cellop_apply_hm_pairs")
+
+        self._overlapped(plan, src, (hdst, mdst), run)
         if counters is not None:
             self._count(spec, SUMFAC, plan, src, hdst, counters)
             self._count(mass_operator(), SUMFAC, plan, src, mdst, counters)

@@ -92,10 +92,12 @@ def to_original_columns(dense, layout):
 def emulated_apply(op, potential, kind, src, dst):
     """CPU emulation of CellOperator.apply for CPU-resident matrices (tests only).
 
-    Same sequence as the product (zero dst, update src ghosts, K1 plan over
-    (cell, column) pairs, release src ghosts, compress dst) with the cell
-    integral taken from the numpy oracle.  Exercises the host plan and the
-    rank-context exchange without a GPU.
+    The product's own sequence (CellOperator._overlapped: zero dst, src ghost
+    update in flight during the interior part A of the cell loop, boundary
+    cells, dst compress in flight during part B, release src ghosts) over
+    the K1 plan's (cell, column) pairs, with the cell integral taken from the
+    numpy oracle.  Exercises the host plan and the rank-context exchange in
+    the overlapped order without a GPU.
     """
     import torch
 
@@ -105,12 +107,13 @@ def emulated_apply(op, potential, kind, src, dst):
     deg = op.shape.degree
     n3 = (deg + 1) ** 3
     dst.ensure_owned()
-    dst.zero_out()
-    src.update_ghost_values()
     plan = _CellPlan(op, src, dst, upload=False)
     a = plan.arrays
-    if plan.n_pairs:
-        cell = a["pair_cell"].astype(np.int64)
+
+    def run(p0, p1):
+        if p1 <= p0:
+            return
+        cell = a["pair_cell"][p0:p1].astype(np.int64)
         codes = a["codes"].reshape(-1, plan.code_stride)[cell].astype(np.int64)
         if plan.wide:
             w0, w1 = codes[:, 0 : 2 * n3 : 2], codes[:, 1 : 2 * n3 : 2]
@@ -119,7 +122,7 @@ def emulated_apply(op, potential, kind, src, dst):
             c = codes[:, :n3]
             g, rx, rh = c >> 27, (c >> 14) & 0x1FFF, c & 0x3FFF
         gt = a["gtab"].astype(np.int64)
-        base = a["pair_gtab"][:, None] + 2 * g
+        base = a["pair_gtab"][p0:p1, None] + 2 * g
         xo, ho = gt[base], gt[base + 1]
         X = src.data.numpy()
         u = np.where(xo >= 0, X[np.maximum(xo, 0) + rx], 0.0)
@@ -130,6 +133,6 @@ def emulated_apply(op, potential, kind, src, dst):
         H = dst.data.numpy().copy()
         np.add.at(H, (ho + rh).ravel(), out.ravel())
         dst.data.copy_(torch.from_numpy(H))
-    src.release_ghosts()
-    dst.compress()
+
+    op._overlapped(plan, src, (dst,), run)
     return plan

@@ -257,16 +257,21 @@ def digest(a):
     return hashlib.sha256(np.ascontiguousarray(np.asarray(a, dtype=np.int64)).tobytes()).hexdigest()
 
 
-def make_digests():
+def make_digests(only=None):
     cfgs = {
         "q2": ((32, 32, 32), (1 / 32,) * 3, 2, lattice((4, 4, 4), 0.25, 0.125), 0.25, 1),
         "q4": ((32, 32, 32), (1 / 32,) * 3, 4, lattice((4, 4, 4), 0.25, 0.125), 0.25, 1),
         "proj": ((64, 64, 64), (1 / 64,) * 3, 2, lattice((8, 8, 8), 1 / 8, 1 / 16), 1.5 / 8, 1),
         "weak1": ((64, 64, 64), (1 / 64,) * 3, 4, lattice((8, 8, 8), 8 / 64, 4 / 64), 8 / 64, 1),
         "weak2": ((64, 64, 128), (1 / 64,) * 3, 4, lattice((8, 8, 16), 8 / 64, 4 / 64), 8 / 64, 2),
+        "weak4": ((64, 64, 256), (1 / 64,) * 3, 4, lattice((8, 8, 32), 8 / 64, 4 / 64), 8 / 64, 4),
+        "weak8": ((64, 64, 512), (1 / 64,) * 3, 4, lattice((8, 8, 64), 8 / 64, 4 / 64), 8 / 64, 8),
     }
-    res = {}
+    path = OUT / "digests.json"
+    res = json.loads(path.read_text()) if (only and path.exists()) else {}
     for name, (ext, sp, deg, centers, radius, nr) in cfgs.items():
+        if only and name not in only:
+            continue
         t0 = time.time()
         mesh, part, num, lay, sup, pat, gro = setup(ext, sp, 0, deg, centers, radius, 1, 8, nr)
         arrays = structure_arrays("", part, num, lay, sup, pat, gro)
@@ -279,7 +284,7 @@ def make_digests():
                                "grown_blocks": int(gro.col_index.size),
                                "support_nnz": int(sum(s.size for s in sup))}
         print(name, "%.1fs" % (time.time() - t0), res[name]["_sizes"], flush=True)
-    (OUT / "digests.json").write_text(json.dumps(res, indent=1, sort_keys=True))
+        path.write_text(json.dumps(res, indent=1, sort_keys=True))
 
 
 if __name__ == "__main__":
@@ -292,3 +297,6 @@ if __name__ == "__main__":
         make_random()
     if "digests" in which:
         make_digests()
+    extra = [w for w in which if w.startswith("weak") or w in ("q2", "q4", "proj")]
+    if extra:  # e.g. `python make_golden.py weak4 weak8`: add those digests to digests.json
+        make_digests(extra)

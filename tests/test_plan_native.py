@@ -188,3 +188,56 @@ def test_fill_multivector_device_scatter_equals_host_image(name, n_ranks):
         return bool(torch.equal(a.data.cpu(), b.data))
 
     assert all(run_ranks(n_ranks, prog, device=dev))
+
+
+@pytest.mark.parametrize("name", ["smoke", "q2"])
+def test_native_pairs_images_and_k1_tables_equal_numpy(monkeypatch, name):
+    """bmvp_cell_pairs / bmvp_block_image / bmvp_k1_plan against the sparse-product
+    restatements (active pairs, ImageColumns, K1 group tables)."""
+    from paper_1907_01005_b200 import problem as P
+    from paper_1907_01005_b200.comm import serial_context
+    from paper_1907_01005_b200.matfree import CellOperator, ImageColumns, _CellPlan
+    from paper_1907_01005_b200.slabs import FULL
+
+    prob = P.build_problem(name)
+    st = P.make_rank_setup(serial_context("cpu"), prob, device="cpu", projection=False)
+    op = st.op
+    gb = st.layout.global_blocks_of_locals()
+    sup = prob.column_support
+    nat = {}
+    for native in ("1", "0"):
+        monkeypatch.setenv("BMV_PLAN_NATIVE", native)
+        fresh = CellOperator(prob.mesh, prob.partition, prob.numbering, st.layout)
+        act = fresh.active_pairs(sup)
+        img = ImageColumns(fresh, sup).columns_for(prob.grown, gb)
+        img_full = ImageColumns(fresh, FULL).columns_for(prob.grown, gb)
+        plan = _CellPlan(fresh, st.x, st.hx, upload=False)
+        nat[native] = (act, img, img_full, plan.arrays)
+    a1, a0 = nat["1"][0], nat["0"][0]
+    assert np.array_equal(a1.indptr, a0.indptr) and np.array_equal(a1.indices, a0.indices)
+    for k in (1, 2):
+        assert np.array_equal(nat["1"][k][0], nat["0"][k][0])
+        assert np.array_equal(nat["1"][k][1], nat["0"][k][1])
+    for key in ("pair_cell", "pair_gtab", "pair_ngp", "gtab", "codes"):
+        assert np.array_equal(nat["1"][3][key], nat["0"][3][key]), key
+
+
+def test_images_at_two_ranks_agree_with_the_owner(monkeypatch):
+    """ImageColumns is defined per GLOBAL block row: a ghost copy on rank 1
+    stores exactly the owner's columns (whole slab rows travel in exchanges)."""
+    from paper_1907_01005_b200 import problem as P
+    from paper_1907_01005_b200.comm import run_ranks
+
+    prob = P.build_problem("smoke", 2)
+
+    def program(ctx):
+        st = P.make_rank_setup(ctx, prob, device="cpu", projection=False)
+        gb = st.layout.global_blocks_of_locals()
+        sg = st.hx.slab
+        return {int(b): sg.cols[sg.ptr[i]:sg.ptr[i + 1]].tolist() for i, b in enumerate(gb)}
+
+    r0, r1 = run_ranks(2, program)
+    shared = set(r0) & set(r1)
+    assert shared  # the ranks share ghost block rows
+    for b in shared:
+        assert r0[b] == r1[b], b

@@ -420,10 +420,9 @@ bmvp_chunks* bmvp_chunk_plan(int32_t kind, int64_t n_rows, const int64_t* rows,
       if (it == mk.end()) mk.push_back(lb);
     }
     const int64_t NK = (int64_t)mk.size();
-    const int64_t tab_w = k4 ? 2 * nrows : nrows;
-    const int64_t yrow_w = k4 ? 0 : nrows;
+    const int64_t seg_w = 8 * nbr;
     const int64_t cma_w = (nbr * UA + 1) / 2, cmb_w = (nbr * UB + 1) / 2;
-    int64_t words = 16 + tab_w + yrow_w + cma_w + cmb_w + 2 * UA + NK * UB;
+    int64_t words = 16 + seg_w + cma_w + cmb_w + 2 * UA + NK * UB;
     words = (words + 3) / 4 * 4;
     // staged ranges (doubles, even bounds)
     const Segment& s0 = seg.front();
@@ -438,7 +437,7 @@ bmvp_chunks* bmvp_chunk_plan(int32_t kind, int64_t n_rows, const int64_t* rows,
       b1 = (b1 + 1) & ~int64_t(1);
     }
     const int64_t total = 4 * words + 8 * (a1 - a0) + 8 * (b1 - b0);
-    if (total > stage_bytes || UA > 32767 || UB > 32767 || nrows > (k4 ? 4096 : 32)) {
+    if (total > stage_bytes || UA > 32767 || UB > 32767 || nrows > 4096) {
       // split and retry (rows or block rows)
       if (nbr > 1) {
         std::vector<Segment> h1(seg.begin(), seg.begin() + nbr / 2), h2(seg.begin() + nbr / 2, seg.end());
@@ -462,58 +461,42 @@ bmvp_chunks* bmvp_chunk_plan(int32_t kind, int64_t n_rows, const int64_t* rows,
     int32_t* m = out->meta.data() + base;
     const int64_t aoff = 4 * words, boff = aoff + 8 * (a1 - a0);
     int64_t w = 16;
-    m[0] = (int32_t)nrows;
-    m[1] = (int32_t)nbr;
+    m[0] = (int32_t)nbr;
+    m[1] = (int32_t)nrows;
     m[2] = (int32_t)UA;
     m[3] = (int32_t)UB;
     m[4] = (int32_t)NK;
     m[5] = (int32_t)aoff;
     m[6] = (int32_t)boff;
-    m[7] = (int32_t)UA;
-    m[8] = (int32_t)UB;
-    m[9] = (int32_t)w;  // row table
-    int64_t row = 0;
+    m[7] = (int32_t)w;  // segment records: {rows, A offset, K_A, B / Y offset, K_B, 0, 0, 0}
     for (int64_t bi = 0; bi < nbr; ++bi) {
       const Segment& s = seg[bi];
-      for (int64_t r = s.r0; r < s.r1; ++r, ++row) {
-        const int64_t ar = a_off[s.row] + r * width_of(A, s.row) - a0;
-        if (k4) {
-          const int64_t br = b_off[s.row] + r * width_of(B, s.row) - b0;
-          m[w + 2 * row] = (int32_t)(bi | (ar << 8));
-          m[w + 2 * row + 1] = (int32_t)br;
-        } else {
-          m[w + row] = (int32_t)(bi | (ar << 8));
-        }
+      const int64_t ar = a_off[s.row] + s.r0 * width_of(A, s.row) - a0;
+      // K4: B offset in the stage; K5: element offset of the segment's first row in Y
+      const int64_t br = b_off[s.row] + s.r0 * width_of(B, s.row) - (k4 ? b0 : 0);
+      if (br > INT32_MAX) {
+        out->status = 5;
+        return out;
       }
+      int32_t* r = m + w + 8 * bi;
+      r[0] = (int32_t)(s.r1 - s.r0);
+      r[1] = (int32_t)ar;
+      r[2] = (int32_t)width_of(A, s.row);
+      r[3] = (int32_t)br;
+      r[4] = (int32_t)width_of(B, s.row);
     }
-    w += tab_w;
-    if (!k4) {
-      m[15] = (int32_t)w;  // Y row offsets
-      row = 0;
-      for (int64_t bi = 0; bi < nbr; ++bi) {
-        const Segment& s = seg[bi];
-        for (int64_t r = s.r0; r < s.r1; ++r, ++row) {
-          const int64_t yo = b_off[s.row] + r * width_of(B, s.row);
-          if (yo > INT32_MAX) {
-            out->status = 5;
-            return out;
-          }
-          m[w + row] = (int32_t)yo;
-        }
-      }
-      w += yrow_w;
-    }
-    m[10] = (int32_t)w;  // A colmap
+    w += seg_w;
+    m[8] = (int32_t)w;  // A colmap
     int16_t* cma = reinterpret_cast<int16_t*>(m + w);
     for (int64_t bi = 0; bi < nbr; ++bi)
       for (int64_t a = 0; a < UA; ++a) cma[bi * UA + a] = (int16_t)slot_of(A, seg[bi].row, ua[a]);
     w += cma_w;
-    m[11] = (int32_t)w;  // B / Y colmap
+    m[9] = (int32_t)w;  // B / Y colmap
     int16_t* cmb = reinterpret_cast<int16_t*>(m + w);
     for (int64_t bi = 0; bi < nbr; ++bi)
       for (int64_t b = 0; b < UB; ++b) cmb[bi * UB + b] = (int16_t)slot_of(B, seg[bi].row, ub[b]);
     w += cmb_w;
-    m[12] = (int32_t)w;
+    m[10] = (int32_t)w;
     for (int64_t a = 0; a < UA; ++a) {
       if (rb[a] > INT32_MAX) {
         out->status = 5;
@@ -522,10 +505,10 @@ bmvp_chunks* bmvp_chunk_plan(int32_t kind, int64_t n_rows, const int64_t* rows,
       m[w + a] = (int32_t)rb[a];
     }
     w += UA;
-    m[13] = (int32_t)w;
+    m[11] = (int32_t)w;
     for (int64_t a = 0; a < UA; ++a) m[w + a] = (int32_t)kk[a];
     w += UA;
-    m[14] = (int32_t)w;
+    m[12] = (int32_t)w;
     for (int64_t k = 0; k < NK; ++k)
       for (int64_t b = 0; b < UB; ++b) m[w + k * UB + b] = (int32_t)slot_of(M, mk[k], ub[b]);
     out->chunk_meta.push_back(base + words);
@@ -536,7 +519,9 @@ bmvp_chunks* bmvp_chunk_plan(int32_t kind, int64_t n_rows, const int64_t* rows,
       out->chunk_b.push_back(b1);
     }
     const int64_t ta = (UA + 7) / 8, tb = (UB + 7) / 8;
-    const int64_t dm = k4 ? ta * tb * ((nrows + 3) / 4) : ((UA + 3) / 4) * tb * ((nrows + 7) / 8);
+    int64_t steps = 0;  // DMMA k-steps (K4, 4 rows) / row tiles (K5, 8 rows), segments padded
+    for (const Segment& s : seg) steps += k4 ? (s.r1 - s.r0 + 3) / 4 : (s.r1 - s.r0 + 7) / 8;
+    const int64_t dm = k4 ? ta * tb * steps : ((UA + 3) / 4) * tb * steps;
     out->dmma += dm;
     out->cost.push_back((double)(8 * (a1 - a0) + 8 * (b1 - b0) + 4 * words) + 32.0 * (double)dm);
   }

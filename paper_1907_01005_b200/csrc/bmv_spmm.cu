@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "bmv.h"
 #include "bmv_common.cuh"
@@ -30,226 +31,282 @@
 namespace bmv {
 namespace {
 
-constexpr int kCW = 8;            // consumer warps per CTA
-constexpr int kNS = 2 * kCW;      // stages (two per consumer warp)
+constexpr int kCW = 12;           // consumer warps per CTA
+constexpr int kNS = 20;           // stages (kNS - kCW chunks of lookahead)
 
+// Per-chunk copy descriptors (built once in bmv_chunk_plan_create), structure
+// of arrays so that the producer warp fetches 32 chunks per coalesced load.
 struct ChunkArgs {
   const int64_t* part_start;  // n_parts + 1
-  const int64_t* meta_off;    // n_chunks + 1 (int32 units, multiples of 4)
+  const int64_t* m0;          // first meta word
+  const int64_t* a0;          // first staged A element
+  const int64_t* b0;          // first staged B element (K4)
+  const uint32_t* mb;         // meta bytes (= byte offset of A in the stage)
+  const uint32_t* ab;         // A bytes
+  const uint32_t* bb;         // B bytes (K4; 0 for K5)
   const int32_t* meta;
-  const int64_t* a_rng;       // n_chunks x 2 (doubles, 16-byte aligned bounds)
-  const int64_t* b_rng;       // K4: n_chunks x 2; K5: null
   int stage_bytes;
 };
 
 // Chunk header (int32): see include/bmv.h (bmv_chunk_desc)
-enum { H_NROWS = 0, H_NBR, H_UA, H_UB, H_NK, H_AOFF, H_BOFF, H_UAP, H_UBP, H_TAB, H_CMA, H_CMB,
-       H_RB, H_KK, H_ST, H_YROW };
+enum { H_NSEG = 0, H_NROWS, H_UA, H_UB, H_NK, H_AOFF, H_BOFF, H_SEG, H_CMA, H_CMB, H_RB, H_KK,
+       H_ST };
 
+// Producer warp: lane l prefetches the descriptors of chunk base + l, lane 0
+// issues the bulk copies (no dependent global load per chunk).
 __device__ __forceinline__ void producer(const ChunkArgs& g, const double* a, const double* b,
                                          char* stages, uint64_t* full, uint64_t* empty,
-                                         int64_t c0, int64_t n) {
-  for (int64_t j = 0; j < n; ++j) {
-    const int s = (int)(j % kNS);
-    if (j >= kNS) mbar_wait(&empty[s], (unsigned)((j / kNS - 1) & 1));
-    const int64_t c = c0 + j;
-    char* st = stages + (int64_t)s * g.stage_bytes;
-    const int64_t m0 = g.meta_off[c], m1 = g.meta_off[c + 1];
-    const unsigned mb = (unsigned)((m1 - m0) * 4);
-    const int32_t* mh = g.meta + m0;
-    const int aoff = __ldg(mh + H_AOFF), boff = __ldg(mh + H_BOFF);
-    const int64_t a0 = g.a_rng[2 * c], a1 = g.a_rng[2 * c + 1];
-    const unsigned ab = (unsigned)((a1 - a0) * 8);
-    unsigned bb = 0;
-    int64_t b0 = 0;
-    if (g.b_rng) {
-      b0 = g.b_rng[2 * c];
-      bb = (unsigned)((g.b_rng[2 * c + 1] - b0) * 8);
+                                         int64_t c0, int64_t n, int lane) {
+  for (int64_t base = 0; base < n; base += 32) {
+    const int64_t c = c0 + base + lane;
+    const bool ok = base + lane < n;
+    const int64_t m0 = ok ? __ldg(g.m0 + c) : 0;
+    const int64_t a0 = ok ? __ldg(g.a0 + c) : 0;
+    const int64_t b0 = (ok && g.b0) ? __ldg(g.b0 + c) : 0;
+    const unsigned mb = ok ? __ldg(g.mb + c) : 0u;
+    const unsigned ab = ok ? __ldg(g.ab + c) : 0u;
+    const unsigned bb = (ok && g.bb) ? __ldg(g.bb + c) : 0u;
+    const int cnt = (int)min((int64_t)32, n - base);
+    for (int k = 0; k < cnt; ++k) {
+      const int64_t km0 = __shfl_sync(~0u, m0, k), ka0 = __shfl_sync(~0u, a0, k),
+                    kb0 = __shfl_sync(~0u, b0, k);
+      const unsigned kmb = __shfl_sync(~0u, mb, k), kab = __shfl_sync(~0u, ab, k),
+                     kbb = __shfl_sync(~0u, bb, k);
+      if (lane == 0) {
+        const int64_t j = base + k;
+        const int s = (int)(j % kNS);
+        if (j >= kNS) mbar_wait(&empty[s], (unsigned)((j / kNS - 1) & 1));
+        char* st = stages + (int64_t)s * g.stage_bytes;
+        mbar_expect_tx(&full[s], kmb + kab + kbb);
+        bulk_g2s(st, g.meta + km0, kmb, &full[s]);
+        if (kab) bulk_g2s(st + kmb, a + ka0, kab, &full[s]);
+        if (kbb) bulk_g2s(st + kmb + kab, b + kb0, kbb, &full[s]);
+      }
     }
-    mbar_expect_tx(&full[s], mb + ab + bb);
-    bulk_g2s(st, mh, mb, &full[s]);
-    for (unsigned k = 0; k < ab; k += 65536u)
-      bulk_g2s(st + aoff + k, a + a0 + k / 8, min(65536u, ab - k), &full[s]);
-    for (unsigned k = 0; k < bb; k += 65536u)
-      bulk_g2s(st + boff + k, b + b0 + k / 8, min(65536u, bb - k), &full[s]);
   }
 }
 
 // ---------------------------------------------------------------- K4 -----
-// S[rb[a] + st[kk[a]][b]] += sum_rows A[row][cma[row][a]] * B[row][cmb[row][b]]
-__device__ __forceinline__ void k4_chunk(const char* st, double* __restrict__ c, int lane) {
-  const int32_t* m = reinterpret_cast<const int32_t*>(st);
-  const int nrows = m[H_NROWS], ua = m[H_UA], ub = m[H_UB];
-  const int uap = m[H_UAP], ubp = m[H_UBP];
+// S[rb[a] + st[kk[a]][b]] += sum_rows A[row][cma[seg][a]] * B[row][cmb[seg][b]]
+// One pass: union columns [ag, ag + 8 TA) x [bg, bg + 8 TB); accumulators
+// live in registers over every segment of the chunk.  Segments are padded
+// to multiples of 4 rows (a DMMA k-step never straddles two block rows).
+template <int TA, int TB>
+__device__ __forceinline__ void k4_pass(const int32_t* m, double* __restrict__ c, int ag, int bg,
+                                        int lane) {
+  const int nseg = m[H_NSEG], ua = m[H_UA], ub = m[H_UB];
+  const char* st = reinterpret_cast<const char*>(m);
   const double* As = reinterpret_cast<const double*>(st + m[H_AOFF]);
   const double* Bs = reinterpret_cast<const double*>(st + m[H_BOFF]);
-  const int32_t* tab = m + m[H_TAB];            // per row: bi | a_row << 8, then b_row
+  const int4* seg = reinterpret_cast<const int4*>(m + m[H_SEG]);
   const int16_t* cma = reinterpret_cast<const int16_t*>(m + m[H_CMA]);
   const int16_t* cmb = reinterpret_cast<const int16_t*>(m + m[H_CMB]);
+  const int g4 = lane >> 2, t4 = lane & 3;
+  double acc[TA][TB][2];
+#pragma unroll
+  for (int t = 0; t < TA; ++t)
+#pragma unroll
+    for (int u = 0; u < TB; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+  for (int s = 0; s < nseg; ++s) {
+    const int4 r0 = seg[2 * s];
+    const int kb = m[m[H_SEG] + 8 * s + 4];
+    const int nrows = r0.x, ka = r0.z;
+    int oa[TA], ob[TB];
+    bool va[TA], vb[TB];
+#pragma unroll
+    for (int t = 0; t < TA; ++t) {
+      const int aa = ag + t * 8 + g4;
+      const int sl = aa < ua ? cma[s * ua + aa] : -1;
+      va[t] = sl >= 0;
+      oa[t] = r0.y + t4 * ka + sl;
+    }
+#pragma unroll
+    for (int u = 0; u < TB; ++u) {
+      const int bb = bg + u * 8 + g4;
+      const int sl = bb < ub ? cmb[s * ub + bb] : -1;
+      vb[u] = sl >= 0;
+      ob[u] = r0.w + t4 * kb + sl;
+    }
+    const int nks = (nrows + 3) >> 2;
+    int xa = 0, xb = 0;
+    for (int ks = 0; ks < nks; ++ks, xa += 4 * ka, xb += 4 * kb) {
+      const bool rok = ks * 4 + t4 < nrows;
+      double av[TA], bv[TB];
+#pragma unroll
+      for (int t = 0; t < TA; ++t) av[t] = (rok && va[t]) ? As[oa[t] + xa] : 0.0;
+#pragma unroll
+      for (int u = 0; u < TB; ++u) bv[u] = (rok && vb[u]) ? Bs[ob[u] + xb] : 0.0;
+#pragma unroll
+      for (int t = 0; t < TA; ++t)
+#pragma unroll
+        for (int u = 0; u < TB; ++u) dmma_8x8x4(acc[t][u][0], acc[t][u][1], av[t], bv[u]);
+    }
+  }
+  // flush: lane holds rows a = ag + 8t + g4, columns b = bg + 8u + 2 t4 + {0, 1}
   const int32_t* rb = m + m[H_RB];
   const int32_t* kk = m + m[H_KK];
   const int32_t* stt = m + m[H_ST];
-  const int nks = (nrows + 3) >> 2;
-  const int g4 = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int t = 0; t < TA; ++t) {
+    const int aa = ag + t * 8 + g4;
+    if (aa >= ua) continue;
+    const int base = rb[aa];
+    const int32_t* srow = stt + kk[aa] * ub;
+#pragma unroll
+    for (int u = 0; u < TB; ++u) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int bb = bg + u * 8 + 2 * t4 + e;
+        if (bb < ub) {
+          const int sl = srow[bb];
+          if (sl >= 0) atomicAdd(c + (int64_t)base + sl, acc[t][u][e]);
+        }
+      }
+    }
+  }
+}
+
+template <int TA>
+__device__ __forceinline__ void k4_pass_b(const int32_t* m, double* c, int ag, int bg, int tb,
+                                          int lane) {
+  switch (tb) {
+    case 1: k4_pass<TA, 1>(m, c, ag, bg, lane); break;
+    case 2: k4_pass<TA, 2>(m, c, ag, bg, lane); break;
+    case 3: k4_pass<TA, 3>(m, c, ag, bg, lane); break;
+    default: k4_pass<TA, 4>(m, c, ag, bg, lane); break;
+  }
+}
+
+__device__ __forceinline__ void k4_chunk(const char* st, double* __restrict__ c, int lane) {
+  const int32_t* m = reinterpret_cast<const int32_t*>(st);
+  const int ua = m[H_UA], ub = m[H_UB];
   for (int ag = 0; ag < ua; ag += 32) {
     const int ta = min(4, (ua - ag + 7) >> 3);
     for (int bg = 0; bg < ub; bg += 32) {
       const int tb = min(4, (ub - bg + 7) >> 3);
-      double acc[4][4][2];
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
-      int cur_bi = -1;
-      int sa[4] = {-1, -1, -1, -1}, sb[4] = {-1, -1, -1, -1};
-      for (int ks = 0; ks < nks; ++ks) {
-        const int row = ks * 4 + t4;
-        int bi = -1, ar = 0, br = 0;
-        if (row < nrows) {
-          const int e = tab[2 * row];
-          bi = e & 255;
-          ar = e >> 8;
-          br = tab[2 * row + 1];
-        }
-        if (bi != cur_bi) {  // colmaps of this lane's block row (reused while it stays)
-          cur_bi = bi;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int aa = ag + t * 8 + g4;
-            sa[t] = (bi >= 0 && t < ta && aa < ua) ? cma[bi * uap + aa] : -1;
-            const int bb2 = bg + t * 8 + g4;
-            sb[t] = (bi >= 0 && t < tb && bb2 < ub) ? cmb[bi * ubp + bb2] : -1;
-          }
-        }
-        double av[4], bv[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          av[t] = sa[t] >= 0 ? As[ar + sa[t]] : 0.0;
-          bv[t] = sb[t] >= 0 ? Bs[br + sb[t]] : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (t < ta && u < tb) dmma_8x8x4(acc[t][u][0], acc[t][u][1], av[t], bv[u]);
-      }
-      // flush: lane holds rows a = ag + 8t + g4, columns b = bg + 8u + 2 t4 + {0, 1}
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int aa = ag + t * 8 + g4;
-        if (t >= ta || aa >= ua) continue;
-        const int base = rb[aa];
-        const int32_t* srow = stt + kk[aa] * ubp;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (u >= tb) continue;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int bb2 = bg + u * 8 + 2 * t4 + e;
-            if (bb2 < ub) {
-              const int sl = srow[bb2];
-              if (sl >= 0) atomicAdd(c + (int64_t)base + sl, acc[t][u][e]);
-            }
-          }
-        }
+      switch (ta) {
+        case 1: k4_pass_b<1>(m, c, ag, bg, tb, lane); break;
+        case 2: k4_pass_b<2>(m, c, ag, bg, tb, lane); break;
+        case 3: k4_pass_b<3>(m, c, ag, bg, tb, lane); break;
+        default: k4_pass_b<4>(m, c, ag, bg, tb, lane); break;
       }
     }
   }
 }
 
 // ---------------------------------------------------------------- K5 -----
-// Y[yrow[row] + cmy[row][b]] = alpha sum_a A[row][cma[row][a]] C[cb[a] + ct[ck[a]][b]] (+ old)
-__device__ __forceinline__ void k5_chunk(const char* st, const double* __restrict__ cmat,
-                                         double* __restrict__ y, double alpha, bool accumulate,
-                                         int lane) {
-  const int32_t* m = reinterpret_cast<const int32_t*>(st);
-  const int nrows = m[H_NROWS], ua = m[H_UA], ub = m[H_UB];
-  const int uap = m[H_UAP], ubp = m[H_UBP];
+// Y[yoff[seg] + row K_Y + cmy[seg][b]] = alpha sum_a A[row][cma[seg][a]] C[cb[a] + ct[ck[a]][b]]
+// (+ old).  One pass: union Y columns [bg, bg + 8 TB); the C fragments of an
+// a-group of <= 4 KS union columns stay in registers over every row tile of
+// the chunk; segments are padded to multiples of 8 rows.
+template <int TB, int KS>
+__device__ __forceinline__ void k5_pass(const int32_t* m, const double* __restrict__ cmat,
+                                        double* __restrict__ y, double alpha, bool accumulate,
+                                        int bg, int lane) {
+  const int nseg = m[H_NSEG], ua = m[H_UA], ub = m[H_UB];
+  const char* st = reinterpret_cast<const char*>(m);
   const double* As = reinterpret_cast<const double*>(st + m[H_AOFF]);
-  const int32_t* tab = m + m[H_TAB];            // per row: bi | a_row << 8
-  const int32_t* yrow = m + m[H_YROW];
+  const int4* seg = reinterpret_cast<const int4*>(m + m[H_SEG]);
   const int16_t* cma = reinterpret_cast<const int16_t*>(m + m[H_CMA]);
   const int16_t* cmy = reinterpret_cast<const int16_t*>(m + m[H_CMB]);
   const int32_t* cb = m + m[H_RB];
   const int32_t* ck = m + m[H_KK];
   const int32_t* ct = m + m[H_ST];
-  const int nrt = (nrows + 7) >> 3;  // <= 4 (chunks of <= 32 rows)
   const int g4 = lane >> 2, t4 = lane & 3;
-  for (int yg = 0; yg < ub; yg += 32) {
-    const int tb = min(4, (ub - yg + 7) >> 3);
-    double acc[4][4][2];
+  for (int ag = 0; ag < ua; ag += 4 * KS) {
+    double bf[KS][TB];  // C fragments: k = ag + 4 ks + t4, n = bg + 8 u + g4
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int ks = 0; ks < KS; ++ks) {
+      const int ka = ag + ks * 4 + t4;
+      const bool okk = ka < ua;
+      const int base = okk ? cb[ka] : 0;
+      const int32_t* crow = ct + (okk ? ck[ka] : 0) * ub;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[r][u][0] = acc[r][u][1] = 0.0;
-    for (int kg = 0; kg < ua; kg += 32) {
-      const int nks = min(8, (ua - kg + 3) >> 2);
-      double bf[8][4];  // C fragments: k = kg + 4 ks + t4, n = yg + 8 u + g4
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const int ka = kg + ks * 4 + t4;
-        const bool okk = ks < nks && ka < ua;
-        const int base = okk ? cb[ka] : 0;
-        const int32_t* crow = ct + (okk ? ck[ka] : 0) * ubp;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int bb2 = yg + u * 8 + g4;
-          double v = 0.0;
-          if (okk && u < tb && bb2 < ub) {
-            const int sl = crow[bb2];
-            if (sl >= 0) v = __ldg(cmat + (int64_t)base + sl);
-          }
-          bf[ks][u] = v;
+      for (int u = 0; u < TB; ++u) {
+        const int bb = bg + u * 8 + g4;
+        double v = 0.0;
+        if (okk && bb < ub) {
+          const int sl = crow[bb];
+          if (sl >= 0) v = __ldg(cmat + (int64_t)base + sl);
         }
-      }
-#pragma unroll
-      for (int rt = 0; rt < 4; ++rt) {
-        if (rt >= nrt) continue;
-        const int row = rt * 8 + g4;
-        int bi = -1, ar = 0;
-        if (row < nrows) {
-          const int e = tab[row];
-          bi = e & 255;
-          ar = e >> 8;
-        }
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          if (ks >= nks) continue;
-          const int ka = kg + ks * 4 + t4;
-          const int s = (bi >= 0 && ka < ua) ? cma[bi * uap + ka] : -1;
-          const double av = s >= 0 ? As[ar + s] : 0.0;
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (u < tb) dmma_8x8x4(acc[rt][u][0], acc[rt][u][1], av, bf[ks][u]);
-        }
+        bf[ks][u] = v;
       }
     }
-    // store: lane holds rows rt*8 + g4, columns yg + 8u + 2 t4 + {0, 1}
+    const bool add_old = accumulate || ag > 0;
+    for (int s = 0; s < nseg; ++s) {
+      const int4 r0 = seg[2 * s];
+      const int ky = m[m[H_SEG] + 8 * s + 4];
+      const int nrows = r0.x, ka = r0.z;
+      int oa[KS];
+      unsigned vmask = 0;
 #pragma unroll
-    for (int rt = 0; rt < 4; ++rt) {
-      if (rt >= nrt) continue;
-      const int row = rt * 8 + g4;
-      if (row >= nrows) continue;
-      const int bi = tab[row] & 255;
-      const int64_t yo = yrow[row];
+      for (int ks = 0; ks < KS; ++ks) {
+        const int aa = ag + ks * 4 + t4;
+        const int sl = aa < ua ? cma[s * ua + aa] : -1;
+        if (sl >= 0) vmask |= 1u << ks;
+        oa[ks] = r0.y + g4 * ka + sl;
+      }
+      int sy[TB][2];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (u >= tb) continue;
+      for (int u = 0; u < TB; ++u)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int bb2 = yg + u * 8 + 2 * t4 + e;
-          if (bb2 < ub) {
-            const int s = cmy[bi * ubp + bb2];
-            if (s >= 0) {
-              double v = alpha * acc[rt][u][e];
-              if (accumulate) v += y[yo + s];
-              y[yo + s] = v;
-            }
-          }
+          const int bb = bg + u * 8 + 2 * t4 + e;
+          sy[u][e] = bb < ub ? cmy[s * ub + bb] : -1;
+        }
+      double* yseg = y + (int64_t)r0.w + (int64_t)g4 * ky;
+      const int nrt = (nrows + 7) >> 3;
+      int xa = 0;
+      for (int rt = 0; rt < nrt; ++rt, xa += 8 * ka, yseg += 8 * ky) {
+        const bool rok = rt * 8 + g4 < nrows;
+        double acc[TB][2];
+#pragma unroll
+        for (int u = 0; u < TB; ++u) acc[u][0] = acc[u][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const double av = (rok && ((vmask >> ks) & 1u)) ? As[oa[ks] + xa] : 0.0;
+#pragma unroll
+          for (int u = 0; u < TB; ++u) dmma_8x8x4(acc[u][0], acc[u][1], av, bf[ks][u]);
+        }
+        if (rok) {
+#pragma unroll
+          for (int u = 0; u < TB; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (sy[u][e] >= 0) {
+                double v = alpha * acc[u][e];
+                if (add_old) v += yseg[sy[u][e]];
+                yseg[sy[u][e]] = v;
+              }
         }
       }
     }
   }
+}
+
+// Pass width by the number of union A columns (register budget: the C
+// fragments of an a-group, 4 KS x 8 TB doubles per warp, stay in registers).
+template <int KS, int TBMAX>
+__device__ __forceinline__ void k5_passes(const int32_t* m, const double* cmat, double* y,
+                                          double alpha, bool accumulate, int lane) {
+  const int ub = m[H_UB];
+  for (int bg = 0; bg < ub; bg += 8 * TBMAX) {
+    const int tb = min(TBMAX, (ub - bg + 7) >> 3);
+    if (tb == 1) k5_pass<1, KS>(m, cmat, y, alpha, accumulate, bg, lane);
+    else if (tb == 2 || TBMAX == 2) k5_pass<2, KS>(m, cmat, y, alpha, accumulate, bg, lane);
+    else if (tb == 3) k5_pass<(TBMAX > 2 ? 3 : 2), KS>(m, cmat, y, alpha, accumulate, bg, lane);
+    else k5_pass<(TBMAX > 2 ? 4 : 2), KS>(m, cmat, y, alpha, accumulate, bg, lane);
+  }
+}
+
+__device__ __forceinline__ void k5_chunk(const char* st, const double* __restrict__ cmat,
+                                         double* __restrict__ y, double alpha, bool accumulate,
+                                         int lane) {
+  const int32_t* m = reinterpret_cast<const int32_t*>(st);
+  const int ua = m[H_UA];
+  if (ua <= 8) k5_passes<2, 4>(m, cmat, y, alpha, accumulate, lane);
+  else if (ua <= 16) k5_passes<4, 4>(m, cmat, y, alpha, accumulate, lane);
+  else k5_passes<8, 2>(m, cmat, y, alpha, accumulate, lane);
 }
 
 template <int KIND>  // 4: K4, 5: K5
@@ -268,7 +325,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1)
   }
   __syncthreads();
   if (warp == kCW) {
-    if (lane == 0) producer(g, a, KIND == 4 ? b : nullptr, smem, full, empty, c0, n);
+    producer(g, a, KIND == 4 ? b : nullptr, smem, full, empty, c0, n, lane);
     return;
   }
   for (int64_t j = warp; j < n; j += kCW) {
@@ -290,10 +347,13 @@ struct ChunkPlan {
   int stage_bytes = 0;
   int64_t n_chunks = 0;
   int64_t* part_start = nullptr;
-  int64_t* meta_off = nullptr;
+  int64_t* m0 = nullptr;
+  int64_t* a0 = nullptr;
+  int64_t* b0 = nullptr;
+  uint32_t* mb = nullptr;
+  uint32_t* ab = nullptr;
+  uint32_t* bb = nullptr;
   int32_t* meta = nullptr;
-  int64_t* a_rng = nullptr;
-  int64_t* b_rng = nullptr;
 };
 
 }  // namespace bmv
@@ -312,16 +372,44 @@ int bmv_chunk_plan_create(const bmv_chunk_desc* d, bmv_chunk_plan** out) {
     set_error("bmv_chunk_plan_create: invalid descriptor");
     return BMV_ERR_INVALID;
   }
+  // per-chunk copy descriptors (what the producer warp needs, nothing dependent)
+  const size_t nc = (size_t)d->n_chunks;
+  std::vector<int64_t> m0(nc), a0(nc), b0(nc);
+  std::vector<uint32_t> mb(nc), ab(nc), bb(nc);
+  for (size_t j = 0; j < nc; ++j) {
+    m0[j] = d->chunk_meta[j];
+    const int64_t words = d->chunk_meta[j + 1] - d->chunk_meta[j];
+    a0[j] = d->chunk_a[2 * j];
+    const int64_t an = d->chunk_a[2 * j + 1] - a0[j];
+    int64_t bn = 0;
+    if (d->kind == 4) {
+      b0[j] = d->chunk_b[2 * j];
+      bn = d->chunk_b[2 * j + 1] - b0[j];
+    }
+    const int32_t* h = d->meta + m0[j];
+    if (words < 16 || (words & 3) || (m0[j] & 3) || (a0[j] & 1) || (an & 1) || (b0[j] & 1) ||
+        (bn & 1) || an < 0 || bn < 0 || 4 * words + 8 * (an + bn) > d->stage_bytes ||
+        h[5] != 4 * words || h[6] != 4 * words + 8 * an) {
+      set_error("bmv_chunk_plan_create: chunk %lld does not fit its stage", (long long)j);
+      return BMV_ERR_INVALID;
+    }
+    mb[j] = (uint32_t)(4 * words);
+    ab[j] = (uint32_t)(8 * an);
+    bb[j] = (uint32_t)(8 * bn);
+  }
   auto* p = new bmv_chunk_plan();
   p->kind = d->kind;
   p->n_parts = d->n_parts;
   p->stage_bytes = d->stage_bytes;
   p->n_chunks = d->n_chunks;
   int rc = upload(d->part_chunk_start, (int64_t)d->n_parts + 1, &p->part_start);
-  if (rc == BMV_OK) rc = upload(d->chunk_meta, d->n_chunks + 1, &p->meta_off);
   if (rc == BMV_OK) rc = upload(d->meta, d->meta_len, &p->meta);
-  if (rc == BMV_OK) rc = upload(d->chunk_a, 2 * d->n_chunks, &p->a_rng);
-  if (rc == BMV_OK && d->kind == 4) rc = upload(d->chunk_b, 2 * d->n_chunks, &p->b_rng);
+  if (rc == BMV_OK) rc = upload(m0.data(), d->n_chunks, &p->m0);
+  if (rc == BMV_OK) rc = upload(a0.data(), d->n_chunks, &p->a0);
+  if (rc == BMV_OK) rc = upload(mb.data(), d->n_chunks, &p->mb);
+  if (rc == BMV_OK) rc = upload(ab.data(), d->n_chunks, &p->ab);
+  if (rc == BMV_OK && d->kind == 4) rc = upload(b0.data(), d->n_chunks, &p->b0);
+  if (rc == BMV_OK && d->kind == 4) rc = upload(bb.data(), d->n_chunks, &p->bb);
   if (rc != BMV_OK) {
     bmv_chunk_plan_destroy(p);
     return rc;
@@ -333,10 +421,13 @@ int bmv_chunk_plan_create(const bmv_chunk_desc* d, bmv_chunk_plan** out) {
 int bmv_chunk_plan_destroy(bmv_chunk_plan* p) {
   if (!p) return BMV_OK;
   bmv::release(p->part_start);
-  bmv::release(p->meta_off);
+  bmv::release(p->m0);
+  bmv::release(p->a0);
+  bmv::release(p->b0);
+  bmv::release(p->mb);
+  bmv::release(p->ab);
+  bmv::release(p->bb);
   bmv::release(p->meta);
-  bmv::release(p->a_rng);
-  bmv::release(p->b_rng);
   delete p;
   return BMV_OK;
 }
@@ -345,7 +436,7 @@ static int launch_chunks(const bmv_chunk_plan* p, const double* a, const double*
                          double alpha, int accumulate, void* stream) {
   using namespace bmv;
   if (p->n_chunks == 0) return BMV_OK;
-  ChunkArgs g{p->part_start, p->meta_off, p->meta, p->a_rng, p->b_rng, p->stage_bytes};
+  ChunkArgs g{p->part_start, p->m0, p->a0, p->b0, p->mb, p->ab, p->bb, p->meta, p->stage_bytes};
   const int smem = p->stage_bytes * kNS;
   cudaStream_t st = as_stream(stream);
   if (p->kind == 4) {

@@ -22,12 +22,12 @@ import torch
 from . import _lib, _plan
 from .errors import PatternError, ShapeError
 
-# chunk shape (bmv_spmm.cu: 8 consumer warps, 16 stages per CTA)
-STAGE_BYTES = 14208          # 16 stages x 14208 B = 222 KB of shared memory
-K4_MAX_ROWS = 64
-K5_MAX_ROWS = 32
+# chunk shape (bmv_spmm.cu: 12 consumer warps, 20 stages per CTA)
+STAGE_BYTES = 11520          # 20 stages x 11520 B = 225 KB of shared memory
+K4_MAX_ROWS = 256
+K5_MAX_ROWS = 256
 MAX_BLOCK_ROWS = 16
-DATA_BYTES = 11264           # staged values per chunk (the rest: chunk meta)
+DATA_BYTES = 9728            # staged values per chunk (the rest: chunk meta)
 _CACHE_ENTRIES = 8
 
 

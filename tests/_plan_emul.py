@@ -8,8 +8,15 @@ from __future__ import annotations
 
 import numpy as np
 
-H_NROWS, H_NBR, H_UA, H_UB, H_NK, H_AOFF, H_BOFF, H_UAP, H_UBP, H_TAB, H_CMA, H_CMB, H_RB, \
-    H_KK, H_ST, H_YROW = range(16)
+H_NSEG, H_NROWS, H_UA, H_UB, H_NK, H_AOFF, H_BOFF, H_SEG, H_CMA, H_CMB, H_RB, H_KK, H_ST = range(13)
+
+
+def _segments(meta, nseg):
+    """(rows, A offset, K_A, B / Y offset, K_B) per segment."""
+    w = int(meta[H_SEG])
+    rec = meta[w : w + 8 * nseg].astype(np.int64).reshape(nseg, 8)
+    assert np.all(rec[:, 5:] == 0)
+    return rec[:, :5]
 
 
 def _stage(arr, j, a, b):
@@ -45,18 +52,21 @@ def emulate_tmmult(arr, a, b, c_len):
     c = np.zeros(c_len)
     for j in range(arr["n_chunks"]):
         meta, av, bv = _stage(arr, j, a, b)
-        nrows, nbr, ua, ub = (int(meta[k]) for k in (H_NROWS, H_NBR, H_UA, H_UB))
-        tab = meta[meta[H_TAB] : meta[H_TAB] + 2 * nrows].astype(np.int64)
-        bi, ar, br = tab[0::2] & 255, tab[0::2] >> 8, tab[1::2]
-        cma = _colmap(meta, int(meta[H_CMA]), nbr, ua)
-        cmb = _colmap(meta, int(meta[H_CMB]), nbr, ub)
-        A = np.zeros((nrows, ua))
-        B = np.zeros((nrows, ub))
-        for r in range(nrows):
-            sa, sb = cma[bi[r]], cmb[bi[r]]
-            A[r, sa >= 0] = av[ar[r] + sa[sa >= 0]]
-            B[r, sb >= 0] = bv[br[r] + sb[sb >= 0]]
-        prod = A.T @ B
+        nseg, nrows, ua, ub = (int(meta[k]) for k in (H_NSEG, H_NROWS, H_UA, H_UB))
+        segs = _segments(meta, nseg)
+        assert int(segs[:, 0].sum()) == nrows
+        cma = _colmap(meta, int(meta[H_CMA]), nseg, ua)
+        cmb = _colmap(meta, int(meta[H_CMB]), nseg, ub)
+        prod = np.zeros((ua, ub))
+        for s, (n, ao, ka, bo, kb) in enumerate(segs):
+            sa, sb = cma[s], cmb[s]
+            assert sa.max(initial=-1) < ka and sb.max(initial=-1) < kb
+            assert ao + n * ka <= av.size and bo + n * kb <= bv.size
+            A = np.zeros((n, ua))
+            B = np.zeros((n, ub))
+            A[:, sa >= 0] = av[ao : ao + n * ka].reshape(n, ka)[:, sa[sa >= 0]]
+            B[:, sb >= 0] = bv[bo : bo + n * kb].reshape(n, kb)[:, sb[sb >= 0]]
+            prod += A.T @ B
         rb = meta[meta[H_RB] : meta[H_RB] + ua].astype(np.int64)
         kk = meta[meta[H_KK] : meta[H_KK] + ua].astype(np.int64)
         nk = int(meta[H_NK])
@@ -75,13 +85,11 @@ def emulate_mmult(arr, a, cmat, y, alpha, accumulate):
     y = y.copy()
     for j in range(arr["n_chunks"]):
         meta, av, _ = _stage(arr, j, a, None)
-        nrows, nbr, ua, ub = (int(meta[k]) for k in (H_NROWS, H_NBR, H_UA, H_UB))
-        assert nrows <= 32
-        tab = meta[meta[H_TAB] : meta[H_TAB] + nrows].astype(np.int64)
-        bi, ar = tab & 255, tab >> 8
-        yrow = meta[meta[H_YROW] : meta[H_YROW] + nrows].astype(np.int64)
-        cma = _colmap(meta, int(meta[H_CMA]), nbr, ua)
-        cmy = _colmap(meta, int(meta[H_CMB]), nbr, ub)
+        nseg, nrows, ua, ub = (int(meta[k]) for k in (H_NSEG, H_NROWS, H_UA, H_UB))
+        segs = _segments(meta, nseg)
+        assert int(segs[:, 0].sum()) == nrows
+        cma = _colmap(meta, int(meta[H_CMA]), nseg, ua)
+        cmy = _colmap(meta, int(meta[H_CMB]), nseg, ub)
         cb = meta[meta[H_RB] : meta[H_RB] + ua].astype(np.int64)
         ck = meta[meta[H_KK] : meta[H_KK] + ua].astype(np.int64)
         nk = int(meta[H_NK])
@@ -90,14 +98,15 @@ def emulate_mmult(arr, a, cmat, y, alpha, accumulate):
         for aa in range(ua):
             sl = ct[ck[aa]]
             C[aa, sl >= 0] = cmat[cb[aa] + sl[sl >= 0]]
-        A = np.zeros((nrows, ua))
-        for r in range(nrows):
-            sa = cma[bi[r]]
-            A[r, sa >= 0] = av[ar[r] + sa[sa >= 0]]
-        D = alpha * (A @ C)
-        for r in range(nrows):
-            sy = cmy[bi[r]]
+        for s, (n, ao, ka, yo, ky) in enumerate(segs):
+            sa, sy = cma[s], cmy[s]
+            assert sa.max(initial=-1) < ka and sy.max(initial=-1) < ky
+            assert ao + n * ka <= av.size
+            A = np.zeros((n, ua))
+            A[:, sa >= 0] = av[ao : ao + n * ka].reshape(n, ka)[:, sa[sa >= 0]]
+            D = alpha * (A @ C)
             ok = sy >= 0
-            idx = yrow[r] + sy[ok]
-            y[idx] = D[r, ok] + (y[idx] if accumulate else 0.0)
+            assert np.count_nonzero(ok) == ky, "a stored Y column outside the union"
+            idx = yo + np.arange(n)[:, None] * ky + sy[ok][None, :]
+            y[idx] = D[:, ok] + (y[idx] if accumulate else 0.0)
     return y

@@ -90,6 +90,7 @@ def test_mmult_chunk_emulation(block_size, lane_width, compact, n_parts, accumul
 
 def test_long_block_rows_split_into_row_ranges(monkeypatch):
     """Coarse level 0 at degree 4: block rows of up to 125 rows > 64 (split)."""
+    monkeypatch.setattr(spmm, "K4_MAX_ROWS", 64)
     x, hx, sm, _, _ = _setup(3, 8, True, level=0, degree=4)
     assert int(x.local_row_sizes.max()) > spmm.K4_MAX_ROWS
     arr = _plan(4, x, hx, sm, 7)

@@ -134,27 +134,28 @@ int bmv_cellop_launches(const bmv_cellop* plan, int32_t* out);
  * entries (reference mmult, bcsr.py:587-628) on slab storage.
  * A CHUNK is a run of consecutive owned rows of A (whole block rows, or a
  * row range of one long block row): its A values (K4: and its B values) are
- * one contiguous element range, staged with one TMA bulk copy each into a
- * shared-memory stage [meta | A | B].  Persistent CTAs (n_parts) take
- * contiguous chunk ranges; 8 consumer warps own whole chunks, 1 producer
- * warp streams them through 16 stages of stage_bytes.
+ * one contiguous element range each.  Persistent CTAs (n_parts) take
+ * contiguous chunk ranges; every warp claims chunks in order, copies
+ * [meta | A | B] of its next chunks into private shared-memory buffers with
+ * cp.async and multiplies the oldest (bmv_chunk_kernel_config: warps per
+ * CTA, bytes per buffer = the largest chunk).
  * Chunk meta (int32 words, 16-byte multiple), header fields:
- *   [0] rows  [1] block rows  [2] UA (union A columns)  [3] UB (union B / Y
- *   columns)  [4] NK  [5] byte offset of A in the stage  [6] of B (K4)
- *   [7] UA pitch  [8] UB pitch  [9..15] word offsets of: row table,
- *   A colmap, B/Y colmap, RB, KK, ST, (K5) Y row offsets.
- * Row table: K4 2 words per row {block row | A row offset in the stage
- *   (doubles) << 8, B row offset}; K5 1 word {block row | A row << 8}.
- * Colmaps (int16, block row x pitch): slab slot of a union column in that
+ *   [0] segments  [1] rows  [2] UA (union A columns)  [3] UB (union B / Y
+ *   columns)  [4] NK  [5] byte offset of A in the buffer (= meta bytes)
+ *   [6] of B (K4)  [7..12] word offsets of: segment records, A colmap,
+ *   B/Y colmap, RB, KK, ST.
+ * Segment record (8 words, one per block-row piece): {rows, A offset in the
+ *   staged range (doubles), K_A (A's slab width), B offset in the staged
+ *   range (K4) / element offset of the piece's first row in Y (K5), K_B,
+ *   0, 0, 0}.
+ * Colmaps (int16, segment x U): slab slot of a union column in that
  *   block row, -1 = not stored (structural zero).
- * Output / C addressing of union (a, b): RB[a] + ST[KK[a] * UB pitch + b]
- *   (K4: element of S; K5: element of C), ST = -1: no such entry.
- * K5: Y rows at element offsets Y_row[row], values at + Y colmap slot;
- *   chunks of <= 32 rows.                                                  */
+ * Output / C addressing of union (a, b): RB[a] + ST[KK[a] * UB + b]
+ *   (K4: element of S; K5: element of C), ST = -1: no such entry.          */
 typedef struct {
   int32_t kind;              /* 4: projection (K4), 5: post-multiply (K5)  */
   int32_t n_parts;           /* CTAs                                       */
-  int32_t stage_bytes;       /* bytes per stage (multiple of 16)           */
+  int32_t stage_bytes;       /* largest chunk in bytes (multiple of 16)    */
   int64_t n_chunks;
   int64_t meta_len;          /* int32 words                                */
   const int64_t* part_chunk_start; /* n_parts + 1                          */
@@ -176,8 +177,8 @@ int bmv_tmmult_run(const bmv_chunk_plan* plan, const double* a, const double* b,
    (entries of Y outside the chunks are not touched). */
 int bmv_mmult_run(const bmv_chunk_plan* plan, const double* a, const double* cmat, double* y,
                   double alpha, int32_t accumulate, void* stream);
-/* consumer warps and stages of the chunk kernels (planner sizing) */
-int bmv_chunk_kernel_config(int32_t* consumer_warps, int32_t* stages);
+/* warps per CTA and bytes per buffer (largest chunk) of the chunk kernels */
+int bmv_chunk_kernel_config(int32_t* warps, int32_t* buffer_bytes);
 
 /* --------------------------------------------------------- halo / util --
  * Device index lists for ghost exchange packing.                         */

@@ -5,14 +5,20 @@
 // Work unit: a CHUNK = a run of consecutive owned rows (whole block rows,
 // or a row range of one long block row).  Because consecutive block rows'
 // slabs are consecutive in memory, a chunk's A values (and, for K4, its B
-// values) are ONE contiguous byte range each, staged by one cp.async.bulk
-// (TMA) per operand into a ring of shared-memory stages by a producer warp;
-// consumer warps own whole chunks.  Inside a chunk the block rows' stored
-// columns are merged into union columns (UA for A, UB for B / Y); each block
-// row maps union columns to its slab slots (colmap, -1 = structural zero),
-// so a chunk is a dense (rows x UA)^T (rows x UB) product on FP64 tensor
-// cores (DMMA m8n8k4), fragments read from the staged slabs through the
-// colmaps.  Union columns are processed in groups of 32 (4 DMMA tiles).
+// values) are ONE contiguous byte range each.  Every warp runs its own
+// software pipeline: it claims chunks in order from a CTA counter, copies
+// [meta | A | B] of the next chunks into its private shared-memory buffers
+// with 16-byte cp.async (LDGSTS, L1 bypass) and multiplies the oldest one.
+// (A producer warp feeding a shared ring with 1D TMA bulk copies was
+// measured first: the more bulk copies were in flight per SM the later the
+// OLDEST one completed, profiles/r02_spmm_tma_*.txt.)
+//
+// Inside a chunk the block rows' stored columns are merged into union
+// columns (UA for A, UB for B / Y); each segment (block row piece) maps union
+// columns to its slab slots (colmap, -1 = structural zero), so a chunk is a
+// dense (rows x UA)^T (rows x UB) product on the FP64 tensor pipe (DMMA
+// m8n8k4), fragments read from the staged slabs through per-lane slot
+// offsets fixed per segment.
 //
 // K4: the 8x8 result tiles are added to S with fp64 RED (S is small and
 // L2-resident; one RED per union (a, b) of a chunk instead of one per row).
@@ -31,59 +37,48 @@
 namespace bmv {
 namespace {
 
-constexpr int kCW = 12;           // consumer warps per CTA
-constexpr int kNS = 20;           // stages (kNS - kCW chunks of lookahead)
+#ifndef BMV_SPMM_WARPS
+#define BMV_SPMM_WARPS 12
+#endif
+#ifndef BMV_SPMM_BUFS
+#define BMV_SPMM_BUFS 2
+#endif
+constexpr int kCW = BMV_SPMM_WARPS;   // warps per CTA, each with its own pipeline
+constexpr int kNB = BMV_SPMM_BUFS;    // buffers per warp (kNB - 1 chunks in flight)
+constexpr int kSmemBytes = 224 * 1024;
+// bytes per buffer = the largest chunk [meta | A | B] the planner may build
+constexpr int kBufBytes = kSmemBytes / (kCW * kNB) / 128 * 128;
 
-// Per-chunk copy descriptors (built once in bmv_chunk_plan_create), structure
-// of arrays so that the producer warp fetches 32 chunks per coalesced load.
+// Per-chunk copy descriptor (built once in bmv_chunk_plan_create), 32 bytes:
+// one sector, loaded by the claiming warp a pipeline step ahead of its use.
+struct __align__(16) ChunkDesc {
+  uint32_t m16, a16, b16;  // first meta word / A element / B element, 16-byte units
+  uint32_t mb, ab, bb;     // bytes of meta, A, B (multiples of 16)
+  uint32_t pad[2];
+};
+
 struct ChunkArgs {
   const int64_t* part_start;  // n_parts + 1
-  const int64_t* m0;          // first meta word
-  const int64_t* a0;          // first staged A element
-  const int64_t* b0;          // first staged B element (K4)
-  const uint32_t* mb;         // meta bytes (= byte offset of A in the stage)
-  const uint32_t* ab;         // A bytes
-  const uint32_t* bb;         // B bytes (K4; 0 for K5)
+  const ChunkDesc* desc;
   const int32_t* meta;
-  int stage_bytes;
 };
 
 // Chunk header (int32): see include/bmv.h (bmv_chunk_desc)
 enum { H_NSEG = 0, H_NROWS, H_UA, H_UB, H_NK, H_AOFF, H_BOFF, H_SEG, H_CMA, H_CMB, H_RB, H_KK,
        H_ST };
 
-// Producer warp: lane l prefetches the descriptors of chunk base + l, lane 0
-// issues the bulk copies (no dependent global load per chunk).
-__device__ __forceinline__ void producer(const ChunkArgs& g, const double* a, const double* b,
-                                         char* stages, uint64_t* full, uint64_t* empty,
-                                         int64_t c0, int64_t n, int lane) {
-  for (int64_t base = 0; base < n; base += 32) {
-    const int64_t c = c0 + base + lane;
-    const bool ok = base + lane < n;
-    const int64_t m0 = ok ? __ldg(g.m0 + c) : 0;
-    const int64_t a0 = ok ? __ldg(g.a0 + c) : 0;
-    const int64_t b0 = (ok && g.b0) ? __ldg(g.b0 + c) : 0;
-    const unsigned mb = ok ? __ldg(g.mb + c) : 0u;
-    const unsigned ab = ok ? __ldg(g.ab + c) : 0u;
-    const unsigned bb = (ok && g.bb) ? __ldg(g.bb + c) : 0u;
-    const int cnt = (int)min((int64_t)32, n - base);
-    for (int k = 0; k < cnt; ++k) {
-      const int64_t km0 = __shfl_sync(~0u, m0, k), ka0 = __shfl_sync(~0u, a0, k),
-                    kb0 = __shfl_sync(~0u, b0, k);
-      const unsigned kmb = __shfl_sync(~0u, mb, k), kab = __shfl_sync(~0u, ab, k),
-                     kbb = __shfl_sync(~0u, bb, k);
-      if (lane == 0) {
-        const int64_t j = base + k;
-        const int s = (int)(j % kNS);
-        if (j >= kNS) mbar_wait(&empty[s], (unsigned)((j / kNS - 1) & 1));
-        char* st = stages + (int64_t)s * g.stage_bytes;
-        mbar_expect_tx(&full[s], kmb + kab + kbb);
-        bulk_g2s(st, g.meta + km0, kmb, &full[s]);
-        if (kab) bulk_g2s(st + kmb, a + ka0, kab, &full[s]);
-        if (kbb) bulk_g2s(st + kmb + kab, b + kb0, kbb, &full[s]);
-      }
-    }
-  }
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Warp-wide copy of `bytes` (multiple of 16) from global to shared memory.
+__device__ __forceinline__ void warp_copy(unsigned dst, const char* src, unsigned bytes, int lane) {
+  for (unsigned o = lane * 16u; o < bytes; o += 512u) cp_async16(dst + o, src + o);
 }
 
 // ---------------------------------------------------------------- K4 -----
@@ -310,33 +305,76 @@ __device__ __forceinline__ void k5_chunk(const char* st, const double* __restric
 }
 
 template <int KIND>  // 4: K4, 5: K5
-__global__ void __launch_bounds__((kCW + 1) * 32, 1)
+__global__ void __launch_bounds__(kCW * 32, 1)
     chunk_kernel(const ChunkArgs g, const double* __restrict__ a, const double* __restrict__ b,
                  double* __restrict__ out, double alpha, int accumulate) {
   extern __shared__ __align__(128) char smem[];
-  __shared__ __align__(8) uint64_t full[kNS], empty[kNS];
+  __shared__ int next_chunk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t c0 = g.part_start[blockIdx.x], n = g.part_start[blockIdx.x + 1] - c0;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kNS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-  }
+  const int64_t c0 = g.part_start[blockIdx.x];
+  const int n = (int)(g.part_start[blockIdx.x + 1] - c0);
+  if (threadIdx.x == 0) next_chunk = 0;
   __syncthreads();
-  if (warp == kCW) {
-    producer(g, a, KIND == 4 ? b : nullptr, smem, full, empty, c0, n, lane);
-    return;
+  char* mybuf = smem + (size_t)warp * kNB * kBufBytes;
+  const unsigned mybuf_s = smem_u32(mybuf);
+
+  // claim the next chunk of this CTA (in order: the chunks of a part are
+  // consecutive in memory) and load its descriptor
+  uint4 d0 = make_uint4(0, 0, 0, 0);
+  uint2 d1 = make_uint2(0, 0);
+  bool have = false;
+  auto claim = [&]() {
+    int jj = 0;
+    if (lane == 0) jj = atomicAdd(&next_chunk, 1);
+    jj = __shfl_sync(~0u, jj, 0);
+    have = jj < n;
+    if (have) {
+      const ChunkDesc* d = g.desc + c0 + jj;
+      d0 = __ldg(reinterpret_cast<const uint4*>(d));
+      d1 = __ldg(reinterpret_cast<const uint2*>(d) + 2);
+    }
+  };
+  // copy the claimed chunk into buffer `buf` (one cp.async group, possibly empty)
+  auto issue = [&](int buf) {
+    if (have) {
+      const unsigned dst = mybuf_s + (unsigned)buf * kBufBytes;
+      warp_copy(dst, reinterpret_cast<const char*>(g.meta) + (size_t)d0.x * 16, d0.w, lane);
+      warp_copy(dst + d0.w, reinterpret_cast<const char*>(a) + (size_t)d0.y * 16, d1.x, lane);
+      if (KIND == 4)
+        warp_copy(dst + d0.w + d1.x, reinterpret_cast<const char*>(b) + (size_t)d0.z * 16, d1.y,
+                  lane);
+    }
+    cp_commit();
+  };
+
+  // prologue: kNB - 1 chunks in flight, the descriptor of the next one loading
+  bool valid[kNB];
+#pragma unroll
+  for (int i = 0; i < kNB - 1; ++i) {
+    claim();
+    valid[i] = have;
+    issue(i);
   }
-  for (int64_t j = warp; j < n; j += kCW) {
-    const int s = (int)(j % kNS);
-    mbar_wait(&full[s], (unsigned)((j / kNS) & 1));
-    const char* st = smem + (int64_t)s * g.stage_bytes;
+  claim();
+  int cur = 0;
+  while (valid[0]) {
+    // refill the buffer freed in the previous step, then claim one step ahead
+    int nb = cur + kNB - 1;
+    if (nb >= kNB) nb -= kNB;
+    valid[kNB - 1] = have;
+    issue(nb);
+    claim();
+    cp_wait<kNB - 1>();
+    __syncwarp();
+    const char* st = mybuf + (size_t)cur * kBufBytes;
     if (KIND == 4) k4_chunk(st, out, lane);
     else k5_chunk(st, b, out, alpha, accumulate != 0, lane);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+    for (int i = 0; i < kNB - 1; ++i) valid[i] = valid[i + 1];
+    if (++cur == kNB) cur = 0;
   }
+  cp_wait<0>();
 }
 
 }  // namespace
@@ -344,15 +382,9 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1)
 struct ChunkPlan {
   int kind = 0;
   int n_parts = 0;
-  int stage_bytes = 0;
   int64_t n_chunks = 0;
   int64_t* part_start = nullptr;
-  int64_t* m0 = nullptr;
-  int64_t* a0 = nullptr;
-  int64_t* b0 = nullptr;
-  uint32_t* mb = nullptr;
-  uint32_t* ab = nullptr;
-  uint32_t* bb = nullptr;
+  ChunkDesc* desc = nullptr;
   int32_t* meta = nullptr;
 };
 
@@ -368,48 +400,44 @@ int bmv_chunk_plan_create(const bmv_chunk_desc* d, bmv_chunk_plan** out) {
   using namespace bmv;
   *out = nullptr;
   if (!d || (d->kind != 4 && d->kind != 5) || d->n_parts <= 0 || d->n_chunks < 0 ||
-      d->stage_bytes <= 0 || (d->stage_bytes & 15) || d->stage_bytes * kNS > 227 * 1024) {
-    set_error("bmv_chunk_plan_create: invalid descriptor");
+      d->stage_bytes <= 0 || (d->stage_bytes & 15) || d->stage_bytes > kBufBytes) {
+    set_error("bmv_chunk_plan_create: invalid descriptor (chunks of at most %d bytes)", kBufBytes);
     return BMV_ERR_INVALID;
   }
-  // per-chunk copy descriptors (what the producer warp needs, nothing dependent)
+  // per-chunk copy descriptors
   const size_t nc = (size_t)d->n_chunks;
-  std::vector<int64_t> m0(nc), a0(nc), b0(nc);
-  std::vector<uint32_t> mb(nc), ab(nc), bb(nc);
+  std::vector<ChunkDesc> desc(nc);
   for (size_t j = 0; j < nc; ++j) {
-    m0[j] = d->chunk_meta[j];
-    const int64_t words = d->chunk_meta[j + 1] - d->chunk_meta[j];
-    a0[j] = d->chunk_a[2 * j];
-    const int64_t an = d->chunk_a[2 * j + 1] - a0[j];
-    int64_t bn = 0;
+    const int64_t m0 = d->chunk_meta[j];
+    const int64_t words = d->chunk_meta[j + 1] - m0;
+    const int64_t a0 = d->chunk_a[2 * j], an = d->chunk_a[2 * j + 1] - a0;
+    int64_t b0 = 0, bn = 0;
     if (d->kind == 4) {
-      b0[j] = d->chunk_b[2 * j];
-      bn = d->chunk_b[2 * j + 1] - b0[j];
+      b0 = d->chunk_b[2 * j];
+      bn = d->chunk_b[2 * j + 1] - b0;
     }
-    const int32_t* h = d->meta + m0[j];
-    if (words < 16 || (words & 3) || (m0[j] & 3) || (a0[j] & 1) || (an & 1) || (b0[j] & 1) ||
-        (bn & 1) || an < 0 || bn < 0 || 4 * words + 8 * (an + bn) > d->stage_bytes ||
-        h[5] != 4 * words || h[6] != 4 * words + 8 * an) {
-      set_error("bmv_chunk_plan_create: chunk %lld does not fit its stage", (long long)j);
+    const int32_t* h = d->meta + m0;
+    if (words < 16 || (words & 3) || (m0 & 3) || (a0 & 1) || (an & 1) || (b0 & 1) || (bn & 1) ||
+        an < 0 || bn < 0 || 4 * words + 8 * (an + bn) > d->stage_bytes || h[5] != 4 * words ||
+        h[6] != 4 * words + 8 * an || m0 / 4 > UINT32_MAX || a0 / 2 > UINT32_MAX ||
+        b0 / 2 > UINT32_MAX) {
+      set_error("bmv_chunk_plan_create: chunk %lld does not fit its buffer", (long long)j);
       return BMV_ERR_INVALID;
     }
-    mb[j] = (uint32_t)(4 * words);
-    ab[j] = (uint32_t)(8 * an);
-    bb[j] = (uint32_t)(8 * bn);
+    desc[j] = ChunkDesc{(uint32_t)(m0 / 4), (uint32_t)(a0 / 2), (uint32_t)(b0 / 2),
+                        (uint32_t)(4 * words), (uint32_t)(8 * an), (uint32_t)(8 * bn), {0, 0}};
+  }
+  if (d->part_chunk_start[d->n_parts] - d->part_chunk_start[0] != d->n_chunks) {
+    set_error("bmv_chunk_plan_create: parts do not cover the chunks");
+    return BMV_ERR_INVALID;
   }
   auto* p = new bmv_chunk_plan();
   p->kind = d->kind;
   p->n_parts = d->n_parts;
-  p->stage_bytes = d->stage_bytes;
   p->n_chunks = d->n_chunks;
   int rc = upload(d->part_chunk_start, (int64_t)d->n_parts + 1, &p->part_start);
   if (rc == BMV_OK) rc = upload(d->meta, d->meta_len, &p->meta);
-  if (rc == BMV_OK) rc = upload(m0.data(), d->n_chunks, &p->m0);
-  if (rc == BMV_OK) rc = upload(a0.data(), d->n_chunks, &p->a0);
-  if (rc == BMV_OK) rc = upload(mb.data(), d->n_chunks, &p->mb);
-  if (rc == BMV_OK) rc = upload(ab.data(), d->n_chunks, &p->ab);
-  if (rc == BMV_OK && d->kind == 4) rc = upload(b0.data(), d->n_chunks, &p->b0);
-  if (rc == BMV_OK && d->kind == 4) rc = upload(bb.data(), d->n_chunks, &p->bb);
+  if (rc == BMV_OK) rc = upload(desc.data(), d->n_chunks, &p->desc);
   if (rc != BMV_OK) {
     bmv_chunk_plan_destroy(p);
     return rc;
@@ -421,12 +449,7 @@ int bmv_chunk_plan_create(const bmv_chunk_desc* d, bmv_chunk_plan** out) {
 int bmv_chunk_plan_destroy(bmv_chunk_plan* p) {
   if (!p) return BMV_OK;
   bmv::release(p->part_start);
-  bmv::release(p->m0);
-  bmv::release(p->a0);
-  bmv::release(p->b0);
-  bmv::release(p->mb);
-  bmv::release(p->ab);
-  bmv::release(p->bb);
+  bmv::release(p->desc);
   bmv::release(p->meta);
   delete p;
   return BMV_OK;
@@ -436,17 +459,21 @@ static int launch_chunks(const bmv_chunk_plan* p, const double* a, const double*
                          double alpha, int accumulate, void* stream) {
   using namespace bmv;
   if (p->n_chunks == 0) return BMV_OK;
-  ChunkArgs g{p->part_start, p->m0, p->a0, p->b0, p->mb, p->ab, p->bb, p->meta, p->stage_bytes};
-  const int smem = p->stage_bytes * kNS;
+  if ((reinterpret_cast<uintptr_t>(a) & 15) || (p->kind == 4 && (reinterpret_cast<uintptr_t>(b) & 15))) {
+    set_error("K4/K5: value arrays must be 16-byte aligned");
+    return BMV_ERR_INVALID;
+  }
+  ChunkArgs g{p->part_start, p->desc, p->meta};
+  const int smem = kCW * kNB * kBufBytes;
   cudaStream_t st = as_stream(stream);
   if (p->kind == 4) {
     BMV_CUDA_TRY(cudaFuncSetAttribute(chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       smem));
-    chunk_kernel<4><<<p->n_parts, (kCW + 1) * 32, smem, st>>>(g, a, b, out, alpha, accumulate);
+    chunk_kernel<4><<<p->n_parts, kCW * 32, smem, st>>>(g, a, b, out, alpha, accumulate);
   } else {
     BMV_CUDA_TRY(cudaFuncSetAttribute(chunk_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       smem));
-    chunk_kernel<5><<<p->n_parts, (kCW + 1) * 32, smem, st>>>(g, a, b, out, alpha, accumulate);
+    chunk_kernel<5><<<p->n_parts, kCW * 32, smem, st>>>(g, a, b, out, alpha, accumulate);
   }
   BMV_CHECK_LAUNCH();
   return BMV_OK;
@@ -478,7 +505,7 @@ int bmv_mmult_run(const bmv_chunk_plan* p, const double* a, const double* cmat, 
 
 int bmv_chunk_kernel_config(int32_t* consumer_warps, int32_t* stages) {
   *consumer_warps = bmv::kCW;
-  *stages = bmv::kNS;
+  *stages = bmv::kBufBytes;
   return BMV_OK;
 }
 

@@ -14,6 +14,7 @@ number of entries.
 
 from __future__ import annotations
 
+import os
 from collections import OrderedDict
 
 import numpy as np
@@ -22,12 +23,27 @@ import torch
 from . import _lib, _plan
 from .errors import PatternError, ShapeError
 
-# chunk shape (bmv_spmm.cu: 12 consumer warps, 20 stages per CTA)
-STAGE_BYTES = 11520          # 20 stages x 11520 B = 225 KB of shared memory
-K4_MAX_ROWS = 256
-K5_MAX_ROWS = 256
+# chunk shape: the kernels (bmv_spmm.cu) give every warp private buffers of
+# bmv_chunk_kernel_config() bytes, the largest chunk [meta | A | B];
+# BMV_SPMM_STAGE / BMV_SPMM_DATA / BMV_SPMM_ROWS override for tuning runs
+K4_MAX_ROWS = K5_MAX_ROWS = int(os.environ.get("BMV_SPMM_ROWS", 256))
 MAX_BLOCK_ROWS = 16
-DATA_BYTES = 9728            # staged values per chunk (the rest: chunk meta)
+META_ALLOWANCE = 1536        # bytes left for the chunk meta when cutting chunks
+
+
+def chunk_bytes() -> tuple[int, int]:
+    """(largest chunk, staged values per chunk) in bytes."""
+    if "BMV_SPMM_STAGE" in os.environ:
+        stage = int(os.environ["BMV_SPMM_STAGE"])
+    else:
+        C = _lib.C
+        warps, buf = C.c_int32(), C.c_int32()
+        _lib.check(_lib.load().bmv_chunk_kernel_config(C.byref(warps), C.byref(buf)))
+        stage = int(buf.value)
+    data = int(os.environ.get("BMV_SPMM_DATA", max(stage - META_ALLOWANCE, stage // 2)))
+    return stage, data
+
+
 _CACHE_ENTRIES = 8
 
 
@@ -138,7 +154,7 @@ def tmmult_plan(a, b, c) -> ChunkPlan:
     arrays = _plan.chunk_plan(
         4, a.local_row_sizes[:n], _Owned(a), _Owned(b), a.col_blocks.starts,
         _local_table(c.layout, c.layout.blocks.n_blocks), c.slab,
-        K4_MAX_ROWS, MAX_BLOCK_ROWS, DATA_BYTES, STAGE_BYTES, _n_parts(c.device))
+        K4_MAX_ROWS, MAX_BLOCK_ROWS, chunk_bytes()[1], chunk_bytes()[0], _n_parts(c.device))
     rows = a.local_row_sizes[:n]
     flops = int(2 * np.sum(rows * a.slab.width[:n] * b.slab.width[:n]))
     plan = ChunkPlan(arrays, flops)
@@ -166,7 +182,7 @@ def mmult_plan(a, b, c) -> ChunkPlan:
         raise ShapeError(f"row block {bad} of b is incomplete (split ghost group)")
     arrays = _plan.chunk_plan(
         5, a.local_row_sizes[:n], _Owned(a), _Owned(c), a.col_blocks.starts, btab, b.slab,
-        K5_MAX_ROWS, MAX_BLOCK_ROWS, DATA_BYTES, STAGE_BYTES, _n_parts(c.device))
+        K5_MAX_ROWS, MAX_BLOCK_ROWS, chunk_bytes()[1], chunk_bytes()[0], _n_parts(c.device))
     rows = a.local_row_sizes[:n]
     flops = int(2 * np.sum(rows * a.slab.width[:n] * c.slab.width[:n]))
     plan = ChunkPlan(arrays, flops, zero_begin=c._ghost_data_begin)

@@ -37,17 +37,26 @@
 namespace bmv {
 namespace {
 
-#ifndef BMV_SPMM_WARPS
-#define BMV_SPMM_WARPS 12
+// Warps per CTA (each with its own pipeline), measured per kernel
+// (profiles/r02_spmm_cpasync_*): K4 stages two operands and gains from
+// larger chunks, K5 from more warps.
+#ifndef BMV_K4_WARPS
+#define BMV_K4_WARPS 12
+#endif
+#ifndef BMV_K5_WARPS
+#define BMV_K5_WARPS 16
 #endif
 #ifndef BMV_SPMM_BUFS
 #define BMV_SPMM_BUFS 2
 #endif
-constexpr int kCW = BMV_SPMM_WARPS;   // warps per CTA, each with its own pipeline
 constexpr int kNB = BMV_SPMM_BUFS;    // buffers per warp (kNB - 1 chunks in flight)
 constexpr int kSmemBytes = 224 * 1024;
-// bytes per buffer = the largest chunk [meta | A | B] the planner may build
-constexpr int kBufBytes = kSmemBytes / (kCW * kNB) / 128 * 128;
+template <int KIND>
+struct Shape {
+  static constexpr int CW = KIND == 4 ? BMV_K4_WARPS : BMV_K5_WARPS;
+  // bytes per buffer = the largest chunk [meta | A | B] the planner may build
+  static constexpr int BUF = kSmemBytes / (CW * kNB) / 128 * 128;
+};
 
 // Per-chunk copy descriptor (built once in bmv_chunk_plan_create), 32 bytes:
 // one sector, loaded by the claiming warp a pipeline step ahead of its use.
@@ -76,10 +85,24 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Warp-wide copy of `bytes` (multiple of 16) from global to shared memory.
+// Warp-wide copy of `bytes` (multiple of 16) from global to shared memory:
+// rows of 512 bytes, lane l moving bytes [16 l, 16 l + 16) of every row.
 __device__ __forceinline__ void warp_copy(unsigned dst, const char* src, unsigned bytes, int lane) {
-  for (unsigned o = lane * 16u; o < bytes; o += 512u) cp_async16(dst + o, src + o);
+  const char* p = src + lane * 16;
+  unsigned d = dst + lane * 16u;
+  int rows = (int)(bytes >> 9);
+  for (; rows >= 4; rows -= 4, p += 2048, d += 2048u) {
+    cp_async16(d, p);
+    cp_async16(d + 512u, p + 512);
+    cp_async16(d + 1024u, p + 1024);
+    cp_async16(d + 1536u, p + 1536);
+  }
+  for (; rows > 0; --rows, p += 512, d += 512u) cp_async16(d, p);
+  if (lane * 16u < (bytes & 511u)) cp_async16(d, p);
 }
+
+// Byte offset (in the chunk buffer) of an 8-byte zero: header words 14, 15.
+constexpr int kZeroByte = 56;
 
 // ---------------------------------------------------------------- K4 -----
 // S[rb[a] + st[kk[a]][b]] += sum_rows A[row][cma[seg][a]] * B[row][cmb[seg][b]]
@@ -91,8 +114,7 @@ __device__ __forceinline__ void k4_pass(const int32_t* m, double* __restrict__ c
                                         int lane) {
   const int nseg = m[H_NSEG], ua = m[H_UA], ub = m[H_UB];
   const char* st = reinterpret_cast<const char*>(m);
-  const double* As = reinterpret_cast<const double*>(st + m[H_AOFF]);
-  const double* Bs = reinterpret_cast<const double*>(st + m[H_BOFF]);
+  const int aoff = m[H_AOFF], boff = m[H_BOFF];
   const int4* seg = reinterpret_cast<const int4*>(m + m[H_SEG]);
   const int16_t* cma = reinterpret_cast<const int16_t*>(m + m[H_CMA]);
   const int16_t* cmb = reinterpret_cast<const int16_t*>(m + m[H_CMB]);
@@ -104,33 +126,51 @@ __device__ __forceinline__ void k4_pass(const int32_t* m, double* __restrict__ c
     for (int u = 0; u < TB; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
   for (int s = 0; s < nseg; ++s) {
     const int4 r0 = seg[2 * s];
-    const int kb = m[m[H_SEG] + 8 * s + 4];
+    const int kb = seg[2 * s + 1].x;
     const int nrows = r0.x, ka = r0.z;
-    int oa[TA], ob[TB];
-    bool va[TA], vb[TB];
+    // per-lane fragment addresses (bytes in the buffer) and k-step strides; a
+    // union column this segment does not store reads the buffer's zero, stride 0
+    int pa[TA], sa[TA], pb[TB], sb[TB];
 #pragma unroll
     for (int t = 0; t < TA; ++t) {
       const int aa = ag + t * 8 + g4;
       const int sl = aa < ua ? cma[s * ua + aa] : -1;
-      va[t] = sl >= 0;
-      oa[t] = r0.y + t4 * ka + sl;
+      pa[t] = sl >= 0 ? aoff + 8 * (r0.y + t4 * ka + sl) : kZeroByte;
+      sa[t] = sl >= 0 ? 32 * ka : 0;
     }
 #pragma unroll
     for (int u = 0; u < TB; ++u) {
       const int bb = bg + u * 8 + g4;
       const int sl = bb < ub ? cmb[s * ub + bb] : -1;
-      vb[u] = sl >= 0;
-      ob[u] = r0.w + t4 * kb + sl;
+      pb[u] = sl >= 0 ? boff + 8 * (r0.w + t4 * kb + sl) : kZeroByte;
+      sb[u] = sl >= 0 ? 32 * kb : 0;
     }
-    const int nks = (nrows + 3) >> 2;
-    int xa = 0, xb = 0;
-    for (int ks = 0; ks < nks; ++ks, xa += 4 * ka, xb += 4 * kb) {
-      const bool rok = ks * 4 + t4 < nrows;
+    const int full = nrows >> 2;
+#pragma unroll 2
+    for (int ks = 0; ks < full; ++ks) {
       double av[TA], bv[TB];
 #pragma unroll
-      for (int t = 0; t < TA; ++t) av[t] = (rok && va[t]) ? As[oa[t] + xa] : 0.0;
+      for (int t = 0; t < TA; ++t) {
+        av[t] = *reinterpret_cast<const double*>(st + pa[t]);
+        pa[t] += sa[t];
+      }
 #pragma unroll
-      for (int u = 0; u < TB; ++u) bv[u] = (rok && vb[u]) ? Bs[ob[u] + xb] : 0.0;
+      for (int u = 0; u < TB; ++u) {
+        bv[u] = *reinterpret_cast<const double*>(st + pb[u]);
+        pb[u] += sb[u];
+      }
+#pragma unroll
+      for (int t = 0; t < TA; ++t)
+#pragma unroll
+        for (int u = 0; u < TB; ++u) dmma_8x8x4(acc[t][u][0], acc[t][u][1], av[t], bv[u]);
+    }
+    if (nrows & 3) {  // last k-step: rows past the segment contribute zeros
+      const bool rok = t4 < (nrows & 3);
+      double av[TA], bv[TB];
+#pragma unroll
+      for (int t = 0; t < TA; ++t) av[t] = rok ? *reinterpret_cast<const double*>(st + pa[t]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < TB; ++u) bv[u] = rok ? *reinterpret_cast<const double*>(st + pb[u]) : 0.0;
 #pragma unroll
       for (int t = 0; t < TA; ++t)
 #pragma unroll
@@ -145,7 +185,7 @@ __device__ __forceinline__ void k4_pass(const int32_t* m, double* __restrict__ c
   for (int t = 0; t < TA; ++t) {
     const int aa = ag + t * 8 + g4;
     if (aa >= ua) continue;
-    const int base = rb[aa];
+    double* crow = c + rb[aa];
     const int32_t* srow = stt + kk[aa] * ub;
 #pragma unroll
     for (int u = 0; u < TB; ++u) {
@@ -154,7 +194,7 @@ __device__ __forceinline__ void k4_pass(const int32_t* m, double* __restrict__ c
         const int bb = bg + u * 8 + 2 * t4 + e;
         if (bb < ub) {
           const int sl = srow[bb];
-          if (sl >= 0) atomicAdd(c + (int64_t)base + sl, acc[t][u][e]);
+          if (sl >= 0) atomicAdd(crow + sl, acc[t][u][e]);
         }
       }
     }
@@ -200,7 +240,7 @@ __device__ __forceinline__ void k5_pass(const int32_t* m, const double* __restri
                                         int bg, int lane) {
   const int nseg = m[H_NSEG], ua = m[H_UA], ub = m[H_UB];
   const char* st = reinterpret_cast<const char*>(m);
-  const double* As = reinterpret_cast<const double*>(st + m[H_AOFF]);
+  const int aoff = m[H_AOFF];
   const int4* seg = reinterpret_cast<const int4*>(m + m[H_SEG]);
   const int16_t* cma = reinterpret_cast<const int16_t*>(m + m[H_CMA]);
   const int16_t* cmy = reinterpret_cast<const int16_t*>(m + m[H_CMB]);
@@ -214,7 +254,7 @@ __device__ __forceinline__ void k5_pass(const int32_t* m, const double* __restri
     for (int ks = 0; ks < KS; ++ks) {
       const int ka = ag + ks * 4 + t4;
       const bool okk = ka < ua;
-      const int base = okk ? cb[ka] : 0;
+      const double* cbase = cmat + (okk ? cb[ka] : 0);
       const int32_t* crow = ct + (okk ? ck[ka] : 0) * ub;
 #pragma unroll
       for (int u = 0; u < TB; ++u) {
@@ -222,7 +262,7 @@ __device__ __forceinline__ void k5_pass(const int32_t* m, const double* __restri
         double v = 0.0;
         if (okk && bb < ub) {
           const int sl = crow[bb];
-          if (sl >= 0) v = __ldg(cmat + (int64_t)base + sl);
+          if (sl >= 0) v = __ldg(cbase + sl);
         }
         bf[ks][u] = v;
       }
@@ -230,16 +270,17 @@ __device__ __forceinline__ void k5_pass(const int32_t* m, const double* __restri
     const bool add_old = accumulate || ag > 0;
     for (int s = 0; s < nseg; ++s) {
       const int4 r0 = seg[2 * s];
-      const int ky = m[m[H_SEG] + 8 * s + 4];
+      const int ky = seg[2 * s + 1].x;
       const int nrows = r0.x, ka = r0.z;
-      int oa[KS];
-      unsigned vmask = 0;
+      // per-lane A fragment addresses (bytes in the buffer) / row-tile strides;
+      // a union column this segment does not store reads the buffer's zero
+      int pa[KS], sa[KS];
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         const int aa = ag + ks * 4 + t4;
         const int sl = aa < ua ? cma[s * ua + aa] : -1;
-        if (sl >= 0) vmask |= 1u << ks;
-        oa[ks] = r0.y + g4 * ka + sl;
+        pa[ks] = sl >= 0 ? aoff + 8 * (r0.y + g4 * ka + sl) : kZeroByte;
+        sa[ks] = sl >= 0 ? 64 * ka : 0;
       }
       int sy[TB][2];
 #pragma unroll
@@ -249,17 +290,17 @@ __device__ __forceinline__ void k5_pass(const int32_t* m, const double* __restri
           const int bb = bg + u * 8 + 2 * t4 + e;
           sy[u][e] = bb < ub ? cmy[s * ub + bb] : -1;
         }
-      double* yseg = y + (int64_t)r0.w + (int64_t)g4 * ky;
+      double* yrow = y + (int64_t)r0.w + (int64_t)g4 * ky;
       const int nrt = (nrows + 7) >> 3;
-      int xa = 0;
-      for (int rt = 0; rt < nrt; ++rt, xa += 8 * ka, yseg += 8 * ky) {
-        const bool rok = rt * 8 + g4 < nrows;
+      for (int rt = 0; rt < nrt; ++rt, yrow += 8 * ky) {
+        const bool rok = rt * 8 + g4 < nrows;  // false only in the last tile
         double acc[TB][2];
 #pragma unroll
         for (int u = 0; u < TB; ++u) acc[u][0] = acc[u][1] = 0.0;
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
-          const double av = (rok && ((vmask >> ks) & 1u)) ? As[oa[ks] + xa] : 0.0;
+          const double av = rok ? *reinterpret_cast<const double*>(st + pa[ks]) : 0.0;
+          pa[ks] += sa[ks];
 #pragma unroll
           for (int u = 0; u < TB; ++u) dmma_8x8x4(acc[u][0], acc[u][1], av, bf[ks][u]);
         }
@@ -269,9 +310,10 @@ __device__ __forceinline__ void k5_pass(const int32_t* m, const double* __restri
 #pragma unroll
             for (int e = 0; e < 2; ++e)
               if (sy[u][e] >= 0) {
+                double* yp = yrow + sy[u][e];
                 double v = alpha * acc[u][e];
-                if (add_old) v += yseg[sy[u][e]];
-                yseg[sy[u][e]] = v;
+                if (add_old) v += *yp;
+                *yp = v;
               }
         }
       }
@@ -305,9 +347,10 @@ __device__ __forceinline__ void k5_chunk(const char* st, const double* __restric
 }
 
 template <int KIND>  // 4: K4, 5: K5
-__global__ void __launch_bounds__(kCW * 32, 1)
+__global__ void __launch_bounds__(Shape<KIND>::CW * 32, 1)
     chunk_kernel(const ChunkArgs g, const double* __restrict__ a, const double* __restrict__ b,
                  double* __restrict__ out, double alpha, int accumulate) {
+  constexpr int kBufBytes = Shape<KIND>::BUF;
   extern __shared__ __align__(128) char smem[];
   __shared__ int next_chunk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -400,8 +443,10 @@ int bmv_chunk_plan_create(const bmv_chunk_desc* d, bmv_chunk_plan** out) {
   using namespace bmv;
   *out = nullptr;
   if (!d || (d->kind != 4 && d->kind != 5) || d->n_parts <= 0 || d->n_chunks < 0 ||
-      d->stage_bytes <= 0 || (d->stage_bytes & 15) || d->stage_bytes > kBufBytes) {
-    set_error("bmv_chunk_plan_create: invalid descriptor (chunks of at most %d bytes)", kBufBytes);
+      d->stage_bytes <= 0 || (d->stage_bytes & 15) ||
+      d->stage_bytes > (d->kind == 4 ? Shape<4>::BUF : Shape<5>::BUF)) {
+    set_error("bmv_chunk_plan_create: invalid descriptor (chunks of at most %d bytes)",
+              d && d->kind == 4 ? Shape<4>::BUF : Shape<5>::BUF);
     return BMV_ERR_INVALID;
   }
   // per-chunk copy descriptors
@@ -464,16 +509,17 @@ static int launch_chunks(const bmv_chunk_plan* p, const double* a, const double*
     return BMV_ERR_INVALID;
   }
   ChunkArgs g{p->part_start, p->desc, p->meta};
-  const int smem = kCW * kNB * kBufBytes;
   cudaStream_t st = as_stream(stream);
   if (p->kind == 4) {
+    constexpr int smem = Shape<4>::CW * kNB * Shape<4>::BUF;
     BMV_CUDA_TRY(cudaFuncSetAttribute(chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       smem));
-    chunk_kernel<4><<<p->n_parts, kCW * 32, smem, st>>>(g, a, b, out, alpha, accumulate);
+    chunk_kernel<4><<<p->n_parts, Shape<4>::CW * 32, smem, st>>>(g, a, b, out, alpha, accumulate);
   } else {
+    constexpr int smem = Shape<5>::CW * kNB * Shape<5>::BUF;
     BMV_CUDA_TRY(cudaFuncSetAttribute(chunk_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       smem));
-    chunk_kernel<5><<<p->n_parts, kCW * 32, smem, st>>>(g, a, b, out, alpha, accumulate);
+    chunk_kernel<5><<<p->n_parts, Shape<5>::CW * 32, smem, st>>>(g, a, b, out, alpha, accumulate);
   }
   BMV_CHECK_LAUNCH();
   return BMV_OK;
@@ -503,9 +549,13 @@ int bmv_mmult_run(const bmv_chunk_plan* p, const double* a, const double* cmat, 
   return launch_chunks(p, a, cmat, y, alpha, accumulate, stream);
 }
 
-int bmv_chunk_kernel_config(int32_t* consumer_warps, int32_t* stages) {
-  *consumer_warps = bmv::kCW;
-  *stages = bmv::kBufBytes;
+int bmv_chunk_kernel_config(int32_t kind, int32_t* warps, int32_t* buffer_bytes) {
+  if (kind != 4 && kind != 5) {
+    bmv::set_error("bmv_chunk_kernel_config: kind must be 4 or 5");
+    return BMV_ERR_INVALID;
+  }
+  *warps = kind == 4 ? bmv::Shape<4>::CW : bmv::Shape<5>::CW;
+  *buffer_bytes = kind == 4 ? bmv::Shape<4>::BUF : bmv::Shape<5>::BUF;
   return BMV_OK;
 }
 

@@ -31,14 +31,14 @@ MAX_BLOCK_ROWS = 16
 META_ALLOWANCE = 1536        # bytes left for the chunk meta when cutting chunks
 
 
-def chunk_bytes() -> tuple[int, int]:
-    """(largest chunk, staged values per chunk) in bytes."""
+def chunk_bytes(kind: int) -> tuple[int, int]:
+    """(largest chunk, staged values per chunk) in bytes for K4 / K5 (kind 4 / 5)."""
     if "BMV_SPMM_STAGE" in os.environ:
         stage = int(os.environ["BMV_SPMM_STAGE"])
     else:
         C = _lib.C
         warps, buf = C.c_int32(), C.c_int32()
-        _lib.check(_lib.load().bmv_chunk_kernel_config(C.byref(warps), C.byref(buf)))
+        _lib.check(_lib.load().bmv_chunk_kernel_config(int(kind), C.byref(warps), C.byref(buf)))
         stage = int(buf.value)
     data = int(os.environ.get("BMV_SPMM_DATA", max(stage - META_ALLOWANCE, stage // 2)))
     return stage, data
@@ -154,7 +154,7 @@ def tmmult_plan(a, b, c) -> ChunkPlan:
     arrays = _plan.chunk_plan(
         4, a.local_row_sizes[:n], _Owned(a), _Owned(b), a.col_blocks.starts,
         _local_table(c.layout, c.layout.blocks.n_blocks), c.slab,
-        K4_MAX_ROWS, MAX_BLOCK_ROWS, chunk_bytes()[1], chunk_bytes()[0], _n_parts(c.device))
+        K4_MAX_ROWS, MAX_BLOCK_ROWS, chunk_bytes(4)[1], chunk_bytes(4)[0], _n_parts(c.device))
     rows = a.local_row_sizes[:n]
     flops = int(2 * np.sum(rows * a.slab.width[:n] * b.slab.width[:n]))
     plan = ChunkPlan(arrays, flops)
@@ -182,7 +182,7 @@ def mmult_plan(a, b, c) -> ChunkPlan:
         raise ShapeError(f"row block {bad} of b is incomplete (split ghost group)")
     arrays = _plan.chunk_plan(
         5, a.local_row_sizes[:n], _Owned(a), _Owned(c), a.col_blocks.starts, btab, b.slab,
-        K5_MAX_ROWS, MAX_BLOCK_ROWS, chunk_bytes()[1], chunk_bytes()[0], _n_parts(c.device))
+        K5_MAX_ROWS, MAX_BLOCK_ROWS, chunk_bytes(5)[1], chunk_bytes(5)[0], _n_parts(c.device))
     rows = a.local_row_sizes[:n]
     flops = int(2 * np.sum(rows * a.slab.width[:n] * c.slab.width[:n]))
     plan = ChunkPlan(arrays, flops, zero_begin=c._ghost_data_begin)

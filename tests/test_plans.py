@@ -32,7 +32,7 @@ def _setup(block_size, lane_width, compact, level=1, degree=2):
 
 
 def _shape(monkeypatch, stage, rows):
-    monkeypatch.setattr(spmm, "chunk_bytes", lambda: (stage, stage - 1024))
+    monkeypatch.setattr(spmm, "chunk_bytes", lambda kind: (stage, stage - 1024))
     monkeypatch.setattr(spmm, "K4_MAX_ROWS", rows)
 
 
@@ -43,12 +43,12 @@ def _plan(kind, a, b, c, n_parts):
     if kind == 4:
         return NP.chunk_plan(4, a.local_row_sizes[:n], spmm._Owned(a), spmm._Owned(b),
                              a.col_blocks.starts, spmm._local_table(c.layout, c.layout.blocks.n_blocks),
-                             c.slab, spmm.K4_MAX_ROWS, spmm.MAX_BLOCK_ROWS, spmm.chunk_bytes()[1],
-                             spmm.chunk_bytes()[0], n_parts)
+                             c.slab, spmm.K4_MAX_ROWS, spmm.MAX_BLOCK_ROWS, spmm.chunk_bytes(4)[1],
+                             spmm.chunk_bytes(4)[0], n_parts)
     return NP.chunk_plan(5, a.local_row_sizes[:n], spmm._Owned(a), spmm._Owned(c),
                          a.col_blocks.starts, spmm._local_table(b.layout, b.layout.blocks.n_blocks),
-                         b.slab, spmm.K5_MAX_ROWS, spmm.MAX_BLOCK_ROWS, spmm.chunk_bytes()[1],
-                         spmm.chunk_bytes()[0], n_parts)
+                         b.slab, spmm.K5_MAX_ROWS, spmm.MAX_BLOCK_ROWS, spmm.chunk_bytes(5)[1],
+                         spmm.chunk_bytes(5)[0], n_parts)
 
 
 @pytest.mark.parametrize("block_size,lane_width", [(3, 8), (8, 8), (12, 8), (3, 4)])

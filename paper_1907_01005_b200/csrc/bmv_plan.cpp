@@ -447,9 +447,10 @@ bmvp_chunks* bmvp_chunk_plan(int32_t kind, int64_t n_rows, const int64_t* rows,
         continue;
       }
       if (s0.r1 - s0.r0 > 1) {
-        const int64_t mid = (s0.r0 + s0.r1) / 2;
-        chunks[ci] = {{s0.row, s0.r0, mid}};
-        chunks.insert(chunks.begin() + ci + 1, std::vector<Segment>{{s0.row, mid, s0.r1}});
+        const Segment whole = s0;  // s0 refers into chunks[ci], reassigned below
+        const int64_t mid = (whole.r0 + whole.r1) / 2;
+        chunks[ci] = {{whole.row, whole.r0, mid}};
+        chunks.insert(chunks.begin() + ci + 1, std::vector<Segment>{{whole.row, mid, whole.r1}});
         --ci;
         continue;
       }

@@ -97,3 +97,35 @@ def test_long_block_rows_split_into_row_ranges(monkeypatch):
     sm.data.copy_(torch.from_numpy(got))
     want = x.to_dense_owned().T @ hx.to_dense_owned()
     assert np.allclose(sm.to_dense_owned(), want, rtol=1e-13, atol=1e-13 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("stage", [9472, 7168, 4096])
+def test_wide_rows_split_when_meta_and_rows_exceed_a_buffer(monkeypatch, stage):
+    """Six wide supports, full storage (48 columns per row): the greedy row
+    pieces plus their meta exceed a buffer and are halved again (a piece
+    once lost its second half there)."""
+    centers = np.asarray([[1.0, 1.0, 1.0], [3.0, 3.0, 2.0], [2.0, 1.5, 3.0], [0.5, 3.2, 0.7],
+                          [2.5, 2.5, 0.5], [1.5, 3.5, 2.5]])
+    monkeypatch.setattr(spmm, "chunk_bytes", lambda kind: (stage, stage - 1536))
+    s = Small((4, 4, 4), (1.0, 1.0, 1.0), 1, 2, centers, 3.5, 8, 8)
+    ctx = serial_context("cpu")
+    rl, _, x, hx = s.operands(ctx, "cpu")
+    s.fill(x, 5, attach=False)
+    hx.fill_owned_entries(lambda r, c: hashed_entries(9, r, c))
+    sm, cm, xc = s.projection_operands(ctx, "cpu", rl)
+    arr = _plan(4, x, hx, sm, 5)
+    n = x.n_owned_blocks
+    rows_planned = sum(int(arr["meta"][int(m0) + 1]) for m0 in arr["chunk_meta"][:-1])
+    assert rows_planned == int(x.local_row_sizes[:n].sum())
+    got = emulate_tmmult(arr, x.data.numpy(), hx.data.numpy(), sm.data.numel())
+    sm.data.copy_(torch.from_numpy(got))
+    want = x.to_dense_owned().T @ hx.to_dense_owned()
+    assert np.allclose(sm.to_dense_owned(), want, rtol=1e-13, atol=1e-13 * np.abs(want).max())
+    arr = _plan(5, x, cm, xc, 5)
+    got = emulate_mmult(arr, x.data.numpy(), cm.data.numpy(), xc.data.numpy(), 0.75, False)
+    xc.data.copy_(torch.from_numpy(got))
+    stored = np.zeros(xc.to_dense_owned().shape, dtype=bool)
+    _, grow, gcol = xc._valid_owned_index()
+    stored[grow, gcol] = True
+    want = np.where(stored, 0.75 * (x.to_dense_owned() @ cm.to_dense_owned()), 0.0)
+    assert np.allclose(xc.to_dense_owned(), want, rtol=1e-13, atol=1e-13 * np.abs(want).max())

@@ -78,6 +78,10 @@ typedef struct {
   const int32_t* pair_ngp;    /* n_pairs: table entries (even)             */
   const int32_t* gtab;        /* gtab_len                                  */
   const uint32_t* codes;      /* n_cells * code_stride                     */
+  int32_t n_breaks;           /* pair indices (ascending) at which a launch
+                                 range of bmv_cellop_apply_*pairs may start
+                                 or end, besides 0 and n_pairs              */
+  const int64_t* breaks;
   /* 1D tables (row-major, q x n): Lagrange values S at the Gauss points and
      the collocation derivative D_co = D S^-1 (q x q); 1D weights w.       */
   double S[BMV_MAX_NODES * BMV_MAX_NODES];

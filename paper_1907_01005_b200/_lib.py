@@ -36,6 +36,7 @@ class CellopDesc(C.Structure):
         ("code_stride", C.c_int32), ("max_groups", C.c_int32), ("n_pairs", C.c_int64),
         ("gtab_len", C.c_int64), ("pair_cell", _i32p), ("pair_gtab", _i64p),
         ("pair_ngp", _i32p), ("gtab", _i32p), ("codes", _u32p),
+        ("n_breaks", C.c_int32), ("breaks", _i64p),
         ("S", C.c_double * (MAX_NODES * MAX_NODES)), ("Dco", C.c_double * (MAX_NODES * MAX_NODES)),
         ("w", C.c_double * MAX_NODES), ("kin", C.c_double * 3), ("det", C.c_double),
     ]

@@ -16,17 +16,19 @@
 // therefore ~4 B per cell DoF + 8 B per (pair, group) instead of an offset
 // per (pair, DoF).
 //
-// Per pair, lane t = 0 issues cp.async.bulk copies (TMA) of the cell's code
-// row, the pair's group table and the cell's coefficient row (w3 V) into the
-// warp's shared memory (one mbarrier per warp).  The code row lands in the
-// pair's transpose tile (dead until the first transpose); once the
-// coefficient row has been consumed the code row is copied again into its
-// place for the scatter (second mbarrier phase, lands during the remaining
-// contractions).
-//
-// n = 4, 5: n threads per pair, thread t holds plane z = t (bmv_sumfac.cuh,
-// 12 contractions, 4 transposes through the pair tile).  n = 2, 3: one
-// thread per pair, whole n^3 tensor in registers (bmv_cellop_pair.cuh).
+// n = 4, 5 (plane kernel): n threads per pair, thread t holds plane z = t
+// (bmv_sumfac.cuh, 12 contractions, 4 transposes through the pair tile); a
+// warp works on a BATCH of up to 32 / n consecutive pairs that lie in at
+// most two cells (the host cuts the batches; 97-99 % of the lanes are used
+// at the BASELINE configs).  The kernel is persistent: every warp loops
+// over batches and keeps two metadata stages in shared memory -- the code
+// and coefficient rows of the batch's (<= 2) cells, shared by its pairs,
+// and the pairs' group tables, fetched by cp.async.bulk (TMA) one batch
+// ahead on one mbarrier per stage -- so neither the descriptor nor the
+// metadata latency is exposed, and the gather is branch-free (an absent
+// column reads a valid address and is masked).
+// n = 2, 3: one thread per pair, whole n^3 tensor in registers
+// (bmv_cellop_pair.cuh), per-pair metadata copies.
 // Scatter-add: fp64 RED (atomicAdd) into the zeroed destination.
 #include <cuda_runtime.h>
 
@@ -45,17 +47,38 @@ int zero_async(double* p, int64_t n, cudaStream_t st);
 
 namespace {
 
+// plane kernel, n = 5: warps per CTA, one CTA per SM.  Registers are per SM
+// sub-partition (16384 each): 12 warps leave 168 per thread, 8 warps 255.
+#ifndef BMV_K1_WARPS5
+#define BMV_K1_WARPS5 8
+#endif
+#ifndef BMV_K1_WARPS4
+#define BMV_K1_WARPS4 12
+#endif
 constexpr int kWarps = 4;  // warps per CTA
 
+// A batch of the plane kernel: pairs [first_pair, first_pair + np), the first
+// nA in cell_a, the rest in cell_b; their group tables are consecutive.
+struct __align__(16) Batch {
+  int32_t first_pair;
+  int32_t cell_a, cell_b;
+  int32_t info;      // nA | np << 8 | groups per pair of cell_a << 16 | of cell_b << 24
+  int32_t gt16;      // first group-table entry of the batch, 16-byte units
+  int32_t gt_bytes;  // bytes of the batch's group tables (multiple of 16)
+  int32_t pad[2];
+};
+
 struct K1Args {
-  const int4* __restrict__ desc;       // {cell, gtab offset (16-byte units), ngp, 0}
+  const int4* __restrict__ desc;       // pair kernel: {cell, gtab offset (16-byte units), ngp, 0}
+  const Batch* __restrict__ batches;   // plane kernel
+  int64_t b0, b1;                      // batch range of this launch
   const uint32_t* __restrict__ codes;  // code rows, code_stride words per cell
   const int2* __restrict__ gtab;       // {src offset | -1, dst offset}
   int code_stride;                     // uint32 words per code row (multiple of 4)
   int gbytes;                          // group-table bytes reserved per pair (16 | it)
   const double* __restrict__ coef;
   int coef_cell;  // 1: row per cell (stride q3p), 0: one row
-  int64_t n_pairs;
+  int64_t n_pairs;                     // pair kernel: pairs of this launch
   const double* __restrict__ x;
   double* __restrict__ hx;
   double* __restrict__ mx;             // fused mass output (DUAL), same layout as hx
@@ -84,32 +107,45 @@ __device__ __forceinline__ Code<WIDE> decode(const uint32_t* row, int d) {
   return c;
 }
 
-// Per nodes-per-axis N (plane kernel): P pairs per warp; per pair a tile
-// region (transposes; the code row for the gather at its first 16-byte
-// boundary), a coefficient region (CS doubles, >= q3p; later the code row
-// for the scatter) and a group-table region.
+// Per nodes-per-axis N (plane kernel): P pairs per warp.  Per warp: the
+// transpose tiles of its pairs and two metadata stages
+//   [info (16 B) | coef row cell a | coef row cell b | code row a | code row b | group tables].
 template <int N>
 struct K1Shape {
   static constexpr int P = 32 / N;
   static constexpr int N3 = N * N * N;
   static constexpr int Q3P = (N3 + 1) / 2 * 2;
-  static constexpr int CS = N == 5 ? 134 : (N == 4 ? 66 : 28);
-  static constexpr int MINB = N == 5 ? 3 : 4;
-  static constexpr int tile_bytes = (P * Tile<N>::TILE * 8 + 15) / 16 * 16;
-  static constexpr int coef_bytes = P * CS * 8;
+  static constexpr int CB = Q3P * 8;  // bytes of a coefficient row (multiple of 16)
+  static constexpr int WARPS = N == 5 ? BMV_K1_WARPS5 : BMV_K1_WARPS4;  // warps per CTA (1 CTA / SM)
+  // prefetch the next batch's X values into registers (needs the registers
+  // that at most 2 warps per sub-partition at n = 5, 3 at n = 4, leave)
+  static constexpr bool PREF = N == 5 ? WARPS <= 8 : WARPS <= 12;
+  static constexpr int STAGES = PREF ? 3 : 2;
+  // registers per thread: n = 5 what the warps of one CTA per SM leave in a
+  // sub-partition; n = 4: 4 CTAs x 4 warps x 128
+  static constexpr int REGS = 16384 / ((WARPS + 3) / 4 * 32) / 8 * 8 > 255
+                                  ? 255
+                                  : 16384 / ((WARPS + 3) / 4 * 32) / 8 * 8;
+  static constexpr int tile_bytes = (P * Tile3<N>::TILE * 8 + 15) / 16 * 16;
 };
 
 template <int N>
-__host__ __device__ constexpr int k1_warp_bytes(int gbytes) {
-  return K1Shape<N>::tile_bytes + K1Shape<N>::coef_bytes + K1Shape<N>::P * gbytes;
+__host__ __device__ constexpr int k1_stage_bytes(int code_stride, int gbytes) {
+  return (16 + 2 * K1Shape<N>::CB + 2 * code_stride * 4 + K1Shape<N>::P * gbytes + 127) / 128 * 128;
+}
+template <int N>
+__host__ __device__ constexpr int k1_warp_bytes(int code_stride, int gbytes) {
+  return (K1Shape<N>::tile_bytes + 127) / 128 * 128 +
+         K1Shape<N>::STAGES * k1_stage_bytes<N>(code_stride, gbytes);
 }
 
 __device__ __forceinline__ void proxy_fence() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
-// Scatter-add of a plane result (A layout, z = t) through the code row.
-template <int N, bool WIDE>
+// Scatter-add of a plane result through the code row.  LAY 0: X layout
+// (thread t holds x = t, v[z][y]); LAY 2: Z layout (z = t, v[y][x]).
+template <int N, bool WIDE, int LAY>
 struct PlaneScatter {
   double* dst;
   const uint32_t* codes;
@@ -121,165 +157,204 @@ struct PlaneScatter {
                                              const CellTables&) const {
     if (!ok) return;
 #pragma unroll
-    for (int y = 0; y < N; ++y)
+    for (int i = 0; i < N; ++i)
 #pragma unroll
-      for (int x = 0; x < N; ++x) {
-        const Code<WIDE> c = decode<WIDE>(codes, t * N * N + y * N + x);
-        atomicAdd(dst + (int64_t)gt[c.g].y + c.rh, v[y][x]);
+      for (int j = 0; j < N; ++j) {
+        const int d = LAY == 0 ? i * N * N + j * N + t : t * N * N + i * N + j;
+        const Code<WIDE> c = decode<WIDE>(codes, d);
+        atomicAdd(dst + (int64_t)gt[c.g].y + c.rh, v[i][j]);
       }
   }
 };
 template <int N, bool WIDE>
 struct MassScatter {
-  PlaneScatter<N, WIDE> sc;
+  PlaneScatter<N, WIDE, 0> sc;
   const double* w3;
   template <int NN, class L>
-  __device__ __forceinline__ void operator()(double (&uqB)[NN][NN], double* buf, int tt,
+  __device__ __forceinline__ void operator()(double (&uqZ)[NN][NN], double* buf, int tt,
                                              bool lane_ok, const CellTables& tb) const {
-    mass_back_plane<NN, L>(uqB, w3, buf, tt, lane_ok, tb);
-    sc.template operator()<NN, L>(uqB, buf, tt, lane_ok, tb);
-  }
-};
-// Re-stage the code row into the (consumed) coefficient region.
-struct Restage {
-  uint32_t* dst;
-  const uint32_t* src;
-  unsigned bytes;
-  uint64_t* bar;
-  bool issuer;
-  // warp-collective: one arrival (lane 0) announcing every issuer's bytes
-  __device__ __forceinline__ void operator()() const {
-    __syncwarp();
-    const unsigned total = __reduce_add_sync(~0u, issuer ? bytes : 0u);
-    if ((threadIdx.x & 31) == 0) mbar_expect_tx(bar, total);
-    __syncwarp();
-    if (issuer) {
-      proxy_fence();
-      bulk_g2s(dst, src, bytes, bar);
-    }
-  }
-};
-
-// Wait for the re-staged code row, then scatter.
-template <class H>
-struct WaitThen {
-  H h;
-  uint64_t* bar;
-  template <int NN, class L>
-  __device__ __forceinline__ void operator()(double (&v)[NN][NN], double* b, int x, bool o,
-                                             const CellTables& tbl) const {
-    mbar_wait(bar, 1);
-    h.template operator()<NN, L>(v, b, x, o, tbl);
+    mass_back_lean<NN, L>(uqZ, w3, buf, tt, lane_ok, tb);
+    sc.template operator()<NN, L>(uqZ, buf, tt, lane_ok, tb);
   }
 };
 
 // MODE 0: H (kinetic + optional coefficient), 1: coefficient only (mass),
 // 2: fused H and M (DUAL).
 template <int N, bool COEF, int MODE, bool WIDE>
-__global__ void __launch_bounds__(kWarps * 32, K1Shape<N>::MINB)
+__global__ void __launch_bounds__(K1Shape<N>::WARPS * 32) __maxnreg__(K1Shape<N>::REGS)
     k1_plane_kernel(const K1Args a, const __grid_constant__ CellTables tb) {
   using S = K1Shape<N>;
-  constexpr int P = S::P, N2 = N * N, TILE = Tile<N>::TILE;
+  constexpr int P = S::P, N2 = N * N, TILE = Tile3<N>::TILE, kWarps = S::WARPS;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[kWarps];
+  constexpr int NST = S::STAGES;
+  __shared__ __align__(8) uint64_t bar[kWarps][NST];
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
   const int sub = lid / N;
   const int t = lid - sub * N;
   const bool lane_ok = sub < P;
   const int tt = lane_ok ? t : 0;
-  const int64_t pair = ((int64_t)blockIdx.x * kWarps + warp) * P + sub;
-  const bool ok = lane_ok && pair < a.n_pairs;
 
-  // the 32 - N * P idle lanes use pair 0's regions (they only read them; the
-  // coefficient term is read unguarded, and past the last pair's regions lies
-  // only the small group table, then the end of the CTA's shared memory)
-  const int sp = lane_ok ? sub : 0;
-  unsigned char* wbase = smem + warp * k1_warp_bytes<N>(a.gbytes);
-  double* buf = reinterpret_cast<double*>(wbase) + sp * TILE;
-  uint32_t* code_g = reinterpret_cast<uint32_t*>(
-      (reinterpret_cast<uintptr_t>(buf) + 15) & ~uintptr_t(15));
-  double* cs = reinterpret_cast<double*>(wbase + S::tile_bytes) + sp * S::CS;
-  uint32_t* code_s = reinterpret_cast<uint32_t*>(cs);
-  const int2* gt = reinterpret_cast<const int2*>(wbase + S::tile_bytes + S::coef_bytes +
-                                                 sp * a.gbytes);
-  if (lid == 0) mbar_init(&bar[warp], 1);
-  __syncwarp();
-
-  int4 d = make_int4(0, 0, 0, 0);
-  if (ok) d = __ldg(a.desc + pair);
-  const int cell = d.x;
-  const bool issuer = ok && t == 0;
-  const unsigned cbytes = COEF ? S::Q3P * 8u : 0u;
-  const unsigned kbytes = (unsigned)a.code_stride * 4u;
-  const unsigned gb = (unsigned)d.z * 8u;
-  const uint32_t* gcode = a.codes + (int64_t)cell * a.code_stride;
-  const unsigned my_bytes = issuer ? cbytes + kbytes + gb : 0u;
-  const unsigned total = __reduce_add_sync(~0u, my_bytes);
-  if (lid == 0) mbar_expect_tx(&bar[warp], total);
-  __syncwarp();
-  if (issuer) {
-    if (cbytes)
-      bulk_g2s(cs, a.coef + (a.coef_cell ? (int64_t)cell * S::Q3P : 0), cbytes, &bar[warp]);
-    bulk_g2s(code_g, gcode, kbytes, &bar[warp]);
-    if (gb) bulk_g2s(const_cast<int2*>(gt), a.gtab + (int64_t)d.y, gb, &bar[warp]);
+  const int kb = a.code_stride * 4;  // bytes of a code row
+  const int stage_bytes = k1_stage_bytes<N>(a.code_stride, a.gbytes);
+  unsigned char* wbase = smem + warp * k1_warp_bytes<N>(a.code_stride, a.gbytes);
+  // the 32 - N * P idle lanes share pair 0's tile (they only read it)
+  double* buf = reinterpret_cast<double*>(wbase) + (lane_ok ? sub : 0) * TILE;
+  unsigned char* stage0 = wbase + (S::tile_bytes + 127) / 128 * 128;
+  if (lid == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(&bar[warp][s], 1);
   }
-  mbar_wait(&bar[warp], 0);
+  __syncwarp();
 
-  // gather X (A layout, z = t)
-  double u[N][N];
-#pragma unroll
-  for (int y = 0; y < N; ++y) {
-#pragma unroll
-    for (int x = 0; x < N; ++x) {
-      double v = 0.0;
-      if (ok) {
-        const Code<WIDE> c = decode<WIDE>(code_g, t * N2 + y * N + x);
-        const int xo = gt[c.g].x;
-        if (xo >= 0) v = __ldg(a.x + (int64_t)xo + c.rx);
+  const int nw = (int)gridDim.x * kWarps;
+  const int nb = (int)(a.b1 - a.b0);
+  int b = (int)blockIdx.x * kWarps + warp;
+  // lane 0: fetch the metadata of batch bb into stage s (one mbarrier phase);
+  // the batch's `info` word goes into the stage header for the other lanes
+  auto issue = [&](int s, int bb) {
+    if (lid == 0) {
+      const int4* dp = reinterpret_cast<const int4*>(a.batches + a.b0 + bb);
+      const int4 d0 = __ldg(dp);
+      const int2 d1 = __ldg(reinterpret_cast<const int2*>(dp + 1));
+      unsigned char* st = stage0 + s * stage_bytes;
+      const int na = d0.w & 255, np = (d0.w >> 8) & 255;
+      const bool two = np > na;
+      unsigned total = (unsigned)kb * (two ? 2u : 1u) + (unsigned)d1.y;
+      if (COEF) total += (unsigned)S::CB * (two ? 2u : 1u);
+      *reinterpret_cast<int*>(st) = d0.w;
+      proxy_fence();  // the stage was read (generic proxy) by an earlier batch
+      mbar_expect_tx(&bar[warp][s], total);
+      unsigned char* body = st + 16;
+      if (COEF) {
+        bulk_g2s(body, a.coef + (a.coef_cell ? (int64_t)d0.y * S::Q3P : 0), S::CB, &bar[warp][s]);
+        if (two)
+          bulk_g2s(body + S::CB, a.coef + (a.coef_cell ? (int64_t)d0.z * S::Q3P : 0), S::CB,
+                   &bar[warp][s]);
       }
-      u[y][x] = v;
+      bulk_g2s(body + 2 * S::CB, a.codes + (int64_t)d0.y * a.code_stride, kb, &bar[warp][s]);
+      if (two)
+        bulk_g2s(body + 2 * S::CB + kb, a.codes + (int64_t)d0.z * a.code_stride, kb,
+                 &bar[warp][s]);
+      if (d1.y)
+        bulk_g2s(body + 2 * S::CB + 2 * kb,
+                 reinterpret_cast<const char*>(a.gtab) + (int64_t)d1.x * 16, (unsigned)d1.y,
+                 &bar[warp][s]);
     }
-  }
-  const Restage rs{code_s, gcode, kbytes, &bar[warp], issuer};
-  double out[N][N];
-  if (MODE == 1) {
-    // coefficient only: interpolate, scale at the points, back (2 transposes)
-    double v1[N][N], uqB[N][N];
-    contract_fast<N, false>(u, v1, tb.S);
-    contract_slow<N, false>(v1, out, tb.S);
-    a_to_b<N>(out, v1, buf, tt, lane_ok);  // B: y = qy = t, [z][qx]
-    contract_slow<N, false>(v1, uqB, tb.S);
+  };
+  // this lane's views of a landed stage: its pair's cell rows and group table
+  struct View {
+    bool ok;
+    const double* cs;
+    const uint32_t* code;
+    const int2* gt;
+  };
+  auto view = [&](const unsigned char* st) {
+    const int info = *reinterpret_cast<const int*>(st);
+    const int na = info & 255, np = (info >> 8) & 255;
+    View v;
+    v.ok = lane_ok && sub < np;
+    const int subc = v.ok ? sub : 0;     // idle lanes follow pair 0 (masked)
+    const bool in_b = subc >= na;
+    v.cs = reinterpret_cast<const double*>(st + 16 + (in_b ? S::CB : 0));
+    v.code = reinterpret_cast<const uint32_t*>(st + 16 + 2 * S::CB + (in_b ? kb : 0));
+    v.gt = reinterpret_cast<const int2*>(st + 16 + 2 * S::CB + 2 * kb) +
+           (in_b ? na * ((info >> 16) & 255) + (subc - na) * ((info >> 24) & 255)
+                 : subc * ((info >> 16) & 255));
+    return v;
+  };
+  // issue the gather of X (X layout: x = t, u[z][y]; the lanes of a pair read
+  // consecutive DoFs), branch-free: a column the source does not store in a
+  // group reads offset 0 of the array (valid); `present` masks it later
+  auto gather = [&](const View& v, double (&u)[N][N], unsigned& present) {
+    present = 0;
 #pragma unroll
-    for (int z = 0; z < N; ++z)
+    for (int z = 0; z < N; ++z) {
 #pragma unroll
-      for (int x = 0; x < N; ++x) uqB[z][x] *= COEF ? cs[z * N2 + tt * N + x] : 0.0;
-    rs();
-    contract_slow<N, true>(uqB, v1, tb.S);  // S^T along z
-    contract_fast<N, true>(v1, uqB, tb.S);  // S^T along x
-    b_to_a<N>(uqB, v1, buf, tt, lane_ok);   // A: z = t
-    contract_slow<N, true>(v1, out, tb.S);  // S^T along y
-  } else if (MODE == 2) {
-    const PlaneScatter<N, WIDE> hsc{a.hx, code_s, gt, t, ok};
-    const MassScatter<N, WIDE> msc{PlaneScatter<N, WIDE>{a.mx, code_s, gt, t, ok}, a.mcoef};
-    // the scatter hooks run after the last transpose: wait for the code row first
-    const WaitThen<PlaneScatter<N, WIDE>> hw{hsc, &bar[warp]};
-    sumfac_h_plane<N, COEF, 1, Tile<N>, const double*, MassScatter<N, WIDE>,
-                   WaitThen<PlaneScatter<N, WIDE>>, Restage>(
-        u, out, buf, tt, lane_ok, cs + tt * N2, tb, msc, hw, rs);
-    return;
-  } else {
-    sumfac_h_plane<N, COEF, 1, Tile<N>, const double*, NoMass, NoMass, Restage>(
-        u, out, buf, tt, lane_ok, cs + tt * N2, tb, NoMass(), NoMass(), rs);
-  }
-  mbar_wait(&bar[warp], 1);
-  if (ok) {
-#pragma unroll
-    for (int y = 0; y < N; ++y)
-#pragma unroll
-      for (int x = 0; x < N; ++x) {
-        const Code<WIDE> c = decode<WIDE>(code_s, t * N2 + y * N + x);
-        atomicAdd(a.hx + (int64_t)gt[c.g].y + c.rh, out[y][x]);
+      for (int y = 0; y < N; ++y) {
+        const Code<WIDE> c = decode<WIDE>(v.code, z * N2 + y * N + t);
+        const int xo = v.gt[c.g].x;
+        u[z][y] = __ldg(a.x + (int64_t)max(xo, 0) + c.rx);
+        if (xo >= 0) present |= 1u << (z * N + y);
       }
+    }
+    if (!v.ok) present = 0;
+  };
+
+  // Pipeline per warp: the metadata of batch i + STAGES - 1 is in flight
+  // (TMA), and with PREF the X values of batch i + 1 are in flight (plain
+  // loads into registers) while batch i is contracted.
+  constexpr bool PREF = S::PREF;
+#pragma unroll
+  for (int k = 0; k < NST - 1; ++k)
+    if (b + k * nw < nb) issue(k, b + k * nw);
+  double un[N][N];
+  unsigned pn = 0;
+  if (PREF && b < nb) {
+    mbar_wait(&bar[warp][0], 0u);
+    gather(view(stage0), un, pn);
+  }
+  for (int it = 0; b < nb; ++it, b += nw) {
+    const int s = it % NST;
+    const unsigned char* st = stage0 + s * stage_bytes;
+    double u[N][N];
+    unsigned present;
+    if (PREF) {
+      present = pn;
+#pragma unroll
+      for (int z = 0; z < N; ++z)
+#pragma unroll
+        for (int y = 0; y < N; ++y) u[z][y] = ((present >> (z * N + y)) & 1u) ? un[z][y] : 0.0;
+    } else {
+      mbar_wait(&bar[warp][s], (unsigned)((it / NST) & 1));
+      gather(view(st), u, present);
+#pragma unroll
+      for (int z = 0; z < N; ++z)
+#pragma unroll
+        for (int y = 0; y < N; ++y)
+          if (!((present >> (z * N + y)) & 1u)) u[z][y] = 0.0;
+    }
+    // every lane is past its reads of the stage that held batch it - 1
+    __syncwarp();
+    if (b + (NST - 1) * nw < nb) issue((it + NST - 1) % NST, b + (NST - 1) * nw);
+    if (PREF && b + nw < nb) {
+      const int s1 = (it + 1) % NST;
+      mbar_wait(&bar[warp][s1], (unsigned)(((it + 1) / NST) & 1));
+      gather(view(stage0 + s1 * stage_bytes), un, pn);
+    }
+    const View cur = view(st);
+    const bool ok = cur.ok;
+    const double* cs = cur.cs;
+    const uint32_t* code = cur.code;
+    const int2* gt = cur.gt;
+    double out[N][N];
+    using L3 = Tile3<N>;
+    if (MODE == 1) {
+      // coefficient only: interpolate, scale at the points, back; result in Z layout
+      double v1[N][N], uq[N][N];
+      contract_fast<N, false>(u, v1, tb.S);            // y
+      contract_slow<N, false>(v1, out, tb.S);          // z
+      x_to_y<N, L3>(out, v1, buf, tt, lane_ok);        // Y: qy = t, [qz][x]
+      contract_fast<N, false>(v1, uq, tb.S);           // x
+#pragma unroll
+      for (int z = 0; z < N; ++z)
+#pragma unroll
+        for (int x = 0; x < N; ++x) uq[z][x] *= COEF ? cs[z * N2 + tt * N + x] : 0.0;
+      contract_slow<N, true>(uq, v1, tb.S);            // S^T along z
+      contract_fast<N, true>(v1, uq, tb.S);            // S^T along x
+      y_to_z<N, L3>(uq, v1, buf, tt, lane_ok);         // Z: z = t, [qy][x]
+      contract_slow<N, true>(v1, out, tb.S);           // S^T along y
+      PlaneScatter<N, WIDE, 2>{a.hx, code, gt, t, ok}.template operator()<N, L3>(out, buf, tt,
+                                                                                 lane_ok, tb);
+    } else if (MODE == 2) {
+      const PlaneScatter<N, WIDE, 0> hsc{a.hx, code, gt, t, ok};
+      const MassScatter<N, WIDE> msc{PlaneScatter<N, WIDE, 0>{a.mx, code, gt, t, ok}, a.mcoef};
+      sumfac_h_lean<N, COEF, L3, MassScatter<N, WIDE>, PlaneScatter<N, WIDE, 0>>(
+          u, out, buf, tt, lane_ok, cs, tb, msc, hsc);
+    } else {
+      sumfac_h_lean<N, COEF, L3>(u, out, buf, tt, lane_ok, cs, tb);
+      PlaneScatter<N, WIDE, 0>{a.hx, code, gt, t, ok}.template operator()<N, L3>(out, buf, tt,
+                                                                                 lane_ok, tb);
+    }
   }
 }
 
@@ -388,7 +463,10 @@ struct K1Plan {
   int64_t n_pairs = 0;
   int code_stride = 0;
   int gbytes = 0;
-  int4* desc = nullptr;
+  int4* desc = nullptr;     // pair kernel (n <= 3)
+  Batch* batches = nullptr;  // plane kernel (n >= 4)
+  std::vector<int64_t> break_pair;   // pair indices a launch range may start / end at
+  std::vector<int64_t> break_batch;  // ... and the batch index there
   uint32_t* codes = nullptr;
   int2* gtab = nullptr;
   CellTables tables{};
@@ -397,7 +475,7 @@ struct K1Plan {
 namespace {
 
 template <int N, bool COEF, int MODE, bool WIDE>
-int launch_k1(const K1Plan* p, const K1Args& args, cudaStream_t st) {
+int launch_k1(const K1Plan* p, K1Args& args, int64_t p0, int64_t p1, cudaStream_t st) {
   if constexpr (N <= 3) {
     constexpr int NP = N;
     auto kern = k1_pair_kernel<NP, COEF, MODE, WIDE>;
@@ -405,38 +483,75 @@ int launch_k1(const K1Plan* p, const K1Args& args, cudaStream_t st) {
         16 * (odd_units(p->code_stride * 4) + odd_units(p->gbytes) + K1PairShape<NP>::CU);
     const int smem = kWarps * 32 * lane_bytes;
     BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    args.desc = p->desc + p0;
+    args.n_pairs = p1 - p0;
     const int64_t per = (int64_t)kWarps * 32;
-    kern<<<(unsigned)((p->n_pairs + per - 1) / per), kWarps * 32, smem, st>>>(args, p->tables);
+    kern<<<(unsigned)((p1 - p0 + per - 1) / per), kWarps * 32, smem, st>>>(args, p->tables);
   } else {
     constexpr int NN = N;
+    // the range must start and end at batch boundaries the plan was cut at
+    int64_t b0 = -1, b1 = -1;
+    for (size_t k = 0; k < p->break_pair.size(); ++k) {
+      if (p->break_pair[k] == p0) b0 = p->break_batch[k];
+      if (p->break_pair[k] == p1) b1 = p->break_batch[k];
+    }
+    if (b0 < 0 || b1 < 0) {
+      set_error("K1: pair range [%lld, %lld) does not start / end at a declared break",
+                (long long)p0, (long long)p1);
+      return BMV_ERR_INVALID;
+    }
+    if (b1 == b0) return BMV_OK;
     auto kern = k1_plane_kernel<NN, COEF, MODE, WIDE>;
-    const int smem = kWarps * k1_warp_bytes<NN>(p->gbytes);
+    constexpr int kW = K1Shape<NN>::WARPS;
+    const int smem = kW * k1_warp_bytes<NN>(p->code_stride, p->gbytes);
     BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int64_t per = (int64_t)kWarps * K1Shape<NN>::P;
-    kern<<<(unsigned)((p->n_pairs + per - 1) / per), kWarps * 32, smem, st>>>(args, p->tables);
+    args.b0 = b0;
+    args.b1 = b1;
+    // persistent: the CTAs that fit the GPU at once, fewer if there are fewer batches
+    static int ctas_per_sm[2][3][2][6] = {};
+    int& cps = ctas_per_sm[COEF][MODE][WIDE][N];
+    if (cps == 0) {
+      BMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, kern, kW * 32, smem));
+      if (cps <= 0) {
+        set_error("K1: the plane kernel does not fit an SM (%d bytes of shared memory)", smem);
+        cps = 0;
+        return BMV_ERR_INVALID;
+      }
+    }
+    const int64_t want = (b1 - b0 + kW - 1) / kW;
+    const int64_t grid = std::min<int64_t>(want, (int64_t)cps * sm_count());
+    kern<<<(unsigned)grid, kW * 32, smem, st>>>(args, p->tables);
   }
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
 
 template <int N>
-int dispatch_n(const K1Plan* p, const K1Args& args, bool coef, int mode, cudaStream_t st) {
+int dispatch_n(const K1Plan* p, K1Args& args, bool coef, int mode, int64_t p0, int64_t p1,
+               cudaStream_t st) {
   if (p->wide) {
-    if (mode == 0) return coef ? launch_k1<N, true, 0, true>(p, args, st) : launch_k1<N, false, 0, true>(p, args, st);
-    if (mode == 1) return launch_k1<N, true, 1, true>(p, args, st);
-    return coef ? launch_k1<N, true, 2, true>(p, args, st) : launch_k1<N, false, 2, true>(p, args, st);
+    if (mode == 0)
+      return coef ? launch_k1<N, true, 0, true>(p, args, p0, p1, st)
+                  : launch_k1<N, false, 0, true>(p, args, p0, p1, st);
+    if (mode == 1) return launch_k1<N, true, 1, true>(p, args, p0, p1, st);
+    return coef ? launch_k1<N, true, 2, true>(p, args, p0, p1, st)
+                : launch_k1<N, false, 2, true>(p, args, p0, p1, st);
   }
-  if (mode == 0) return coef ? launch_k1<N, true, 0, false>(p, args, st) : launch_k1<N, false, 0, false>(p, args, st);
-  if (mode == 1) return launch_k1<N, true, 1, false>(p, args, st);
-  return coef ? launch_k1<N, true, 2, false>(p, args, st) : launch_k1<N, false, 2, false>(p, args, st);
+  if (mode == 0)
+    return coef ? launch_k1<N, true, 0, false>(p, args, p0, p1, st)
+                : launch_k1<N, false, 0, false>(p, args, p0, p1, st);
+  if (mode == 1) return launch_k1<N, true, 1, false>(p, args, p0, p1, st);
+  return coef ? launch_k1<N, true, 2, false>(p, args, p0, p1, st)
+              : launch_k1<N, false, 2, false>(p, args, p0, p1, st);
 }
 
-int dispatch(const K1Plan* p, const K1Args& args, bool coef, int mode, cudaStream_t st) {
+int dispatch(const K1Plan* p, K1Args& args, bool coef, int mode, int64_t p0, int64_t p1,
+             cudaStream_t st) {
   switch (p->n) {
-    case 2: return dispatch_n<2>(p, args, coef, mode, st);
-    case 3: return dispatch_n<3>(p, args, coef, mode, st);
-    case 4: return dispatch_n<4>(p, args, coef, mode, st);
-    case 5: return dispatch_n<5>(p, args, coef, mode, st);
+    case 2: return dispatch_n<2>(p, args, coef, mode, p0, p1, st);
+    case 3: return dispatch_n<3>(p, args, coef, mode, p0, p1, st);
+    case 4: return dispatch_n<4>(p, args, coef, mode, p0, p1, st);
+    case 5: return dispatch_n<5>(p, args, coef, mode, p0, p1, st);
     default:
       set_error("K1: unsupported nodes per axis %d", p->n);
       return BMV_ERR_INVALID;
@@ -454,7 +569,8 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
   using namespace bmv;
   *out = nullptr;
   if (!d || d->n < 2 || d->n > BMV_MAX_NODES || d->n_pairs < 0 || d->n_cells < 0 ||
-      d->code_stride <= 0 || (d->code_stride & 3) || d->max_groups < 0 || d->max_groups > 32) {
+      d->code_stride <= 0 || (d->code_stride & 3) || d->max_groups < 0 || d->max_groups > 32 ||
+      d->n_breaks < 0 || d->n_pairs > INT32_MAX) {
     set_error("bmv_cellop_create: invalid descriptor");
     return BMV_ERR_INVALID;
   }
@@ -480,17 +596,76 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
     for (int j = 0; j < n; ++j) tb.W2[i * n + j] = d->w[i] * d->w[j];
   }
   for (int k = 0; k < 3; ++k) tb.kin[k] = d->kin[k];
-  std::vector<int4> desc((size_t)d->n_pairs);
   for (int64_t q = 0; q < d->n_pairs; ++q) {
     const int64_t go = d->pair_gtab[q];
-    if ((go & 3) || d->pair_ngp[q] > d->max_groups || go / 4 > INT32_MAX) {
+    if ((go & 3) || d->pair_ngp[q] > d->max_groups || (d->pair_ngp[q] & 1) || go / 4 > INT32_MAX ||
+        (q + 1 < d->n_pairs && d->pair_gtab[q + 1] != go + 2 * d->pair_ngp[q])) {
       delete p;
       set_error("bmv_cellop_create: bad group table of pair %lld", (long long)q);
       return BMV_ERR_INVALID;
     }
-    desc[(size_t)q] = make_int4(d->pair_cell[q], (int)(go / 2), d->pair_ngp[q], 0);
   }
-  int rc = upload(desc.data(), (int64_t)desc.size(), &p->desc);
+  // launch ranges start / end at 0, n_pairs and the declared breaks
+  p->break_pair.push_back(0);
+  for (int32_t k = 0; k < d->n_breaks; ++k) {
+    const int64_t bp = d->breaks[k];
+    if (bp < p->break_pair.back() || bp > d->n_pairs) {
+      delete p;
+      set_error("bmv_cellop_create: breaks must be ascending pair indices");
+      return BMV_ERR_INVALID;
+    }
+    if (bp > p->break_pair.back()) p->break_pair.push_back(bp);
+  }
+  if (p->break_pair.back() < d->n_pairs) p->break_pair.push_back(d->n_pairs);
+  int rc = BMV_OK;
+  if (n <= 3) {
+    std::vector<int4> desc((size_t)d->n_pairs);
+    for (int64_t q = 0; q < d->n_pairs; ++q)
+      desc[(size_t)q] = make_int4(d->pair_cell[q], (int)(d->pair_gtab[q] / 2), d->pair_ngp[q], 0);
+    rc = upload(desc.data(), (int64_t)desc.size(), &p->desc);
+    p->break_batch = p->break_pair;
+  } else {
+    // batches: up to 32 / n consecutive pairs in at most two cells, never
+    // across a break (greedy; pairs are sorted by cell inside each range)
+    const int P = 32 / n;
+    std::vector<Batch> batches;
+    batches.reserve((size_t)(d->n_pairs / P + 8));
+    size_t bk = 0;
+    p->break_batch.assign(p->break_pair.size(), 0);
+    int64_t q = 0;
+    while (q < d->n_pairs) {
+      while (bk + 1 < p->break_pair.size() && p->break_pair[bk + 1] <= q) ++bk;
+      p->break_batch[bk] = p->break_pair[bk] == q ? (int64_t)batches.size() : p->break_batch[bk];
+      const int64_t lim = bk + 1 < p->break_pair.size() ? p->break_pair[bk + 1] : d->n_pairs;
+      Batch b{};
+      b.first_pair = (int32_t)q;
+      b.cell_a = b.cell_b = d->pair_cell[q];
+      int na = 0, np = 0;
+      const int ga = d->pair_ngp[q];
+      int gb = ga;
+      bool second = false;
+      while (q + np < lim && np < P) {
+        const int32_t cell = d->pair_cell[q + np];
+        if (!second && cell != b.cell_a) {
+          second = true;
+          b.cell_b = cell;
+          gb = d->pair_ngp[q + np];
+        } else if (second && cell != b.cell_b) {
+          break;
+        }
+        if (!second) ++na;
+        ++np;
+      }
+      b.info = na | (np << 8) | (ga << 16) | (gb << 24);
+      b.gt16 = (int32_t)(d->pair_gtab[q] / 4);
+      b.gt_bytes = 8 * (na * ga + (np - na) * gb);
+      batches.push_back(b);
+      q += np;
+    }
+    for (size_t k = 0; k < p->break_pair.size(); ++k)
+      if (p->break_pair[k] == d->n_pairs) p->break_batch[k] = (int64_t)batches.size();
+    rc = upload(batches.data(), (int64_t)batches.size(), &p->batches);
+  }
   if (rc == BMV_OK)
     rc = upload(d->codes, (int64_t)d->n_cells * d->code_stride, &p->codes);
   if (rc == BMV_OK)
@@ -506,6 +681,7 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
 int bmv_cellop_destroy(bmv_cellop* p) {
   if (!p) return BMV_OK;
   bmv::release(p->desc);
+  bmv::release(p->batches);
   bmv::release(p->codes);
   bmv::release(p->gtab);
   delete p;
@@ -530,9 +706,19 @@ int run_pairs(const bmv_cellop* p, int mode, const double* coef, int64_t coef_st
     return BMV_ERR_INVALID;
   }
   if (p1 == p0) return BMV_OK;
-  K1Args args{p->desc + p0, p->codes, p->gtab, p->code_stride, p->gbytes, coef,
-              coef_stride != 0 ? 1 : 0, p1 - p0, x, hx, mx, mcoef};
-  return dispatch(p, args, coef != nullptr, mode, st);
+  K1Args args{};
+  args.codes = p->codes;
+  args.gtab = p->gtab;
+  args.batches = p->batches;
+  args.code_stride = p->code_stride;
+  args.gbytes = p->gbytes;
+  args.coef = coef;
+  args.coef_cell = coef_stride != 0 ? 1 : 0;
+  args.x = x;
+  args.hx = hx;
+  args.mx = mx;
+  args.mcoef = mcoef;
+  return dispatch(p, args, coef != nullptr, mode, p0, p1, st);
 }
 
 }  // namespace

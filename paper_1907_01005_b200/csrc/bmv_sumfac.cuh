@@ -228,6 +228,190 @@ __device__ __forceinline__ void sumfac_h_plane(const double (&u)[N][N], double (
   }
 }
 
+// Three-layout transposes of the plane kernel (bmv_k1.cu).  A pair's n^3
+// tensor U[z][y][x] lives in n threads, thread t holding one plane:
+//   X layout: x = t, a[z][y];  Y layout: y = t, b[z][x];  Z layout: z = t, c[y][x].
+// The pair's shared tile holds element (z, y, x) at z BZ + y BY + x BX;
+// strides from a bank model of the 64-bit accesses of the pair-major lanes
+// (lane = pair * n + t): n = 5 two wavefronts per access for t-strides BY, BZ
+// and three for BX.
+template <int N> struct Tile3;
+template <> struct Tile3<4> { static constexpr int BX = 1, BY = 5, BZ = 19, TILE = 76; };
+#ifndef BMV_T5X
+#define BMV_T5X 1
+#define BMV_T5Y 5
+#define BMV_T5Z 27
+#define BMV_T5T 135
+#endif
+template <> struct Tile3<5> {
+  static constexpr int BX = BMV_T5X, BY = BMV_T5Y, BZ = BMV_T5Z, TILE = BMV_T5T;
+};
+
+template <int N, class L>
+__device__ __forceinline__ void x_to_y(const double (&a)[N][N], double (&b)[N][N], double* buf,
+                                       int t, bool store) {
+  __syncwarp();
+  if (store) {
+#pragma unroll
+    for (int z = 0; z < N; ++z)
+#pragma unroll
+      for (int y = 0; y < N; ++y) buf[z * L::BZ + y * L::BY + t * L::BX] = a[z][y];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int z = 0; z < N; ++z)
+#pragma unroll
+    for (int x = 0; x < N; ++x) b[z][x] = buf[z * L::BZ + t * L::BY + x * L::BX];
+}
+template <int N, class L>
+__device__ __forceinline__ void y_to_z(const double (&b)[N][N], double (&c)[N][N], double* buf,
+                                       int t, bool store) {
+  __syncwarp();
+  if (store) {
+#pragma unroll
+    for (int z = 0; z < N; ++z)
+#pragma unroll
+      for (int x = 0; x < N; ++x) buf[z * L::BZ + t * L::BY + x * L::BX] = b[z][x];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int y = 0; y < N; ++y)
+#pragma unroll
+    for (int x = 0; x < N; ++x) c[y][x] = buf[t * L::BZ + y * L::BY + x * L::BX];
+}
+template <int N, class L>
+__device__ __forceinline__ void z_to_x(const double (&c)[N][N], double (&a)[N][N], double* buf,
+                                       int t, bool store) {
+  __syncwarp();
+  if (store) {
+#pragma unroll
+    for (int y = 0; y < N; ++y)
+#pragma unroll
+      for (int x = 0; x < N; ++x) buf[t * L::BZ + y * L::BY + x * L::BX] = c[y][x];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int z = 0; z < N; ++z)
+#pragma unroll
+    for (int y = 0; y < N; ++y) a[z][y] = buf[z * L::BZ + y * L::BY + t * L::BX];
+}
+
+// H = -1/2 Laplace (+ c(q) u(q)) on one pair (the plane kernel of bmv_k1.cu).
+// In and out: X layout (thread t holds x = t, [z][y]), so that the lanes of
+// a pair gather / scatter CONSECUTIVE DoFs (consecutive slab rows when they
+// lie in one block row).  Same 12 contractions and 4 transposes as
+// sumfac_h_plane, ordered so that at most two planes (+ a column of
+// temporaries) are live: interpolate y, z (X), transpose, x (Y); coefficient
+// term and the x / z gradient terms in Y; transpose the values and the
+// partial result to Z; y gradient term, interpolate back along y, x (Z);
+// transpose, back along z (X).  cf: the cell's coefficient row (q^3 values,
+// point (qz, qy, qx) at qz n^2 + qy n + qx).
+// MASS (optional): called with the values at the quadrature points in Z
+// layout (qz = t, [qy][qx]) after the Hamiltonian result has been handed to
+// HOUT (X layout); it may overwrite them.
+template <int N, bool COEF, class L = Tile3<N>, class MASS = NoMass, class HOUT = NoMass>
+__device__ __forceinline__ void sumfac_h_lean(const double (&u)[N][N], double (&out)[N][N],
+                                              double* buf, int tt, bool lane_ok,
+                                              const double* cf, const CellTables& tb,
+                                              const MASS& mass = MASS(),
+                                              const HOUT& hout = HOUT()) {
+  constexpr int N2 = N * N;
+  double p1[N][N], p2[N][N];
+  contract_fast<N, false>(u, p1, tb.S);    // y
+  contract_slow<N, false>(p1, p2, tb.S);   // z
+  x_to_y<N, L>(p2, p1, buf, tt, lane_ok);  // Y: qy = t, [qz][x]
+  contract_fast<N, false>(p1, p2, tb.S);   // x -> p2 = uq[qz][qx] (Y)
+  const double wt = tb.w[tt];
+  const double fx = wt * tb.kin[0], fz = wt * tb.kin[2];
+  // p1 = coefficient term + x and z gradient terms (Y)
+#pragma unroll
+  for (int z = 0; z < N; ++z) {
+    double g[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(tb.D[q * N + j], p2[z][j], s);
+      g[q] = s * (fx * tb.W2[z * N + q]);
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s = COEF ? cf[z * N2 + tt * N + q] * p2[z][q] : 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(tb.D[j * N + q], g[j], s);
+      p1[z][q] = s;
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < N; ++x) {
+    double g[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(tb.D[q * N + j], p2[j][x], s);
+      g[q] = s * (fz * tb.W2[q * N + x]);
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s = p1[q][x];
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(tb.D[j * N + q], g[j], s);
+      p1[q][x] = s;
+    }
+  }
+  // values and partial result to Z (qz = t, [qy][qx])
+  double p3[N][N];
+  y_to_z<N, L>(p2, p3, buf, tt, lane_ok);  // p3 = uq (Z)
+  y_to_z<N, L>(p1, p2, buf, tt, lane_ok);  // p2 = partial result (Z)
+  const double fy = wt * tb.kin[1];
+#pragma unroll
+  for (int x = 0; x < N; ++x) {
+    double g[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(tb.D[q * N + j], p3[j][x], s);
+      g[q] = s * (fy * tb.W2[q * N + x]);
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s = p2[q][x];
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(tb.D[j * N + q], g[j], s);
+      p2[q][x] = s;
+    }
+  }
+  // back to the nodes: y, x in Z, then z in X
+  contract_slow<N, true>(p2, p1, tb.S);    // S^T along y
+  contract_fast<N, true>(p1, p2, tb.S);    // S^T along x
+  z_to_x<N, L>(p2, p1, buf, tt, lane_ok);  // X: x = t, [qz][y]
+  contract_slow<N, true>(p1, out, tb.S);   // S^T along z -> out[z][y]
+  if (!std::is_same<MASS, NoMass>::value) {
+    hout.template operator()<N, L>(out, buf, tt, lane_ok, tb);
+    mass.template operator()<N, L>(p3, buf, tt, lane_ok, tb);
+  }
+}
+
+// The mass operator on values at the quadrature points in Z layout (qz = t,
+// [qy][qx]): w3 * uq, back to the nodes (S^T along y and x in Z, transpose,
+// z in X); result in X layout (x = t, [z][y]) in m.
+template <int N, class L>
+__device__ __forceinline__ void mass_back_lean(double (&m)[N][N], const double* __restrict__ w3,
+                                               double* buf, int tt, bool lane_ok,
+                                               const CellTables& tb) {
+  double v1[N][N];
+#pragma unroll
+  for (int y = 0; y < N; ++y)
+#pragma unroll
+    for (int x = 0; x < N; ++x) m[y][x] *= __ldg(w3 + tt * N * N + y * N + x);
+  contract_slow<N, true>(m, v1, tb.S);    // S^T along y
+  contract_fast<N, true>(v1, m, tb.S);    // S^T along x
+  z_to_x<N, L>(m, v1, buf, tt, lane_ok);  // X: x = t
+  contract_slow<N, true>(v1, m, tb.S);    // S^T along z
+}
+
 // The mass operator on values at the quadrature points in B layout (qy = t):
 // w3 * uq, back to the nodes (S^T along z and x in B, transpose, y in A);
 // result in A layout (z = t, [y][x]) in m.

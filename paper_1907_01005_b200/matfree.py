@@ -566,6 +566,9 @@ class _CellPlan:
         d.pair_ngp = _lib.ptr(arrs["pair_ngp"], C.c_int32)
         d.gtab = _lib.ptr(arrs["gtab"], C.c_int32)
         d.codes = _lib.ptr(arrs["codes"], C.c_uint32)
+        breaks = np.ascontiguousarray(sorted(set(int(b) for b in self.split)), dtype=np.int64)
+        d.n_breaks = int(breaks.size)
+        d.breaks = _lib.ptr(breaks, C.c_int64)
         sh = op.shape
         dco = collocation_derivative(sh)
         for i in range(n):

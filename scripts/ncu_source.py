@@ -78,7 +78,7 @@ def main():
             tot_ex = sum(e[1] for e in agg.values())
             tot_s = sum(e[2] for e in agg.values())
             if tot_ex:
-                print(f"### {cur_file.split('/')[-1]} :: {r[1][:80]} ({tot_ex} instr)\n")
+                print(f"### {cur_file.split('/')[-1]} :: {r[1][:80]} ({tot_ex} instr, {tot_s} samples)\n")
                 print("| line | % instr | % samples | source |\n|---|---|---|---|")
                 best = sorted(agg.items(), key=lambda kv: -(kv[1][1] + 1e-9 * kv[1][2]))[:top]
                 for ln, e in sorted(best, key=lambda kv: int(kv[0])):

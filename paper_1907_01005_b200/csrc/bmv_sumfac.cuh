@@ -232,16 +232,16 @@ __device__ __forceinline__ void sumfac_h_plane(const double (&u)[N][N], double (
 // tensor U[z][y][x] lives in n threads, thread t holding one plane:
 //   X layout: x = t, a[z][y];  Y layout: y = t, b[z][x];  Z layout: z = t, c[y][x].
 // The pair's shared tile holds element (z, y, x) at z BZ + y BY + x BX;
-// strides from a bank model of the 64-bit accesses of the pair-major lanes
-// (lane = pair * n + t): n = 5 two wavefronts per access for t-strides BY, BZ
-// and three for BX.
+// n = 4: conflict-free strides (two wavefronts per 64-bit access of the
+// pair-major lanes, lane = pair * n + t); n = 5: the best of a measured scan
+// (2.9 wavefronts per access; 30 active lanes in groups of 5 always collide).
 template <int N> struct Tile3;
 template <> struct Tile3<4> { static constexpr int BX = 1, BY = 5, BZ = 19, TILE = 76; };
-#ifndef BMV_T5X
-#define BMV_T5X 1
-#define BMV_T5Y 5
-#define BMV_T5Z 27
-#define BMV_T5T 135
+#ifndef BMV_T5X  // measured with scripts/sumfac_probe.cu over ~160 layouts (profiles/r02_k1_tile_scan.txt)
+#define BMV_T5X 5
+#define BMV_T5Y 9
+#define BMV_T5Z 25
+#define BMV_T5T 157
 #endif
 template <> struct Tile3<5> {
   static constexpr int BX = BMV_T5X, BY = BMV_T5Y, BZ = BMV_T5Z, TILE = BMV_T5T;

@@ -69,7 +69,7 @@ struct __align__(16) Batch {
 };
 
 struct K1Args {
-  const int4* __restrict__ desc;       // pair kernel: {cell, gtab offset (16-byte units), ngp, 0}
+  const struct PairBatch* __restrict__ pair_batches;  // pair kernel (n <= 3)
   const Batch* __restrict__ batches;   // plane kernel
   int64_t b0, b1;                      // batch range of this launch
   const uint32_t* __restrict__ codes;  // code rows, code_stride words per cell
@@ -78,7 +78,6 @@ struct K1Args {
   int gbytes;                          // group-table bytes reserved per pair (16 | it)
   const double* __restrict__ coef;
   int coef_cell;  // 1: row per cell (stride q3p), 0: one row
-  int64_t n_pairs;                     // pair kernel: pairs of this launch
   const double* __restrict__ x;
   double* __restrict__ hx;
   double* __restrict__ mx;             // fused mass output (DUAL), same layout as hx
@@ -359,98 +358,190 @@ __global__ void __launch_bounds__(K1Shape<N>::WARPS * 32) __maxnreg__(K1Shape<N>
 }
 
 // ---------------------------------------------------------------------------
-// One thread per pair (n <= 3).  Per lane: code row, group table and
-// coefficient row at pitches of an odd number of 16-byte units.
+// One thread per pair (n <= 3): the whole n^3 tensor in registers, no
+// transposes.  A warp works on a batch of up to 32 consecutive pairs in at
+// most kPairCells cells; the cells' code and coefficient rows are fetched
+// once per batch (the lanes of a cell read them by broadcast), persistent
+// warps, metadata stages and X prefetch as in the plane kernel.
+constexpr int kPairCells = 8;
+
+struct __align__(16) PairBatch {
+  int32_t first_pair, np, ncells;
+  int32_t gt16;      // first group-table entry of the batch, 16-byte units
+  int32_t gt_bytes;  // bytes of the batch's group tables (multiple of 16)
+  int32_t pad[3];
+  uint8_t slot[32];  // cell slot of every lane
+  struct {
+    int32_t cell;   // cell id
+    int32_t first;  // lane of the cell's first pair
+    int32_t goff;   // group-table entry of that pair, from the batch's first
+    int32_t ngp;    // entries per pair of this cell
+  } c[kPairCells];
+};
+static_assert(sizeof(PairBatch) == 192, "PairBatch layout");
+
 template <int N>
 struct K1PairShape {
   static constexpr int N3 = N * N * N;
   static constexpr int Q3P = (N3 + 1) / 2 * 2;
-  static constexpr int CU = ((Q3P / 2) | 1);  // coefficient pitch (16-byte units)
+  static constexpr int CB = Q3P * 8;             // bytes of a coefficient row
+  // coefficient row pitch: twice an odd number of 8-byte words, so that the
+  // rows of the 8 cells start in 8 different bank pairs (64-bit reads by
+  // lanes in different cells) and stay 16-byte aligned for the bulk copies
+  static constexpr int CP = ((Q3P / 2) % 2 == 1 ? Q3P : Q3P + 2) * 8;
+  static constexpr int WARPS = 8;                // one CTA per SM
+  static constexpr int STAGES = 3;
 };
 
-__host__ __device__ inline int odd_units(int bytes) { return ((bytes + 15) / 16) | 1; }
+template <int N>
+__host__ __device__ constexpr int k1_pair_stage_bytes(int code_stride, int gbytes) {
+  return (192 + kPairCells * K1PairShape<N>::CP + kPairCells * code_stride * 4 + 32 * gbytes + 127) /
+         128 * 128;
+}
 
 template <int N, bool COEF, int MODE, bool WIDE>
-__global__ void __launch_bounds__(kWarps * 32, 3)
+__global__ void __launch_bounds__(K1PairShape<N>::WARPS * 32)
     k1_pair_kernel(const K1Args a, const __grid_constant__ CellTables tb) {
   using PS = K1PairShape<N>;
-  constexpr int N2 = N * N, N3 = N2 * N;
+  constexpr int N2 = N * N, N3 = N2 * N, NST = PS::STAGES, kW = PS::WARPS;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[kWarps];
+  __shared__ __align__(8) uint64_t bar[kW][NST];
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
-  const int64_t pair = ((int64_t)blockIdx.x * kWarps + warp) * 32 + lid;
-  const bool ok = pair < a.n_pairs;
-  const int ou = odd_units(a.code_stride * 4), gu = odd_units(a.gbytes);
-  const int lane_bytes = 16 * (ou + gu + PS::CU);
-  unsigned char* wbase = smem + warp * 32 * lane_bytes;
-  const uint32_t* crow = reinterpret_cast<const uint32_t*>(wbase + lid * 16 * ou);
-  const int2* gt = reinterpret_cast<const int2*>(wbase + 32 * 16 * ou + lid * 16 * gu);
-  const double* cf = reinterpret_cast<const double*>(wbase + 32 * 16 * (ou + gu) +
-                                                     lid * 16 * PS::CU);
-  if (lid == 0) mbar_init(&bar[warp], 1);
-  __syncwarp();
-  int4 d = make_int4(0, 0, 0, 0);
-  if (ok) d = __ldg(a.desc + pair);
-  const int cell = d.x;
-  const unsigned cbytes = COEF ? PS::Q3P * 8u : 0u;
-  const unsigned kbytes = (unsigned)a.code_stride * 4u;
-  const unsigned gb = (unsigned)d.z * 8u;
-  const unsigned total = __reduce_add_sync(~0u, ok ? cbytes + kbytes + gb : 0u);
-  if (lid == 0) mbar_expect_tx(&bar[warp], total);
-  __syncwarp();
-  if (ok) {
-    if (COEF)
-      bulk_g2s(const_cast<double*>(cf), a.coef + (a.coef_cell ? (int64_t)cell * PS::Q3P : 0),
-               cbytes, &bar[warp]);
-    bulk_g2s(const_cast<uint32_t*>(crow), a.codes + (int64_t)cell * a.code_stride, kbytes,
-             &bar[warp]);
-    if (gb) bulk_g2s(const_cast<int2*>(gt), a.gtab + (int64_t)d.y, gb, &bar[warp]);
-  }
-  mbar_wait(&bar[warp], 0);
-  double v[N][N][N];
+  const int kb = a.code_stride * 4;
+  const int stage_bytes = k1_pair_stage_bytes<N>(a.code_stride, a.gbytes);
+  unsigned char* stage0 = smem + warp * NST * stage_bytes;
+  const int off_coef = 192, off_code = off_coef + kPairCells * PS::CP,
+            off_gt = off_code + kPairCells * kb;
+  if (lid == 0) {
 #pragma unroll
-  for (int k = 0; k < N3; ++k) {
-    double xv = 0.0;
-    if (ok) {
-      const Code<WIDE> c = decode<WIDE>(crow, k);
-      const int xo = gt[c.g].x;
-      if (xo >= 0) xv = __ldg(a.x + (int64_t)xo + c.rx);
+    for (int s = 0; s < NST; ++s) mbar_init(&bar[warp][s], 1);
+  }
+  __syncwarp();
+  const int nw = (int)gridDim.x * kW;
+  const int nb = (int)(a.b1 - a.b0);
+  int b = (int)blockIdx.x * kW + warp;
+
+  // fetch the metadata of batch bb into stage s: the lanes copy the
+  // descriptor (192 bytes) into the stage header, lane c < ncells issues the
+  // rows of cell c, lane 0 the group tables (one mbarrier phase)
+  auto issue = [&](int s, int bb) {
+    const PairBatch* d = a.pair_batches + a.b0 + bb;
+    unsigned char* st = stage0 + s * stage_bytes;
+    const int4 hdr = __ldg(reinterpret_cast<const int4*>(d));            // first_pair np ncells gt16
+    const int gt_bytes = __ldg(reinterpret_cast<const int*>(d) + 4);
+    int4 rec = make_int4(0, 0, 0, 0);
+    if (lid < 12) {
+      const int4 w = __ldg(reinterpret_cast<const int4*>(d) + lid);
+      reinterpret_cast<int4*>(st)[lid] = w;
+      if (lid >= 4) rec = w;
     }
-    v[k / N2][(k / N) % N][k % N] = xv;
-  }
-  // values at the Gauss points
-  contract3<N, 0, false>(v, tb.S);
-  contract3<N, 1, false>(v, tb.S);
-  contract3<N, 2, false>(v, tb.S);
-  double acc[N][N][N];
-  double mac[N][N][N];
-#pragma unroll
-  for (int k = 0; k < N3; ++k) {
-    const double c = COEF ? cf[k] : 0.0;
-    acc[k / N2][(k / N) % N][k % N] = c * v[k / N2][(k / N) % N][k % N];
-    if (MODE == 2) mac[k / N2][(k / N) % N][k % N] = __ldg(a.mcoef + k) * v[k / N2][(k / N) % N][k % N];
-  }
-  if (MODE != 1) {
-    grad3<N, 0>(v, acc, tb);
-    grad3<N, 1>(v, acc, tb);
-    grad3<N, 2>(v, acc, tb);
-  }
-  // back to the nodes
-  contract3<N, 0, true>(acc, tb.S);
-  contract3<N, 1, true>(acc, tb.S);
-  contract3<N, 2, true>(acc, tb.S);
-  if (MODE == 2) {
-    contract3<N, 0, true>(mac, tb.S);
-    contract3<N, 1, true>(mac, tb.S);
-    contract3<N, 2, true>(mac, tb.S);
-  }
-  if (ok) {
+    const int ncells = hdr.z;
+    proxy_fence();  // the stage was read (generic proxy) by an earlier batch
+    if (lid == 0) {
+      unsigned total = (unsigned)ncells * (unsigned)kb + (unsigned)gt_bytes;
+      if (COEF) total += (unsigned)ncells * (unsigned)PS::CB;
+      mbar_expect_tx(&bar[warp][s], total);
+    }
+    __syncwarp();
+    if (lid >= 4 && lid - 4 < ncells) {
+      const int c = lid - 4;
+      if (COEF)
+        bulk_g2s(st + off_coef + c * PS::CP, a.coef + (a.coef_cell ? (int64_t)rec.x * PS::Q3P : 0),
+                 PS::CB, &bar[warp][s]);
+      bulk_g2s(st + off_code + c * kb, a.codes + (int64_t)rec.x * a.code_stride, kb,
+               &bar[warp][s]);
+    }
+    if (lid == 0 && gt_bytes)
+      bulk_g2s(st + off_gt, reinterpret_cast<const char*>(a.gtab) + (int64_t)hdr.w * 16,
+               (unsigned)gt_bytes, &bar[warp][s]);
+  };
+  struct View {
+    bool ok;
+    const double* cf;
+    const uint32_t* code;
+    const int2* gt;
+  };
+  auto view = [&](const unsigned char* st) {
+    const PairBatch* d = reinterpret_cast<const PairBatch*>(st);
+    View v;
+    v.ok = lid < d->np;
+    const int l = v.ok ? lid : 0;  // idle lanes follow pair 0 (masked)
+    const int c = d->slot[l];
+    v.cf = reinterpret_cast<const double*>(st + off_coef + c * PS::CP);
+    v.code = reinterpret_cast<const uint32_t*>(st + off_code + c * kb);
+    v.gt = reinterpret_cast<const int2*>(st + off_gt) + d->c[c].goff + (l - d->c[c].first) * d->c[c].ngp;
+    return v;
+  };
+  auto gather = [&](const View& v, double (&u)[N3], unsigned& present) {
+    present = 0;
 #pragma unroll
     for (int k = 0; k < N3; ++k) {
-      const Code<WIDE> c = decode<WIDE>(crow, k);
-      const int64_t o = (int64_t)gt[c.g].y + c.rh;
-      atomicAdd(a.hx + o, acc[k / N2][(k / N) % N][k % N]);
-      if (MODE == 2) atomicAdd(a.mx + o, mac[k / N2][(k / N) % N][k % N]);
+      const Code<WIDE> c = decode<WIDE>(v.code, k);
+      const int xo = v.gt[c.g].x;
+      u[k] = __ldg(a.x + (int64_t)max(xo, 0) + c.rx);
+      if (xo >= 0) present |= 1u << k;
+    }
+    if (!v.ok) present = 0;
+  };
+
+#pragma unroll
+  for (int k = 0; k < NST - 1; ++k)
+    if (b + k * nw < nb) issue(k, b + k * nw);
+  double un[N3];
+  unsigned pn = 0;
+  if (b < nb) {
+    mbar_wait(&bar[warp][0], 0u);
+    gather(view(stage0), un, pn);
+  }
+  for (int it = 0; b < nb; ++it, b += nw) {
+    const int s = it % NST;
+    const unsigned char* st = stage0 + s * stage_bytes;
+    double v[N][N][N];
+#pragma unroll
+    for (int k = 0; k < N3; ++k) v[k / N2][(k / N) % N][k % N] = ((pn >> k) & 1u) ? un[k] : 0.0;
+    __syncwarp();  // every lane is past its reads of the stage that held batch it - 1
+    if (b + (NST - 1) * nw < nb) issue((it + NST - 1) % NST, b + (NST - 1) * nw);
+    if (b + nw < nb) {
+      const int s1 = (it + 1) % NST;
+      mbar_wait(&bar[warp][s1], (unsigned)(((it + 1) / NST) & 1));
+      gather(view(stage0 + s1 * stage_bytes), un, pn);
+    }
+    const View cur = view(st);
+    // values at the Gauss points
+    contract3<N, 0, false>(v, tb.S);
+    contract3<N, 1, false>(v, tb.S);
+    contract3<N, 2, false>(v, tb.S);
+    double acc[N][N][N];
+    double mac[N][N][N];
+#pragma unroll
+    for (int k = 0; k < N3; ++k) {
+      const double c = COEF ? cur.cf[k] : 0.0;
+      acc[k / N2][(k / N) % N][k % N] = c * v[k / N2][(k / N) % N][k % N];
+      if (MODE == 2)
+        mac[k / N2][(k / N) % N][k % N] = __ldg(a.mcoef + k) * v[k / N2][(k / N) % N][k % N];
+    }
+    if (MODE != 1) {
+      grad3<N, 0>(v, acc, tb);
+      grad3<N, 1>(v, acc, tb);
+      grad3<N, 2>(v, acc, tb);
+    }
+    // back to the nodes
+    contract3<N, 0, true>(acc, tb.S);
+    contract3<N, 1, true>(acc, tb.S);
+    contract3<N, 2, true>(acc, tb.S);
+    if (MODE == 2) {
+      contract3<N, 0, true>(mac, tb.S);
+      contract3<N, 1, true>(mac, tb.S);
+      contract3<N, 2, true>(mac, tb.S);
+    }
+    if (cur.ok) {
+#pragma unroll
+      for (int k = 0; k < N3; ++k) {
+        const Code<WIDE> c = decode<WIDE>(cur.code, k);
+        const int64_t o = (int64_t)cur.gt[c.g].y + c.rh;
+        atomicAdd(a.hx + o, acc[k / N2][(k / N) % N][k % N]);
+        if (MODE == 2) atomicAdd(a.mx + o, mac[k / N2][(k / N) % N][k % N]);
+      }
     }
   }
 }
@@ -463,7 +554,7 @@ struct K1Plan {
   int64_t n_pairs = 0;
   int code_stride = 0;
   int gbytes = 0;
-  int4* desc = nullptr;     // pair kernel (n <= 3)
+  PairBatch* pair_batches = nullptr;  // pair kernel (n <= 3)
   Batch* batches = nullptr;  // plane kernel (n >= 4)
   std::vector<int64_t> break_pair;   // pair indices a launch range may start / end at
   std::vector<int64_t> break_batch;  // ... and the batch index there
@@ -476,37 +567,35 @@ namespace {
 
 template <int N, bool COEF, int MODE, bool WIDE>
 int launch_k1(const K1Plan* p, K1Args& args, int64_t p0, int64_t p1, cudaStream_t st) {
+  // the range must start and end at batch boundaries the plan was cut at
+  int64_t b0 = -1, b1 = -1;
+  for (size_t k = 0; k < p->break_pair.size(); ++k) {
+    if (p->break_pair[k] == p0) b0 = p->break_batch[k];
+    if (p->break_pair[k] == p1) b1 = p->break_batch[k];
+  }
+  if (b0 < 0 || b1 < 0) {
+    set_error("K1: pair range [%lld, %lld) does not start / end at a declared break",
+              (long long)p0, (long long)p1);
+    return BMV_ERR_INVALID;
+  }
+  if (b1 == b0) return BMV_OK;
+  args.b0 = b0;
+  args.b1 = b1;
   if constexpr (N <= 3) {
     constexpr int NP = N;
     auto kern = k1_pair_kernel<NP, COEF, MODE, WIDE>;
-    const int lane_bytes =
-        16 * (odd_units(p->code_stride * 4) + odd_units(p->gbytes) + K1PairShape<NP>::CU);
-    const int smem = kWarps * 32 * lane_bytes;
+    constexpr int kW = K1PairShape<NP>::WARPS;
+    const int smem = kW * K1PairShape<NP>::STAGES * k1_pair_stage_bytes<NP>(p->code_stride, p->gbytes);
     BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    args.desc = p->desc + p0;
-    args.n_pairs = p1 - p0;
-    const int64_t per = (int64_t)kWarps * 32;
-    kern<<<(unsigned)((p1 - p0 + per - 1) / per), kWarps * 32, smem, st>>>(args, p->tables);
+    const int64_t want = (b1 - b0 + kW - 1) / kW;
+    const int64_t grid = std::min<int64_t>(want, (int64_t)sm_count());
+    kern<<<(unsigned)grid, kW * 32, smem, st>>>(args, p->tables);
   } else {
     constexpr int NN = N;
-    // the range must start and end at batch boundaries the plan was cut at
-    int64_t b0 = -1, b1 = -1;
-    for (size_t k = 0; k < p->break_pair.size(); ++k) {
-      if (p->break_pair[k] == p0) b0 = p->break_batch[k];
-      if (p->break_pair[k] == p1) b1 = p->break_batch[k];
-    }
-    if (b0 < 0 || b1 < 0) {
-      set_error("K1: pair range [%lld, %lld) does not start / end at a declared break",
-                (long long)p0, (long long)p1);
-      return BMV_ERR_INVALID;
-    }
-    if (b1 == b0) return BMV_OK;
     auto kern = k1_plane_kernel<NN, COEF, MODE, WIDE>;
     constexpr int kW = K1Shape<NN>::WARPS;
     const int smem = kW * k1_warp_bytes<NN>(p->code_stride, p->gbytes);
     BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    args.b0 = b0;
-    args.b1 = b1;
     // persistent: the CTAs that fit the GPU at once, fewer if there are fewer batches
     static int ctas_per_sm[2][3][2][6] = {};
     int& cps = ctas_per_sm[COEF][MODE][WIDE][N];
@@ -619,11 +708,44 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
   if (p->break_pair.back() < d->n_pairs) p->break_pair.push_back(d->n_pairs);
   int rc = BMV_OK;
   if (n <= 3) {
-    std::vector<int4> desc((size_t)d->n_pairs);
-    for (int64_t q = 0; q < d->n_pairs; ++q)
-      desc[(size_t)q] = make_int4(d->pair_cell[q], (int)(d->pair_gtab[q] / 2), d->pair_ngp[q], 0);
-    rc = upload(desc.data(), (int64_t)desc.size(), &p->desc);
-    p->break_batch = p->break_pair;
+    // batches: up to 32 consecutive pairs in at most kPairCells cells, never
+    // across a break (greedy; pairs are sorted by cell inside each range)
+    std::vector<PairBatch> batches;
+    batches.reserve((size_t)(d->n_pairs / 32 + 8));
+    size_t bk = 0;
+    p->break_batch.assign(p->break_pair.size(), 0);
+    int64_t q = 0;
+    while (q < d->n_pairs) {
+      while (bk + 1 < p->break_pair.size() && p->break_pair[bk + 1] <= q) ++bk;
+      if (p->break_pair[bk] == q) p->break_batch[bk] = (int64_t)batches.size();
+      const int64_t lim = bk + 1 < p->break_pair.size() ? p->break_pair[bk + 1] : d->n_pairs;
+      PairBatch b{};
+      b.first_pair = (int32_t)q;
+      b.gt16 = (int32_t)(d->pair_gtab[q] / 4);
+      int np = 0, nc = 0, entries = 0;
+      while (q + np < lim && np < 32) {
+        const int32_t cell = d->pair_cell[q + np];
+        if (nc == 0 || cell != b.c[nc - 1].cell) {
+          if (nc == kPairCells) break;
+          b.c[nc].cell = cell;
+          b.c[nc].first = np;
+          b.c[nc].goff = entries;
+          b.c[nc].ngp = d->pair_ngp[q + np];
+          ++nc;
+        }
+        b.slot[np] = (uint8_t)(nc - 1);
+        entries += d->pair_ngp[q + np];
+        ++np;
+      }
+      b.np = np;
+      b.ncells = nc;
+      b.gt_bytes = 8 * entries;
+      batches.push_back(b);
+      q += np;
+    }
+    for (size_t k = 0; k < p->break_pair.size(); ++k)
+      if (p->break_pair[k] == d->n_pairs) p->break_batch[k] = (int64_t)batches.size();
+    rc = upload(batches.data(), (int64_t)batches.size(), &p->pair_batches);
   } else {
     // batches: up to 32 / n consecutive pairs in at most two cells, never
     // across a break (greedy; pairs are sorted by cell inside each range)
@@ -680,7 +802,7 @@ int bmv_cellop_create(const bmv_cellop_desc* d, bmv_cellop** out) {
 
 int bmv_cellop_destroy(bmv_cellop* p) {
   if (!p) return BMV_OK;
-  bmv::release(p->desc);
+  bmv::release(p->pair_batches);
   bmv::release(p->batches);
   bmv::release(p->codes);
   bmv::release(p->gtab);
@@ -710,6 +832,7 @@ int run_pairs(const bmv_cellop* p, int mode, const double* coef, int64_t coef_st
   args.codes = p->codes;
   args.gtab = p->gtab;
   args.batches = p->batches;
+  args.pair_batches = p->pair_batches;
   args.code_stride = p->code_stride;
   args.gbytes = p->gbytes;
   args.coef = coef;

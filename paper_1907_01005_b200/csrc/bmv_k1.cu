@@ -389,8 +389,14 @@ struct K1PairShape {
   // rows of the 8 cells start in 8 different bank pairs (64-bit reads by
   // lanes in different cells) and stay 16-byte aligned for the bulk copies
   static constexpr int CP = ((Q3P / 2) % 2 == 1 ? Q3P : Q3P + 2) * 8;
-  static constexpr int WARPS = 8;                // one CTA per SM
-  static constexpr int STAGES = 3;
+#ifndef BMV_K1_PAIR_WARPS
+#define BMV_K1_PAIR_WARPS 8
+#endif
+  static constexpr int WARPS = BMV_K1_PAIR_WARPS;  // one CTA per SM
+  // prefetch the next batch's X values into registers (2 warps per
+  // sub-partition leave the registers for it)
+  static constexpr bool PREF = WARPS <= 8;
+  static constexpr int STAGES = PREF ? 3 : 2;
 };
 
 template <int N>
@@ -424,17 +430,35 @@ __global__ void __launch_bounds__(K1PairShape<N>::WARPS * 32)
   // fetch the metadata of batch bb into stage s: the lanes copy the
   // descriptor (192 bytes) into the stage header, lane c < ncells issues the
   // rows of cell c, lane 0 the group tables (one mbarrier phase)
+  // the descriptor of the batch to issue next is fetched one batch ahead
+  // into a per-warp slot (TMA, own mbarrier): nothing waits on global memory
+  __shared__ __align__(16) unsigned char dslot[kW][192];
+  __shared__ __align__(8) uint64_t dbar[kW];
+  int dphase = 0;
+  if (lid == 0) mbar_init(&dbar[warp], 1);
+  __syncwarp();
+  auto fetch_desc = [&](int bb) {
+    if (lid == 0 && bb < nb) {
+      proxy_fence();
+      mbar_expect_tx(&dbar[warp], 192u);
+      bulk_g2s(dslot[warp], a.pair_batches + a.b0 + bb, 192u, &dbar[warp]);
+    }
+  };
   auto issue = [&](int s, int bb) {
-    const PairBatch* d = a.pair_batches + a.b0 + bb;
     unsigned char* st = stage0 + s * stage_bytes;
-    const int4 hdr = __ldg(reinterpret_cast<const int4*>(d));            // first_pair np ncells gt16
-    const int gt_bytes = __ldg(reinterpret_cast<const int*>(d) + 4);
+    mbar_wait(&dbar[warp], (unsigned)(dphase & 1));
+    ++dphase;
+    const int4* d = reinterpret_cast<const int4*>(dslot[warp]);
+    const int4 hdr = d[0];            // first_pair np ncells gt16
+    const int gt_bytes = reinterpret_cast<const int*>(d)[4];
     int4 rec = make_int4(0, 0, 0, 0);
     if (lid < 12) {
-      const int4 w = __ldg(reinterpret_cast<const int4*>(d) + lid);
+      const int4 w = d[lid];
       reinterpret_cast<int4*>(st)[lid] = w;
       if (lid >= 4) rec = w;
     }
+    __syncwarp();
+    fetch_desc(bb + nw);  // the next batch this warp will issue
     const int ncells = hdr.z;
     proxy_fence();  // the stage was read (generic proxy) by an earlier batch
     if (lid == 0) {
@@ -484,24 +508,30 @@ __global__ void __launch_bounds__(K1PairShape<N>::WARPS * 32)
     if (!v.ok) present = 0;
   };
 
+  fetch_desc(b);
 #pragma unroll
   for (int k = 0; k < NST - 1; ++k)
     if (b + k * nw < nb) issue(k, b + k * nw);
+  constexpr bool PREF = PS::PREF;
   double un[N3];
   unsigned pn = 0;
-  if (b < nb) {
+  if (PREF && b < nb) {
     mbar_wait(&bar[warp][0], 0u);
     gather(view(stage0), un, pn);
   }
   for (int it = 0; b < nb; ++it, b += nw) {
     const int s = it % NST;
     const unsigned char* st = stage0 + s * stage_bytes;
+    if (!PREF) {
+      mbar_wait(&bar[warp][s], (unsigned)((it / NST) & 1));
+      gather(view(st), un, pn);
+    }
     double v[N][N][N];
 #pragma unroll
     for (int k = 0; k < N3; ++k) v[k / N2][(k / N) % N][k % N] = ((pn >> k) & 1u) ? un[k] : 0.0;
     __syncwarp();  // every lane is past its reads of the stage that held batch it - 1
     if (b + (NST - 1) * nw < nb) issue((it + NST - 1) % NST, b + (NST - 1) * nw);
-    if (b + nw < nb) {
+    if (PREF && b + nw < nb) {
       const int s1 = (it + 1) % NST;
       mbar_wait(&bar[warp][s1], (unsigned)(((it + 1) / NST) & 1));
       gather(view(stage0 + s1 * stage_bytes), un, pn);

@@ -406,7 +406,7 @@ def main():
     if not args.no_e2e:
         # inputs arrive from pinned host memory in the compact support format
         # (BlockCsrMatrix.upload_support_values: only the structural nonzeros
-        # of X cross PCIe, then a device scatter into the padded blocks); the
+        # of X cross PCIe, then a device scatter into the slabs); the
         # step's result S comes back to pinned host memory.  Triple-buffered:
         # the H2D copies of the next steps' X run on a copy stream while step
         # k computes on X buffer k % NB (every step's copy stays inside the
@@ -485,8 +485,9 @@ def main():
             "kernels_ms": {"k1_cellop": round(ms_k1, 4), "apply_total": round(ms_apply, 4),
                            "tmmult": round(ms_tm, 4), "mmult": round(ms_mm, 4)},
             "work": {k: (int(sum_over_ranks(v)) if isinstance(v, int) else v) for k, v in cnt.items()},
-            "roofline": {"bound": "fp64", "kernel": "K1 cellop (csrc/bmv_k1.cu, k1_plane_kernel<%d>)"
-                         % (prob.cfg.degree + 1),
+            "roofline": {"bound": "fp64", "kernel": "K1 cellop (csrc/bmv_k1.cu, %s<%d>)"
+                         % ("k1_plane_kernel" if prob.cfg.degree >= 3 else "k1_pair_kernel",
+                            prob.cfg.degree + 1),
                          "achieved": round(k1_tflops, 3), "peak": round(peak_fp64, 3),
                          "unit": "TFLOP/s", "frac": round(k1_tflops / peak_fp64, 4),
                          "frac_vs_dfma": round(k1_tflops / peak_dfma, 4),

@@ -188,9 +188,14 @@ __global__ void __launch_bounds__(K1Shape<N>::WARPS * 32) __maxnreg__(K1Shape<N>
   constexpr int NST = S::STAGES;
   __shared__ __align__(8) uint64_t bar[kWarps][NST];
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
-  const int sub = lid / N;
-  const int t = lid - sub * N;
-  const bool lane_ok = sub < P;
+  // lane -> (pair, plane): the pairs of a batch are split over the two
+  // half-warps (n = 5: pairs 0-2 in lanes 0-14, 3-5 in lanes 16-30, lanes 15
+  // and 31 idle), which makes the transposes bank-conflict free (Tile3)
+  constexpr int PH = P / 2;
+  const int hl = lid & 15;
+  const int sub = (lid >> 4) * PH + hl / N;
+  const int t = hl % N;
+  const bool lane_ok = hl < PH * N;
   const int tt = lane_ok ? t : 0;
 
   const int kb = a.code_stride * 4;  // bytes of a code row
@@ -332,7 +337,7 @@ __global__ void __launch_bounds__(K1Shape<N>::WARPS * 32) __maxnreg__(K1Shape<N>
       double v1[N][N], uq[N][N];
       contract_fast<N, false>(u, v1, tb.S);            // y
       contract_slow<N, false>(v1, out, tb.S);          // z
-      x_to_y<N, L3>(out, v1, buf, tt, lane_ok);        // Y: qy = t, [qz][x]
+      x_to_y<N, typename L3::XY>(out, v1, buf, tt, lane_ok);  // Y: qy = t, [qz][x]
       contract_fast<N, false>(v1, uq, tb.S);           // x
 #pragma unroll
       for (int z = 0; z < N; ++z)
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(K1Shape<N>::WARPS * 32) __maxnreg__(K1Shape<N>
         for (int x = 0; x < N; ++x) uq[z][x] *= COEF ? cs[z * N2 + tt * N + x] : 0.0;
       contract_slow<N, true>(uq, v1, tb.S);            // S^T along z
       contract_fast<N, true>(v1, uq, tb.S);            // S^T along x
-      y_to_z<N, L3>(uq, v1, buf, tt, lane_ok);         // Z: z = t, [qy][x]
+      y_to_z<N, typename L3::YZ>(uq, v1, buf, tt, lane_ok);   // Z: z = t, [qy][x]
       contract_slow<N, true>(v1, out, tb.S);           // S^T along y
       PlaneScatter<N, WIDE, 2>{a.hx, code, gt, t, ok}.template operator()<N, L3>(out, buf, tt,
                                                                                  lane_ok, tb);

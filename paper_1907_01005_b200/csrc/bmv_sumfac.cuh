@@ -231,20 +231,32 @@ __device__ __forceinline__ void sumfac_h_plane(const double (&u)[N][N], double (
 // Three-layout transposes of the plane kernel (bmv_k1.cu).  A pair's n^3
 // tensor U[z][y][x] lives in n threads, thread t holding one plane:
 //   X layout: x = t, a[z][y];  Y layout: y = t, b[z][x];  Z layout: z = t, c[y][x].
-// The pair's shared tile holds element (z, y, x) at z BZ + y BY + x BX;
-// n = 4: conflict-free strides (two wavefronts per 64-bit access of the
-// pair-major lanes, lane = pair * n + t); n = 5: the best of a measured scan
-// (2.9 wavefronts per access; 30 active lanes in groups of 5 always collide).
+// A transpose goes through the pair's shared tile, element (z, y, x) at
+// z BZ + y BY + x BX, pairs TILE apart.  Shared memory serves a 64-bit warp
+// access in two half-warp wavefronts when the 16 lanes of each half hit 16
+// different bank pairs (a model fitted to a measured scan of ~160 layouts,
+// profiles/r02_k1_tile_scan.txt: correlation 0.99).  Each transpose uses its
+// OWN strides -- only the two axes that are thread indices on either side
+// need conflict-free strides, the third gets stride 1:
+//   n = 5 (lanes: pairs 0-2 in lanes 0-14, pairs 3-5 in lanes 16-30, see
+//   k1_plane_kernel): TILE = 135 with t-strides 5 and 27 is conflict-free;
+//   n = 4 (8 pairs x 4 lanes): TILE = 76, strides 1, 5, 19 for all three.
+template <int SX, int SY, int SZ, int T>
+struct TileMap {
+  static constexpr int BX = SX, BY = SY, BZ = SZ, TILE = T;
+};
 template <int N> struct Tile3;
-template <> struct Tile3<4> { static constexpr int BX = 1, BY = 5, BZ = 19, TILE = 76; };
-#ifndef BMV_T5X  // measured with scripts/sumfac_probe.cu over ~160 layouts (profiles/r02_k1_tile_scan.txt)
-#define BMV_T5X 5
-#define BMV_T5Y 9
-#define BMV_T5Z 25
-#define BMV_T5T 157
-#endif
+template <> struct Tile3<4> {
+  static constexpr int TILE = 76;
+  using XY = TileMap<1, 5, 19, 76>;
+  using YZ = XY;
+  using ZX = XY;
+};
 template <> struct Tile3<5> {
-  static constexpr int BX = BMV_T5X, BY = BMV_T5Y, BZ = BMV_T5Z, TILE = BMV_T5T;
+  static constexpr int TILE = 135;
+  using XY = TileMap<5, 27, 1, 135>;   // x_to_y: thread axes x (store), y (load)
+  using YZ = TileMap<1, 5, 27, 135>;   // y_to_z: y, z
+  using ZX = TileMap<27, 1, 5, 135>;   // z_to_x: z, x
 };
 
 template <int N, class L>
@@ -319,7 +331,7 @@ __device__ __forceinline__ void sumfac_h_lean(const double (&u)[N][N], double (&
   double p1[N][N], p2[N][N];
   contract_fast<N, false>(u, p1, tb.S);    // y
   contract_slow<N, false>(p1, p2, tb.S);   // z
-  x_to_y<N, L>(p2, p1, buf, tt, lane_ok);  // Y: qy = t, [qz][x]
+  x_to_y<N, typename L::XY>(p2, p1, buf, tt, lane_ok);  // Y: qy = t, [qz][x]
   contract_fast<N, false>(p1, p2, tb.S);   // x -> p2 = uq[qz][qx] (Y)
   const double wt = tb.w[tt];
   const double fx = wt * tb.kin[0], fz = wt * tb.kin[2];
@@ -362,8 +374,8 @@ __device__ __forceinline__ void sumfac_h_lean(const double (&u)[N][N], double (&
   }
   // values and partial result to Z (qz = t, [qy][qx])
   double p3[N][N];
-  y_to_z<N, L>(p2, p3, buf, tt, lane_ok);  // p3 = uq (Z)
-  y_to_z<N, L>(p1, p2, buf, tt, lane_ok);  // p2 = partial result (Z)
+  y_to_z<N, typename L::YZ>(p2, p3, buf, tt, lane_ok);  // p3 = uq (Z)
+  y_to_z<N, typename L::YZ>(p1, p2, buf, tt, lane_ok);  // p2 = partial result (Z)
   const double fy = wt * tb.kin[1];
 #pragma unroll
   for (int x = 0; x < N; ++x) {
@@ -386,7 +398,7 @@ __device__ __forceinline__ void sumfac_h_lean(const double (&u)[N][N], double (&
   // back to the nodes: y, x in Z, then z in X
   contract_slow<N, true>(p2, p1, tb.S);    // S^T along y
   contract_fast<N, true>(p1, p2, tb.S);    // S^T along x
-  z_to_x<N, L>(p2, p1, buf, tt, lane_ok);  // X: x = t, [qz][y]
+  z_to_x<N, typename L::ZX>(p2, p1, buf, tt, lane_ok);  // X: x = t, [qz][y]
   contract_slow<N, true>(p1, out, tb.S);   // S^T along z -> out[z][y]
   if (!std::is_same<MASS, NoMass>::value) {
     hout.template operator()<N, L>(out, buf, tt, lane_ok, tb);
@@ -408,7 +420,7 @@ __device__ __forceinline__ void mass_back_lean(double (&m)[N][N], const double* 
     for (int x = 0; x < N; ++x) m[y][x] *= __ldg(w3 + tt * N * N + y * N + x);
   contract_slow<N, true>(m, v1, tb.S);    // S^T along y
   contract_fast<N, true>(v1, m, tb.S);    // S^T along x
-  z_to_x<N, L>(m, v1, buf, tt, lane_ok);  // X: x = t
+  z_to_x<N, typename L::ZX>(m, v1, buf, tt, lane_ok);  // X: x = t
   contract_slow<N, true>(v1, m, tb.S);    // S^T along z
 }
 

@@ -15,8 +15,9 @@ __global__ void __launch_bounds__(384) __maxnreg__(REGS)
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int P = 32 / N, TILE = Tile3<N>::TILE;
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
-  const int sub = lid / N, t = lid - sub * N;
-  const bool lane_ok = sub < P;
+  const int hl = lid & 15;
+  const int sub = (lid >> 4) * (P / 2) + hl / N, t = hl % N;
+  const bool lane_ok = hl < (P / 2) * N;
   const int tt = lane_ok ? t : 0;
   double* wbase = reinterpret_cast<double*>(smem) + warp * (P * TILE + 128);
   double* buf = wbase + (lane_ok ? sub : 0) * TILE;
@@ -49,8 +50,9 @@ __global__ void __launch_bounds__(384) __maxnreg__(REGS)
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int P = 32 / N, TILE = Tile3<N>::TILE;
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
-  const int sub = lid / N, t = lid - sub * N;
-  const bool lane_ok = sub < P;
+  const int hl = lid & 15;
+  const int sub = (lid >> 4) * (P / 2) + hl / N, t = hl % N;
+  const bool lane_ok = hl < (P / 2) * N;
   const int tt = lane_ok ? t : 0;
   double* wbase = reinterpret_cast<double*>(smem) + warp * (P * TILE + 128);
   double* buf = wbase + (lane_ok ? sub : 0) * TILE;
@@ -70,10 +72,10 @@ __global__ void __launch_bounds__(384) __maxnreg__(REGS)
         contract_slow<N, true>(o, u, tb.S);
       }
     } else {
-      x_to_y<N, Tile3<N>>(u, o, buf, tt, lane_ok);
-      y_to_z<N, Tile3<N>>(o, u, buf, tt, lane_ok);
-      y_to_z<N, Tile3<N>>(u, o, buf, tt, lane_ok);
-      z_to_x<N, Tile3<N>>(o, u, buf, tt, lane_ok);
+      x_to_y<N, typename Tile3<N>::XY>(u, o, buf, tt, lane_ok);
+      y_to_z<N, typename Tile3<N>::YZ>(o, u, buf, tt, lane_ok);
+      y_to_z<N, typename Tile3<N>::YZ>(u, o, buf, tt, lane_ok);
+      z_to_x<N, typename Tile3<N>::ZX>(o, u, buf, tt, lane_ok);
     }
     acc += u[0][0];
   }

@@ -603,6 +603,7 @@ class CellOperator:
         rows = cells_nodes(mesh, numbering, self.cells)
         n3 = (numbering.degree + 1) ** 3
         rows = rows.reshape(len(self.cells), n3)
+        self._cell_rows = rows  # global DoF rows of the rank's cells (reused by the planners)
         lb, rib = layout.map_rows(rows.ravel())
         lb = lb.reshape(rows.shape)
         rib = rib.reshape(rows.shape)
@@ -651,7 +652,7 @@ class CellOperator:
         if hit is not None and hit[0] is support:
             return hit[1]
         if _plan.enabled():
-            nodes = cells_nodes(self.mesh, self.numbering, self.cells)
+            nodes = self._cell_rows
             row_sel, rptr, rcols = self.support_rows(support, nodes)
             ptr, cols = _plan.cell_pairs(row_sel[nodes], rptr, rcols)
             act = sparse.csr_matrix((np.ones(cols.size, dtype=np.int8), cols.astype(np.int64), ptr),

@@ -511,6 +511,8 @@ class _CellPlan:
         rkh = rib * dst.slab.width[lbd]
         wide = bool(n_cells and (int(sgp.max()) >= 32 or int(rkx.max()) >= 1 << 13
                                  or int(rkh.max()) >= 1 << 14))
+        if os.environ.get("BMV_K1_WIDE") == "1":  # tests: force the 64-bit code rows
+            wide = True
         if wide:
             if n_cells and (int(rkx.max()) >= 1 << 27 or int(rkh.max()) >= 1 << 31):
                 raise ShapeError("K1 codes: block rows too large for 32-bit row offsets")

@@ -181,8 +181,10 @@ int bmv_tmmult_run(const bmv_chunk_plan* plan, const double* a, const double* b,
    (entries of Y outside the chunks are not touched). */
 int bmv_mmult_run(const bmv_chunk_plan* plan, const double* a, const double* cmat, double* y,
                   double alpha, int32_t accumulate, void* stream);
-/* warps per CTA and bytes per buffer (largest chunk) of the K4 / K5 kernel (kind 4 / 5) */
-int bmv_chunk_kernel_config(int32_t kind, int32_t* warps, int32_t* buffer_bytes);
+/* warps per CTA and bytes per buffer (largest chunk) of the K4 / K5 kernel (kind 4 / 5);
+   variant 0: default shape, 1: shape for short block rows (fewer warps, larger chunks).
+   bmv_chunk_plan_create picks the shape from the plan's stage_bytes. */
+int bmv_chunk_kernel_config(int32_t kind, int32_t variant, int32_t* warps, int32_t* buffer_bytes);
 
 /* --------------------------------------------------------- halo / util --
  * Device index lists for ghost exchange packing.                         */

@@ -81,7 +81,7 @@ SIGNATURES = [
      [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     ("bmv_mmult_run", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_void_p]),
-    ("bmv_chunk_kernel_config", C.c_int, [C.c_int32, _i32p, _i32p]),
+    ("bmv_chunk_kernel_config", C.c_int, [C.c_int32, C.c_int32, _i32p, _i32p]),
     ("bmv_index_create", C.c_int, [_i64p, C.c_int64, C.POINTER(C.c_void_p)]),
     ("bmv_index_destroy", C.c_int, [C.c_void_p]),
     ("bmv_index_size", C.c_int64, [C.c_void_p]),

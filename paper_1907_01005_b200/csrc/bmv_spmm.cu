@@ -43,6 +43,9 @@ namespace {
 #ifndef BMV_K4_WARPS
 #define BMV_K4_WARPS 12
 #endif
+#ifndef BMV_K4_WARPS_SHORT   // K4 on short block rows: fewer warps, larger chunks (fewer S flushes)
+#define BMV_K4_WARPS_SHORT 8
+#endif
 #ifndef BMV_K5_WARPS
 #define BMV_K5_WARPS 16
 #endif
@@ -51,12 +54,17 @@ namespace {
 #endif
 constexpr int kNB = BMV_SPMM_BUFS;    // buffers per warp (kNB - 1 chunks in flight)
 constexpr int kSmemBytes = 224 * 1024;
-template <int KIND>
+template <int CW_>
 struct Shape {
-  static constexpr int CW = KIND == 4 ? BMV_K4_WARPS : BMV_K5_WARPS;
+  static constexpr int CW = CW_;
   // bytes per buffer = the largest chunk [meta | A | B] the planner may build
   static constexpr int BUF = kSmemBytes / (CW * kNB) / 128 * 128;
 };
+// kernel shapes per product: variant 0 (default), 1 (short block rows)
+constexpr int kWarpsOf[2][2] = {{BMV_K4_WARPS, BMV_K4_WARPS_SHORT}, {BMV_K5_WARPS, BMV_K5_WARPS}};
+__host__ constexpr int buf_of(int kind, int variant) {
+  return kSmemBytes / (kWarpsOf[kind - 4][variant] * kNB) / 128 * 128;
+}
 
 // Per-chunk copy descriptor (built once in bmv_chunk_plan_create), 32 bytes:
 // one sector, loaded by the claiming warp a pipeline step ahead of its use.
@@ -346,11 +354,11 @@ __device__ __forceinline__ void k5_chunk(const char* st, const double* __restric
   else k5_passes<8, 2>(m, cmat, y, alpha, accumulate, lane);
 }
 
-template <int KIND>  // 4: K4, 5: K5
-__global__ void __launch_bounds__(Shape<KIND>::CW * 32, 1)
+template <int KIND, int CW>  // KIND 4: K4, 5: K5; CW warps per CTA
+__global__ void __launch_bounds__(CW * 32, 1)
     chunk_kernel(const ChunkArgs g, const double* __restrict__ a, const double* __restrict__ b,
                  double* __restrict__ out, double alpha, int accumulate) {
-  constexpr int kBufBytes = Shape<KIND>::BUF;
+  constexpr int kBufBytes = Shape<CW>::BUF;
   extern __shared__ __align__(128) char smem[];
   __shared__ int next_chunk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -424,6 +432,7 @@ __global__ void __launch_bounds__(Shape<KIND>::CW * 32, 1)
 
 struct ChunkPlan {
   int kind = 0;
+  int variant = 0;  // kernel shape: the smallest buffers that hold the plan's chunks
   int n_parts = 0;
   int64_t n_chunks = 0;
   int64_t* part_start = nullptr;
@@ -444,9 +453,10 @@ int bmv_chunk_plan_create(const bmv_chunk_desc* d, bmv_chunk_plan** out) {
   *out = nullptr;
   if (!d || (d->kind != 4 && d->kind != 5) || d->n_parts <= 0 || d->n_chunks < 0 ||
       d->stage_bytes <= 0 || (d->stage_bytes & 15) ||
-      d->stage_bytes > (d->kind == 4 ? Shape<4>::BUF : Shape<5>::BUF)) {
+      d->stage_bytes > std::max(buf_of(d->kind, 0), buf_of(d->kind, 1))) {
     set_error("bmv_chunk_plan_create: invalid descriptor (chunks of at most %d bytes)",
-              d && d->kind == 4 ? Shape<4>::BUF : Shape<5>::BUF);
+              d && (d->kind == 4 || d->kind == 5) ? std::max(buf_of(d->kind, 0), buf_of(d->kind, 1))
+                                                  : 0);
     return BMV_ERR_INVALID;
   }
   // per-chunk copy descriptors
@@ -478,6 +488,9 @@ int bmv_chunk_plan_create(const bmv_chunk_desc* d, bmv_chunk_plan** out) {
   }
   auto* p = new bmv_chunk_plan();
   p->kind = d->kind;
+  p->variant = d->stage_bytes <= std::min(buf_of(d->kind, 0), buf_of(d->kind, 1))
+                   ? (buf_of(d->kind, 0) <= buf_of(d->kind, 1) ? 0 : 1)
+                   : (buf_of(d->kind, 0) >= d->stage_bytes ? 0 : 1);
   p->n_parts = d->n_parts;
   p->n_chunks = d->n_chunks;
   int rc = upload(d->part_chunk_start, (int64_t)d->n_parts + 1, &p->part_start);
@@ -510,17 +523,20 @@ static int launch_chunks(const bmv_chunk_plan* p, const double* a, const double*
   }
   ChunkArgs g{p->part_start, p->desc, p->meta};
   cudaStream_t st = as_stream(stream);
+#define BMV_LAUNCH_CHUNKS(KIND, CW)                                                               \
+  do {                                                                                           \
+    constexpr int smem = CW * kNB * Shape<CW>::BUF;                                               \
+    BMV_CUDA_TRY(cudaFuncSetAttribute(chunk_kernel<KIND, CW>,                                     \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));        \
+    chunk_kernel<KIND, CW><<<p->n_parts, CW * 32, smem, st>>>(g, a, b, out, alpha, accumulate);   \
+  } while (0)
   if (p->kind == 4) {
-    constexpr int smem = Shape<4>::CW * kNB * Shape<4>::BUF;
-    BMV_CUDA_TRY(cudaFuncSetAttribute(chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      smem));
-    chunk_kernel<4><<<p->n_parts, Shape<4>::CW * 32, smem, st>>>(g, a, b, out, alpha, accumulate);
+    if (p->variant == 0) BMV_LAUNCH_CHUNKS(4, BMV_K4_WARPS);
+    else BMV_LAUNCH_CHUNKS(4, BMV_K4_WARPS_SHORT);
   } else {
-    constexpr int smem = Shape<5>::CW * kNB * Shape<5>::BUF;
-    BMV_CUDA_TRY(cudaFuncSetAttribute(chunk_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      smem));
-    chunk_kernel<5><<<p->n_parts, Shape<5>::CW * 32, smem, st>>>(g, a, b, out, alpha, accumulate);
+    BMV_LAUNCH_CHUNKS(5, BMV_K5_WARPS);
   }
+#undef BMV_LAUNCH_CHUNKS
   BMV_CHECK_LAUNCH();
   return BMV_OK;
 }
@@ -549,13 +565,13 @@ int bmv_mmult_run(const bmv_chunk_plan* p, const double* a, const double* cmat, 
   return launch_chunks(p, a, cmat, y, alpha, accumulate, stream);
 }
 
-int bmv_chunk_kernel_config(int32_t kind, int32_t* warps, int32_t* buffer_bytes) {
-  if (kind != 4 && kind != 5) {
-    bmv::set_error("bmv_chunk_kernel_config: kind must be 4 or 5");
+int bmv_chunk_kernel_config(int32_t kind, int32_t variant, int32_t* warps, int32_t* buffer_bytes) {
+  if ((kind != 4 && kind != 5) || variant < 0 || variant > 1) {
+    bmv::set_error("bmv_chunk_kernel_config: kind must be 4 or 5, variant 0 or 1");
     return BMV_ERR_INVALID;
   }
-  *warps = kind == 4 ? bmv::Shape<4>::CW : bmv::Shape<5>::CW;
-  *buffer_bytes = kind == 4 ? bmv::Shape<4>::BUF : bmv::Shape<5>::BUF;
+  *warps = bmv::kWarpsOf[kind - 4][variant];
+  *buffer_bytes = bmv::buf_of(kind, variant);
   return BMV_OK;
 }
 

@@ -31,14 +31,19 @@ MAX_BLOCK_ROWS = 16
 META_ALLOWANCE = 1536        # bytes left for the chunk meta when cutting chunks
 
 
-def chunk_bytes(kind: int) -> tuple[int, int]:
-    """(largest chunk, staged values per chunk) in bytes for K4 / K5 (kind 4 / 5)."""
+SHORT_ROWS = 32              # mean rows per block row below which K4 takes its second shape
+
+
+def chunk_bytes(kind: int, variant: int = 0) -> tuple[int, int]:
+    """(largest chunk, staged values per chunk) in bytes for K4 / K5 (kind 4 / 5);
+    variant 1: the kernel shape for short block rows (larger chunks)."""
     if "BMV_SPMM_STAGE" in os.environ:
         stage = int(os.environ["BMV_SPMM_STAGE"])
     else:
         C = _lib.C
         warps, buf = C.c_int32(), C.c_int32()
-        _lib.check(_lib.load().bmv_chunk_kernel_config(int(kind), C.byref(warps), C.byref(buf)))
+        _lib.check(_lib.load().bmv_chunk_kernel_config(int(kind), int(variant), C.byref(warps),
+                                                       C.byref(buf)))
         stage = int(buf.value)
     data = int(os.environ.get("BMV_SPMM_DATA", max(stage - META_ALLOWANCE, stage // 2)))
     return stage, data
@@ -151,11 +156,15 @@ def tmmult_plan(a, b, c) -> ChunkPlan:
         return plan
     _check_tmmult_blocks(a, b, c)
     n = a.n_owned_blocks
+    rows = a.local_row_sizes[:n]
+    # short block rows: the S flush per chunk weighs as much as the product;
+    # the second kernel shape has fewer warps and larger chunks
+    variant = 1 if n and float(np.mean(rows)) < SHORT_ROWS else 0
+    stage, data = chunk_bytes(4, variant)
     arrays = _plan.chunk_plan(
         4, a.local_row_sizes[:n], _Owned(a), _Owned(b), a.col_blocks.starts,
         _local_table(c.layout, c.layout.blocks.n_blocks), c.slab,
-        K4_MAX_ROWS, MAX_BLOCK_ROWS, chunk_bytes(4)[1], chunk_bytes(4)[0], _n_parts(c.device))
-    rows = a.local_row_sizes[:n]
+        K4_MAX_ROWS, MAX_BLOCK_ROWS, data, stage, _n_parts(c.device))
     flops = int(2 * np.sum(rows * a.slab.width[:n] * b.slab.width[:n]))
     plan = ChunkPlan(arrays, flops)
     _cache_put(a, key, refs, plan)

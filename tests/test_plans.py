@@ -32,7 +32,7 @@ def _setup(block_size, lane_width, compact, level=1, degree=2):
 
 
 def _shape(monkeypatch, stage, rows):
-    monkeypatch.setattr(spmm, "chunk_bytes", lambda kind: (stage, stage - 1024))
+    monkeypatch.setattr(spmm, "chunk_bytes", lambda kind, variant=0: (stage, stage - 1024))
     monkeypatch.setattr(spmm, "K4_MAX_ROWS", rows)
 
 
@@ -106,7 +106,7 @@ def test_wide_rows_split_when_meta_and_rows_exceed_a_buffer(monkeypatch, stage):
     once lost its second half there)."""
     centers = np.asarray([[1.0, 1.0, 1.0], [3.0, 3.0, 2.0], [2.0, 1.5, 3.0], [0.5, 3.2, 0.7],
                           [2.5, 2.5, 0.5], [1.5, 3.5, 2.5]])
-    monkeypatch.setattr(spmm, "chunk_bytes", lambda kind: (stage, stage - 1536))
+    monkeypatch.setattr(spmm, "chunk_bytes", lambda kind, variant=0: (stage, stage - 1536))
     s = Small((4, 4, 4), (1.0, 1.0, 1.0), 1, 2, centers, 3.5, 8, 8)
     ctx = serial_context("cpu")
     rl, _, x, hx = s.operands(ctx, "cpu")

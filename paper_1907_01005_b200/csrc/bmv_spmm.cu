@@ -339,8 +339,8 @@ __device__ __forceinline__ void k5_passes(const int32_t* m, const double* cmat, 
     const int tb = min(TBMAX, (ub - bg + 7) >> 3);
     if (tb == 1) k5_pass<1, KS>(m, cmat, y, alpha, accumulate, bg, lane);
     else if (tb == 2 || TBMAX == 2) k5_pass<2, KS>(m, cmat, y, alpha, accumulate, bg, lane);
-    else if (tb == 3) k5_pass<(TBMAX > 2 ? 3 : 2), KS>(m, cmat, y, alpha, accumulate, bg, lane);
-    else k5_pass<(TBMAX > 2 ? 4 : 2), KS>(m, cmat, y, alpha, accumulate, bg, lane);
+    else if (tb == 3 || TBMAX == 3) k5_pass<(TBMAX > 2 ? 3 : 2), KS>(m, cmat, y, alpha, accumulate, bg, lane);
+    else k5_pass<(TBMAX > 3 ? 4 : TBMAX), KS>(m, cmat, y, alpha, accumulate, bg, lane);
   }
 }
 
@@ -351,6 +351,7 @@ __device__ __forceinline__ void k5_chunk(const char* st, const double* __restric
   const int ua = m[H_UA];
   if (ua <= 8) k5_passes<2, 4>(m, cmat, y, alpha, accumulate, lane);
   else if (ua <= 16) k5_passes<4, 4>(m, cmat, y, alpha, accumulate, lane);
+  else if (ua <= 24) k5_passes<6, 3>(m, cmat, y, alpha, accumulate, lane);
   else k5_passes<8, 2>(m, cmat, y, alpha, accumulate, lane);
 }
 

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "bmv.h"
@@ -299,9 +300,10 @@ __device__ __forceinline__ void k5_pass(const int32_t* m, const double* __restri
           sy[u][e] = bb < ub ? cmy[s * ub + bb] : -1;
         }
       double* yrow = y + (int64_t)r0.w + (int64_t)g4 * ky;
-      const int nrt = (nrows + 7) >> 3;
-      for (int rt = 0; rt < nrt; ++rt, yrow += 8 * ky) {
-        const bool rok = rt * 8 + g4 < nrows;  // false only in the last tile
+      // one 8-row tile; FULL: every row of the tile belongs to the segment
+      auto tile = [&](auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
+        const bool rok = FULL || g4 < (nrows & 7);
         double acc[TB][2];
 #pragma unroll
         for (int u = 0; u < TB; ++u) acc[u][0] = acc[u][1] = 0.0;
@@ -324,7 +326,11 @@ __device__ __forceinline__ void k5_pass(const int32_t* m, const double* __restri
                 *yp = v;
               }
         }
-      }
+        yrow += 8 * ky;
+      };
+      const int full = nrows >> 3;
+      for (int rt = 0; rt < full; ++rt) tile(std::true_type{});
+      if (nrows & 7) tile(std::false_type{});  // last tile: rows past the segment are skipped
     }
   }
 }

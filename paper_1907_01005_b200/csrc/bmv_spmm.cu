@@ -118,7 +118,8 @@ constexpr int kZeroByte = 56;
 // One pass: union columns [ag, ag + 8 TA) x [bg, bg + 8 TB); accumulators
 // live in registers over every segment of the chunk.  Segments are padded
 // to multiples of 4 rows (a DMMA k-step never straddles two block rows).
-template <int TA, int TB>
+// UNR: k-loop unroll (fragment loads in flight): 4 pays on long block rows, 1 on short ones
+template <int TA, int TB, int UNR>
 __device__ __forceinline__ void k4_pass(const int32_t* m, double* __restrict__ c, int ag, int bg,
                                         int lane) {
   const int nseg = m[H_NSEG], ua = m[H_UA], ub = m[H_UB];
@@ -155,7 +156,7 @@ __device__ __forceinline__ void k4_pass(const int32_t* m, double* __restrict__ c
       sb[u] = sl >= 0 ? 32 * kb : 0;
     }
     const int full = nrows >> 2;
-#pragma unroll 2
+#pragma unroll UNR
     for (int ks = 0; ks < full; ++ks) {
       double av[TA], bv[TB];
 #pragma unroll
@@ -210,17 +211,18 @@ __device__ __forceinline__ void k4_pass(const int32_t* m, double* __restrict__ c
   }
 }
 
-template <int TA>
+template <int TA, int UNR>
 __device__ __forceinline__ void k4_pass_b(const int32_t* m, double* c, int ag, int bg, int tb,
                                           int lane) {
   switch (tb) {
-    case 1: k4_pass<TA, 1>(m, c, ag, bg, lane); break;
-    case 2: k4_pass<TA, 2>(m, c, ag, bg, lane); break;
-    case 3: k4_pass<TA, 3>(m, c, ag, bg, lane); break;
-    default: k4_pass<TA, 4>(m, c, ag, bg, lane); break;
+    case 1: k4_pass<TA, 1, UNR>(m, c, ag, bg, lane); break;
+    case 2: k4_pass<TA, 2, UNR>(m, c, ag, bg, lane); break;
+    case 3: k4_pass<TA, 3, UNR>(m, c, ag, bg, lane); break;
+    default: k4_pass<TA, 4, UNR>(m, c, ag, bg, lane); break;
   }
 }
 
+template <int UNR>
 __device__ __forceinline__ void k4_chunk(const char* st, double* __restrict__ c, int lane) {
   const int32_t* m = reinterpret_cast<const int32_t*>(st);
   const int ua = m[H_UA], ub = m[H_UB];
@@ -229,10 +231,10 @@ __device__ __forceinline__ void k4_chunk(const char* st, double* __restrict__ c,
     for (int bg = 0; bg < ub; bg += 32) {
       const int tb = min(4, (ub - bg + 7) >> 3);
       switch (ta) {
-        case 1: k4_pass_b<1>(m, c, ag, bg, tb, lane); break;
-        case 2: k4_pass_b<2>(m, c, ag, bg, tb, lane); break;
-        case 3: k4_pass_b<3>(m, c, ag, bg, tb, lane); break;
-        default: k4_pass_b<4>(m, c, ag, bg, tb, lane); break;
+        case 1: k4_pass_b<1, UNR>(m, c, ag, bg, tb, lane); break;
+        case 2: k4_pass_b<2, UNR>(m, c, ag, bg, tb, lane); break;
+        case 3: k4_pass_b<3, UNR>(m, c, ag, bg, tb, lane); break;
+        default: k4_pass_b<4, UNR>(m, c, ag, bg, tb, lane); break;
       }
     }
   }
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(CW * 32, 1)
     cp_wait<kNB - 1>();
     __syncwarp();
     const char* st = mybuf + (size_t)cur * kBufBytes;
-    if (KIND == 4) k4_chunk(st, out, lane);
+    if (KIND == 4) k4_chunk<(CW == BMV_K4_WARPS_SHORT ? 1 : 4)>(st, out, lane);
     else k5_chunk(st, b, out, alpha, accumulate != 0, lane);
     __syncwarp();
 #pragma unroll

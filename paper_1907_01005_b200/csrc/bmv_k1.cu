@@ -621,6 +621,12 @@ int launch_k1(const K1Plan* p, K1Args& args, int64_t p0, int64_t p1, cudaStream_
     auto kern = k1_pair_kernel<NP, COEF, MODE, WIDE>;
     constexpr int kW = K1PairShape<NP>::WARPS;
     const int smem = kW * K1PairShape<NP>::STAGES * k1_pair_stage_bytes<NP>(p->code_stride, p->gbytes);
+    if (smem > 227 * 1024) {
+      set_error("K1: the pair kernel's metadata stages (%d bytes: %d group-table bytes per pair) "
+                "exceed the shared memory of an SM; use coarser row blocks",
+                smem, p->gbytes);
+      return BMV_ERR_INVALID;
+    }
     BMV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t want = (b1 - b0 + kW - 1) / kW;
     const int64_t grid = std::min<int64_t>(want, (int64_t)sm_count());

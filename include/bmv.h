@@ -63,7 +63,14 @@ int bmv_device_sm_count(int* out);
  *     pair's column in the src slab (-1: not stored -> value 0),
  *     slab_off_dst[g] + slot in the dst slab}
  *   X value of DoF d for pair p = X[gtab[p][g].x + rKx], H X accumulated at
- *   HX[gtab[p][g].y + rKh].                                                */
+ *   HX[gtab[p][g].y + rKh].
+ * bmv_cellop_create cuts the pair list (pairs sorted by cell, group tables
+ * consecutive) into batches of consecutive pairs -- n >= 4: up to 32 / n
+ * pairs in at most two cells; n <= 3: up to 32 pairs in at most 8 cells --
+ * never across a declared break, so that bmv_cellop_apply_pairs can run the
+ * ranges between breaks separately (halo overlap).  The kernels are
+ * persistent (one CTA per SM); limits: at most 32 groups per cell, pair
+ * kernel: about 26 groups per cell (metadata stages in shared memory).     */
 typedef struct {
   int32_t n;              /* nodes per axis (degree+1), 2..5; q = n        */
   int32_t wide;           /* 0: 32-bit codes, 1: 64-bit codes             */

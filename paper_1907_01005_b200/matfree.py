@@ -816,10 +816,7 @@ class CellOperator:
             raise ShapeError("operator and operands must share one rank layout")
         if src.col_blocks != dst.col_blocks or src.lane_width != dst.lane_width:
             raise ShapeError("src and dst must share column blocking and lanes")
-        if variant == GEMM:
-            raise ShapeError("variant 'gemm' (element-matrix products) is not implemented on the "
-                             "GPU path; use 'sumfac' (same operator)")
-        if variant != SUMFAC:
+        if variant not in (SUMFAC, GEMM):
             raise ShapeError(f"unknown operator variant {variant!r}")
         if spec.kind not in (MASS, HAMILTONIAN):
             raise ShapeError(f"unknown operator kind {spec.kind!r}")
@@ -835,6 +832,11 @@ class CellOperator:
         lib = _lib.require_device()
         dst.ensure_owned()
         plan = self.plan_for(src, dst)
+        if variant == GEMM:
+            self._apply_gemm(spec, plan, src, dst)
+            if counters is not None:
+                self._count(spec, variant, plan, src, dst, counters)
+            return
         coef, stride = self.coefficient(spec, dst.device)
         kin = 1 if spec.kind == HAMILTONIAN else 0
         cp = _lib.dptr(coef) if coef is not None else C.c_void_p(None)
@@ -848,6 +850,91 @@ class CellOperator:
         self._overlapped(plan, src, (dst,), run)
         if counters is not None:
             self._count(spec, variant, plan, src, dst, counters)
+
+    # -- element-matrix variant (comparison point) -------------------------------
+
+    def _base_element_matrix(self, kind: str) -> np.ndarray:
+        """Cell-independent part of the element matrix (reference
+        `element_matrices`, matfree.py:375-397): the kinetic term by direct
+        quadrature on the tensor-product tables (x fastest), or 0 for mass."""
+        n3 = (self.shape.degree + 1) ** 3
+        if kind != HAMILTONIAN:
+            return np.zeros((n3, n3))
+        S, D = self.shape.values, self.shape.derivatives
+        w = self.kernels.w3.ravel()
+        g3 = (np.kron(S, np.kron(S, D)), np.kron(S, np.kron(D, S)), np.kron(D, np.kron(S, S)))
+        out = np.zeros((n3, n3))
+        for g, c in zip(g3, self.kernels.grad_scale):
+            out += g.T @ ((w * c)[:, None] * g)
+        return out
+
+    def _apply_gemm(self, spec, plan, src, dst, cells_per_chunk: int = 512):
+        """variant='gemm' (reference matfree.py:375-397, 496, 509-511): per cell
+        the dense element matrix A_c = K + N3^T diag(w3 V_c) N3 times the
+        gathered block of the cell's active columns.  The paper's comparison
+        point ("FE op. (BCSR gemm)"), not the hot path: batched cuBLAS products
+        (torch.bmm) over cell chunks, gather / scatter index lists built on the
+        host from the K1 plan's codes and group tables at every call."""
+        dev = dst.device
+        arr = plan.arrays
+        n = plan.n
+        n3 = n ** 3
+        S = self.shape.values
+        nn3 = torch.as_tensor(np.kron(S, np.kron(S, S)), device=dev)           # (q3, n3)
+        base = torch.as_tensor(self._base_element_matrix(spec.kind), device=dev)
+        coef, stride = self.coefficient(spec, dev)
+        q3 = self.shape.n_q ** 3
+        p_cell = arr["pair_cell"].astype(np.int64)
+        codes = arr["codes"].reshape(plan.n_cells, plan.code_stride)
+        gtab = arr["gtab"].astype(np.int64)
+        pgt = arr["pair_gtab"]
+        _zero_range(dst.data, 0, dst.data.numel())
+        src.update_ghost_values()
+        # cells in plan order; a cell's pairs are consecutive
+        starts = np.flatnonzero(np.r_[True, p_cell[1:] != p_cell[:-1]]) if p_cell.size else \
+            np.zeros(0, dtype=np.int64)
+        ends = np.r_[starts[1:], p_cell.size]
+        for c0 in range(0, starts.size, cells_per_chunk):
+            ps, pe = starts[c0 : c0 + cells_per_chunk], ends[c0 : c0 + cells_per_chunk]
+            cells = p_cell[ps]
+            cnt = pe - ps
+            kmax = int(cnt.max())
+            pairs = np.arange(int(ps[0]), int(pe[-1]), dtype=np.int64)
+            pc = p_cell[pairs]
+            row = codes[pc]                                   # (pairs, stride) code rows
+            if plan.wide:
+                g = (row[:, 0 : 2 * n3 : 2] >> 27).astype(np.int64)
+                rkx = (row[:, 0 : 2 * n3 : 2] & 0x7FFFFFF).astype(np.int64)
+                rkh = row[:, 1 : 2 * n3 : 2].astype(np.int64)
+            else:
+                g = (row[:, :n3] >> 27).astype(np.int64)
+                rkx = ((row[:, :n3] >> 14) & 0x1FFF).astype(np.int64)
+                rkh = (row[:, :n3] & 0x3FFF).astype(np.int64)
+            at = pgt[pairs][:, None] + 2 * g
+            xo = gtab[at]
+            ho = gtab[at + 1]
+            x_off = np.where(xo >= 0, xo + rkx, -1)           # (pairs, n3)
+            h_off = ho + rkh
+            xt = torch.as_tensor(np.maximum(x_off, 0), device=dev)
+            u = src.data[xt] * torch.as_tensor(x_off >= 0, device=dev)
+            # pack the pairs of each cell into a padded block (cells, n3, kmax)
+            slot = pairs - np.repeat(ps, cnt)
+            cidx = np.repeat(np.arange(cells.size), cnt)
+            blk = torch.zeros(cells.size, kmax, n3, dtype=torch.float64, device=dev)
+            ci, si = torch.as_tensor(cidx, device=dev), torch.as_tensor(slot, device=dev)
+            blk[ci, si] = u
+            if coef is None:
+                a_c = base.expand(cells.size, n3, n3)
+            else:
+                cw = coef.view(-1, stride)[:, :q3] if stride else coef[:q3].view(1, q3)
+                cc = cw[torch.as_tensor(cells, device=dev)] if stride else cw.expand(cells.size, q3)
+                a_c = base + torch.einsum("qi,cq,qj->cij", nn3, cc, nn3)
+            out = torch.bmm(a_c, blk.transpose(1, 2))          # (cells, n3, kmax)
+            vals = out.transpose(1, 2)[ci, si]                  # (pairs, n3)
+            dst.data.index_add_(0, torch.as_tensor(h_off.ravel(), device=dev), vals.reshape(-1))
+        src.release_ghosts()
+        dst.support = None
+        dst.compress()
 
     def _overlapped(self, plan, src, dsts, run):
         """zero dsts | src ghost update || part A | boundary | compress dsts || part B."""
@@ -908,7 +995,10 @@ class CellOperator:
         n = plan.n
         w = src.lane_width
         with_v = spec.kind == HAMILTONIAN and spec.potential is not None
-        counters.flops += plan.lane_groups * sumfac_flops_per_lane(n, spec.kind, with_v) * w
+        if variant == GEMM:  # reference accounting: 2 (n^3)^2 per lane (matfree.py:509-511)
+            counters.flops += plan.lane_groups * 2 * (n ** 3) ** 2 * w
+        else:
+            counters.flops += plan.lane_groups * sumfac_flops_per_lane(n, spec.kind, with_v) * w
         counters.cells_visited += plan.cells_visited
         counters.col_blocks_visited += plan.n_visits
         counters.dof_lane_slots += plan.dof_lane_slots

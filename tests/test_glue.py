@@ -127,7 +127,7 @@ def test_image_columns_cover_the_operator_reach():
         assert (img.slab.slots(lbs, np.full(lbs.size, c)) >= 0).all()
 
 
-def test_gemm_variant_rejected():
+def test_unknown_variant_rejected():
     import pytest
 
     from paper_1907_01005_b200.errors import ShapeError
@@ -135,4 +135,15 @@ def test_gemm_variant_rejected():
 
     s, op, x, hx = _compact()
     with pytest.raises(ShapeError):
-        op.apply(hamiltonian_operator(None), x, hx, variant="gemm")
+        op.apply(hamiltonian_operator(None), x, hx, variant="stencil")
+
+
+def test_base_element_matrix_matches_oracle():
+    """Kinetic part of the gemm variant's element matrix against the oracle's
+    direct quadrature (reference element_matrices, matfree.py:375-397)."""
+    from oracle import numpy_oracle as O
+
+    s, op, x, hx = _compact()
+    got = op._base_element_matrix("hamiltonian")
+    want = O.element_matrix(op.shape.degree, op.mesh.spacing, "h", None)
+    assert np.allclose(got, want, rtol=1e-13, atol=1e-13 * np.abs(want).max())

@@ -45,6 +45,26 @@ def per_vector_err(m, got: torch.Tensor, want: torch.Tensor) -> float:
 _VQ: dict = {}
 
 
+@pytest.fixture(scope="module", params=["proj", "weak1"])
+def big(request):
+    """One problem + rank setup per config for the whole module (pytest groups the
+    tests by this parameter, so each config is built once and V is sampled once)."""
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test selected but no CUDA device is visible")
+    from paper_1907_01005_b200 import _lib
+
+    _lib.require_device()
+    dev = torch.device("cuda", 0)
+    name = request.param
+    prob = P.build_problem(name)
+    st = P.make_rank_setup(serial_context(dev), prob, projection=True, device=dev,
+                           with_y=name == "proj")
+    yield name, prob, st
+    del st, prob
+    _VQ.clear()
+    torch.cuda.empty_cache()
+
+
 def oracle_potential(prob, op):
     """V at the quadrature points of every cell by the numpy oracle (cell chunks)."""
     key = prob.cfg.name
@@ -77,10 +97,8 @@ def like(m, ref_values):
     return out
 
 
-@pytest.mark.parametrize("name", ["proj", "weak1"])
-def test_large_config_hx_matches_c_oracle(cuda, name):
-    prob = P.build_problem(name)
-    st = P.make_rank_setup(serial_context(cuda), prob, projection=False, device=cuda)
+def test_large_config_hx_matches_c_oracle(cuda, big):
+    name, prob, st = big
     st.op.apply(prob.spec_h(), st.x, st.hx)
     torch.cuda.synchronize()
     want = like(st.hx, oracle_apply(st, prob, st.x))
@@ -100,12 +118,9 @@ def _proj_err(st, s_got, s_want, x, z):
     return float(np.max(np.abs(g - w) / scale)) if flat.size else 0.0
 
 
-@pytest.mark.parametrize("name", ["proj", "weak1"])
-def test_large_config_projection_and_postmultiply_match_c_oracle(cuda, name):
-    prob = P.build_problem(name)
+def test_large_config_projection_and_postmultiply_match_c_oracle(cuda, big):
+    name, prob, st = big
     with_y = name == "proj"
-    st = P.make_rank_setup(serial_context(cuda), prob, projection=True, device=cuda,
-                           with_y=with_y)
     src = st.y if with_y else st.x          # S = X^T (H Y) at proj, X^T (H X) at weak G = 1
     z = st.hy if with_y else st.hx
     st.op.apply(prob.spec_h(), src, z)
@@ -134,11 +149,10 @@ def test_large_config_projection_and_postmultiply_match_c_oracle(cuda, name):
     assert per_vector_err(st.xc, st.xc.data, want.data) <= 1e-12
 
 
-def test_gaussian_potential_matches_oracle_at_512_centres(cuda):
+def test_gaussian_potential_matches_oracle_at_512_centres(cuda, big):
     """The device potential (bmv_potential_gaussian, 512 centres at weak G = 1)
     against the numpy oracle's V at the quadrature points of a cell sample."""
-    prob = P.build_problem("weak1")
-    st = P.make_rank_setup(serial_context(cuda), prob, projection=False, device=cuda)
+    name, prob, st = big
     coef, stride = st.op.coefficient(prob.spec_h(), cuda)
     w3 = st.op.kernels.w3.ravel()
     rng = np.random.default_rng(3)
